@@ -151,6 +151,26 @@ def item_codes(X, part, V, norm2_, A, want_z=False):
     return (codes, z) if want_z else codes
 
 
+def item_codes_parallel(X, part, V, norm2_, A, threads=None, chunk=1 << 15):
+    """item_codes over row chunks on host threads (ctypes releases the GIL); each
+    item's arithmetic is unchanged -- the oracle is a per-item function."""
+    from concurrent.futures import ThreadPoolExecutor
+    X = _c(X, np.float32)
+    n = X.shape[0]
+    L = A.shape[1]
+    out = np.empty((n, (L + 31) // 32), np.uint32)
+    part = _c(part, np.int32)
+    nv = _c(norm2_, np.float64)
+
+    def work(r0):
+        r1 = min(n, r0 + chunk)
+        out[r0:r1] = item_codes(X[r0:r1], part[r0:r1], V, nv[r0:r1], A)
+
+    with ThreadPoolExecutor(max_workers=threads or os.cpu_count()) as ex:
+        list(ex.map(work, range(0, n, chunk)))
+    return out
+
+
 def query_codes(Q, A, want_z=False):
     Q = _c(Q, np.float32)
     nq, d = Q.shape

@@ -1,0 +1,283 @@
+"""ctypes binding of libnrlsh.so (include/nrlsh.h) — argument marshalling only.
+
+Every step of the method runs in the library's sm_100a kernels; this module
+only converts torch tensors / numpy arrays into pointers, allocates outputs and
+maps status codes to exceptions.  There is no fallback: if the shared library
+is missing, every entry point raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libnrlsh.so")
+
+_STATUS = {0: "OK", 1: "EINVAL", 2: "ENONFINITE", 3: "EZERONORM", 4: "ENOMEM", 5: "ECUDA",
+           6: "ENOTIMPL"}
+
+EXPORTS = [
+    "nrlsh_default_options", "nrlsh_build", "nrlsh_build_ex", "nrlsh_query", "nrlsh_exact_topk",
+    "nrlsh_free", "nrlsh_last_error", "nrlsh_get_info", "nrlsh_get_partition",
+    "nrlsh_get_projection", "nrlsh_get_rank_table", "nrlsh_get_codes", "nrlsh_set_codes",
+    "nrlsh_query_codes", "nrlsh_query_candidates", "nrlsh_last_query_stats",
+    "nrlsh_index_exact_topk", "nrlsh_profile_enable", "nrlsh_profile_read",
+    "nrlsh_profile_slot_name", "nrlsh_launch_count",
+]
+
+
+class NrlshError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+        self.code = _STATUS.get(status, str(status))
+
+
+class Options(C.Structure):
+    _fields_ = [("eps", C.c_double), ("scheme", C.c_int32), ("index_bits_in_budget", C.c_int32),
+                ("query_batch", C.c_int32), ("reserved", C.c_int32)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: build it with `python -c \"import __graft_entry__ as g; "
+                "g.build()\"` (there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        p, i64, i32, u64 = C.c_void_p, C.c_int64, C.c_int32, C.c_uint64
+        st = C.c_int
+        L.nrlsh_default_options.argtypes = [C.POINTER(Options)]
+        L.nrlsh_default_options.restype = None
+        L.nrlsh_build.argtypes = [p, i64, i32, i32, i32, u64, C.POINTER(p), p]
+        L.nrlsh_build.restype = st
+        L.nrlsh_build_ex.argtypes = [p, i64, i32, i32, i32, u64, C.POINTER(Options), C.POINTER(p), p]
+        L.nrlsh_build_ex.restype = st
+        L.nrlsh_query.argtypes = [p, p, i64, i32, i64, p, p, p]
+        L.nrlsh_query.restype = st
+        L.nrlsh_exact_topk.argtypes = [p, i64, i32, p, i64, i32, p, p, p]
+        L.nrlsh_exact_topk.restype = st
+        L.nrlsh_free.argtypes = [p]
+        L.nrlsh_free.restype = None
+        L.nrlsh_last_error.argtypes = []
+        L.nrlsh_last_error.restype = C.c_char_p
+        L.nrlsh_get_info.argtypes = [p, p, p, p, p, p]
+        L.nrlsh_get_info.restype = st
+        L.nrlsh_get_partition.argtypes = [p, p, p, p, p]
+        L.nrlsh_get_partition.restype = st
+        L.nrlsh_get_projection.argtypes = [p, p]
+        L.nrlsh_get_projection.restype = st
+        L.nrlsh_get_rank_table.argtypes = [p, p]
+        L.nrlsh_get_rank_table.restype = st
+        L.nrlsh_get_codes.argtypes = [p, p]
+        L.nrlsh_get_codes.restype = st
+        L.nrlsh_set_codes.argtypes = [p, p]
+        L.nrlsh_set_codes.restype = st
+        L.nrlsh_query_codes.argtypes = [p, p, i64, p, p]
+        L.nrlsh_query_codes.restype = st
+        L.nrlsh_query_candidates.argtypes = [p, p, p, i64, i64, p, p, p]
+        L.nrlsh_query_candidates.restype = st
+        L.nrlsh_last_query_stats.argtypes = [p, p, p]
+        L.nrlsh_last_query_stats.restype = st
+        L.nrlsh_index_exact_topk.argtypes = [p, p, i64, i32, p, p, p]
+        L.nrlsh_index_exact_topk.restype = st
+        L.nrlsh_profile_enable.argtypes = [C.c_int]
+        L.nrlsh_profile_enable.restype = None
+        L.nrlsh_profile_read.argtypes = [p, p, i32, C.c_int]
+        L.nrlsh_profile_read.restype = C.c_int
+        L.nrlsh_profile_slot_name.argtypes = [i32]
+        L.nrlsh_profile_slot_name.restype = C.c_char_p
+        L.nrlsh_launch_count.argtypes = []
+        L.nrlsh_launch_count.restype = C.c_int64
+        _lib = L
+    return _lib
+
+
+def _check(rc):
+    if rc != 0:
+        raise NrlshError(rc, lib().nrlsh_last_error().decode())
+
+
+def _ptr(a):
+    """Pointer of a torch tensor (device or host) or numpy array (host)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        assert a.flags["C_CONTIGUOUS"]
+        return C.c_void_p(a.ctypes.data)
+    assert a.is_contiguous()
+    return C.c_void_p(a.data_ptr())
+
+
+def _stream(stream):
+    if stream is not None:
+        return C.c_void_p(int(stream))
+    try:
+        import torch
+        if torch.cuda.is_available() and torch.cuda.is_initialized():
+            return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    except Exception:
+        pass
+    return None
+
+
+def _is_np(a):
+    return isinstance(a, np.ndarray)
+
+
+def _empty_like_io(ref, shape, np_dtype, torch_dtype):
+    if _is_np(ref):
+        return np.empty(shape, np_dtype)
+    import torch
+    return torch.empty(shape, dtype=torch_dtype, device=ref.device)
+
+
+class Index:
+    """An nrlsh_index handle (Alg. 1).  Keeps the item buffer alive (borrowed)."""
+
+    def __init__(self, items, code_bits, num_parts, seed=0, eps=0.01, scheme="percentile",
+                 index_bits_in_budget=False, query_batch=0, stream=None):
+        self._items = items
+        opt = Options()
+        lib().nrlsh_default_options(C.byref(opt))
+        opt.eps = float(eps)
+        opt.scheme = {"percentile": 0, "uniform": 1}[scheme]
+        opt.index_bits_in_budget = 1 if index_bits_in_budget else 0
+        opt.query_batch = int(query_batch)
+        n, d = items.shape
+        h = C.c_void_p()
+        _check(lib().nrlsh_build_ex(_ptr(items), n, d, int(code_bits), int(num_parts),
+                                    C.c_uint64(seed & (2 ** 64 - 1)), C.byref(opt), C.byref(h),
+                                    _stream(stream)))
+        self._h = h
+        ni, di, hb, npart, w = C.c_int64(), C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()
+        _check(lib().nrlsh_get_info(h, C.byref(ni), C.byref(di), C.byref(hb), C.byref(npart),
+                                    C.byref(w)))
+        self.n, self.d, self.hash_bits, self.num_parts, self.words = (
+            ni.value, di.value, hb.value, npart.value, w.value)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().nrlsh_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -------------------------------------------------------------- query
+    def query(self, queries, k, probe_budget, out_ids=None, out_scores=None, stream=None):
+        nq = queries.shape[0]
+        if out_ids is None:
+            out_ids = _empty_like_io(queries, (nq, k), np.int64, _torch_dtype("int64"))
+        if out_scores is None:
+            out_scores = _empty_like_io(queries, (nq, k), np.float32, _torch_dtype("float32"))
+        _check(lib().nrlsh_query(self._h, _ptr(queries), nq, int(k), int(probe_budget),
+                                 _ptr(out_ids), _ptr(out_scores), _stream(stream)))
+        return out_ids, out_scores
+
+    def exact_topk(self, queries, k, out_ids=None, out_scores=None, stream=None):
+        """Ground truth against the index's own items (no re-staging of host items)."""
+        nq = queries.shape[0]
+        if out_ids is None:
+            out_ids = _empty_like_io(queries, (nq, k), np.int64, _torch_dtype("int64"))
+        if out_scores is None:
+            out_scores = _empty_like_io(queries, (nq, k), np.float32, _torch_dtype("float32"))
+        _check(lib().nrlsh_index_exact_topk(self._h, _ptr(queries), nq, int(k), _ptr(out_ids),
+                                            _ptr(out_scores), _stream(stream)))
+        return out_ids, out_scores
+
+    def query_codes(self, queries, stream=None):
+        nq = queries.shape[0]
+        out = _empty_like_io(queries, (nq, self.words), np.uint32, _torch_dtype("int32"))
+        _check(lib().nrlsh_query_codes(self._h, _ptr(queries), nq, _ptr(out), _stream(stream)))
+        return out
+
+    def candidates(self, probe_budget, queries=None, qcodes=None, stream=None):
+        ref = queries if queries is not None else qcodes
+        nq = ref.shape[0]
+        T = min(int(probe_budget), self.n)
+        ids = _empty_like_io(ref, (nq, T), np.int32, _torch_dtype("int32"))
+        rk = _empty_like_io(ref, (nq, T), np.uint16, _torch_dtype("int16"))
+        _check(lib().nrlsh_query_candidates(self._h, _ptr(queries), _ptr(qcodes), nq,
+                                            int(probe_budget), _ptr(ids), _ptr(rk),
+                                            _stream(stream)))
+        return ids, rk
+
+    # -------------------------------------------------------------- hooks (host copies)
+    def partition(self):
+        norm2 = np.empty(self.n, np.float64)
+        perm = np.empty(self.n, np.int32)
+        offsets = np.empty(self.num_parts + 1, np.int64)
+        V = np.empty(self.num_parts, np.float64)
+        _check(lib().nrlsh_get_partition(self._h, _ptr(norm2), _ptr(perm), _ptr(offsets),
+                                         _ptr(V)))
+        return norm2, perm, offsets, V
+
+    def projection(self):
+        A = np.empty((self.d + 1, self.hash_bits), np.float32)
+        _check(lib().nrlsh_get_projection(self._h, _ptr(A)))
+        return A
+
+    def rank_table(self):
+        R = np.empty((self.num_parts, self.hash_bits + 1), np.uint16)
+        _check(lib().nrlsh_get_rank_table(self._h, _ptr(R)))
+        return R
+
+    def codes(self):
+        c = np.empty((self.n, self.words), np.uint32)
+        _check(lib().nrlsh_get_codes(self._h, _ptr(c)))
+        return c
+
+    def set_codes(self, codes):
+        codes = np.ascontiguousarray(codes, dtype=np.uint32)
+        assert codes.shape == (self.n, self.words)
+        _check(lib().nrlsh_set_codes(self._h, _ptr(codes)))
+
+
+def _torch_dtype(name):
+    import torch
+    return getattr(torch, name)
+
+
+def exact_topk(items, queries, k, out_ids=None, out_scores=None, stream=None):
+    n, d = items.shape
+    nq = queries.shape[0]
+    if out_ids is None:
+        out_ids = _empty_like_io(queries, (nq, k), np.int64, _torch_dtype("int64"))
+    if out_scores is None:
+        out_scores = _empty_like_io(queries, (nq, k), np.float32, _torch_dtype("float32"))
+    _check(lib().nrlsh_exact_topk(_ptr(items), n, d, _ptr(queries), nq, int(k), _ptr(out_ids),
+                                  _ptr(out_scores), _stream(stream)))
+    return out_ids, out_scores
+
+
+def last_query_stats():
+    a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
+    _check(lib().nrlsh_last_query_stats(C.byref(a), C.byref(b), C.byref(c)))
+    return {"fallback_queries": a.value, "kernel_launches": b.value, "scanned_pairs": c.value}
+
+
+def profile_enable(on=True):
+    lib().nrlsh_profile_enable(1 if on else 0)
+
+
+def profile_read(reset=False):
+    """{slot name: (total ms, ranges)} of the library's per-kernel-class CUDA events."""
+    n = 32
+    ms = (C.c_double * n)()
+    cnt = (C.c_int64 * n)()
+    k = lib().nrlsh_profile_read(ms, cnt, n, 1 if reset else 0)
+    return {lib().nrlsh_profile_slot_name(i).decode(): (ms[i], cnt[i]) for i in range(k)}
+
+
+def launch_count():
+    return int(lib().nrlsh_launch_count())

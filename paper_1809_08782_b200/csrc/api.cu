@@ -1,0 +1,713 @@
+// api.cu — the C ABI of libnrlsh (include/nrlsh.h): validation, device memory,
+// launch orchestration, and the two small host-side steps of the build (the
+// seeded projection matrix and the sorted (U_j, l) structure of PAPER:217).
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "internal.h"
+
+using namespace nrlsh;
+
+namespace {
+
+thread_local std::string g_last_error;
+thread_local int64_t g_last_fallbacks = 0;
+thread_local int64_t g_last_launches = 0;
+thread_local int64_t g_last_pairs = 0;
+
+nrlsh_status fail(nrlsh_status st, const std::string &msg) {
+    g_last_error = msg;
+    return st;
+}
+
+nrlsh_status cuda_fail(cudaError_t e, const char *where) {
+    return fail(NRLSH_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+bool is_device_ptr(const void *p) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// RAII device allocation (stream-ordered).
+struct DBuf {
+    void *p = nullptr;
+    cudaStream_t s = nullptr;
+    DBuf() = default;
+    DBuf(const DBuf &) = delete;
+    ~DBuf() { if (p) cudaFreeAsync(p, s); }
+    cudaError_t alloc(size_t bytes, cudaStream_t st) {
+        s = st;
+        return cudaMallocAsync(&p, bytes ? bytes : 16, st);
+    }
+    template <class T> T *get() const { return (T *)p; }
+};
+
+void configure_pool() {
+    static bool done = false;
+    if (done) return;
+    done = true;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+}
+
+// -------------------------------------------------------------- projection
+// Documented generator (include/nrlsh.h): SplitMix64 at counter c, two 53-bit
+// uniforms, Box-Muller in fp64, fp32, then round-to-nearest-even to TF32.
+inline uint64_t mix64_at(uint64_t seed, uint64_t c) {
+    uint64_t x = seed + (c + 1ull) * 0x9E3779B97F4A7C15ull;
+    x ^= x >> 30;
+    x *= 0xBF58476D1CE4E5B9ull;
+    x ^= x >> 27;
+    x *= 0x94D049BB133111EBull;
+    x ^= x >> 31;
+    return x;
+}
+
+float tf32_rne(float f) {
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    u += 0x0FFFu + ((u >> 13) & 1u);
+    u &= ~0x1FFFu;
+    float r;
+    std::memcpy(&r, &u, 4);
+    return r;
+}
+
+void make_projection(uint64_t seed, int rows, int L, std::vector<float> &A) {
+    A.resize((size_t)rows * L);
+    const double k2pi = 2.0 * M_PI;
+    const double inv53 = 1.0 / 9007199254740992.0;
+    for (size_t e = 0; e < A.size(); ++e) {
+        const double u1 = (double)((mix64_at(seed, 2 * e) >> 11) + 1ull) * inv53;
+        const double u2 = (double)(mix64_at(seed, 2 * e + 1) >> 11) * inv53;
+        const double g = std::sqrt(-2.0 * std::log(u1)) * std::cos(k2pi * u2);
+        A[e] = tf32_rne((float)g);
+    }
+}
+
+// -------------------------------------------------------------- rank table
+// s_hat(j, h) = U_j cos(pi (1 - eps) h / L)  (Eq. (12) + eps);
+// order: s_hat desc, U desc, h asc, j asc.  R[j][h] = position; order[pos] = j*(L+1)+h.
+void make_rank_table(const std::vector<double> &U, int L, double eps, std::vector<uint16_t> &R,
+                     std::vector<int32_t> &order) {
+    const int m = (int)U.size();
+    struct E { double s, u; int j, h; };
+    std::vector<E> es;
+    es.reserve((size_t)m * (L + 1));
+    for (int j = 0; j < m; ++j)
+        for (int h = 0; h <= L; ++h)
+            es.push_back({U[j] * std::cos(M_PI * (1.0 - eps) * (double)h / (double)L), U[j], j, h});
+    std::sort(es.begin(), es.end(), [](const E &a, const E &b) {
+        if (a.s != b.s) return a.s > b.s;
+        if (a.u != b.u) return a.u > b.u;
+        if (a.h != b.h) return a.h < b.h;
+        return a.j < b.j;
+    });
+    R.assign(es.size(), 0);
+    order.assign(es.size(), 0);
+    for (size_t p = 0; p < es.size(); ++p) {
+        R[(size_t)es[p].j * (L + 1) + es[p].h] = (uint16_t)p;
+        order[p] = es[p].j * (L + 1) + es[p].h;
+    }
+}
+
+int words_for(int L) { return L <= 32 ? 1 : (L <= 64 ? 2 : 4); }
+
+void free_index(nrlsh_index *ix) {
+    if (!ix) return;
+    void *ps[] = {ix->X_owned, ix->norm2, ix->perm, ix->pos_of_id, ix->part_of_id,
+                  ix->part_of_pos, ix->offsets_d, ix->V_d, ix->codes, ix->A, ix->Apad,
+                  ix->R_d, ix->chunks_d, ix->order_d};
+    for (void *p : ps)
+        if (p) cudaFree(p);
+    delete ix;
+}
+
+// Stage a possibly-host input into device memory.
+struct Staged {
+    const void *dev = nullptr;
+    DBuf buf;
+    cudaError_t in(const void *p, size_t bytes, cudaStream_t s) {
+        if (is_device_ptr(p)) { dev = p; return cudaSuccess; }
+        cudaError_t e = buf.alloc(bytes, s);
+        if (e) return e;
+        dev = buf.p;
+        return cudaMemcpyAsync(buf.p, p, bytes, cudaMemcpyHostToDevice, s);
+    }
+};
+// Device destination for a possibly-host output.
+struct OutBuf {
+    void *user = nullptr;
+    void *dev = nullptr;
+    size_t bytes = 0;
+    bool host = false;
+    DBuf buf;
+    cudaError_t init(void *p, size_t b, cudaStream_t s) {
+        user = p;
+        bytes = b;
+        host = !is_device_ptr(p);
+        if (!host) { dev = p; return cudaSuccess; }
+        cudaError_t e = buf.alloc(b, s);
+        dev = buf.p;
+        return e;
+    }
+    cudaError_t finish(cudaStream_t s) {
+        if (!host) return cudaSuccess;
+        return cudaMemcpyAsync(user, dev, bytes, cudaMemcpyDeviceToHost, s);
+    }
+};
+
+}  // namespace
+
+// ============================================================================ ABI
+extern "C" {
+
+void nrlsh_default_options(nrlsh_options *opt) {
+    if (!opt) return;
+    opt->eps = 0.01;
+    opt->scheme = NRLSH_SCHEME_PERCENTILE;
+    opt->index_bits_in_budget = 0;
+    opt->query_batch = 0;
+    opt->reserved = 0;
+}
+
+const char *nrlsh_last_error(void) { return g_last_error.c_str(); }
+
+void nrlsh_free(nrlsh_index *index) { free_index(index); }
+
+nrlsh_status nrlsh_build(const float *items, int64_t n, int32_t d, int32_t code_bits,
+                         int32_t num_parts, uint64_t seed, nrlsh_index **out, void *cuda_stream) {
+    nrlsh_options o;
+    nrlsh_default_options(&o);
+    return nrlsh_build_ex(items, n, d, code_bits, num_parts, seed, &o, out, cuda_stream);
+}
+
+nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t code_bits,
+                            int32_t num_parts, uint64_t seed, const nrlsh_options *opt,
+                            nrlsh_index **out, void *cuda_stream) {
+    if (!out) return fail(NRLSH_EINVAL, "out is NULL");
+    *out = nullptr;
+    nrlsh_options o;
+    nrlsh_default_options(&o);
+    if (opt) o = *opt;
+    if (!items) return fail(NRLSH_EINVAL, "items is NULL");
+    if (n < 1 || n >= (1ll << 31)) return fail(NRLSH_EINVAL, "n must be in [1, 2^31)");
+    if (d < 1 || d > 4096) return fail(NRLSH_EINVAL, "d must be in [1, 4096]");
+    if (!(o.eps >= 0.0 && o.eps < 1.0)) return fail(NRLSH_EINVAL, "eps must be in [0, 1)");
+    if (o.scheme != NRLSH_SCHEME_PERCENTILE && o.scheme != NRLSH_SCHEME_UNIFORM)
+        return fail(NRLSH_EINVAL, "unknown partition scheme");
+    if (num_parts < 1 || num_parts > kMaxParts)
+        return fail(NRLSH_EINVAL, "num_parts must be in [1, 256]");
+    if (o.scheme == NRLSH_SCHEME_PERCENTILE && (int64_t)num_parts > n)
+        return fail(NRLSH_EINVAL, "num_parts > n (percentile partitioning needs m <= n)");
+    int L = code_bits;
+    if (o.index_bits_in_budget) {
+        int ib = 0;
+        while ((1 << ib) < num_parts) ++ib;   // ceil(log2 m)
+        L = code_bits - ib;
+    }
+    if (L < 1 || L > 128 || (L > 64 && L <= 96))
+        return fail(NRLSH_EINVAL, "hash bits L_h must be in [1,64] or [97,128] (got " +
+                                      std::to_string(L) + ")");
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    configure_pool();
+
+    std::unique_ptr<nrlsh_index, void (*)(nrlsh_index *)> ix(new nrlsh_index(), free_index);
+    ix->n = n;
+    ix->d = d;
+    ix->L = L;
+    ix->W = words_for(L);
+    ix->m = num_parts;
+    ix->code_bits = code_bits;
+    ix->seed = seed;
+    ix->eps = o.eps;
+    ix->scheme = o.scheme;
+    ix->query_batch = o.query_batch > 0 ? o.query_batch : 1024;
+    cudaGetDevice(&ix->device);
+    const int m = num_parts, W = ix->W;
+
+#define NR_ALLOC(ptr, bytes)                                                      \
+    do {                                                                          \
+        cudaError_t e_ = cudaMalloc((void **)&(ptr), (bytes) ? (bytes) : 16);    \
+        if (e_ != cudaSuccess) { cudaGetLastError(); return fail(NRLSH_ENOMEM, "cudaMalloc " #ptr); } \
+    } while (0)
+
+    if (is_device_ptr(items)) {
+        ix->X = items;
+    } else {
+        NR_ALLOC(ix->X_owned, (size_t)n * d * 4);
+        cudaError_t e = cudaMemcpyAsync(ix->X_owned, items, (size_t)n * d * 4,
+                                        cudaMemcpyHostToDevice, s);
+        if (e) return cuda_fail(e, "copy items");
+        ix->X = ix->X_owned;
+    }
+    NR_ALLOC(ix->norm2, (size_t)n * 8);
+    NR_ALLOC(ix->perm, (size_t)n * 4);
+    NR_ALLOC(ix->pos_of_id, (size_t)n * 4);
+    NR_ALLOC(ix->part_of_id, (size_t)n);
+    NR_ALLOC(ix->part_of_pos, (size_t)n);
+    NR_ALLOC(ix->offsets_d, (size_t)(m + 1) * 8);
+    NR_ALLOC(ix->V_d, (size_t)m * 8);
+    NR_ALLOC(ix->codes, (size_t)n * W * 4);
+
+    // K1: norms + finite check
+    DBuf bad;
+    if (bad.alloc(8, s)) return fail(NRLSH_ENOMEM, "cudaMallocAsync");
+    cudaMemsetAsync(bad.p, 0xff, 8, s);
+    {
+        ProfScope p(SLOT_NORMS, s);
+        launch_norms(ix->X, n, d, ix->norm2, bad.get<unsigned long long>(), s);
+    }
+    unsigned long long badidx = 0;
+    cudaMemcpyAsync(&badidx, bad.p, 8, cudaMemcpyDeviceToHost, s);
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e) return cuda_fail(e, "norms");
+    if (badidx != ~0ull)
+        return fail(NRLSH_ENONFINITE, "non-finite item at index " + std::to_string(badidx));
+
+    // K2: partition + stable scatter
+    std::string err;
+    int rc;
+    {
+        ProfScope p(SLOT_PARTITION, s);
+        rc = (o.scheme == NRLSH_SCHEME_PERCENTILE)
+                 ? partition_percentile(ix->norm2, n, m, ix->part_of_id, s, &err)
+                 : partition_uniform(ix->norm2, n, m, ix->part_of_id, s, &err);
+    }
+    if (rc) return fail((nrlsh_status)rc, err);
+    {
+        ProfScope p(SLOT_SCATTER, s);
+        rc = partition_scatter(ix->norm2, ix->part_of_id, n, m, ix->perm, ix->pos_of_id,
+                               ix->part_of_pos, ix->offsets_d, ix->V_d, s, &err);
+    }
+    if (rc) return fail((nrlsh_status)rc, err);
+    ix->offsets.resize(m + 1);
+    ix->V.resize(m);
+    cudaMemcpyAsync(ix->offsets.data(), ix->offsets_d, (size_t)(m + 1) * 8, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(ix->V.data(), ix->V_d, (size_t)m * 8, cudaMemcpyDeviceToHost, s);
+    e = cudaStreamSynchronize(s);
+    if (e) return cuda_fail(e, "partition readback");
+    ix->U.resize(m);
+    for (int j = 0; j < m; ++j) ix->U[j] = std::sqrt(ix->V[j]);
+
+    // K4 (host): projection and the sorted (U_j, l) structure
+    make_projection(seed, d + 1, L, ix->A_h);
+    std::vector<float> Apad((size_t)(d + 1) * 32 * W, 0.f);
+    for (int k = 0; k <= d; ++k)
+        for (int b = 0; b < L; ++b) Apad[(size_t)k * 32 * W + b] = ix->A_h[(size_t)k * L + b];
+    std::vector<int32_t> order;
+    make_rank_table(ix->U, L, ix->eps, ix->R_h, order);
+    // scan work units: chunks of <= scan_chunk_items() positions inside one sub-dataset
+    std::vector<int4> chunks;
+    const int CH = scan_chunk_items();
+    for (int j = 0; j < m; ++j)
+        for (int64_t p = ix->offsets[j]; p < ix->offsets[j + 1]; p += CH)
+            chunks.push_back(make_int4(j, (int)p, (int)std::min<int64_t>(p + CH, ix->offsets[j + 1]), 0));
+    ix->nchunks = (int32_t)chunks.size();
+    NR_ALLOC(ix->A, ix->A_h.size() * 4);
+    NR_ALLOC(ix->Apad, Apad.size() * 4);
+    NR_ALLOC(ix->R_d, ix->R_h.size() * 2);
+    NR_ALLOC(ix->order_d, order.size() * 4);
+    NR_ALLOC(ix->chunks_d, chunks.size() * sizeof(int4));
+    cudaMemcpyAsync(ix->A, ix->A_h.data(), ix->A_h.size() * 4, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(ix->Apad, Apad.data(), Apad.size() * 4, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(ix->R_d, ix->R_h.data(), ix->R_h.size() * 2, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(ix->order_d, order.data(), order.size() * 4, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(ix->chunks_d, chunks.data(), chunks.size() * sizeof(int4), cudaMemcpyHostToDevice, s);
+
+    // K3: codes
+    {
+        ProfScope p(SLOT_CODES, s);
+        launch_item_codes(ix->X, n, d, ix->norm2, ix->part_of_id, ix->V_d, ix->Apad, L, W,
+                          ix->pos_of_id, ix->codes, s);
+    }
+    e = cudaStreamSynchronize(s);
+    if (e) return cuda_fail(e, "codes");
+    prof_collect();
+    e = cudaGetLastError();
+    if (e) return cuda_fail(e, "build launch");
+#undef NR_ALLOC
+    *out = ix.release();
+    return NRLSH_OK;
+}
+
+nrlsh_status nrlsh_get_info(const nrlsh_index *ix, int64_t *n, int32_t *d, int32_t *hash_bits,
+                            int32_t *num_parts, int32_t *words) {
+    if (!ix) return fail(NRLSH_EINVAL, "index is NULL");
+    if (n) *n = ix->n;
+    if (d) *d = ix->d;
+    if (hash_bits) *hash_bits = ix->L;
+    if (num_parts) *num_parts = ix->m;
+    if (words) *words = ix->W;
+    return NRLSH_OK;
+}
+
+// ------------------------------------------------------------------ query
+namespace {
+
+int pilot_stride(int64_t n) {
+    if (n <= (1 << 18)) return 1;                 // exact histogram: no fallback needed
+    int64_t s = n / 65536;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(64, s));
+}
+
+int64_t buffer_capacity(int64_t Tq, int stride, int64_t n) {
+    double c = 2.0 * Tq + 16.0 * std::sqrt((double)Tq * stride) + 4096.0;
+    int64_t C = (int64_t)c;
+    C = std::max<int64_t>(C, Tq);
+    return std::min<int64_t>(C, n);
+}
+
+// The candidate pipeline for one sub-batch; leaves cand [Qb x Tq] (item ids).
+void run_candidates(const nrlsh_index *ix, const float *Qd, const uint32_t *qcodes_in, int Qb,
+                    int64_t qbase, int64_t Tq, int stride, int64_t C, uint32_t *qcodes,
+                    int8_t *delta, uint32_t *cnt, unsigned long long *buf, int32_t *cand,
+                    uint16_t *cand_rank, int *flags, unsigned long long *pairs, cudaStream_t s) {
+    if (qcodes_in) {
+        cudaMemcpyAsync(qcodes, qcodes_in + qbase * ix->W, (size_t)Qb * ix->W * 4,
+                        cudaMemcpyDeviceToDevice, s);
+    } else {
+        ProfScope p(SLOT_QCODES, s);
+        launch_qcodes(Qd, Qb, ix->d, ix->Apad, ix->L, ix->W, qcodes, flags, qbase, s);
+    }
+    {
+        ProfScope p(SLOT_PILOT, s);
+        launch_pilot(ix, qcodes, Qb, Tq, stride, delta, cnt, s);
+    }
+    if (getenv("NRLSH_TEST_FORCE_FALLBACK"))   // test switch: empty pilot bound -> fallback
+        cudaMemsetAsync(delta, 0xff, (size_t)Qb * ix->m, s);
+    {
+        ProfScope p(SLOT_SCAN, s);
+        launch_scan(ix, qcodes, delta, Qb, buf, cnt, C, pairs, s);
+    }
+    {
+        ProfScope p(SLOT_FALLBACK, s);
+        launch_fallback(ix, qcodes, Qb, Tq, buf, cnt, C, flags, s);
+    }
+    {
+        ProfScope p(SLOT_SELECT, s);
+        launch_select(ix, Qb, Tq, buf, cnt, C, cand, cand_rank, s);
+    }
+}
+
+nrlsh_status check_flags(const int *hflags) {
+    if (hflags[1] != INT_MAX)
+        return fail(NRLSH_ENONFINITE, "non-finite query at index " + std::to_string(hflags[1]));
+    if (hflags[0] != INT_MAX)
+        return fail(NRLSH_EZERONORM, "zero-norm query at index " + std::to_string(hflags[0]));
+    return NRLSH_OK;
+}
+
+}  // namespace
+
+static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
+                               const uint32_t *qcodes_user, int64_t nq, int32_t k,
+                               int64_t probe_budget, int64_t *out_ids, float *out_scores,
+                               int32_t *cand_out, uint16_t *rank_out, void *cuda_stream) {
+    if (!ix) return fail(NRLSH_EINVAL, "index is NULL");
+    if (nq < 1) return fail(NRLSH_EINVAL, "nq must be >= 1");
+    if (probe_budget < 1) return fail(NRLSH_EINVAL, "probe_budget must be >= 1");
+    const bool want_topk = out_ids != nullptr;
+    if (want_topk && (k < 1 || k > 1024)) return fail(NRLSH_EINVAL, "k must be in [1, 1024]");
+    if (!queries && !qcodes_user) return fail(NRLSH_EINVAL, "queries is NULL");
+    if (want_topk && !queries) return fail(NRLSH_EINVAL, "queries is NULL");
+    if (want_topk && !out_scores) return fail(NRLSH_EINVAL, "out_scores is NULL");
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    configure_pool();
+    const int64_t n = ix->n;
+    const int64_t Tq = std::min<int64_t>(probe_budget, n);
+    const int stride = pilot_stride(n);
+    const int64_t C = buffer_capacity(Tq, stride, n);
+    int Qmax = (int)std::min<int64_t>(ix->query_batch, nq);
+    // keep the candidate buffers bounded (~2.5 GB)
+    const int64_t per_q = C * 8 + Tq * 10;
+    while (Qmax > 64 && (int64_t)Qmax * per_q > (int64_t)2500 << 20) Qmax >>= 1;
+
+    Staged Qs, QCs;
+    cudaError_t e;
+    if (queries) {
+        e = Qs.in(queries, (size_t)nq * ix->d * 4, s);
+        if (e) return cuda_fail(e, "stage queries");
+    }
+    if (qcodes_user) {
+        e = QCs.in(qcodes_user, (size_t)nq * ix->W * 4, s);
+        if (e) return cuda_fail(e, "stage qcodes");
+    }
+    OutBuf oi, os, oc, orr;
+    if (want_topk) {
+        if ((e = oi.init(out_ids, (size_t)nq * k * 8, s))) return cuda_fail(e, "out_ids");
+        if ((e = os.init(out_scores, (size_t)nq * k * 4, s))) return cuda_fail(e, "out_scores");
+    }
+    if (cand_out) {
+        if ((e = oc.init(cand_out, (size_t)nq * Tq * 4, s))) return cuda_fail(e, "cand_ids");
+        if (rank_out && (e = orr.init(rank_out, (size_t)nq * Tq * 2, s))) return cuda_fail(e, "cand_rank");
+    }
+    DBuf qc, dl, cn, bf, cd, sc, fl;
+    if (qc.alloc((size_t)Qmax * ix->W * 4, s) || dl.alloc((size_t)Qmax * ix->m, s) ||
+        cn.alloc((size_t)Qmax * 4, s) || bf.alloc((size_t)Qmax * C * 8, s) ||
+        cd.alloc((size_t)Qmax * Tq * 4, s) || sc.alloc((size_t)Qmax * Tq * 4, s) ||
+        fl.alloc(32, s))
+        return fail(NRLSH_ENOMEM, "query workspace");
+    const int init_flags[8] = {INT_MAX, INT_MAX, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyAsync(fl.p, init_flags, 32, cudaMemcpyHostToDevice, s);
+    unsigned long long *pairs = (unsigned long long *)(fl.get<int>() + 4);
+    const long long launches0 = launch_count();
+    for (int64_t q0 = 0; q0 < nq; q0 += Qmax) {
+        const int Qb = (int)std::min<int64_t>(Qmax, nq - q0);
+        const float *Qd = queries ? (const float *)Qs.dev + q0 * ix->d : nullptr;
+        int32_t *cand = cand_out ? (int32_t *)oc.dev + q0 * Tq : cd.get<int32_t>();
+        uint16_t *crank = (cand_out && rank_out) ? (uint16_t *)orr.dev + q0 * Tq : nullptr;
+        run_candidates(ix, Qd, qcodes_user ? (const uint32_t *)QCs.dev : nullptr, Qb, q0, Tq,
+                       stride, C, qc.get<uint32_t>(), dl.get<int8_t>(), cn.get<uint32_t>(),
+                       bf.get<unsigned long long>(), cand, crank, fl.get<int>(), pairs, s);
+        if (want_topk) {
+            {
+                ProfScope p(SLOT_SCORE, s);
+                launch_score(ix->X, ix->d, Qd, Qb, cand, Tq, Tq, nullptr, 1, nullptr, nullptr,
+                             0.f, sc.get<float>(), s);
+            }
+            ProfScope p(SLOT_TOPK, s);
+            launch_topk(sc.get<float>(), cand, Qb, Tq, Tq, nullptr, 1, k,
+                        (int64_t *)oi.dev + q0 * k, (float *)os.dev + q0 * k, nullptr, s);
+        }
+    }
+    if (want_topk) {
+        if ((e = oi.finish(s)) || (e = os.finish(s))) return cuda_fail(e, "copy results");
+    }
+    if (cand_out) {
+        if ((e = oc.finish(s))) return cuda_fail(e, "copy candidates");
+        if (rank_out && (e = orr.finish(s))) return cuda_fail(e, "copy ranks");
+    }
+    int hflags[8];
+    cudaMemcpyAsync(hflags, fl.p, 32, cudaMemcpyDeviceToHost, s);
+    e = cudaStreamSynchronize(s);
+    if (e) return cuda_fail(e, "query");
+    e = cudaGetLastError();
+    if (e) return cuda_fail(e, "query launch");
+    prof_collect();
+    g_last_fallbacks = hflags[2];
+    g_last_launches = launch_count() - launches0;
+    unsigned long long pr;
+    std::memcpy(&pr, hflags + 4, 8);
+    g_last_pairs = (int64_t)pr;
+    return check_flags(hflags);
+}
+
+nrlsh_status nrlsh_query(const nrlsh_index *ix, const float *queries, int64_t nq, int32_t k,
+                         int64_t probe_budget, int64_t *out_ids, float *out_scores,
+                         void *cuda_stream) {
+    if (!out_ids) return fail(NRLSH_EINVAL, "out_ids is NULL");
+    return query_impl(ix, queries, nullptr, nq, k, probe_budget, out_ids, out_scores, nullptr,
+                      nullptr, cuda_stream);
+}
+
+nrlsh_status nrlsh_query_candidates(const nrlsh_index *ix, const float *queries,
+                                    const uint32_t *qcodes, int64_t nq, int64_t probe_budget,
+                                    int32_t *cand_ids, uint16_t *cand_rank, void *cuda_stream) {
+    if (!cand_ids) return fail(NRLSH_EINVAL, "cand_ids is NULL");
+    return query_impl(ix, queries, qcodes, nq, 1, probe_budget, nullptr, nullptr, cand_ids,
+                      cand_rank, cuda_stream);
+}
+
+nrlsh_status nrlsh_query_codes(const nrlsh_index *ix, const float *queries, int64_t nq,
+                               uint32_t *qcodes, void *cuda_stream) {
+    if (!ix || !queries || !qcodes || nq < 1) return fail(NRLSH_EINVAL, "bad argument");
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    configure_pool();
+    Staged Qs;
+    cudaError_t e = Qs.in(queries, (size_t)nq * ix->d * 4, s);
+    if (e) return cuda_fail(e, "stage queries");
+    OutBuf oq;
+    if ((e = oq.init(qcodes, (size_t)nq * ix->W * 4, s))) return cuda_fail(e, "qcodes");
+    DBuf fl;
+    if (fl.alloc(16, s)) return fail(NRLSH_ENOMEM, "flags");
+    const int init_flags[4] = {INT_MAX, INT_MAX, 0, 0};
+    cudaMemcpyAsync(fl.p, init_flags, 16, cudaMemcpyHostToDevice, s);
+    for (int64_t q0 = 0; q0 < nq; q0 += 65535) {
+        const int Qb = (int)std::min<int64_t>(65535, nq - q0);
+        launch_qcodes((const float *)Qs.dev + q0 * ix->d, Qb, ix->d, ix->Apad, ix->L, ix->W,
+                      (uint32_t *)oq.dev + q0 * ix->W, fl.get<int>(), q0, s);
+    }
+    if ((e = oq.finish(s))) return cuda_fail(e, "copy qcodes");
+    int hflags[4];
+    cudaMemcpyAsync(hflags, fl.p, 16, cudaMemcpyDeviceToHost, s);
+    e = cudaStreamSynchronize(s);
+    if (e) return cuda_fail(e, "query codes");
+    return check_flags(hflags);
+}
+
+nrlsh_status nrlsh_last_query_stats(int64_t *fallback_queries, int64_t *kernel_launches,
+                                    int64_t *scanned_pairs) {
+    if (fallback_queries) *fallback_queries = g_last_fallbacks;
+    if (kernel_launches) *kernel_launches = g_last_launches;
+    if (scanned_pairs) *scanned_pairs = g_last_pairs;
+    return NRLSH_OK;
+}
+
+// ------------------------------------------------------------ exact top-k
+static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const float *queries,
+                               int64_t nq, int32_t k, int64_t *out_ids, float *out_scores,
+                               void *cuda_stream) {
+    if (!items || !queries || !out_ids || !out_scores) return fail(NRLSH_EINVAL, "NULL argument");
+    if (n < 1 || n >= (1ll << 31)) return fail(NRLSH_EINVAL, "n must be in [1, 2^31)");
+    if (d < 1 || d > 4096) return fail(NRLSH_EINVAL, "d must be in [1, 4096]");
+    if (nq < 1) return fail(NRLSH_EINVAL, "nq must be >= 1");
+    if (k < 1 || k > 1024) return fail(NRLSH_EINVAL, "k must be in [1, 1024]");
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    configure_pool();
+    cudaError_t e;
+    Staged Xs, Qs;
+    if ((e = Xs.in(items, (size_t)n * d * 4, s))) return cuda_fail(e, "stage items");
+    if ((e = Qs.in(queries, (size_t)nq * d * 4, s))) return cuda_fail(e, "stage queries");
+    OutBuf oi, os;
+    if ((e = oi.init(out_ids, (size_t)nq * k * 8, s))) return cuda_fail(e, "out_ids");
+    if ((e = os.init(out_scores, (size_t)nq * k * 4, s))) return cuda_fail(e, "out_scores");
+    const float *X = (const float *)Xs.dev;
+    const float *Q = (const float *)Qs.dev;
+    // fp32 error bound of any summation order of d products: gamma_d |q||x|, inflated
+    const float eps_rel = (float)(1.25 * (d + 2) * std::ldexp(1.0, -24));
+    const int S = (int)std::max<int64_t>(1, std::min<int64_t>(64, n / (4 * (int64_t)k)));
+    const int64_t ns = (n + S - 1) / S;
+    const int64_t Cg = std::min<int64_t>(n, std::max<int64_t>(4 * (int64_t)S * k + 4096, 2 * k));
+    int Qmax = (int)std::min<int64_t>(1024, nq);
+    while (Qmax > 64 && (int64_t)Qmax * (ns * 4 + Cg * 8) > ((int64_t)2500 << 20)) Qmax >>= 1;
+    DBuf xn, qn, ss, lb, tid, tsc, cc, cd, cs, fl;
+    if (xn.alloc((size_t)n * 4, s) || qn.alloc((size_t)nq * 4, s) ||
+        ss.alloc((size_t)Qmax * ns * 4, s) || lb.alloc((size_t)Qmax * 4, s) ||
+        tid.alloc((size_t)Qmax * k * 8, s) || tsc.alloc((size_t)Qmax * k * 4, s) ||
+        cc.alloc((size_t)Qmax * 4, s) || cd.alloc((size_t)Qmax * Cg * 4, s) ||
+        cs.alloc((size_t)Qmax * Cg * 4, s))
+        return fail(NRLSH_ENOMEM, "exact_topk workspace");
+    {
+        ProfScope p(SLOT_GT_NORMS, s);
+        launch_vec_norms(X, n, d, xn.get<float>(), s);
+        launch_vec_norms(Q, nq, d, qn.get<float>(), s);
+    }
+    std::vector<uint32_t> hcnt(Qmax);
+    DBuf full;
+    for (int64_t q0 = 0; q0 < nq; q0 += Qmax) {
+        const int Qb = (int)std::min<int64_t>(Qmax, nq - q0);
+        const float *Qb_ptr = Q + q0 * d;
+        const float *qnb = qn.get<float>() + q0;
+        int64_t *oid = (int64_t *)oi.dev + q0 * k;
+        float *osc = (float *)os.dev + q0 * k;
+        // pilot: certified lower bound of the k-th best score
+        {
+            ProfScope p(SLOT_SCORE, s);
+            launch_score(X, d, Qb_ptr, Qb, nullptr, ns, ns, nullptr, S, xn.get<float>(), qnb,
+                         eps_rel, ss.get<float>(), s);
+        }
+        {
+            ProfScope p(SLOT_TOPK, s);
+            launch_topk(ss.get<float>(), nullptr, Qb, ns, ns, nullptr, S, k, tid.get<int64_t>(),
+                        tsc.get<float>(), lb.get<float>(), s);
+        }
+        cudaMemsetAsync(cc.p, 0, (size_t)Qb * 4, s);
+        {
+            ProfScope p(SLOT_GT_FILTER, s);
+            launch_gt_filter(X, n, d, Qb_ptr, Qb, xn.get<float>(), qnb, lb.get<float>(), eps_rel,
+                             cd.get<int32_t>(), cc.get<uint32_t>(), Cg, s);
+        }
+        {
+            ProfScope p(SLOT_SCORE, s);
+            launch_score(X, d, Qb_ptr, Qb, cd.get<int32_t>(), Cg, Cg, cc.get<uint32_t>(), 1,
+                         nullptr, nullptr, 0.f, cs.get<float>(), s);
+        }
+        {
+            ProfScope p(SLOT_TOPK, s);
+            launch_topk(cs.get<float>(), cd.get<int32_t>(), Qb, Cg, Cg, cc.get<uint32_t>(), 1, k,
+                        oid, osc, nullptr, s);
+        }
+        // overflowing queries (rare): exact scoring of every item
+        cudaMemcpyAsync(hcnt.data(), cc.p, (size_t)Qb * 4, cudaMemcpyDeviceToHost, s);
+        if ((e = cudaStreamSynchronize(s))) return cuda_fail(e, "exact_topk");
+        for (int qi = 0; qi < Qb; ++qi) {
+            if (hcnt[qi] <= (uint32_t)Cg) continue;
+            if (!full.p && full.alloc((size_t)n * 4, s)) return fail(NRLSH_ENOMEM, "exact_topk scratch");
+            launch_score(X, d, Qb_ptr + (int64_t)qi * d, 1, nullptr, n, n, nullptr, 1, nullptr,
+                         nullptr, 0.f, full.get<float>(), s);
+            launch_topk(full.get<float>(), nullptr, 1, n, n, nullptr, 1, k, oid + (int64_t)qi * k,
+                        osc + (int64_t)qi * k, nullptr, s);
+        }
+    }
+    if ((e = oi.finish(s)) || (e = os.finish(s))) return cuda_fail(e, "copy results");
+    e = cudaStreamSynchronize(s);
+    if (e) return cuda_fail(e, "exact_topk");
+    e = cudaGetLastError();
+    if (e) return cuda_fail(e, "exact_topk launch");
+    prof_collect();
+    return NRLSH_OK;
+}
+
+nrlsh_status nrlsh_exact_topk(const float *items, int64_t n, int32_t d, const float *queries,
+                              int64_t nq, int32_t k, int64_t *out_ids, float *out_scores,
+                              void *cuda_stream) {
+    return exact_impl(items, n, d, queries, nq, k, out_ids, out_scores, cuda_stream);
+}
+
+nrlsh_status nrlsh_index_exact_topk(const nrlsh_index *ix, const float *queries, int64_t nq,
+                                    int32_t k, int64_t *out_ids, float *out_scores,
+                                    void *cuda_stream) {
+    if (!ix) return fail(NRLSH_EINVAL, "index is NULL");
+    return exact_impl(ix->X, ix->n, ix->d, queries, nq, k, out_ids, out_scores, cuda_stream);
+}
+
+// ------------------------------------------------------------------ hooks
+static nrlsh_status copy_out(void *dst, const void *src, size_t bytes) {
+    if (!dst) return NRLSH_OK;
+    cudaError_t e = cudaMemcpy(dst, src, bytes, cudaMemcpyDefault);
+    if (e) return cuda_fail(e, "copy");
+    return NRLSH_OK;
+}
+
+nrlsh_status nrlsh_get_partition(const nrlsh_index *ix, double *norm2, int32_t *perm,
+                                 int64_t *offsets, double *V) {
+    if (!ix) return fail(NRLSH_EINVAL, "index is NULL");
+    nrlsh_status st;
+    if ((st = copy_out(norm2, ix->norm2, (size_t)ix->n * 8))) return st;
+    if ((st = copy_out(perm, ix->perm, (size_t)ix->n * 4))) return st;
+    if ((st = copy_out(offsets, ix->offsets_d, (size_t)(ix->m + 1) * 8))) return st;
+    return copy_out(V, ix->V_d, (size_t)ix->m * 8);
+}
+
+nrlsh_status nrlsh_get_projection(const nrlsh_index *ix, float *A) {
+    if (!ix || !A) return fail(NRLSH_EINVAL, "bad argument");
+    return copy_out(A, ix->A, ix->A_h.size() * 4);
+}
+
+nrlsh_status nrlsh_get_rank_table(const nrlsh_index *ix, uint16_t *R) {
+    if (!ix || !R) return fail(NRLSH_EINVAL, "bad argument");
+    return copy_out(R, ix->R_d, ix->R_h.size() * 2);
+}
+
+nrlsh_status nrlsh_get_codes(const nrlsh_index *ix, uint32_t *codes) {
+    if (!ix || !codes) return fail(NRLSH_EINVAL, "bad argument");
+    return copy_out(codes, ix->codes, (size_t)ix->n * ix->W * 4);
+}
+
+nrlsh_status nrlsh_set_codes(nrlsh_index *ix, const uint32_t *codes) {
+    if (!ix || !codes) return fail(NRLSH_EINVAL, "bad argument");
+    cudaError_t e = cudaMemcpy(ix->codes, codes, (size_t)ix->n * ix->W * 4, cudaMemcpyDefault);
+    if (e) return cuda_fail(e, "set codes");
+    return NRLSH_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,752 @@
+// build_kernels.cu — index building kernels (Alg. 1) for sm_100a.
+//
+//  K1  norms:      ||x_i||^2 in fp64, sequential over k (bit-identical to the
+//                  plain definition; Alg. 1 l.3).  HBM stream of X.
+//  K2  partition:  exact multi-select of the m-1 percentile boundaries on the
+//                  (norm2 bits, id) keys (Alg. 1 l.4; ties by id,
+//                  PAPER:173), then a stable scatter into sub-dataset order.
+//  K3  codes:      y = X A[:d] + A[d] t,  t = sqrt(V_j - ||x||^2)  (the
+//                  SIMPLE-LSH transform of Eq. (8) scaled by U_j > 0), bit =
+//                  [y >= 0] (Eq. (4)), packed LSB-first, written at the item's
+//                  position in sub-dataset order.
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace nrlsh {
+
+// =========================================================================== K1
+// One CTA tile = RT rows.  Warps stage rows coalesced into shared memory (row
+// stride ld odd -> conflict-free column walk), then thread r sums row r in
+// order k = 0..d-1 in fp64 (each square is exact, so the result is the
+// correctly-defined sequential sum).
+template <int RT>
+__global__ void __launch_bounds__(RT) k1_norms_tiled(const float *__restrict__ X, int64_t n, int d,
+                                                     int ld, double *__restrict__ norm2,
+                                                     unsigned long long *__restrict__ bad) {
+    extern __shared__ float tile[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int NW = RT / 32;
+    for (int64_t base = (int64_t)blockIdx.x * RT; base < n; base += (int64_t)gridDim.x * RT) {
+        const int rows = (int)min((int64_t)RT, n - base);
+#pragma unroll 4
+        for (int r = warp; r < rows; r += NW) {
+            const float *src = X + (base + r) * (int64_t)d;
+            for (int k = lane; k < d; k += 32) tile[r * ld + k] = __ldg(src + k);
+        }
+        __syncthreads();
+        const int r = threadIdx.x;
+        if (r < rows) {
+            double s = 0.0;
+            const float *t = tile + r * ld;
+            for (int k = 0; k < d; ++k) {
+                double v = (double)t[k];
+                s = __dadd_rn(s, __dmul_rn(v, v));
+            }
+            norm2[base + r] = s;
+            if (!isfinite(s)) atomicMin(bad, (unsigned long long)(base + r));
+        }
+        __syncthreads();
+    }
+}
+
+// Very wide rows: one thread per row straight from global memory.
+__global__ void k1_norms_direct(const float *__restrict__ X, int64_t n, int d,
+                                double *__restrict__ norm2, unsigned long long *__restrict__ bad) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const float *src = X + i * (int64_t)d;
+        double s = 0.0;
+        for (int k = 0; k < d; ++k) {
+            double v = (double)__ldg(src + k);
+            s = __dadd_rn(s, __dmul_rn(v, v));
+        }
+        norm2[i] = s;
+        if (!isfinite(s)) atomicMin(bad, (unsigned long long)i);
+    }
+}
+
+void launch_norms(const float *X, int64_t n, int d, double *norm2, unsigned long long *bad,
+                  cudaStream_t s) {
+    const int ld = (d % 2 == 1) ? d : d + 1;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const size_t lim = 200 * 1024;
+    if ((size_t)256 * ld * 4 <= lim / 2) {
+        size_t sm = (size_t)256 * ld * 4;
+        cudaFuncSetAttribute(k1_norms_tiled<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        k1_norms_tiled<256><<<grid_for(n, 256, sms * 8), 256, sm, s>>>(X, n, d, ld, norm2, bad);
+    } else if ((size_t)128 * ld * 4 <= lim) {
+        size_t sm = (size_t)128 * ld * 4;
+        cudaFuncSetAttribute(k1_norms_tiled<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        k1_norms_tiled<128><<<grid_for(n, 128, sms * 8), 128, sm, s>>>(X, n, d, ld, norm2, bad);
+    } else if ((size_t)32 * ld * 4 <= lim) {
+        size_t sm = (size_t)32 * ld * 4;
+        cudaFuncSetAttribute(k1_norms_tiled<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        k1_norms_tiled<32><<<grid_for(n, 32, sms * 16), 32, sm, s>>>(X, n, d, ld, norm2, bad);
+    } else {
+        k1_norms_direct<<<grid_for(n, 256, sms * 8), 256, 0, s>>>(X, n, d, norm2, bad);
+    }
+    note_launch();
+}
+
+// =========================================================================== K2
+// Exact multi-select.  The 96-bit composite key c_i = (bits(norm2_i) : id_i) is
+// unique and its unsigned order is the ranking order of Alg. 1 (norm2 >= 0, so
+// the IEEE bit pattern is monotone).  Rank r goes to sub-dataset floor(r m / n);
+// boundary b_j = ceil(j n / m) is the first rank of sub-dataset j.  A level
+// histograms one digit of c over a candidate list, locates the boundaries, and
+// (i) assigns every item of a bin that no boundary splits directly, (ii) moves
+// items of split bins into per-bin sub-lists, which are either sorted in shared
+// memory (small) or refined by the next digit (large).
+struct SelGroup {
+    uint32_t bin;
+    uint32_t count;
+    int64_t base;     // rank of the bin's first item
+    int64_t cand_off; // offset of the bin's sub-list
+};
+
+struct SelLevel {
+    int shift, width;
+};
+// digits over bits 95..0 of (key64 : id32), most significant first
+static const SelLevel kLevels[] = {{72, 24}, {56, 16}, {40, 16}, {32, 8}, {16, 16}, {0, 16}};
+constexpr int kNumLevels = 6;
+constexpr int kSmallGroup = 2048;
+constexpr int kMaxGroups = kMaxParts;
+
+__device__ __forceinline__ uint32_t digit96(uint64_t key, uint32_t id, int shift, int width) {
+    const uint32_t mask = (width >= 32) ? 0xffffffffu : ((1u << width) - 1u);
+    if (shift >= 32) return (uint32_t)(key >> (shift - 32)) & mask;
+    return (id >> shift) & mask;
+}
+
+template <bool Implicit>
+__device__ __forceinline__ void load_item(const double *norm2, const uint64_t *keys,
+                                          const uint32_t *ids, int64_t i, uint64_t &key,
+                                          uint32_t &id) {
+    if (Implicit) {
+        key = (uint64_t)__double_as_longlong(norm2[i]);
+        id = (uint32_t)i;
+    } else {
+        key = keys[i];
+        id = ids[i];
+    }
+}
+
+template <bool Implicit>
+__global__ void sel_hist(const double *__restrict__ norm2, const uint64_t *__restrict__ keys,
+                         const uint32_t *__restrict__ ids, int64_t count, int shift, int width,
+                         uint32_t *__restrict__ H) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t key;
+        uint32_t id;
+        load_item<Implicit>(norm2, keys, ids, i, key, id);
+        atomicAdd(&H[digit96(key, id, shift, width)], 1u);
+    }
+}
+
+// 3-phase exclusive scan of uint32 (nbins <= 4096 * 4096).
+__global__ void __launch_bounds__(1024) scan_tiles(const uint32_t *__restrict__ in,
+                                                   uint32_t *__restrict__ out, int64_t nbins,
+                                                   uint32_t *__restrict__ tile_sums) {
+    __shared__ uint32_t ws[32];
+    const int64_t base = (int64_t)blockIdx.x * 4096 + threadIdx.x * 4;
+    uint32_t v[4];
+    uint32_t loc = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        v[e] = (base + e < nbins) ? in[base + e] : 0u;
+        loc += v[e];
+    }
+    uint32_t tot;
+    uint32_t ex = block_excl_scan(loc, ws, &tot);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        if (base + e < nbins) out[base + e] = ex;
+        ex += v[e];
+    }
+    if (threadIdx.x == 0) tile_sums[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(1024) scan_sums(uint32_t *__restrict__ tile_sums, int ntiles) {
+    __shared__ uint32_t ws[32];
+    uint32_t v[4];
+    uint32_t loc = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        int t = threadIdx.x * 4 + e;
+        v[e] = t < ntiles ? tile_sums[t] : 0u;
+        loc += v[e];
+    }
+    uint32_t ex = block_excl_scan(loc, ws, nullptr);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        int t = threadIdx.x * 4 + e;
+        if (t < ntiles) tile_sums[t] = ex;
+        ex += v[e];
+    }
+}
+
+__global__ void scan_add(uint32_t *__restrict__ out, int64_t nbins,
+                         const uint32_t *__restrict__ tile_sums) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < nbins) out[i] += tile_sums[i / 4096];
+}
+
+static void scan_excl(const uint32_t *in, uint32_t *out, int64_t nbins, uint32_t *tile_sums,
+                      cudaStream_t s) {
+    const int ntiles = (int)((nbins + 4095) / 4096);
+    scan_tiles<<<ntiles, 1024, 0, s>>>(in, out, nbins, tile_sums);
+    if (ntiles > 1) {
+        scan_sums<<<1, 1024, 0, s>>>(tile_sums, ntiles);
+        scan_add<<<(int)((nbins + 255) / 256), 256, 0, s>>>(out, nbins, tile_sums);
+    }
+}
+
+// Locate the boundaries inside [base, base+count) and list the bins they split.
+// One block of >= m threads.  out_meta[0] = ngroups, out_meta[1] = total candidates.
+__global__ void sel_locate(const uint32_t *__restrict__ H, const uint32_t *__restrict__ P,
+                           int64_t nbins, int64_t base, int64_t count, int64_t n, int m,
+                           SelGroup *__restrict__ groups, int64_t *__restrict__ out_meta) {
+    __shared__ int64_t sbin[kMaxParts];
+    const int j = threadIdx.x;
+    if (j < m) {
+        sbin[j] = -1;
+        if (j >= 1) {
+            const int64_t b = (j * n + m - 1) / m;   // ceil(j n / m)
+            if (b > base && b < base + count) {      // boundary strictly inside the list
+                const uint32_t loc = (uint32_t)(b - base);
+                int64_t lo = 0, hi = nbins - 1;      // largest bin with P[bin] <= loc
+                while (lo < hi) {
+                    int64_t mid = (lo + hi + 1) >> 1;
+                    if (P[mid] <= loc) lo = mid; else hi = mid - 1;
+                }
+                // the bin containing rank loc; it is split only if loc is not its first rank
+                if (P[lo] < loc) sbin[j] = lo;
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int g = 0;
+        int64_t last = -1, off = 0;
+        for (int jj = 1; jj < m; ++jj) {
+            int64_t bn = sbin[jj];
+            if (bn < 0 || bn == last) continue;
+            last = bn;
+            groups[g].bin = (uint32_t)bn;
+            groups[g].count = H[bn];
+            groups[g].base = base + P[bn];
+            groups[g].cand_off = off;
+            off += H[bn];
+            ++g;
+        }
+        out_meta[0] = g;
+        out_meta[1] = off;
+    }
+}
+
+template <bool Implicit>
+__global__ void sel_classify(const double *__restrict__ norm2, const uint64_t *__restrict__ keys,
+                             const uint32_t *__restrict__ ids, int64_t count, int shift,
+                             int width, const uint32_t *__restrict__ P, int64_t base, int64_t n,
+                             int m, const SelGroup *__restrict__ groups,
+                             const int64_t *__restrict__ meta, uint32_t *__restrict__ fill,
+                             uint64_t *__restrict__ out_keys, uint32_t *__restrict__ out_ids,
+                             uint8_t *__restrict__ part) {
+    __shared__ uint32_t gbin[kMaxGroups];
+    __shared__ int64_t goff[kMaxGroups];
+    const int ng = (int)meta[0];
+    for (int g = threadIdx.x; g < ng; g += blockDim.x) {
+        gbin[g] = groups[g].bin;
+        goff[g] = groups[g].cand_off;
+    }
+    __syncthreads();
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t key;
+        uint32_t id;
+        load_item<Implicit>(norm2, keys, ids, i, key, id);
+        const uint32_t dg = digit96(key, id, shift, width);
+        int lo = 0, hi = ng;   // first group with bin >= dg
+        while (lo < hi) {
+            int mid = (lo + hi) >> 1;
+            if (gbin[mid] < dg) lo = mid + 1; else hi = mid;
+        }
+        if (lo < ng && gbin[lo] == dg) {
+            const uint32_t slot = atomicAdd(&fill[lo], 1u);
+            out_keys[goff[lo] + slot] = key;
+            out_ids[goff[lo] + slot] = id;
+        } else {
+            const int64_t r = base + (int64_t)P[dg];
+            part[id] = (uint8_t)((r * m) / n);
+        }
+    }
+}
+
+// Sort each small group's (key, id) list in shared memory and assign ranks.
+__global__ void __launch_bounds__(1024) sel_resolve_small(
+    const SelGroup *__restrict__ groups, const int *__restrict__ gidx,
+    const uint64_t *__restrict__ keys, const uint32_t *__restrict__ ids, int64_t n, int m,
+    uint8_t *__restrict__ part) {
+    __shared__ uint64_t sk[kSmallGroup];
+    __shared__ uint32_t si[kSmallGroup];
+    const SelGroup g = groups[gidx[blockIdx.x]];
+    const int cnt = (int)g.count;
+    int np2 = 1;
+    while (np2 < cnt) np2 <<= 1;
+    for (int t = threadIdx.x; t < np2; t += blockDim.x) {
+        if (t < cnt) {
+            sk[t] = keys[g.cand_off + t];
+            si[t] = ids[g.cand_off + t];
+        } else {
+            sk[t] = ~0ull;
+            si[t] = 0xffffffffu;
+        }
+    }
+    __syncthreads();
+    for (int size = 2; size <= np2; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int t = threadIdx.x; t < np2; t += blockDim.x) {
+                const int o = t ^ stride;
+                if (o > t) {
+                    const bool up = ((t & size) == 0);
+                    const bool gt = (sk[t] > sk[o]) || (sk[t] == sk[o] && si[t] > si[o]);
+                    if (gt == up) {
+                        uint64_t tk = sk[t]; sk[t] = sk[o]; sk[o] = tk;
+                        uint32_t ti = si[t]; si[t] = si[o]; si[o] = ti;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int t = threadIdx.x; t < cnt; t += blockDim.x) {
+        const int64_t r = g.base + t;
+        part[si[t]] = (uint8_t)((r * m) / n);
+    }
+}
+
+namespace {
+struct DevBuf {
+    void *p = nullptr;
+    ~DevBuf() { if (p) cudaFree(p); }
+    template <class T> T *get() { return (T *)p; }
+    cudaError_t alloc(size_t bytes) {
+        if (p) { cudaFree(p); p = nullptr; }
+        return cudaMalloc(&p, bytes ? bytes : 16);
+    }
+};
+}  // namespace
+
+int partition_percentile(const double *norm2, int64_t n, int m, uint8_t *part, cudaStream_t s,
+                         std::string *err) {
+    if (m == 1) {
+        cudaMemsetAsync(part, 0, (size_t)n, s);
+        return 0;
+    }
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int64_t maxbins = 1ll << 24;
+    DevBuf H, P, TS, G, META, FILL;
+    if (H.alloc(maxbins * 4) || P.alloc(maxbins * 4) || TS.alloc(4096 * 4) ||
+        G.alloc(sizeof(SelGroup) * kMaxGroups) || META.alloc(16) || FILL.alloc(kMaxGroups * 4)) {
+        *err = "partition: cudaMalloc failed";
+        return NRLSH_ENOMEM;
+    }
+    struct Problem {
+        const uint64_t *keys;  // nullptr => implicit (all items)
+        const uint32_t *ids;
+        int64_t count, base;
+        int level;
+        std::shared_ptr<DevBuf> kbuf, ibuf;  // keep parent lists alive
+    };
+    std::vector<Problem> stack;
+    stack.push_back({nullptr, nullptr, n, 0, 0, nullptr, nullptr});
+    std::vector<SelGroup> hg(kMaxGroups);
+    while (!stack.empty()) {
+        Problem pb = stack.back();
+        stack.pop_back();
+        if (pb.level >= kNumLevels) {
+            *err = "partition: exhausted key digits";
+            return NRLSH_ECUDA;
+        }
+        const SelLevel lv = kLevels[pb.level];
+        const int64_t nbins = 1ll << lv.width;
+        cudaMemsetAsync(H.p, 0, nbins * 4, s);
+        const int grid = grid_for(pb.count, 256, sms * 16);
+        if (pb.keys == nullptr)
+            sel_hist<true><<<grid, 256, 0, s>>>(norm2, nullptr, nullptr, pb.count, lv.shift,
+                                                lv.width, H.get<uint32_t>());
+        else
+            sel_hist<false><<<grid, 256, 0, s>>>(nullptr, pb.keys, pb.ids, pb.count, lv.shift,
+                                                 lv.width, H.get<uint32_t>());
+        scan_excl(H.get<uint32_t>(), P.get<uint32_t>(), nbins, TS.get<uint32_t>(), s);
+        note_launch(nbins > 4096 ? 5 : 3);
+        sel_locate<<<1, kMaxParts, 0, s>>>(H.get<uint32_t>(), P.get<uint32_t>(), nbins, pb.base,
+                                           pb.count, n, m, G.get<SelGroup>(), META.get<int64_t>());
+        int64_t meta[2];
+        cudaMemcpyAsync(meta, META.p, 16, cudaMemcpyDeviceToHost, s);
+        cudaError_t e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) {
+            *err = std::string("partition: ") + cudaGetErrorString(e);
+            return NRLSH_ECUDA;
+        }
+        const int ng = (int)meta[0];
+        const int64_t tot = meta[1];
+        auto kb = std::make_shared<DevBuf>();
+        auto ib = std::make_shared<DevBuf>();
+        if (kb->alloc(tot * 8) || ib->alloc(tot * 4)) {
+            *err = "partition: cudaMalloc failed (candidates)";
+            return NRLSH_ENOMEM;
+        }
+        cudaMemsetAsync(FILL.p, 0, kMaxGroups * 4, s);
+        if (pb.keys == nullptr)
+            sel_classify<true><<<grid, 256, 0, s>>>(
+                norm2, nullptr, nullptr, pb.count, lv.shift, lv.width, P.get<uint32_t>(), pb.base,
+                n, m, G.get<SelGroup>(), META.get<int64_t>(), FILL.get<uint32_t>(),
+                kb->get<uint64_t>(), ib->get<uint32_t>(), part);
+        else
+            sel_classify<false><<<grid, 256, 0, s>>>(
+                nullptr, pb.keys, pb.ids, pb.count, lv.shift, lv.width, P.get<uint32_t>(), pb.base,
+                n, m, G.get<SelGroup>(), META.get<int64_t>(), FILL.get<uint32_t>(),
+                kb->get<uint64_t>(), ib->get<uint32_t>(), part);
+        if (ng == 0) continue;
+        cudaMemcpyAsync(hg.data(), G.p, sizeof(SelGroup) * ng, cudaMemcpyDeviceToHost, s);
+        e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) {
+            *err = std::string("partition: ") + cudaGetErrorString(e);
+            return NRLSH_ECUDA;
+        }
+        std::vector<int> small;
+        for (int g = 0; g < ng; ++g) {
+            if (hg[g].count <= (uint32_t)kSmallGroup) {
+                small.push_back(g);
+            } else {
+                Problem ch;
+                ch.keys = kb->get<uint64_t>() + hg[g].cand_off;
+                ch.ids = ib->get<uint32_t>() + hg[g].cand_off;
+                ch.count = hg[g].count;
+                ch.base = hg[g].base;
+                ch.level = pb.level + 1;
+                ch.kbuf = kb;
+                ch.ibuf = ib;
+                stack.push_back(ch);
+            }
+        }
+        if (!small.empty()) {
+            DevBuf gi;
+            if (gi.alloc(small.size() * 4)) {
+                *err = "partition: cudaMalloc failed";
+                return NRLSH_ENOMEM;
+            }
+            // groups table is reused by the next level: copy this level's groups aside
+            DevBuf gcopy;
+            gcopy.alloc(sizeof(SelGroup) * ng);
+            cudaMemcpyAsync(gcopy.p, G.p, sizeof(SelGroup) * ng, cudaMemcpyDeviceToDevice, s);
+            cudaMemcpyAsync(gi.p, small.data(), small.size() * 4, cudaMemcpyHostToDevice, s);
+            note_launch();
+            sel_resolve_small<<<(int)small.size(), 1024, 0, s>>>(
+                gcopy.get<SelGroup>(), gi.get<int>(), kb->get<uint64_t>(), ib->get<uint32_t>(), n,
+                m, part);
+            e = cudaStreamSynchronize(s);   // gi/gcopy are freed on scope exit
+            if (e != cudaSuccess) {
+                *err = std::string("partition: ") + cudaGetErrorString(e);
+                return NRLSH_ECUDA;
+            }
+        }
+    }
+    return 0;
+}
+
+// ------------------------------------------------------------- uniform (NEXT-2)
+__global__ void minmax_bits(const double *__restrict__ norm2, int64_t n,
+                            unsigned long long *__restrict__ mm) {
+    unsigned long long lo = ~0ull, hi = 0ull;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        unsigned long long b = (unsigned long long)__double_as_longlong(norm2[i]);
+        lo = b < lo ? b : lo;
+        hi = b > hi ? b : hi;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long l2 = __shfl_xor_sync(NR_FULL, lo, o);
+        unsigned long long h2 = __shfl_xor_sync(NR_FULL, hi, o);
+        lo = l2 < lo ? l2 : lo;
+        hi = h2 > hi ? h2 : hi;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(&mm[0], lo);
+        atomicMax(&mm[1], hi);
+    }
+}
+
+// Sub-dataset j holds norms in the j-th of m equal-width intervals of
+// [min ||x||, max ||x||] (Fig. 3(a)).  sqrt is monotone, so the
+// interval ends are sqrt(min norm2), sqrt(max norm2).
+__global__ void uniform_assign(const double *__restrict__ norm2, int64_t n, int m,
+                               const unsigned long long *__restrict__ mm,
+                               uint8_t *__restrict__ part) {
+    const double lo = sqrt(__longlong_as_double((long long)mm[0]));
+    const double hi = sqrt(__longlong_as_double((long long)mm[1]));
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double r = sqrt(norm2[i]);
+        long long j = 0;
+        if (hi > lo) {
+            j = (long long)floor(__dmul_rn(__ddiv_rn(__dsub_rn(r, lo), __dsub_rn(hi, lo)), (double)m));
+            if (j >= m) j = m - 1;
+            if (j < 0) j = 0;
+        }
+        part[i] = (uint8_t)j;
+    }
+}
+
+int partition_uniform(const double *norm2, int64_t n, int m, uint8_t *part, cudaStream_t s,
+                      std::string *err) {
+    DevBuf mm;
+    if (mm.alloc(16)) {
+        *err = "partition: cudaMalloc failed";
+        return NRLSH_ENOMEM;
+    }
+    unsigned long long init[2] = {~0ull, 0ull};
+    cudaMemcpyAsync(mm.p, init, 16, cudaMemcpyHostToDevice, s);
+    minmax_bits<<<grid_for(n, 256, 1024), 256, 0, s>>>(norm2, n, mm.get<unsigned long long>());
+    note_launch(2);
+    uniform_assign<<<grid_for(n, 256, 4096), 256, 0, s>>>(norm2, n, m,
+                                                         mm.get<unsigned long long>(), part);
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+        *err = std::string("partition: ") + cudaGetErrorString(e);
+        return NRLSH_ECUDA;
+    }
+    return 0;
+}
+
+// ------------------------------------------------------------ stable scatter
+constexpr int kScatTile = 4096;   // items per tile (16 rounds of 256)
+
+__global__ void __launch_bounds__(256) scat_hist(const double *__restrict__ norm2,
+                                                 const uint8_t *__restrict__ part, int64_t n,
+                                                 int m, uint32_t *__restrict__ tile_cnt,
+                                                 unsigned long long *__restrict__ vmax) {
+    __shared__ uint32_t c[kMaxParts];
+    __shared__ unsigned long long v[kMaxParts];
+    for (int j = threadIdx.x; j < m; j += blockDim.x) { c[j] = 0; v[j] = 0; }
+    __syncthreads();
+    const int64_t base = (int64_t)blockIdx.x * kScatTile;
+    for (int t = threadIdx.x; t < kScatTile; t += blockDim.x) {
+        const int64_t i = base + t;
+        if (i < n) {
+            const int j = part[i];
+            atomicAdd(&c[j], 1u);
+            atomicMax(&v[j], (unsigned long long)__double_as_longlong(norm2[i]));
+        }
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < m; j += blockDim.x) {
+        tile_cnt[(int64_t)blockIdx.x * m + j] = c[j];
+        if (c[j]) atomicMax(&vmax[j], v[j]);
+    }
+}
+
+// one block of 256 threads: offsets (exclusive over j) and per-tile bases
+__global__ void __launch_bounds__(256) scat_scan(uint32_t *__restrict__ tile_cnt, int ntiles,
+                                                 int m, int64_t *__restrict__ offsets,
+                                                 const unsigned long long *__restrict__ vmax,
+                                                 double *__restrict__ V) {
+    __shared__ uint32_t ws[32];
+    const int j = threadIdx.x;
+    uint32_t tot = 0;
+    if (j < m)
+        for (int t = 0; t < ntiles; ++t) tot += tile_cnt[(int64_t)t * m + j];
+    uint32_t all;
+    const uint32_t ex = block_excl_scan(tot, ws, &all);
+    if (j < m) {
+        offsets[j] = ex;
+        V[j] = __longlong_as_double((long long)vmax[j]);
+        uint32_t run = ex;
+        for (int t = 0; t < ntiles; ++t) {
+            const uint32_t c = tile_cnt[(int64_t)t * m + j];
+            tile_cnt[(int64_t)t * m + j] = run;
+            run += c;
+        }
+    }
+    if (j == 0) offsets[m] = all;
+}
+
+__global__ void __launch_bounds__(256) scat_write(const uint8_t *__restrict__ part, int64_t n,
+                                                  int m, const uint32_t *__restrict__ tile_base,
+                                                  int32_t *__restrict__ perm,
+                                                  int32_t *__restrict__ pos_of_id,
+                                                  uint8_t *__restrict__ part_of_pos) {
+    __shared__ uint32_t run[kMaxParts];
+    __shared__ uint32_t wc[8][kMaxParts];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int j = threadIdx.x; j < m; j += blockDim.x)
+        run[j] = tile_base[(int64_t)blockIdx.x * m + j];
+    const int64_t base = (int64_t)blockIdx.x * kScatTile;
+    for (int round = 0; round < kScatTile / 256; ++round) {
+        for (int e = threadIdx.x; e < 8 * kMaxParts; e += blockDim.x) (&wc[0][0])[e] = 0;
+        __syncthreads();
+        const int64_t i = base + round * 256 + threadIdx.x;
+        const bool valid = i < n;
+        const int j = valid ? part[i] : 0x7fffffff;
+        const unsigned peers = __match_any_sync(NR_FULL, j);
+        const int rank = __popc(peers & lanemask_lt());
+        if (valid && rank == 0) wc[warp][j] = __popc(peers);
+        __syncthreads();
+        if (valid) {
+            uint32_t off = run[j];
+            for (int w = 0; w < warp; ++w) off += wc[w][j];
+            const uint32_t pos = off + rank;
+            perm[pos] = (int32_t)i;
+            pos_of_id[i] = (int32_t)pos;
+            part_of_pos[pos] = (uint8_t)j;
+        }
+        __syncthreads();
+        for (int jj = threadIdx.x; jj < m; jj += blockDim.x) {
+            uint32_t add = 0;
+#pragma unroll
+            for (int w = 0; w < 8; ++w) add += wc[w][jj];
+            run[jj] += add;
+        }
+        __syncthreads();
+    }
+    (void)lane;
+}
+
+int partition_scatter(const double *norm2, const uint8_t *part, int64_t n, int m, int32_t *perm,
+                      int32_t *pos_of_id, uint8_t *part_of_pos, int64_t *offsets_d, double *V_d,
+                      cudaStream_t s, std::string *err) {
+    const int ntiles = (int)((n + kScatTile - 1) / kScatTile);
+    DevBuf tc, vm;
+    if (tc.alloc((size_t)ntiles * m * 4) || vm.alloc((size_t)m * 8)) {
+        *err = "partition: cudaMalloc failed";
+        return NRLSH_ENOMEM;
+    }
+    cudaMemsetAsync(vm.p, 0, (size_t)m * 8, s);
+    scat_hist<<<ntiles, 256, 0, s>>>(norm2, part, n, m, tc.get<uint32_t>(),
+                                     vm.get<unsigned long long>());
+    scat_scan<<<1, 256, 0, s>>>(tc.get<uint32_t>(), ntiles, m, offsets_d,
+                                vm.get<unsigned long long>(), V_d);
+    scat_write<<<ntiles, 256, 0, s>>>(part, n, m, tc.get<uint32_t>(), perm, pos_of_id,
+                                      part_of_pos);
+    note_launch(3);
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+        *err = std::string("partition scatter: ") + cudaGetErrorString(e);
+        return NRLSH_ECUDA;
+    }
+    return 0;
+}
+
+// =========================================================================== K3
+// SIMT fp32 reference path for the projection (kept for d/L shapes the tensor
+// core kernel does not cover).  CTA tile: 64 items x 32W columns, k-chunks of 32.
+template <int W>
+__global__ void __launch_bounds__(256) k3_codes_simt(
+    const float *__restrict__ X, int64_t n, int d, const double *__restrict__ norm2,
+    const uint8_t *__restrict__ part, const double *__restrict__ V,
+    const float *__restrict__ Apad, int L, const int32_t *__restrict__ pos_of_id,
+    uint32_t *__restrict__ codes) {
+    constexpr int TB = 32 * W;         // columns
+    constexpr int CPT = TB / 16;       // columns per thread
+    __shared__ float Xs[32][65];
+    __shared__ float As[32][TB];
+    __shared__ uint32_t sw[64][W];
+    __shared__ float st[64];
+    const int tid = threadIdx.x;
+    const int tb = tid & 15, ti = tid >> 4;
+    for (int64_t i0 = (int64_t)blockIdx.x * 64; i0 < n; i0 += (int64_t)gridDim.x * 64) {
+        float acc[4][CPT];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) acc[a][c] = 0.f;
+        if (tid < 64) {
+            const int64_t i = i0 + tid;
+            float t = 0.f;
+            if (i < n) {
+                const double Vj = V[part[i]];
+                if (Vj == 0.0) t = 1.f;
+                else {
+                    const double df = Vj - norm2[i];
+                    t = (float)sqrt(df > 0.0 ? df : 0.0);
+                }
+            }
+            st[tid] = t;
+        }
+        for (int k0 = 0; k0 < d; k0 += 32) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const int idx = tid + 256 * e;
+                const int r = idx >> 5, k = idx & 31;
+                const int64_t i = i0 + r;
+                Xs[k][r] = (i < n && k0 + k < d) ? __ldg(X + i * (int64_t)d + k0 + k) : 0.f;
+            }
+            for (int idx = tid; idx < 32 * TB; idx += 256) {
+                const int k = idx / TB, b = idx % TB;
+                As[k][b] = (k0 + k < d) ? Apad[(int64_t)(k0 + k) * TB + b] : 0.f;
+            }
+            __syncthreads();
+#pragma unroll 8
+            for (int kk = 0; kk < 32; ++kk) {
+                float a[4], bb[CPT];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) a[u] = Xs[kk][ti * 4 + u];
+#pragma unroll
+                for (int c = 0; c < CPT; ++c) bb[c] = As[kk][tb * CPT + c];
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int c = 0; c < CPT; ++c) acc[u][c] = fmaf(a[u], bb[c], acc[u][c]);
+            }
+            __syncthreads();
+        }
+        for (int e = tid; e < 64 * W; e += 256) (&sw[0][0])[e] = 0u;
+        __syncthreads();
+        const float *Ad = Apad + (int64_t)d * TB;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int r = ti * 4 + u;
+            uint32_t mask = 0;
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) {
+                const int b = tb * CPT + c;
+                const float y = fmaf(__ldg(Ad + b), st[r], acc[u][c]);
+                if (b < L && y >= 0.f) mask |= 1u << (b & 31);
+            }
+            atomicOr(&sw[r][(tb * CPT) >> 5], mask);
+        }
+        __syncthreads();
+        for (int e = tid; e < 64 * W; e += 256) {
+            const int r = e / W, w = e % W;
+            const int64_t i = i0 + r;
+            if (i < n) codes[(int64_t)pos_of_id[i] * W + w] = sw[r][w];
+        }
+        __syncthreads();
+    }
+}
+
+void launch_item_codes(const float *X, int64_t n, int d, const double *norm2,
+                       const uint8_t *part, const double *V, const float *Apad, int L, int W,
+                       const int32_t *pos_of_id, uint32_t *codes, cudaStream_t s) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int grid = grid_for(n, 64, sms * 8);
+    switch (W) {
+        case 1: k3_codes_simt<1><<<grid, 256, 0, s>>>(X, n, d, norm2, part, V, Apad, L, pos_of_id, codes); break;
+        case 2: k3_codes_simt<2><<<grid, 256, 0, s>>>(X, n, d, norm2, part, V, Apad, L, pos_of_id, codes); break;
+        case 3: k3_codes_simt<3><<<grid, 256, 0, s>>>(X, n, d, norm2, part, V, Apad, L, pos_of_id, codes); break;
+        default: k3_codes_simt<4><<<grid, 256, 0, s>>>(X, n, d, norm2, part, V, Apad, L, pos_of_id, codes); break;
+    }
+    note_launch();
+}
+
+}  // namespace nrlsh

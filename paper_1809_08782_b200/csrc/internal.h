@@ -1,0 +1,129 @@
+// internal.h — host-side structures and kernel launchers of libnrlsh.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/nrlsh.h"
+
+struct nrlsh_index {
+    int64_t n = 0;
+    int32_t d = 0;
+    int32_t L = 0;        // SRP hash bits L_h
+    int32_t W = 0;        // 32-bit words per code = ceil(L/32)
+    int32_t m = 0;        // sub-datasets
+    int32_t code_bits = 0;
+    uint64_t seed = 0;
+    double eps = 0.01;
+    int32_t scheme = NRLSH_SCHEME_PERCENTILE;
+    int32_t query_batch = 1024;
+    int device = 0;
+
+    const float *X = nullptr;   // items, device, borrowed unless X_owned
+    float *X_owned = nullptr;
+
+    double *norm2 = nullptr;      // [n] item order
+    int32_t *perm = nullptr;      // [n] position -> id
+    int32_t *pos_of_id = nullptr; // [n] id -> position
+    uint8_t *part_of_id = nullptr;  // [n]
+    uint8_t *part_of_pos = nullptr; // [n]
+    int64_t *offsets_d = nullptr;   // [m+1]
+    double *V_d = nullptr;          // [m]
+    uint32_t *codes = nullptr;      // [n x W], partition order
+    float *A = nullptr;             // [(d+1) x L] row-major (as generated)
+    float *Apad = nullptr;          // [(d+1) x 32W], zero columns >= L
+    uint16_t *R_d = nullptr;        // [m x (L+1)]
+    int4 *chunks_d = nullptr;       // scan work units (j, pos0, pos1, 0)
+    int32_t *order_d = nullptr;     // [m*(L+1)] structure position -> j*(L+1)+h
+    int32_t nchunks = 0;
+
+    std::vector<int64_t> offsets;
+    std::vector<double> V, U;
+    std::vector<float> A_h;
+    std::vector<uint16_t> R_h;
+};
+
+namespace nrlsh {
+
+// ---------------------------------------------------------------- tracing
+enum ProfSlot { SLOT_NORMS = 0, SLOT_PARTITION, SLOT_SCATTER, SLOT_CODES, SLOT_QCODES,
+                SLOT_PILOT, SLOT_SCAN, SLOT_FALLBACK, SLOT_SELECT, SLOT_SCORE, SLOT_TOPK,
+                SLOT_GT_NORMS, SLOT_GT_FILTER, SLOT_OTHER, kNumSlots };
+void note_launch(int k = 1);
+long long launch_count();
+void prof_collect();
+// CUDA-event range on stream s around the kernels launched in its scope
+struct ProfScope {
+    ProfScope(int slot, cudaStream_t s);
+    ~ProfScope();
+    int slot_;
+    cudaStream_t s_;
+    void *a_;
+};
+
+// ---------------------------------------------------------------- build
+void launch_norms(const float *X, int64_t n, int d, double *norm2, unsigned long long *bad,
+                  cudaStream_t s);
+// K2 (percentile): fills part_of_id.  Host-orchestrated; may synchronise `s`.
+int partition_percentile(const double *norm2, int64_t n, int m, uint8_t *part_of_id,
+                         cudaStream_t s, std::string *err);
+int partition_uniform(const double *norm2, int64_t n, int m, uint8_t *part_of_id,
+                      cudaStream_t s, std::string *err);
+// stable scatter by sub-dataset: perm, pos_of_id, part_of_pos, offsets, V
+int partition_scatter(const double *norm2, const uint8_t *part_of_id, int64_t n, int m,
+                      int32_t *perm, int32_t *pos_of_id, uint8_t *part_of_pos,
+                      int64_t *offsets_d, double *V_d, cudaStream_t s, std::string *err);
+// K3: SRP codes of P(x) in partition order
+void launch_item_codes(const float *X, int64_t n, int d, const double *norm2,
+                       const uint8_t *part_of_id, const double *V_d, const float *Apad,
+                       int L, int W, const int32_t *pos_of_id, uint32_t *codes,
+                       cudaStream_t s);
+
+// ---------------------------------------------------------------- query
+struct QueryWS {
+    uint32_t *qcodes;   // [Qb x W]
+    int8_t *delta;      // [Qb x m]
+    uint32_t *cnt;      // [Qb]
+    unsigned long long *buf;  // [Qb x C]  (R << 32 | pos)
+    int32_t *cand;      // [Qb x Tq]   item ids
+    uint16_t *cand_rank;// [Qb x Tq]   (optional)
+    float *scores;      // [Qb x Tq]
+    int *flags;         // [4]: zero-norm min index, nonfinite min index, fallback count
+    int64_t C;          // buffer capacity per query
+};
+
+void launch_qcodes(const float *Q, int64_t nq, int d, const float *Apad, int L, int W,
+                   uint32_t *qcodes, int *flags, int64_t q_index_base, cudaStream_t s);
+void launch_pilot(const nrlsh_index *ix, const uint32_t *qcodes, int Qb, int64_t Tq,
+                  int stride, int8_t *delta, uint32_t *cnt, cudaStream_t s);
+void launch_scan(const nrlsh_index *ix, const uint32_t *qcodes, const int8_t *delta, int Qb,
+                 unsigned long long *buf, uint32_t *cnt, int64_t C,
+                 unsigned long long *pairs, cudaStream_t s);
+void launch_fallback(const nrlsh_index *ix, const uint32_t *qcodes, int Qb, int64_t Tq,
+                     unsigned long long *buf, uint32_t *cnt, int64_t C, int *flags,
+                     cudaStream_t s);
+void launch_select(const nrlsh_index *ix, int Qb, int64_t Tq, const unsigned long long *buf,
+                   const uint32_t *cnt, int64_t C, int32_t *cand, uint16_t *cand_rank,
+                   cudaStream_t s);
+// scores[q][t] = q . X[cand[q][t]] (fp32); if lb_eps > 0 writes fl(s) - lb_eps*|q|*|x|
+// (a certified lower bound, for the ground-truth pilot).  cand == nullptr means the
+// implicit list cand[q][t] = t * stride.
+void launch_score(const float *X, int d, const float *Q, int Qb, const int32_t *cand,
+                  int64_t ncand, int64_t cand_ld, const uint32_t *ncand_per_q, int stride,
+                  const float *xnorm, const float *qnorm, float lb_eps, float *scores,
+                  cudaStream_t s);
+// top-k by (score desc, id asc) over scores[q][0..ncand_q)
+void launch_topk(const float *scores, const int32_t *cand, int Qb, int64_t ncand,
+                 int64_t cand_ld, const uint32_t *ncand_per_q, int stride, int k,
+                 int64_t *out_ids, float *out_scores, float *kth_out, cudaStream_t s);
+
+// ---------------------------------------------------------------- ground truth
+void launch_vec_norms(const float *X, int64_t n, int d, float *xnorm, cudaStream_t s);
+void launch_gt_filter(const float *X, int64_t n, int d, const float *Q, int Qb,
+                      const float *xnorm, const float *qnorm, const float *lb, float eps_rel,
+                      int32_t *cand, uint32_t *cnt, int64_t C, cudaStream_t s);
+int scan_chunk_items();
+
+}  // namespace nrlsh

@@ -1,0 +1,602 @@
+// query_kernels.cu — batched query processing (Alg. 2 + single-table multi-probe,
+// PAPER:160-171, 207-217) for sm_100a.
+//
+//  K5  qcodes:   bit b of P(q) = [q; 0] is [sum_k A[k][b] q_k >= 0]  (Eq. (8), Eq. (4)).
+//  K6  pilot:    per query, the (j, h) histogram of a strided item sample gives a
+//                bound B(q) on the position in the sorted (U_j, l) structure
+//                 holding ~T items; it becomes per-sub-dataset Hamming
+//                radii delta_j(q) = max{h : R[j][h] <= B(q)}.
+//      scan:     every (query, item) pair: h = popc(code ^ qcode); keep (R, pos)
+//                iff h <= delta_j(q) — one compare per pair, j uniform per chunk.
+//      fallback: exact two-pass path for any query whose buffer under- or
+//                overflowed.
+//  K7  select:   the exact T smallest keys (R[j][h], position) per query — the
+//                first T items of the traversal; positions within a sub-dataset
+//                follow ascending item id, so this is the (R, id) order of D10.
+//  K8  re-rank:  exact fp32 inner products of the candidates (Alg. 2 l.6,
+//                PAPER:169) and top-k by (score desc, id asc).
+#include <algorithm>
+#include <climits>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace nrlsh {
+
+// =========================================================================== K5
+template <int W>
+__global__ void __launch_bounds__(32 * W) k5_qcodes(const float *__restrict__ Q, int d,
+                                                    const float *__restrict__ Apad, int L,
+                                                    uint32_t *__restrict__ qcodes,
+                                                    int *__restrict__ flags, int64_t qbase) {
+    extern __shared__ float sq[];
+    const int64_t q = blockIdx.x;
+    const float *qp = Q + q * (int64_t)d;
+    int bad = 0, nz = 0;
+    for (int k = threadIdx.x; k < d; k += blockDim.x) {
+        const float v = qp[k];
+        sq[k] = v;
+        bad |= !isfinite(v);
+        nz |= (v != 0.f);
+    }
+    const int anybad = __syncthreads_or(bad);
+    const int anynz = __syncthreads_or(nz);
+    if (threadIdx.x == 0) {
+        if (anybad) atomicMin(&flags[1], (int)(qbase + q));
+        else if (!anynz) atomicMin(&flags[0], (int)(qbase + q));
+    }
+    const int b = threadIdx.x;
+    float acc = 0.f;
+    for (int k = 0; k < d; ++k) acc = fmaf(__ldg(Apad + (int64_t)k * 32 * W + b), sq[k], acc);
+    const bool bit = (b < L) && (acc >= 0.f);
+    const unsigned word = __ballot_sync(NR_FULL, bit);
+    if ((threadIdx.x & 31) == 0) qcodes[q * W + (threadIdx.x >> 5)] = word;
+}
+
+void launch_qcodes(const float *Q, int64_t nq, int d, const float *Apad, int L, int W,
+                   uint32_t *qcodes, int *flags, int64_t qbase, cudaStream_t s) {
+    const size_t sm = (size_t)d * 4;
+    switch (W) {
+        case 1: k5_qcodes<1><<<(int)nq, 32, sm, s>>>(Q, d, Apad, L, qcodes, flags, qbase); break;
+        case 2: k5_qcodes<2><<<(int)nq, 64, sm, s>>>(Q, d, Apad, L, qcodes, flags, qbase); break;
+        default: k5_qcodes<4><<<(int)nq, 128, sm, s>>>(Q, d, Apad, L, qcodes, flags, qbase); break;
+    }
+    note_launch();
+}
+
+// ------------------------------------------------------------------ helpers
+template <int W>
+__device__ __forceinline__ void load_code(const uint32_t *__restrict__ codes, int64_t p,
+                                          uint32_t (&c)[W]) {
+    if (W == 4) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4 *>(codes) + p);
+        c[0] = v.x; c[1] = v.y; c[2] = v.z; c[3] = v.w;
+    } else if (W == 2) {
+        const uint2 v = __ldg(reinterpret_cast<const uint2 *>(codes) + p);
+        c[0] = v.x; c[1] = v.y;
+    } else {
+#pragma unroll
+        for (int w = 0; w < W; ++w) c[w] = __ldg(codes + p * W + w);
+    }
+}
+
+// Histogram of (j, h) over positions p = tid*stride, ... (stride 1 = exact) into
+// smem `hist` [m*(L+1)]; then the smallest structure position r whose cumulative
+// count reaches `need` (in histogram units).  Returns r (NR-1 if never reached)
+// and the count strictly before r in *cum_lt.
+template <int W>
+__device__ void hist_and_bound(const uint32_t *__restrict__ codes,
+                               const uint8_t *__restrict__ part_of_pos, int64_t n, int stride,
+                               const uint32_t (&qc)[W], int L, int NR,
+                               const int32_t *__restrict__ order, uint32_t *hist, uint32_t need,
+                               uint32_t *ws, int *sB, uint32_t *sLt) {
+    for (int e = threadIdx.x; e < NR; e += blockDim.x) hist[e] = 0u;
+    if (threadIdx.x == 0) { *sB = NR - 1; *sLt = 0u; }
+    __syncthreads();
+    for (int64_t p = (int64_t)threadIdx.x * stride; p < n; p += (int64_t)blockDim.x * stride) {
+        uint32_t c[W];
+        load_code<W>(codes, p, c);
+        const int h = hamming<W>(c, qc);
+        const int j = part_of_pos[p];
+        atomicAdd(&hist[j * (L + 1) + h], 1u);
+    }
+    __syncthreads();
+    const int seg = (NR + blockDim.x - 1) / blockDim.x;
+    const int r0 = threadIdx.x * seg, r1 = min(NR, r0 + seg);
+    uint32_t loc = 0;
+    for (int r = r0; r < r1; ++r) loc += hist[order[r]];
+    uint32_t tot;
+    const uint32_t ex = block_excl_scan(loc, ws, &tot);
+    if (ex < need && ex + loc >= need) {
+        uint32_t c = ex;
+        for (int r = r0; r < r1; ++r) {
+            const uint32_t hr = hist[order[r]];
+            if (c + hr >= need) { *sB = r; *sLt = c; break; }
+            c += hr;
+        }
+    } else if (threadIdx.x == 0 && tot < need) {
+        *sLt = tot;  // bound never reached: everything qualifies
+    }
+    __syncthreads();
+}
+
+// =========================================================================== K6 pilot
+template <int W>
+__global__ void __launch_bounds__(1024) k6_pilot(
+    const uint32_t *__restrict__ codes, const uint8_t *__restrict__ part_of_pos, int64_t n,
+    int stride, const uint32_t *__restrict__ qcodes, int L, int m,
+    const int32_t *__restrict__ order, const uint16_t *__restrict__ R, uint32_t need,
+    int8_t *__restrict__ delta, uint32_t *__restrict__ cnt) {
+    extern __shared__ uint32_t hist[];
+    __shared__ uint32_t ws[32];
+    __shared__ int sB;
+    __shared__ uint32_t sLt;
+    const int q = blockIdx.x;
+    const int NR = m * (L + 1);
+    uint32_t qc[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) qc[w] = qcodes[q * W + w];
+    hist_and_bound<W>(codes, part_of_pos, n, stride, qc, L, NR, order, hist, need, ws, &sB, &sLt);
+    const int B = sB;
+    for (int j = threadIdx.x; j < m; j += blockDim.x) {
+        int c = 0;
+        for (int h = 0; h <= L; ++h) c += (R[j * (L + 1) + h] <= B);
+        delta[q * m + j] = (int8_t)(c - 1);
+    }
+    if (threadIdx.x == 0) cnt[q] = 0u;
+}
+
+void launch_pilot(const nrlsh_index *ix, const uint32_t *qcodes, int Qb, int64_t Tq, int stride,
+                  int8_t *delta, uint32_t *cnt, cudaStream_t s) {
+    // target: T plus 4 standard deviations of the sampled estimate (+ one stride of
+    // discreteness); exact (= T) when stride == 1.
+    double target = (double)Tq;
+    if (stride > 1) target += 4.0 * sqrt((double)Tq * stride) + stride;
+    uint32_t need = (uint32_t)ceil(target / stride);
+    if (need < 1) need = 1;
+    const int NR = ix->m * (ix->L + 1);
+    const size_t sm = (size_t)NR * 4;
+    const int32_t *order = ix->order_d;
+    switch (ix->W) {
+        case 1:
+            cudaFuncSetAttribute(k6_pilot<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            k6_pilot<1><<<Qb, 1024, sm, s>>>(ix->codes, ix->part_of_pos, ix->n, stride, qcodes, ix->L, ix->m, order, ix->R_d, need, delta, cnt);
+            break;
+        case 2:
+            cudaFuncSetAttribute(k6_pilot<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            k6_pilot<2><<<Qb, 1024, sm, s>>>(ix->codes, ix->part_of_pos, ix->n, stride, qcodes, ix->L, ix->m, order, ix->R_d, need, delta, cnt);
+            break;
+        default:
+            cudaFuncSetAttribute(k6_pilot<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            k6_pilot<4><<<Qb, 1024, sm, s>>>(ix->codes, ix->part_of_pos, ix->n, stride, qcodes, ix->L, ix->m, order, ix->R_d, need, delta, cnt);
+            break;
+    }
+    note_launch();
+}
+
+// =========================================================================== K6 scan
+constexpr int kScanThreads = 256;
+constexpr int kScanIPT = 4;                       // items per thread
+constexpr int kChunk = kScanThreads * kScanIPT;   // items per work unit
+constexpr int kQG = 64;                           // queries per CTA
+
+template <int W>
+__global__ void __launch_bounds__(kScanThreads) k6_scan(
+    const uint32_t *__restrict__ codes, const int4 *__restrict__ chunks,
+    const uint32_t *__restrict__ qcodes, const int8_t *__restrict__ delta, int Qb, int m,
+    const uint16_t *__restrict__ R, int L, unsigned long long *__restrict__ buf,
+    uint32_t *__restrict__ cnt, int64_t C, unsigned long long *__restrict__ pairs) {
+    __shared__ uint32_t sq[kQG][W];
+    __shared__ int sd[kQG];
+    __shared__ uint32_t sR[129];
+    // consecutive CTAs share a chunk (different query groups): the chunk's codes
+    // are read from HBM once and re-served from L2
+    const int ngroups = (Qb + kQG - 1) / kQG;
+    const int4 ch = chunks[blockIdx.x / ngroups];
+    const int j = ch.x, p0 = ch.y, p1 = ch.z;
+    const int q0 = (blockIdx.x % ngroups) * kQG;
+    const int nqg = min(kQG, Qb - q0);
+    int act = 0;
+    for (int t = threadIdx.x; t < kQG; t += blockDim.x) {
+        int dl = -1;
+        if (t < nqg) {
+            dl = delta[(int64_t)(q0 + t) * m + j];
+#pragma unroll
+            for (int w = 0; w < W; ++w) sq[t][w] = qcodes[(int64_t)(q0 + t) * W + w];
+        }
+        sd[t] = dl;
+        act |= (dl >= 0);
+    }
+    for (int h = threadIdx.x; h <= L; h += blockDim.x) sR[h] = R[j * (L + 1) + h];
+    const int nact = __syncthreads_count(act);
+    if (nact == 0) return;
+    if (threadIdx.x == 0 && pairs) atomicAdd(pairs, (unsigned long long)nact * (p1 - p0));
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = lanemask_lt();
+    uint32_t c[kScanIPT][W];
+    bool valid[kScanIPT];
+#pragma unroll
+    for (int u = 0; u < kScanIPT; ++u) {
+        const int p = p0 + threadIdx.x + kScanThreads * u;
+        valid[u] = p < p1;
+        if (valid[u]) load_code<W>(codes, p, c[u]);
+        else
+#pragma unroll
+            for (int w = 0; w < W; ++w) c[u][w] = 0u;
+    }
+    for (int qq = 0; qq < nqg; ++qq) {
+        const int dl = sd[qq];
+        if (dl < 0) continue;
+        uint32_t qc[W];
+#pragma unroll
+        for (int w = 0; w < W; ++w) qc[w] = sq[qq][w];
+        int h[kScanIPT];
+        bool pass[kScanIPT];
+        bool any = false;
+#pragma unroll
+        for (int u = 0; u < kScanIPT; ++u) {
+            h[u] = hamming<W>(c[u], qc);
+            pass[u] = valid[u] && (h[u] <= dl);
+            any |= pass[u];
+        }
+        if (!__any_sync(NR_FULL, any)) continue;
+        const int q = q0 + qq;
+#pragma unroll
+        for (int u = 0; u < kScanIPT; ++u) {
+            const unsigned bal = __ballot_sync(NR_FULL, pass[u]);
+            if (bal == 0u) continue;
+            const int leader = __ffs(bal) - 1;
+            uint32_t base = 0;
+            if (lane == leader) base = atomicAdd(&cnt[q], (uint32_t)__popc(bal));
+            base = __shfl_sync(NR_FULL, base, leader);
+            if (pass[u]) {
+                const uint32_t slot = base + __popc(bal & lt);
+                if (slot < C) {
+                    const uint32_t p = p0 + threadIdx.x + kScanThreads * u;
+                    buf[(int64_t)q * C + slot] = ((unsigned long long)sR[h[u]] << 32) | p;
+                }
+            }
+        }
+    }
+}
+
+void launch_scan(const nrlsh_index *ix, const uint32_t *qcodes, const int8_t *delta, int Qb,
+                 unsigned long long *buf, uint32_t *cnt, int64_t C, unsigned long long *pairs,
+                 cudaStream_t s) {
+    const int64_t ngroups = (Qb + kQG - 1) / kQG;
+    const unsigned grid = (unsigned)(ix->nchunks * ngroups);
+    switch (ix->W) {
+        case 1: k6_scan<1><<<grid, kScanThreads, 0, s>>>(ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs); break;
+        case 2: k6_scan<2><<<grid, kScanThreads, 0, s>>>(ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs); break;
+        default: k6_scan<4><<<grid, kScanThreads, 0, s>>>(ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs); break;
+    }
+    note_launch();
+}
+
+int scan_chunk_items() { return kChunk; }
+
+// =========================================================================== fallback
+template <int W>
+__global__ void __launch_bounds__(1024) k6_fallback(
+    const uint32_t *__restrict__ codes, const uint8_t *__restrict__ part_of_pos, int64_t n,
+    const uint32_t *__restrict__ qcodes, int L, int m, const int32_t *__restrict__ order,
+    const uint16_t *__restrict__ R, int64_t Tq, unsigned long long *__restrict__ buf,
+    uint32_t *__restrict__ cnt, int64_t C, int *__restrict__ flags) {
+    extern __shared__ uint32_t hist[];
+    __shared__ uint32_t ws[32];
+    __shared__ int sB;
+    __shared__ uint32_t sLt, s_out, s_eq;
+    const int q = blockIdx.x;
+    const uint32_t c0 = cnt[q];
+    if (c0 >= (uint64_t)Tq && c0 <= (uint64_t)C) return;
+    if (threadIdx.x == 0) atomicAdd(&flags[2], 1);
+    const int NR = m * (L + 1);
+    uint32_t qc[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) qc[w] = qcodes[q * W + w];
+    hist_and_bound<W>(codes, part_of_pos, n, 1, qc, L, NR, order, hist, (uint32_t)Tq, ws, &sB,
+                      &sLt);
+    const int B = sB;
+    const uint32_t need_eq = (uint32_t)Tq - sLt;
+    // R[j][h] lookup straight from the structure (global, cached)
+    if (threadIdx.x == 0) { s_out = 0; s_eq = 0; }
+    __syncthreads();
+    for (int64_t base = 0; base < n; base += blockDim.x) {
+        const int64_t p = base + threadIdx.x;
+        int r = NR;
+        if (p < n) {
+            uint32_t c[W];
+            load_code<W>(codes, p, c);
+            const int h = hamming<W>(c, qc);
+            r = R[part_of_pos[p] * (L + 1) + h];
+        }
+        const uint32_t lt = r < B, eq = r == B;
+        uint32_t tot_eq, tot_take;
+        const uint32_t eq_rank = block_excl_scan(eq, ws, &tot_eq) + s_eq;
+        const uint32_t take = lt || (eq && eq_rank < need_eq);
+        const uint32_t slot = block_excl_scan(take, ws, &tot_take) + s_out;
+        if (take) buf[(int64_t)q * C + slot] = ((unsigned long long)r << 32) | (uint32_t)p;
+        __syncthreads();
+        if (threadIdx.x == 0) { s_out += tot_take; s_eq += tot_eq; }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) cnt[q] = (uint32_t)Tq;
+}
+
+void launch_fallback(const nrlsh_index *ix, const uint32_t *qcodes, int Qb, int64_t Tq,
+                     unsigned long long *buf, uint32_t *cnt, int64_t C, int *flags,
+                     cudaStream_t s) {
+    const int NR = ix->m * (ix->L + 1);
+    const size_t sm = (size_t)NR * 4;
+    const int32_t *order = ix->order_d;
+    switch (ix->W) {
+        case 1:
+            cudaFuncSetAttribute(k6_fallback<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            k6_fallback<1><<<Qb, 1024, sm, s>>>(ix->codes, ix->part_of_pos, ix->n, qcodes, ix->L, ix->m, order, ix->R_d, Tq, buf, cnt, C, flags);
+            break;
+        case 2:
+            cudaFuncSetAttribute(k6_fallback<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            k6_fallback<2><<<Qb, 1024, sm, s>>>(ix->codes, ix->part_of_pos, ix->n, qcodes, ix->L, ix->m, order, ix->R_d, Tq, buf, cnt, C, flags);
+            break;
+        default:
+            cudaFuncSetAttribute(k6_fallback<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            k6_fallback<4><<<Qb, 1024, sm, s>>>(ix->codes, ix->part_of_pos, ix->n, qcodes, ix->L, ix->m, order, ix->R_d, Tq, buf, cnt, C, flags);
+            break;
+    }
+    note_launch();
+}
+
+// =========================================================================== K7 select
+__global__ void __launch_bounds__(1024) k7_select(
+    const unsigned long long *__restrict__ buf, const uint32_t *__restrict__ cnt, int64_t C,
+    int64_t Tq, int NR, const int32_t *__restrict__ perm, int32_t *__restrict__ cand,
+    uint16_t *__restrict__ cand_rank) {
+    extern __shared__ uint32_t hist[];
+    __shared__ uint32_t ws[32];
+    __shared__ uint32_t h256[256];
+    __shared__ int sB;
+    __shared__ uint32_t sLt, s_out, s_pfx, s_kth;
+    const int q = blockIdx.x;
+    const int64_t c = min((int64_t)cnt[q], C);
+    const unsigned long long *b = buf + (int64_t)q * C;
+    for (int e = threadIdx.x; e < NR; e += blockDim.x) hist[e] = 0u;
+    if (threadIdx.x == 0) { sB = NR - 1; sLt = 0; s_out = 0; }
+    __syncthreads();
+    for (int64_t e = threadIdx.x; e < c; e += blockDim.x) atomicAdd(&hist[(uint32_t)(b[e] >> 32)], 1u);
+    __syncthreads();
+    const uint32_t need = (uint32_t)Tq;
+    {
+        const int seg = (NR + blockDim.x - 1) / blockDim.x;
+        const int r0 = threadIdx.x * seg, r1 = min(NR, r0 + seg);
+        uint32_t loc = 0;
+        for (int r = r0; r < r1; ++r) loc += hist[r];
+        uint32_t tot;
+        const uint32_t ex = block_excl_scan(loc, ws, &tot);
+        if (ex < need && ex + loc >= need) {
+            uint32_t cc = ex;
+            for (int r = r0; r < r1; ++r) {
+                if (cc + hist[r] >= need) { sB = r; sLt = cc; break; }
+                cc += hist[r];
+            }
+        }
+        __syncthreads();
+    }
+    const uint32_t B = (uint32_t)sB;
+    const uint32_t need_eq = need - sLt;
+    const uint32_t n_eq = hist[B];
+    // the need_eq-th smallest position among the ties (R == B): radix select, 8 bits/round
+    if (threadIdx.x == 0) { s_pfx = 0; s_kth = need_eq; }
+    __syncthreads();
+    if (need_eq < n_eq) {
+        for (int shift = 24; shift >= 0; shift -= 8) {
+            for (int e = threadIdx.x; e < 256; e += blockDim.x) h256[e] = 0;
+            __syncthreads();
+            const uint32_t pfx = s_pfx;
+            for (int64_t e = threadIdx.x; e < c; e += blockDim.x) {
+                const unsigned long long v = b[e];
+                if ((uint32_t)(v >> 32) != B) continue;
+                const uint32_t pos = (uint32_t)v;
+                if (shift < 24 && (pos >> (shift + 8)) != (pfx >> (shift + 8))) continue;
+                atomicAdd(&h256[(pos >> shift) & 255u], 1u);
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                uint32_t k = s_kth, acc = 0;
+                for (int dg = 0; dg < 256; ++dg) {
+                    if (acc + h256[dg] >= k) { s_pfx = pfx | ((uint32_t)dg << shift); s_kth = k - acc; break; }
+                    acc += h256[dg];
+                }
+            }
+            __syncthreads();
+        }
+    } else if (threadIdx.x == 0) {
+        s_pfx = 0xffffffffu;
+    }
+    __syncthreads();
+    const uint32_t pk = s_pfx;
+    for (int64_t e = threadIdx.x; e < c; e += blockDim.x) {
+        const unsigned long long v = b[e];
+        const uint32_t r = (uint32_t)(v >> 32), pos = (uint32_t)v;
+        if (r < B || (r == B && pos <= pk)) {
+            const uint32_t slot = atomicAdd(&s_out, 1u);
+            if (slot < need) {
+                cand[(int64_t)q * Tq + slot] = perm[pos];
+                if (cand_rank) cand_rank[(int64_t)q * Tq + slot] = (uint16_t)r;
+            }
+        }
+    }
+}
+
+void launch_select(const nrlsh_index *ix, int Qb, int64_t Tq, const unsigned long long *buf,
+                   const uint32_t *cnt, int64_t C, int32_t *cand, uint16_t *cand_rank,
+                   cudaStream_t s) {
+    const int NR = ix->m * (ix->L + 1);
+    const size_t sm = (size_t)NR * 4;
+    cudaFuncSetAttribute(k7_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k7_select<<<Qb, 1024, sm, s>>>(buf, cnt, C, Tq, NR, ix->perm, cand, cand_rank);
+    note_launch();
+}
+
+// =========================================================================== K8 score
+// CTA = (query, slice of candidates); one warp per candidate row, lanes stride d
+// (coalesced 128 B), fp32 FMA + xor-shuffle reduction.
+__global__ void __launch_bounds__(256) k8_score(
+    const float *__restrict__ X, int d, const float *__restrict__ Q,
+    const int32_t *__restrict__ cand, int64_t ncand, int64_t cand_ld,
+    const uint32_t *__restrict__ ncand_per_q, int stride, const float *__restrict__ xnorm,
+    const float *__restrict__ qnorm, float lb_eps, float *__restrict__ scores) {
+    extern __shared__ float sq[];
+    const int q = blockIdx.x;
+    for (int k = threadIdx.x; k < d; k += blockDim.x) sq[k] = Q[(int64_t)q * d + k];
+    __syncthreads();
+    int64_t nc = ncand;
+    if (ncand_per_q) nc = min((int64_t)ncand_per_q[q], cand_ld);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const float qn = qnorm ? qnorm[q] : 0.f;
+    for (int64_t t = (int64_t)blockIdx.y * 8 + warp; t < nc; t += (int64_t)gridDim.y * 8) {
+        const int64_t id = cand ? (int64_t)cand[(int64_t)q * cand_ld + t] : t * stride;
+        const float *x = X + id * d;
+        float acc = 0.f;
+        for (int k = lane; k < d; k += 32) acc = fmaf(sq[k], __ldg(x + k), acc);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(NR_FULL, acc, o);
+        if (lane == 0) {
+            float sc = acc;
+            if (lb_eps > 0.f) sc = __fsub_rd(acc, lb_eps * qn * xnorm[id]);
+            scores[(int64_t)q * cand_ld + t] = sc;
+        }
+    }
+}
+
+void launch_score(const float *X, int d, const float *Q, int Qb, const int32_t *cand,
+                  int64_t ncand, int64_t cand_ld, const uint32_t *ncand_per_q, int stride,
+                  const float *xnorm, const float *qnorm, float lb_eps, float *scores,
+                  cudaStream_t s) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    int64_t per = (ncand + 7) / 8;
+    int gy = (int)std::min<int64_t>(std::max<int64_t>(1, per / 16), std::max(1, (sms * 16) / std::max(1, Qb)));
+    if (gy < 1) gy = 1;
+    dim3 grid(Qb, gy);
+    k8_score<<<grid, 256, (size_t)d * 4, s>>>(X, d, Q, cand, ncand, cand_ld, ncand_per_q, stride,
+                                             xnorm, qnorm, lb_eps, scores);
+    note_launch();
+}
+
+// =========================================================================== K8 top-k
+// Key = (~order(score)) << 32 | id: ascending key order is (score desc, id asc).
+// Radix-select the k-th smallest key (8 rounds of 8 bits), collect the k keys <=
+// it, bitonic-sort them.  Keys are cached in shared memory when they fit.
+constexpr int kTopkSmemKeys = 16384;
+constexpr int kMaxK = 1024;
+
+__device__ __forceinline__ unsigned long long topk_key(float sc, uint32_t id) {
+    return ((unsigned long long)(~float_order(sc)) << 32) | id;
+}
+
+__global__ void __launch_bounds__(1024) k8_topk(
+    const float *__restrict__ scores, const int32_t *__restrict__ cand, int64_t ncand,
+    int64_t cand_ld, const uint32_t *__restrict__ ncand_per_q, int stride, int k,
+    int64_t smem_cap, int64_t *__restrict__ out_ids, float *__restrict__ out_scores,
+    float *__restrict__ kth_out) {
+    extern __shared__ unsigned long long skeys[];
+    __shared__ uint32_t h256[256];
+    __shared__ unsigned long long s_pfx;
+    __shared__ uint32_t s_kth, s_n;
+    __shared__ unsigned long long sel[kMaxK];
+    const int q = blockIdx.x;
+    int64_t c = ncand;
+    if (ncand_per_q) c = min((int64_t)ncand_per_q[q], cand_ld);
+    const bool cached = c <= smem_cap;
+    auto key_at = [&](int64_t e) -> unsigned long long {
+        const float sc = scores[(int64_t)q * cand_ld + e];
+        const uint32_t id = cand ? (uint32_t)cand[(int64_t)q * cand_ld + e] : (uint32_t)(e * stride);
+        return topk_key(sc, id);
+    };
+    if (cached)
+        for (int64_t e = threadIdx.x; e < c; e += blockDim.x) skeys[e] = key_at(e);
+    const int kk = (int)min((int64_t)k, c);
+    if (threadIdx.x == 0) { s_pfx = 0; s_kth = kk; s_n = 0; }
+    __syncthreads();
+    if (kk > 0 && kk < c) {
+        for (int shift = 56; shift >= 0; shift -= 8) {
+            for (int e = threadIdx.x; e < 256; e += blockDim.x) h256[e] = 0;
+            __syncthreads();
+            const unsigned long long pfx = s_pfx;
+            for (int64_t e = threadIdx.x; e < c; e += blockDim.x) {
+                const unsigned long long v = cached ? skeys[e] : key_at(e);
+                if (shift < 56 && (v >> (shift + 8)) != (pfx >> (shift + 8))) continue;
+                atomicAdd(&h256[(v >> shift) & 255u], 1u);
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                uint32_t kt = s_kth, acc = 0;
+                for (int dg = 0; dg < 256; ++dg) {
+                    if (acc + h256[dg] >= kt) {
+                        s_pfx = pfx | ((unsigned long long)dg << shift);
+                        s_kth = kt - acc;
+                        break;
+                    }
+                    acc += h256[dg];
+                }
+            }
+            __syncthreads();
+        }
+    } else if (threadIdx.x == 0) {
+        s_pfx = ~0ull;
+    }
+    __syncthreads();
+    const unsigned long long thr = s_pfx;
+    for (int64_t e = threadIdx.x; e < c; e += blockDim.x) {
+        const unsigned long long v = cached ? skeys[e] : key_at(e);
+        if (v <= thr) {
+            const uint32_t slot = atomicAdd(&s_n, 1u);
+            if (slot < (uint32_t)kMaxK) sel[slot] = v;
+        }
+    }
+    __syncthreads();
+    int np2 = 1;
+    while (np2 < kk) np2 <<= 1;
+    for (int t = threadIdx.x; t < np2; t += blockDim.x)
+        if (t >= kk) sel[t] = ~0ull;
+    __syncthreads();
+    for (int size = 2; size <= np2; size <<= 1) {
+        for (int st = size >> 1; st > 0; st >>= 1) {
+            for (int t = threadIdx.x; t < np2; t += blockDim.x) {
+                const int o = t ^ st;
+                if (o > t) {
+                    const bool up = (t & size) == 0;
+                    if ((sel[t] > sel[o]) == up) {
+                        unsigned long long tmp = sel[t]; sel[t] = sel[o]; sel[o] = tmp;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int t = threadIdx.x; t < k; t += blockDim.x) {
+        if (t < kk) {
+            const unsigned long long v = sel[t];
+            out_ids[(int64_t)q * k + t] = (int64_t)(uint32_t)v;
+            out_scores[(int64_t)q * k + t] = float_unorder(~(uint32_t)(v >> 32));
+        } else {
+            out_ids[(int64_t)q * k + t] = -1;
+            out_scores[(int64_t)q * k + t] = -INFINITY;
+        }
+    }
+    if (kth_out && threadIdx.x == 0)
+        kth_out[q] = (kk == k && kk > 0) ? float_unorder(~(uint32_t)(sel[kk - 1] >> 32)) : -INFINITY;
+}
+
+void launch_topk(const float *scores, const int32_t *cand, int Qb, int64_t ncand,
+                 int64_t cand_ld, const uint32_t *ncand_per_q, int stride, int k,
+                 int64_t *out_ids, float *out_scores, float *kth_out, cudaStream_t s) {
+    const int64_t cap = std::min<int64_t>(std::max<int64_t>(ncand, 1), kTopkSmemKeys);
+    const size_t sm = (size_t)cap * 8;
+    cudaFuncSetAttribute(k8_topk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k8_topk<<<Qb, 1024, sm, s>>>(scores, cand, ncand, cand_ld, ncand_per_q, stride, k, cap,
+                                 out_ids, out_scores, kth_out);
+    note_launch();
+}
+
+}  // namespace nrlsh

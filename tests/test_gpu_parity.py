@@ -1,0 +1,405 @@
+"""GPU <-> oracle parity of every step of the hot path, through the C ABI.
+
+Rules (BASELINE.json north_star):
+  * partition (perm, offsets, V), norms, projection, rank table: bit-exact;
+  * codes: bit-exact except bits whose fp64 projection |z| < 1e-5 * ||P(x)|| (= 1e-5);
+  * Hamming scores, candidate sets (and their (R, id) order), returned ids:
+    bit-exact when both sides are given identical codes;
+  * inner products within 1e-4 relative; top-k ids equal except at ties within it.
+Sizes: small cases the oracle finishes in seconds (several tiles + ragged
+tails), and BASELINE.json's full sizes on sampled outputs.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def _P():
+    import paper_1809_08782_b200 as P
+    return P
+
+
+@pytest.fixture(scope="session", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    P = _P()
+    P.lib()
+
+
+_DATA = {}
+
+
+def dataset(cfg, n=None, nq=None):
+    key = (cfg.name, n, nq)
+    if key not in _DATA:
+        c = cfg if n is None else workloads.scaled(cfg, n, nq or cfg.nq)
+        X = workloads.make_items(c)
+        Q = workloads.make_queries(c, nq=nq or c.nq)
+        _DATA[key] = (c, X, Q)
+    return _DATA[key]
+
+
+def bits_of(codes, L):
+    c = np.ascontiguousarray(codes, dtype=np.uint32)
+    b = ((c[:, :, None] >> np.arange(32, dtype=np.uint32)) & 1).reshape(c.shape[0], -1)
+    return b[:, :L].astype(bool)
+
+
+def assert_codes_match(gpu_codes, orc_codes, z, L, band=1e-5):
+    diff = bits_of(gpu_codes, L) != bits_of(orc_codes, L)
+    bad = diff & (np.abs(z[:, :L]) >= band)
+    assert not bad.any(), f"{bad.sum()} code bits differ with |z| >= {band}"
+    # bits beyond L are zero on both sides
+    if gpu_codes.shape[1] * 32 > L:
+        allb = ((np.ascontiguousarray(gpu_codes)[:, :, None] >> np.arange(32, dtype=np.uint32)) & 1)
+        assert not allb.reshape(gpu_codes.shape[0], -1)[:, L:].any()
+    return int(diff.sum())
+
+
+def assert_topk_match(ids, scores, ref_ids, ref_scores, X, q, rtol=1e-4):
+    """ids equal except where swapped items' oracle scores differ by <= rtol relative;
+    scores within rtol of the oracle's fp64 values."""
+    ids = np.asarray(ids)
+    valid = ref_ids >= 0
+    assert np.array_equal(ids >= 0, valid)
+    s_ref = ref_scores[valid]
+    assert np.allclose(np.asarray(scores)[valid], s_ref, rtol=rtol, atol=rtol * np.abs(s_ref).max())
+    if np.array_equal(ids, ref_ids):
+        return
+    # differing positions must be near-ties: compare exact scores of the returned items
+    got = ids[valid].astype(np.int64)
+    exact = X[got].astype(np.float64) @ q.astype(np.float64)
+    scale = max(1e-30, np.abs(s_ref).max())
+    assert np.all(np.abs(exact - s_ref) <= rtol * scale), (ids, ref_ids)
+
+
+# ------------------------------------------------------------------ configs
+SMALL = [
+    ("tiny", None, None, 32, 8),
+    ("c2", None, 200, 64, 32),
+    ("c3", 40_000, 64, 64, 64),
+    ("c3", 40_000, 64, 64, 1),
+    ("c4", 300_000, 32, 32, 128),    # pilot stride > 1 (n > 2^18)
+    ("c4", 300_000, 32, 64, 128),
+    ("scale", 70_000, 16, 128, 256),
+]
+
+
+def _ids(case):
+    return "-".join(str(x) for x in case)
+
+
+@pytest.fixture(scope="session")
+def built():
+    cache = {}
+
+    def get(name, n, nq, L, m, **kw):
+        key = (name, n, nq, L, m, tuple(sorted(kw.items())))
+        if key not in cache:
+            P = _P()
+            cfg, X, Q = dataset(workloads.CONFIGS[name], n, nq)
+            Xd = torch.from_numpy(X).cuda()
+            idx = P.Index(Xd, L, m, seed=cfg.seed, **kw)
+            orc = oracle.OracleIndex(X, idx.hash_bits, m, seed=cfg.seed,
+                                     eps=kw.get("eps", 0.01),
+                                     scheme=kw.get("scheme", "percentile"))
+            cache[key] = (cfg, X, Q, Xd, idx, orc)
+        return cache[key]
+    return get
+
+
+@pytest.mark.parametrize("case", SMALL, ids=_ids)
+def test_build_parity(built, case):
+    cfg, X, Q, Xd, idx, orc = built(*case)
+    norm2, perm, offsets, V = idx.partition()
+    assert np.array_equal(norm2.view(np.uint64), orc.norm2.view(np.uint64))   # bit-exact
+    assert np.array_equal(perm, orc.perm)
+    assert np.array_equal(offsets, orc.offsets)
+    assert np.array_equal(V, orc.V)
+    assert np.array_equal(idx.projection(), orc.A)
+    assert np.array_equal(idx.rank_table(), orc.R)
+    ocodes, z = orc.codes(want_z=True)
+    gcodes = idx.codes()[np.argsort(perm, kind="stable")]
+    assert_codes_match(gcodes, ocodes, z, idx.hash_bits)
+
+
+@pytest.mark.parametrize("case", SMALL, ids=_ids)
+def test_query_codes_parity(built, case):
+    cfg, X, Q, Xd, idx, orc = built(*case)
+    g = idx.query_codes(torch.from_numpy(Q).cuda()).cpu().numpy().view(np.uint32)
+    o, z = oracle.query_codes(Q, orc.A, want_z=True)
+    assert_codes_match(g, o, z, idx.hash_bits)
+
+
+def _budgets(cfg, n):
+    Ts = sorted(set([1, 7, 100, (n + 99) // 100, n // 7, n, n + 5]
+                    + [min(cfg.T(b), n) for b in cfg.budgets]))
+    return [t for t in Ts if t >= 1]
+
+
+@pytest.mark.parametrize("case", SMALL, ids=_ids)
+def test_candidates_parity(built, case):
+    """Identical codes -> identical candidate sets, ranks and (R, id) order."""
+    cfg, X, Q, Xd, idx, orc = built(*case)
+    n = X.shape[0]
+    ocodes = orc.codes()
+    idx.set_codes(ocodes[orc.perm])
+    qc = oracle.query_codes(Q, orc.A)
+    nq = min(len(Q), 16)
+    qcd = torch.from_numpy(qc[:nq].view(np.int32)).cuda()
+    for T in _budgets(cfg, n):
+        gid, grk = idx.candidates(T, qcodes=qcd)
+        gid = gid.cpu().numpy()
+        grk = grk.cpu().numpy().view(np.uint16)
+        for qi in range(nq):
+            oid, ork = oracle.candidates(ocodes, orc.part, qc[qi], orc.R, T)
+            order = np.lexsort((gid[qi], grk[qi]))
+            assert np.array_equal(gid[qi][order], oid), (T, qi)
+            assert np.array_equal(grk[qi][order], ork), (T, qi)
+
+
+@pytest.mark.parametrize("case", SMALL, ids=_ids)
+def test_query_parity(built, case):
+    """End-to-end nrlsh_query with the oracle's codes injected."""
+    cfg, X, Q, Xd, idx, orc = built(*case)
+    n = X.shape[0]
+    ocodes = orc.codes()
+    idx.set_codes(ocodes[orc.perm])
+    nq = min(len(Q), 24)
+    Qd = torch.from_numpy(Q[:nq]).cuda()
+    gq = idx.query_codes(Qd).cpu().numpy().view(np.uint32)
+    oq = oracle.query_codes(Q[:nq], orc.A)
+    k = cfg.k
+    for T in [t for t in _budgets(cfg, n) if t <= n][:5] + [n]:
+        ids, sc = idx.query(Qd, k, T)
+        ids, sc = ids.cpu().numpy(), sc.cpu().numpy()
+        for qi in range(nq):
+            if not np.array_equal(gq[qi], oq[qi]):
+                continue     # a query bit inside the 1e-5 band: different probe order allowed
+            a, s = oracle.query(X, ocodes, orc.part, orc.R, orc.A, Q[qi], T, k)
+            assert_topk_match(ids[qi], sc[qi], a, s, X, Q[qi])
+
+
+@pytest.mark.parametrize("name,n,nq,k", [("tiny", None, 50, 10), ("c2", None, 40, 10),
+                                         ("c3", 60_000, 24, 10), ("scale", 80_000, 8, 100)])
+def test_exact_topk_parity(name, n, nq, k):
+    P = _P()
+    cfg, X, Q = dataset(workloads.CONFIGS[name], n, nq)
+    Q = Q[:nq]
+    ids, sc = P.exact_topk(torch.from_numpy(X).cuda(), torch.from_numpy(Q).cuda(), k)
+    ids, sc = ids.cpu().numpy(), sc.cpu().numpy()
+    for qi in range(len(Q)):
+        a, s = oracle.exact_topk(X, Q[qi], k)
+        assert_topk_match(ids[qi], sc[qi], a, s, X, Q[qi])
+
+
+# --------------------------------------------------------------- edge cases
+def test_full_budget_equals_brute_force(built):
+    cfg, X, Q, Xd, idx, orc = built("tiny", None, None, 32, 8)
+    P = _P()
+    Qd = torch.from_numpy(Q[:20]).cuda()
+    a, sa = idx.query(Qd, 10, X.shape[0])
+    b, sb = P.exact_topk(Xd, Qd, 10)
+    assert np.array_equal(a.cpu().numpy(), b.cpu().numpy())
+
+
+def test_budget_below_k_pads(built):
+    cfg, X, Q, Xd, idx, orc = built("tiny", None, None, 32, 8)
+    ids, sc = idx.query(torch.from_numpy(Q[:5]).cuda(), 10, 3)
+    ids, sc = ids.cpu().numpy(), sc.cpu().numpy()
+    assert np.all(ids[:, 3:] == -1) and np.all(np.isneginf(sc[:, 3:]))
+    assert np.all(ids[:, :3] >= 0)
+
+
+def test_host_pointers_match_device(built):
+    """HOST buffers through the same ABI (the e2e path) give the same answers."""
+    P = _P()
+    cfg, X, Q, Xd, idx, orc = built("tiny", None, None, 32, 8)
+    idx_h = P.Index(X, 32, 8, seed=cfg.seed)          # numpy -> host pointer, owned copy
+    assert np.array_equal(idx_h.codes(), idx.codes())
+    a, sa = idx_h.query(Q[:10], 10, 100)
+    b, sb = idx.query(torch.from_numpy(Q[:10]).cuda(), 10, 100)
+    assert np.array_equal(a, b.cpu().numpy()) and np.array_equal(sa, sb.cpu().numpy())
+    g1, _ = P.exact_topk(X, Q[:10], 10)
+    g2, _ = P.exact_topk(Xd, torch.from_numpy(Q[:10]).cuda(), 10)
+    assert np.array_equal(g1, g2.cpu().numpy())
+
+
+def test_m_equals_n_and_m1_degenerate():
+    P = _P()
+    cfg, X, Q = dataset(workloads.CONFIGS["tiny"], 200, 8)
+    for m in (1, 200):
+        idx = P.Index(torch.from_numpy(X).cuda(), 32, m, seed=3)
+        orc = oracle.OracleIndex(X, 32, m, seed=3)
+        _, perm, off, V = idx.partition()
+        assert np.array_equal(perm, orc.perm) and np.array_equal(V, orc.V)
+        ocodes = orc.codes()
+        idx.set_codes(ocodes[orc.perm])
+        qc = oracle.query_codes(Q, orc.A)
+        gid, grk = idx.candidates(50, qcodes=torch.from_numpy(qc.view(np.int32)).cuda())
+        for qi in range(len(Q)):
+            oid, ork = oracle.candidates(ocodes, orc.part, qc[qi], orc.R, 50)
+            g = gid[qi].cpu().numpy()
+            r = grk[qi].cpu().numpy().view(np.uint16)
+            o = np.lexsort((g, r))
+            assert np.array_equal(g[o], oid)
+
+
+@pytest.mark.parametrize("kind", ["all_equal", "duplicates", "zeros"])
+def test_degenerate_norms(kind):
+    """Ties in the ranking, duplicated items, zero-norm items and a
+    sub-dataset of zero vectors (V_j = 0).  n > 2048 forces the multi-level
+    refinement of the exact selection."""
+    P = _P()
+    rng = np.random.default_rng(5)
+    n, d = 50_000, 16
+    X = rng.standard_normal((n, d)).astype(np.float32)
+    if kind == "all_equal":
+        X = (X / np.linalg.norm(X, axis=1, keepdims=True)).astype(np.float32)
+        X[:, 0] = 1.0
+        X[:, 1:] = 0.0
+        X[::2, 0] = 0.0
+        X[::2, 1] = 1.0            # every norm exactly 1, two directions
+    elif kind == "duplicates":
+        X[: n // 2] = X[n // 2:]
+    else:
+        X[: n // 3] = 0.0
+    idx = P.Index(torch.from_numpy(X).cuda(), 64, 16, seed=9)
+    orc = oracle.OracleIndex(X, 64, 16, seed=9)
+    norm2, perm, off, V = idx.partition()
+    assert np.array_equal(perm, orc.perm) and np.array_equal(V, orc.V)
+    ocodes, z = orc.codes(want_z=True)
+    gc = idx.codes()[np.argsort(perm, kind="stable")]
+    assert_codes_match(gc, ocodes, z, 64)
+
+
+def test_uniform_scheme_and_bit_accounting():
+    """NEXT-2 uniform partitioning and NEXT-1 index bits inside the
+    code budget (32 bits with 32 sub-datasets -> 27 hash bits)."""
+    P = _P()
+    cfg, X, Q = dataset(workloads.CONFIGS["c3"], 20_000, 16)
+    idx = P.Index(torch.from_numpy(X).cuda(), 32, 32, seed=1, scheme="uniform",
+                  index_bits_in_budget=True)
+    assert idx.hash_bits == 27
+    orc = oracle.OracleIndex(X, 27, 32, seed=1, scheme="uniform")
+    _, perm, off, V = idx.partition()
+    assert np.array_equal(perm, orc.perm) and np.array_equal(off, orc.offsets)
+    assert np.array_equal(V, orc.V)
+    assert np.array_equal(idx.rank_table(), orc.R)
+    ocodes, z = orc.codes(want_z=True)
+    assert_codes_match(idx.codes()[np.argsort(perm, kind="stable")], ocodes, z, 27)
+    idx.set_codes(ocodes[orc.perm])
+    qc = oracle.query_codes(Q, orc.A)
+    gid, grk = idx.candidates(300, qcodes=torch.from_numpy(qc.view(np.int32)).cuda())
+    for qi in range(len(Q)):
+        oid, ork = oracle.candidates(ocodes, orc.part, qc[qi], orc.R, 300)
+        g = gid[qi].cpu().numpy()
+        r = grk[qi].cpu().numpy().view(np.uint16)
+        o = np.lexsort((g, r))
+        assert np.array_equal(g[o], oid) and np.array_equal(r[o], ork)
+
+
+def test_forced_fallback_path(built, monkeypatch):
+    """The exact fallback (taken when the pilot bound under/overflows) gives the
+    same candidates as the oracle; forced for every query via a test switch."""
+    cfg, X, Q, Xd, idx, orc = built("c4", 300_000, 32, 32, 128)
+    monkeypatch.setenv("NRLSH_TEST_FORCE_FALLBACK", "1")
+    P = _P()
+    ocodes = orc.codes()
+    idx.set_codes(ocodes[orc.perm])
+    qc = oracle.query_codes(Q[:6], orc.A)
+    gid, grk = idx.candidates(2000, qcodes=torch.from_numpy(qc.view(np.int32)).cuda())
+    assert P.last_query_stats()["fallback_queries"] == 6
+    for qi in range(6):
+        oid, ork = oracle.candidates(ocodes, orc.part, qc[qi], orc.R, 2000)
+        g = gid[qi].cpu().numpy()
+        r = grk[qi].cpu().numpy().view(np.uint16)
+        o = np.lexsort((g, r))
+        assert np.array_equal(g[o], oid) and np.array_equal(r[o], ork)
+
+
+def test_errors():
+    P = _P()
+    X = np.random.default_rng(0).standard_normal((1000, 8)).astype(np.float32)
+    Xb = X.copy()
+    Xb[17, 3] = np.nan
+    with pytest.raises(P.NrlshError) as e:
+        P.Index(torch.from_numpy(Xb).cuda(), 32, 4)
+    assert e.value.code == "ENONFINITE" and "17" in str(e.value)
+    idx = P.Index(torch.from_numpy(X).cuda(), 32, 4)
+    Qz = np.random.default_rng(1).standard_normal((9, 8)).astype(np.float32)
+    Qz[7] = 0.0
+    with pytest.raises(P.NrlshError) as e:
+        idx.query(torch.from_numpy(Qz).cuda(), 5, 10)
+    assert e.value.code == "EZERONORM" and "7" in str(e.value)
+    with pytest.raises(P.NrlshError) as e:
+        idx.query(torch.from_numpy(X[:3]).cuda(), 0, 10)
+    assert e.value.code == "EINVAL"
+    with pytest.raises(P.NrlshError) as e:
+        idx.query(torch.from_numpy(X[:3]).cuda(), 5, 0)
+    assert e.value.code == "EINVAL"
+
+
+# ------------------------------------------------------- full (BASELINE) sizes
+@pytest.mark.parametrize("name,L,m", [("c4", 64, 128), ("c4", 32, 128), ("scale", 128, 256)])
+def test_full_size_sampled(name, L, m):
+    """BASELINE.json full sizes, in the launch configuration bench.py times:
+    partition bit-exact over all n; every code bit (band-exempt); candidates and
+    top-k on sampled queries with the oracle's codes injected; ground truth on
+    sampled queries."""
+    P = _P()
+    cfg = workloads.CONFIGS[name]
+    _, X, Q = dataset(cfg)
+    Xd = torch.from_numpy(X).cuda()
+    idx = P.Index(Xd, L, m, seed=cfg.seed)
+    n = X.shape[0]
+    nv = oracle.norm2(X)
+    norm2, perm, off, V = idx.partition()
+    assert np.array_equal(norm2.view(np.uint64), nv.view(np.uint64))
+    part, operm, ooff, oV = oracle.partition(nv, m)
+    assert np.array_equal(perm, operm) and np.array_equal(off, ooff) and np.array_equal(V, oV)
+    A = oracle.projection(cfg.seed, X.shape[1] + 1, L)
+    assert np.array_equal(idx.projection(), A)
+    R, _ = oracle.rank_table(np.sqrt(oV), L, 0.01)
+    assert np.array_equal(idx.rank_table(), R)
+    ocodes = oracle.item_codes_parallel(X, part, oV, nv, A)
+    pos_of_id = np.empty(n, np.int64)
+    pos_of_id[perm] = np.arange(n)
+    gcodes = idx.codes()[pos_of_id]
+    rows = np.nonzero((gcodes != ocodes).any(axis=1))[0]
+    assert len(rows) < max(10, n // 1000)
+    if len(rows):
+        oc, z = oracle.item_codes(X[rows], part[rows], oV, nv[rows], A, want_z=True)
+        assert_codes_match(gcodes[rows], oc, z, L)
+    idx.set_codes(ocodes[perm])
+    qs = Q[:6]
+    qc = oracle.query_codes(qs, A)
+    T = min(cfg.T(cfg.budgets[0]), n)
+    gid, grk = idx.candidates(T, qcodes=torch.from_numpy(qc.view(np.int32)).cuda())
+    gid, grk = gid.cpu().numpy(), grk.cpu().numpy().view(np.uint16)
+    for qi in range(len(qs)):
+        oid, ork = oracle.candidates(ocodes, part, qc[qi], R, T)
+        o = np.lexsort((gid[qi], grk[qi]))
+        assert np.array_equal(gid[qi][o], oid) and np.array_equal(grk[qi][o], ork)
+    Qd = torch.from_numpy(qs).cuda()
+    gq = idx.query_codes(Qd).cpu().numpy().view(np.uint32)
+    ids, sc = idx.query(Qd, cfg.k, T)
+    ids, sc = ids.cpu().numpy(), sc.cpu().numpy()
+    for qi in range(len(qs)):
+        if np.array_equal(gq[qi], qc[qi]):
+            a, s = oracle.query(X, ocodes, part, R, A, qs[qi], T, cfg.k)
+            assert_topk_match(ids[qi], sc[qi], a, s, X, qs[qi])
+    gt_ids, gt_sc = P.exact_topk(Xd, torch.from_numpy(Q[:3]).cuda(), cfg.k)
+    gt_ids, gt_sc = gt_ids.cpu().numpy(), gt_sc.cpu().numpy()
+    for qi in range(3):
+        a, s = oracle.exact_topk(X, Q[qi], cfg.k)
+        assert_topk_match(gt_ids[qi], gt_sc[qi], a, s, X, Q[qi])
