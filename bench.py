@@ -1,0 +1,441 @@
+#!/usr/bin/env python
+"""bench.py — RANGE-LSH hot path on B200 (driver contract: one JSON line on rank 0).
+
+A step is one pass of the whole hot path over one
+batch of synthetic input: index build (norms, percentile partition, transform +
+SRP codes, rank table), the batched query (query codes, Hamming scan + metric +
+filter, top-T select, exact re-rank + top-k) and the exact brute-force ground
+truth used for recall@10.  Default workload: BASELINE.json configs[3] (c4,
+ImageNet-SIFT-shaped, "index build time and batched query throughput"),
+64-bit codes, probe budget 1% of n.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+                  [--config c4|scale|...] [--bits 64] [--budget-permille 10]
+
+Multi-GPU (torchrun): every rank builds the same index and answers its own
+query shard (queries are independent units) — weak scaling, no data-path
+collective; torch.distributed is used for the barrier and the max-over-ranks
+time only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads  # noqa: E402
+
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+# measured on this pool's B200 by tools/ubench.cu (profiles/r01/ubench_popc.txt):
+# 4.569e12 POPC/s at 1965 MHz = 15.7 POPC/clk/SM x 148 SM (guide value 16/clk/SM)
+POPC_PEAK_PER_S = 4.569e12
+FFMA_PEAK_FLOPS = 148 * 128 * 2 * 1.965e9       # 74.4 TFLOP/s fp32 SIMT (128 FMA/clk/SM)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--bits", type=int, default=None)
+    ap.add_argument("--parts", type=int, default=None)
+    ap.add_argument("--budget-permille", type=float, default=None,
+                    help="probe budget T as per-mille of n (default: config's largest budget)")
+    ap.add_argument("--nq", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    return ap.parse_args()
+
+
+def workload(args):
+    cfg = workloads.CONFIGS[args.config]
+    L = args.bits or cfg.code_bits[-1]
+    m = args.parts or cfg.num_parts[0]
+    nq = args.nq or cfg.nq
+    if args.budget_permille is not None:
+        T = int(np.ceil(args.budget_permille * cfg.n / 1000.0))
+    else:
+        T = max(cfg.budget_list())
+    desc = {
+        "workload": f"{cfg.name}: n={cfg.n:,} d={cfg.d} {cfg.norm_law} norms x unit Gaussian "
+                    f"directions, {L}-bit SRP codes, m={m} percentile sub-datasets, "
+                    f"{nq:,} unit queries (sub-batches of {cfg.query_batch}), top-{cfg.k}, "
+                    f"T={T:,} ({T / cfg.n:.2%} of n); step = build + query batch + exact "
+                    f"ground truth",
+        "n": cfg.n, "d": cfg.d, "code_bits": L, "num_parts": m, "nq_per_gpu": nq, "k": cfg.k,
+        "probe_budget": T, "query_batch": cfg.query_batch, "seed": cfg.seed,
+        "l2": "flushed between timed steps (512 MiB write)",
+    }
+    return cfg, L, m, nq, T, desc
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.rows = []
+        self.proc = None
+        self.gpu = gpu_index
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(self.gpu)], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = [], None, set()
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx = float(r[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, r[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------- roofline
+def load_peaks():
+    try:
+        with open(PEAKS_FILE) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+def roofline_for(slot, ms_total, count, info, peaks, peaks_src):
+    """Algorithmic work per launch of the dominant kernel class / its mean duration."""
+    if count == 0 or ms_total <= 0:
+        return None
+    per_launch_s = ms_total / count / 1e3
+    n, d, L, W, nq = info["n"], info["d"], info["L"], info["W"], info["nq"]
+    T, k, m = info["T"], info["k"], info["m"]
+    traffic = info.get("traffic", {}).get(slot)
+    if slot == "scan":
+        # L/32 POPC per (query, item) pair the scan must evaluate;
+        # pairs of sub-datasets whose radius is < 0 are skipped exactly.
+        ops = info["scanned_pairs"] * W / count
+        ach = ops / per_launch_s
+        return {"bound": "alu", "kernel": "k6_scan (XOR+POPC Hamming scan + metric filter)",
+                "achieved": ach / 1e12, "peak": POPC_PEAK_PER_S / 1e12, "unit": "TPOPC/s",
+                "frac": ach / POPC_PEAK_PER_S, "traffic": traffic,
+                "peak_source": "tools/ubench.cu measured POPC rate (profiles/r01/ubench_popc.txt)",
+                "logical_pairs_per_s": nq * n / (ms_total / 1e3)}
+    if slot == "gt_filter":
+        fl = 2.0 * nq * n * d / count
+        ach = fl / per_launch_s
+        if info.get("gt_tensor"):
+            pk = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")) * 1e12
+            return {"bound": "tensor", "kernel": "gt_filter (tcgen05 bf16)", "achieved": ach / 1e12,
+                    "peak": pk / 1e12, "unit": "TFLOP/s", "frac": ach / pk, "traffic": traffic,
+                    "peak_source": f"MEASURED_PEAKS.json bf16 sustained ({peaks_src})"}
+        return {"bound": "alu", "kernel": "gt_filter_simt (fp32 FFMA filter GEMM)",
+                "achieved": ach / 1e12, "peak": FFMA_PEAK_FLOPS / 1e12, "unit": "TFLOP/s",
+                "frac": ach / FFMA_PEAK_FLOPS, "traffic": traffic,
+                "peak_source": "148 SM x 128 FFMA/clk x 2 x 1965 MHz"}
+    hbm = peaks["hbm_gbs"] * 1e9
+    if slot == "score":
+        by = info["score_bytes"] / count
+    elif slot in ("codes", "norms"):
+        by = n * d * 4.0 + (n * W * 4.0 if slot == "codes" else n * 8.0)
+    else:
+        return None
+    ach = by / per_launch_s
+    return {"bound": "hbm", "kernel": slot, "achieved": ach / 1e9, "peak": hbm / 1e9,
+            "unit": "GB/s", "frac": ach / hbm, "traffic": traffic,
+            "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peaks_src})"}
+
+
+def load_traffic():
+    """dram bytes per launch from the committed ncu --set full summary, if any."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+# ----------------------------------------------------------------- CPU oracle
+def cpu_oracle_step(cfg, X, Q, L, m, T, k, nq_full, nsample, threads):
+    """The oracle, as it stands, on the host cores: full index build (Alg. 1) over
+    all n items, then `nsample` whole queries (codes, candidates, re-rank) plus
+    their exact top-k; returns extrapolated seconds for the full step."""
+    import oracle
+    from concurrent.futures import ThreadPoolExecutor
+    t0 = time.perf_counter()
+    nv = oracle.norm2(X)
+    part, perm, off, V = oracle.partition(nv, m)
+    A = oracle.projection(cfg.seed, X.shape[1] + 1, L)
+    R, _ = oracle.rank_table(np.sqrt(V), L, 0.01)
+    codes = oracle.item_codes_parallel(X, part, V, nv, A, threads=threads)
+    t_build = time.perf_counter() - t0
+
+    def one(q):
+        a, _ = oracle.query(X, codes, part, R, A, q, T, k)
+        b, _ = oracle.exact_topk(X, q, k)
+        return a, b
+
+    t1 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        list(ex.map(one, list(Q[:nsample])))
+    t_q = (time.perf_counter() - t1) / nsample       # wall seconds per query at `threads`
+    return t_build, t_q, t_build + nq_full * t_q
+
+
+# ----------------------------------------------------------------- main arms
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def run_reference(args):
+    """The oracle arm (--impl reference): rank 0 only; the oracle as it stands on
+    the host cores, same config/metric/unit as the native arm."""
+    world, rank, local = dist_setup(args)
+    if rank != 0:
+        return
+    import oracle
+    from concurrent.futures import ThreadPoolExecutor
+    cfg, L, m, nq, T, desc = workload(args)
+    X = workloads.make_items(cfg)
+    Q = workloads.make_queries(cfg, nq=8 * (args.warmup + args.steps))
+    threads = os.cpu_count() or 1
+    nsample = 8
+    t0 = time.perf_counter()
+    nv = oracle.norm2(X)
+    part, perm, off, V = oracle.partition(nv, m)
+    A = oracle.projection(cfg.seed, X.shape[1] + 1, L)
+    R, _ = oracle.rank_table(np.sqrt(V), L, 0.01)
+    codes = oracle.item_codes_parallel(X, part, V, nv, A, threads=threads)
+    t_build = time.perf_counter() - t0
+
+    def one(q):
+        oracle.query(X, codes, part, R, A, q, T, cfg.k)
+        oracle.exact_topk(X, q, cfg.k)
+
+    tq = []
+    for i in range(args.warmup + args.steps):
+        t1 = time.perf_counter()
+        with ThreadPoolExecutor(max_workers=threads) as ex:
+            list(ex.map(one, list(Q[i * nsample:(i + 1) * nsample])))
+        if i >= args.warmup:
+            tq.append((time.perf_counter() - t1) / nsample)
+    t_q = float(np.mean(tq)) if tq else 0.0
+    t_step = t_build + nq * t_q
+    value = nq / t_step
+    sample = (f"oracle build over all {cfg.n:,} items once ({t_build:.1f} s, item codes on "
+              f"{threads} threads) + per step {nsample} whole queries (codes, candidates, "
+              f"re-rank, exact top-k) on {threads} threads ({t_q * 1e3:.0f} ms/query wall), "
+              f"extrapolated to a {nq:,}-query step")
+    line = {"impl": "reference", "metric": "queries/s at fixed probe budget with recall@10",
+            "value": value, "unit": "queries/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": desc,
+            "cpu_baseline": {"value": value, "unit": "queries/s", "cores": threads,
+                             "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_native(args):
+    import torch
+    world, rank, local = dist_setup(args)
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    else:
+        dist = None
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    import paper_1809_08782_b200 as P
+
+    cfg, L, m, nq, T, desc = workload(args)
+    t_gen = time.perf_counter()
+    X = workloads.make_items(cfg)
+    Q = workloads.make_queries(cfg, nq=nq, shard=rank)
+    t_gen = time.perf_counter() - t_gen
+    Xd = torch.from_numpy(X).to(dev)
+    Qd = torch.from_numpy(Q).to(dev)
+    k = cfg.k
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+
+    def step():
+        idx = P.Index(Xd, L, m, seed=cfg.seed, query_batch=cfg.query_batch)
+        ids, sc = idx.query(Qd, k, T)
+        qstats = P.last_query_stats()
+        gid, gsc = idx.exact_topk(Qd, k)
+        idx.close()
+        return ids, gid, qstats
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(local)
+    P.profile_read(reset=True)
+    P.profile_enable(True)
+    launches0 = P.launch_count()
+    scanned = 0
+    evs = []
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    for _ in range(args.steps):
+        flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        ids, gid, qstats = step()
+        e1.record(stream)
+        evs.append((e0, e1))
+        scanned += qstats["scanned_pairs"]
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clocks = sampler.stop()
+    launches = P.launch_count() - launches0
+    P.profile_enable(False)
+    prof = P.profile_read(reset=True)
+    ms = [a.elapsed_time(b) for a, b in evs]
+    ms_step = float(np.mean(ms))
+    if dist:
+        t = torch.tensor([ms_step], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step = float(t.item())
+    value = world * nq / (ms_step / 1e3)
+
+    ids_h = ids.cpu().numpy()
+    gid_h = gid.cpu().numpy()
+    rec = float(np.mean([len(set(a.tolist()) & set(b.tolist())) / k for a, b in zip(ids_h, gid_h)]))
+
+    # -------- end to end through the public API with HOST buffers (pinned)
+    e2e = None
+    if not args.no_e2e:
+        Xh = torch.from_numpy(X).pin_memory()
+        Qh = torch.from_numpy(Q).pin_memory()
+        oid = torch.empty((nq, k), dtype=torch.int64).pin_memory()
+        osc = torch.empty((nq, k), dtype=torch.float32).pin_memory()
+        gid2 = torch.empty((nq, k), dtype=torch.int64).pin_memory()
+        gsc2 = torch.empty((nq, k), dtype=torch.float32).pin_memory()
+        e2e_ms = []
+        for _ in range(args.e2e_steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            idx = P.Index(Xh, L, m, seed=cfg.seed, query_batch=cfg.query_batch)
+            idx.query(Qh, k, T, out_ids=oid, out_scores=osc)
+            idx.exact_topk(Qh, k, out_ids=gid2, out_scores=gsc2)
+            idx.close()
+            torch.cuda.synchronize()
+            e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        e2 = float(np.mean(e2e_ms))
+        if dist:
+            t = torch.tensor([e2], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2 = float(t.item())
+        e2e = {"value": world * nq / (e2 / 1e3), "unit": "queries/s",
+               "h2d_bytes_per_step": int(X.nbytes + 2 * Q.nbytes),
+               "d2h_bytes_per_step": int(2 * (oid.numel() * 8 + osc.numel() * 4)),
+               "ms_per_step": e2}
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    peaks, peaks_src = load_peaks()
+    stage = {name: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps}
+             for name, v in prof.items() if v[1] > 0}
+    W = 1 if L <= 32 else (2 if L <= 64 else 4)
+    info = {"n": cfg.n, "d": cfg.d, "L": L, "W": W, "nq": nq, "T": T, "k": k, "m": m,
+            "scanned_pairs": scanned, "traffic": load_traffic(),
+            "score_bytes": float(nq) * T * cfg.d * 4.0 * args.steps, "gt_tensor": False}
+    dom = max(((n_, v) for n_, v in prof.items() if v[1] > 0), key=lambda x: x[1][0])
+    roof = roofline_for(dom[0], dom[1][0], dom[1][1], info, peaks, peaks_src)
+    scan_roof = roofline_for("scan", *prof["scan"], info, peaks, peaks_src) if prof["scan"][1] else None
+
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        threads = os.cpu_count() or 1
+        nsample = 8
+        t_build, t_q, t_step = cpu_oracle_step(cfg, X, Q, L, m, T, k, nq, nsample, threads)
+        cpu = {"value": nq / t_step, "unit": "queries/s", "cores": threads, "kind": "oracle",
+               "sample": f"oracle build over all {cfg.n:,} items ({t_build:.1f} s; item codes "
+                         f"on {threads} threads) + {nsample} whole queries incl. exact top-k "
+                         f"({t_q * 1e3:.0f} ms/query wall on {threads} threads), extrapolated "
+                         f"to {nq:,} queries"}
+
+    line = {
+        "metric": "queries/s at fixed probe budget with recall@10",
+        "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32 codes / f32 scores",
+        "data": "synthetic", "config": desc,
+        "recall_at_10": rec,
+        "stage_ms_per_step": stage,
+        "roofline": roof, "scan_roofline": scan_roof,
+        "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+        "clocks": clocks,
+        "notes": {"input_gen_s": t_gen, "peaks": peaks_src,
+                  "step_ms_all": ms},
+    }
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_native(args)
+
+
+if __name__ == "__main__":
+    main()
