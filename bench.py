@@ -171,7 +171,7 @@ def roofline_for(slot, ms_total, count, info, peaks, peaks_src):
                 "frac": ach / FFMA_PEAK_FLOPS, "traffic": traffic,
                 "peak_source": "148 SM x 128 FFMA/clk x 2 x 1965 MHz"}
     hbm = peaks["hbm_gbs"] * 1e9
-    if slot == "score":
+    if slot == "rerank":
         by = info["score_bytes"] / count
     elif slot in ("codes", "norms"):
         by = n * d * 4.0 + (n * W * 4.0 if slot == "codes" else n * 8.0)
@@ -394,10 +394,12 @@ def run_native(args):
     W = 1 if L <= 32 else (2 if L <= 64 else 4)
     info = {"n": cfg.n, "d": cfg.d, "L": L, "W": W, "nq": nq, "T": T, "k": k, "m": m,
             "scanned_pairs": scanned, "traffic": load_traffic(),
-            "score_bytes": float(nq) * T * cfg.d * 4.0 * args.steps, "gt_tensor": False}
+            "score_bytes": float(nq) * T * cfg.d * 4.0 * args.steps, "gt_tensor": True}
     dom = max(((n_, v) for n_, v in prof.items() if v[1] > 0), key=lambda x: x[1][0])
     roof = roofline_for(dom[0], dom[1][0], dom[1][1], info, peaks, peaks_src)
     scan_roof = roofline_for("scan", *prof["scan"], info, peaks, peaks_src) if prof["scan"][1] else None
+    others = {s_: roofline_for(s_, *prof[s_], info, peaks, peaks_src)
+              for s_ in ("gt_filter", "rerank", "codes", "norms") if prof.get(s_, (0, 0))[1]}
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:
@@ -418,7 +420,7 @@ def run_native(args):
         "data": "synthetic", "config": desc,
         "recall_at_10": rec,
         "stage_ms_per_step": stage,
-        "roofline": roof, "scan_roofline": scan_roof,
+        "roofline": roof, "scan_roofline": scan_roof, "other_rooflines": others,
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
         "clocks": clocks,
         "notes": {"input_gen_s": t_gen, "peaks": peaks_src,

@@ -160,6 +160,11 @@ nrlsh_status nrlsh_index_exact_topk(const nrlsh_index *index, const float *queri
                                     int32_t k, int64_t *out_ids, float *out_scores,
                                     void *cuda_stream);
 
+/* Statistics of the last exact top-k on this thread: the largest and the total
+   number of filter survivors per query (re-scored exactly), and the number of
+   queries whose survivors overflowed the buffer (answered by a full exact scan). */
+nrlsh_status nrlsh_last_exact_stats(int64_t *max_cand, int64_t *sum_cand, int64_t *overflow);
+
 /* ---- tracing ------------------------------------------------------------
    With profiling on, every kernel class is bracketed by CUDA events recorded on
    the stream it is launched on; elapsed times are accumulated per class at the

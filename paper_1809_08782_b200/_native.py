@@ -24,7 +24,7 @@ EXPORTS = [
     "nrlsh_get_projection", "nrlsh_get_rank_table", "nrlsh_get_codes", "nrlsh_set_codes",
     "nrlsh_query_codes", "nrlsh_query_candidates", "nrlsh_last_query_stats",
     "nrlsh_index_exact_topk", "nrlsh_profile_enable", "nrlsh_profile_read",
-    "nrlsh_profile_slot_name", "nrlsh_launch_count",
+    "nrlsh_profile_slot_name", "nrlsh_launch_count", "nrlsh_last_exact_stats",
 ]
 
 
@@ -93,6 +93,8 @@ def lib():
         L.nrlsh_profile_read.restype = C.c_int
         L.nrlsh_profile_slot_name.argtypes = [i32]
         L.nrlsh_profile_slot_name.restype = C.c_char_p
+        L.nrlsh_last_exact_stats.argtypes = [p, p, p]
+        L.nrlsh_last_exact_stats.restype = st
         L.nrlsh_launch_count.argtypes = []
         L.nrlsh_launch_count.restype = C.c_int64
         _lib = L
@@ -264,6 +266,12 @@ def last_query_stats():
     a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
     _check(lib().nrlsh_last_query_stats(C.byref(a), C.byref(b), C.byref(c)))
     return {"fallback_queries": a.value, "kernel_launches": b.value, "scanned_pairs": c.value}
+
+
+def last_exact_stats():
+    a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
+    _check(lib().nrlsh_last_exact_stats(C.byref(a), C.byref(b), C.byref(c)))
+    return {"max_survivors": a.value, "sum_survivors": b.value, "overflow_queries": c.value}
 
 
 def profile_enable(on=True):

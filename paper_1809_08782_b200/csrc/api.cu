@@ -21,6 +21,7 @@ thread_local std::string g_last_error;
 thread_local int64_t g_last_fallbacks = 0;
 thread_local int64_t g_last_launches = 0;
 thread_local int64_t g_last_pairs = 0;
+thread_local int64_t g_last_gt_max_cand = 0, g_last_gt_sum_cand = 0, g_last_gt_overflow = 0;
 
 nrlsh_status fail(nrlsh_status st, const std::string &msg) {
     g_last_error = msg;
@@ -480,11 +481,11 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
                        bf.get<unsigned long long>(), cand, crank, fl.get<int>(), pairs, s);
         if (want_topk) {
             {
-                ProfScope p(SLOT_SCORE, s);
+                ProfScope p(SLOT_RERANK, s);
                 launch_score(ix->X, ix->d, Qd, Qb, cand, Tq, Tq, nullptr, 1, nullptr, nullptr,
                              0.f, sc.get<float>(), s);
             }
-            ProfScope p(SLOT_TOPK, s);
+            ProfScope p(SLOT_RERANK_TOPK, s);
             launch_topk(sc.get<float>(), cand, Qb, Tq, Tq, nullptr, 1, k,
                         (int64_t *)oi.dev + q0 * k, (float *)os.dev + q0 * k, nullptr, s);
         }
@@ -573,6 +574,7 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
     if (k < 1 || k > 1024) return fail(NRLSH_EINVAL, "k must be in [1, 1024]");
     cudaStream_t s = (cudaStream_t)cuda_stream;
     configure_pool();
+    g_last_gt_max_cand = g_last_gt_sum_cand = g_last_gt_overflow = 0;
     cudaError_t e;
     Staged Xs, Qs;
     if ((e = Xs.in(items, (size_t)n * d * 4, s))) return cuda_fail(e, "stage items");
@@ -582,21 +584,38 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
     if ((e = os.init(out_scores, (size_t)nq * k * 4, s))) return cuda_fail(e, "out_scores");
     const float *X = (const float *)Xs.dev;
     const float *Q = (const float *)Qs.dev;
-    // fp32 error bound of any summation order of d products: gamma_d |q||x|, inflated
-    const float eps_rel = (float)(1.25 * (d + 2) * std::ldexp(1.0, -24));
+    const bool use_tc = gt_tc_supported(d, k) && !getenv("NRLSH_GT_SIMT");
+    const int dp = (d + 7) / 8 * 8;
+    // certified error bound of fl(q.x) relative to |q||x|:
+    //  tensor path: bf16 operands (u = 2^-8: 2u + u^2) + fp32 accumulation of dp
+    //  exact products (dp * 2^-23 with truncating adds), x1.05 slack;
+    //  SIMT path: fp32 FMA chain, gamma_d inflated.
+    const double u = std::ldexp(1.0, -8);
+    const float eps_rel = use_tc ? (float)(1.05 * ((2 * u + u * u) + (1 + u) * (1 + u) * dp *
+                                                   std::ldexp(1.0, -23)))
+                                 : (float)(1.25 * (d + 2) * std::ldexp(1.0, -24));
     const int S = (int)std::max<int64_t>(1, std::min<int64_t>(64, n / (4 * (int64_t)k)));
-    const int64_t ns = (n + S - 1) / S;
-    const int64_t Cg = std::min<int64_t>(n, std::max<int64_t>(4 * (int64_t)S * k + 4096, 2 * k));
+    const int64_t ns = use_tc ? 1 : (n + S - 1) / S;
+    const int64_t Cg = use_tc ? std::min<int64_t>(n, std::max<int64_t>(16384, 256 * (int64_t)k))
+                              : std::min<int64_t>(n, std::max<int64_t>(4 * (int64_t)S * k + 4096, 2 * k));
     int Qmax = (int)std::min<int64_t>(1024, nq);
     while (Qmax > 64 && (int64_t)Qmax * (ns * 4 + Cg * 8) > ((int64_t)2500 << 20)) Qmax >>= 1;
-    DBuf xn, qn, ss, lb, tid, tsc, cc, cd, cs, fl;
-    if (xn.alloc((size_t)n * 4, s) || qn.alloc((size_t)nq * 4, s) ||
+    DBuf xn, qn, ss, lb, tid, tsc, cc, cd, cs, xb, qb, th;
+    const int64_t npad = (n + 255) / 256 * 256;   // |x| padded: the tc kernel bulk-loads 1 KB tiles
+    if (xn.alloc((size_t)npad * 4, s) || qn.alloc((size_t)nq * 4, s) ||
         ss.alloc((size_t)Qmax * ns * 4, s) || lb.alloc((size_t)Qmax * 4, s) ||
         tid.alloc((size_t)Qmax * k * 8, s) || tsc.alloc((size_t)Qmax * k * 4, s) ||
         cc.alloc((size_t)Qmax * 4, s) || cd.alloc((size_t)Qmax * Cg * 4, s) ||
-        cs.alloc((size_t)Qmax * Cg * 4, s))
+        cs.alloc((size_t)Qmax * Cg * 4, s) || th.alloc((size_t)Qmax * 4, s))
         return fail(NRLSH_ENOMEM, "exact_topk workspace");
-    {
+    if (use_tc) {
+        if (xb.alloc((size_t)n * dp * 2, s) || qb.alloc((size_t)nq * dp * 2, s))
+            return fail(NRLSH_ENOMEM, "exact_topk bf16 workspace");
+        ProfScope p(SLOT_GT_NORMS, s);
+        cudaMemsetAsync(xn.get<float>() + n, 0, (size_t)(npad - n) * 4, s);
+        launch_bf16_prep(X, n, d, dp, xb.p, xn.get<float>(), s);
+        launch_bf16_prep(Q, nq, d, dp, qb.p, qn.get<float>(), s);
+    } else {
         ProfScope p(SLOT_GT_NORMS, s);
         launch_vec_norms(X, n, d, xn.get<float>(), s);
         launch_vec_norms(Q, nq, d, qn.get<float>(), s);
@@ -609,19 +628,26 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
         const float *qnb = qn.get<float>() + q0;
         int64_t *oid = (int64_t *)oi.dev + q0 * k;
         float *osc = (float *)os.dev + q0 * k;
-        // pilot: certified lower bound of the k-th best score
-        {
-            ProfScope p(SLOT_SCORE, s);
-            launch_score(X, d, Qb_ptr, Qb, nullptr, ns, ns, nullptr, S, xn.get<float>(), qnb,
-                         eps_rel, ss.get<float>(), s);
-        }
-        {
-            ProfScope p(SLOT_TOPK, s);
-            launch_topk(ss.get<float>(), nullptr, Qb, ns, ns, nullptr, S, k, tid.get<int64_t>(),
-                        tsc.get<float>(), lb.get<float>(), s);
-        }
         cudaMemsetAsync(cc.p, 0, (size_t)Qb * 4, s);
-        {
+        if (use_tc) {
+            cudaMemsetAsync(th.p, 0, (size_t)Qb * 4, s);
+            ProfScope p(SLOT_GT_FILTER, s);
+            if (launch_gt_filter_tc(xb.p, n, dp, (const uint16_t *)qb.p + q0 * dp, Qb, xn.get<float>(),
+                                    qnb, eps_rel, k, th.get<uint32_t>(), cd.get<int32_t>(),
+                                    cc.get<uint32_t>(), Cg, s))
+                return fail(NRLSH_ECUDA, "tensor map encoding failed");
+        } else {
+            // pilot: certified lower bound of the k-th best score from a strided sample
+            {
+                ProfScope p(SLOT_SCORE, s);
+                launch_score(X, d, Qb_ptr, Qb, nullptr, ns, ns, nullptr, S, xn.get<float>(), qnb,
+                             eps_rel, ss.get<float>(), s);
+            }
+            {
+                ProfScope p(SLOT_TOPK, s);
+                launch_topk(ss.get<float>(), nullptr, Qb, ns, ns, nullptr, S, k, tid.get<int64_t>(),
+                            tsc.get<float>(), lb.get<float>(), s);
+            }
             ProfScope p(SLOT_GT_FILTER, s);
             launch_gt_filter(X, n, d, Qb_ptr, Qb, xn.get<float>(), qnb, lb.get<float>(), eps_rel,
                              cd.get<int32_t>(), cc.get<uint32_t>(), Cg, s);
@@ -640,7 +666,10 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
         cudaMemcpyAsync(hcnt.data(), cc.p, (size_t)Qb * 4, cudaMemcpyDeviceToHost, s);
         if ((e = cudaStreamSynchronize(s))) return cuda_fail(e, "exact_topk");
         for (int qi = 0; qi < Qb; ++qi) {
+            g_last_gt_max_cand = std::max<int64_t>(g_last_gt_max_cand, hcnt[qi]);
+            g_last_gt_sum_cand += hcnt[qi];
             if (hcnt[qi] <= (uint32_t)Cg) continue;
+            ++g_last_gt_overflow;
             if (!full.p && full.alloc((size_t)n * 4, s)) return fail(NRLSH_ENOMEM, "exact_topk scratch");
             launch_score(X, d, Qb_ptr + (int64_t)qi * d, 1, nullptr, n, n, nullptr, 1, nullptr,
                          nullptr, 0.f, full.get<float>(), s);
@@ -654,6 +683,13 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
     e = cudaGetLastError();
     if (e) return cuda_fail(e, "exact_topk launch");
     prof_collect();
+    return NRLSH_OK;
+}
+
+nrlsh_status nrlsh_last_exact_stats(int64_t *max_cand, int64_t *sum_cand, int64_t *overflow) {
+    if (max_cand) *max_cand = g_last_gt_max_cand;
+    if (sum_cand) *sum_cand = g_last_gt_sum_cand;
+    if (overflow) *overflow = g_last_gt_overflow;
     return NRLSH_OK;
 }
 

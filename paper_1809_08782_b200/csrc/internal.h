@@ -50,7 +50,8 @@ namespace nrlsh {
 // ---------------------------------------------------------------- tracing
 enum ProfSlot { SLOT_NORMS = 0, SLOT_PARTITION, SLOT_SCATTER, SLOT_CODES, SLOT_QCODES,
                 SLOT_PILOT, SLOT_SCAN, SLOT_FALLBACK, SLOT_SELECT, SLOT_SCORE, SLOT_TOPK,
-                SLOT_GT_NORMS, SLOT_GT_FILTER, SLOT_OTHER, kNumSlots };
+                SLOT_GT_NORMS, SLOT_GT_FILTER, SLOT_RERANK, SLOT_RERANK_TOPK, SLOT_OTHER,
+                kNumSlots };
 void note_launch(int k = 1);
 long long launch_count();
 void prof_collect();
@@ -125,5 +126,13 @@ void launch_gt_filter(const float *X, int64_t n, int d, const float *Q, int Qb,
                       const float *xnorm, const float *qnorm, const float *lb, float eps_rel,
                       int32_t *cand, uint32_t *cnt, int64_t C, cudaStream_t s);
 int scan_chunk_items();
+// tensor-core ground truth (tc_kernels.cu)
+void launch_bf16_prep(const float *X, int64_t n, int d, int dp, void *Xb, float *xnorm,
+                      cudaStream_t s);
+bool gt_tc_supported(int d, int k);
+int launch_gt_filter_tc(const void *Xb, int64_t n, int dp, const void *Qb16, int Qb,
+                        const float *xnorm, const float *qnorm, float eps_rel, int k,
+                        uint32_t *theta_glob, int32_t *cand, uint32_t *cnt, int64_t C,
+                        cudaStream_t s);
 
 }  // namespace nrlsh

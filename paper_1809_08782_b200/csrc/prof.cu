@@ -13,7 +13,7 @@ namespace nrlsh {
 
 static const char *kSlotNames[kNumSlots] = {
     "norms", "partition", "scatter", "codes", "qcodes", "pilot", "scan", "fallback",
-    "select", "score", "topk", "gt_norms", "gt_filter", "other"};
+    "select", "gt_score", "gt_topk", "gt_norms", "gt_filter", "rerank", "rerank_topk", "other"};
 
 static std::atomic<long long> g_launches{0};
 static std::atomic<int> g_prof_on{0};
