@@ -137,8 +137,10 @@ void free_index(nrlsh_index *ix) {
     void *ps[] = {ix->X_owned, ix->norm2, ix->perm, ix->pos_of_id, ix->part_of_id,
                   ix->part_of_pos, ix->offsets_d, ix->V_d, ix->codes, ix->A, ix->Apad,
                   ix->R_d, ix->chunks_d, ix->order_d};
+    // pool-backed (cudaMallocAsync at build); the index may have been used on any stream
+    cudaDeviceSynchronize();
     for (void *p : ps)
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, nullptr);
     delete ix;
 }
 
@@ -247,7 +249,7 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
 
 #define NR_ALLOC(ptr, bytes)                                                      \
     do {                                                                          \
-        cudaError_t e_ = cudaMalloc((void **)&(ptr), (bytes) ? (bytes) : 16);    \
+        cudaError_t e_ = cudaMallocAsync((void **)&(ptr), (bytes) ? (bytes) : 16, s); \
         if (e_ != cudaSuccess) { cudaGetLastError(); return fail(NRLSH_ENOMEM, "cudaMalloc " #ptr); } \
     } while (0)
 

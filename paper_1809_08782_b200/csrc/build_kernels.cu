@@ -333,13 +333,16 @@ __global__ void __launch_bounds__(1024) sel_resolve_small(
 }
 
 namespace {
+// stream-ordered scratch (memory pool): no device-wide synchronisation on free
 struct DevBuf {
     void *p = nullptr;
-    ~DevBuf() { if (p) cudaFree(p); }
+    cudaStream_t s = nullptr;
+    explicit DevBuf(cudaStream_t st = nullptr) : s(st) {}
+    ~DevBuf() { if (p) cudaFreeAsync(p, s); }
     template <class T> T *get() { return (T *)p; }
     cudaError_t alloc(size_t bytes) {
-        if (p) { cudaFree(p); p = nullptr; }
-        return cudaMalloc(&p, bytes ? bytes : 16);
+        if (p) { cudaFreeAsync(p, s); p = nullptr; }
+        return cudaMallocAsync(&p, bytes ? bytes : 16, s);
     }
 };
 }  // namespace
@@ -353,7 +356,7 @@ int partition_percentile(const double *norm2, int64_t n, int m, uint8_t *part, c
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     const int64_t maxbins = 1ll << 24;
-    DevBuf H, P, TS, G, META, FILL;
+    DevBuf H(s), P(s), TS(s), G(s), META(s), FILL(s);
     if (H.alloc(maxbins * 4) || P.alloc(maxbins * 4) || TS.alloc(4096 * 4) ||
         G.alloc(sizeof(SelGroup) * kMaxGroups) || META.alloc(16) || FILL.alloc(kMaxGroups * 4)) {
         *err = "partition: cudaMalloc failed";
@@ -392,6 +395,7 @@ int partition_percentile(const double *norm2, int64_t n, int m, uint8_t *part, c
                                            pb.count, n, m, G.get<SelGroup>(), META.get<int64_t>());
         int64_t meta[2];
         cudaMemcpyAsync(meta, META.p, 16, cudaMemcpyDeviceToHost, s);
+        cudaMemcpyAsync(hg.data(), G.p, sizeof(SelGroup) * kMaxGroups, cudaMemcpyDeviceToHost, s);
         cudaError_t e = cudaStreamSynchronize(s);
         if (e != cudaSuccess) {
             *err = std::string("partition: ") + cudaGetErrorString(e);
@@ -399,8 +403,8 @@ int partition_percentile(const double *norm2, int64_t n, int m, uint8_t *part, c
         }
         const int ng = (int)meta[0];
         const int64_t tot = meta[1];
-        auto kb = std::make_shared<DevBuf>();
-        auto ib = std::make_shared<DevBuf>();
+        auto kb = std::make_shared<DevBuf>(s);
+        auto ib = std::make_shared<DevBuf>(s);
         if (kb->alloc(tot * 8) || ib->alloc(tot * 4)) {
             *err = "partition: cudaMalloc failed (candidates)";
             return NRLSH_ENOMEM;
@@ -417,12 +421,6 @@ int partition_percentile(const double *norm2, int64_t n, int m, uint8_t *part, c
                 n, m, G.get<SelGroup>(), META.get<int64_t>(), FILL.get<uint32_t>(),
                 kb->get<uint64_t>(), ib->get<uint32_t>(), part);
         if (ng == 0) continue;
-        cudaMemcpyAsync(hg.data(), G.p, sizeof(SelGroup) * ng, cudaMemcpyDeviceToHost, s);
-        e = cudaStreamSynchronize(s);
-        if (e != cudaSuccess) {
-            *err = std::string("partition: ") + cudaGetErrorString(e);
-            return NRLSH_ECUDA;
-        }
         std::vector<int> small;
         for (int g = 0; g < ng; ++g) {
             if (hg[g].count <= (uint32_t)kSmallGroup) {
@@ -440,25 +438,21 @@ int partition_percentile(const double *norm2, int64_t n, int m, uint8_t *part, c
             }
         }
         if (!small.empty()) {
-            DevBuf gi;
-            if (gi.alloc(small.size() * 4)) {
-                *err = "partition: cudaMalloc failed";
+            // per-launch argument block: this level's group table + the small-group list
+            DevBuf gi(s);
+            const size_t gbytes = sizeof(SelGroup) * ng;
+            if (gi.alloc(gbytes + small.size() * 4)) {
+                *err = "partition: cudaMallocAsync failed";
                 return NRLSH_ENOMEM;
             }
-            // groups table is reused by the next level: copy this level's groups aside
-            DevBuf gcopy;
-            gcopy.alloc(sizeof(SelGroup) * ng);
-            cudaMemcpyAsync(gcopy.p, G.p, sizeof(SelGroup) * ng, cudaMemcpyDeviceToDevice, s);
-            cudaMemcpyAsync(gi.p, small.data(), small.size() * 4, cudaMemcpyHostToDevice, s);
+            cudaMemcpyAsync(gi.p, G.p, gbytes, cudaMemcpyDeviceToDevice, s);
+            cudaMemcpyAsync((uint8_t *)gi.p + gbytes, small.data(), small.size() * 4,
+                            cudaMemcpyHostToDevice, s);
             note_launch();
             sel_resolve_small<<<(int)small.size(), 1024, 0, s>>>(
-                gcopy.get<SelGroup>(), gi.get<int>(), kb->get<uint64_t>(), ib->get<uint32_t>(), n,
-                m, part);
-            e = cudaStreamSynchronize(s);   // gi/gcopy are freed on scope exit
-            if (e != cudaSuccess) {
-                *err = std::string("partition: ") + cudaGetErrorString(e);
-                return NRLSH_ECUDA;
-            }
+                gi.get<SelGroup>(), (const int *)((uint8_t *)gi.p + gbytes), kb->get<uint64_t>(),
+                ib->get<uint32_t>(), n, m, part);
+            // (pageable H2D copies are staged before cudaMemcpyAsync returns)
         }
     }
     return 0;
@@ -509,7 +503,7 @@ __global__ void uniform_assign(const double *__restrict__ norm2, int64_t n, int 
 
 int partition_uniform(const double *norm2, int64_t n, int m, uint8_t *part, cudaStream_t s,
                       std::string *err) {
-    DevBuf mm;
+    DevBuf mm(s);
     if (mm.alloc(16)) {
         *err = "partition: cudaMalloc failed";
         return NRLSH_ENOMEM;
@@ -625,7 +619,7 @@ int partition_scatter(const double *norm2, const uint8_t *part, int64_t n, int m
                       int32_t *pos_of_id, uint8_t *part_of_pos, int64_t *offsets_d, double *V_d,
                       cudaStream_t s, std::string *err) {
     const int ntiles = (int)((n + kScatTile - 1) / kScatTile);
-    DevBuf tc, vm;
+    DevBuf tc(s), vm(s);
     if (tc.alloc((size_t)ntiles * m * 4) || vm.alloc((size_t)m * 8)) {
         *err = "partition: cudaMalloc failed";
         return NRLSH_ENOMEM;
@@ -638,11 +632,6 @@ int partition_scatter(const double *norm2, const uint8_t *part, int64_t n, int m
     scat_write<<<ntiles, 256, 0, s>>>(part, n, m, tc.get<uint32_t>(), perm, pos_of_id,
                                       part_of_pos);
     note_launch(3);
-    cudaError_t e = cudaStreamSynchronize(s);
-    if (e != cudaSuccess) {
-        *err = std::string("partition scatter: ") + cudaGetErrorString(e);
-        return NRLSH_ECUDA;
-    }
     return 0;
 }
 
