@@ -463,11 +463,11 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
         if ((e = oc.init(cand_out, (size_t)nq * Tq * 4, s))) return cuda_fail(e, "cand_ids");
         if (rank_out && (e = orr.init(rank_out, (size_t)nq * Tq * 2, s))) return cuda_fail(e, "cand_rank");
     }
-    DBuf qc, dl, cn, bf, cd, sc, fl;
+    DBuf qc, dl, cn, bf, cd, pt, fl;
     if (qc.alloc((size_t)Qmax * ix->W * 4, s) || dl.alloc((size_t)Qmax * ix->m, s) ||
         cn.alloc((size_t)Qmax * 4, s) || bf.alloc((size_t)Qmax * C * 8, s) ||
-        cd.alloc((size_t)Qmax * Tq * 4, s) || sc.alloc((size_t)Qmax * Tq * 4, s) ||
-        fl.alloc(32, s))
+        cd.alloc((size_t)Qmax * Tq * 4, s) ||
+        pt.alloc(want_topk ? rerank_partial_bytes(Qmax, Tq, k) : 0, s) || fl.alloc(32, s))
         return fail(NRLSH_ENOMEM, "query workspace");
     const int init_flags[8] = {INT_MAX, INT_MAX, 0, 0, 0, 0, 0, 0};
     cudaMemcpyAsync(fl.p, init_flags, 32, cudaMemcpyHostToDevice, s);
@@ -482,14 +482,10 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
                        stride, C, qc.get<uint32_t>(), dl.get<int8_t>(), cn.get<uint32_t>(),
                        bf.get<unsigned long long>(), cand, crank, fl.get<int>(), pairs, s);
         if (want_topk) {
-            {
-                ProfScope p(SLOT_RERANK, s);
-                launch_score(ix->X, ix->d, Qd, Qb, cand, Tq, Tq, nullptr, 1, nullptr, nullptr,
-                             0.f, sc.get<float>(), s);
-            }
-            ProfScope p(SLOT_RERANK_TOPK, s);
-            launch_topk(sc.get<float>(), cand, Qb, Tq, Tq, nullptr, 1, k,
-                        (int64_t *)oi.dev + q0 * k, (float *)os.dev + q0 * k, nullptr, s);
+            ProfScope p(SLOT_RERANK, s);
+            launch_rerank(ix->X, ix->d, Qd, Qb, cand, Tq, Tq, nullptr, 1, k,
+                          pt.get<unsigned long long>(), (int64_t *)oi.dev + q0 * k,
+                          (float *)os.dev + q0 * k, s);
         }
     }
     if (want_topk) {
@@ -602,13 +598,14 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
                               : std::min<int64_t>(n, std::max<int64_t>(4 * (int64_t)S * k + 4096, 2 * k));
     int Qmax = (int)std::min<int64_t>(1024, nq);
     while (Qmax > 64 && (int64_t)Qmax * (ns * 4 + Cg * 8) > ((int64_t)2500 << 20)) Qmax >>= 1;
-    DBuf xn, qn, ss, lb, tid, tsc, cc, cd, cs, xb, qb, th;
+    DBuf xn, qn, ss, lb, tid, tsc, cc, cd, cs, xb, qb, th, pt;
     const int64_t npad = (n + 255) / 256 * 256;   // |x| padded: the tc kernel bulk-loads 1 KB tiles
     if (xn.alloc((size_t)npad * 4, s) || qn.alloc((size_t)nq * 4, s) ||
         ss.alloc((size_t)Qmax * ns * 4, s) || lb.alloc((size_t)Qmax * 4, s) ||
         tid.alloc((size_t)Qmax * k * 8, s) || tsc.alloc((size_t)Qmax * k * 4, s) ||
         cc.alloc((size_t)Qmax * 4, s) || cd.alloc((size_t)Qmax * Cg * 4, s) ||
-        cs.alloc((size_t)Qmax * Cg * 4, s) || th.alloc((size_t)Qmax * 4, s))
+        cs.alloc((size_t)Qmax * Cg * 4, s) || th.alloc((size_t)Qmax * 4, s) ||
+        pt.alloc(std::max(rerank_partial_bytes(Qmax, Cg, k), rerank_partial_bytes(1, n, k)), s))
         return fail(NRLSH_ENOMEM, "exact_topk workspace");
     if (use_tc) {
         if (xb.alloc((size_t)n * dp * 2, s) || qb.alloc((size_t)nq * dp * 2, s))
@@ -623,7 +620,6 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
         launch_vec_norms(Q, nq, d, qn.get<float>(), s);
     }
     std::vector<uint32_t> hcnt(Qmax);
-    DBuf full;
     for (int64_t q0 = 0; q0 < nq; q0 += Qmax) {
         const int Qb = (int)std::min<int64_t>(Qmax, nq - q0);
         const float *Qb_ptr = Q + q0 * d;
@@ -656,13 +652,8 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
         }
         {
             ProfScope p(SLOT_SCORE, s);
-            launch_score(X, d, Qb_ptr, Qb, cd.get<int32_t>(), Cg, Cg, cc.get<uint32_t>(), 1,
-                         nullptr, nullptr, 0.f, cs.get<float>(), s);
-        }
-        {
-            ProfScope p(SLOT_TOPK, s);
-            launch_topk(cs.get<float>(), cd.get<int32_t>(), Qb, Cg, Cg, cc.get<uint32_t>(), 1, k,
-                        oid, osc, nullptr, s);
+            launch_rerank(X, d, Qb_ptr, Qb, cd.get<int32_t>(), Cg, Cg, cc.get<uint32_t>(), 1, k,
+                          pt.get<unsigned long long>(), oid, osc, s);
         }
         // overflowing queries (rare): exact scoring of every item
         cudaMemcpyAsync(hcnt.data(), cc.p, (size_t)Qb * 4, cudaMemcpyDeviceToHost, s);
@@ -672,11 +663,9 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
             g_last_gt_sum_cand += hcnt[qi];
             if (hcnt[qi] <= (uint32_t)Cg) continue;
             ++g_last_gt_overflow;
-            if (!full.p && full.alloc((size_t)n * 4, s)) return fail(NRLSH_ENOMEM, "exact_topk scratch");
-            launch_score(X, d, Qb_ptr + (int64_t)qi * d, 1, nullptr, n, n, nullptr, 1, nullptr,
-                         nullptr, 0.f, full.get<float>(), s);
-            launch_topk(full.get<float>(), nullptr, 1, n, n, nullptr, 1, k, oid + (int64_t)qi * k,
-                        osc + (int64_t)qi * k, nullptr, s);
+            launch_rerank(X, d, Qb_ptr + (int64_t)qi * d, 1, nullptr, n, n, nullptr, 1, k,
+                          pt.get<unsigned long long>(), oid + (int64_t)qi * k,
+                          osc + (int64_t)qi * k, s);
         }
     }
     if ((e = oi.finish(s)) || (e = os.finish(s))) return cuda_fail(e, "copy results");

@@ -120,6 +120,14 @@ void launch_topk(const float *scores, const int32_t *cand, int Qb, int64_t ncand
                  int64_t cand_ld, const uint32_t *ncand_per_q, int stride, int k,
                  int64_t *out_ids, float *out_scores, float *kth_out, cudaStream_t s);
 
+// fused exact re-rank + top-k (score desc, id asc) over cand[q][0..ncand_q); cand ==
+// nullptr means cand[q][t] = t * stride.  `partial` needs rerank_partial_bytes().
+size_t rerank_partial_bytes(int Qb, int64_t ncand, int k);
+void launch_rerank(const float *X, int d, const float *Q, int Qb, const int32_t *cand,
+                   int64_t ncand, int64_t cand_ld, const uint32_t *ncand_per_q, int stride,
+                   int k, unsigned long long *partial, int64_t *out_ids, float *out_scores,
+                   cudaStream_t s);
+
 // ---------------------------------------------------------------- ground truth
 void launch_vec_norms(const float *X, int64_t n, int d, float *xnorm, cudaStream_t s);
 void launch_gt_filter(const float *X, int64_t n, int d, const float *Q, int Qb,

@@ -599,4 +599,252 @@ void launch_topk(const float *scores, const int32_t *cand, int Qb, int64_t ncand
     note_launch();
 }
 
+// =========================================================================== K8 fused re-rank
+// Exact re-rank (Alg. 2 l.6) fused with the top-k of (score desc, id asc).
+// CTA = (query q, slice of its candidate list).  A warp scores 4 candidate rows at a
+// time, 8 lanes per row, VEC-wide loads: every lane keeps ceil(d / 8VEC) independent
+// loads in flight (the gather is latency-bound otherwise), and the 32 candidate ids a
+// warp needs per round come from one coalesced load.  Scores never go to HBM: keys
+// (~order(score) << 32 | id) better than the CTA's running k-th best enter a shared
+// buffer that is bitonic-sorted and truncated to k when it fills.
+constexpr int kRrThreads = 256;
+constexpr int kRrRound = kRrThreads;          // candidate rows per CTA round
+constexpr int kRrLPR = 8;                     // lanes per row
+constexpr int kRrMaxIt = 8;                   // loads per lane kept in flight
+
+__device__ __forceinline__ void bitonic_sort_smem(unsigned long long *a, int np2) {
+    for (int size = 2; size <= np2; size <<= 1) {
+        for (int st = size >> 1; st > 0; st >>= 1) {
+            for (int t = threadIdx.x; t < np2; t += blockDim.x) {
+                const int o = t ^ st;
+                if (o > t) {
+                    const bool up = (t & size) == 0;
+                    const unsigned long long x = a[t], y = a[o];
+                    if ((x > y) == up) { a[t] = y; a[o] = x; }
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+template <int VEC>
+__device__ __forceinline__ void vload(const float *p, float (&v)[VEC]) {
+    if (VEC == 4) {
+        const float4 t = __ldg(reinterpret_cast<const float4 *>(p));
+        v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+    } else if (VEC == 2) {
+        const float2 t = __ldg(reinterpret_cast<const float2 *>(p));
+        v[0] = t.x; v[1] = t.y;
+    } else {
+        v[0] = __ldg(p);
+    }
+}
+
+// one lane's share of q.x for one row: xl = row + sub*VEC, ql = sq + sub*VEC,
+// rem = d - sub*VEC.  NIT = ceil(d / (8 VEC)) loads, all issued before any use;
+// only the last one can leave the row (its address is clamped, its value zeroed).
+template <int VEC, int NIT>
+__device__ __forceinline__ float row_dot(const float *__restrict__ xl, const float *ql, int rem) {
+    float xv[NIT][VEC];
+#pragma unroll
+    for (int i = 0; i < NIT; ++i) {
+        const int off = i * kRrLPR * VEC;
+        vload<VEC>(xl + (i < NIT - 1 ? off : max(0, min(off, rem - VEC))), xv[i]);
+    }
+    float acc = 0.f;
+#pragma unroll
+    for (int i = 0; i < NIT; ++i) {
+        const int off = i * kRrLPR * VEC;
+        const bool ok = (i < NIT - 1) || off < rem;
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) acc = fmaf(ql[ok ? off + v : v], ok ? xv[i][v] : 0.f, acc);
+    }
+    return acc;
+}
+
+// any d: blocks of kRrMaxIt loads with clamped addresses
+template <int VEC>
+__device__ __forceinline__ float row_dot_any(const float *__restrict__ xl, const float *ql, int rem) {
+    float acc = 0.f;
+    for (int o0 = 0; o0 < rem; o0 += kRrMaxIt * kRrLPR * VEC) {
+        float xv[kRrMaxIt][VEC];
+#pragma unroll
+        for (int u = 0; u < kRrMaxIt; ++u)
+            vload<VEC>(xl + max(0, min(o0 + u * kRrLPR * VEC, rem - VEC)), xv[u]);
+#pragma unroll
+        for (int u = 0; u < kRrMaxIt; ++u) {
+            const int off = o0 + u * kRrLPR * VEC;
+            const bool ok = off < rem;
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) acc = fmaf(ql[ok ? off + v : v], ok ? xv[u][v] : 0.f, acc);
+        }
+    }
+    return acc;
+}
+
+template <int VEC, int NIT>
+__global__ void __launch_bounds__(kRrThreads) k8_rerank(
+    const float *__restrict__ X, int d, const float *__restrict__ Q,
+    const int32_t *__restrict__ cand, int64_t cand_ld, int64_t ncand,
+    const uint32_t *__restrict__ ncand_per_q, int stride, int k, int cap, int64_t slice,
+    unsigned long long *__restrict__ partial, int64_t *__restrict__ out_ids,
+    float *__restrict__ out_scores) {
+    extern __shared__ __align__(16) unsigned long long rr_smem[];
+    unsigned long long *buf = rr_smem;                       // [cap]
+    float *sq = reinterpret_cast<float *>(buf + cap);        // [dpad]
+    __shared__ unsigned int s_cnt;
+    __shared__ unsigned long long s_thr;
+    const int q = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int sub = lane & (kRrLPR - 1), grp = lane >> 3;
+    const int dpad = (d + 8 * VEC - 1) / (8 * VEC) * (8 * VEC);
+    for (int e = threadIdx.x; e < dpad; e += blockDim.x) sq[e] = e < d ? Q[(int64_t)q * d + e] : 0.f;
+    if (threadIdx.x == 0) { s_cnt = 0; s_thr = ~0ull; }
+    int64_t nc = ncand;
+    if (ncand_per_q) nc = min((int64_t)ncand_per_q[q], cand_ld);
+    const int64_t t0 = (int64_t)blockIdx.y * slice;
+    const int64_t t1 = min(nc, t0 + slice);
+    const int32_t *cl = cand ? cand + (int64_t)q * cand_ld : nullptr;
+    const float *ql = sq + sub * VEC;
+    const int rem = d - sub * VEC;
+    __syncthreads();
+    for (int64_t base = t0; base < t1; base += kRrRound) {
+        // ids of this warp's 32 rows (one coalesced load)
+        const int64_t tw = base + warp * 32 + lane;
+        int myid = -1;
+        if (tw < t1) myid = cl ? cl[tw] : (int)(tw * stride);
+#pragma unroll 1
+        for (int st = 0; st < 8; ++st) {
+            const int id = __shfl_sync(NR_FULL, myid, st * 4 + grp);
+            float acc = 0.f;
+            if (id >= 0) {
+                const float *xl = X + (int64_t)id * d + sub * VEC;
+                acc = NIT > 0 ? row_dot<VEC, (NIT > 0 ? NIT : 1)>(xl, ql, rem)
+                              : row_dot_any<VEC>(xl, ql, rem);
+            }
+            acc += __shfl_xor_sync(NR_FULL, acc, 1);
+            acc += __shfl_xor_sync(NR_FULL, acc, 2);
+            acc += __shfl_xor_sync(NR_FULL, acc, 4);
+            if (sub == 0 && id >= 0) {
+                const unsigned long long key = topk_key(acc, (uint32_t)id);
+                if (key < *((volatile unsigned long long *)&s_thr)) {
+                    const unsigned slot = atomicAdd(&s_cnt, 1u);
+                    buf[slot] = key;
+                }
+            }
+        }
+        __syncthreads();
+        if (s_cnt > (unsigned)(cap - kRrRound)) {   // compact: keep the k best
+            const int c = (int)s_cnt;
+            for (int e = c + threadIdx.x; e < cap; e += blockDim.x) buf[e] = ~0ull;
+            __syncthreads();
+            bitonic_sort_smem(buf, cap);
+            if (threadIdx.x == 0) {
+                s_cnt = (unsigned)min(c, k);
+                if (c >= k) s_thr = buf[k - 1];
+            }
+            __syncthreads();
+        }
+    }
+    __syncthreads();
+    const int c = (int)s_cnt;
+    for (int e = c + threadIdx.x; e < cap; e += blockDim.x) buf[e] = ~0ull;
+    __syncthreads();
+    bitonic_sort_smem(buf, cap);
+    if (partial) {
+        unsigned long long *pp = partial + ((int64_t)q * gridDim.y + blockIdx.y) * k;
+        for (int t = threadIdx.x; t < k; t += blockDim.x) pp[t] = t < c ? buf[t] : ~0ull;
+    } else {
+        for (int t = threadIdx.x; t < k; t += blockDim.x) {
+            const unsigned long long v = t < c ? buf[t] : ~0ull;
+            out_ids[(int64_t)q * k + t] = v == ~0ull ? -1 : (int64_t)(uint32_t)v;
+            out_scores[(int64_t)q * k + t] = v == ~0ull ? -INFINITY : float_unorder(~(uint32_t)(v >> 32));
+        }
+    }
+}
+
+// merge the gy partial top-k lists of each query
+__global__ void __launch_bounds__(256) k8_rerank_merge(const unsigned long long *__restrict__ partial,
+                                                       int gy, int k, int np2,
+                                                       int64_t *__restrict__ out_ids,
+                                                       float *__restrict__ out_scores) {
+    extern __shared__ unsigned long long mk[];
+    const int q = blockIdx.x;
+    const int tot = gy * k;
+    for (int e = threadIdx.x; e < np2; e += blockDim.x)
+        mk[e] = e < tot ? partial[(int64_t)q * tot + e] : ~0ull;
+    __syncthreads();
+    bitonic_sort_smem(mk, np2);
+    for (int t = threadIdx.x; t < k; t += blockDim.x) {
+        const unsigned long long v = mk[t];
+        out_ids[(int64_t)q * k + t] = v == ~0ull ? -1 : (int64_t)(uint32_t)v;
+        out_scores[(int64_t)q * k + t] = v == ~0ull ? -INFINITY : float_unorder(~(uint32_t)(v >> 32));
+    }
+}
+
+static int pow2_at_least(int64_t v) {
+    int p = 1;
+    while (p < v) p <<= 1;
+    return p;
+}
+
+size_t rerank_partial_bytes(int Qb, int64_t ncand, int k) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int64_t rounds = std::max<int64_t>(1, (ncand + kRrRound - 1) / kRrRound);
+    int gy = (int)std::min<int64_t>(rounds, std::max(1, (sms * 8) / std::max(1, Qb)));
+    gy = std::min(gy, std::max(1, 8192 / k));
+    return gy > 1 ? (size_t)Qb * gy * k * 8 : 0;
+}
+
+void launch_rerank(const float *X, int d, const float *Q, int Qb, const int32_t *cand,
+                   int64_t ncand, int64_t cand_ld, const uint32_t *ncand_per_q, int stride,
+                   int k, unsigned long long *partial, int64_t *out_ids, float *out_scores,
+                   cudaStream_t s) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int64_t rounds = std::max<int64_t>(1, (ncand + kRrRound - 1) / kRrRound);
+    int gy = (int)std::min<int64_t>(rounds, std::max(1, (sms * 8) / std::max(1, Qb)));
+    gy = std::min(gy, std::max(1, 8192 / k));
+    if (!partial) gy = 1;
+    const int64_t slice = ((rounds + gy - 1) / gy) * kRrRound;
+    gy = (int)std::max<int64_t>(1, (ncand + slice - 1) / slice);
+    const int cap = pow2_at_least(k + 2 * kRrRound);
+    const int vec = (d % 4 == 0) ? 4 : ((d % 2 == 0) ? 2 : 1);
+    const int dpad = (d + 8 * vec - 1) / (8 * vec) * (8 * vec);
+    const size_t sm = (size_t)cap * 8 + (size_t)dpad * 4;
+    unsigned long long *pp = gy > 1 ? partial : nullptr;
+    dim3 grid(Qb, gy);
+    const int nit = dpad / (8 * vec);
+#define NR_RR(V, N)                                                                            \
+    do {                                                                                       \
+        cudaFuncSetAttribute(k8_rerank<V, N>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+                             (int)sm);                                                         \
+        k8_rerank<V, N><<<grid, kRrThreads, sm, s>>>(X, d, Q, cand, cand_ld, ncand,            \
+                                                     ncand_per_q, stride, k, cap, slice, pp,   \
+                                                     out_ids, out_scores);                     \
+    } while (0)
+#define NR_RR_V(V)                                                                             \
+    switch (nit) {                                                                             \
+        case 1: NR_RR(V, 1); break;   case 2: NR_RR(V, 2); break;                              \
+        case 3: NR_RR(V, 3); break;   case 4: NR_RR(V, 4); break;                              \
+        case 5: NR_RR(V, 5); break;   case 6: NR_RR(V, 6); break;                              \
+        case 7: NR_RR(V, 7); break;   case 8: NR_RR(V, 8); break;                              \
+        case 9: NR_RR(V, 9); break;   case 10: NR_RR(V, 10); break;                            \
+        case 11: NR_RR(V, 11); break; case 12: NR_RR(V, 12); break;                            \
+        default: NR_RR(V, 0); break;                                                           \
+    }
+    if (vec == 4) { NR_RR_V(4) } else if (vec == 2) { NR_RR_V(2) } else { NR_RR_V(1) }
+#undef NR_RR_V
+#undef NR_RR
+    note_launch();
+    if (gy > 1) {
+        const int np2 = pow2_at_least((int64_t)gy * k);
+        cudaFuncSetAttribute(k8_rerank_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, np2 * 8);
+        k8_rerank_merge<<<Qb, 256, (size_t)np2 * 8, s>>>(partial, gy, k, np2, out_ids, out_scores);
+        note_launch();
+    }
+}
+
 }  // namespace nrlsh
