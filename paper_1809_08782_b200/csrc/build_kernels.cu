@@ -9,12 +9,15 @@
 //                  SIMPLE-LSH transform of Eq. (8) scaled by U_j > 0), bit =
 //                  [y >= 0] (Eq. (4)), packed LSB-first, written at the item's
 //                  position in sub-dataset order.
+#include <algorithm>
+#include <cstdlib>
 #include <memory>
 #include <string>
 #include <vector>
 
 #include "common.cuh"
 #include "internal.h"
+#include "tc_sm100.cuh"
 
 namespace nrlsh {
 
@@ -69,11 +72,88 @@ __global__ void k1_norms_direct(const float *__restrict__ X, int64_t n, int d,
     }
 }
 
+// Streaming version: blocks of RT consecutive rows (one contiguous byte range of
+// X) are bulk-copied (cp.async.bulk, 1-D TMA) into a 2-stage smem ring while the
+// previous block is summed.  Thread r owns row r and adds x_r0^2, x_r1^2, ... in
+// order; for even d the row stride makes a warp's lanes hit one bank, so lane r
+// runs r steps behind lane 0 (element k at step k + r): banks (r(d-1) + step) mod
+// 32 are distinct, and the order of the sum is unchanged.
+__global__ void __launch_bounds__(128) k1_norms_bulk(const float *__restrict__ X, int64_t n, int d,
+                                                     int RT, double *__restrict__ norm2,
+                                                     unsigned long long *__restrict__ bad) {
+    extern __shared__ __align__(128) float nbuf[];       // [2][RT * d]
+    __shared__ __align__(8) uint64_t full[2];
+    const int64_t ntiles = (n + RT - 1) / RT;
+    const int skew = (d % 2 == 0) ? 1 : 0;
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        tc::mbar_init(&full[0], 1);
+        tc::mbar_init(&full[1], 1);
+        tc::fence_mbar_init();
+    }
+    __syncthreads();
+    auto issue = [&](int64_t tile, int st) {
+        const int64_t r0 = tile * RT;
+        const int rows = (int)min((int64_t)RT, n - r0);
+        const uint32_t bytes = (uint32_t)rows * d * 4;
+        if ((bytes & 15u) == 0) {
+            tc::mbar_arrive_expect_tx(&full[st], bytes);
+            tc::bulk_load(nbuf + (size_t)st * RT * d, X + r0 * d, bytes, &full[st]);
+        } else {
+            tc::mbar_arrive(&full[st]);   // ragged tail: read straight from global
+        }
+    };
+    int64_t tile = blockIdx.x;
+    if (threadIdx.x == 0) {
+        if (tile < ntiles) issue(tile, 0);
+        if (tile + gridDim.x < ntiles) issue(tile + gridDim.x, 1);
+    }
+    for (uint32_t it = 0; tile < ntiles; ++it, tile += gridDim.x) {
+        const int st = it & 1;
+        tc::mbar_wait(&full[st], (it >> 1) & 1);
+        const int64_t r0 = tile * RT;
+        const int rows = (int)min((int64_t)RT, n - r0);
+        const bool in_smem = (((uint32_t)rows * d * 4) & 15u) == 0;
+        const float *src = in_smem ? nbuf + (size_t)st * RT * d : X + r0 * d;
+        for (int r = threadIdx.x; r < RT; r += blockDim.x) {
+            const float *row = src + (size_t)min(r, rows - 1) * d;
+            const int lag = skew * lane;
+            double s = 0.0;
+            for (int step = 0; step < d + 31 * skew; ++step) {
+                const int k = step - lag;
+                if (k >= 0 && k < d) {
+                    const double v = (double)row[k];
+                    s = __fma_rn(v, v, s);        // v*v is exact: one rounding, as s + v*v
+                }
+            }
+            if (r < rows) {
+                norm2[r0 + r] = s;
+                if (!isfinite(s)) atomicMin(bad, (unsigned long long)(r0 + r));
+            }
+        }
+        __syncthreads();                            // stage st fully read
+        if (threadIdx.x == 0 && tile + 2 * (int64_t)gridDim.x < ntiles)
+            issue(tile + 2 * (int64_t)gridDim.x, st);
+    }
+}
+
 void launch_norms(const float *X, int64_t n, int d, double *norm2, unsigned long long *bad,
                   cudaStream_t s) {
     const int ld = (d % 2 == 1) ? d : d + 1;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    int RT = 64;   // two stages of <= 100 KB: >= 2 CTAs (>= 128 summing threads) per SM
+    while (RT > 32 && (size_t)2 * RT * d * 4 > 100 * 1024) RT >>= 1;
+    if (((uintptr_t)X & 15u) == 0 && (size_t)2 * RT * d * 4 <= 200 * 1024 && !getenv("NRLSH_NORMS_OLD")) {
+        const size_t sm = (size_t)2 * RT * d * 4;
+        cudaFuncSetAttribute(k1_norms_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        const int64_t ntiles = (n + RT - 1) / RT;
+        const int per_sm = std::max(1, (int)((227 * 1024) / (sm + 1024)));
+        const int grid = (int)std::min<int64_t>(ntiles, (int64_t)sms * per_sm);
+        k1_norms_bulk<<<grid, RT, sm, s>>>(X, n, d, RT, norm2, bad);
+        note_launch();
+        return;
+    }
     const size_t lim = 200 * 1024;
     if ((size_t)256 * ld * 4 <= lim / 2) {
         size_t sm = (size_t)256 * ld * 4;
@@ -726,6 +806,10 @@ __global__ void __launch_bounds__(256) k3_codes_simt(
 void launch_item_codes(const float *X, int64_t n, int d, const double *norm2,
                        const uint8_t *part, const double *V, const float *Apad, int L, int W,
                        const int32_t *pos_of_id, uint32_t *codes, cudaStream_t s) {
+    if (codes_tc_supported(d, W)) {
+        launch_item_codes_tc(X, n, d, norm2, part, V, Apad, L, W, pos_of_id, codes, s);
+        return;
+    }
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     const int grid = grid_for(n, 64, sms * 8);

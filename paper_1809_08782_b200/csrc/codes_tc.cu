@@ -1,0 +1,320 @@
+// codes_tc.cu — K3 on the 5th-generation tensor cores (sm_100a): the SRP
+// projection of the SIMPLE-LSH-transformed items, fused with sign and bit-pack.
+//
+//   y_ib = sum_k x_ik A_kb + A_db t_i,   t_i = sqrt(max(0, V_j - ||x_i||^2))
+//   bit b of item i = [y_ib >= 0]
+//
+// y = U_j * (A_b . P(x_i)) with P(x) = [x/U_j; sqrt(1 - ||x/U_j||^2)] (Eq. (8),
+// PAPER:85-87, applied after Alg. 1 l.6), and U_j > 0 does not change the sign of
+// Eq. (4); V_j = 0 (a sub-dataset of zero vectors) gives P(x) = [0;1],
+// i.e. t = 1.  Codes are written at the item's position in sub-dataset order.
+//
+// Precision: A is TF32-exact by construction (include/nrlsh.h), so two kind::tf32
+// MMAs on X = X_big + X_small (X_big = the top 11 significant bits of x, written
+// explicitly; X_small = x - X_big, exact in fp32) give fp32-grade products
+// (|x - X_big - tf32(X_small)| < 2^-20 |x|), far inside the 1e-5 parity band.
+//
+// CTA (persistent, one per SM): tile = 128 items (TMEM lanes) x N = 32W columns.
+//   warps 0-7  convert: coalesced loads of X (next K-block prefetched in
+//              registers), split, store both halves into 128B-swizzled K-major
+//              smem K-blocks (32 tf32 wide), ring of CT_STAGES stages
+//   warp  8    TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 9-12 epilogue: tcgen05.ld the accumulator row, add A_d t_i, sign, pack,
+//              scatter the W code words to pos_of_id[i]
+// The projection matrix (B operand, N x K) stays resident in smem.
+#include <cuda.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "internal.h"
+#include "tc_sm100.cuh"
+
+namespace nrlsh {
+
+constexpr int CT_M = 128;
+constexpr int CT_KB = 32;                 // tf32 elements per K-block (128-byte rows)
+constexpr int CT_A_BLK = CT_M * 128;      // 16 KB per operand per K-block
+constexpr int CT_STAGE = 2 * CT_A_BLK;    // big + small
+constexpr int CT_CONV = 256;              // converter threads (warps 0-7)
+constexpr int CT_THREADS = 13 * 32;
+
+struct CodesArgs {
+    const float *X;
+    int64_t n;
+    int d, KB, L, N, stages;
+    int64_t ntiles;
+    const double *norm2;
+    const uint8_t *part;
+    const double *V;
+    const float *Apad;       // [(d+1) x N]
+    const int32_t *pos_of_id;
+    uint32_t *codes;         // [n x N/32], partition order
+};
+
+__device__ __forceinline__ uint32_t swz(int row, int kbyte) {
+    return (uint32_t)(row * 128 + ((((kbyte >> 4) ^ (row & 7))) << 4) + (kbyte & 15));
+}
+
+template <int VEC>
+__device__ __forceinline__ void conv_load(const CodesArgs &a, int64_t tile, int kb, int w, int l,
+                                          float (&v)[16]) {
+    constexpr int lpr = VEC == 4 ? 8 : (VEC == 2 ? 16 : 32);   // lanes per 128-byte row
+    constexpr int rpi = 32 / lpr;                               // rows per instruction
+    constexpr int ni = 16 / rpi;                                // instructions per K-block
+    const int col = kb * CT_KB + (l % lpr) * VEC;
+    const int cc = min(col, a.d - VEC);
+#pragma unroll
+    for (int j = 0; j < ni; ++j) {
+        const int rr = 16 * w + j * rpi + l / lpr;
+        const int64_t i = tile * CT_M + rr;
+        const int64_t ic = i < a.n ? i : a.n - 1;
+        const float *p = a.X + ic * a.d + cc;
+        float t[VEC];
+        if (VEC == 4) {
+            const float4 q = __ldg(reinterpret_cast<const float4 *>(p));
+            t[0] = q.x; t[1] = q.y; t[2] = q.z; t[3] = q.w;
+        } else if (VEC == 2) {
+            const float2 q = __ldg(reinterpret_cast<const float2 *>(p));
+            t[0] = q.x; t[1] = q.y;
+        } else {
+            t[0] = __ldg(p);
+        }
+        const bool ok = (i < a.n) && (col < a.d);
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) v[j * VEC + e] = ok ? t[e] : 0.f;
+    }
+}
+
+template <int VEC>
+__device__ __forceinline__ void conv_store(uint8_t *stage, int w, int l, const float (&v)[16]) {
+    constexpr int lpr = VEC == 4 ? 8 : (VEC == 2 ? 16 : 32);
+    constexpr int rpi = 32 / lpr;
+    constexpr int ni = 16 / rpi;
+    const int kbyte = (l % lpr) * VEC * 4;
+#pragma unroll
+    for (int j = 0; j < ni; ++j) {
+        const int rr = 16 * w + j * rpi + l / lpr;
+        const uint32_t off = swz(rr, kbyte);
+        uint32_t bg[VEC], sm[VEC];
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) {
+            const float x = v[j * VEC + e];
+            const uint32_t b = __float_as_uint(x) & 0xFFFFE000u;   // top 11 significant bits
+            bg[e] = b;
+            sm[e] = __float_as_uint(x - __uint_as_float(b));       // exact residual
+        }
+        if (VEC == 4) {
+            *reinterpret_cast<uint4 *>(stage + off) = make_uint4(bg[0], bg[1], bg[2], bg[3]);
+            *reinterpret_cast<uint4 *>(stage + CT_A_BLK + off) = make_uint4(sm[0], sm[1], sm[2], sm[3]);
+        } else if (VEC == 2) {
+            *reinterpret_cast<uint2 *>(stage + off) = make_uint2(bg[0], bg[1]);
+            *reinterpret_cast<uint2 *>(stage + CT_A_BLK + off) = make_uint2(sm[0], sm[1]);
+        } else {
+            *reinterpret_cast<uint32_t *>(stage + off) = bg[0];
+            *reinterpret_cast<uint32_t *>(stage + CT_A_BLK + off) = sm[0];
+        }
+    }
+}
+
+template <int VEC>
+__global__ void __launch_bounds__(CT_THREADS, 1) k3_codes_tc(CodesArgs a) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
+    uint8_t *ring = smem;                                        // stages x 32 KB
+    uint8_t *Bs = ring + a.stages * CT_STAGE;                    // KB x N x 128 B
+    float *Ad = reinterpret_cast<float *>(Bs + (size_t)a.KB * a.N * 128);   // [N]
+    uint64_t *bars = reinterpret_cast<uint64_t *>(Ad + a.N);
+    uint64_t *full = bars, *empty = bars + a.stages;
+    uint64_t *tfull = bars + 2 * a.stages, *tempty = tfull + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int N = a.N;
+    // resident B operand (A^T, K-major, swizzled) and A_d
+    for (int e = threadIdx.x; e < a.KB * N * CT_KB; e += blockDim.x) {
+        const int kb = e / (N * CT_KB), rem = e % (N * CT_KB);
+        const int b = rem / CT_KB, k = rem % CT_KB;
+        const int kg = kb * CT_KB + k;
+        const float v = kg < a.d ? a.Apad[(size_t)kg * N + b] : 0.f;
+        *reinterpret_cast<float *>(Bs + (size_t)kb * N * 128 + swz(b, k * 4)) = v;
+    }
+    for (int b = threadIdx.x; b < N; b += blockDim.x) Ad[b] = a.Apad[(size_t)a.d * N + b];
+    tc::fence_async_shared();
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < a.stages; ++s) {
+            tc::mbar_init(&full[s], CT_CONV / 32);
+            tc::mbar_init(&empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            tc::mbar_init(&tfull[s], 1);
+            tc::mbar_init(&tempty[s], 4);
+        }
+        tc::fence_mbar_init();
+    }
+    const uint32_t tcols = N <= 16 ? 32 : (2 * N <= 64 ? 64 : (2 * N <= 128 ? 128 : 256));
+    if (warp == 8) tc::tmem_alloc(tmem_slot, tcols);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp < 8) {
+        // ================= converters
+        int64_t tile = blockIdx.x;
+        int kb = 0;
+        float cur[16];
+        if (tile < a.ntiles) conv_load<VEC>(a, tile, 0, warp, lane, cur);
+        for (uint32_t g = 0; tile < a.ntiles; ++g) {
+            int64_t ntile = tile;
+            int nkb = kb + 1;
+            if (nkb == a.KB) { nkb = 0; ntile += gridDim.x; }
+            float nxt[16];
+            if (ntile < a.ntiles) conv_load<VEC>(a, ntile, nkb, warp, lane, nxt);
+            const uint32_t s = g % a.stages, ph = (g / a.stages) & 1;
+            tc::mbar_wait(&empty[s], ph ^ 1);
+            conv_store<VEC>(ring + s * CT_STAGE, warp, lane, cur);
+            tc::fence_async_shared();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&full[s]);
+#pragma unroll
+            for (int e = 0; e < 16; ++e) cur[e] = nxt[e];
+            tile = ntile;
+            kb = nkb;
+        }
+    } else if (warp == 8) {
+        if (lane == 0) {
+            // ================= MMA issuer
+            const uint32_t idesc = tc::umma_idesc(2, CT_M, N);
+            uint32_t g = 0, t = 0;
+            for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++t) {
+                const uint32_t acc = t & 1, tr = t >> 1;
+                tc::mbar_wait(&tempty[acc], (tr & 1) ^ 1);
+                tc::tc_fence_after();
+                const uint32_t dt = tmem_base + acc * N;
+                for (int kb = 0; kb < a.KB; ++kb, ++g) {
+                    const uint32_t s = g % a.stages, ph = (g / a.stages) & 1;
+                    tc::mbar_wait(&full[s], ph);
+                    tc::tc_fence_after();
+                    const uint32_t abig = tc::smem_u32(ring + s * CT_STAGE);
+                    const uint32_t bb = tc::smem_u32(Bs + (size_t)kb * N * 128);
+                    const int nk = min(4, (a.d - kb * CT_KB + 7) / 8);   // K = 8 per MMA
+                    for (int kk = 0; kk < nk; ++kk)
+                        tc::mma_tf32(dt, tc::umma_desc_sw128(abig + kk * 32),
+                                     tc::umma_desc_sw128(bb + kk * 32), idesc, (kb | kk) != 0);
+                    for (int kk = 0; kk < nk; ++kk)
+                        tc::mma_tf32(dt, tc::umma_desc_sw128(abig + CT_A_BLK + kk * 32),
+                                     tc::umma_desc_sw128(bb + kk * 32), idesc, 1);
+                    tc::mma_commit(&empty[s]);
+                }
+                tc::mma_commit(&tfull[acc]);
+            }
+        }
+        __syncwarp();
+    } else {
+        // ================= epilogue: thread <-> item row (TMEM lane)
+        const int qd = warp & 3;
+        const int row = qd * 32 + lane;
+        const int W = N / 32;
+        uint32_t t = 0;
+        for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++t) {
+            const uint32_t acc = t & 1, tr = t >> 1;
+            const int64_t i = tile * CT_M + row;
+            const bool valid = i < a.n;
+            float tt = 0.f;
+            int64_t pos = 0;
+            if (valid) {
+                const double Vj = a.V[a.part[i]];
+                if (Vj == 0.0) tt = 1.f;
+                else {
+                    const double df = Vj - a.norm2[i];
+                    tt = (float)sqrt(df > 0.0 ? df : 0.0);
+                }
+                pos = a.pos_of_id[i];
+            }
+            tc::mbar_wait(&tfull[acc], tr & 1);
+            tc::tc_fence_after();
+            uint32_t words[4] = {0u, 0u, 0u, 0u};
+            const uint32_t taddr = tmem_base + ((uint32_t)(qd * 32) << 16) + acc * N;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                if (c < W) {
+                    uint32_t r[32];
+                    tc::tmem_ld_32x32b_x32(taddr + c * 32, r);
+                    tc::tmem_ld_wait();
+                    uint32_t wd = 0u;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const int b = c * 32 + j;
+                        const float y = fmaf(Ad[b], tt, __uint_as_float(r[j]));
+                        wd |= (uint32_t)(b < a.L && y >= 0.f) << j;
+                    }
+                    words[c] = wd;
+                }
+            }
+            tc::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+            if (valid) {
+                uint32_t *dst = a.codes + pos * W;
+                if (W == 4) *reinterpret_cast<uint4 *>(dst) = make_uint4(words[0], words[1], words[2], words[3]);
+                else if (W == 2) *reinterpret_cast<uint2 *>(dst) = make_uint2(words[0], words[1]);
+                else dst[0] = words[0];
+            }
+        }
+    }
+    __syncthreads();
+    if (warp == 8) {
+        tc::tc_fence_after();
+        tc::tmem_dealloc(tmem_base, tcols);
+    }
+}
+
+static size_t codes_tc_smem(int KB, int N, int stages) {
+    return 1024 + (size_t)stages * CT_STAGE + (size_t)KB * N * 128 + (size_t)N * 4 +
+           (2 * stages + 4) * 8 + 16;
+}
+
+static int codes_tc_stages(int d, int N) {
+    const int KB = (d + CT_KB - 1) / CT_KB;
+    for (int st = 4; st >= 2; --st)
+        if (codes_tc_smem(KB, N, st) <= 227 * 1024) return st;
+    return 0;
+}
+
+bool codes_tc_supported(int d, int W) {
+    return W != 3 && codes_tc_stages(d, 32 * W) > 0 && !getenv("NRLSH_CODES_SIMT");
+}
+
+void launch_item_codes_tc(const float *X, int64_t n, int d, const double *norm2,
+                          const uint8_t *part, const double *V, const float *Apad, int L, int W,
+                          const int32_t *pos_of_id, uint32_t *codes, cudaStream_t s) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    CodesArgs a;
+    a.X = X;
+    a.n = n;
+    a.d = d;
+    a.KB = (d + CT_KB - 1) / CT_KB;
+    a.L = L;
+    a.N = 32 * W;
+    a.stages = codes_tc_stages(d, a.N);
+    a.ntiles = (n + CT_M - 1) / CT_M;
+    a.norm2 = norm2;
+    a.part = part;
+    a.V = V;
+    a.Apad = Apad;
+    a.pos_of_id = pos_of_id;
+    a.codes = codes;
+    const size_t sm = codes_tc_smem(a.KB, a.N, a.stages);
+    const int grid = (int)std::min<int64_t>(sms, a.ntiles);
+    const int vec = (d % 4 == 0) ? 4 : ((d % 2 == 0) ? 2 : 1);
+#define NR_CT(V)                                                                               \
+    cudaFuncSetAttribute(k3_codes_tc<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+    k3_codes_tc<V><<<grid, CT_THREADS, sm, s>>>(a)
+    if (vec == 4) { NR_CT(4); } else if (vec == 2) { NR_CT(2); } else { NR_CT(1); }
+#undef NR_CT
+    note_launch();
+}
+
+}  // namespace nrlsh

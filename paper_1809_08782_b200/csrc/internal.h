@@ -82,6 +82,13 @@ void launch_item_codes(const float *X, int64_t n, int d, const double *norm2,
                        int L, int W, const int32_t *pos_of_id, uint32_t *codes,
                        cudaStream_t s);
 
+// K3 on tcgen05 (codes_tc.cu); the SIMT kernel above covers the other shapes
+bool codes_tc_supported(int d, int W);
+void launch_item_codes_tc(const float *X, int64_t n, int d, const double *norm2,
+                          const uint8_t *part_of_id, const double *V_d, const float *Apad,
+                          int L, int W, const int32_t *pos_of_id, uint32_t *codes,
+                          cudaStream_t s);
+
 // ---------------------------------------------------------------- query
 struct QueryWS {
     uint32_t *qcodes;   // [Qb x W]
