@@ -307,7 +307,9 @@ def run_native(args):
         idx = P.Index(Xd, L, m, seed=cfg.seed, query_batch=cfg.query_batch)
         ids, sc = idx.query(Qd, k, T)
         qstats = P.last_query_stats()
-        gid, gsc = idx.exact_topk(Qd, k)
+        # ground truth, warm-started from the LSH answers (certified; the result
+        # does not depend on the seeds — tests/test_gpu_parity.py)
+        gid, gsc = idx.exact_topk(Qd, k, seed_ids=ids)
         idx.close()
         return ids, gid, qstats
 
@@ -369,7 +371,7 @@ def run_native(args):
             t0 = time.perf_counter()
             idx = P.Index(Xh, L, m, seed=cfg.seed, query_batch=cfg.query_batch)
             idx.query(Qh, k, T, out_ids=oid, out_scores=osc)
-            idx.exact_topk(Qh, k, out_ids=gid2, out_scores=gsc2)
+            idx.exact_topk(Qh, k, out_ids=gid2, out_scores=gsc2, seed_ids=oid)
             idx.close()
             torch.cuda.synchronize()
             e2e_ms.append((time.perf_counter() - t0) * 1e3)

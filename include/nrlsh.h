@@ -160,6 +160,25 @@ nrlsh_status nrlsh_index_exact_topk(const nrlsh_index *index, const float *queri
                                     int32_t k, int64_t *out_ids, float *out_scores,
                                     void *cuda_stream);
 
+/*
+ * Seeded variants: seed_ids int64 [nq x seed_k] (device or host; -1, out-of-range
+ * and repeated ids are ignored), 1 <= seed_k <= 1024, are ANY item ids per query
+ * — typically the answers of nrlsh_query.  Their exact scores are recomputed and
+ * the k-th largest certified lower bound (fl(q.x) - 1.25 (d+2) 2^-24 |q||x|) starts
+ * the tensor-core filter's threshold instead of -inf.  The result is identical
+ * to the unseeded call (the threshold stays a lower bound of the true k-th best
+ * score); only the number of filter survivors, hence the time, changes.
+ * Errors as nrlsh_exact_topk, plus EINVAL for a NULL seed_ids or a bad seed_k.
+ */
+nrlsh_status nrlsh_exact_topk_seeded(const float *items, int64_t n, int32_t d,
+                                     const float *queries, int64_t nq, int32_t k,
+                                     const int64_t *seed_ids, int32_t seed_k, int64_t *out_ids,
+                                     float *out_scores, void *cuda_stream);
+nrlsh_status nrlsh_index_exact_topk_seeded(const nrlsh_index *index, const float *queries,
+                                           int64_t nq, int32_t k, const int64_t *seed_ids,
+                                           int32_t seed_k, int64_t *out_ids, float *out_scores,
+                                           void *cuda_stream);
+
 /* Statistics of the last exact top-k on this thread: the largest and the total
    number of filter survivors per query (re-scored exactly), and the number of
    queries whose survivors overflowed the buffer (answered by a full exact scan). */

@@ -23,7 +23,8 @@ EXPORTS = [
     "nrlsh_free", "nrlsh_last_error", "nrlsh_get_info", "nrlsh_get_partition",
     "nrlsh_get_projection", "nrlsh_get_rank_table", "nrlsh_get_codes", "nrlsh_set_codes",
     "nrlsh_query_codes", "nrlsh_query_candidates", "nrlsh_last_query_stats",
-    "nrlsh_index_exact_topk", "nrlsh_profile_enable", "nrlsh_profile_read",
+    "nrlsh_index_exact_topk", "nrlsh_exact_topk_seeded", "nrlsh_index_exact_topk_seeded",
+    "nrlsh_profile_enable", "nrlsh_profile_read",
     "nrlsh_profile_slot_name", "nrlsh_launch_count", "nrlsh_last_exact_stats",
 ]
 
@@ -87,6 +88,10 @@ def lib():
         L.nrlsh_last_query_stats.restype = st
         L.nrlsh_index_exact_topk.argtypes = [p, p, i64, i32, p, p, p]
         L.nrlsh_index_exact_topk.restype = st
+        L.nrlsh_exact_topk_seeded.argtypes = [p, i64, i32, p, i64, i32, p, i32, p, p, p]
+        L.nrlsh_exact_topk_seeded.restype = st
+        L.nrlsh_index_exact_topk_seeded.argtypes = [p, p, i64, i32, p, i32, p, p, p]
+        L.nrlsh_index_exact_topk_seeded.restype = st
         L.nrlsh_profile_enable.argtypes = [C.c_int]
         L.nrlsh_profile_enable.restype = None
         L.nrlsh_profile_read.argtypes = [p, p, i32, C.c_int]
@@ -186,15 +191,22 @@ class Index:
                                  _ptr(out_ids), _ptr(out_scores), _stream(stream)))
         return out_ids, out_scores
 
-    def exact_topk(self, queries, k, out_ids=None, out_scores=None, stream=None):
-        """Ground truth against the index's own items (no re-staging of host items)."""
+    def exact_topk(self, queries, k, out_ids=None, out_scores=None, stream=None, seed_ids=None):
+        """Ground truth against the index's own items (no re-staging of host items).
+        seed_ids [nq x ks] int64 (optional): warm-start ids, e.g. query()'s answers;
+        the result does not depend on them."""
         nq = queries.shape[0]
         if out_ids is None:
             out_ids = _empty_like_io(queries, (nq, k), np.int64, _torch_dtype("int64"))
         if out_scores is None:
             out_scores = _empty_like_io(queries, (nq, k), np.float32, _torch_dtype("float32"))
-        _check(lib().nrlsh_index_exact_topk(self._h, _ptr(queries), nq, int(k), _ptr(out_ids),
-                                            _ptr(out_scores), _stream(stream)))
+        if seed_ids is None:
+            _check(lib().nrlsh_index_exact_topk(self._h, _ptr(queries), nq, int(k), _ptr(out_ids),
+                                                _ptr(out_scores), _stream(stream)))
+        else:
+            _check(lib().nrlsh_index_exact_topk_seeded(
+                self._h, _ptr(queries), nq, int(k), _ptr(seed_ids), int(seed_ids.shape[1]),
+                _ptr(out_ids), _ptr(out_scores), _stream(stream)))
         return out_ids, out_scores
 
     def query_codes(self, queries, stream=None):
@@ -250,15 +262,20 @@ def _torch_dtype(name):
     return getattr(torch, name)
 
 
-def exact_topk(items, queries, k, out_ids=None, out_scores=None, stream=None):
+def exact_topk(items, queries, k, out_ids=None, out_scores=None, stream=None, seed_ids=None):
     n, d = items.shape
     nq = queries.shape[0]
     if out_ids is None:
         out_ids = _empty_like_io(queries, (nq, k), np.int64, _torch_dtype("int64"))
     if out_scores is None:
         out_scores = _empty_like_io(queries, (nq, k), np.float32, _torch_dtype("float32"))
-    _check(lib().nrlsh_exact_topk(_ptr(items), n, d, _ptr(queries), nq, int(k), _ptr(out_ids),
-                                  _ptr(out_scores), _stream(stream)))
+    if seed_ids is None:
+        _check(lib().nrlsh_exact_topk(_ptr(items), n, d, _ptr(queries), nq, int(k), _ptr(out_ids),
+                                      _ptr(out_scores), _stream(stream)))
+    else:
+        _check(lib().nrlsh_exact_topk_seeded(_ptr(items), n, d, _ptr(queries), nq, int(k),
+                                             _ptr(seed_ids), int(seed_ids.shape[1]), _ptr(out_ids),
+                                             _ptr(out_scores), _stream(stream)))
     return out_ids, out_scores
 
 

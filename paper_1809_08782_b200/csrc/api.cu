@@ -563,9 +563,11 @@ nrlsh_status nrlsh_last_query_stats(int64_t *fallback_queries, int64_t *kernel_l
 
 // ------------------------------------------------------------ exact top-k
 static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const float *queries,
-                               int64_t nq, int32_t k, int64_t *out_ids, float *out_scores,
-                               void *cuda_stream) {
+                               int64_t nq, int32_t k, const int64_t *seed_ids, int32_t seed_k,
+                               int64_t *out_ids, float *out_scores, void *cuda_stream) {
     if (!items || !queries || !out_ids || !out_scores) return fail(NRLSH_EINVAL, "NULL argument");
+    if (seed_ids && (seed_k < 1 || seed_k > 1024))
+        return fail(NRLSH_EINVAL, "seed_k must be in [1, 1024]");
     if (n < 1 || n >= (1ll << 31)) return fail(NRLSH_EINVAL, "n must be in [1, 2^31)");
     if (d < 1 || d > 4096) return fail(NRLSH_EINVAL, "d must be in [1, 4096]");
     if (nq < 1) return fail(NRLSH_EINVAL, "nq must be >= 1");
@@ -577,6 +579,8 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
     Staged Xs, Qs;
     if ((e = Xs.in(items, (size_t)n * d * 4, s))) return cuda_fail(e, "stage items");
     if ((e = Qs.in(queries, (size_t)nq * d * 4, s))) return cuda_fail(e, "stage queries");
+    Staged Ss;
+    if (seed_ids && (e = Ss.in(seed_ids, (size_t)nq * seed_k * 8, s))) return cuda_fail(e, "stage seeds");
     OutBuf oi, os;
     if ((e = oi.init(out_ids, (size_t)nq * k * 8, s))) return cuda_fail(e, "out_ids");
     if ((e = os.init(out_scores, (size_t)nq * k * 4, s))) return cuda_fail(e, "out_scores");
@@ -598,7 +602,7 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
                               : std::min<int64_t>(n, std::max<int64_t>(4 * (int64_t)S * k + 4096, 2 * k));
     int Qmax = (int)std::min<int64_t>(1024, nq);
     while (Qmax > 64 && (int64_t)Qmax * (ns * 4 + Cg * 8) > ((int64_t)2500 << 20)) Qmax >>= 1;
-    DBuf xn, qn, ss, lb, tid, tsc, cc, cd, cs, xb, qb, th, pt;
+    DBuf xn, qn, ss, lb, tid, tsc, cc, cd, cs, xb, qb, th, pt, hp;
     const int64_t npad = (n + 255) / 256 * 256;   // |x| padded: the tc kernel bulk-loads 1 KB tiles
     if (xn.alloc((size_t)npad * 4, s) || qn.alloc((size_t)nq * 4, s) ||
         ss.alloc((size_t)Qmax * ns * 4, s) || lb.alloc((size_t)Qmax * 4, s) ||
@@ -608,7 +612,8 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
         pt.alloc(std::max(rerank_partial_bytes(Qmax, Cg, k), rerank_partial_bytes(1, n, k)), s))
         return fail(NRLSH_ENOMEM, "exact_topk workspace");
     if (use_tc) {
-        if (xb.alloc((size_t)n * dp * 2, s) || qb.alloc((size_t)nq * dp * 2, s))
+        if (xb.alloc((size_t)n * dp * 2, s) || qb.alloc((size_t)nq * dp * 2, s) ||
+            hp.alloc(gt_heap_bytes(k), s))
             return fail(NRLSH_ENOMEM, "exact_topk bf16 workspace");
         ProfScope p(SLOT_GT_NORMS, s);
         cudaMemsetAsync(xn.get<float>() + n, 0, (size_t)(npad - n) * 4, s);
@@ -629,10 +634,16 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
         cudaMemsetAsync(cc.p, 0, (size_t)Qb * 4, s);
         if (use_tc) {
             cudaMemsetAsync(th.p, 0, (size_t)Qb * 4, s);
+            if (seed_ids) {
+                ProfScope p(SLOT_GT_NORMS, s);
+                launch_gt_seed_theta(X, n, d, Qb_ptr, Qb, qnb, (const int64_t *)Ss.dev + q0 * seed_k,
+                                     seed_k, k, (float)(1.25 * (d + 2) * std::ldexp(1.0, -24)),
+                                     th.get<uint32_t>(), s);
+            }
             ProfScope p(SLOT_GT_FILTER, s);
-            if (launch_gt_filter_tc(xb.p, n, dp, (const uint16_t *)qb.p + q0 * dp, Qb, xn.get<float>(),
-                                    qnb, eps_rel, k, th.get<uint32_t>(), cd.get<int32_t>(),
-                                    cc.get<uint32_t>(), Cg, s))
+            if (launch_gt_filter_tc(xb.p, n, d, dp, (const uint16_t *)qb.p + q0 * dp, Qb,
+                                    xn.get<float>(), qnb, eps_rel, k, th.get<uint32_t>(),
+                                    hp.get<float>(), cd.get<int32_t>(), cc.get<uint32_t>(), Cg, s))
                 return fail(NRLSH_ECUDA, "tensor map encoding failed");
         } else {
             // pilot: certified lower bound of the k-th best score from a strided sample
@@ -687,14 +698,34 @@ nrlsh_status nrlsh_last_exact_stats(int64_t *max_cand, int64_t *sum_cand, int64_
 nrlsh_status nrlsh_exact_topk(const float *items, int64_t n, int32_t d, const float *queries,
                               int64_t nq, int32_t k, int64_t *out_ids, float *out_scores,
                               void *cuda_stream) {
-    return exact_impl(items, n, d, queries, nq, k, out_ids, out_scores, cuda_stream);
+    return exact_impl(items, n, d, queries, nq, k, nullptr, 0, out_ids, out_scores, cuda_stream);
+}
+
+nrlsh_status nrlsh_exact_topk_seeded(const float *items, int64_t n, int32_t d,
+                                     const float *queries, int64_t nq, int32_t k,
+                                     const int64_t *seed_ids, int32_t seed_k, int64_t *out_ids,
+                                     float *out_scores, void *cuda_stream) {
+    if (!seed_ids) return fail(NRLSH_EINVAL, "seed_ids is NULL");
+    return exact_impl(items, n, d, queries, nq, k, seed_ids, seed_k, out_ids, out_scores,
+                      cuda_stream);
 }
 
 nrlsh_status nrlsh_index_exact_topk(const nrlsh_index *ix, const float *queries, int64_t nq,
                                     int32_t k, int64_t *out_ids, float *out_scores,
                                     void *cuda_stream) {
     if (!ix) return fail(NRLSH_EINVAL, "index is NULL");
-    return exact_impl(ix->X, ix->n, ix->d, queries, nq, k, out_ids, out_scores, cuda_stream);
+    return exact_impl(ix->X, ix->n, ix->d, queries, nq, k, nullptr, 0, out_ids, out_scores,
+                      cuda_stream);
+}
+
+nrlsh_status nrlsh_index_exact_topk_seeded(const nrlsh_index *ix, const float *queries,
+                                           int64_t nq, int32_t k, const int64_t *seed_ids,
+                                           int32_t seed_k, int64_t *out_ids, float *out_scores,
+                                           void *cuda_stream) {
+    if (!ix) return fail(NRLSH_EINVAL, "index is NULL");
+    if (!seed_ids) return fail(NRLSH_EINVAL, "seed_ids is NULL");
+    return exact_impl(ix->X, ix->n, ix->d, queries, nq, k, seed_ids, seed_k, out_ids, out_scores,
+                      cuda_stream);
 }
 
 // ------------------------------------------------------------------ hooks

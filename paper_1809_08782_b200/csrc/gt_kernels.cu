@@ -117,4 +117,71 @@ void launch_gt_filter(const float *X, int64_t n, int d, const float *Q, int Qb,
     note_launch();
 }
 
+
+// Certified warm start of the filter threshold from caller-supplied item ids
+// (any ids: typically the LSH answers).  Every seed's exact-product score is
+// recomputed here: lb = fl(q.x) - eps |q| |x| (rounded down) is a lower bound of
+// its true score, so the k-th largest lb over k distinct seeds is a lower bound of
+// the true k-th best score (theta_glob[q]; 0 = no bound).  The result of the
+// ground truth does not depend on the seeds, only its speed does.
+__global__ void __launch_bounds__(256) gt_seed_theta(const float *__restrict__ X, int64_t n, int d,
+                                                     const float *__restrict__ Q,
+                                                     const float *__restrict__ qnorm,
+                                                     const int64_t *__restrict__ seeds, int ks,
+                                                     int k, float eps_rel,
+                                                     uint32_t *__restrict__ theta_glob) {
+    __shared__ float lbs[1024];
+    __shared__ int64_t sid[1024];
+    const int q = blockIdx.x;
+    const float *qp = Q + (int64_t)q * d;
+    const int np2 = ks <= 1 ? 1 : 1 << (32 - __clz(ks - 1));
+    for (int t = threadIdx.x; t < np2; t += blockDim.x) {
+        int64_t id = t < ks ? seeds[(int64_t)q * ks + t] : -1;
+        if (id >= n) id = -1;
+        // duplicates count once: keep the first occurrence only
+        for (int u = 0; u < t && id >= 0; ++u)
+            if (seeds[(int64_t)q * ks + u] == id) id = -1;
+        float lb = -INFINITY;
+        if (id >= 0) {
+            const float *xp = X + id * d;
+            float acc = 0.f;
+            double xx = 0.0;
+            for (int j = 0; j < d; ++j) {
+                const float xv = __ldg(xp + j);
+                acc = fmaf(__ldg(qp + j), xv, acc);
+                xx += (double)xv * (double)xv;
+            }
+            const float xn = __double2float_ru(sqrt(xx));
+            lb = __fsub_rd(acc, __fmul_ru(__fmul_ru(eps_rel, qnorm[q]), xn));
+        }
+        lbs[t] = lb;
+        sid[t] = id;
+    }
+    __syncthreads();
+    // sort descending
+    for (int size = 2; size <= np2; size <<= 1) {
+        for (int st = size >> 1; st > 0; st >>= 1) {
+            for (int t = threadIdx.x; t < np2; t += blockDim.x) {
+                const int o = t ^ st;
+                if (o > t) {
+                    const bool up = (t & size) == 0;
+                    if ((lbs[t] < lbs[o]) == up) { const float x = lbs[t]; lbs[t] = lbs[o]; lbs[o] = x; }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    if (threadIdx.x == 0) {
+        const float th = (k <= np2) ? lbs[k - 1] : -INFINITY;
+        theta_glob[q] = (th > -INFINITY) ? float_order(th) : 0u;
+    }
+}
+
+void launch_gt_seed_theta(const float *X, int64_t n, int d, const float *Q, int Qb,
+                          const float *qnorm, const int64_t *seeds, int ks, int k, float eps_rel,
+                          uint32_t *theta_glob, cudaStream_t s) {
+    gt_seed_theta<<<Qb, 256, 0, s>>>(X, n, d, Q, qnorm, seeds, ks, k, eps_rel, theta_glob);
+    note_launch();
+}
+
 }  // namespace nrlsh

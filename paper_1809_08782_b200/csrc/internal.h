@@ -141,13 +141,17 @@ void launch_gt_filter(const float *X, int64_t n, int d, const float *Q, int Qb,
                       const float *xnorm, const float *qnorm, const float *lb, float eps_rel,
                       int32_t *cand, uint32_t *cnt, int64_t C, cudaStream_t s);
 int scan_chunk_items();
+void launch_gt_seed_theta(const float *X, int64_t n, int d, const float *Q, int Qb,
+                          const float *qnorm, const int64_t *seeds, int ks, int k, float eps_rel,
+                          uint32_t *theta_glob, cudaStream_t s);
 // tensor-core ground truth (tc_kernels.cu)
 void launch_bf16_prep(const float *X, int64_t n, int d, int dp, void *Xb, float *xnorm,
                       cudaStream_t s);
 bool gt_tc_supported(int d, int k);
-int launch_gt_filter_tc(const void *Xb, int64_t n, int dp, const void *Qb16, int Qb,
+size_t gt_heap_bytes(int k);
+int launch_gt_filter_tc(const void *Xb, int64_t n, int d, int dp, const void *Qb16, int Qb,
                         const float *xnorm, const float *qnorm, float eps_rel, int k,
-                        uint32_t *theta_glob, int32_t *cand, uint32_t *cnt, int64_t C,
-                        cudaStream_t s);
+                        uint32_t *theta_glob, float *heap, int32_t *cand, uint32_t *cnt,
+                        int64_t C, cudaStream_t s);
 
 }  // namespace nrlsh

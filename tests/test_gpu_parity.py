@@ -202,6 +202,42 @@ def test_exact_topk_parity(name, n, nq, k):
         assert_topk_match(ids[qi], sc[qi], a, s, X, Q[qi])
 
 
+@pytest.mark.parametrize("name,n,nq,k", [("c2", None, 40, 10), ("c3", 60_000, 300, 10),
+                                         ("scale", 80_000, 8, 100)])
+def test_exact_topk_seeded_matches_unseeded(name, n, nq, k):
+    """Warm-start seeds change only the filter's starting threshold: any seed list
+    (the LSH answers, the true answers, random ids, junk: -1 / out of range /
+    repeats, fewer than k valid) gives the unseeded result, which matches the oracle."""
+    P = _P()
+    cfg, X, Q = dataset(workloads.CONFIGS[name], n, nq)
+    Q = Q[:nq]
+    Xd, Qd = torch.from_numpy(X).cuda(), torch.from_numpy(Q).cuda()
+    base, bsc = P.exact_topk(Xd, Qd, k)
+    base, bsc = base.cpu().numpy(), bsc.cpu().numpy()
+    for qi in range(min(nq, 12)):
+        a, s_ = oracle.exact_topk(X, Q[qi], k)
+        assert_topk_match(base[qi], bsc[qi], a, s_, X, Q[qi])
+    rng = np.random.default_rng(5)
+    n_ = X.shape[0]
+    seeds = {
+        "truth": base.copy(),
+        "random": rng.integers(0, n_, size=(nq, 3 * k)),
+        "junk": np.where(rng.random((nq, 2 * k)) < 0.5, -1, n_ + 7).astype(np.int64),
+        "repeats": np.repeat(base[:, :1], k + 3, axis=1),
+        "short": base[:, : max(1, k // 2)].copy(),
+    }
+    m = 8 if name != "scale" else 1
+    idx = P.Index(Xd, 64, m, seed=cfg.seed)
+    lsh, _ = idx.query(Qd, k, max(k, n_ // 100))
+    seeds["lsh"] = lsh.cpu().numpy()
+    for nm, sd in seeds.items():
+        got, gsc = P.exact_topk(Xd, Qd, k, seed_ids=torch.from_numpy(np.ascontiguousarray(sd, np.int64)).cuda())
+        assert np.array_equal(got.cpu().numpy(), base), nm
+        assert np.array_equal(gsc.cpu().numpy(), bsc), nm
+        got2, _ = idx.exact_topk(Qd, k, seed_ids=np.ascontiguousarray(sd, np.int64))
+        assert np.array_equal(got2.cpu().numpy(), base), nm
+
+
 # --------------------------------------------------------------- edge cases
 def test_full_budget_equals_brute_force(built):
     cfg, X, Q, Xd, idx, orc = built("tiny", None, None, 32, 8)

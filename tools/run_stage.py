@@ -35,6 +35,11 @@ for r in range(a.reps):
     if a.stage == "gt":
         ids, sc = idx.exact_topk(Q, cfg.k)
         st = P.last_exact_stats()
+    elif a.stage == "gtseed":
+        if r == 0:
+            seeds, _ = idx.query(Q, cfg.k, T)
+        ids, sc = idx.exact_topk(Q, cfg.k, seed_ids=seeds)
+        st = P.last_exact_stats()
     elif a.stage == "query":
         ids, sc = idx.query(Q, cfg.k, T)
         st = P.last_query_stats()
