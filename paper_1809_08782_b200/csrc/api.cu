@@ -136,7 +136,7 @@ void free_index(nrlsh_index *ix) {
     if (!ix) return;
     void *ps[] = {ix->X_owned, ix->norm2, ix->perm, ix->pos_of_id, ix->part_of_id,
                   ix->part_of_pos, ix->offsets_d, ix->V_d, ix->codes, ix->A, ix->Apad,
-                  ix->R_d, ix->chunks_d, ix->order_d};
+                  ix->R_d, ix->chunks_d, ix->order_d, ix->samp_codes, ix->samp_part};
     // pool-backed (cudaMallocAsync at build); the index may have been used on any stream
     cudaDeviceSynchronize();
     for (void *p : ps)
@@ -179,6 +179,14 @@ struct OutBuf {
 };
 
 }  // namespace
+
+namespace nrlsh {
+int pilot_stride(int64_t n) {
+    if (n <= (1 << 18)) return 1;                 // exact histogram: no fallback needed
+    int64_t s = n / 65536;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(64, s));
+}
+}  // namespace nrlsh
 
 // ============================================================================ ABI
 extern "C" {
@@ -342,6 +350,17 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
         launch_item_codes(ix->X, n, d, ix->norm2, ix->part_of_id, ix->V_d, ix->Apad, L, W,
                           ix->pos_of_id, ix->codes, s);
     }
+    // compacted pilot sample (query-time pilots read it contiguously)
+    {
+        const int stride = pilot_stride(n);
+        if (stride > 1) {
+            ix->nsamp = (n + stride - 1) / stride;
+            NR_ALLOC(ix->samp_codes, (size_t)ix->nsamp * W * 4);
+            NR_ALLOC(ix->samp_part, (size_t)ix->nsamp);
+            ProfScope p(SLOT_CODES, s);
+            launch_gather_sample(ix.get(), stride, ix->samp_codes, ix->samp_part, s);
+        }
+    }
     e = cudaStreamSynchronize(s);
     if (e) return cuda_fail(e, "codes");
     prof_collect();
@@ -366,11 +385,6 @@ nrlsh_status nrlsh_get_info(const nrlsh_index *ix, int64_t *n, int32_t *d, int32
 // ------------------------------------------------------------------ query
 namespace {
 
-int pilot_stride(int64_t n) {
-    if (n <= (1 << 18)) return 1;                 // exact histogram: no fallback needed
-    int64_t s = n / 65536;
-    return (int)std::max<int64_t>(1, std::min<int64_t>(64, s));
-}
 
 int64_t buffer_capacity(int64_t Tq, int stride, int64_t n) {
     double c = 2.0 * Tq + 16.0 * std::sqrt((double)Tq * stride) + 4096.0;
@@ -765,6 +779,10 @@ nrlsh_status nrlsh_set_codes(nrlsh_index *ix, const uint32_t *codes) {
     if (!ix || !codes) return fail(NRLSH_EINVAL, "bad argument");
     cudaError_t e = cudaMemcpy(ix->codes, codes, (size_t)ix->n * ix->W * 4, cudaMemcpyDefault);
     if (e) return cuda_fail(e, "set codes");
+    if (ix->samp_codes) {   // keep the pilot sample in step with the codes
+        launch_gather_sample(ix, pilot_stride(ix->n), ix->samp_codes, ix->samp_part, nullptr);
+        if ((e = cudaDeviceSynchronize())) return cuda_fail(e, "set codes (sample)");
+    }
     return NRLSH_OK;
 }
 

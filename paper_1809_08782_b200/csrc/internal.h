@@ -38,6 +38,9 @@ struct nrlsh_index {
     int4 *chunks_d = nullptr;       // scan work units (j, pos0, pos1, 0)
     int32_t *order_d = nullptr;     // [m*(L+1)] structure position -> j*(L+1)+h
     int32_t nchunks = 0;
+    uint32_t *samp_codes = nullptr; // pilot sample: codes of positions t * stride (compacted)
+    uint8_t *samp_part = nullptr;
+    int64_t nsamp = 0;
 
     std::vector<int64_t> offsets;
     std::vector<double> V, U;
@@ -104,6 +107,9 @@ struct QueryWS {
 
 void launch_qcodes(const float *Q, int64_t nq, int d, const float *Apad, int L, int W,
                    uint32_t *qcodes, int *flags, int64_t q_index_base, cudaStream_t s);
+int pilot_stride(int64_t n);
+void launch_gather_sample(const nrlsh_index *ix, int stride, uint32_t *sc, uint8_t *sp,
+                          cudaStream_t s);
 void launch_pilot(const nrlsh_index *ix, const uint32_t *qcodes, int Qb, int64_t Tq,
                   int stride, int8_t *delta, uint32_t *cnt, cudaStream_t s);
 void launch_scan(const nrlsh_index *ix, const uint32_t *qcodes, const int8_t *delta, int Qb,

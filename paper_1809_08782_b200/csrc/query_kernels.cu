@@ -80,25 +80,32 @@ __device__ __forceinline__ void load_code(const uint32_t *__restrict__ codes, in
     }
 }
 
-// Histogram of (j, h) over positions p = tid*stride, ... (stride 1 = exact) into
-// smem `hist` [m*(L+1)]; then the smallest structure position r whose cumulative
+// Histogram of (j, h) over the ns sample entries (codes[t], part[t]) into smem
+// `hist` [m*(L+1)] (the sample is every position, or the index's compacted
+// strided sample); then the smallest structure position r whose cumulative
 // count reaches `need` (in histogram units).  Returns r (NR-1 if never reached)
-// and the count strictly before r in *cum_lt.
+// and the count strictly before r in *cum_lt.  Lanes holding the same bin add
+// once (match_any), which turns most shared atomics of a warp into one.
 template <int W>
 __device__ void hist_and_bound(const uint32_t *__restrict__ codes,
-                               const uint8_t *__restrict__ part_of_pos, int64_t n, int stride,
+                               const uint8_t *__restrict__ part, int64_t ns,
                                const uint32_t (&qc)[W], int L, int NR,
                                const int32_t *__restrict__ order, uint32_t *hist, uint32_t need,
                                uint32_t *ws, int *sB, uint32_t *sLt) {
     for (int e = threadIdx.x; e < NR; e += blockDim.x) hist[e] = 0u;
     if (threadIdx.x == 0) { *sB = NR - 1; *sLt = 0u; }
     __syncthreads();
-    for (int64_t p = (int64_t)threadIdx.x * stride; p < n; p += (int64_t)blockDim.x * stride) {
-        uint32_t c[W];
-        load_code<W>(codes, p, c);
-        const int h = hamming<W>(c, qc);
-        const int j = part_of_pos[p];
-        atomicAdd(&hist[j * (L + 1) + h], 1u);
+    const int lane = threadIdx.x & 31;
+    for (int64_t b0 = 0; b0 < ns; b0 += blockDim.x) {
+        const int64_t t = b0 + threadIdx.x;
+        int bin = -1;
+        if (t < ns) {
+            uint32_t c[W];
+            load_code<W>(codes, t, c);
+            bin = (int)part[t] * (L + 1) + hamming<W>(c, qc);
+        }
+        const unsigned peers = __match_any_sync(NR_FULL, bin);
+        if (bin >= 0 && lane == __ffs(peers) - 1) atomicAdd(&hist[bin], (uint32_t)__popc(peers));
     }
     __syncthreads();
     const int seg = (NR + blockDim.x - 1) / blockDim.x;
@@ -120,11 +127,37 @@ __device__ void hist_and_bound(const uint32_t *__restrict__ codes,
     __syncthreads();
 }
 
+// ------------------------------------------------------------------ pilot sample
+template <int W>
+__global__ void gather_sample(const uint32_t *__restrict__ codes, const uint8_t *__restrict__ part,
+                              int64_t ns, int stride, uint32_t *__restrict__ sc,
+                              uint8_t *__restrict__ sp) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ns;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = t * stride;
+#pragma unroll
+        for (int w = 0; w < W; ++w) sc[t * W + w] = codes[p * W + w];
+        sp[t] = part[p];
+    }
+}
+
+void launch_gather_sample(const nrlsh_index *ix, int stride, uint32_t *sc, uint8_t *sp,
+                          cudaStream_t s) {
+    const int64_t ns = (ix->n + stride - 1) / stride;
+    const int grid = grid_for(ns, 256, 1024);
+    switch (ix->W) {
+        case 1: gather_sample<1><<<grid, 256, 0, s>>>(ix->codes, ix->part_of_pos, ns, stride, sc, sp); break;
+        case 2: gather_sample<2><<<grid, 256, 0, s>>>(ix->codes, ix->part_of_pos, ns, stride, sc, sp); break;
+        default: gather_sample<4><<<grid, 256, 0, s>>>(ix->codes, ix->part_of_pos, ns, stride, sc, sp); break;
+    }
+    note_launch();
+}
+
 // =========================================================================== K6 pilot
 template <int W>
 __global__ void __launch_bounds__(1024) k6_pilot(
     const uint32_t *__restrict__ codes, const uint8_t *__restrict__ part_of_pos, int64_t n,
-    int stride, const uint32_t *__restrict__ qcodes, int L, int m,
+    const uint32_t *__restrict__ qcodes, int L, int m,
     const int32_t *__restrict__ order, const uint16_t *__restrict__ R, uint32_t need,
     int8_t *__restrict__ delta, uint32_t *__restrict__ cnt) {
     extern __shared__ uint32_t hist[];
@@ -136,7 +169,7 @@ __global__ void __launch_bounds__(1024) k6_pilot(
     uint32_t qc[W];
 #pragma unroll
     for (int w = 0; w < W; ++w) qc[w] = qcodes[q * W + w];
-    hist_and_bound<W>(codes, part_of_pos, n, stride, qc, L, NR, order, hist, need, ws, &sB, &sLt);
+    hist_and_bound<W>(codes, part_of_pos, n, qc, L, NR, order, hist, need, ws, &sB, &sLt);
     const int B = sB;
     for (int j = threadIdx.x; j < m; j += blockDim.x) {
         int c = 0;
@@ -157,18 +190,23 @@ void launch_pilot(const nrlsh_index *ix, const uint32_t *qcodes, int Qb, int64_t
     const int NR = ix->m * (ix->L + 1);
     const size_t sm = (size_t)NR * 4;
     const int32_t *order = ix->order_d;
+    // the strided sample p = t * stride, compacted at build time (or every position)
+    const bool cmp = stride > 1 && ix->samp_codes;
+    const uint32_t *sc = cmp ? ix->samp_codes : ix->codes;
+    const uint8_t *sp = cmp ? ix->samp_part : ix->part_of_pos;
+    const int64_t ns = cmp ? ix->nsamp : ix->n;
     switch (ix->W) {
         case 1:
             cudaFuncSetAttribute(k6_pilot<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            k6_pilot<1><<<Qb, 1024, sm, s>>>(ix->codes, ix->part_of_pos, ix->n, stride, qcodes, ix->L, ix->m, order, ix->R_d, need, delta, cnt);
+            k6_pilot<1><<<Qb, 1024, sm, s>>>(sc, sp, ns, qcodes, ix->L, ix->m, order, ix->R_d, need, delta, cnt);
             break;
         case 2:
             cudaFuncSetAttribute(k6_pilot<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            k6_pilot<2><<<Qb, 1024, sm, s>>>(ix->codes, ix->part_of_pos, ix->n, stride, qcodes, ix->L, ix->m, order, ix->R_d, need, delta, cnt);
+            k6_pilot<2><<<Qb, 1024, sm, s>>>(sc, sp, ns, qcodes, ix->L, ix->m, order, ix->R_d, need, delta, cnt);
             break;
         default:
             cudaFuncSetAttribute(k6_pilot<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            k6_pilot<4><<<Qb, 1024, sm, s>>>(ix->codes, ix->part_of_pos, ix->n, stride, qcodes, ix->L, ix->m, order, ix->R_d, need, delta, cnt);
+            k6_pilot<4><<<Qb, 1024, sm, s>>>(sc, sp, ns, qcodes, ix->L, ix->m, order, ix->R_d, need, delta, cnt);
             break;
     }
     note_launch();
@@ -179,7 +217,11 @@ constexpr int kScanThreads = 256;
 constexpr int kScanIPT = 4;                       // items per thread
 constexpr int kChunk = kScanThreads * kScanIPT;   // items per work unit
 constexpr int kQG = 64;                           // queries per CTA
+constexpr int kSB = 64;                           // staged appends per (CTA, query)
 
+// Appends (R << 32 | pos) are staged per query in shared memory (one shared
+// atomic per warp ballot) and copied out with one global reservation per
+// (CTA, query); a query whose stage fills spills the rest straight to global.
 template <int W>
 __global__ void __launch_bounds__(kScanThreads) k6_scan(
     const uint32_t *__restrict__ codes, const int4 *__restrict__ chunks,
@@ -189,6 +231,9 @@ __global__ void __launch_bounds__(kScanThreads) k6_scan(
     __shared__ uint32_t sq[kQG][W];
     __shared__ int sd[kQG];
     __shared__ uint32_t sR[129];
+    __shared__ unsigned long long sbuf[kQG][kSB];
+    __shared__ uint32_t scnt[kQG];
+    __shared__ uint32_t sbase[kQG];
     // consecutive CTAs share a chunk (different query groups): the chunk's codes
     // are read from HBM once and re-served from L2
     const int ngroups = (Qb + kQG - 1) / kQG;
@@ -196,19 +241,29 @@ __global__ void __launch_bounds__(kScanThreads) k6_scan(
     const int j = ch.x, p0 = ch.y, p1 = ch.z;
     const int q0 = (blockIdx.x % ngroups) * kQG;
     const int nqg = min(kQG, Qb - q0);
-    int act = 0;
-    for (int t = threadIdx.x; t < kQG; t += blockDim.x) {
-        int dl = -1;
-        if (t < nqg) {
-            dl = delta[(int64_t)(q0 + t) * m + j];
+    __shared__ int sact[kQG];     // compacted list of the queries with delta_j(q) >= 0
+    __shared__ int s_nact;
+    if (threadIdx.x < 32) {       // warp 0 compacts the group's active queries
+        int base = 0;
+        for (int t0 = 0; t0 < kQG; t0 += 32) {
+            const int t = t0 + threadIdx.x;
+            int dl = -1;
+            if (t < nqg) {
+                dl = delta[(int64_t)(q0 + t) * m + j];
 #pragma unroll
-            for (int w = 0; w < W; ++w) sq[t][w] = qcodes[(int64_t)(q0 + t) * W + w];
+                for (int w = 0; w < W; ++w) sq[t][w] = qcodes[(int64_t)(q0 + t) * W + w];
+            }
+            sd[t] = dl;
+            scnt[t] = 0;
+            const unsigned bal = __ballot_sync(NR_FULL, dl >= 0);
+            if (dl >= 0) sact[base + __popc(bal & lanemask_lt())] = t;
+            base += __popc(bal);
         }
-        sd[t] = dl;
-        act |= (dl >= 0);
+        if (threadIdx.x == 0) s_nact = base;
     }
     for (int h = threadIdx.x; h <= L; h += blockDim.x) sR[h] = R[j * (L + 1) + h];
-    const int nact = __syncthreads_count(act);
+    __syncthreads();
+    const int nact = s_nact;
     if (nact == 0) return;
     if (threadIdx.x == 0 && pairs) atomicAdd(pairs, (unsigned long long)nact * (p1 - p0));
     const int lane = threadIdx.x & 31;
@@ -224,9 +279,9 @@ __global__ void __launch_bounds__(kScanThreads) k6_scan(
 #pragma unroll
             for (int w = 0; w < W; ++w) c[u][w] = 0u;
     }
-    for (int qq = 0; qq < nqg; ++qq) {
+    for (int ia = 0; ia < nact; ++ia) {
+        const int qq = sact[ia];
         const int dl = sd[qq];
-        if (dl < 0) continue;
         uint32_t qc[W];
 #pragma unroll
         for (int w = 0; w < W; ++w) qc[w] = sq[qq][w];
@@ -240,22 +295,42 @@ __global__ void __launch_bounds__(kScanThreads) k6_scan(
             any |= pass[u];
         }
         if (!__any_sync(NR_FULL, any)) continue;
-        const int q = q0 + qq;
 #pragma unroll
         for (int u = 0; u < kScanIPT; ++u) {
             const unsigned bal = __ballot_sync(NR_FULL, pass[u]);
             if (bal == 0u) continue;
             const int leader = __ffs(bal) - 1;
             uint32_t base = 0;
-            if (lane == leader) base = atomicAdd(&cnt[q], (uint32_t)__popc(bal));
+            if (lane == leader) base = atomicAdd(&scnt[qq], (uint32_t)__popc(bal));
             base = __shfl_sync(NR_FULL, base, leader);
             if (pass[u]) {
                 const uint32_t slot = base + __popc(bal & lt);
-                if (slot < C) {
-                    const uint32_t p = p0 + threadIdx.x + kScanThreads * u;
-                    buf[(int64_t)q * C + slot] = ((unsigned long long)sR[h[u]] << 32) | p;
+                const uint32_t p = p0 + threadIdx.x + kScanThreads * u;
+                const unsigned long long e = ((unsigned long long)sR[h[u]] << 32) | p;
+                if (slot < kSB) {
+                    sbuf[qq][slot] = e;
+                } else {   // stage full: direct global append (rare)
+                    const int q = q0 + qq;
+                    const uint32_t g = atomicAdd(&cnt[q], 1u);
+                    if (g < C) buf[(int64_t)q * C + g] = e;
                 }
             }
+        }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < nqg; t += blockDim.x) {
+        const uint32_t nst = min(scnt[t], (uint32_t)kSB);
+        sbase[t] = nst ? atomicAdd(&cnt[q0 + t], nst) : 0u;
+    }
+    __syncthreads();
+    // copy-out: warp w handles queries w, w+8, ...; lanes stride the staged entries
+    const int warp = threadIdx.x >> 5;
+    for (int t = warp; t < nqg; t += kScanThreads / 32) {
+        const uint32_t nst = min(scnt[t], (uint32_t)kSB);
+        const int64_t q = q0 + t;
+        for (uint32_t e = lane; e < nst; e += 32) {
+            const uint32_t g = sbase[t] + e;
+            if (g < C) buf[q * C + g] = sbuf[t][e];
         }
     }
 }
@@ -294,8 +369,7 @@ __global__ void __launch_bounds__(1024) k6_fallback(
     uint32_t qc[W];
 #pragma unroll
     for (int w = 0; w < W; ++w) qc[w] = qcodes[q * W + w];
-    hist_and_bound<W>(codes, part_of_pos, n, 1, qc, L, NR, order, hist, (uint32_t)Tq, ws, &sB,
-                      &sLt);
+    hist_and_bound<W>(codes, part_of_pos, n, qc, L, NR, order, hist, (uint32_t)Tq, ws, &sB, &sLt);
     const int B = sB;
     const uint32_t need_eq = (uint32_t)Tq - sLt;
     // R[j][h] lookup straight from the structure (global, cached)
@@ -349,9 +423,9 @@ void launch_fallback(const nrlsh_index *ix, const uint32_t *qcodes, int Qb, int6
 // =========================================================================== K7 select
 __global__ void __launch_bounds__(1024) k7_select(
     const unsigned long long *__restrict__ buf, const uint32_t *__restrict__ cnt, int64_t C,
-    int64_t Tq, int NR, const int32_t *__restrict__ perm, int32_t *__restrict__ cand,
-    uint16_t *__restrict__ cand_rank) {
-    extern __shared__ uint32_t hist[];
+    int64_t Tq, int NR, int tie_cap, const int32_t *__restrict__ perm,
+    int32_t *__restrict__ cand, uint16_t *__restrict__ cand_rank) {
+    extern __shared__ uint32_t hist[];   // [max(NR, tie_cap)]
     __shared__ uint32_t ws[32];
     __shared__ uint32_t h256[256];
     __shared__ int sB;
@@ -384,10 +458,58 @@ __global__ void __launch_bounds__(1024) k7_select(
     const uint32_t B = (uint32_t)sB;
     const uint32_t need_eq = need - sLt;
     const uint32_t n_eq = hist[B];
-    // the need_eq-th smallest position among the ties (R == B): radix select, 8 bits/round
-    if (threadIdx.x == 0) { s_pfx = 0; s_kth = need_eq; }
+    // the need_eq-th smallest position among the ties (R == B): when they fit, one
+    // pass gathers them into shared memory (reusing the histogram's space) and a
+    // radix select runs there; otherwise radix select over the buffer, 8 bits/round
+    if (threadIdx.x == 0) { s_pfx = 0; s_kth = need_eq; s_out = 0; }
     __syncthreads();
-    if (need_eq < n_eq) {
+    uint32_t *teq = hist;   // the histogram is dead once B and n_eq are known
+    const bool in_smem = need_eq < n_eq && n_eq <= (uint32_t)tie_cap;
+    if (in_smem) {
+        for (int64_t e = threadIdx.x; e < c; e += blockDim.x) {
+            const unsigned long long v = b[e];
+            if ((uint32_t)(v >> 32) == B) teq[atomicAdd(&s_out, 1u)] = (uint32_t)v;
+        }
+        __syncthreads();
+        for (int shift = 24; shift >= 0; shift -= 8) {
+            for (int e = threadIdx.x; e < 256; e += blockDim.x) h256[e] = 0;
+            __syncthreads();
+            const uint32_t pfx = s_pfx;
+            for (uint32_t e = threadIdx.x; e < n_eq; e += blockDim.x) {
+                const uint32_t pos = teq[e];
+                if (shift < 24 && (pos >> (shift + 8)) != (pfx >> (shift + 8))) continue;
+                atomicAdd(&h256[(pos >> shift) & 255u], 1u);
+            }
+            __syncthreads();
+            if (threadIdx.x < 32) {   // warp-parallel scan of the 256 digit counts
+                uint32_t v[8], loc = 0;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) { v[i] = h256[threadIdx.x * 8 + i]; loc += v[i]; }
+                uint32_t inc = loc;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(NR_FULL, inc, o);
+                    if (threadIdx.x >= o) inc += y;
+                }
+                const uint32_t k = s_kth;
+                uint32_t ex = inc - loc;
+                if (ex < k && inc >= k) {
+                    for (int i = 0; i < 8; ++i) {
+                        if (ex + v[i] >= k) {
+                            s_pfx = pfx | ((uint32_t)(threadIdx.x * 8 + i) << shift);
+                            s_kth = k - ex;
+                            break;
+                        }
+                        ex += v[i];
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) s_out = 0;
+        __syncthreads();
+    }
+    if (!in_smem && need_eq < n_eq) {
         for (int shift = 24; shift >= 0; shift -= 8) {
             for (int e = threadIdx.x; e < 256; e += blockDim.x) h256[e] = 0;
             __syncthreads();
@@ -409,7 +531,7 @@ __global__ void __launch_bounds__(1024) k7_select(
             }
             __syncthreads();
         }
-    } else if (threadIdx.x == 0) {
+    } else if (!in_smem && threadIdx.x == 0) {
         s_pfx = 0xffffffffu;
     }
     __syncthreads();
@@ -431,9 +553,10 @@ void launch_select(const nrlsh_index *ix, int Qb, int64_t Tq, const unsigned lon
                    const uint32_t *cnt, int64_t C, int32_t *cand, uint16_t *cand_rank,
                    cudaStream_t s) {
     const int NR = ix->m * (ix->L + 1);
-    const size_t sm = (size_t)NR * 4;
+    const int tie_cap = std::max(NR, 16384);
+    const size_t sm = (size_t)tie_cap * 4;
     cudaFuncSetAttribute(k7_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k7_select<<<Qb, 1024, sm, s>>>(buf, cnt, C, Tq, NR, ix->perm, cand, cand_rank);
+    k7_select<<<Qb, 1024, sm, s>>>(buf, cnt, C, Tq, NR, tie_cap, ix->perm, cand, cand_rank);
     note_launch();
 }
 
