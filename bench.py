@@ -221,6 +221,28 @@ def cpu_oracle_step(cfg, X, Q, L, m, T, k, nq_full, nsample, threads):
 
 
 # ----------------------------------------------------------------- main arms
+def max_over_ranks(x, dist, device=None):
+    """Max of a per-rank float over all ranks (identity without torch.distributed)."""
+    if dist is None:
+        return float(x)
+    import torch
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def whole_job_rate(units_per_rank, world, ms_max):
+    """Weak scaling: every rank answers its own `units_per_rank` queries; the job
+    rate is all ranks' units over the slowest rank's time."""
+    return world * units_per_rank / (ms_max / 1e3)
+
+
+def rank_queries(cfg, nq, rank):
+    """Rank r's query shard: an independent seeded stream (queries are independent
+    units, so the index is replicated and nothing is exchanged on the data path)."""
+    return workloads.make_queries(cfg, nq=nq, shard=rank)
+
+
 def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -295,7 +317,7 @@ def run_native(args):
     cfg, L, m, nq, T, desc = workload(args)
     t_gen = time.perf_counter()
     X = workloads.make_items(cfg)
-    Q = workloads.make_queries(cfg, nq=nq, shard=rank)
+    Q = rank_queries(cfg, nq, rank)
     t_gen = time.perf_counter() - t_gen
     Xd = torch.from_numpy(X).to(dev)
     Qd = torch.from_numpy(Q).to(dev)
@@ -345,11 +367,8 @@ def run_native(args):
     prof = P.profile_read(reset=True)
     ms = [a.elapsed_time(b) for a, b in evs]
     ms_step = float(np.mean(ms))
-    if dist:
-        t = torch.tensor([ms_step], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_step = float(t.item())
-    value = world * nq / (ms_step / 1e3)
+    ms_step = max_over_ranks(ms_step, dist, dev)
+    value = whole_job_rate(nq, world, ms_step)
 
     ids_h = ids.cpu().numpy()
     gid_h = gid.cpu().numpy()
@@ -376,11 +395,8 @@ def run_native(args):
             torch.cuda.synchronize()
             e2e_ms.append((time.perf_counter() - t0) * 1e3)
         e2 = float(np.mean(e2e_ms))
-        if dist:
-            t = torch.tensor([e2], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2 = float(t.item())
-        e2e = {"value": world * nq / (e2 / 1e3), "unit": "queries/s",
+        e2 = max_over_ranks(e2, dist, dev)
+        e2e = {"value": whole_job_rate(nq, world, e2), "unit": "queries/s",
                "h2d_bytes_per_step": int(X.nbytes + 2 * Q.nbytes),
                "d2h_bytes_per_step": int(2 * (oid.numel() * 8 + osc.numel() * 4)),
                "ms_per_step": e2}

@@ -136,7 +136,8 @@ void free_index(nrlsh_index *ix) {
     if (!ix) return;
     void *ps[] = {ix->X_owned, ix->norm2, ix->perm, ix->pos_of_id, ix->part_of_id,
                   ix->part_of_pos, ix->offsets_d, ix->V_d, ix->codes, ix->A, ix->Apad,
-                  ix->R_d, ix->chunks_d, ix->order_d, ix->samp_codes, ix->samp_part};
+                  ix->R_d, ix->chunks_d, ix->order_d, ix->samp_codes, ix->samp_part,
+                  ix->tiles_d};
     // pool-backed (cudaMallocAsync at build); the index may have been used on any stream
     cudaDeviceSynchronize();
     for (void *p : ps)
@@ -333,16 +334,24 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
         for (int64_t p = ix->offsets[j]; p < ix->offsets[j + 1]; p += CH)
             chunks.push_back(make_int4(j, (int)p, (int)std::min<int64_t>(p + CH, ix->offsets[j + 1]), 0));
     ix->nchunks = (int32_t)chunks.size();
+    // tensor-core scan tiles: <= 256 consecutive positions inside one sub-dataset
+    std::vector<int4> tiles;
+    for (int j = 0; j < m; ++j)
+        for (int64_t p = ix->offsets[j]; p < ix->offsets[j + 1]; p += 256)
+            tiles.push_back(make_int4(j, (int)p, (int)std::min<int64_t>(p + 256, ix->offsets[j + 1]), 0));
+    ix->ntiles = (int32_t)tiles.size();
     NR_ALLOC(ix->A, ix->A_h.size() * 4);
     NR_ALLOC(ix->Apad, Apad.size() * 4);
     NR_ALLOC(ix->R_d, ix->R_h.size() * 2);
     NR_ALLOC(ix->order_d, order.size() * 4);
     NR_ALLOC(ix->chunks_d, chunks.size() * sizeof(int4));
+    NR_ALLOC(ix->tiles_d, tiles.size() * sizeof(int4));
     cudaMemcpyAsync(ix->A, ix->A_h.data(), ix->A_h.size() * 4, cudaMemcpyHostToDevice, s);
     cudaMemcpyAsync(ix->Apad, Apad.data(), Apad.size() * 4, cudaMemcpyHostToDevice, s);
     cudaMemcpyAsync(ix->R_d, ix->R_h.data(), ix->R_h.size() * 2, cudaMemcpyHostToDevice, s);
     cudaMemcpyAsync(ix->order_d, order.data(), order.size() * 4, cudaMemcpyHostToDevice, s);
     cudaMemcpyAsync(ix->chunks_d, chunks.data(), chunks.size() * sizeof(int4), cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(ix->tiles_d, tiles.data(), tiles.size() * sizeof(int4), cudaMemcpyHostToDevice, s);
 
     // K3: codes
     {
@@ -396,8 +405,9 @@ int64_t buffer_capacity(int64_t Tq, int stride, int64_t n) {
 // The candidate pipeline for one sub-batch; leaves cand [Qb x Tq] (item ids).
 void run_candidates(const nrlsh_index *ix, const float *Qd, const uint32_t *qcodes_in, int Qb,
                     int64_t qbase, int64_t Tq, int stride, int64_t C, uint32_t *qcodes,
-                    int8_t *delta, uint32_t *cnt, unsigned long long *buf, int32_t *cand,
-                    uint16_t *cand_rank, int *flags, unsigned long long *pairs, cudaStream_t s) {
+                    int8_t *delta, uint32_t *cnt, uint32_t *cntv, uint8_t *blk_act,
+                    unsigned long long *buf, int32_t *cand, uint16_t *cand_rank, int *flags,
+                    unsigned long long *pairs, cudaStream_t s) {
     if (qcodes_in) {
         cudaMemcpyAsync(qcodes, qcodes_in + qbase * ix->W, (size_t)Qb * ix->W * 4,
                         cudaMemcpyDeviceToDevice, s);
@@ -411,13 +421,19 @@ void run_candidates(const nrlsh_index *ix, const float *Qd, const uint32_t *qcod
     }
     if (getenv("NRLSH_TEST_FORCE_FALLBACK"))   // test switch: empty pilot bound -> fallback
         cudaMemsetAsync(delta, 0xff, (size_t)Qb * ix->m, s);
+    const bool tc = scan_tc_supported(ix);
     {
         ProfScope p(SLOT_SCAN, s);
-        launch_scan(ix, qcodes, delta, Qb, buf, cnt, C, pairs, s);
+        if (tc) {
+            cudaMemsetAsync(cntv, 0, (size_t)Qb * 4, s);
+            launch_scan_tc(ix, qcodes, delta, Qb, blk_act, buf, cnt, cntv, C, pairs, s);
+        } else {
+            launch_scan(ix, qcodes, delta, Qb, buf, cnt, C, pairs, s);
+        }
     }
     {
         ProfScope p(SLOT_FALLBACK, s);
-        launch_fallback(ix, qcodes, Qb, Tq, buf, cnt, C, flags, s);
+        launch_fallback(ix, qcodes, Qb, Tq, buf, cnt, tc ? cntv : cnt, C, flags, s);
     }
     {
         ProfScope p(SLOT_SELECT, s);
@@ -477,9 +493,10 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
         if ((e = oc.init(cand_out, (size_t)nq * Tq * 4, s))) return cuda_fail(e, "cand_ids");
         if (rank_out && (e = orr.init(rank_out, (size_t)nq * Tq * 2, s))) return cuda_fail(e, "cand_rank");
     }
-    DBuf qc, dl, cn, bf, cd, pt, fl;
+    DBuf qc, dl, cn, cv, ba, bf, cd, pt, fl;
     if (qc.alloc((size_t)Qmax * ix->W * 4, s) || dl.alloc((size_t)Qmax * ix->m, s) ||
-        cn.alloc((size_t)Qmax * 4, s) || bf.alloc((size_t)Qmax * C * 8, s) ||
+        cn.alloc((size_t)Qmax * 4, s) || cv.alloc((size_t)Qmax * 4, s) ||
+        ba.alloc((size_t)((Qmax + 127) / 128) * ix->m, s) || bf.alloc((size_t)Qmax * C * 8, s) ||
         cd.alloc((size_t)Qmax * Tq * 4, s) ||
         pt.alloc(want_topk ? rerank_partial_bytes(Qmax, Tq, k) : 0, s) || fl.alloc(32, s))
         return fail(NRLSH_ENOMEM, "query workspace");
@@ -494,7 +511,8 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
         uint16_t *crank = (cand_out && rank_out) ? (uint16_t *)orr.dev + q0 * Tq : nullptr;
         run_candidates(ix, Qd, qcodes_user ? (const uint32_t *)QCs.dev : nullptr, Qb, q0, Tq,
                        stride, C, qc.get<uint32_t>(), dl.get<int8_t>(), cn.get<uint32_t>(),
-                       bf.get<unsigned long long>(), cand, crank, fl.get<int>(), pairs, s);
+                       cv.get<uint32_t>(), ba.get<uint8_t>(), bf.get<unsigned long long>(), cand,
+                       crank, fl.get<int>(), pairs, s);
         if (want_topk) {
             ProfScope p(SLOT_RERANK, s);
             launch_rerank(ix->X, ix->d, Qd, Qb, cand, Tq, Tq, nullptr, 1, k,

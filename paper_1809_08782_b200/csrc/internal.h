@@ -36,6 +36,8 @@ struct nrlsh_index {
     float *Apad = nullptr;          // [(d+1) x 32W], zero columns >= L
     uint16_t *R_d = nullptr;        // [m x (L+1)]
     int4 *chunks_d = nullptr;       // scan work units (j, pos0, pos1, 0)
+    int4 *tiles_d = nullptr;        // tensor-core scan tiles: <= 256 positions of one j
+    int32_t ntiles = 0;
     int32_t *order_d = nullptr;     // [m*(L+1)] structure position -> j*(L+1)+h
     int32_t nchunks = 0;
     uint32_t *samp_codes = nullptr; // pilot sample: codes of positions t * stride (compacted)
@@ -115,9 +117,15 @@ void launch_pilot(const nrlsh_index *ix, const uint32_t *qcodes, int Qb, int64_t
 void launch_scan(const nrlsh_index *ix, const uint32_t *qcodes, const int8_t *delta, int Qb,
                  unsigned long long *buf, uint32_t *cnt, int64_t C,
                  unsigned long long *pairs, cudaStream_t s);
+// cntv: entries of the buffer that are real (the tensor-core scan pads append
+// chunks with ~0 sentinels); == cnt for the popcount scan
 void launch_fallback(const nrlsh_index *ix, const uint32_t *qcodes, int Qb, int64_t Tq,
-                     unsigned long long *buf, uint32_t *cnt, int64_t C, int *flags,
-                     cudaStream_t s);
+                     unsigned long long *buf, uint32_t *cnt, const uint32_t *cntv, int64_t C,
+                     int *flags, cudaStream_t s);
+bool scan_tc_supported(const nrlsh_index *ix);
+void launch_scan_tc(const nrlsh_index *ix, const uint32_t *qcodes, const int8_t *delta, int Qb,
+                    uint8_t *blk_act, unsigned long long *buf, uint32_t *cnt, uint32_t *cntv,
+                    int64_t C, unsigned long long *pairs, cudaStream_t s);
 void launch_select(const nrlsh_index *ix, int Qb, int64_t Tq, const unsigned long long *buf,
                    const uint32_t *cnt, int64_t C, int32_t *cand, uint16_t *cand_rank,
                    cudaStream_t s);

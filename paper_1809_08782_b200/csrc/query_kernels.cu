@@ -230,7 +230,6 @@ __global__ void __launch_bounds__(kScanThreads) k6_scan(
     uint32_t *__restrict__ cnt, int64_t C, unsigned long long *__restrict__ pairs) {
     __shared__ uint32_t sq[kQG][W];
     __shared__ int sd[kQG];
-    __shared__ uint32_t sR[129];
     __shared__ unsigned long long sbuf[kQG][kSB];
     __shared__ uint32_t scnt[kQG];
     __shared__ uint32_t sbase[kQG];
@@ -261,7 +260,6 @@ __global__ void __launch_bounds__(kScanThreads) k6_scan(
         }
         if (threadIdx.x == 0) s_nact = base;
     }
-    for (int h = threadIdx.x; h <= L; h += blockDim.x) sR[h] = R[j * (L + 1) + h];
     __syncthreads();
     const int nact = s_nact;
     if (nact == 0) return;
@@ -306,7 +304,9 @@ __global__ void __launch_bounds__(kScanThreads) k6_scan(
             if (pass[u]) {
                 const uint32_t slot = base + __popc(bal & lt);
                 const uint32_t p = p0 + threadIdx.x + kScanThreads * u;
-                const unsigned long long e = ((unsigned long long)sR[h[u]] << 32) | p;
+                // entry: (flat (j, h) index of the sorted structure << 32) | position;
+                // select maps it to the structure position R[j][h]
+                const unsigned long long e = ((unsigned long long)(j * (L + 1) + h[u]) << 32) | p;
                 if (slot < kSB) {
                     sbuf[qq][slot] = e;
                 } else {   // stage full: direct global append (rare)
@@ -356,14 +356,15 @@ __global__ void __launch_bounds__(1024) k6_fallback(
     const uint32_t *__restrict__ codes, const uint8_t *__restrict__ part_of_pos, int64_t n,
     const uint32_t *__restrict__ qcodes, int L, int m, const int32_t *__restrict__ order,
     const uint16_t *__restrict__ R, int64_t Tq, unsigned long long *__restrict__ buf,
-    uint32_t *__restrict__ cnt, int64_t C, int *__restrict__ flags) {
+    uint32_t *__restrict__ cnt, const uint32_t *__restrict__ cntv, int64_t C,
+    int *__restrict__ flags) {
     extern __shared__ uint32_t hist[];
     __shared__ uint32_t ws[32];
     __shared__ int sB;
     __shared__ uint32_t sLt, s_out, s_eq;
     const int q = blockIdx.x;
-    const uint32_t c0 = cnt[q];
-    if (c0 >= (uint64_t)Tq && c0 <= (uint64_t)C) return;
+    const uint32_t c0 = cnt[q], cv = cntv[q];
+    if (cv >= (uint64_t)Tq && c0 <= (uint64_t)C) return;
     if (threadIdx.x == 0) atomicAdd(&flags[2], 1);
     const int NR = m * (L + 1);
     uint32_t qc[W];
@@ -377,19 +378,19 @@ __global__ void __launch_bounds__(1024) k6_fallback(
     __syncthreads();
     for (int64_t base = 0; base < n; base += blockDim.x) {
         const int64_t p = base + threadIdx.x;
-        int r = NR;
+        int r = NR, f = 0;
         if (p < n) {
             uint32_t c[W];
             load_code<W>(codes, p, c);
-            const int h = hamming<W>(c, qc);
-            r = R[part_of_pos[p] * (L + 1) + h];
+            f = part_of_pos[p] * (L + 1) + hamming<W>(c, qc);
+            r = R[f];
         }
         const uint32_t lt = r < B, eq = r == B;
         uint32_t tot_eq, tot_take;
         const uint32_t eq_rank = block_excl_scan(eq, ws, &tot_eq) + s_eq;
         const uint32_t take = lt || (eq && eq_rank < need_eq);
         const uint32_t slot = block_excl_scan(take, ws, &tot_take) + s_out;
-        if (take) buf[(int64_t)q * C + slot] = ((unsigned long long)r << 32) | (uint32_t)p;
+        if (take) buf[(int64_t)q * C + slot] = ((unsigned long long)f << 32) | (uint32_t)p;
         __syncthreads();
         if (threadIdx.x == 0) { s_out += tot_take; s_eq += tot_eq; }
         __syncthreads();
@@ -398,23 +399,23 @@ __global__ void __launch_bounds__(1024) k6_fallback(
 }
 
 void launch_fallback(const nrlsh_index *ix, const uint32_t *qcodes, int Qb, int64_t Tq,
-                     unsigned long long *buf, uint32_t *cnt, int64_t C, int *flags,
-                     cudaStream_t s) {
+                     unsigned long long *buf, uint32_t *cnt, const uint32_t *cntv, int64_t C,
+                     int *flags, cudaStream_t s) {
     const int NR = ix->m * (ix->L + 1);
     const size_t sm = (size_t)NR * 4;
     const int32_t *order = ix->order_d;
     switch (ix->W) {
         case 1:
             cudaFuncSetAttribute(k6_fallback<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            k6_fallback<1><<<Qb, 1024, sm, s>>>(ix->codes, ix->part_of_pos, ix->n, qcodes, ix->L, ix->m, order, ix->R_d, Tq, buf, cnt, C, flags);
+            k6_fallback<1><<<Qb, 1024, sm, s>>>(ix->codes, ix->part_of_pos, ix->n, qcodes, ix->L, ix->m, order, ix->R_d, Tq, buf, cnt, cntv, C, flags);
             break;
         case 2:
             cudaFuncSetAttribute(k6_fallback<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            k6_fallback<2><<<Qb, 1024, sm, s>>>(ix->codes, ix->part_of_pos, ix->n, qcodes, ix->L, ix->m, order, ix->R_d, Tq, buf, cnt, C, flags);
+            k6_fallback<2><<<Qb, 1024, sm, s>>>(ix->codes, ix->part_of_pos, ix->n, qcodes, ix->L, ix->m, order, ix->R_d, Tq, buf, cnt, cntv, C, flags);
             break;
         default:
             cudaFuncSetAttribute(k6_fallback<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            k6_fallback<4><<<Qb, 1024, sm, s>>>(ix->codes, ix->part_of_pos, ix->n, qcodes, ix->L, ix->m, order, ix->R_d, Tq, buf, cnt, C, flags);
+            k6_fallback<4><<<Qb, 1024, sm, s>>>(ix->codes, ix->part_of_pos, ix->n, qcodes, ix->L, ix->m, order, ix->R_d, Tq, buf, cnt, cntv, C, flags);
             break;
     }
     note_launch();
@@ -423,9 +424,11 @@ void launch_fallback(const nrlsh_index *ix, const uint32_t *qcodes, int Qb, int6
 // =========================================================================== K7 select
 __global__ void __launch_bounds__(1024) k7_select(
     const unsigned long long *__restrict__ buf, const uint32_t *__restrict__ cnt, int64_t C,
-    int64_t Tq, int NR, int tie_cap, const int32_t *__restrict__ perm,
-    int32_t *__restrict__ cand, uint16_t *__restrict__ cand_rank) {
-    extern __shared__ uint32_t hist[];   // [max(NR, tie_cap)]
+    int64_t Tq, int NR, int tie_cap, const uint16_t *__restrict__ R,
+    const int32_t *__restrict__ perm, int32_t *__restrict__ cand,
+    uint16_t *__restrict__ cand_rank) {
+    extern __shared__ uint32_t hist[];   // [max(NR, tie_cap)] + R copy [NR] (uint16)
+    uint16_t *sRt = reinterpret_cast<uint16_t *>(hist + tie_cap);
     __shared__ uint32_t ws[32];
     __shared__ uint32_t h256[256];
     __shared__ int sB;
@@ -433,10 +436,15 @@ __global__ void __launch_bounds__(1024) k7_select(
     const int q = blockIdx.x;
     const int64_t c = min((int64_t)cnt[q], C);
     const unsigned long long *b = buf + (int64_t)q * C;
-    for (int e = threadIdx.x; e < NR; e += blockDim.x) hist[e] = 0u;
+    for (int e = threadIdx.x; e < NR; e += blockDim.x) { hist[e] = 0u; sRt[e] = R[e]; }
     if (threadIdx.x == 0) { sB = NR - 1; sLt = 0; s_out = 0; }
     __syncthreads();
-    for (int64_t e = threadIdx.x; e < c; e += blockDim.x) atomicAdd(&hist[(uint32_t)(b[e] >> 32)], 1u);
+    // entries carry the flat (j, h) index; R maps it to the structure position
+    // (~0 = unused append slot of the tensor-core scan)
+    for (int64_t e = threadIdx.x; e < c; e += blockDim.x) {
+        const uint32_t f = (uint32_t)(b[e] >> 32);
+        if (f < (uint32_t)NR) atomicAdd(&hist[sRt[f]], 1u);
+    }
     __syncthreads();
     const uint32_t need = (uint32_t)Tq;
     {
@@ -468,7 +476,8 @@ __global__ void __launch_bounds__(1024) k7_select(
     if (in_smem) {
         for (int64_t e = threadIdx.x; e < c; e += blockDim.x) {
             const unsigned long long v = b[e];
-            if ((uint32_t)(v >> 32) == B) teq[atomicAdd(&s_out, 1u)] = (uint32_t)v;
+            const uint32_t f = (uint32_t)(v >> 32);
+            if (f < (uint32_t)NR && sRt[f] == B) teq[atomicAdd(&s_out, 1u)] = (uint32_t)v;
         }
         __syncthreads();
         for (int shift = 24; shift >= 0; shift -= 8) {
@@ -516,7 +525,8 @@ __global__ void __launch_bounds__(1024) k7_select(
             const uint32_t pfx = s_pfx;
             for (int64_t e = threadIdx.x; e < c; e += blockDim.x) {
                 const unsigned long long v = b[e];
-                if ((uint32_t)(v >> 32) != B) continue;
+                const uint32_t f = (uint32_t)(v >> 32);
+                if (f >= (uint32_t)NR || sRt[f] != B) continue;
                 const uint32_t pos = (uint32_t)v;
                 if (shift < 24 && (pos >> (shift + 8)) != (pfx >> (shift + 8))) continue;
                 atomicAdd(&h256[(pos >> shift) & 255u], 1u);
@@ -538,7 +548,9 @@ __global__ void __launch_bounds__(1024) k7_select(
     const uint32_t pk = s_pfx;
     for (int64_t e = threadIdx.x; e < c; e += blockDim.x) {
         const unsigned long long v = b[e];
-        const uint32_t r = (uint32_t)(v >> 32), pos = (uint32_t)v;
+        const uint32_t f = (uint32_t)(v >> 32), pos = (uint32_t)v;
+        if (f >= (uint32_t)NR) continue;
+        const uint32_t r = sRt[f];
         if (r < B || (r == B && pos <= pk)) {
             const uint32_t slot = atomicAdd(&s_out, 1u);
             if (slot < need) {
@@ -554,9 +566,9 @@ void launch_select(const nrlsh_index *ix, int Qb, int64_t Tq, const unsigned lon
                    cudaStream_t s) {
     const int NR = ix->m * (ix->L + 1);
     const int tie_cap = std::max(NR, 16384);
-    const size_t sm = (size_t)tie_cap * 4;
+    const size_t sm = (size_t)tie_cap * 4 + (size_t)NR * 2;
     cudaFuncSetAttribute(k7_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k7_select<<<Qb, 1024, sm, s>>>(buf, cnt, C, Tq, NR, tie_cap, ix->perm, cand, cand_rank);
+    k7_select<<<Qb, 1024, sm, s>>>(buf, cnt, C, Tq, NR, tie_cap, ix->R_d, ix->perm, cand, cand_rank);
     note_launch();
 }
 

@@ -141,6 +141,17 @@ __device__ __forceinline__ void mma_tf32_warp(uint32_t d_tmem, uint64_t a_desc, 
         "}\n" ::"r"(d_tmem),
         "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
+__device__ __forceinline__ void mma_i8_warp(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                            uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p, e;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
 __device__ __forceinline__ void mma_commit_warp(uint64_t *bar) {
     asm volatile(
         "{\n"
@@ -195,6 +206,11 @@ __host__ __device__ constexpr uint32_t umma_idesc(uint32_t ab_format, uint32_t M
            | (ab_format << 10)       // B format
            | ((N >> 3) << 17)        // N / 8
            | ((M >> 4) << 24);       // M / 16
+}
+
+// kind::i8: signed 8-bit A and B (format 1 = S8), S32 accumulator (D format 2).
+__host__ __device__ constexpr uint32_t umma_idesc_i8(uint32_t M, uint32_t N) {
+    return (2u << 4) | (1u << 7) | (1u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
 }
 
 }  // namespace tc

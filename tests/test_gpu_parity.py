@@ -439,3 +439,27 @@ def test_full_size_sampled(name, L, m):
     for qi in range(3):
         a, s = oracle.exact_topk(X, Q[qi], cfg.k)
         assert_topk_match(gt_ids[qi], gt_sc[qi], a, s, X, Q[qi])
+
+
+@pytest.mark.parametrize("case", [("c4", 300_000, 32, 64, 128), ("scale", 70_000, 16, 128, 256),
+                                  ("tiny", None, None, 32, 8)], ids=_ids)
+def test_candidates_parity_tensor_core_scan(built, case, monkeypatch):
+    """The opt-in tcgen05 int8 Hamming scan (scan_tc.cu) gives the same candidate
+    sets, ranks and (R, id) order as the oracle (identical codes injected)."""
+    monkeypatch.setenv("NRLSH_SCAN_TC", "1")
+    cfg, X, Q, Xd, idx, orc = built(*case)
+    n = X.shape[0]
+    ocodes = orc.codes()
+    idx.set_codes(ocodes[orc.perm])
+    qc = oracle.query_codes(Q, orc.A)
+    nq = min(len(Q), 16)
+    qcd = torch.from_numpy(qc[:nq].view(np.int32)).cuda()
+    for T in _budgets(cfg, n):
+        gid, grk = idx.candidates(T, qcodes=qcd)
+        gid = gid.cpu().numpy()
+        grk = grk.cpu().numpy().view(np.uint16)
+        for qi in range(nq):
+            oid, ork = oracle.candidates(ocodes, orc.part, qc[qi], orc.R, T)
+            order = np.lexsort((gid[qi], grk[qi]))
+            assert np.array_equal(gid[qi][order], oid), (T, qi)
+            assert np.array_equal(grk[qi][order], ork), (T, qi)

@@ -32,13 +32,17 @@ __global__ void __launch_bounds__(128, 1) mma_loop(int N, int kind, int iters, i
     const uint32_t tbase = slot;
     if (warpwide && warp == 1) {
         const uint32_t idesc = tc::umma_idesc(kind == 0 ? 1 : 2, 128, N);
+        const uint32_t idesc_i8 = tc::umma_idesc_i8(128, N);
         const uint32_t a = tc::smem_u32(A), b = tc::smem_u32(B);
         uint32_t ph = 0;
         const long long t0 = clock64();
         for (int it = 0; it < iters; ++it) {
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {
-                if (kind == 0)
+                if (kind == 2)
+                    tc::mma_i8_warp(tbase + (it & 1) * 256, tc::umma_desc_sw128(a + kk * 32),
+                                    tc::umma_desc_sw128(b + kk * 32), idesc_i8, 1);
+                else if (kind == 0)
                     tc::mma_f16_warp(tbase + (it & 1) * 256, tc::umma_desc_sw128(a + kk * 32),
                                      tc::umma_desc_sw128(b + kk * 32), idesc, 1);
                 else
@@ -123,8 +127,8 @@ int main(int argc, char **argv) {
     const int smem = 16384 + 32768 + 1024;
     cudaFuncSetAttribute(mma_loop, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const int iters = 20000;
-    for (int ww = 0; ww < 2; ++ww)
-    for (int kind = 0; kind < 2; ++kind)
+    for (int ww = 1; ww < 2; ++ww)
+    for (int kind = 0; kind < 3; ++kind)
         for (int N : {64, 128, 256})
             for (int se : {0, 1, 4}) {
                 mma_loop<<<sms, 128, smem>>>(N, kind, iters, se, ww, cyc);
@@ -140,10 +144,10 @@ int main(int argc, char **argv) {
                 cudaEventElapsedTime(&ms, e0, e1);
                 unsigned long long h[1];
                 cudaMemcpy(h, cyc, 8, cudaMemcpyDeviceToHost);
-                const double k_per = kind == 0 ? 16 : 8;
+                const double k_per = kind == 0 ? 16 : (kind == 2 ? 32 : 8);
                 const double macs = 128.0 * N * k_per * 4 * iters;
                 printf("%s %s N=%3d sync_every=%d: %.1f cyc/MMA, %.0f MAC/clk/SM, %.1f TFLOP/s chip (%s)\n",
-                       ww ? "warp  " : "thread", kind == 0 ? "bf16" : "tf32", N, se, (double)h[0] / (4.0 * iters),
+                       ww ? "warp  " : "thread", kind == 0 ? "bf16" : (kind == 2 ? "i8  " : "tf32"), N, se, (double)h[0] / (4.0 * iters),
                        macs / (double)h[0], 2.0 * macs * sms / (ms * 1e-3) / 1e12,
                        cudaGetErrorString(err));
             }
