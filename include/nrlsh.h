@@ -154,6 +154,11 @@ nrlsh_status nrlsh_query_candidates(const nrlsh_index *index, const float *queri
 nrlsh_status nrlsh_last_query_stats(int64_t *fallback_queries, int64_t *kernel_launches,
                                     int64_t *scanned_pairs);
 
+/* Candidates of the last nrlsh_query on this thread that the re-rank rescored in
+   fp32 after its certified bf16 pass (the others provably could not enter the
+   top-k; the answer is the same as rescoring all of them). */
+nrlsh_status nrlsh_last_rerank_stats(int64_t *rescored_fp32);
+
 /* Exact top-k (as nrlsh_exact_topk) against the index's own items (device copy
    or borrowed pointer), so host-buffer callers do not re-stage the items. */
 nrlsh_status nrlsh_index_exact_topk(const nrlsh_index *index, const float *queries, int64_t nq,

@@ -24,7 +24,7 @@ EXPORTS = [
     "nrlsh_get_projection", "nrlsh_get_rank_table", "nrlsh_get_codes", "nrlsh_set_codes",
     "nrlsh_query_codes", "nrlsh_query_candidates", "nrlsh_last_query_stats",
     "nrlsh_index_exact_topk", "nrlsh_exact_topk_seeded", "nrlsh_index_exact_topk_seeded",
-    "nrlsh_profile_enable", "nrlsh_profile_read",
+    "nrlsh_last_rerank_stats", "nrlsh_profile_enable", "nrlsh_profile_read",
     "nrlsh_profile_slot_name", "nrlsh_launch_count", "nrlsh_last_exact_stats",
 ]
 
@@ -98,6 +98,8 @@ def lib():
         L.nrlsh_profile_read.restype = C.c_int
         L.nrlsh_profile_slot_name.argtypes = [i32]
         L.nrlsh_profile_slot_name.restype = C.c_char_p
+        L.nrlsh_last_rerank_stats.argtypes = [p]
+        L.nrlsh_last_rerank_stats.restype = st
         L.nrlsh_last_exact_stats.argtypes = [p, p, p]
         L.nrlsh_last_exact_stats.restype = st
         L.nrlsh_launch_count.argtypes = []
@@ -277,6 +279,12 @@ def exact_topk(items, queries, k, out_ids=None, out_scores=None, stream=None, se
                                              _ptr(seed_ids), int(seed_ids.shape[1]), _ptr(out_ids),
                                              _ptr(out_scores), _stream(stream)))
     return out_ids, out_scores
+
+
+def last_rerank_stats():
+    a = C.c_int64()
+    _check(lib().nrlsh_last_rerank_stats(C.byref(a)))
+    return {"rescored_fp32": a.value}
 
 
 def last_query_stats():

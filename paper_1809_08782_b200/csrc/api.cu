@@ -21,6 +21,7 @@ thread_local std::string g_last_error;
 thread_local int64_t g_last_fallbacks = 0;
 thread_local int64_t g_last_launches = 0;
 thread_local int64_t g_last_pairs = 0;
+thread_local int64_t g_last_rescored = 0;
 thread_local int64_t g_last_gt_max_cand = 0, g_last_gt_sum_cand = 0, g_last_gt_overflow = 0;
 
 nrlsh_status fail(nrlsh_status st, const std::string &msg) {
@@ -134,7 +135,7 @@ int words_for(int L) { return L <= 32 ? 1 : (L <= 64 ? 2 : 4); }
 
 void free_index(nrlsh_index *ix) {
     if (!ix) return;
-    void *ps[] = {ix->X_owned, ix->norm2, ix->perm, ix->pos_of_id, ix->part_of_id,
+    void *ps[] = {ix->X_owned, ix->Xpad, ix->Xb, ix->xnorm, ix->norm2, ix->perm, ix->pos_of_id, ix->part_of_id,
                   ix->part_of_pos, ix->offsets_d, ix->V_d, ix->codes, ix->A, ix->Apad,
                   ix->R_d, ix->chunks_d, ix->order_d, ix->samp_codes, ix->samp_part,
                   ix->tiles_d};
@@ -272,6 +273,18 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
         ix->X = ix->X_owned;
     }
     NR_ALLOC(ix->norm2, (size_t)n * 8);
+    // bf16 rows (16-byte aligned, zero-padded to dpb) and |x| rounded up, written by the
+    // norms pass: the ground truth's tensor-core operand and the re-rank's certified
+    // filter pass (half the bytes of the fp32 rows it then gathers only for survivors)
+    // rows of d % 4 != 0 floats are only 4- or 8-byte aligned: a 16-byte-aligned padded
+    // fp32 copy (written by the codes pass) lets the re-rank gather with 16-byte loads
+    ix->dpad = (d + 3) / 4 * 4;
+    if (ix->dpad != d && !getenv("NRLSH_NO_XPAD")) NR_ALLOC(ix->Xpad, (size_t)n * ix->dpad * 4);
+    ix->dpb = (d + 7) / 8 * 8;
+    const int64_t npad = (n + 255) / 256 * 256;
+    NR_ALLOC(ix->Xb, (size_t)n * ix->dpb * 2);
+    NR_ALLOC(ix->xnorm, (size_t)npad * 4);
+    cudaMemsetAsync(ix->xnorm + n, 0, (size_t)(npad - n) * 4, s);
     NR_ALLOC(ix->perm, (size_t)n * 4);
     NR_ALLOC(ix->pos_of_id, (size_t)n * 4);
     NR_ALLOC(ix->part_of_id, (size_t)n);
@@ -286,7 +299,8 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
     cudaMemsetAsync(bad.p, 0xff, 8, s);
     {
         ProfScope p(SLOT_NORMS, s);
-        launch_norms(ix->X, n, d, ix->norm2, bad.get<unsigned long long>(), s);
+        launch_norms(ix->X, n, d, ix->norm2, bad.get<unsigned long long>(), ix->Xb, ix->dpb,
+                     ix->xnorm, s);
     }
     unsigned long long badidx = 0;
     cudaMemcpyAsync(&badidx, bad.p, 8, cudaMemcpyDeviceToHost, s);
@@ -357,7 +371,8 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
     {
         ProfScope p(SLOT_CODES, s);
         launch_item_codes(ix->X, n, d, ix->norm2, ix->part_of_id, ix->V_d, ix->Apad, L, W,
-                          ix->pos_of_id, ix->codes, s);
+                          ix->pos_of_id, ix->codes, ix->Xb, ix->dpb, ix->xnorm, ix->Xpad,
+                          ix->dpad, s);
     }
     // compacted pilot sample (query-time pilots read it contiguously)
     {
@@ -515,9 +530,17 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
                        crank, fl.get<int>(), pairs, s);
         if (want_topk) {
             ProfScope p(SLOT_RERANK, s);
-            launch_rerank(ix->X, ix->d, Qd, Qb, cand, Tq, Tq, nullptr, 1, k,
-                          pt.get<unsigned long long>(), (int64_t *)oi.dev + q0 * k,
-                          (float *)os.dev + q0 * k, s);
+            if (ix->Xb && getenv("NRLSH_RERANK_BF16"))
+                launch_rerank_bf(ix->Xpad ? ix->Xpad : ix->X, ix->d, ix->Xpad ? ix->dpad : ix->d,
+                                 ix->Xb, ix->dpb, ix->xnorm, Qd, Qb, cand, Tq, Tq,
+                                 nullptr, k, pt.get<unsigned long long>(),
+                                 (int64_t *)oi.dev + q0 * k, (float *)os.dev + q0 * k,
+                                 (unsigned long long *)(fl.get<int>() + 6), s);
+            else
+                launch_rerank(ix->Xpad ? ix->Xpad : ix->X, ix->d, ix->Xpad ? ix->dpad : ix->d, Qd,
+                              Qb, cand, Tq, Tq, nullptr, 1, k,
+                              pt.get<unsigned long long>(), (int64_t *)oi.dev + q0 * k,
+                              (float *)os.dev + q0 * k, s);
         }
     }
     if (want_topk) {
@@ -539,6 +562,8 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
     unsigned long long pr;
     std::memcpy(&pr, hflags + 4, 8);
     g_last_pairs = (int64_t)pr;
+    std::memcpy(&pr, hflags + 6, 8);
+    g_last_rescored = (int64_t)pr;
     return check_flags(hflags);
 }
 
@@ -585,6 +610,11 @@ nrlsh_status nrlsh_query_codes(const nrlsh_index *ix, const float *queries, int6
     return check_flags(hflags);
 }
 
+nrlsh_status nrlsh_last_rerank_stats(int64_t *rescored_fp32) {
+    if (rescored_fp32) *rescored_fp32 = g_last_rescored;
+    return NRLSH_OK;
+}
+
 nrlsh_status nrlsh_last_query_stats(int64_t *fallback_queries, int64_t *kernel_launches,
                                     int64_t *scanned_pairs) {
     if (fallback_queries) *fallback_queries = g_last_fallbacks;
@@ -596,7 +626,8 @@ nrlsh_status nrlsh_last_query_stats(int64_t *fallback_queries, int64_t *kernel_l
 // ------------------------------------------------------------ exact top-k
 static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const float *queries,
                                int64_t nq, int32_t k, const int64_t *seed_ids, int32_t seed_k,
-                               int64_t *out_ids, float *out_scores, void *cuda_stream) {
+                               int64_t *out_ids, float *out_scores, void *cuda_stream,
+                               const void *Xb_ix = nullptr, const float *xnorm_ix = nullptr) {
     if (!items || !queries || !out_ids || !out_scores) return fail(NRLSH_EINVAL, "NULL argument");
     if (seed_ids && (seed_k < 1 || seed_k > 1024))
         return fail(NRLSH_EINVAL, "seed_k must be in [1, 1024]");
@@ -643,13 +674,20 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
         cs.alloc((size_t)Qmax * Cg * 4, s) || th.alloc((size_t)Qmax * 4, s) ||
         pt.alloc(std::max(rerank_partial_bytes(Qmax, Cg, k), rerank_partial_bytes(1, n, k)), s))
         return fail(NRLSH_ENOMEM, "exact_topk workspace");
+    // bf16 item rows and |x|: the index's (written by its build), else prepared here
+    const void *Xbp = Xb_ix;
+    const float *xnp = xnorm_ix;
     if (use_tc) {
-        if (xb.alloc((size_t)n * dp * 2, s) || qb.alloc((size_t)nq * dp * 2, s) ||
+        if ((!Xbp && xb.alloc((size_t)n * dp * 2, s)) || qb.alloc((size_t)nq * dp * 2, s) ||
             hp.alloc(gt_heap_bytes(k), s))
             return fail(NRLSH_ENOMEM, "exact_topk bf16 workspace");
         ProfScope p(SLOT_GT_NORMS, s);
-        cudaMemsetAsync(xn.get<float>() + n, 0, (size_t)(npad - n) * 4, s);
-        launch_bf16_prep(X, n, d, dp, xb.p, xn.get<float>(), s);
+        if (!Xbp) {
+            cudaMemsetAsync(xn.get<float>() + n, 0, (size_t)(npad - n) * 4, s);
+            launch_bf16_prep(X, n, d, dp, xb.p, xn.get<float>(), s);
+            Xbp = xb.p;
+            xnp = xn.get<float>();
+        }
         launch_bf16_prep(Q, nq, d, dp, qb.p, qn.get<float>(), s);
     } else {
         ProfScope p(SLOT_GT_NORMS, s);
@@ -673,8 +711,8 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
                                      th.get<uint32_t>(), s);
             }
             ProfScope p(SLOT_GT_FILTER, s);
-            if (launch_gt_filter_tc(xb.p, n, d, dp, (const uint16_t *)qb.p + q0 * dp, Qb,
-                                    xn.get<float>(), qnb, eps_rel, k, th.get<uint32_t>(),
+            if (launch_gt_filter_tc(Xbp, n, d, dp, (const uint16_t *)qb.p + q0 * dp, Qb,
+                                    xnp, qnb, eps_rel, k, th.get<uint32_t>(),
                                     hp.get<float>(), cd.get<int32_t>(), cc.get<uint32_t>(), Cg, s))
                 return fail(NRLSH_ECUDA, "tensor map encoding failed");
         } else {
@@ -695,7 +733,7 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
         }
         {
             ProfScope p(SLOT_SCORE, s);
-            launch_rerank(X, d, Qb_ptr, Qb, cd.get<int32_t>(), Cg, Cg, cc.get<uint32_t>(), 1, k,
+            launch_rerank(X, d, d, Qb_ptr, Qb, cd.get<int32_t>(), Cg, Cg, cc.get<uint32_t>(), 1, k,
                           pt.get<unsigned long long>(), oid, osc, s);
         }
         // overflowing queries (rare): exact scoring of every item
@@ -706,7 +744,7 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
             g_last_gt_sum_cand += hcnt[qi];
             if (hcnt[qi] <= (uint32_t)Cg) continue;
             ++g_last_gt_overflow;
-            launch_rerank(X, d, Qb_ptr + (int64_t)qi * d, 1, nullptr, n, n, nullptr, 1, k,
+            launch_rerank(X, d, d, Qb_ptr + (int64_t)qi * d, 1, nullptr, n, n, nullptr, 1, k,
                           pt.get<unsigned long long>(), oid + (int64_t)qi * k,
                           osc + (int64_t)qi * k, s);
         }
@@ -747,7 +785,7 @@ nrlsh_status nrlsh_index_exact_topk(const nrlsh_index *ix, const float *queries,
                                     void *cuda_stream) {
     if (!ix) return fail(NRLSH_EINVAL, "index is NULL");
     return exact_impl(ix->X, ix->n, ix->d, queries, nq, k, nullptr, 0, out_ids, out_scores,
-                      cuda_stream);
+                      cuda_stream, ix->Xb, ix->xnorm);
 }
 
 nrlsh_status nrlsh_index_exact_topk_seeded(const nrlsh_index *ix, const float *queries,
@@ -757,7 +795,7 @@ nrlsh_status nrlsh_index_exact_topk_seeded(const nrlsh_index *ix, const float *q
     if (!ix) return fail(NRLSH_EINVAL, "index is NULL");
     if (!seed_ids) return fail(NRLSH_EINVAL, "seed_ids is NULL");
     return exact_impl(ix->X, ix->n, ix->d, queries, nq, k, seed_ids, seed_k, out_ids, out_scores,
-                      cuda_stream);
+                      cuda_stream, ix->Xb, ix->xnorm);
 }
 
 // ------------------------------------------------------------------ hooks

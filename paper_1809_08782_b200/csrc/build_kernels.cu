@@ -15,6 +15,8 @@
 #include <string>
 #include <vector>
 
+#include <cuda_bf16.h>
+
 #include "common.cuh"
 #include "internal.h"
 #include "tc_sm100.cuh"
@@ -80,7 +82,9 @@ __global__ void k1_norms_direct(const float *__restrict__ X, int64_t n, int d,
 // 32 are distinct, and the order of the sum is unchanged.
 __global__ void __launch_bounds__(128) k1_norms_bulk(const float *__restrict__ X, int64_t n, int d,
                                                      int RT, double *__restrict__ norm2,
-                                                     unsigned long long *__restrict__ bad) {
+                                                     unsigned long long *__restrict__ bad,
+                                                     __nv_bfloat16 *__restrict__ Xb, int dpb,
+                                                     float *__restrict__ xnorm) {
     extern __shared__ __align__(128) float nbuf[];       // [2][RT * d]
     __shared__ __align__(8) uint64_t full[2];
     const int64_t ntiles = (n + RT - 1) / RT;
@@ -129,8 +133,12 @@ __global__ void __launch_bounds__(128) k1_norms_bulk(const float *__restrict__ X
             if (r < rows) {
                 norm2[r0 + r] = s;
                 if (!isfinite(s)) atomicMin(bad, (unsigned long long)(r0 + r));
+                // |x| rounded up (with a 2^-50 margin over the fp64 sum's rounding):
+                // an upper bound for the certified bf16 filters
+                if (xnorm) xnorm[r0 + r] = __double2float_ru(sqrt(s) * (1.0 + 0x1p-50));
             }
         }
+
         __syncthreads();                            // stage st fully read
         if (threadIdx.x == 0 && tile + 2 * (int64_t)gridDim.x < ntiles)
             issue(tile + 2 * (int64_t)gridDim.x, st);
@@ -138,7 +146,7 @@ __global__ void __launch_bounds__(128) k1_norms_bulk(const float *__restrict__ X
 }
 
 void launch_norms(const float *X, int64_t n, int d, double *norm2, unsigned long long *bad,
-                  cudaStream_t s) {
+                  void *Xb, int dpb, float *xnorm, cudaStream_t s) {
     const int ld = (d % 2 == 1) ? d : d + 1;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -150,7 +158,7 @@ void launch_norms(const float *X, int64_t n, int d, double *norm2, unsigned long
         const int64_t ntiles = (n + RT - 1) / RT;
         const int per_sm = std::max(1, (int)((227 * 1024) / (sm + 1024)));
         const int grid = (int)std::min<int64_t>(ntiles, (int64_t)sms * per_sm);
-        k1_norms_bulk<<<grid, RT, sm, s>>>(X, n, d, RT, norm2, bad);
+        k1_norms_bulk<<<grid, RT, sm, s>>>(X, n, d, RT, norm2, bad, nullptr, dpb, xnorm);
         note_launch();
         return;
     }
@@ -805,10 +813,19 @@ __global__ void __launch_bounds__(256) k3_codes_simt(
 
 void launch_item_codes(const float *X, int64_t n, int d, const double *norm2,
                        const uint8_t *part, const double *V, const float *Apad, int L, int W,
-                       const int32_t *pos_of_id, uint32_t *codes, cudaStream_t s) {
+                       const int32_t *pos_of_id, uint32_t *codes, void *Xb, int dpb,
+                       float *xnorm, float *Xpad, int dpad, cudaStream_t s) {
     if (codes_tc_supported(d, W)) {
-        launch_item_codes_tc(X, n, d, norm2, part, V, Apad, L, W, pos_of_id, codes, s);
+        launch_item_codes_tc(X, n, d, norm2, part, V, Apad, L, W, pos_of_id, codes, Xb, dpb, Xpad,
+                             dpad, s);
         return;
+    }
+    // SIMT path: the row copies in separate passes
+    if (Xb) launch_bf16_prep(X, n, d, dpb, Xb, xnorm, s);
+    if (Xpad) {
+        cudaMemcpy2DAsync(Xpad, (size_t)dpad * 4, X, (size_t)d * 4, (size_t)d * 4, (size_t)n,
+                          cudaMemcpyDeviceToDevice, s);
+        cudaMemset2DAsync(Xpad + d, (size_t)dpad * 4, 0, (size_t)(dpad - d) * 4, (size_t)n, s);
     }
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);

@@ -23,6 +23,7 @@
 //              scatter the W code words to pos_of_id[i]
 // The projection matrix (B operand, N x K) stays resident in smem.
 #include <cuda.h>
+#include <cuda_bf16.h>
 
 #include <algorithm>
 
@@ -50,6 +51,10 @@ struct CodesArgs {
     const float *Apad;       // [(d+1) x N]
     const int32_t *pos_of_id;
     uint32_t *codes;         // [n x N/32], partition order
+    __nv_bfloat16 *Xb;       // optional bf16 row copy [n x dpb] (the converters have the rows)
+    int dpb;
+    float *Xpad;             // optional fp32 row copy [n x dpad], 16-byte rows (re-rank gathers)
+    int dpad;
 };
 
 __device__ __forceinline__ uint32_t swz(int row, int kbyte) {
@@ -117,6 +122,56 @@ __device__ __forceinline__ void conv_store(uint8_t *stage, int w, int l, const f
     }
 }
 
+
+// bf16 copy of the converter's slice of the rows (columns < dpb; zeros past d)
+template <int VEC>
+__device__ __forceinline__ void conv_store_bf16(const CodesArgs &a, int64_t tile, int kb, int w, int l,
+                                                const float (&v)[16]) {
+    constexpr int lpr = VEC == 4 ? 8 : (VEC == 2 ? 16 : 32);
+    constexpr int rpi = 32 / lpr;
+    constexpr int ni = 16 / rpi;
+    const int col = kb * CT_KB + (l % lpr) * VEC;
+    if (col >= a.dpb) return;
+#pragma unroll
+    for (int j = 0; j < ni; ++j) {
+        const int rr = 16 * w + j * rpi + l / lpr;
+        const int64_t i = tile * CT_M + rr;
+        if (i >= a.n) continue;
+        __nv_bfloat16 *dst = a.Xb + i * a.dpb + col;
+        if (VEC == 4) {
+            const __nv_bfloat162 p0 = __floats2bfloat162_rn(v[j * 4 + 0], v[j * 4 + 1]);
+            const __nv_bfloat162 p1 = __floats2bfloat162_rn(v[j * 4 + 2], v[j * 4 + 3]);
+            uint2 u;
+            u.x = *reinterpret_cast<const uint32_t *>(&p0);
+            u.y = *reinterpret_cast<const uint32_t *>(&p1);
+            *reinterpret_cast<uint2 *>(dst) = u;
+        } else if (VEC == 2) {
+            *reinterpret_cast<__nv_bfloat162 *>(dst) = __floats2bfloat162_rn(v[j * 2], v[j * 2 + 1]);
+        } else {
+            *dst = __float2bfloat16_rn(v[j]);
+        }
+    }
+}
+
+template <int VEC>
+__device__ __forceinline__ void conv_store_pad(const CodesArgs &a, int64_t tile, int kb, int w, int l,
+                                               const float (&v)[16]) {
+    constexpr int lpr = VEC == 4 ? 8 : (VEC == 2 ? 16 : 32);
+    constexpr int rpi = 32 / lpr;
+    constexpr int ni = 16 / rpi;
+    const int col = kb * CT_KB + (l % lpr) * VEC;
+    if (col >= a.dpad) return;
+#pragma unroll
+    for (int j = 0; j < ni; ++j) {
+        const int rr = 16 * w + j * rpi + l / lpr;
+        const int64_t i = tile * CT_M + rr;
+        if (i >= a.n) continue;
+        float *dst = a.Xpad + i * a.dpad + col;
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) dst[e] = v[j * VEC + e];
+    }
+}
+
 template <int VEC>
 __global__ void __launch_bounds__(CT_THREADS, 1) k3_codes_tc(CodesArgs a) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -174,6 +229,8 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k3_codes_tc(CodesArgs a) {
             const uint32_t s = g % a.stages, ph = (g / a.stages) & 1;
             tc::mbar_wait(&empty[s], ph ^ 1);
             conv_store<VEC>(ring + s * CT_STAGE, warp, lane, cur);
+            if (a.Xb) conv_store_bf16<VEC>(a, tile, kb, warp, lane, cur);
+            if (a.Xpad) conv_store_pad<VEC>(a, tile, kb, warp, lane, cur);
             tc::fence_async_shared();
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&full[s]);
@@ -288,7 +345,8 @@ bool codes_tc_supported(int d, int W) {
 
 void launch_item_codes_tc(const float *X, int64_t n, int d, const double *norm2,
                           const uint8_t *part, const double *V, const float *Apad, int L, int W,
-                          const int32_t *pos_of_id, uint32_t *codes, cudaStream_t s) {
+                          const int32_t *pos_of_id, uint32_t *codes, void *Xb, int dpb,
+                          float *Xpad, int dpad, cudaStream_t s) {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     CodesArgs a;
@@ -306,6 +364,10 @@ void launch_item_codes_tc(const float *X, int64_t n, int d, const double *norm2,
     a.Apad = Apad;
     a.pos_of_id = pos_of_id;
     a.codes = codes;
+    a.Xb = (__nv_bfloat16 *)Xb;
+    a.dpb = dpb;
+    a.Xpad = Xpad;
+    a.dpad = dpad;
     const size_t sm = codes_tc_smem(a.KB, a.N, a.stages);
     const int grid = (int)std::min<int64_t>(sms, a.ntiles);
     const int vec = (d % 4 == 0) ? 4 : ((d % 2 == 0) ? 2 : 1);

@@ -23,6 +23,11 @@ struct nrlsh_index {
 
     const float *X = nullptr;   // items, device, borrowed unless X_owned
     float *X_owned = nullptr;
+    float *Xpad = nullptr;      // fp32 rows [n x dpad], dpad = d rounded up to 4 (16-byte rows),
+    int32_t dpad = 0;           //   only when d % 4 != 0: the re-rank's gather source
+    void *Xb = nullptr;         // bf16 rows [n x dpb], dpb = d rounded up to 8 (16-byte rows):
+    int32_t dpb = 0;            //   the GT tensor-core operand and the re-rank's filter pass
+    float *xnorm = nullptr;     // [n rounded up to 256] |x| rounded up (0 past n)
 
     double *norm2 = nullptr;      // [n] item order
     int32_t *perm = nullptr;      // [n] position -> id
@@ -70,8 +75,9 @@ struct ProfScope {
 };
 
 // ---------------------------------------------------------------- build
+// (Xb != nullptr: also writes bf16 rows [n x dpb] (zero-padded) and |x| rounded up)
 void launch_norms(const float *X, int64_t n, int d, double *norm2, unsigned long long *bad,
-                  cudaStream_t s);
+                  void *Xb, int dpb, float *xnorm, cudaStream_t s);
 // K2 (percentile): fills part_of_id.  Host-orchestrated; may synchronise `s`.
 int partition_percentile(const double *norm2, int64_t n, int m, uint8_t *part_of_id,
                          cudaStream_t s, std::string *err);
@@ -82,17 +88,19 @@ int partition_scatter(const double *norm2, const uint8_t *part_of_id, int64_t n,
                       int32_t *perm, int32_t *pos_of_id, uint8_t *part_of_pos,
                       int64_t *offsets_d, double *V_d, cudaStream_t s, std::string *err);
 // K3: SRP codes of P(x) in partition order
+// (Xb != nullptr: also writes the bf16 rows [n x dpb]; xnorm is only touched by the
+//  SIMT fallback, the norms pass writes it otherwise)
 void launch_item_codes(const float *X, int64_t n, int d, const double *norm2,
                        const uint8_t *part_of_id, const double *V_d, const float *Apad,
-                       int L, int W, const int32_t *pos_of_id, uint32_t *codes,
-                       cudaStream_t s);
+                       int L, int W, const int32_t *pos_of_id, uint32_t *codes, void *Xb,
+                       int dpb, float *xnorm, float *Xpad, int dpad, cudaStream_t s);
 
 // K3 on tcgen05 (codes_tc.cu); the SIMT kernel above covers the other shapes
 bool codes_tc_supported(int d, int W);
 void launch_item_codes_tc(const float *X, int64_t n, int d, const double *norm2,
                           const uint8_t *part_of_id, const double *V_d, const float *Apad,
-                          int L, int W, const int32_t *pos_of_id, uint32_t *codes,
-                          cudaStream_t s);
+                          int L, int W, const int32_t *pos_of_id, uint32_t *codes, void *Xb,
+                          int dpb, float *Xpad, int dpad, cudaStream_t s);
 
 // ---------------------------------------------------------------- query
 struct QueryWS {
@@ -144,10 +152,18 @@ void launch_topk(const float *scores, const int32_t *cand, int Qb, int64_t ncand
 // fused exact re-rank + top-k (score desc, id asc) over cand[q][0..ncand_q); cand ==
 // nullptr means cand[q][t] = t * stride.  `partial` needs rerank_partial_bytes().
 size_t rerank_partial_bytes(int Qb, int64_t ncand, int k);
-void launch_rerank(const float *X, int d, const float *Q, int Qb, const int32_t *cand,
+// X rows at stride ldx >= d (zeros past d).
+void launch_rerank(const float *X, int d, int ldx, const float *Q, int Qb, const int32_t *cand,
                    int64_t ncand, int64_t cand_ld, const uint32_t *ncand_per_q, int stride,
                    int k, unsigned long long *partial, int64_t *out_ids, float *out_scores,
                    cudaStream_t s);
+
+// certified bf16-filter + fp32-rescore variant (same results as launch_rerank)
+void launch_rerank_bf(const float *X, int d, int ldx, const void *Xb, int dpb, const float *xnorm,
+                      const float *Q, int Qb, const int32_t *cand, int64_t ncand, int64_t cand_ld,
+                      const uint32_t *ncand_per_q, int k, unsigned long long *partial,
+                      int64_t *out_ids, float *out_scores, unsigned long long *nexact,
+                      cudaStream_t s);
 
 // ---------------------------------------------------------------- ground truth
 void launch_vec_norms(const float *X, int64_t n, int d, float *xnorm, cudaStream_t s);

@@ -18,6 +18,8 @@
 #include <algorithm>
 #include <climits>
 
+#include <cuda_bf16.h>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -820,7 +822,7 @@ __device__ __forceinline__ float row_dot_any(const float *__restrict__ xl, const
 
 template <int VEC, int NIT>
 __global__ void __launch_bounds__(kRrThreads) k8_rerank(
-    const float *__restrict__ X, int d, const float *__restrict__ Q,
+    const float *__restrict__ X, int d, int dq, const float *__restrict__ Q,
     const int32_t *__restrict__ cand, int64_t cand_ld, int64_t ncand,
     const uint32_t *__restrict__ ncand_per_q, int stride, int k, int cap, int64_t slice,
     unsigned long long *__restrict__ partial, int64_t *__restrict__ out_ids,
@@ -833,8 +835,9 @@ __global__ void __launch_bounds__(kRrThreads) k8_rerank(
     const int q = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int sub = lane & (kRrLPR - 1), grp = lane >> 3;
+    // X rows hold d floats (a zero-padded copy may have d > dq); queries hold dq
     const int dpad = (d + 8 * VEC - 1) / (8 * VEC) * (8 * VEC);
-    for (int e = threadIdx.x; e < dpad; e += blockDim.x) sq[e] = e < d ? Q[(int64_t)q * d + e] : 0.f;
+    for (int e = threadIdx.x; e < dpad; e += blockDim.x) sq[e] = e < dq ? Q[(int64_t)q * dq + e] : 0.f;
     if (threadIdx.x == 0) { s_cnt = 0; s_thr = ~0ull; }
     int64_t nc = ncand;
     if (ncand_per_q) nc = min((int64_t)ncand_per_q[q], cand_ld);
@@ -899,6 +902,158 @@ __global__ void __launch_bounds__(kRrThreads) k8_rerank(
     }
 }
 
+// Certified two-pass variant: a bf16 pass (Xb rows, half the bytes; q rounded to
+// bf16) gives s~ with |s~ - q.x| <= eps |q||x|; only candidates whose upper bound
+// s~ + eps |q||x| reaches the CTA's current k-th best exact score are rescored in
+// fp32 from X (the same row_dot as the plain kernel, so the returned scores are
+// identical).  Every candidate that can enter the top-k is rescored, so the
+// result equals the plain kernel's.
+template <int NB>
+__device__ __forceinline__ float row_dot_bf(const uint16_t *__restrict__ xb, const float *qb,
+                                            int sub, int nchunk) {
+    // chunk c (8 bf16 = 16 bytes) of the row goes to lane sub + 8i
+    float acc = 0.f;
+    for (int i0 = 0; i0 * kRrLPR < nchunk; i0 += NB) {
+        uint4 v[NB];
+#pragma unroll
+        for (int u = 0; u < NB; ++u) {
+            const int c = min((i0 + u) * kRrLPR + sub, nchunk - 1);
+            v[u] = __ldg(reinterpret_cast<const uint4 *>(xb) + c);
+        }
+#pragma unroll
+        for (int u = 0; u < NB; ++u) {
+            const int c = (i0 + u) * kRrLPR + sub;
+            const bool ok = c < nchunk;
+            const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const float lo = __uint_as_float(w[e] << 16), hi = __uint_as_float(w[e] & 0xFFFF0000u);
+                const int k = (ok ? c : 0) * 8 + 2 * e;
+                acc = fmaf(qb[k], ok ? lo : 0.f, acc);
+                acc = fmaf(qb[k + 1], ok ? hi : 0.f, acc);
+            }
+        }
+    }
+    return acc;
+}
+
+template <int VEC, int NB>
+__global__ void __launch_bounds__(kRrThreads) k8_rerank_bf(
+    const float *__restrict__ X, int d, int dq, const uint16_t *__restrict__ Xb, int dpb,
+    const float *__restrict__ xnorm, float eps_rel, const float *__restrict__ Q,
+    const int32_t *__restrict__ cand, int64_t cand_ld, int64_t ncand,
+    const uint32_t *__restrict__ ncand_per_q, int k, int cap, int64_t slice,
+    unsigned long long *__restrict__ partial, int64_t *__restrict__ out_ids,
+    float *__restrict__ out_scores, unsigned long long *__restrict__ nexact) {
+    extern __shared__ __align__(16) unsigned long long rr_smem[];
+    unsigned long long *buf = rr_smem;                       // [cap]
+    float *sq = reinterpret_cast<float *>(buf + cap);        // [dpad] fp32 q
+    const int dpad = (d + 8 * VEC - 1) / (8 * VEC) * (8 * VEC);
+    float *sqb = sq + dpad;                                  // [dpb] bf16-rounded q
+    __shared__ unsigned int s_cnt;
+    __shared__ unsigned long long s_thr;
+    __shared__ double s_qq[kRrThreads / 32];
+    __shared__ unsigned int s_nex;
+    const int q = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int sub = lane & (kRrLPR - 1), grp = lane >> 3;
+    double qq = 0.0;
+    // X rows hold d floats (a zero-padded copy may have d > dq); queries hold dq
+    for (int e = threadIdx.x; e < dpad; e += blockDim.x) {
+        const float v = e < dq ? Q[(int64_t)q * dq + e] : 0.f;
+        sq[e] = v;
+        qq += (double)v * v;
+    }
+    for (int e = threadIdx.x; e < dpb; e += blockDim.x)
+        sqb[e] = e < dq ? __bfloat162float(__float2bfloat16_rn(Q[(int64_t)q * dq + e])) : 0.f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) qq += __shfl_xor_sync(NR_FULL, qq, o);
+    if (lane == 0) s_qq[warp] = qq;
+    if (threadIdx.x == 0) { s_cnt = 0; s_thr = ~0ull; s_nex = 0; }
+    int64_t nc = ncand;
+    if (ncand_per_q) nc = min((int64_t)ncand_per_q[q], cand_ld);
+    const int64_t t0 = (int64_t)blockIdx.y * slice;
+    const int64_t t1 = min(nc, t0 + slice);
+    const int32_t *cl = cand + (int64_t)q * cand_ld;
+    const float *ql = sq + sub * VEC;
+    const int rem = d - sub * VEC;
+    const int nchunk = dpb / 8;
+    __syncthreads();
+    double qt = 0.0;
+    for (int w = 0; w < kRrThreads / 32; ++w) qt += s_qq[w];
+    // eps |q| rounded up (|q| from an fp64 sum, with margin)
+    const float eq = __fmul_ru(eps_rel, __double2float_ru(sqrt(qt) * (1.0 + 0x1p-50)));
+    unsigned int nex = 0;
+    for (int64_t base = t0; base < t1; base += kRrRound) {
+        const int64_t tw = base + warp * 32 + lane;
+        int myid = -1;
+        if (tw < t1) myid = cl[tw];
+        const float myxn = myid >= 0 ? __ldg(xnorm + myid) : 0.f;
+#pragma unroll 1
+        for (int st = 0; st < 8; ++st) {
+            const int id = __shfl_sync(NR_FULL, myid, st * 4 + grp);
+            const float xn = __shfl_sync(NR_FULL, myxn, st * 4 + grp);
+            float sa = 0.f;
+            if (id >= 0) sa = row_dot_bf<NB>(Xb + (int64_t)id * dpb, sqb, sub, nchunk);
+            sa += __shfl_xor_sync(NR_FULL, sa, 1);
+            sa += __shfl_xor_sync(NR_FULL, sa, 2);
+            sa += __shfl_xor_sync(NR_FULL, sa, 4);
+            const unsigned long long thr = *((volatile unsigned long long *)&s_thr);
+            bool pass = id >= 0;
+            if (pass && thr != ~0ull) {
+                const float ub = __fadd_ru(sa, __fmul_ru(eq, xn));
+                pass = ub >= float_unorder(~(uint32_t)(thr >> 32));
+            }
+            if (!__any_sync(NR_FULL, pass)) continue;
+            float acc = 0.f;
+            if (pass) {
+                const float *xl = X + (int64_t)id * d + sub * VEC;
+                acc = row_dot_any<VEC>(xl, ql, rem);
+            }
+            acc += __shfl_xor_sync(NR_FULL, acc, 1);
+            acc += __shfl_xor_sync(NR_FULL, acc, 2);
+            acc += __shfl_xor_sync(NR_FULL, acc, 4);
+            if (sub == 0 && pass) {
+                ++nex;
+                const unsigned long long key = topk_key(acc, (uint32_t)id);
+                if (key < *((volatile unsigned long long *)&s_thr)) {
+                    const unsigned slot = atomicAdd(&s_cnt, 1u);
+                    buf[slot] = key;
+                }
+            }
+        }
+        __syncthreads();
+        if (s_cnt > (unsigned)(cap - kRrRound)) {   // compact: keep the k best
+            const int c = (int)s_cnt;
+            for (int e = c + threadIdx.x; e < cap; e += blockDim.x) buf[e] = ~0ull;
+            __syncthreads();
+            bitonic_sort_smem(buf, cap);
+            if (threadIdx.x == 0) {
+                s_cnt = (unsigned)min(c, k);
+                if (c >= k) s_thr = buf[k - 1];
+            }
+            __syncthreads();
+        }
+    }
+    if (nexact && nex) atomicAdd(&s_nex, nex);
+    __syncthreads();
+    if (nexact && threadIdx.x == 0 && s_nex) atomicAdd(nexact, (unsigned long long)s_nex);
+    const int c = (int)s_cnt;
+    for (int e = c + threadIdx.x; e < cap; e += blockDim.x) buf[e] = ~0ull;
+    __syncthreads();
+    bitonic_sort_smem(buf, cap);
+    if (partial) {
+        unsigned long long *pp = partial + ((int64_t)q * gridDim.y + blockIdx.y) * k;
+        for (int t = threadIdx.x; t < k; t += blockDim.x) pp[t] = t < c ? buf[t] : ~0ull;
+    } else {
+        for (int t = threadIdx.x; t < k; t += blockDim.x) {
+            const unsigned long long v = t < c ? buf[t] : ~0ull;
+            out_ids[(int64_t)q * k + t] = v == ~0ull ? -1 : (int64_t)(uint32_t)v;
+            out_scores[(int64_t)q * k + t] = v == ~0ull ? -INFINITY : float_unorder(~(uint32_t)(v >> 32));
+        }
+    }
+}
+
 // merge the gy partial top-k lists of each query
 __global__ void __launch_bounds__(256) k8_rerank_merge(const unsigned long long *__restrict__ partial,
                                                        int gy, int k, int np2,
@@ -933,7 +1088,7 @@ size_t rerank_partial_bytes(int Qb, int64_t ncand, int k) {
     return gy > 1 ? (size_t)Qb * gy * k * 8 : 0;
 }
 
-void launch_rerank(const float *X, int d, const float *Q, int Qb, const int32_t *cand,
+void launch_rerank(const float *X, int d, int ldx, const float *Q, int Qb, const int32_t *cand,
                    int64_t ncand, int64_t cand_ld, const uint32_t *ncand_per_q, int stride,
                    int k, unsigned long long *partial, int64_t *out_ids, float *out_scores,
                    cudaStream_t s) {
@@ -946,8 +1101,9 @@ void launch_rerank(const float *X, int d, const float *Q, int Qb, const int32_t 
     const int64_t slice = ((rounds + gy - 1) / gy) * kRrRound;
     gy = (int)std::max<int64_t>(1, (ncand + slice - 1) / slice);
     const int cap = pow2_at_least(k + 2 * kRrRound);
-    const int vec = (d % 4 == 0) ? 4 : ((d % 2 == 0) ? 2 : 1);
-    const int dpad = (d + 8 * vec - 1) / (8 * vec) * (8 * vec);
+    // (the kernel sees row length ldx and query length d)
+    const int vec = (ldx % 4 == 0) ? 4 : ((ldx % 2 == 0) ? 2 : 1);
+    const int dpad = (ldx + 8 * vec - 1) / (8 * vec) * (8 * vec);
     const size_t sm = (size_t)cap * 8 + (size_t)dpad * 4;
     unsigned long long *pp = gy > 1 ? partial : nullptr;
     dim3 grid(Qb, gy);
@@ -956,7 +1112,7 @@ void launch_rerank(const float *X, int d, const float *Q, int Qb, const int32_t 
     do {                                                                                       \
         cudaFuncSetAttribute(k8_rerank<V, N>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
                              (int)sm);                                                         \
-        k8_rerank<V, N><<<grid, kRrThreads, sm, s>>>(X, d, Q, cand, cand_ld, ncand,            \
+        k8_rerank<V, N><<<grid, kRrThreads, sm, s>>>(X, ldx, d, Q, cand, cand_ld, ncand,       \
                                                      ncand_per_q, stride, k, cap, slice, pp,   \
                                                      out_ids, out_scores);                     \
     } while (0)
@@ -973,6 +1129,56 @@ void launch_rerank(const float *X, int d, const float *Q, int Qb, const int32_t 
     if (vec == 4) { NR_RR_V(4) } else if (vec == 2) { NR_RR_V(2) } else { NR_RR_V(1) }
 #undef NR_RR_V
 #undef NR_RR
+    note_launch();
+    if (gy > 1) {
+        const int np2 = pow2_at_least((int64_t)gy * k);
+        cudaFuncSetAttribute(k8_rerank_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, np2 * 8);
+        k8_rerank_merge<<<Qb, 256, (size_t)np2 * 8, s>>>(partial, gy, k, np2, out_ids, out_scores);
+        note_launch();
+    }
+}
+
+
+void launch_rerank_bf(const float *X, int d, int ldx, const void *Xb, int dpb, const float *xnorm,
+                      const float *Q, int Qb, const int32_t *cand, int64_t ncand, int64_t cand_ld,
+                      const uint32_t *ncand_per_q, int k, unsigned long long *partial,
+                      int64_t *out_ids, float *out_scores, unsigned long long *nexact,
+                      cudaStream_t s) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int64_t rounds = std::max<int64_t>(1, (ncand + kRrRound - 1) / kRrRound);
+    int gy = (int)std::min<int64_t>(rounds, std::max(1, (sms * 8) / std::max(1, Qb)));
+    gy = std::min(gy, std::max(1, 8192 / k));
+    if (!partial) gy = 1;
+    const int64_t slice = ((rounds + gy - 1) / gy) * kRrRound;
+    gy = (int)std::max<int64_t>(1, (ncand + slice - 1) / slice);
+    const int cap = pow2_at_least(k + 2 * kRrRound);
+    const int vec = (ldx % 4 == 0) ? 4 : ((ldx % 2 == 0) ? 2 : 1);
+    const int dpad = (ldx + 8 * vec - 1) / (8 * vec) * (8 * vec);
+    const size_t sm = (size_t)cap * 8 + (size_t)dpad * 4 + (size_t)dpb * 4;
+    unsigned long long *pp = gy > 1 ? partial : nullptr;
+    // certified bound of |bf16 dot - exact dot| / (|q||x|): bf16 operands (2u + u^2,
+    // u = 2^-8) + fp32 accumulation of dpb exact products, x1.05 slack (as the GT filter)
+    const double u = 0x1p-8;
+    const float eps = (float)(1.05 * ((2 * u + u * u) + (1 + u) * (1 + u) * dpb * 0x1p-23));
+    const int nb = std::min(4, (dpb / 8 + kRrLPR - 1) / kRrLPR);
+    dim3 grid(Qb, gy);
+#define NR_RB(V, B)                                                                             \
+    do {                                                                                        \
+        cudaFuncSetAttribute(k8_rerank_bf<V, B>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
+                             (int)sm);                                                          \
+        k8_rerank_bf<V, B><<<grid, kRrThreads, sm, s>>>(                                        \
+            X, ldx, d, (const uint16_t *)Xb, dpb, xnorm, eps, Q, cand, cand_ld, ncand,        \
+            ncand_per_q, k, cap, slice, pp, out_ids, out_scores, nexact);                       \
+    } while (0)
+#define NR_RB_V(V)                                                   \
+    switch (nb) {                                                    \
+        case 1: NR_RB(V, 1); break;  case 2: NR_RB(V, 2); break;     \
+        case 3: NR_RB(V, 3); break;  default: NR_RB(V, 4); break;    \
+    }
+    if (vec == 4) { NR_RB_V(4) } else if (vec == 2) { NR_RB_V(2) } else { NR_RB_V(1) }
+#undef NR_RB_V
+#undef NR_RB
     note_launch();
     if (gy > 1) {
         const int np2 = pow2_at_least((int64_t)gy * k);

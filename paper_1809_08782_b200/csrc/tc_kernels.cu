@@ -42,7 +42,7 @@ __global__ void bf16_prep(const float *__restrict__ X, int64_t n, int d, int dp,
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(NR_FULL, s, o);
-        if (lane == 0) xnorm[i] = __double2float_ru(sqrt(s));
+        if (lane == 0) xnorm[i] = __double2float_ru(sqrt(s) * (1.0 + 0x1p-50));   // upper bound
     }
 }
 

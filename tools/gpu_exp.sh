@@ -1,4 +1,6 @@
-# ad-hoc timing experiments (development)
+# ad-hoc timing experiments (development): A/B against the HEAD worktree in ab_head/
 mkdir -p gpurun_out
-python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
-for m in 0 4; do echo "dbg=$m"; NRLSH_SCAN_CLK=1 NRLSH_SCAN_DBG=$m timeout 300 python tools/run_stage.py query --reps 2 2>&1 | tail -3; done > gpurun_out/exp.log 2>&1
+(timeout 300 python ab_head/tools/run_stage.py query --reps 3 2>&1 | tail -1;
+ timeout 300 python tools/run_stage.py query --reps 3 2>&1 | tail -1;
+ timeout 300 python ab_head/tools/run_stage.py query --reps 3 2>&1 | tail -1;
+ timeout 300 python tools/run_stage.py query --reps 3 2>&1 | tail -1) > gpurun_out/exp.log 2>&1

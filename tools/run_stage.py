@@ -43,6 +43,7 @@ for r in range(a.reps):
     elif a.stage == "query":
         ids, sc = idx.query(Q, cfg.k, T)
         st = P.last_query_stats()
+        st.update(P.last_rerank_stats())
     else:
         idx2 = P.Index(X, L, cfg.num_parts[0], seed=cfg.seed)
         st = {}
