@@ -422,7 +422,8 @@ void run_candidates(const nrlsh_index *ix, const float *Qd, const uint32_t *qcod
                     int64_t qbase, int64_t Tq, int stride, int64_t C, uint32_t *qcodes,
                     int8_t *delta, uint32_t *cnt, uint32_t *cntv, uint8_t *blk_act,
                     unsigned long long *buf, int32_t *cand, uint16_t *cand_rank, int *flags,
-                    unsigned long long *pairs, cudaStream_t s) {
+                    unsigned long long *pairs, cudaStream_t s, uint32_t *sel_B = nullptr,
+                    uint32_t *sel_pk = nullptr, uint32_t *cnt_part = nullptr) {
     if (qcodes_in) {
         cudaMemcpyAsync(qcodes, qcodes_in + qbase * ix->W, (size_t)Qb * ix->W * 4,
                         cudaMemcpyDeviceToDevice, s);
@@ -452,7 +453,13 @@ void run_candidates(const nrlsh_index *ix, const float *Qd, const uint32_t *qcod
     }
     {
         ProfScope p(SLOT_SELECT, s);
-        launch_select(ix, Qb, Tq, buf, cnt, C, cand, cand_rank, s);
+        if (sel_B) {   // bound pass only (the dense re-rank path emits later)
+            cudaMemsetAsync(cnt_part, 0, (size_t)ix->m * 4, s);
+            launch_select_split(ix, Qb, Tq, buf, cnt, C, 1, sel_B, sel_pk, cnt_part, nullptr,
+                                nullptr, nullptr, s);
+        } else {
+            launch_select(ix, Qb, Tq, buf, cnt, C, cand, cand_rank, s);
+        }
     }
 }
 
@@ -515,6 +522,20 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
         cd.alloc((size_t)Qmax * Tq * 4, s) ||
         pt.alloc(want_topk ? rerank_partial_bytes(Qmax, Tq, k) : 0, s) || fl.alloc(32, s))
         return fail(NRLSH_ENOMEM, "query workspace");
+    // dense re-rank of the sub-datasets most of whose pairs are candidates (rerank_dense.cu)
+    const float *Xr = ix->Xpad ? ix->Xpad : ix->X;
+    const int ldr = ix->Xpad ? ix->dpad : ix->d;
+    const bool use_dense = want_topk && dense_rerank_supported(ldr, ix->W, k);
+    const int S = use_dense ? dense_splits(Qmax) : 0;
+    DBuf sb, spk, cpart, dmask, dinf, nco, gid, gsc, dpart;
+    if (use_dense &&
+        (sb.alloc((size_t)Qmax * 4, s) || spk.alloc((size_t)Qmax * 4, s) ||
+         cpart.alloc((size_t)ix->m * 4, s) || dmask.alloc((size_t)ix->m, s) ||
+         dinf.alloc((size_t)(2 * ix->m + 2) * 4, s) || nco.alloc((size_t)Qmax * 4, s) ||
+         gid.alloc((size_t)Qmax * k * 8, s) || gsc.alloc((size_t)Qmax * k * 4, s) ||
+         dpart.alloc((size_t)Qmax * S * k * 8, s)))
+        return fail(NRLSH_ENOMEM, "query workspace (dense re-rank)");
+    const float dense_frac = getenv("NRLSH_DENSE_FRAC") ? (float)atof(getenv("NRLSH_DENSE_FRAC")) : 0.10f;
     const int init_flags[8] = {INT_MAX, INT_MAX, 0, 0, 0, 0, 0, 0};
     cudaMemcpyAsync(fl.p, init_flags, 32, cudaMemcpyHostToDevice, s);
     unsigned long long *pairs = (unsigned long long *)(fl.get<int>() + 4);
@@ -527,8 +548,32 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
         run_candidates(ix, Qd, qcodes_user ? (const uint32_t *)QCs.dev : nullptr, Qb, q0, Tq,
                        stride, C, qc.get<uint32_t>(), dl.get<int8_t>(), cn.get<uint32_t>(),
                        cv.get<uint32_t>(), ba.get<uint8_t>(), bf.get<unsigned long long>(), cand,
-                       crank, fl.get<int>(), pairs, s);
-        if (want_topk) {
+                       crank, fl.get<int>(), pairs, s, use_dense ? sb.get<uint32_t>() : nullptr,
+                       use_dense ? spk.get<uint32_t>() : nullptr,
+                       use_dense ? cpart.get<uint32_t>() : nullptr);
+        if (use_dense) {
+            {
+                ProfScope p(SLOT_SELECT, s);
+                launch_dense_decide(cpart.get<uint32_t>(), ix->offsets_d, ix->m, Qb, dense_frac,
+                                    dmask.get<uint8_t>(), dinf.get<int32_t>(), s);
+                launch_select_split(ix, Qb, Tq, bf.get<unsigned long long>(), cn.get<uint32_t>(),
+                                    C, 2, sb.get<uint32_t>(), spk.get<uint32_t>(), nullptr,
+                                    dmask.get<uint8_t>(), cand, nco.get<uint32_t>(), s);
+            }
+            {
+                ProfScope p(SLOT_RERANK, s);
+                launch_rerank(Xr, ix->d, ldr, Qd, Qb, cand, Tq, Tq, nco.get<uint32_t>(), 1, k,
+                              pt.get<unsigned long long>(), gid.get<int64_t>(), gsc.get<float>(),
+                              s);
+            }
+            ProfScope p(SLOT_RERANK_TOPK, s);
+            launch_rerank_dense(Xr, ldr, ix->d, Qd, qc.get<uint32_t>(), sb.get<uint32_t>(),
+                                spk.get<uint32_t>(), ix, Qb, k, dinf.get<int32_t>(),
+                                dpart.get<unsigned long long>(), S, s);
+            launch_dense_merge(dpart.get<unsigned long long>(), S, k, gid.get<int64_t>(),
+                               gsc.get<float>(), Qb, (int64_t *)oi.dev + q0 * k,
+                               (float *)os.dev + q0 * k, s);
+        } else if (want_topk) {
             ProfScope p(SLOT_RERANK, s);
             if (ix->Xb && getenv("NRLSH_RERANK_BF16"))
                 launch_rerank_bf(ix->Xpad ? ix->Xpad : ix->X, ix->d, ix->Xpad ? ix->dpad : ix->d,

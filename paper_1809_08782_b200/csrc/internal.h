@@ -165,6 +165,25 @@ void launch_rerank_bf(const float *X, int d, int ldx, const void *Xb, int dpb, c
                       int64_t *out_ids, float *out_scores, unsigned long long *nexact,
                       cudaStream_t s);
 
+// select split in two passes (query_kernels.cu): mode 1 = bound (B, pk, per-sub-dataset
+// candidate counts), mode 2 = emit the candidates outside dense sub-datasets
+void launch_select_split(const nrlsh_index *ix, int Qb, int64_t Tq, const unsigned long long *buf,
+                         const uint32_t *cnt, int64_t C, int mode, uint32_t *sel_B,
+                         uint32_t *sel_pk, uint32_t *cnt_part, const uint8_t *dense,
+                         int32_t *cand, uint32_t *ncand_out, cudaStream_t s);
+// dense re-rank of the hot sub-datasets (rerank_dense.cu)
+bool dense_rerank_supported(int ld, int W, int k);
+int dense_splits(int Qb);
+void launch_dense_decide(const uint32_t *cnt_part, const int64_t *offsets, int m, int Qb,
+                         float frac, uint8_t *dense, int32_t *dinfo, cudaStream_t s);
+void launch_rerank_dense(const float *X, int ld, int dq, const float *Q, const uint32_t *qcodes,
+                         const uint32_t *sel_B, const uint32_t *sel_pk, const nrlsh_index *ix,
+                         int Qb, int k, const int32_t *dinfo, unsigned long long *partial, int S,
+                         cudaStream_t s);
+void launch_dense_merge(const unsigned long long *partial, int S, int k, const int64_t *g_ids,
+                        const float *g_sc, int Qb, int64_t *out_ids, float *out_scores,
+                        cudaStream_t s);
+
 // ---------------------------------------------------------------- ground truth
 void launch_vec_norms(const float *X, int64_t n, int d, float *xnorm, cudaStream_t s);
 void launch_gt_filter(const float *X, int64_t n, int d, const float *Q, int Qb,

@@ -424,11 +424,18 @@ void launch_fallback(const nrlsh_index *ix, const uint32_t *qcodes, int Qb, int6
 }
 
 // =========================================================================== K7 select
+// mode 0: bound + emit (all candidates); mode 1: bound only — writes the boundary
+// structure position B and tie position bound pk per query and adds every
+// sub-dataset's candidate count of the query to cnt_part; mode 2: emit from the
+// stored (B, pk), skipping sub-datasets flagged dense (they are re-ranked by the
+// dense kernel) and writing the number emitted to ncand_out.
 __global__ void __launch_bounds__(1024) k7_select(
     const unsigned long long *__restrict__ buf, const uint32_t *__restrict__ cnt, int64_t C,
     int64_t Tq, int NR, int tie_cap, const uint16_t *__restrict__ R,
     const int32_t *__restrict__ perm, int32_t *__restrict__ cand,
-    uint16_t *__restrict__ cand_rank) {
+    uint16_t *__restrict__ cand_rank, int mode, int L, uint32_t *__restrict__ sel_B,
+    uint32_t *__restrict__ sel_pk, uint32_t *__restrict__ cnt_part,
+    const uint8_t *__restrict__ dense, uint32_t *__restrict__ ncand_out) {
     extern __shared__ uint32_t hist[];   // [max(NR, tie_cap)] + R copy [NR] (uint16)
     uint16_t *sRt = reinterpret_cast<uint16_t *>(hist + tie_cap);
     __shared__ uint32_t ws[32];
@@ -438,6 +445,25 @@ __global__ void __launch_bounds__(1024) k7_select(
     const int q = blockIdx.x;
     const int64_t c = min((int64_t)cnt[q], C);
     const unsigned long long *b = buf + (int64_t)q * C;
+    if (mode == 2) {
+        for (int e = threadIdx.x; e < NR; e += blockDim.x) sRt[e] = R[e];
+        if (threadIdx.x == 0) s_out = 0;
+        __syncthreads();
+        const uint32_t B = sel_B[q], pk = sel_pk[q];
+        for (int64_t e = threadIdx.x; e < c; e += blockDim.x) {
+            const unsigned long long v = b[e];
+            const uint32_t f = (uint32_t)(v >> 32), pos = (uint32_t)v;
+            if (f >= (uint32_t)NR || dense[f / (L + 1)]) continue;
+            const uint32_t r = sRt[f];
+            if (r < B || (r == B && pos <= pk)) {
+                const uint32_t slot = atomicAdd(&s_out, 1u);
+                if (slot < (uint32_t)Tq) cand[(int64_t)q * Tq + slot] = perm[pos];
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) ncand_out[q] = min(s_out, (uint32_t)Tq);
+        return;
+    }
     for (int e = threadIdx.x; e < NR; e += blockDim.x) { hist[e] = 0u; sRt[e] = R[e]; }
     if (threadIdx.x == 0) { sB = NR - 1; sLt = 0; s_out = 0; }
     __syncthreads();
@@ -468,6 +494,17 @@ __global__ void __launch_bounds__(1024) k7_select(
     const uint32_t B = (uint32_t)sB;
     const uint32_t need_eq = need - sLt;
     const uint32_t n_eq = hist[B];
+    if (cnt_part) {   // the query's candidates per sub-dataset (hist is still intact here)
+        const int m = NR / (L + 1);
+        for (int j = threadIdx.x; j < m; j += blockDim.x) {
+            uint32_t cj = 0;
+            for (int h = 0; h <= L; ++h) {
+                const uint32_t r = sRt[j * (L + 1) + h];
+                cj += r < B ? hist[r] : (r == B ? min(need_eq, n_eq) : 0u);
+            }
+            if (cj) atomicAdd(&cnt_part[j], cj);
+        }
+    }
     // the need_eq-th smallest position among the ties (R == B): when they fit, one
     // pass gathers them into shared memory (reusing the histogram's space) and a
     // radix select runs there; otherwise radix select over the buffer, 8 bits/round
@@ -548,6 +585,10 @@ __global__ void __launch_bounds__(1024) k7_select(
     }
     __syncthreads();
     const uint32_t pk = s_pfx;
+    if (mode == 1) {
+        if (threadIdx.x == 0) { sel_B[q] = B; sel_pk[q] = pk; }
+        return;
+    }
     for (int64_t e = threadIdx.x; e < c; e += blockDim.x) {
         const unsigned long long v = b[e];
         const uint32_t f = (uint32_t)(v >> 32), pos = (uint32_t)v;
@@ -570,7 +611,22 @@ void launch_select(const nrlsh_index *ix, int Qb, int64_t Tq, const unsigned lon
     const int tie_cap = std::max(NR, 16384);
     const size_t sm = (size_t)tie_cap * 4 + (size_t)NR * 2;
     cudaFuncSetAttribute(k7_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k7_select<<<Qb, 1024, sm, s>>>(buf, cnt, C, Tq, NR, tie_cap, ix->R_d, ix->perm, cand, cand_rank);
+    k7_select<<<Qb, 1024, sm, s>>>(buf, cnt, C, Tq, NR, tie_cap, ix->R_d, ix->perm, cand, cand_rank,
+                                   0, ix->L, nullptr, nullptr, nullptr, nullptr, nullptr);
+    note_launch();
+}
+
+
+void launch_select_split(const nrlsh_index *ix, int Qb, int64_t Tq, const unsigned long long *buf,
+                         const uint32_t *cnt, int64_t C, int mode, uint32_t *sel_B,
+                         uint32_t *sel_pk, uint32_t *cnt_part, const uint8_t *dense,
+                         int32_t *cand, uint32_t *ncand_out, cudaStream_t s) {
+    const int NR = ix->m * (ix->L + 1);
+    const int tie_cap = std::max(NR, 16384);
+    const size_t sm = (size_t)tie_cap * 4 + (size_t)NR * 2;
+    cudaFuncSetAttribute(k7_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k7_select<<<Qb, 1024, sm, s>>>(buf, cnt, C, Tq, NR, tie_cap, ix->R_d, ix->perm, cand, nullptr,
+                                   mode, ix->L, sel_B, sel_pk, cnt_part, dense, ncand_out);
     note_launch();
 }
 

@@ -476,6 +476,7 @@ def test_rerank_bf16_filter_matches_fp32(built, case, monkeypatch):
     """The certified bf16 first pass of the re-rank only skips candidates that cannot
     enter the top-k: ids and fp32 scores equal the all-fp32 re-rank's, bit for bit."""
     P = _P()
+    monkeypatch.setenv("NRLSH_NO_DENSE", "1")    # both sides through the gather kernels
     cfg, X, Q, Xd, idx, orc = built(*case)
     n = X.shape[0]
     Qd = torch.from_numpy(Q[: min(len(Q), 64)]).cuda()
@@ -488,3 +489,28 @@ def test_rerank_bf16_filter_matches_fp32(built, case, monkeypatch):
         assert np.array_equal(a.cpu().numpy(), b.cpu().numpy()), T
         assert np.array_equal(sa.cpu().numpy(), sb.cpu().numpy()), T
         assert resc <= Qd.shape[0] * min(T, n)
+
+
+@pytest.mark.parametrize("case", [("c4", 300_000, 64, 64, 128), ("tiny", None, None, 32, 8),
+                                  ("scale", 70_000, 16, 128, 256)], ids=_ids)
+def test_dense_rerank_path(built, case, monkeypatch):
+    """The opt-in dense re-rank of hot sub-datasets (rerank_dense.cu) returns the
+    oracle's top-k (identical codes injected), like the gather path."""
+    monkeypatch.setenv("NRLSH_DENSE", "1")
+    monkeypatch.setenv("NRLSH_DENSE_FRAC", "0.02")    # make several sub-datasets dense
+    cfg, X, Q, Xd, idx, orc = built(*case)
+    n = X.shape[0]
+    ocodes = orc.codes()
+    idx.set_codes(ocodes[orc.perm])
+    nq = min(len(Q), 24)
+    Qd = torch.from_numpy(Q[:nq]).cuda()
+    gq = idx.query_codes(Qd).cpu().numpy().view(np.uint32)
+    oq = oracle.query_codes(Q[:nq], orc.A)
+    for T in sorted(set([cfg.k, (n + 99) // 100, n // 7, n])):
+        ids, sc = idx.query(Qd, cfg.k, T)
+        ids, sc = ids.cpu().numpy(), sc.cpu().numpy()
+        for qi in range(nq):
+            if not np.array_equal(gq[qi], oq[qi]):
+                continue
+            a, s = oracle.query(X, ocodes, orc.part, orc.R, orc.A, Q[qi], T, cfg.k)
+            assert_topk_match(ids[qi], sc[qi], a, s, X, Q[qi])
