@@ -56,6 +56,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--sweep", default=None,
+                    help="comma-separated configs: per probe budget queries/s and recall@k "
+                         "(no driver line; writes --sweep-out)")
+    ap.add_argument("--sweep-out", default=None)
     return ap.parse_args()
 
 
@@ -449,8 +453,80 @@ def run_native(args):
         dist.destroy_process_group()
 
 
+def _sweep_plan(cfg):
+    """(code_bits, num_parts, budgets) runs of a config: its stated budgets plus the
+    paper's 2^i probe grid (Fig. 2 x-axis) where BASELINE.json asks
+    for recall curves (c3, c4)."""
+    runs = []
+    for L in cfg.code_bits:
+        for m in cfg.num_parts:
+            Ts = sorted(set(cfg.budget_list()) | set(t for t in cfg.extra_T if t <= cfg.n))
+            runs.append((L, m, Ts))
+    return runs
+
+
+def run_sweep(args):
+    """queries/s (nrlsh_query only, device-resident queries, CUDA events) and
+    recall@k against the exact top-k, at every probe budget of each config."""
+    import torch
+    import paper_1809_08782_b200 as P
+    dev = torch.device("cuda", 0)
+    rows = []
+    for name in args.sweep.split(","):
+        cfg = workloads.CONFIGS[name]
+        X = workloads.make_items(cfg)
+        Q = workloads.make_queries(cfg)
+        Xd = torch.from_numpy(X).to(dev)
+        Qd = torch.from_numpy(Q).to(dev)
+        k = cfg.k
+        gt = None
+        for L, m, Ts in _sweep_plan(cfg):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            idx = P.Index(Xd, L, m, seed=cfg.seed, query_batch=cfg.query_batch)
+            e1.record()
+            torch.cuda.synchronize()
+            build_ms = e0.elapsed_time(e1)
+            if gt is None:
+                gt, _ = idx.exact_topk(Qd, k)
+                gt = gt.cpu().numpy()
+            for T in Ts:
+                idx.query(Qd[: min(len(Q), 256)], k, T)          # warm-up
+                ms = []
+                for _ in range(3):
+                    e0.record()
+                    ids, sc = idx.query(Qd, k, T)
+                    e1.record()
+                    torch.cuda.synchronize()
+                    ms.append(e0.elapsed_time(e1))
+                ids = ids.cpu().numpy()
+                rec = float(np.mean([len(set(a.tolist()) & set(b.tolist())) / k
+                                     for a, b in zip(ids, gt)]))
+                row = {"config": name, "n": cfg.n, "d": cfg.d, "code_bits": L, "num_parts": m,
+                       "nq": len(Q), "k": k, "probe_budget": int(T), "budget_frac": T / cfg.n,
+                       "queries_per_s": len(Q) / (float(np.median(ms)) / 1e3),
+                       "query_ms": float(np.median(ms)), "recall_at_k": rec,
+                       "build_ms": build_ms}
+                if k > 10:   # recall@10: the first 10 returned against the true top-10
+                    row["recall_at_10"] = float(np.mean([
+                        len(set(a[:10].tolist()) & set(b[:10].tolist())) / 10
+                        for a, b in zip(ids, gt)]))
+                rows.append(row)
+                print(json.dumps(row), flush=True)
+            idx.close()
+        del Xd, Qd
+        torch.cuda.empty_cache()
+    if args.sweep_out:
+        with open(args.sweep_out, "w") as f:
+            json.dump(rows, f, indent=1)
+
+
 def main():
     args = parse()
+    if args.sweep:
+        run_sweep(args)
+        return
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -1135,13 +1135,15 @@ static int pow2_at_least(int64_t v) {
     return p;
 }
 
-size_t rerank_partial_bytes(int Qb, int64_t ncand, int k) {
+// Partial-list capacity for ANY sub-batch of at most Qmax queries: launch_rerank picks
+// gy <= max(1, 8 SMs' worth / Qb), so Qb * gy <= max(Qmax, 8 * sms).  (Sizing it for
+// Qmax alone under-allocates the smaller last sub-batch, which splits finer.)
+size_t rerank_partial_bytes(int Qmax, int64_t ncand, int k) {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     const int64_t rounds = std::max<int64_t>(1, (ncand + kRrRound - 1) / kRrRound);
-    int gy = (int)std::min<int64_t>(rounds, std::max(1, (sms * 8) / std::max(1, Qb)));
-    gy = std::min(gy, std::max(1, 8192 / k));
-    return gy > 1 ? (size_t)Qb * gy * k * 8 : 0;
+    if (rounds <= 1) return 0;
+    return (size_t)std::max(Qmax, sms * 8) * k * 8;
 }
 
 void launch_rerank(const float *X, int d, int ldx, const float *Q, int Qb, const int32_t *cand,

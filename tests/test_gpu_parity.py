@@ -514,3 +514,25 @@ def test_dense_rerank_path(built, case, monkeypatch):
                 continue
             a, s = oracle.query(X, ocodes, orc.part, orc.R, orc.A, Q[qi], T, cfg.k)
             assert_topk_match(ids[qi], sc[qi], a, s, X, Q[qi])
+
+
+def test_small_last_sub_batch_large_budget(built):
+    """nq = one full sub-batch + a few queries, T spanning several re-rank rounds: the
+    short last sub-batch splits its candidates finer than the full one (regression:
+    its partial top-k lists once overflowed a buffer sized for the full sub-batch)."""
+    cfg, X, Q, Xd, idx, orc = built("c2", None, 200, 64, 32)
+    n = X.shape[0]
+    Qbig = np.concatenate([Q] * 6)[:1024 + 9]                 # 1024 + 9 queries
+    Qd = torch.from_numpy(np.ascontiguousarray(Qbig)).cuda()
+    ocodes = orc.codes()
+    idx.set_codes(ocodes[orc.perm])
+    gq = idx.query_codes(Qd).cpu().numpy().view(np.uint32)
+    oq = oracle.query_codes(Qbig, orc.A)
+    for T in (1777, n // 2):
+        ids, sc = idx.query(Qd, cfg.k, T)
+        ids, sc = ids.cpu().numpy(), sc.cpu().numpy()
+        for qi in list(range(1024, 1033)) + [0, 511]:
+            if not np.array_equal(gq[qi], oq[qi]):
+                continue
+            a, s = oracle.query(X, ocodes, orc.part, orc.R, orc.A, Qbig[qi], T, cfg.k)
+            assert_topk_match(ids[qi], sc[qi], a, s, X, Qbig[qi])

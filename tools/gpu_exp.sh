@@ -1,6 +1,3 @@
-# ad-hoc timing experiments (development): A/B against the HEAD worktree in ab_head/
+# ad-hoc timing experiments (development)
 mkdir -p gpurun_out
-(timeout 300 python ab_head/tools/run_stage.py query --reps 3 2>&1 | tail -1;
- timeout 300 python tools/run_stage.py query --reps 3 2>&1 | tail -1;
- timeout 300 python ab_head/tools/run_stage.py query --reps 3 2>&1 | tail -1;
- timeout 300 python tools/run_stage.py query --reps 3 2>&1 | tail -1) > gpurun_out/exp.log 2>&1
+(for sd in 65536 32768 16384; do echo "samples=$sd"; NRLSH_PILOT_SAMPLES=$sd timeout 300 python tools/run_stage.py query --reps 3 2>&1 | tail -1; done) > gpurun_out/exp.log 2>&1
