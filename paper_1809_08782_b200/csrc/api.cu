@@ -413,8 +413,12 @@ nrlsh_status nrlsh_get_info(const nrlsh_index *ix, int64_t *n, int32_t *d, int32
 namespace {
 
 
-int64_t buffer_capacity(int64_t Tq, int stride, int64_t n) {
-    double c = 2.0 * Tq + 16.0 * std::sqrt((double)Tq * stride) + 4096.0;
+// Per-query append capacity: the pilot bound's count before its boundary cell
+// (T + sampling noise) plus the boundary cell itself, which can hold a whole
+// sub-dataset (items of a large-U_j sub-dataset with small ||x||/U_j all map
+// close to e_{d+1}, so their codes — and their h — nearly coincide).
+int64_t buffer_capacity(int64_t Tq, int stride, int64_t n, int64_t max_part) {
+    double c = 2.0 * Tq + 16.0 * std::sqrt((double)Tq * stride) + 4096.0 + (double)max_part;
     int64_t C = (int64_t)c;
     C = std::max<int64_t>(C, Tq);
     return std::min<int64_t>(C, n);
@@ -493,7 +497,9 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
     const int64_t n = ix->n;
     const int64_t Tq = std::min<int64_t>(probe_budget, n);
     const int stride = pilot_stride(n);
-    const int64_t C = buffer_capacity(Tq, stride, n);
+    int64_t max_part = 0;
+    for (int j = 0; j < ix->m; ++j) max_part = std::max(max_part, ix->offsets[j + 1] - ix->offsets[j]);
+    const int64_t C = buffer_capacity(Tq, stride, n, max_part);
     int Qmax = (int)std::min<int64_t>(ix->query_batch, nq);
     // keep the candidate buffers bounded (~2.5 GB)
     const int64_t per_q = C * 8 + Tq * 10;

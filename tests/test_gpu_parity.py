@@ -536,3 +536,24 @@ def test_small_last_sub_batch_large_budget(built):
                 continue
             a, s = oracle.query(X, ocodes, orc.part, orc.R, orc.A, Qbig[qi], T, cfg.k)
             assert_topk_match(ids[qi], sc[qi], a, s, X, Qbig[qi])
+
+
+def test_coarse_cells_no_overflow(built):
+    """Few sub-datasets over heavy-tailed norms: most items of the top sub-dataset
+    have ||x|| << U_j, map close to e_{d+1} and share (nearly) one code, so the
+    pilot's boundary cell can hold tens of thousands of items for a tiny budget.
+    The per-query capacity covers a whole sub-dataset: no query may overflow into
+    the exact fallback, and the candidates still equal the oracle's."""
+    cfg, X, Q, Xd, idx, orc = built("c4", 300_000, 32, 32, 4)
+    P = _P()
+    ocodes = orc.codes()
+    idx.set_codes(ocodes[orc.perm])
+    qc = oracle.query_codes(Q, orc.A)
+    for T in (1, 128, 4096):
+        gid, grk = idx.candidates(T, qcodes=torch.from_numpy(qc.view(np.int32)).cuda())
+        assert P.last_query_stats()["fallback_queries"] == 0, T
+        gid, grk = gid.cpu().numpy(), grk.cpu().numpy().view(np.uint16)
+        for qi in range(4):
+            oid, ork = oracle.candidates(ocodes, orc.part, qc[qi], orc.R, T)
+            o = np.lexsort((gid[qi], grk[qi]))
+            assert np.array_equal(gid[qi][o], oid) and np.array_equal(grk[qi][o], ork)
