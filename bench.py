@@ -145,9 +145,11 @@ def load_peaks():
 
 
 def roofline_for(slot, ms_total, count, info, peaks, peaks_src):
-    """Algorithmic work per launch of the dominant kernel class / its mean duration."""
+    """Algorithmic work of a stage over the timed steps / its device time there (CUDA
+    events on the launching stream around the stage's launches)."""
     if count == 0 or ms_total <= 0:
         return None
+    steps = info["steps"]
     per_launch_s = ms_total / count / 1e3
     n, d, L, W, nq = info["n"], info["d"], info["L"], info["W"], info["nq"]
     T, k, m = info["T"], info["k"], info["m"]
@@ -162,9 +164,16 @@ def roofline_for(slot, ms_total, count, info, peaks, peaks_src):
                 "frac": ach / POPC_PEAK_PER_S, "traffic": traffic,
                 "peak_source": "tools/ubench.cu measured POPC rate (profiles/r01/ubench_popc.txt)",
                 "logical_pairs_per_s": nq * n / (ms_total / 1e3)}
-    if slot == "gt_filter":
-        fl = 2.0 * nq * n * d / count
+    if slot == "gt_filter" or (slot == "rerank" and info.get("rerank_path") == "tensor"):
+        # one bf16 pass over every item per query (member-mode for the re-rank)
+        fl = 2.0 * nq * n * d * steps / count
         ach = fl / per_launch_s
+        if slot == "rerank":
+            pk = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")) * 1e12
+            return {"bound": "tensor", "kernel": "rerank (tcgen05 bf16 filter pass, member mode)",
+                    "achieved": ach / 1e12, "peak": pk / 1e12, "unit": "TFLOP/s",
+                    "frac": ach / pk, "traffic": traffic,
+                    "peak_source": f"MEASURED_PEAKS.json bf16 sustained ({peaks_src})"}
         if info.get("gt_tensor"):
             pk = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")) * 1e12
             return {"bound": "tensor", "kernel": "gt_filter (tcgen05 bf16)", "achieved": ach / 1e12,
@@ -178,7 +187,7 @@ def roofline_for(slot, ms_total, count, info, peaks, peaks_src):
     if slot == "rerank":
         by = info["score_bytes"] / count
     elif slot in ("codes", "norms"):
-        by = n * d * 4.0 + (n * W * 4.0 if slot == "codes" else n * 8.0)
+        by = (n * d * 4.0 + (n * W * 4.0 if slot == "codes" else n * 8.0)) * steps / count
     else:
         return None
     ach = by / per_launch_s
@@ -363,6 +372,7 @@ def run_native(args):
         evs.append((e0, e1))
         scanned += qstats["scanned_pairs"]
     torch.cuda.synchronize()
+    rerank_path = P.last_rerank_path()["path"]
     if dist:
         dist.barrier()
     clocks = sampler.stop()
@@ -415,7 +425,8 @@ def run_native(args):
              for name, v in prof.items() if v[1] > 0}
     W = 1 if L <= 32 else (2 if L <= 64 else 4)
     info = {"n": cfg.n, "d": cfg.d, "L": L, "W": W, "nq": nq, "T": T, "k": k, "m": m,
-            "scanned_pairs": scanned, "traffic": load_traffic(),
+            "scanned_pairs": scanned, "traffic": load_traffic(), "steps": args.steps,
+            "rerank_path": rerank_path,
             "score_bytes": float(nq) * T * cfg.d * 4.0 * args.steps, "gt_tensor": True}
     dom = max(((n_, v) for n_, v in prof.items() if v[1] > 0), key=lambda x: x[1][0])
     roof = roofline_for(dom[0], dom[1][0], dom[1][1], info, peaks, peaks_src)

@@ -155,9 +155,31 @@ nrlsh_status nrlsh_last_query_stats(int64_t *fallback_queries, int64_t *kernel_l
                                     int64_t *scanned_pairs);
 
 /* Candidates of the last nrlsh_query on this thread that the re-rank rescored in
-   fp32 after its certified bf16 pass (the others provably could not enter the
-   top-k; the answer is the same as rescoring all of them). */
+   fp32 after a certified bf16 pass (the others provably could not enter the
+   top-k; the answer is the same as rescoring all of them): the tensor-core
+   re-rank's survivor slots, or the opt-in bf16 gather pre-pass's survivors;
+   0 for the plain gather path. */
 nrlsh_status nrlsh_last_rerank_stats(int64_t *rescored_fp32);
+
+/* Which implementation re-ranked the last nrlsh_query on this thread (all return
+   the same answer: the exact fp32 top-k of the probed candidates):
+     NRLSH_RERANK_GATHER       per-candidate row gather + fp32 dot (default for
+                               small budgets);
+     NRLSH_RERANK_TENSOR       one bf16 tcgen05 pass over every item with a certified
+                               filter (|s~ - s_f| <= eps |q||x|) against a running
+                               lower bound of the k-th best candidate score,
+                               keeping survivors that pass the select's candidate
+                               rule, then the same fp32 re-rank of the survivors
+                               (default when probe_budget >= n / 160);
+     NRLSH_RERANK_DENSE        dense SIMT re-rank of hot sub-datasets (opt-in);
+     NRLSH_RERANK_GATHER_BF16  gather with a certified bf16 pre-pass (opt-in).
+   overflow_redone: queries whose tensor-core survivor list overflowed and were
+   re-ranked by the gather path instead.  Either pointer may be NULL. */
+#define NRLSH_RERANK_GATHER 0
+#define NRLSH_RERANK_TENSOR 1
+#define NRLSH_RERANK_DENSE 2
+#define NRLSH_RERANK_GATHER_BF16 3
+nrlsh_status nrlsh_last_rerank_path(int32_t *path, int64_t *overflow_redone);
 
 /* Exact top-k (as nrlsh_exact_topk) against the index's own items (device copy
    or borrowed pointer), so host-buffer callers do not re-stage the items. */

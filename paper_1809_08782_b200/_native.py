@@ -24,7 +24,7 @@ EXPORTS = [
     "nrlsh_get_projection", "nrlsh_get_rank_table", "nrlsh_get_codes", "nrlsh_set_codes",
     "nrlsh_query_codes", "nrlsh_query_candidates", "nrlsh_last_query_stats",
     "nrlsh_index_exact_topk", "nrlsh_exact_topk_seeded", "nrlsh_index_exact_topk_seeded",
-    "nrlsh_last_rerank_stats", "nrlsh_profile_enable", "nrlsh_profile_read",
+    "nrlsh_last_rerank_stats", "nrlsh_last_rerank_path", "nrlsh_profile_enable", "nrlsh_profile_read",
     "nrlsh_profile_slot_name", "nrlsh_launch_count", "nrlsh_last_exact_stats",
 ]
 
@@ -100,6 +100,8 @@ def lib():
         L.nrlsh_profile_slot_name.restype = C.c_char_p
         L.nrlsh_last_rerank_stats.argtypes = [p]
         L.nrlsh_last_rerank_stats.restype = st
+        L.nrlsh_last_rerank_path.argtypes = [p, p]
+        L.nrlsh_last_rerank_path.restype = st
         L.nrlsh_last_exact_stats.argtypes = [p, p, p]
         L.nrlsh_last_exact_stats.restype = st
         L.nrlsh_launch_count.argtypes = []
@@ -285,6 +287,17 @@ def last_rerank_stats():
     a = C.c_int64()
     _check(lib().nrlsh_last_rerank_stats(C.byref(a)))
     return {"rescored_fp32": a.value}
+
+
+RERANK_PATHS = {0: "gather", 1: "tensor", 2: "dense", 3: "gather_bf16"}
+
+
+def last_rerank_path():
+    """Which re-rank implementation the last query on this thread used, and how many
+    of its queries overflowed the tensor-core survivor list (re-ranked by gather)."""
+    a, b = C.c_int32(), C.c_int64()
+    _check(lib().nrlsh_last_rerank_path(C.byref(a), C.byref(b)))
+    return {"path": RERANK_PATHS.get(a.value, str(a.value)), "overflow_redone": b.value}
 
 
 def last_query_stats():

@@ -22,6 +22,9 @@ thread_local int64_t g_last_fallbacks = 0;
 thread_local int64_t g_last_launches = 0;
 thread_local int64_t g_last_pairs = 0;
 thread_local int64_t g_last_rescored = 0;
+thread_local int64_t g_last_rtc_overflow = 0;   // tensor-core re-rank: queries redone by gather
+thread_local int64_t g_last_rtc = 0;            // 1 if the last query used the tensor-core re-rank
+thread_local bool g_in_rtc_redo = false;
 thread_local int64_t g_last_gt_max_cand = 0, g_last_gt_sum_cand = 0, g_last_gt_overflow = 0;
 
 nrlsh_status fail(nrlsh_status st, const std::string &msg) {
@@ -138,7 +141,7 @@ void free_index(nrlsh_index *ix) {
     void *ps[] = {ix->X_owned, ix->Xpad, ix->Xb, ix->xnorm, ix->norm2, ix->perm, ix->pos_of_id, ix->part_of_id,
                   ix->part_of_pos, ix->offsets_d, ix->V_d, ix->codes, ix->A, ix->Apad,
                   ix->R_d, ix->chunks_d, ix->order_d, ix->samp_codes, ix->samp_part,
-                  ix->tiles_d};
+                  ix->tiles_d, ix->codes_id};
     // pool-backed (cudaMallocAsync at build); the index may have been used on any stream
     cudaDeviceSynchronize();
     for (void *p : ps)
@@ -290,11 +293,14 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
     cudaMemsetAsync(ix->xnorm + n, 0, (size_t)(npad - n) * 4, s);
     NR_ALLOC(ix->perm, (size_t)n * 4);
     NR_ALLOC(ix->pos_of_id, (size_t)n * 4);
-    NR_ALLOC(ix->part_of_id, (size_t)n);
+    NR_ALLOC(ix->part_of_id, (size_t)npad);
+    cudaMemsetAsync(ix->part_of_id + n, 0, (size_t)(npad - n), s);
     NR_ALLOC(ix->part_of_pos, (size_t)n);
     NR_ALLOC(ix->offsets_d, (size_t)(m + 1) * 8);
     NR_ALLOC(ix->V_d, (size_t)m * 8);
     NR_ALLOC(ix->codes, (size_t)n * W * 4);
+    NR_ALLOC(ix->codes_id, (size_t)npad * W * 4);
+    cudaMemsetAsync(ix->codes_id + n * W, 0, (size_t)(npad - n) * W * 4, s);
 
     // K1: norms + finite check
     DBuf bad;
@@ -377,6 +383,11 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
                           ix->pos_of_id, ix->codes, ix->Xb, ix->dpb, ix->xnorm, ix->Xpad,
                           ix->dpad, s);
     }
+    // item-order codes (the tensor-core re-rank's membership test)
+    {
+        ProfScope p(SLOT_CODES, s);
+        launch_codes_by_id(ix.get(), s);
+    }
     // compacted pilot sample (query-time pilots read it contiguously)
     {
         const int stride = pilot_stride(n);
@@ -430,7 +441,8 @@ void run_candidates(const nrlsh_index *ix, const float *Qd, const uint32_t *qcod
                     int8_t *delta, uint32_t *cnt, uint32_t *cntv, uint8_t *blk_act,
                     unsigned long long *buf, int32_t *cand, uint16_t *cand_rank, int *flags,
                     unsigned long long *pairs, cudaStream_t s, uint32_t *sel_B = nullptr,
-                    uint32_t *sel_pk = nullptr, uint32_t *cnt_part = nullptr) {
+                    uint32_t *sel_pk = nullptr, uint32_t *cnt_part = nullptr,
+                    int32_t *seeds = nullptr, int ks = 0) {
     if (qcodes_in) {
         cudaMemcpyAsync(qcodes, qcodes_in + qbase * ix->W, (size_t)Qb * ix->W * 4,
                         cudaMemcpyDeviceToDevice, s);
@@ -460,7 +472,9 @@ void run_candidates(const nrlsh_index *ix, const float *Qd, const uint32_t *qcod
     }
     {
         ProfScope p(SLOT_SELECT, s);
-        if (sel_B) {   // bound pass only (the dense re-rank path emits later)
+        if (seeds) {   // bound pass + seed members (the tensor-core re-rank)
+            launch_select_seeds(ix, Qb, Tq, buf, cnt, C, sel_B, sel_pk, seeds, ks, s);
+        } else if (sel_B) {   // bound pass only (the dense re-rank path emits later)
             cudaMemsetAsync(cnt_part, 0, (size_t)ix->m * 4, s);
             launch_select_split(ix, Qb, Tq, buf, cnt, C, 1, sel_B, sel_pk, cnt_part, nullptr,
                                 nullptr, nullptr, s);
@@ -468,6 +482,17 @@ void run_candidates(const nrlsh_index *ix, const float *Qd, const uint32_t *qcod
             launch_select(ix, Qb, Tq, buf, cnt, C, cand, cand_rank, s);
         }
     }
+}
+
+// Certified bound of |s~ - s_f| / (|q| |x|) for the tensor-core filter: s~ is the
+// bf16-operand, fp32-accumulated MMA value over dp columns (operand rounding
+// 2u + u^2 with u = 2^-8, accumulation of dp exact products dp * 2^-23, x1.05
+// slack), s_f the fp32 FMA-chain score the exact re-rank computes (gamma_{dp+2}
+// inflated); |s~ - s| and |s - s_f| add.
+float gt_eps_rel(int dp) {
+    const double u = std::ldexp(1.0, -8);
+    return (float)(1.05 * ((2 * u + u * u) + (1 + u) * (1 + u) * dp * std::ldexp(1.0, -23)) +
+                   1.25 * (dp + 2) * std::ldexp(1.0, -24));
 }
 
 nrlsh_status check_flags(const int *hflags) {
@@ -545,6 +570,39 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
          dpart.alloc((size_t)Qmax * S * k * 8, s)))
         return fail(NRLSH_ENOMEM, "query workspace (dense re-rank)");
     const float dense_frac = getenv("NRLSH_DENSE_FRAC") ? (float)atof(getenv("NRLSH_DENSE_FRAC")) : 0.10f;
+    // tensor-core re-rank (tc_kernels.cu member mode): a bf16 GEMM pass over every
+    // item with the certified filter, keeping only candidates; chosen when the
+    // candidate budget is a large enough share of n (a gathered row costs ~170x a
+    // streamed one, measured on c4) — NRLSH_RERANK_TC=0/1 forces it off/on
+    const char *rtc_env = getenv("NRLSH_RERANK_TC");
+    const double rtc_ratio = getenv("NRLSH_RERANK_TC_RATIO") ? atof(getenv("NRLSH_RERANK_TC_RATIO")) : 160.0;
+    const bool use_rtc = want_topk && !use_dense && !g_in_rtc_redo && ix->Xb && ix->codes_id &&
+                         gt_tc_supported(ix->d, k) &&
+                         (rtc_env ? atoi(rtc_env) != 0 : (double)Tq * rtc_ratio >= (double)n);
+    const int KS = std::min(1024, std::max(256, 4 * k));
+    // survivor list capacity per query (NRLSH_RERANK_TC_CAP: test switch forcing the
+    // overflow redo path)
+    const int64_t Cg = getenv("NRLSH_RERANK_TC_CAP")
+                           ? std::max<int64_t>(16, atoll(getenv("NRLSH_RERANK_TC_CAP")))
+                           : std::min<int64_t>(n, std::max<int64_t>(16384, 256 * (int64_t)k));
+    DBuf rsb, rspk, rseed, rtid, rtsc, rth, rqb, rqn, rhp, rcd, rcc, rov, rovn, rpt;
+    if (use_rtc &&
+        (rsb.alloc((size_t)Qmax * 4, s) || rspk.alloc((size_t)Qmax * 4, s) ||
+         rseed.alloc((size_t)Qmax * KS * 4, s) || rtid.alloc((size_t)Qmax * k * 8, s) ||
+         rtsc.alloc((size_t)Qmax * k * 4, s) || rth.alloc((size_t)Qmax * 4, s) ||
+         rqb.alloc((size_t)Qmax * ix->dpb * 2, s) || rqn.alloc((size_t)Qmax * 4, s) ||
+         rhp.alloc(gt_heap_bytes(k), s) || rcd.alloc((size_t)Qmax * Cg * 4, s) ||
+         rcc.alloc((size_t)Qmax * 4, s) || rov.alloc((size_t)nq * 8, s) || rovn.alloc(4, s) ||
+         rpt.alloc(std::max(rerank_partial_bytes(Qmax, Cg, k), rerank_partial_bytes(Qmax, KS, k)), s)))
+        return fail(NRLSH_ENOMEM, "query workspace (tensor-core re-rank)");
+    if (use_rtc) cudaMemsetAsync(rovn.p, 0, 4, s);
+    GtMember mb;
+    mb.codes_id = ix->codes_id;
+    mb.part_id = ix->part_of_id;
+    mb.pos_of_id = ix->pos_of_id;
+    mb.R = ix->R_d;
+    mb.L = ix->L;
+    mb.W = ix->W;
     const int init_flags[8] = {INT_MAX, INT_MAX, 0, 0, 0, 0, 0, 0};
     cudaMemcpyAsync(fl.p, init_flags, 32, cudaMemcpyHostToDevice, s);
     unsigned long long *pairs = (unsigned long long *)(fl.get<int>() + 4);
@@ -557,10 +615,43 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
         run_candidates(ix, Qd, qcodes_user ? (const uint32_t *)QCs.dev : nullptr, Qb, q0, Tq,
                        stride, C, qc.get<uint32_t>(), dl.get<int8_t>(), cn.get<uint32_t>(),
                        cv.get<uint32_t>(), ba.get<uint8_t>(), bf.get<unsigned long long>(), cand,
-                       crank, fl.get<int>(), pairs, s, use_dense ? sb.get<uint32_t>() : nullptr,
-                       use_dense ? spk.get<uint32_t>() : nullptr,
-                       use_dense ? cpart.get<uint32_t>() : nullptr);
-        if (use_dense) {
+                       crank, fl.get<int>(), pairs, s,
+                       use_dense ? sb.get<uint32_t>() : (use_rtc ? rsb.get<uint32_t>() : nullptr),
+                       use_dense ? spk.get<uint32_t>() : (use_rtc ? rspk.get<uint32_t>() : nullptr),
+                       use_dense ? cpart.get<uint32_t>() : nullptr,
+                       use_rtc ? rseed.get<int32_t>() : nullptr, KS);
+        if (use_rtc) {
+            {
+                ProfScope p(SLOT_SCORE, s);
+                // certified warm start: the k-th best fp32 score (the final re-rank's own
+                // arithmetic) over KS best-ranked candidates bounds the answer's k-th score
+                launch_rerank(Xr, ix->d, ldr, Qd, Qb, rseed.get<int32_t>(), KS, KS, nullptr, 1, k,
+                              rpt.get<unsigned long long>(), rtid.get<int64_t>(), rtsc.get<float>(), s);
+                launch_theta_from_topk(rtid.get<int64_t>(), rtsc.get<float>(), Qb, k,
+                                       rth.get<uint32_t>(), s);
+            }
+            ProfScope p(SLOT_RERANK, s);
+            launch_bf16_prep(Qd, Qb, ix->d, ix->dpb, rqb.p, rqn.get<float>(), s);
+            cudaMemsetAsync(rcc.p, 0, (size_t)Qb * 4, s);
+            mb.qcodes = qc.get<uint32_t>();
+            mb.sel_B = rsb.get<uint32_t>();
+            mb.sel_pk = rspk.get<uint32_t>();
+            if (launch_gt_filter_tc(ix->Xb, n, ix->d, ix->dpb, rqb.p, Qb, ix->xnorm,
+                                    rqn.get<float>(), gt_eps_rel(ix->dpb), k, rth.get<uint32_t>(),
+                                    rhp.get<float>(), rcd.get<int32_t>(), rcc.get<uint32_t>(), Cg,
+                                    s, &mb))
+                return fail(NRLSH_ECUDA, "tensor map encoding failed");
+            // exact fp32 re-rank of the surviving candidates (same arithmetic as the
+            // gather path: identical scores and order)
+            ProfScope p2(SLOT_RERANK_TOPK, s);
+            launch_rerank(Xr, ix->d, ldr, Qd, Qb, rcd.get<int32_t>(), Cg, Cg, rcc.get<uint32_t>(),
+                          1, k, rpt.get<unsigned long long>(), (int64_t *)oi.dev + q0 * k,
+                          (float *)os.dev + q0 * k, s);
+            launch_collect_overflow(rcc.get<uint32_t>(), Qb, Cg, q0, rov.get<int64_t>(),
+                                    rovn.get<uint32_t>(), s);
+            // survivors re-scored in fp32 (incl. the unused slots of their last chunk)
+            launch_sum_counts(rcc.get<uint32_t>(), Qb, Cg, (unsigned long long *)(fl.get<int>() + 6), s);
+        } else if (use_dense) {
             {
                 ProfScope p(SLOT_SELECT, s);
                 launch_dense_decide(cpart.get<uint32_t>(), ix->offsets_d, ix->m, Qb, dense_frac,
@@ -597,6 +688,26 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
                               (float *)os.dev + q0 * k, s);
         }
     }
+    if (use_rtc) {   // queries whose survivor list overflowed (rare): the gather path
+        uint32_t nov = 0;
+        cudaMemcpyAsync(&nov, rovn.p, 4, cudaMemcpyDeviceToHost, s);
+        if ((e = cudaStreamSynchronize(s))) return cuda_fail(e, "query (re-rank overflow)");
+        g_last_rtc_overflow = nov;
+        if (nov) {
+            std::vector<int64_t> ql(nov);
+            cudaMemcpy(ql.data(), rov.p, (size_t)nov * 8, cudaMemcpyDeviceToHost);
+            g_in_rtc_redo = true;
+            for (int64_t qi : ql) {
+                const nrlsh_status st = query_impl(
+                    ix, (const float *)Qs.dev + qi * ix->d, nullptr, 1, k, probe_budget,
+                    (int64_t *)oi.dev + qi * k, (float *)os.dev + qi * k, nullptr, nullptr, s);
+                if (st != NRLSH_OK) { g_in_rtc_redo = false; return st; }
+            }
+            g_in_rtc_redo = false;
+        }
+    } else if (!g_in_rtc_redo) {
+        g_last_rtc_overflow = 0;
+    }
     if (want_topk) {
         if ((e = oi.finish(s)) || (e = os.finish(s))) return cuda_fail(e, "copy results");
     }
@@ -618,6 +729,11 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
     g_last_pairs = (int64_t)pr;
     std::memcpy(&pr, hflags + 6, 8);
     g_last_rescored = (int64_t)pr;
+    if (!g_in_rtc_redo)
+        g_last_rtc = use_rtc ? NRLSH_RERANK_TENSOR
+                             : (use_dense ? NRLSH_RERANK_DENSE
+                                          : (ix->Xb && getenv("NRLSH_RERANK_BF16") ? NRLSH_RERANK_GATHER_BF16
+                                                                               : NRLSH_RERANK_GATHER));
     return check_flags(hflags);
 }
 
@@ -669,6 +785,12 @@ nrlsh_status nrlsh_last_rerank_stats(int64_t *rescored_fp32) {
     return NRLSH_OK;
 }
 
+nrlsh_status nrlsh_last_rerank_path(int32_t *path, int64_t *overflow_redone) {
+    if (path) *path = (int32_t)g_last_rtc;
+    if (overflow_redone) *overflow_redone = g_last_rtc_overflow;
+    return NRLSH_OK;
+}
+
 nrlsh_status nrlsh_last_query_stats(int64_t *fallback_queries, int64_t *kernel_launches,
                                     int64_t *scanned_pairs) {
     if (fallback_queries) *fallback_queries = g_last_fallbacks;
@@ -706,13 +828,9 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
     const bool use_tc = gt_tc_supported(d, k) && !getenv("NRLSH_GT_SIMT");
     const int dp = (d + 7) / 8 * 8;
     // certified error bound of fl(q.x) relative to |q||x|:
-    //  tensor path: bf16 operands (u = 2^-8: 2u + u^2) + fp32 accumulation of dp
-    //  exact products (dp * 2^-23 with truncating adds), x1.05 slack;
-    //  SIMT path: fp32 FMA chain, gamma_d inflated.
-    const double u = std::ldexp(1.0, -8);
-    const float eps_rel = use_tc ? (float)(1.05 * ((2 * u + u * u) + (1 + u) * (1 + u) * dp *
-                                                   std::ldexp(1.0, -23)))
-                                 : (float)(1.25 * (d + 2) * std::ldexp(1.0, -24));
+    //  tensor path: gt_eps_rel (bf16 operands, fp32 accumulation, + the fp32
+    //  re-rank's own error); SIMT path: fp32 FMA chain, gamma_d inflated.
+    const float eps_rel = use_tc ? gt_eps_rel(dp) : (float)(1.25 * (d + 2) * std::ldexp(1.0, -24));
     const int S = (int)std::max<int64_t>(1, std::min<int64_t>(64, n / (4 * (int64_t)k)));
     const int64_t ns = use_tc ? 1 : (n + S - 1) / S;
     const int64_t Cg = use_tc ? std::min<int64_t>(n, std::max<int64_t>(16384, 256 * (int64_t)k))
@@ -889,6 +1007,8 @@ nrlsh_status nrlsh_set_codes(nrlsh_index *ix, const uint32_t *codes) {
     if (!ix || !codes) return fail(NRLSH_EINVAL, "bad argument");
     cudaError_t e = cudaMemcpy(ix->codes, codes, (size_t)ix->n * ix->W * 4, cudaMemcpyDefault);
     if (e) return cuda_fail(e, "set codes");
+    launch_codes_by_id(ix, nullptr);
+    if ((e = cudaDeviceSynchronize())) return cuda_fail(e, "set codes (item order)");
     if (ix->samp_codes) {   // keep the pilot sample in step with the codes
         launch_gather_sample(ix, pilot_stride(ix->n), ix->samp_codes, ix->samp_part, nullptr);
         if ((e = cudaDeviceSynchronize())) return cuda_fail(e, "set codes (sample)");

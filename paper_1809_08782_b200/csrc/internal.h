@@ -32,11 +32,13 @@ struct nrlsh_index {
     double *norm2 = nullptr;      // [n] item order
     int32_t *perm = nullptr;      // [n] position -> id
     int32_t *pos_of_id = nullptr; // [n] id -> position
-    uint8_t *part_of_id = nullptr;  // [n]
+    uint8_t *part_of_id = nullptr;  // [n rounded up to 256] (0 past n)
     uint8_t *part_of_pos = nullptr; // [n]
     int64_t *offsets_d = nullptr;   // [m+1]
     double *V_d = nullptr;          // [m]
     uint32_t *codes = nullptr;      // [n x W], partition order
+    uint32_t *codes_id = nullptr;   // [n rounded up to 256 x W], item order (0 past n): the
+                                    //   tensor-core re-rank's membership test
     float *A = nullptr;             // [(d+1) x L] row-major (as generated)
     float *Apad = nullptr;          // [(d+1) x 32W], zero columns >= L
     uint16_t *R_d = nullptr;        // [m x (L+1)]
@@ -184,6 +186,23 @@ void launch_dense_merge(const unsigned long long *partial, int S, int k, const i
                         const float *g_sc, int Qb, int64_t *out_ids, float *out_scores,
                         cudaStream_t s);
 
+// item-order copy of the codes (codes_id[i] = codes[pos_of_id[i]])
+void launch_codes_by_id(const nrlsh_index *ix, cudaStream_t s);
+// theta_glob[q] = orderable image of out_scores[q][k-1] when that slot holds an item
+void launch_theta_from_topk(const int64_t *ids, const float *scores, int Qb, int k,
+                            uint32_t *theta_glob, cudaStream_t s);
+// *out += sum_q min(cnt[q], C)
+void launch_sum_counts(const uint32_t *cnt, int Qb, int64_t C, unsigned long long *out,
+                       cudaStream_t s);
+// appends q0 + q to list (count at *n) for every q with cnt[q] > C
+void launch_collect_overflow(const uint32_t *cnt, int Qb, int64_t C, int64_t q0, int64_t *list,
+                             uint32_t *n, cudaStream_t s);
+// select bound pass that also picks `ks` seed members per query: members in the
+// best-ranked structure positions (int32 ids, -1 padded)
+void launch_select_seeds(const nrlsh_index *ix, int Qb, int64_t Tq, const unsigned long long *buf,
+                         const uint32_t *cnt, int64_t C, uint32_t *sel_B, uint32_t *sel_pk,
+                         int32_t *seeds, int ks, cudaStream_t s);
+
 // ---------------------------------------------------------------- ground truth
 void launch_vec_norms(const float *X, int64_t n, int d, float *xnorm, cudaStream_t s);
 void launch_gt_filter(const float *X, int64_t n, int d, const float *Q, int Qb,
@@ -198,9 +217,20 @@ void launch_bf16_prep(const float *X, int64_t n, int d, int dp, void *Xb, float 
                       cudaStream_t s);
 bool gt_tc_supported(int d, int k);
 size_t gt_heap_bytes(int k);
+// Candidate membership for the tensor-core re-rank (the select's rule): item i is a
+// candidate of query q iff r = R[part(i)][h(q,i)] < B_q or (r == B_q and pos(i) <= pk_q)
+struct GtMember {
+    const uint32_t *codes_id;   // [npad x W] item order
+    const uint8_t *part_id;     // [npad]
+    const int32_t *pos_of_id;   // [n]
+    const uint16_t *R;          // [m x (L+1)]
+    int L, W;
+    const uint32_t *qcodes;     // [Qb x W]
+    const uint32_t *sel_B, *sel_pk;   // [Qb]
+};
 int launch_gt_filter_tc(const void *Xb, int64_t n, int d, int dp, const void *Qb16, int Qb,
                         const float *xnorm, const float *qnorm, float eps_rel, int k,
                         uint32_t *theta_glob, float *heap, int32_t *cand, uint32_t *cnt,
-                        int64_t C, cudaStream_t s);
+                        int64_t C, cudaStream_t s, const GtMember *member = nullptr);
 
 }  // namespace nrlsh

@@ -435,12 +435,13 @@ __global__ void __launch_bounds__(1024) k7_select(
     const int32_t *__restrict__ perm, int32_t *__restrict__ cand,
     uint16_t *__restrict__ cand_rank, int mode, int L, uint32_t *__restrict__ sel_B,
     uint32_t *__restrict__ sel_pk, uint32_t *__restrict__ cnt_part,
-    const uint8_t *__restrict__ dense, uint32_t *__restrict__ ncand_out) {
+    const uint8_t *__restrict__ dense, uint32_t *__restrict__ ncand_out,
+    int32_t *__restrict__ seeds, int ks) {
     extern __shared__ uint32_t hist[];   // [max(NR, tie_cap)] + R copy [NR] (uint16)
     uint16_t *sRt = reinterpret_cast<uint16_t *>(hist + tie_cap);
     __shared__ uint32_t ws[32];
     __shared__ uint32_t h256[256];
-    __shared__ int sB;
+    __shared__ int sB, s_bseed;
     __shared__ uint32_t sLt, s_out, s_pfx, s_kth;
     const int q = blockIdx.x;
     const int64_t c = min((int64_t)cnt[q], C);
@@ -465,7 +466,7 @@ __global__ void __launch_bounds__(1024) k7_select(
         return;
     }
     for (int e = threadIdx.x; e < NR; e += blockDim.x) { hist[e] = 0u; sRt[e] = R[e]; }
-    if (threadIdx.x == 0) { sB = NR - 1; sLt = 0; s_out = 0; }
+    if (threadIdx.x == 0) { sB = NR - 1; sLt = 0; s_out = 0; s_bseed = NR - 1; }
     __syncthreads();
     // entries carry the flat (j, h) index; R maps it to the structure position
     // (~0 = unused append slot of the tensor-core scan)
@@ -486,6 +487,22 @@ __global__ void __launch_bounds__(1024) k7_select(
             uint32_t cc = ex;
             for (int r = r0; r < r1; ++r) {
                 if (cc + hist[r] >= need) { sB = r; sLt = cc; break; }
+                cc += hist[r];
+            }
+        }
+        __syncthreads();
+    }
+    if (seeds) {   // structure position holding the ks-th best-ranked entry
+        const int seg = (NR + blockDim.x - 1) / blockDim.x;
+        const int r0 = threadIdx.x * seg, r1 = min(NR, r0 + seg);
+        uint32_t loc = 0;
+        for (int r = r0; r < r1; ++r) loc += hist[r];
+        uint32_t tot;
+        const uint32_t ex = block_excl_scan(loc, ws, &tot);
+        if (ex < (uint32_t)ks && ex + loc >= (uint32_t)ks) {
+            uint32_t cc = ex;
+            for (int r = r0; r < r1; ++r) {
+                if (cc + hist[r] >= (uint32_t)ks) { s_bseed = r; break; }
                 cc += hist[r];
             }
         }
@@ -587,6 +604,24 @@ __global__ void __launch_bounds__(1024) k7_select(
     const uint32_t pk = s_pfx;
     if (mode == 1) {
         if (threadIdx.x == 0) { sel_B[q] = B; sel_pk[q] = pk; }
+        if (seeds) {   // up to ks candidates among the best-ranked structure positions
+            if (threadIdx.x == 0) s_out = 0;
+            __syncthreads();
+            const uint32_t Bs = (uint32_t)s_bseed;
+            for (int64_t e = threadIdx.x; e < c; e += blockDim.x) {
+                const unsigned long long v = b[e];
+                const uint32_t f = (uint32_t)(v >> 32), pos = (uint32_t)v;
+                if (f >= (uint32_t)NR) continue;
+                const uint32_t r = sRt[f];
+                if (r <= Bs && (r < B || (r == B && pos <= pk))) {
+                    const uint32_t slot = atomicAdd(&s_out, 1u);
+                    if (slot < (uint32_t)ks) seeds[(int64_t)q * ks + slot] = perm[pos];
+                }
+            }
+            __syncthreads();
+            for (uint32_t t = s_out + threadIdx.x; t < (uint32_t)ks; t += blockDim.x)
+                seeds[(int64_t)q * ks + t] = -1;
+        }
         return;
     }
     for (int64_t e = threadIdx.x; e < c; e += blockDim.x) {
@@ -612,7 +647,7 @@ void launch_select(const nrlsh_index *ix, int Qb, int64_t Tq, const unsigned lon
     const size_t sm = (size_t)tie_cap * 4 + (size_t)NR * 2;
     cudaFuncSetAttribute(k7_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     k7_select<<<Qb, 1024, sm, s>>>(buf, cnt, C, Tq, NR, tie_cap, ix->R_d, ix->perm, cand, cand_rank,
-                                   0, ix->L, nullptr, nullptr, nullptr, nullptr, nullptr);
+                                   0, ix->L, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0);
     note_launch();
 }
 
@@ -626,7 +661,83 @@ void launch_select_split(const nrlsh_index *ix, int Qb, int64_t Tq, const unsign
     const size_t sm = (size_t)tie_cap * 4 + (size_t)NR * 2;
     cudaFuncSetAttribute(k7_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     k7_select<<<Qb, 1024, sm, s>>>(buf, cnt, C, Tq, NR, tie_cap, ix->R_d, ix->perm, cand, nullptr,
-                                   mode, ix->L, sel_B, sel_pk, cnt_part, dense, ncand_out);
+                                   mode, ix->L, sel_B, sel_pk, cnt_part, dense, ncand_out, nullptr, 0);
+    note_launch();
+}
+
+void launch_select_seeds(const nrlsh_index *ix, int Qb, int64_t Tq, const unsigned long long *buf,
+                         const uint32_t *cnt, int64_t C, uint32_t *sel_B, uint32_t *sel_pk,
+                         int32_t *seeds, int ks, cudaStream_t s) {
+    const int NR = ix->m * (ix->L + 1);
+    const int tie_cap = std::max(NR, 16384);
+    const size_t sm = (size_t)tie_cap * 4 + (size_t)NR * 2;
+    cudaFuncSetAttribute(k7_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k7_select<<<Qb, 1024, sm, s>>>(buf, cnt, C, Tq, NR, tie_cap, ix->R_d, ix->perm, nullptr, nullptr,
+                                   1, ix->L, sel_B, sel_pk, nullptr, nullptr, nullptr, seeds, ks);
+    note_launch();
+}
+
+// ------------------------------------------------------- tensor-core re-rank helpers
+template <int W>
+__global__ void codes_by_id(const uint32_t *__restrict__ codes, const int32_t *__restrict__ pos_of_id,
+                            int64_t n, uint32_t *__restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t c[W];
+        load_code<W>(codes, pos_of_id[i], c);
+#pragma unroll
+        for (int w = 0; w < W; ++w) out[i * W + w] = c[w];
+    }
+}
+
+void launch_codes_by_id(const nrlsh_index *ix, cudaStream_t s) {
+    const int grid = grid_for(ix->n, 256, 4096);
+    switch (ix->W) {
+        case 1: codes_by_id<1><<<grid, 256, 0, s>>>(ix->codes, ix->pos_of_id, ix->n, ix->codes_id); break;
+        case 2: codes_by_id<2><<<grid, 256, 0, s>>>(ix->codes, ix->pos_of_id, ix->n, ix->codes_id); break;
+        default: codes_by_id<4><<<grid, 256, 0, s>>>(ix->codes, ix->pos_of_id, ix->n, ix->codes_id); break;
+    }
+    note_launch();
+}
+
+__global__ void theta_from_topk(const int64_t *__restrict__ ids, const float *__restrict__ sc, int Qb,
+                                int k, uint32_t *__restrict__ theta_glob) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= Qb) return;
+    const int64_t e = (int64_t)q * k + k - 1;
+    theta_glob[q] = ids[e] >= 0 ? float_order(sc[e]) : 0u;
+}
+
+void launch_theta_from_topk(const int64_t *ids, const float *scores, int Qb, int k,
+                            uint32_t *theta_glob, cudaStream_t s) {
+    theta_from_topk<<<(Qb + 255) / 256, 256, 0, s>>>(ids, scores, Qb, k, theta_glob);
+    note_launch();
+}
+
+__global__ void collect_overflow(const uint32_t *__restrict__ cnt, int Qb, int64_t C, int64_t q0,
+                                 int64_t *__restrict__ list, uint32_t *__restrict__ n) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q < Qb && (int64_t)cnt[q] > C) list[atomicAdd(n, 1u)] = q0 + q;
+}
+
+__global__ void sum_counts(const uint32_t *__restrict__ cnt, int Qb, int64_t C,
+                           unsigned long long *__restrict__ out) {
+    unsigned long long v = 0;
+    for (int q = threadIdx.x; q < Qb; q += blockDim.x) v += (unsigned long long)min((int64_t)cnt[q], C);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(NR_FULL, v, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out, v);
+}
+
+void launch_sum_counts(const uint32_t *cnt, int Qb, int64_t C, unsigned long long *out,
+                       cudaStream_t s) {
+    sum_counts<<<1, 256, 0, s>>>(cnt, Qb, C, out);
+    note_launch();
+}
+
+void launch_collect_overflow(const uint32_t *cnt, int Qb, int64_t C, int64_t q0, int64_t *list,
+                             uint32_t *n, cudaStream_t s) {
+    collect_overflow<<<(Qb + 255) / 256, 256, 0, s>>>(cnt, Qb, C, q0, list, n);
     note_launch();
 }
 

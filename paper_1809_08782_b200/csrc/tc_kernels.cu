@@ -91,22 +91,22 @@ static bool make_tmap(CUtensorMap *m, const void *base, CUtensorMapDataType dt, 
 
 // ------------------------------------------------------------ the kernel
 // CTA unit = (pair of 128-query blocks, split of the items).  The two query blocks
-// stay resident in smem (A operands, K-major, 128B-swizzled); every 128-item tile
+// stay resident in smem (A operands, K-major, 128B-swizzled); every 256-item tile
 // of X (B operand) is TMA-loaded once and multiplied into two TMEM accumulators
-// (one per query block), so each X byte fetched from L2 feeds 256 query rows.
-// TMEM: 2 buffers x 2 query blocks x 128 fp32 columns = 512 columns.
+// (one per query block, M=128 x N=256 MMAs: the N that runs the tensor core at its
+// full rate), so each X byte fetched from L2 feeds 256 query rows.
+// TMEM: 2 query blocks x 256 fp32 columns = all 512 columns, single-buffered: a
+// block's next tile waits for its epilogue warps to drain it (an M=128 x N=128 MMA
+// runs at half rate, so halving N for double buffering costs more).  Rows longer
+// than 192 bf16 leave no room for a 3-deep ring of 32 KB tiles: NT = 128 there,
+// double-buffered.
 constexpr int GT_M = 128;          // queries per block (TMEM lanes)
-constexpr int GT_QB = 2;           // query blocks per CTA (1 or 2)
-constexpr int GT_N = 128;          // items per tile (fp32 TMEM columns per accumulator)
-constexpr int GT_EPI_SUB = 2 / GT_QB;   // epilogue warps per TMEM lane quadrant and query block
-constexpr int GT_EPI_COLS = GT_N / GT_EPI_SUB;
-static_assert(GT_EPI_COLS == 128, "epilogue thread = one 128-column slice of a query row");
+constexpr int GT_QB = 2;           // query blocks per CTA
 constexpr int GT_KB = 64;          // bf16 per K block (128-byte swizzled rows)
 constexpr int GT_MAX_STAGES = 8;
-constexpr int GT_PREFETCH = 6;        // item tiles prefetched into L2 ahead of the ring
+constexpr int GT_PREFETCH = 0;        // L2 prefetch distance (tiles): measured harmful
 constexpr int GT_A_BLK = GT_M * 128;   // 16 KB
-constexpr int GT_B_BLK = GT_N * 128;   // 16 KB
-constexpr int GT_THREADS = 384;        // warps 0-3 control, 4-11 epilogue
+constexpr int GT_THREADS = 384;        // warps 0-3 control, 4-7 epilogue of block 0, 8-11 of block 1
 constexpr int GT_MAX_KBLK = 5;         // d <= 320
 constexpr int GT_MAX_K = 256;
 
@@ -127,54 +127,235 @@ struct GtArgs {
     int nqp;                // query-block pairs
     int nsplit;
     int64_t split_items;    // multiple of GT_N
-    int stages;             // B ring depth (3 or 4)
+    int stages;             // B ring depth
     int heap_smem;          // 1: heaps in shared memory, 0: global scratch
     int dbg;                // profiling experiments only (NRLSH_GT_DBG): 1 = skip the
                             // epilogue arithmetic, 2 = skip the TMEM reads too,
                             // 3 = also skip the MMAs (TMA stream only)
+    int prefetch;           // item tiles prefetched into L2 ahead of the ring
+    int kps;                // (pair kernel) K blocks per ring stage: 1 or kblocks
+    // candidate-membership mode (the tensor-core re-rank): survivors must also be
+    // candidates of their query; the running bound is over candidates only
+    int member;
+    const uint32_t *codes_id;
+    const uint8_t *part_id;
+    const int32_t *pos_of_id;
+    const uint16_t *R;
+    int L, W;
+    const uint32_t *qcodes;
+    const uint32_t *sel_B, *sel_pk;
 };
 
-__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+__device__ __forceinline__ float fmax3f(float a, float b, float c) {
+    float r;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
 }
 
+// Tiles of a unit's item range, in order (concurrent readers of one tile — the
+// CTAs of the other query pairs of the same split — share its L2 fetch; rotating
+// their start tiles was measured 20% slower).
+// Per-(query row, column range) epilogue state of the certified filter: the
+// running bound theta (k-th best lower bound s~ - e seen, or shared / warm-started),
+// the survivor list cursor and (member mode) the query's code and select bound.
+struct GtEpiRow {
+    const GtArgs *a;
+    int q;
+    bool vq;
+    float qe, theta, thr_adj, pub;
+    int hs;
+    float *hp;
+    int32_t *cl;
+    uint32_t sbase, sleft;
+    uint32_t qcw[4], Bq, pkq;
 
-// Tiles of a unit's item range in a rotated order: the CTAs of the different query
-// blocks that share an item split start at different tiles, so they do not all
-// request the same L2 lines at the same time.
-__device__ __forceinline__ int64_t gt_tile_at(int64_t ib, int64_t ie, int qp, int nqp, int64_t jt) {
-    const int64_t nt = (ie - ib + GT_N - 1) / GT_N;
-    const int64_t rot = 0;   // measured: concurrent readers of one tile share its L2
-                             // fetch; rotating the start (nt * qp / nqp) was 20% slower
-    int64_t j = jt + rot;
-    if (j >= nt) j -= nt;
-    return ib + j * GT_N;
+    __device__ __forceinline__ void set_theta(float th) {
+        // the hot-loop test uses a round-to-nearest FMA; thr_adj absorbs its rounding
+        // (<= 2^-24 |result| near the threshold) so the filter stays certified
+        theta = th;
+        thr_adj = th - fabsf(th) * 2.384185791015625e-7f;   // 2^-22
+    }
+    __device__ __forceinline__ void begin(const GtArgs &args, int q_, bool vq_, float *heap_) {
+        a = &args;
+        q = q_;
+        vq = vq_;
+        qe = vq ? args.eps_rel * args.qnorm[q] : 0.f;
+        theta = -INFINITY;
+        thr_adj = -INFINITY;
+        pub = -INFINITY;
+        hs = 0;
+        hp = heap_;
+        // survivors go to 16-slot chunks of the query's list reserved with one
+        // atomic each; unused slots of the last chunk are filled with -1
+        cl = args.cand + (int64_t)(vq ? q : 0) * args.C;
+        sbase = 0;
+        sleft = 0;
+        qcw[0] = qcw[1] = qcw[2] = qcw[3] = 0u;
+        Bq = pkq = 0u;
+        if (vq) {
+            const uint32_t o = args.theta_glob[q];
+            if (o) set_theta(float_unorder(o));
+            if (args.member) {
+#pragma unroll
+                for (int w = 0; w < 4; ++w)
+                    if (w < args.W) qcw[w] = args.qcodes[(int64_t)q * args.W + w];
+                Bq = args.sel_B[q];
+                pkq = args.sel_pk[q];
+            }
+        }
+    }
+    __device__ __forceinline__ void end() {
+        for (; sleft > 0; --sleft)
+            if (sbase + (16 - sleft) < a->C) cl[sbase + (16 - sleft)] = -1;
+    }
+    // share the bound across CTAs (called every few tiles; o_next was loaded earlier)
+    __device__ __forceinline__ void share(uint32_t o_next) {
+        if (hs == a->k && hp[0] > pub) {
+            pub = hp[0];
+            atomicMax(&a->theta_glob[q], float_order(pub));
+        }
+        if (o_next) {
+            const float g = float_unorder(o_next);
+            if (g > theta) set_theta(g);
+        }
+    }
+    // 64 accumulator columns [c, c+64) of the row (r0: c..c+31, r1: c+32..c+63) of the
+    // tile starting at item i0; xn = the tile's |x| (rounded up), xmax = its largest
+    // over the chunk's columns; scode/spart = the tile's codes / sub-datasets.
+    __device__ __forceinline__ void chunk(const uint32_t (&r0)[32], const uint32_t (&r1)[32], int c,
+                                          const float *xn, float xmax, int64_t i0,
+                                          const uint32_t *scode, const uint8_t *spart) {
+        const float thr_tile = __fmaf_rd(-xmax, qe, thr_adj);
+        // cheap screen: max of the 64 approximate scores against the threshold
+        // loosened by the chunk's largest error term
+        float m0 = __uint_as_float(r0[0]), m1 = __uint_as_float(r1[0]);
+        float m2 = __uint_as_float(r0[1]), m3 = __uint_as_float(r1[1]);
+#pragma unroll
+        for (int j = 2; j < 32; j += 4) {   // 3-input max (FMNMX3)
+            m0 = fmax3f(m0, __uint_as_float(r0[j]), __uint_as_float(r0[j + 1]));
+            m1 = fmax3f(m1, __uint_as_float(r1[j]), __uint_as_float(r1[j + 1]));
+            if (j + 3 < 32) {
+                m2 = fmax3f(m2, __uint_as_float(r0[j + 2]), __uint_as_float(r0[j + 3]));
+                m3 = fmax3f(m3, __uint_as_float(r1[j + 2]), __uint_as_float(r1[j + 3]));
+            }
+        }
+        if (fmax3f(fmaxf(m0, m1), m2, m3) < thr_tile) return;
+        const float4 *x4 = reinterpret_cast<const float4 *>(xn + c);
+        unsigned hit = 0u, hit2 = 0u;
+#pragma unroll
+        for (int j4 = 0; j4 < 8; ++j4) {
+            const float4 xa = x4[j4];
+            const float4 xb = x4[j4 + 8];
+            hit |= (fmaf(xa.x, qe, __uint_as_float(r0[4 * j4 + 0])) >= thr_adj) << (4 * j4 + 0);
+            hit |= (fmaf(xa.y, qe, __uint_as_float(r0[4 * j4 + 1])) >= thr_adj) << (4 * j4 + 1);
+            hit |= (fmaf(xa.z, qe, __uint_as_float(r0[4 * j4 + 2])) >= thr_adj) << (4 * j4 + 2);
+            hit |= (fmaf(xa.w, qe, __uint_as_float(r0[4 * j4 + 3])) >= thr_adj) << (4 * j4 + 3);
+            hit2 |= (fmaf(xb.x, qe, __uint_as_float(r1[4 * j4 + 0])) >= thr_adj) << (4 * j4 + 0);
+            hit2 |= (fmaf(xb.y, qe, __uint_as_float(r1[4 * j4 + 1])) >= thr_adj) << (4 * j4 + 1);
+            hit2 |= (fmaf(xb.z, qe, __uint_as_float(r1[4 * j4 + 2])) >= thr_adj) << (4 * j4 + 2);
+            hit2 |= (fmaf(xb.w, qe, __uint_as_float(r1[4 * j4 + 3])) >= thr_adj) << (4 * j4 + 3);
+        }
+        // rare path: survivors (pushed + fed to the running top-k bound)
+        for (int hh = 0; hh < 2; ++hh) {
+            unsigned m = hh ? hit2 : hit;
+            while (m) {
+                const int j = __ffs(m) - 1;
+                m &= m - 1;
+                const int col = c + 32 * hh + j;
+                float s_j = 0.f;
+#pragma unroll
+                for (int jj = 0; jj < 32; ++jj)
+                    if (jj == j) s_j = __uint_as_float(hh ? r1[jj] : r0[jj]);
+                const float x = xn[col];
+                if (__fmaf_ru(x, qe, s_j) < theta) continue;   // exact re-test
+                const int64_t i = i0 + col;
+                if (i >= a->n) continue;
+                if (a->member) {   // candidate of q? (the select's rule)
+                    const uint32_t *cw = scode + col * a->W;
+                    int hq = 0;
+#pragma unroll
+                    for (int w = 0; w < 4; ++w)
+                        if (w < a->W) hq += __popc(cw[w] ^ qcw[w]);
+                    const uint32_t r = __ldg(a->R + spart[col] * (a->L + 1) + hq);
+                    if (!(r < Bq || (r == Bq && (uint32_t)__ldg(a->pos_of_id + i) <= pkq))) continue;
+                }
+                if (sleft == 0) { sbase = atomicAdd(&a->cnt[q], 16u); sleft = 16; }
+                if (sbase + (16 - sleft) < a->C) cl[sbase + (16 - sleft)] = (int32_t)i;
+                --sleft;
+                const float lb = __fmaf_rd(-x, qe, s_j);
+                const int k = a->k;
+                if (hs < k) {            // min-heap push
+                    int p = hs++;
+                    while (p > 0) {
+                        const int par = (p - 1) >> 1;
+                        if (hp[par] <= lb) break;
+                        hp[p] = hp[par];
+                        p = par;
+                    }
+                    hp[p] = lb;
+                    if (hs == k && hp[0] > theta) set_theta(hp[0]);
+                } else if (lb > hp[0]) { // replace the minimum
+                    int p = 0;
+                    while (true) {
+                        int ch = 2 * p + 1;
+                        if (ch >= k) break;
+                        if (ch + 1 < k && hp[ch + 1] < hp[ch]) ++ch;
+                        if (hp[ch] >= lb) break;
+                        hp[p] = hp[ch];
+                        p = ch;
+                    }
+                    hp[p] = lb;
+                    if (hp[0] > theta) set_theta(hp[0]);
+                }
+            }
+        }
+    }
+};
+
+// largest |x| over 128 consecutive entries (one warp, 4 per lane)
+__device__ __forceinline__ float warp_max128(const float *xn, int lane) {
+    const float4 xv = reinterpret_cast<const float4 *>(xn)[lane];
+    float m = fmaxf(fmaxf(xv.x, xv.y), fmaxf(xv.z, xv.w));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(NR_FULL, m, o));
+    return m;
 }
 
+template <int NT>
 __global__ void __launch_bounds__(GT_THREADS, 1)
     gt_filter_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmX,
                  GtArgs a) {
+    constexpr int GT_N = NT;                     // items per tile
+    constexpr int GT_B_BLK = NT * 128;           // one K block of a tile
+    constexpr int NBUF = 512 / (GT_QB * NT);     // TMEM accumulator buffers per block
+    auto gt_tile_at = [&](int64_t ib, int64_t jt) -> int64_t { return ib + jt * GT_N; };
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
     uint8_t *sA = smem;                                        // QB x kblocks x 16 KB
-    uint8_t *sB = sA + GT_QB * a.kblocks * GT_A_BLK;           // stages x 16 KB
-    float *sxn = (float *)(sB + a.stages * GT_B_BLK);          // [2][GT_N]
-    uint64_t *bars = (uint64_t *)(sxn + 2 * GT_N);
+    uint8_t *sB = sA + GT_QB * a.kblocks * GT_A_BLK;           // stages x 32 KB
+    float *sxn = (float *)(sB + a.stages * GT_B_BLK);          // [2][GT_N] |x| tiles
+    uint32_t *scode = (uint32_t *)(sxn + 2 * GT_N);            // [2][GT_N x W<=4] (member mode)
+    uint8_t *spart = (uint8_t *)(scode + 2 * GT_N * 4);        // [2][GT_N]        (member mode)
+    uint64_t *bars = (uint64_t *)(spart + 2 * GT_N);
     uint64_t *full = bars, *empty = bars + GT_MAX_STAGES;
     uint64_t *a_full = bars + 2 * GT_MAX_STAGES, *a_empty = a_full + 1;
-    uint64_t *tfull = a_empty + 1, *tempty = tfull + 2;
-    uint64_t *xfull = tempty + 2;                              // xnorm tile landed
-    uint32_t *tmem_slot = (uint32_t *)(xfull + 2);
+    uint64_t *tfull = a_empty + 1, *tempty = tfull + 4;        // [NBUF][GT_QB]
+    uint64_t *xfull = tempty + 4, *xempty = xfull + 2;         // per |x| tile buffer
+    uint32_t *tmem_slot = (uint32_t *)(xempty + 2);
+    float *sheap = reinterpret_cast<float *>(tmem_slot + 4);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int s = 0; s < a.stages; ++s) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
         tc::mbar_init(a_full, 1);
         tc::mbar_init(a_empty, 1);
-        for (int s = 0; s < 2; ++s) {
-            tc::mbar_init(&tfull[s], 1);
-            tc::mbar_init(&tempty[s], 8);
-            tc::mbar_init(&xfull[s], 1);
+        for (int h = 0; h < NBUF * GT_QB; ++h) {
+            tc::mbar_init(&tfull[h], 1);
+            tc::mbar_init(&tempty[h], 4);
+        }
+        for (int b = 0; b < 2; ++b) {
+            tc::mbar_init(&xfull[b], 1);
+            tc::mbar_init(&xempty[b], 8);
         }
         tc::fence_mbar_init();
     }
@@ -204,9 +385,9 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
                                     (qp * GT_QB + h) * GT_M);
             const int64_t ntu = (ie - ib + GT_N - 1) / GT_N;
             for (int64_t jt = 0; jt < ntu; ++jt) {
-                const int64_t i0 = gt_tile_at(ib, ie, qp, a.nqp, jt);
-                if (jt + GT_PREFETCH < ntu) {
-                    const int64_t ip = gt_tile_at(ib, ie, qp, a.nqp, jt + GT_PREFETCH);
+                const int64_t i0 = gt_tile_at(ib, jt);
+                if (a.prefetch > 0 && jt + a.prefetch < ntu) {
+                    const int64_t ip = gt_tile_at(ib, jt + a.prefetch);
                     for (int kb = 0; kb < a.kblocks; ++kb) tc::tma_prefetch_2d(&tmX, kb * GT_KB, (int)ip);
                 }
                 for (int kb = 0; kb < a.kblocks; ++kb, ++g) {
@@ -228,202 +409,113 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
             const int64_t ie = min(a.n, ib + a.split_items);
             tc::mbar_wait(a_full, ul & 1);
             tc::tc_fence_after();
-            for (int64_t i0 = ib; i0 < ie; i0 += GT_N, ++t) {   // (order irrelevant here)
-                const uint32_t acc = t & 1, tr = t >> 1;
-                tc::mbar_wait(&tempty[acc], (tr & 1) ^ 1);
-                tc::tc_fence_after();
+            for (int64_t i0 = ib; i0 < ie; i0 += GT_N, ++t) {
+                const uint32_t buf = t % NBUF, tr = t / NBUF;
                 for (int kb = 0; kb < a.kblocks; ++kb, ++g) {
                     const uint32_t s = g % a.stages, r = g / a.stages;
                     tc::mbar_wait(&full[s], r & 1);
                     tc::tc_fence_after();
                     const uint32_t bbase = tc::smem_u32(sB + s * GT_B_BLK);
                     const int nk = min(GT_KB / 16, (a.d - kb * GT_KB + 15) / 16);   // K = 16 per MMA
-                    for (int h = 0; h < nh; ++h) {
+                    // (every block's barriers advance once per tile, holding queries or
+                    // not, so their phases stay in step across units)
+                    for (int h = 0; h < GT_QB; ++h) {
+                        if (kb == 0) {   // the block's accumulator drained by its epilogue
+                            tc::mbar_wait(&tempty[buf * GT_QB + h], (tr & 1) ^ 1);
+                            tc::tc_fence_after();
+                        }
+                        if (h >= nh) continue;
                         const uint32_t abase = tc::smem_u32(sA + (h * a.kblocks + kb) * GT_A_BLK);
-                        const uint32_t dt = tmem_base + (acc * GT_QB + h) * GT_N;
+                        const uint32_t dt = tmem_base + (buf * GT_QB + h) * GT_N;
                         for (int kk = 0; kk < (a.dbg == 3 ? 0 : nk); ++kk)
                             tc::mma_f16_warp(dt, tc::umma_desc_sw128(abase + kk * 32),
-                                        tc::umma_desc_sw128(bbase + kk * 32), idesc, (kb | kk) != 0);
+                                             tc::umma_desc_sw128(bbase + kk * 32), idesc, (kb | kk) != 0);
                     }
                     tc::mma_commit_warp(&empty[s]);
                 }
-                tc::mma_commit_warp(&tfull[acc]);
+                for (int h = 0; h < GT_QB; ++h) tc::mma_commit_warp(&tfull[buf * GT_QB + h]);
             }
             tc::mma_commit_warp(a_empty);
         }
     } else if (warp == 3 && lane == 0) {
-        // ================= |x| tile loader: bulk copy per tile into the buffer of its
-        // TMEM stage, once the epilogue released that stage
+        // ================= |x| (and member-mode code / sub-dataset) tile loader: bulk
+        // copies into the tile's buffer once both epilogue groups released it
         uint32_t t = 0;
         for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
             const int sp = u / a.nqp;
             const int64_t ib = (int64_t)sp * a.split_items;
             const int64_t ie = min(a.n, ib + a.split_items);
-            const int qp = u % a.nqp;
             const int64_t ntu = (ie - ib + GT_N - 1) / GT_N;
             for (int64_t jt = 0; jt < ntu; ++jt, ++t) {
-                const int64_t i0 = gt_tile_at(ib, ie, qp, a.nqp, jt);
-                const uint32_t acc = t & 1, tr = t >> 1;
-                tc::mbar_wait(&tempty[acc], (tr & 1) ^ 1);
-                tc::mbar_arrive_expect_tx(&xfull[acc], GT_N * 4);
-                tc::bulk_load(sxn + acc * GT_N, a.xnorm + i0, GT_N * 4, &xfull[acc]);
+                const int64_t i0 = gt_tile_at(ib, jt);
+                const uint32_t b = t & 1, tr = t >> 1;
+                tc::mbar_wait(&xempty[b], (tr & 1) ^ 1);
+                tc::mbar_arrive_expect_tx(&xfull[b], GT_N * 4 + (a.member ? GT_N * (a.W * 4 + 1) : 0));
+                tc::bulk_load(sxn + b * GT_N, a.xnorm + i0, GT_N * 4, &xfull[b]);
+                if (a.member) {   // the tile's codes and sub-datasets (item order)
+                    tc::bulk_load(scode + b * GT_N * 4, a.codes_id + i0 * a.W, GT_N * a.W * 4, &xfull[b]);
+                    tc::bulk_load(spart + b * GT_N, a.part_id + i0, GT_N, &xfull[b]);
+                }
             }
         }
     } else if (warp >= 4) {
-        // ================= epilogue: thread <-> query row (TMEM lane); warps 4-7 own
-        // query block 0 of the pair, warps 8-11 block 1
-        // warps 4-11: lane quadrant = warp % 4; with two query blocks per CTA the
-        // upper four own block 1, with one block they own the upper half of the columns
+        // ================= epilogue: warps 4-7 drain query block 0, warps 8-11 block 1;
+        // thread <-> query row (TMEM lane quadrant = warp % 4), all NT columns
         const int grp = warp & 3;
-        const int esub = (warp - 4) >> 2;
-        const int h = GT_QB == 2 ? esub : 0;
-        const int c_lo = GT_QB == 2 ? 0 : esub * GT_EPI_COLS;
+        const int h = (warp - 4) >> 2;
         const int row = grp * 32 + lane;
         uint32_t t = 0;
+        GtEpiRow er;
         for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
             const int qp = u % a.nqp, sp = u / a.nqp;
+            const int nh = min(GT_QB, (a.Qb - qp * GT_QB * GT_M + GT_M - 1) / GT_M);
+            const bool hact = h < nh;   // this group's block holds queries in this unit
             const int64_t ib = (int64_t)sp * a.split_items;
             const int64_t ie = min(a.n, ib + a.split_items);
             const int q = (qp * GT_QB + h) * GT_M + row;
-            const bool vq = q < a.Qb;
-            const float qe = vq ? a.eps_rel * a.qnorm[q] : 0.f;
             // heap of this CTA's query row (CTAs of other item splits keep their own)
-            float *hp = a.heap_smem
-                            ? reinterpret_cast<float *>(tmem_slot + 4) + (esub * GT_M + row) * a.k
-                            : a.heap + ((int64_t)(blockIdx.x * 2 + esub) * GT_M + row) * a.k;
-            // survivors go to 16-slot chunks of the query's list reserved with one
-            // atomic each; unused slots of the last chunk are filled with -1
-            int32_t *cl = a.cand + (int64_t)(vq ? q : 0) * a.C;
-            uint32_t sbase = 0, sleft = 0;
-            float theta = -INFINITY, pub = -INFINITY;
-            int hs = 0;
-            if (vq) {
-                const uint32_t o = a.theta_glob[q];
-                if (o) theta = float_unorder(o);
-            }
-            // the hot-loop test uses a round-to-nearest FMA; thr_adj absorbs its rounding
-            // (<= 2^-24 |result| near the threshold) so the filter stays certified
-            float thr_adj = -INFINITY;
-            auto set_theta = [&](float th) {
-                theta = th;
-                thr_adj = th - fabsf(th) * 2.384185791015625e-7f;   // 2^-22
-            };
-            if (theta > -INFINITY) set_theta(theta);
+            er.begin(a, q, hact && q < a.Qb,
+                     a.heap_smem ? sheap + (h * GT_M + row) * a.k
+                                 : a.heap + ((int64_t)(blockIdx.x * 2 + h) * GT_M + row) * a.k);
             const int64_t ntu = (ie - ib + GT_N - 1) / GT_N;
             for (int64_t jt = 0; jt < ntu; ++jt, ++t) {
-                const int64_t i0 = gt_tile_at(ib, ie, qp, a.nqp, jt);
-                const uint32_t acc = t & 1, tr = t >> 1;
-                const float *xn = sxn + acc * GT_N;
+                const int64_t i0 = gt_tile_at(ib, jt);
+                const uint32_t b = t & 1;
+                const float *xn = sxn + b * GT_N;
                 uint32_t o_next = 0;
-                const bool share = vq && ((t & 3) == 0);
+                const bool share = er.vq && ((t & 3) == 0);
                 if (share) o_next = *((volatile uint32_t *)&a.theta_glob[q]);   // consumed below
-                tc::mbar_wait(&xfull[acc], tr & 1);
-                tc::mbar_wait(&tfull[acc], tr & 1);
+                tc::mbar_wait(&xfull[b], (t >> 1) & 1);
+                const uint32_t buf = t % NBUF, tr = t / NBUF;
+                tc::mbar_wait(&tfull[buf * GT_QB + h], tr & 1);
                 tc::tc_fence_after();
-                const uint32_t taddr = tmem_base + ((uint32_t)(grp * 32) << 16) + (acc * GT_QB + h) * GT_N;
-                // largest |x| of the tile (the loader's buffer): s~ + qe |x| >= thr_adj
-                // implies s~ >= thr_adj - qe xmax
-                float xmax = 0.f;
-                {
-                    const float4 xv = reinterpret_cast<const float4 *>(xn + c_lo)[lane];
-                    xmax = fmaxf(fmaxf(xv.x, xv.y), fmaxf(xv.z, xv.w));
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) xmax = fmaxf(xmax, __shfl_xor_sync(NR_FULL, xmax, o));
-                }
-                const float thr_tile = __fmaf_rd(-xmax, qe, thr_adj);
+                if (hact) {
+                    const uint32_t taddr = tmem_base + ((uint32_t)(grp * 32) << 16) + (buf * GT_QB + h) * GT_N;
+                    // largest |x| of each 128-column part: s~ + qe |x| >= thr_adj
+                    // implies s~ >= thr_adj - qe xmax
+                    const float xm0 = warp_max128(xn, lane);
+                    const float xm1 = GT_N == 256 ? warp_max128(xn + 128, lane) : 0.f;
 #pragma unroll 1
-                for (int c = c_lo; c < c_lo + GT_EPI_COLS; c += 64) {
-                    if (a.dbg >= 2) break;
-                    uint32_t r0[32], r1[32];
-                    tc::tmem_ld_32x32b_x32(taddr + c, r0);
-                    tc::tmem_ld_32x32b_x32(taddr + c + 32, r1);
-                    tc::tmem_ld_wait();
-                    if (!vq || a.dbg) continue;
-                    // cheap screen: max of the 64 approximate scores against the
-                    // threshold loosened by the tile's largest error term
-                    float m0 = __uint_as_float(r0[0]), m1 = __uint_as_float(r1[0]);
-#pragma unroll
-                    for (int j = 1; j < 32; ++j) {
-                        m0 = fmaxf(m0, __uint_as_float(r0[j]));
-                        m1 = fmaxf(m1, __uint_as_float(r1[j]));
-                    }
-                    if (fmaxf(m0, m1) < thr_tile) continue;
-                    const float4 *x4 = reinterpret_cast<const float4 *>(xn + c);
-                    unsigned hit = 0u, hit2 = 0u;
-#pragma unroll
-                    for (int j4 = 0; j4 < 8; ++j4) {
-                        const float4 xa = x4[j4];
-                        const float4 xb = x4[j4 + 8];
-                        hit |= (fmaf(xa.x, qe, __uint_as_float(r0[4 * j4 + 0])) >= thr_adj) << (4 * j4 + 0);
-                        hit |= (fmaf(xa.y, qe, __uint_as_float(r0[4 * j4 + 1])) >= thr_adj) << (4 * j4 + 1);
-                        hit |= (fmaf(xa.z, qe, __uint_as_float(r0[4 * j4 + 2])) >= thr_adj) << (4 * j4 + 2);
-                        hit |= (fmaf(xa.w, qe, __uint_as_float(r0[4 * j4 + 3])) >= thr_adj) << (4 * j4 + 3);
-                        hit2 |= (fmaf(xb.x, qe, __uint_as_float(r1[4 * j4 + 0])) >= thr_adj) << (4 * j4 + 0);
-                        hit2 |= (fmaf(xb.y, qe, __uint_as_float(r1[4 * j4 + 1])) >= thr_adj) << (4 * j4 + 1);
-                        hit2 |= (fmaf(xb.z, qe, __uint_as_float(r1[4 * j4 + 2])) >= thr_adj) << (4 * j4 + 2);
-                        hit2 |= (fmaf(xb.w, qe, __uint_as_float(r1[4 * j4 + 3])) >= thr_adj) << (4 * j4 + 3);
-                    }
-                    // rare path: survivors (pushed + fed to the running top-k bound)
-                    for (int hh = 0; hh < 2; ++hh) {
-                        unsigned m = hh ? hit2 : hit;
-                        while (m) {
-                            const int j = __ffs(m) - 1;
-                            m &= m - 1;
-                            const int col = c + 32 * hh + j;
-                            float s_j = 0.f;
-#pragma unroll
-                            for (int jj = 0; jj < 32; ++jj)
-                                if (jj == j) s_j = __uint_as_float(hh ? r1[jj] : r0[jj]);
-                            const float x = xn[col];
-                            if (__fmaf_ru(x, qe, s_j) < theta) continue;   // exact re-test
-                            const int64_t i = i0 + col;
-                            if (i >= a.n) continue;
-                            if (sleft == 0) { sbase = atomicAdd(&a.cnt[q], 16u); sleft = 16; }
-                            if (sbase + (16 - sleft) < a.C) cl[sbase + (16 - sleft)] = (int32_t)i;
-                            --sleft;
-                            const float lb = __fmaf_rd(-x, qe, s_j);
-                            if (hs < a.k) {          // min-heap push
-                                int p = hs++;
-                                while (p > 0) {
-                                    const int par = (p - 1) >> 1;
-                                    if (hp[par] <= lb) break;
-                                    hp[p] = hp[par];
-                                    p = par;
-                                }
-                                hp[p] = lb;
-                                if (hs == a.k && hp[0] > theta) set_theta(hp[0]);
-                            } else if (lb > hp[0]) { // replace the minimum
-                                int p = 0;
-                                while (true) {
-                                    int ch = 2 * p + 1;
-                                    if (ch >= a.k) break;
-                                    if (ch + 1 < a.k && hp[ch + 1] < hp[ch]) ++ch;
-                                    if (hp[ch] >= lb) break;
-                                    hp[p] = hp[ch];
-                                    p = ch;
-                                }
-                                hp[p] = lb;
-                                if (hp[0] > theta) set_theta(hp[0]);
-                            }
-                        }
+                    for (int c = 0; c < GT_N; c += 64) {
+                        if (a.dbg >= 2) break;
+                        uint32_t r0[32], r1[32];
+                        tc::tmem_ld_32x32b_x32(taddr + c, r0);
+                        tc::tmem_ld_32x32b_x32(taddr + c + 32, r1);
+                        tc::tmem_ld_wait();
+                        if (!er.vq || a.dbg) continue;
+                        er.chunk(r0, r1, c, xn, c < 128 ? xm0 : xm1, i0, scode + b * GT_N * 4,
+                                 spart + b * GT_N);
                     }
                 }
                 tc::tc_fence_before();
                 __syncwarp();
-                if (lane == 0) tc::mbar_arrive(&tempty[acc]);
-                if (share) {   // share the bound across CTAs (every 4 tiles)
-                    if (hs == a.k && hp[0] > pub) {
-                        pub = hp[0];
-                        atomicMax(&a.theta_glob[q], float_order(pub));
-                    }
-                    if (o_next) {
-                        const float g = float_unorder(o_next);
-                        if (g > theta) set_theta(g);
-                    }
+                if (lane == 0) {
+                    tc::mbar_arrive(&tempty[buf * GT_QB + h]);
+                    tc::mbar_arrive(&xempty[b]);
                 }
+                if (share) er.share(o_next);
             }
-            for (; sleft > 0; --sleft)
-                if (sbase + (16 - sleft) < a.C) cl[sbase + (16 - sleft)] = -1;
+            er.end();
         }
     }
     __syncthreads();
@@ -433,9 +525,210 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
     }
 }
 
-static size_t gt_tc_smem_bytes(int kblocks, int stages, int heap_k) {
-    return 1024 + (size_t)GT_QB * kblocks * GT_A_BLK + (size_t)stages * GT_B_BLK + 2 * GT_N * 4 +
-           (2 * GT_MAX_STAGES + 8) * 8 + 16 + (size_t)2 * GT_M * heap_k * 4;
+
+// ------------------------------------------------------------ CTA-pair variant
+// The same filter on a CTA pair (cluster of 2, tcgen05 cta_group::2): the pair's
+// M = 256 query rows (128 per CTA, resident in smem) x N = 256 items per MMA; each
+// CTA TMA-loads its 128-item half of every tile (signalled on the leader's
+// barrier) and the leader CTA issues the pair MMAs, which read the B halves of both
+// CTAs — so each CTA receives half the item bytes it multiplies (the L2->SM feed
+// bounds the single-CTA kernel) while the tensor cores run at the N = 256 rate, and
+// each CTA's 128 x 256 accumulator is double-buffered in its TMEM (epilogue overlapped).
+constexpr int GP_HN = 128;                 // items per CTA half tile
+constexpr int GP_PN = 2 * GP_HN;           // items per pair tile (MMA N)
+constexpr int GP_B_BLK = GP_HN * 128;      // 16 KB: one K block of a half tile
+constexpr int GP_MAX_STAGES = 12;
+
+__global__ void __launch_bounds__(GT_THREADS, 1)
+    gt_filter_pair(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmX,
+                   GtArgs a) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
+    uint8_t *sA = smem;                                        // kblocks x 16 KB (this CTA's rows)
+    uint8_t *sB = sA + a.kblocks * GT_A_BLK;                   // stages x 16 KB (this CTA's half)
+    const int SB = a.kps * GP_B_BLK;                           // bytes per stage
+    float *sxn = (float *)(sB + a.stages * SB);                // [2][GP_PN] |x| tiles
+    uint32_t *scode = (uint32_t *)(sxn + 2 * GP_PN);           // [2][GP_PN x W<=4] (member mode)
+    uint8_t *spart = (uint8_t *)(scode + 2 * GP_PN * 4);       // [2][GP_PN]        (member mode)
+    uint64_t *bars = (uint64_t *)(spart + 2 * GP_PN);
+    uint64_t *full = bars, *empty = bars + GP_MAX_STAGES;
+    uint64_t *a_full = bars + 2 * GP_MAX_STAGES, *a_empty = a_full + 1;
+    uint64_t *tfull = a_empty + 1, *tempty = tfull + 2;        // per TMEM buffer
+    uint64_t *xfull = tempty + 2, *xempty = xfull + 2;         // per |x| tile buffer
+    uint32_t *tmem_slot = (uint32_t *)(xempty + 2);
+    float *sheap = reinterpret_cast<float *>(tmem_slot + 4);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = tc::cluster_ctarank();
+    const bool leader = rank == 0;
+    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < a.stages; ++s) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
+        tc::mbar_init(a_full, 1);
+        tc::mbar_init(a_empty, 1);
+        for (int b = 0; b < 2; ++b) {
+            tc::mbar_init(&tfull[b], 1);
+            tc::mbar_init(&tempty[b], 16);   // 8 epilogue warps x 2 CTAs (leader's is used)
+            tc::mbar_init(&xfull[b], 1);
+            tc::mbar_init(&xempty[b], 8);
+        }
+        tc::fence_mbar_init();
+    }
+    if (warp == 2) tc::tmem_alloc_pair(tmem_slot, 512);
+    if (warp == 0 && lane == 0) { tc::tma_prefetch(&tmQ); tc::tma_prefetch(&tmX); }
+    tc::tc_fence_before();
+    tc::cluster_sync();   // both CTAs' barriers initialised and TMEM allocated
+    tc::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const int nunits = a.nqp * a.nsplit;   // (query group of 256, item split)
+
+    if (warp == 0 && lane == 0) {
+        // ================= TMA producer (both CTAs; completion on the leader's barriers)
+        uint32_t g = 0, ul = 0;
+        const uint32_t a_full_l = tc::mapa_shared(a_full, 0);
+        for (int u = pair; u < nunits; u += npairs, ++ul) {
+            const int qg = u % a.nqp, sp = u / a.nqp;
+            const int64_t ib = (int64_t)sp * a.split_items;
+            const int64_t ie = min(a.n, ib + a.split_items);
+            if (ul > 0) tc::mbar_wait_cluster(a_empty, (ul - 1) & 1);
+            if (leader) tc::mbar_arrive_expect_tx(a_full, 2 * a.kblocks * GT_A_BLK);
+            for (int kb = 0; kb < a.kblocks; ++kb)
+                tc::tma_load_2d_pair(sA + kb * GT_A_BLK, &tmQ, a_full_l, kb * GT_KB,
+                                     qg * 2 * GT_M + (int)rank * GT_M);
+            const int64_t ntu = (ie - ib + GP_PN - 1) / GP_PN;
+            for (int64_t jt = 0; jt < ntu; ++jt) {
+                const int64_t i0 = ib + jt * GP_PN + rank * GP_HN;
+                for (int kb0 = 0; kb0 < a.kblocks; kb0 += a.kps, ++g) {
+                    const uint32_t s = g % a.stages, r = g / a.stages;
+                    tc::mbar_wait_cluster(&empty[s], (r & 1) ^ 1);
+                    if (leader) tc::mbar_arrive_expect_tx(&full[s], 2 * SB);
+                    const uint32_t fb = tc::mapa_shared(&full[s], 0);
+                    for (int e = 0; e < a.kps; ++e)
+                        tc::tma_load_2d_pair(sB + s * SB + e * GP_B_BLK, &tmX, fb, (kb0 + e) * GT_KB, (int)i0);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ================= MMA issuer: the leader CTA's warp 1 drives the pair
+        if (leader) {
+            constexpr uint32_t idesc = tc::umma_idesc(1, 2 * GT_M, GP_PN);
+            uint32_t g = 0, t = 0, ul = 0;
+            for (int u = pair; u < nunits; u += npairs, ++ul) {
+                const int sp = u / a.nqp;
+                const int64_t ib = (int64_t)sp * a.split_items;
+                const int64_t ie = min(a.n, ib + a.split_items);
+                tc::mbar_wait_cluster(a_full, ul & 1);
+                tc::tc_fence_after();
+                for (int64_t i0 = ib; i0 < ie; i0 += GP_PN, ++t) {
+                    const uint32_t buf = t & 1, tr = t >> 1;
+                    tc::mbar_wait_cluster(&tempty[buf], (tr & 1) ^ 1);   // both CTAs drained it
+                    tc::tc_fence_after();
+                    const uint32_t dt = tmem_base + buf * GP_PN;
+                    for (int kb0 = 0; kb0 < a.kblocks; kb0 += a.kps, ++g) {
+                        const uint32_t s = g % a.stages, r = g / a.stages;
+                        tc::mbar_wait_cluster(&full[s], r & 1);
+                        tc::tc_fence_after();
+                        for (int e = 0; e < a.kps; ++e) {
+                            const int kb = kb0 + e;
+                            const uint32_t abase = tc::smem_u32(sA + kb * GT_A_BLK);
+                            const uint32_t bbase = tc::smem_u32(sB + s * SB + e * GP_B_BLK);
+                            const int nk = min(GT_KB / 16, (a.d - kb * GT_KB + 15) / 16);
+                            for (int kk = 0; kk < (a.dbg == 3 ? 0 : nk); ++kk)
+                                tc::mma_f16_pair_warp(dt, tc::umma_desc_sw128(abase + kk * 32),
+                                                      tc::umma_desc_sw128(bbase + kk * 32), idesc,
+                                                      (kb | kk) != 0);
+                        }
+                        tc::mma_commit_pair_mc(&empty[s], 3);
+                    }
+                    tc::mma_commit_pair_mc(&tfull[buf], 3);
+                }
+                tc::mma_commit_pair_mc(a_empty, 3);
+            }
+        }
+    } else if (warp == 3 && lane == 0) {
+        // ================= |x| (and member-mode code / sub-dataset) loader: all 256
+        // items of each pair tile, into this CTA's tile buffer
+        uint32_t t = 0;
+        for (int u = pair; u < nunits; u += npairs) {
+            const int sp = u / a.nqp;
+            const int64_t ib = (int64_t)sp * a.split_items;
+            const int64_t ie = min(a.n, ib + a.split_items);
+            for (int64_t i0 = ib; i0 < ie; i0 += GP_PN, ++t) {
+                const uint32_t b = t & 1, tr = t >> 1;
+                tc::mbar_wait(&xempty[b], (tr & 1) ^ 1);
+                tc::mbar_arrive_expect_tx(&xfull[b], GP_PN * 4 + (a.member ? GP_PN * (a.W * 4 + 1) : 0));
+                tc::bulk_load(sxn + b * GP_PN, a.xnorm + i0, GP_PN * 4, &xfull[b]);
+                if (a.member) {
+                    tc::bulk_load(scode + b * GP_PN * 4, a.codes_id + i0 * a.W, GP_PN * a.W * 4, &xfull[b]);
+                    tc::bulk_load(spart + b * GP_PN, a.part_id + i0, GP_PN, &xfull[b]);
+                }
+            }
+        }
+    } else if (warp >= 4) {
+        // ================= epilogue: thread <-> (query row = TMEM lane, 128-column half)
+        const int grp = warp & 3;
+        const int half = (warp - 4) >> 2;
+        const int row = grp * 32 + lane;
+        uint32_t t = 0;
+        GtEpiRow er;
+        for (int u = pair; u < nunits; u += npairs) {
+            const int qg = u % a.nqp, sp = u / a.nqp;
+            const int64_t ib = (int64_t)sp * a.split_items;
+            const int64_t ie = min(a.n, ib + a.split_items);
+            const int q = qg * 2 * GT_M + (int)rank * GT_M + row;
+            er.begin(a, q, q < a.Qb,
+                     a.heap_smem ? sheap + (half * GT_M + row) * a.k
+                                 : a.heap + ((int64_t)(blockIdx.x * 2 + half) * GT_M + row) * a.k);
+            for (int64_t i0 = ib; i0 < ie; i0 += GP_PN, ++t) {
+                const uint32_t b = t & 1, tr = t >> 1;
+                const float *xn = sxn + b * GP_PN;
+                uint32_t o_next = 0;
+                const bool share = er.vq && ((t & 3) == 0);
+                if (share) o_next = *((volatile uint32_t *)&a.theta_glob[q]);
+                tc::mbar_wait(&xfull[b], tr & 1);
+                tc::mbar_wait_cluster(&tfull[b], tr & 1);
+                tc::tc_fence_after();
+                const uint32_t taddr = tmem_base + ((uint32_t)(grp * 32) << 16) + b * GP_PN + half * 128;
+                const float xm = warp_max128(xn + half * 128, lane);
+#pragma unroll 1
+                for (int c = half * 128; c < half * 128 + 128; c += 64) {
+                    if (a.dbg >= 2) break;
+                    uint32_t r0[32], r1[32];
+                    tc::tmem_ld_32x32b_x32(taddr + (c - half * 128), r0);
+                    tc::tmem_ld_32x32b_x32(taddr + (c - half * 128) + 32, r1);
+                    tc::tmem_ld_wait();
+                    if (!er.vq || a.dbg) continue;
+                    er.chunk(r0, r1, c, xn, xm, i0, scode + b * GP_PN * 4, spart + b * GP_PN);
+                }
+                tc::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    tc::mbar_arrive_cluster(tc::mapa_shared(&tempty[b], 0));
+                    tc::mbar_arrive(&xempty[b]);
+                }
+                if (share) er.share(o_next);
+            }
+            er.end();
+        }
+    }
+    __syncthreads();
+    tc::cluster_sync();   // no CTA leaves while its peer may still touch its smem / barriers
+    if (warp == 2) {
+        tc::tc_fence_after();
+        tc::tmem_dealloc_pair(tmem_base, 512);
+    }
+}
+
+static size_t gp_smem_bytes(int kblocks, int stages, int heap_k, int kps = 1) {
+    return 1024 + (size_t)kblocks * GT_A_BLK + (size_t)stages * kps * GP_B_BLK + 2 * GP_PN * 4 +
+           2 * GP_PN * 16 + 2 * GP_PN + (2 * GP_MAX_STAGES + 2 + 8) * 8 + 16 +
+           (size_t)2 * GT_M * heap_k * 4;
+}
+
+static size_t gt_tc_smem_bytes(int nt, int kblocks, int stages, int heap_k) {
+    return 1024 + (size_t)GT_QB * kblocks * GT_A_BLK + (size_t)stages * nt * 128 + 2 * nt * 4 +
+           2 * nt * 16 + 2 * nt + (2 * GT_MAX_STAGES + 2 + 8 + 4) * 8 + 16 +
+           (size_t)GT_QB * GT_M * heap_k * 4;
 }
 
 size_t gt_heap_bytes(int k) {
@@ -444,28 +737,36 @@ size_t gt_heap_bytes(int k) {
     return (size_t)sms * 2 * GT_M * k * 4;
 }
 
+static int gt_pick_nt(int kb) {
+    if (getenv("NRLSH_GT_NT") && atoi(getenv("NRLSH_GT_NT")) == 128) return 128;
+    return gt_tc_smem_bytes(256, kb, 3, 0) <= 227 * 1024 ? 256 : 128;
+}
+
 bool gt_tc_supported(int d, int k) {
     const int dp = (d + 7) / 8 * 8;
     const int kb = (dp + GT_KB - 1) / GT_KB;
     return encode_fn() != nullptr && kb <= GT_MAX_KBLK && k <= GT_MAX_K &&
-           gt_tc_smem_bytes(kb, 3, 0) <= 227 * 1024;
+           gt_tc_smem_bytes(128, kb, 3, 0) <= 227 * 1024;
 }
 
 int launch_gt_filter_tc(const void *Xb, int64_t n, int d, int dp, const void *Qb16, int Qb,
                         const float *xnorm, const float *qnorm, float eps_rel, int k,
                         uint32_t *theta_glob, float *heap, int32_t *cand, uint32_t *cnt, int64_t C,
-                        cudaStream_t s) {
+                        cudaStream_t s, const GtMember *mb) {
+    const int kblocks = (dp + GT_KB - 1) / GT_KB;
+    const int NT = gt_pick_nt(kblocks);
     CUtensorMap tq, tx;
     if (!make_tmap(&tq, Qb16, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dp, Qb, GT_KB, GT_M) ||
-        !make_tmap(&tx, Xb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dp, n, GT_KB, GT_N))
+        !make_tmap(&tx, Xb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dp, n, GT_KB, NT))
         return -1;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     GtArgs a;
+    a.kps = 1;
     a.n = n;
     a.Qb = Qb;
     a.d = d;
-    a.kblocks = (dp + GT_KB - 1) / GT_KB;
+    a.kblocks = kblocks;
     a.k = k;
     a.eps_rel = eps_rel;
     a.xnorm = xnorm;
@@ -476,24 +777,101 @@ int launch_gt_filter_tc(const void *Xb, int64_t n, int d, int dp, const void *Qb
     a.cnt = cnt;
     a.C = C;
     a.dbg = getenv("NRLSH_GT_DBG") ? atoi(getenv("NRLSH_GT_DBG")) : 0;
+    a.prefetch = getenv("NRLSH_GT_PREFETCH") ? atoi(getenv("NRLSH_GT_PREFETCH")) : GT_PREFETCH;
+    a.member = mb != nullptr;
+    a.codes_id = mb ? mb->codes_id : nullptr;
+    a.part_id = mb ? mb->part_id : nullptr;
+    a.pos_of_id = mb ? mb->pos_of_id : nullptr;
+    a.R = mb ? mb->R : nullptr;
+    a.L = mb ? mb->L : 0;
+    a.W = mb ? mb->W : 1;
+    a.qcodes = mb ? mb->qcodes : nullptr;
+    a.sel_B = mb ? mb->sel_B : nullptr;
+    a.sel_pk = mb ? mb->sel_pk : nullptr;
+    if (mb && (mb->W < 1 || mb->W > 4)) return -1;
+    // CTA-pair kernel: opt-in (NRLSH_GT_PAIR=1) — correct, but measured slower than
+    // the single-CTA N=256 kernel on c4 (0.84 vs 0.72 ms per 1024 queries: ~6.7K
+    // cycles per pair tile against 1.3K of MMA work)
+    const bool use_pair = Qb > GT_M && getenv("NRLSH_GT_PAIR") && atoi(getenv("NRLSH_GT_PAIR")) == 1 &&
+                          gp_smem_bytes(kblocks, 4, 0) <= 227 * 1024;
+    if (use_pair) {
+        CUtensorMap tq2, tx2;
+        if (!make_tmap(&tq2, Qb16, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dp, Qb, GT_KB, GT_M) ||
+            !make_tmap(&tx2, Xb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dp, n, GT_KB, GP_HN))
+            return -1;
+        int npairs = sms / 2;
+        a.nqp = (Qb + 2 * GT_M - 1) / (2 * GT_M);   // query groups of 256
+        // one unit per pair when the query groups divide the pairs (the pairs reading
+        // one split then run concurrently and share its L2 fetches)
+        if (npairs >= a.nqp && npairs % a.nqp) npairs -= npairs % a.nqp;
+        if (getenv("NRLSH_GT_PAIRS")) npairs = std::max(1, std::min(sms / 2, atoi(getenv("NRLSH_GT_PAIRS"))));
+        const int64_t ntiles = (n + GP_PN - 1) / GP_PN;
+        int nsplit = std::max(1, npairs / a.nqp);
+        nsplit = (int)std::min<int64_t>(nsplit, ntiles);
+        a.split_items = ((ntiles + nsplit - 1) / nsplit) * GP_PN;
+        a.nsplit = (int)((n + a.split_items - 1) / a.split_items);
+        // whole K per stage (one barrier round trip per tile) when three such stages fit
+        a.kps = (gp_smem_bytes(kblocks, 3, 0, kblocks) <= 227 * 1024) ? kblocks : 1;
+        if (getenv("NRLSH_GT_KPS")) a.kps = atoi(getenv("NRLSH_GT_KPS")) == 1 ? 1 : kblocks;
+        const int smin = a.kps == 1 ? 4 : 3;
+        a.stages = smin;
+        a.heap_smem = 0;
+        for (int st = GP_MAX_STAGES; st >= smin; --st)
+            if (gp_smem_bytes(kblocks, st, k, a.kps) <= 227 * 1024) { a.stages = st; a.heap_smem = 1; break; }
+        if (!a.heap_smem)
+            for (int st = GP_MAX_STAGES; st >= smin; --st)
+                if (gp_smem_bytes(kblocks, st, 0, a.kps) <= 227 * 1024) { a.stages = st; break; }
+        if (getenv("NRLSH_GT_STAGES")) {
+            a.stages = std::max(2, std::min(GP_MAX_STAGES, atoi(getenv("NRLSH_GT_STAGES"))));
+            a.heap_smem = gp_smem_bytes(kblocks, a.stages, k, a.kps) <= 227 * 1024;
+        }
+        const size_t sm = gp_smem_bytes(kblocks, a.stages, a.heap_smem ? k : 0, a.kps);
+        cudaFuncSetAttribute(gt_filter_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(2 * std::min(npairs, a.nqp * a.nsplit));
+        cfg.blockDim = dim3(GT_THREADS);
+        cfg.dynamicSmemBytes = sm;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        if (cudaLaunchKernelEx(&cfg, gt_filter_pair, tq2, tx2, a) != cudaSuccess) return -1;
+        note_launch();
+        return 0;
+    }
     a.nqp = (Qb + GT_QB * GT_M - 1) / (GT_QB * GT_M);
-    const int64_t ntiles = (n + GT_N - 1) / GT_N;
+    const int64_t ntiles = (n + NT - 1) / NT;
     int nsplit = std::max(1, sms / a.nqp);     // one unit per CTA: no tail wave
     nsplit = (int)std::min<int64_t>(nsplit, ntiles);
-    a.split_items = ((ntiles + nsplit - 1) / nsplit) * GT_N;
+    a.split_items = ((ntiles + nsplit - 1) / nsplit) * NT;
     a.nsplit = (int)((n + a.split_items - 1) / a.split_items);
     // deepest ring that fits, with the heaps in smem if they fit too
+    const int smax = NT == 256 ? 6 : GT_MAX_STAGES;
     a.stages = 3;
     a.heap_smem = 0;
-    for (int st = GT_MAX_STAGES; st >= 3; --st)
-        if (gt_tc_smem_bytes(a.kblocks, st, k) <= 227 * 1024) { a.stages = st; a.heap_smem = 1; break; }
-    if (a.stages < 6)
-        for (int st = GT_MAX_STAGES; st > a.stages; --st)
-            if (gt_tc_smem_bytes(a.kblocks, st, 0) <= 227 * 1024) { a.stages = st; a.heap_smem = 0; break; }
-    const size_t sm = gt_tc_smem_bytes(a.kblocks, a.stages, a.heap_smem ? k : 0);
-    cudaFuncSetAttribute(gt_filter_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    for (int st = smax; st >= 3; --st)
+        if (gt_tc_smem_bytes(NT, kblocks, st, k) <= 227 * 1024) { a.stages = st; a.heap_smem = 1; break; }
+    if (!a.heap_smem || (NT == 128 && a.stages < 6))
+        for (int st = smax; st > (a.heap_smem ? a.stages : 2); --st)
+            if (gt_tc_smem_bytes(NT, kblocks, st, 0) <= 227 * 1024) { a.stages = st; a.heap_smem = 0; break; }
+    if (getenv("NRLSH_GT_STAGES")) {   // experiments: force a ring depth (heaps to global)
+        a.stages = std::max(2, std::min(smax, atoi(getenv("NRLSH_GT_STAGES"))));
+        a.heap_smem = gt_tc_smem_bytes(NT, kblocks, a.stages, k) <= 227 * 1024;
+        if (gt_tc_smem_bytes(NT, kblocks, a.stages, 0) > 227 * 1024) return -1;
+    }
+    const size_t sm = gt_tc_smem_bytes(NT, kblocks, a.stages, a.heap_smem ? k : 0);
     const int grid = std::min(sms, a.nqp * a.nsplit);
-    gt_filter_tc<<<grid, GT_THREADS, sm, s>>>(tq, tx, a);
+    if (NT == 256) {
+        cudaFuncSetAttribute(gt_filter_tc<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        gt_filter_tc<256><<<grid, GT_THREADS, sm, s>>>(tq, tx, a);
+    } else {
+        cudaFuncSetAttribute(gt_filter_tc<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        gt_filter_tc<128><<<grid, GT_THREADS, sm, s>>>(tq, tx, a);
+    }
     note_launch();
     return 0;
 }

@@ -477,6 +477,7 @@ def test_rerank_bf16_filter_matches_fp32(built, case, monkeypatch):
     enter the top-k: ids and fp32 scores equal the all-fp32 re-rank's, bit for bit."""
     P = _P()
     monkeypatch.setenv("NRLSH_NO_DENSE", "1")    # both sides through the gather kernels
+    monkeypatch.setenv("NRLSH_RERANK_TC", "0")
     cfg, X, Q, Xd, idx, orc = built(*case)
     n = X.shape[0]
     Qd = torch.from_numpy(Q[: min(len(Q), 64)]).cuda()
@@ -557,3 +558,53 @@ def test_coarse_cells_no_overflow(built):
             oid, ork = oracle.candidates(ocodes, orc.part, qc[qi], orc.R, T)
             o = np.lexsort((gid[qi], grk[qi]))
             assert np.array_equal(gid[qi][o], oid) and np.array_equal(grk[qi][o], ork)
+
+
+@pytest.mark.parametrize("case", [("c4", 300_000, 32, 64, 128), ("c4", 300_000, 32, 32, 4),
+                                  ("scale", 70_000, 16, 128, 256), ("c2", None, 200, 64, 32),
+                                  ("tiny", None, None, 32, 8)], ids=_ids)
+def test_rerank_tensor_matches_gather(built, case, monkeypatch):
+    """The tensor-core re-rank (bf16 pass over every item, certified filter against a
+    running bound of the k-th best candidate score, candidate rule in the epilogue,
+    fp32 re-rank of the survivors) returns exactly the gather path's answer — same
+    ids, bit-identical scores — at budgets from tiny to all of n; and through its
+    overflow redo (survivor lists capped at 16)."""
+    cfg, X, Q, Xd, idx, orc = built(*case)
+    P = _P()
+    n = X.shape[0]
+    Qd = torch.from_numpy(Q).cuda()
+    for T in sorted({1, 7, max(1, n // 100), n // 3, n}):
+        for k in (1, cfg.k, 64):
+            monkeypatch.setenv("NRLSH_RERANK_TC", "0")
+            gi, gs = idx.query(Qd, k, T)
+            assert P.last_rerank_path()["path"] == "gather"
+            monkeypatch.setenv("NRLSH_RERANK_TC", "1")
+            ti, ts = idx.query(Qd, k, T)
+            assert P.last_rerank_path()["path"] == "tensor"
+            assert torch.equal(gi, ti), (T, k)
+            assert torch.equal(gs.view(torch.int32), ts.view(torch.int32)), (T, k)
+    monkeypatch.setenv("NRLSH_RERANK_TC_CAP", "16")
+    T = max(1, n // 10)
+    ti, ts = idx.query(Qd, cfg.k, T)
+    info = P.last_rerank_path()
+    assert info["path"] == "tensor" and info["overflow_redone"] > 0
+    monkeypatch.setenv("NRLSH_RERANK_TC", "0")
+    gi, gs = idx.query(Qd, cfg.k, T)
+    assert torch.equal(gi, ti) and torch.equal(gs.view(torch.int32), ts.view(torch.int32))
+
+
+@pytest.mark.parametrize("name,n,nq,k", [("c4", 300_000, 300, 10), ("c3", 40_000, 260, 100)])
+def test_exact_topk_cta_pair_kernel(name, n, nq, k, monkeypatch):
+    """The opt-in CTA-pair (cta_group::2) ground-truth filter returns exactly the
+    single-CTA kernel's top-k (ids and fp32 scores), over a ragged query count."""
+    P = _P()
+    cfg, X, Q = dataset(workloads.CONFIGS[name], n, nq)
+    Xd, Qd = torch.from_numpy(X).cuda(), torch.from_numpy(Q).cuda()
+    monkeypatch.setenv("NRLSH_GT_PAIR", "0")
+    a, sa = P.exact_topk(Xd, Qd, k)
+    monkeypatch.setenv("NRLSH_GT_PAIR", "1")
+    b, sb = P.exact_topk(Xd, Qd, k)
+    assert torch.equal(a, b) and torch.equal(sa.view(torch.int32), sb.view(torch.int32))
+    for qi in (0, nq - 1):
+        ids, s = oracle.exact_topk(X, Q[qi], k)
+        assert_topk_match(b[qi].cpu().numpy(), sb[qi].cpu().numpy(), ids, s, X, Q[qi])
