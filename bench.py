@@ -165,8 +165,10 @@ def roofline_for(slot, ms_total, count, info, peaks, peaks_src):
                 "peak_source": "tools/ubench.cu measured POPC rate (profiles/r01/ubench_popc.txt)",
                 "logical_pairs_per_s": nq * n / (ms_total / 1e3)}
     if slot == "gt_filter" or (slot == "rerank" and info.get("rerank_path") == "tensor"):
-        # one bf16 pass over every item per query (member-mode for the re-rank)
-        fl = 2.0 * nq * n * d * steps / count
+        # one bf16 pass over every item per query; the re-rank's member-mode pass
+        # multiplies only the tiles of sub-datasets holding candidates (its own count)
+        pairs = nq * n if slot == "gt_filter" else info["rerank_filter_pairs"]
+        fl = 2.0 * pairs * d * steps / count
         ach = fl / per_launch_s
         if slot == "rerank":
             pk = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")) * 1e12
@@ -372,7 +374,8 @@ def run_native(args):
         evs.append((e0, e1))
         scanned += qstats["scanned_pairs"]
     torch.cuda.synchronize()
-    rerank_path = P.last_rerank_path()["path"]
+    rinfo = P.last_rerank_path()
+    rerank_path = rinfo["path"]
     if dist:
         dist.barrier()
     clocks = sampler.stop()
@@ -426,7 +429,7 @@ def run_native(args):
     W = 1 if L <= 32 else (2 if L <= 64 else 4)
     info = {"n": cfg.n, "d": cfg.d, "L": L, "W": W, "nq": nq, "T": T, "k": k, "m": m,
             "scanned_pairs": scanned, "traffic": load_traffic(), "steps": args.steps,
-            "rerank_path": rerank_path,
+            "rerank_path": rerank_path, "rerank_filter_pairs": rinfo["filter_pairs"],
             "score_bytes": float(nq) * T * cfg.d * 4.0 * args.steps, "gt_tensor": True}
     dom = max(((n_, v) for n_, v in prof.items() if v[1] > 0), key=lambda x: x[1][0])
     roof = roofline_for(dom[0], dom[1][0], dom[1][1], info, peaks, peaks_src)
@@ -457,7 +460,9 @@ def run_native(args):
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
         "clocks": clocks,
         "notes": {"input_gen_s": t_gen, "peaks": peaks_src,
-                  "step_ms_all": ms},
+                  "step_ms_all": ms, "rerank_path": rerank_path,
+                  "rerank_filter_pairs_per_step": rinfo["filter_pairs"],
+                  "rerank_overflow_redone": rinfo["overflow_redone"]},
     }
     print(json.dumps(line), flush=True)
     if dist:

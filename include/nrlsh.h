@@ -165,21 +165,24 @@ nrlsh_status nrlsh_last_rerank_stats(int64_t *rescored_fp32);
    the same answer: the exact fp32 top-k of the probed candidates):
      NRLSH_RERANK_GATHER       per-candidate row gather + fp32 dot (default for
                                small budgets);
-     NRLSH_RERANK_TENSOR       one bf16 tcgen05 pass over every item with a certified
+     NRLSH_RERANK_TENSOR       one bf16 tcgen05 pass over the items of the
+                               sub-datasets holding candidates, with a certified
                                filter (|s~ - s_f| <= eps |q||x|) against a running
                                lower bound of the k-th best candidate score,
                                keeping survivors that pass the select's candidate
                                rule, then the same fp32 re-rank of the survivors
-                               (default when probe_budget >= n / 160);
+                               (default when probe_budget >= n / 300);
      NRLSH_RERANK_DENSE        dense SIMT re-rank of hot sub-datasets (opt-in);
      NRLSH_RERANK_GATHER_BF16  gather with a certified bf16 pre-pass (opt-in).
    overflow_redone: queries whose tensor-core survivor list overflowed and were
-   re-ranked by the gather path instead.  Either pointer may be NULL. */
+   re-ranked by the gather path instead; filter_pairs: (query, item) pairs the
+   tensor-core filter multiplied (0 on the other paths).  Any pointer may be NULL. */
 #define NRLSH_RERANK_GATHER 0
 #define NRLSH_RERANK_TENSOR 1
 #define NRLSH_RERANK_DENSE 2
 #define NRLSH_RERANK_GATHER_BF16 3
-nrlsh_status nrlsh_last_rerank_path(int32_t *path, int64_t *overflow_redone);
+nrlsh_status nrlsh_last_rerank_path(int32_t *path, int64_t *overflow_redone,
+                                    int64_t *filter_pairs);
 
 /* Exact top-k (as nrlsh_exact_topk) against the index's own items (device copy
    or borrowed pointer), so host-buffer callers do not re-stage the items. */

@@ -100,7 +100,7 @@ def lib():
         L.nrlsh_profile_slot_name.restype = C.c_char_p
         L.nrlsh_last_rerank_stats.argtypes = [p]
         L.nrlsh_last_rerank_stats.restype = st
-        L.nrlsh_last_rerank_path.argtypes = [p, p]
+        L.nrlsh_last_rerank_path.argtypes = [p, p, p]
         L.nrlsh_last_rerank_path.restype = st
         L.nrlsh_last_exact_stats.argtypes = [p, p, p]
         L.nrlsh_last_exact_stats.restype = st
@@ -295,9 +295,10 @@ RERANK_PATHS = {0: "gather", 1: "tensor", 2: "dense", 3: "gather_bf16"}
 def last_rerank_path():
     """Which re-rank implementation the last query on this thread used, and how many
     of its queries overflowed the tensor-core survivor list (re-ranked by gather)."""
-    a, b = C.c_int32(), C.c_int64()
-    _check(lib().nrlsh_last_rerank_path(C.byref(a), C.byref(b)))
-    return {"path": RERANK_PATHS.get(a.value, str(a.value)), "overflow_redone": b.value}
+    a, b, c = C.c_int32(), C.c_int64(), C.c_int64()
+    _check(lib().nrlsh_last_rerank_path(C.byref(a), C.byref(b), C.byref(c)))
+    return {"path": RERANK_PATHS.get(a.value, str(a.value)), "overflow_redone": b.value,
+            "filter_pairs": c.value}
 
 
 def last_query_stats():

@@ -24,6 +24,7 @@ thread_local int64_t g_last_pairs = 0;
 thread_local int64_t g_last_rescored = 0;
 thread_local int64_t g_last_rtc_overflow = 0;   // tensor-core re-rank: queries redone by gather
 thread_local int64_t g_last_rtc = 0;            // 1 if the last query used the tensor-core re-rank
+thread_local int64_t g_last_rtc_pairs = 0;      // (query, item) pairs its filter multiplied
 thread_local bool g_in_rtc_redo = false;
 thread_local int64_t g_last_gt_max_cand = 0, g_last_gt_sum_cand = 0, g_last_gt_overflow = 0;
 
@@ -141,7 +142,7 @@ void free_index(nrlsh_index *ix) {
     void *ps[] = {ix->X_owned, ix->Xpad, ix->Xb, ix->xnorm, ix->norm2, ix->perm, ix->pos_of_id, ix->part_of_id,
                   ix->part_of_pos, ix->offsets_d, ix->V_d, ix->codes, ix->A, ix->Apad,
                   ix->R_d, ix->chunks_d, ix->order_d, ix->samp_codes, ix->samp_part,
-                  ix->tiles_d, ix->codes_id};
+                  ix->tiles_d, ix->xnorm_pos};
     // pool-backed (cudaMallocAsync at build); the index may have been used on any stream
     cudaDeviceSynchronize();
     for (void *p : ps)
@@ -295,12 +296,13 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
     NR_ALLOC(ix->pos_of_id, (size_t)n * 4);
     NR_ALLOC(ix->part_of_id, (size_t)npad);
     cudaMemsetAsync(ix->part_of_id + n, 0, (size_t)(npad - n), s);
-    NR_ALLOC(ix->part_of_pos, (size_t)n);
+    NR_ALLOC(ix->part_of_pos, (size_t)npad);
+    cudaMemsetAsync(ix->part_of_pos + n, 0, (size_t)(npad - n), s);
+    NR_ALLOC(ix->xnorm_pos, (size_t)npad * 4);
+    cudaMemsetAsync(ix->xnorm_pos + n, 0, (size_t)(npad - n) * 4, s);
     NR_ALLOC(ix->offsets_d, (size_t)(m + 1) * 8);
     NR_ALLOC(ix->V_d, (size_t)m * 8);
     NR_ALLOC(ix->codes, (size_t)n * W * 4);
-    NR_ALLOC(ix->codes_id, (size_t)npad * W * 4);
-    cudaMemsetAsync(ix->codes_id + n * W, 0, (size_t)(npad - n) * W * 4, s);
 
     // K1: norms + finite check
     DBuf bad;
@@ -381,12 +383,12 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
         ProfScope p(SLOT_CODES, s);
         launch_item_codes(ix->X, n, d, ix->norm2, ix->part_of_id, ix->V_d, ix->Apad, L, W,
                           ix->pos_of_id, ix->codes, ix->Xb, ix->dpb, ix->xnorm, ix->Xpad,
-                          ix->dpad, s);
+                          ix->dpad, s, ix->perm);
     }
-    // item-order codes (the tensor-core re-rank's membership test)
+    // |x| in partition order (the tensor-core filter's tiles)
     {
         ProfScope p(SLOT_CODES, s);
-        launch_codes_by_id(ix.get(), s);
+        launch_gather_f32(ix->xnorm, ix->perm, n, ix->xnorm_pos, s);
     }
     // compacted pilot sample (query-time pilots read it contiguously)
     {
@@ -554,7 +556,7 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
         cn.alloc((size_t)Qmax * 4, s) || cv.alloc((size_t)Qmax * 4, s) ||
         ba.alloc((size_t)((Qmax + 127) / 128) * ix->m, s) || bf.alloc((size_t)Qmax * C * 8, s) ||
         cd.alloc((size_t)Qmax * Tq * 4, s) ||
-        pt.alloc(want_topk ? rerank_partial_bytes(Qmax, Tq, k) : 0, s) || fl.alloc(32, s))
+        pt.alloc(want_topk ? rerank_partial_bytes(Qmax, Tq, k) : 0, s) || fl.alloc(40, s))
         return fail(NRLSH_ENOMEM, "query workspace");
     // dense re-rank of the sub-datasets most of whose pairs are candidates (rerank_dense.cu)
     const float *Xr = ix->Xpad ? ix->Xpad : ix->X;
@@ -570,13 +572,13 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
          dpart.alloc((size_t)Qmax * S * k * 8, s)))
         return fail(NRLSH_ENOMEM, "query workspace (dense re-rank)");
     const float dense_frac = getenv("NRLSH_DENSE_FRAC") ? (float)atof(getenv("NRLSH_DENSE_FRAC")) : 0.10f;
-    // tensor-core re-rank (tc_kernels.cu member mode): a bf16 GEMM pass over every
-    // item with the certified filter, keeping only candidates; chosen when the
-    // candidate budget is a large enough share of n (a gathered row costs ~170x a
-    // streamed one, measured on c4) — NRLSH_RERANK_TC=0/1 forces it off/on
+    // tensor-core re-rank (tc_kernels.cu member mode): a bf16 GEMM pass over the
+    // tiles of the sub-datasets holding candidates, certified filter, keeping only
+    // candidates; chosen when the candidate budget is a large enough share of n
+    // (measured on c4: break-even near T = n / 300) — NRLSH_RERANK_TC=0/1 forces it
     const char *rtc_env = getenv("NRLSH_RERANK_TC");
-    const double rtc_ratio = getenv("NRLSH_RERANK_TC_RATIO") ? atof(getenv("NRLSH_RERANK_TC_RATIO")) : 160.0;
-    const bool use_rtc = want_topk && !use_dense && !g_in_rtc_redo && ix->Xb && ix->codes_id &&
+    const double rtc_ratio = getenv("NRLSH_RERANK_TC_RATIO") ? atof(getenv("NRLSH_RERANK_TC_RATIO")) : 300.0;
+    const bool use_rtc = want_topk && !use_dense && !g_in_rtc_redo && ix->Xb && ix->xnorm_pos &&
                          gt_tc_supported(ix->d, k) &&
                          (rtc_env ? atoi(rtc_env) != 0 : (double)Tq * rtc_ratio >= (double)n);
     const int KS = std::min(1024, std::max(256, 4 * k));
@@ -585,7 +587,7 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
     const int64_t Cg = getenv("NRLSH_RERANK_TC_CAP")
                            ? std::max<int64_t>(16, atoll(getenv("NRLSH_RERANK_TC_CAP")))
                            : std::min<int64_t>(n, std::max<int64_t>(16384, 256 * (int64_t)k));
-    DBuf rsb, rspk, rseed, rtid, rtsc, rth, rqb, rqn, rhp, rcd, rcc, rov, rovn, rpt;
+    DBuf rsb, rspk, rseed, rtid, rtsc, rth, rqb, rqn, rhp, rcd, rcc, rov, rovn, rpt, rtl;
     if (use_rtc &&
         (rsb.alloc((size_t)Qmax * 4, s) || rspk.alloc((size_t)Qmax * 4, s) ||
          rseed.alloc((size_t)Qmax * KS * 4, s) || rtid.alloc((size_t)Qmax * k * 8, s) ||
@@ -593,18 +595,22 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
          rqb.alloc((size_t)Qmax * ix->dpb * 2, s) || rqn.alloc((size_t)Qmax * 4, s) ||
          rhp.alloc(gt_heap_bytes(k), s) || rcd.alloc((size_t)Qmax * Cg * 4, s) ||
          rcc.alloc((size_t)Qmax * 4, s) || rov.alloc((size_t)nq * 8, s) || rovn.alloc(4, s) ||
-         rpt.alloc(std::max(rerank_partial_bytes(Qmax, Cg, k), rerank_partial_bytes(Qmax, KS, k)), s)))
+         rpt.alloc(std::max(rerank_partial_bytes(Qmax, Cg, k), rerank_partial_bytes(Qmax, KS, k)), s) ||
+         rtl.alloc(gt_tile_ws_bytes(n, Qmax), s)))
         return fail(NRLSH_ENOMEM, "query workspace (tensor-core re-rank)");
     if (use_rtc) cudaMemsetAsync(rovn.p, 0, 4, s);
     GtMember mb;
-    mb.codes_id = ix->codes_id;
-    mb.part_id = ix->part_of_id;
-    mb.pos_of_id = ix->pos_of_id;
+    mb.codes = ix->codes;
+    mb.part = ix->part_of_pos;
+    mb.offsets = ix->offsets_d;
+    mb.m = ix->m;
     mb.R = ix->R_d;
     mb.L = ix->L;
     mb.W = ix->W;
-    const int init_flags[8] = {INT_MAX, INT_MAX, 0, 0, 0, 0, 0, 0};
-    cudaMemcpyAsync(fl.p, init_flags, 32, cudaMemcpyHostToDevice, s);
+    mb.tile_ws = use_rtc ? rtl.get<int32_t>() : nullptr;
+    mb.pairs = (unsigned long long *)(fl.get<int>() + 8);
+    const int init_flags[10] = {INT_MAX, INT_MAX, 0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyAsync(fl.p, init_flags, 40, cudaMemcpyHostToDevice, s);
     unsigned long long *pairs = (unsigned long long *)(fl.get<int>() + 4);
     const long long launches0 = launch_count();
     for (int64_t q0 = 0; q0 < nq; q0 += Qmax) {
@@ -636,10 +642,10 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
             mb.qcodes = qc.get<uint32_t>();
             mb.sel_B = rsb.get<uint32_t>();
             mb.sel_pk = rspk.get<uint32_t>();
-            if (launch_gt_filter_tc(ix->Xb, n, ix->d, ix->dpb, rqb.p, Qb, ix->xnorm,
+            if (launch_gt_filter_tc(ix->Xb, n, ix->d, ix->dpb, rqb.p, Qb, ix->xnorm_pos,
                                     rqn.get<float>(), gt_eps_rel(ix->dpb), k, rth.get<uint32_t>(),
                                     rhp.get<float>(), rcd.get<int32_t>(), rcc.get<uint32_t>(), Cg,
-                                    s, &mb))
+                                    s, ix->perm, &mb))
                 return fail(NRLSH_ECUDA, "tensor map encoding failed");
             // exact fp32 re-rank of the surviving candidates (same arithmetic as the
             // gather path: identical scores and order)
@@ -680,7 +686,7 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
                                  ix->Xb, ix->dpb, ix->xnorm, Qd, Qb, cand, Tq, Tq,
                                  nullptr, k, pt.get<unsigned long long>(),
                                  (int64_t *)oi.dev + q0 * k, (float *)os.dev + q0 * k,
-                                 (unsigned long long *)(fl.get<int>() + 6), s);
+                                 (unsigned long long *)(fl.get<int>() + 6), s, ix->pos_of_id);
             else
                 launch_rerank(ix->Xpad ? ix->Xpad : ix->X, ix->d, ix->Xpad ? ix->dpad : ix->d, Qd,
                               Qb, cand, Tq, Tq, nullptr, 1, k,
@@ -715,8 +721,8 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
         if ((e = oc.finish(s))) return cuda_fail(e, "copy candidates");
         if (rank_out && (e = orr.finish(s))) return cuda_fail(e, "copy ranks");
     }
-    int hflags[8];
-    cudaMemcpyAsync(hflags, fl.p, 32, cudaMemcpyDeviceToHost, s);
+    int hflags[10];
+    cudaMemcpyAsync(hflags, fl.p, 40, cudaMemcpyDeviceToHost, s);
     e = cudaStreamSynchronize(s);
     if (e) return cuda_fail(e, "query");
     e = cudaGetLastError();
@@ -729,6 +735,8 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
     g_last_pairs = (int64_t)pr;
     std::memcpy(&pr, hflags + 6, 8);
     g_last_rescored = (int64_t)pr;
+    std::memcpy(&pr, hflags + 8, 8);
+    if (!g_in_rtc_redo) g_last_rtc_pairs = (int64_t)pr;
     if (!g_in_rtc_redo)
         g_last_rtc = use_rtc ? NRLSH_RERANK_TENSOR
                              : (use_dense ? NRLSH_RERANK_DENSE
@@ -785,9 +793,11 @@ nrlsh_status nrlsh_last_rerank_stats(int64_t *rescored_fp32) {
     return NRLSH_OK;
 }
 
-nrlsh_status nrlsh_last_rerank_path(int32_t *path, int64_t *overflow_redone) {
+nrlsh_status nrlsh_last_rerank_path(int32_t *path, int64_t *overflow_redone,
+                                    int64_t *filter_pairs) {
     if (path) *path = (int32_t)g_last_rtc;
     if (overflow_redone) *overflow_redone = g_last_rtc_overflow;
+    if (filter_pairs) *filter_pairs = g_last_rtc == NRLSH_RERANK_TENSOR ? g_last_rtc_pairs : 0;
     return NRLSH_OK;
 }
 
@@ -803,7 +813,8 @@ nrlsh_status nrlsh_last_query_stats(int64_t *fallback_queries, int64_t *kernel_l
 static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const float *queries,
                                int64_t nq, int32_t k, const int64_t *seed_ids, int32_t seed_k,
                                int64_t *out_ids, float *out_scores, void *cuda_stream,
-                               const void *Xb_ix = nullptr, const float *xnorm_ix = nullptr) {
+                               const void *Xb_ix = nullptr, const float *xnorm_ix = nullptr,
+                               const int32_t *perm_ix = nullptr) {
     if (!items || !queries || !out_ids || !out_scores) return fail(NRLSH_EINVAL, "NULL argument");
     if (seed_ids && (seed_k < 1 || seed_k > 1024))
         return fail(NRLSH_EINVAL, "seed_k must be in [1, 1024]");
@@ -885,7 +896,8 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
             ProfScope p(SLOT_GT_FILTER, s);
             if (launch_gt_filter_tc(Xbp, n, d, dp, (const uint16_t *)qb.p + q0 * dp, Qb,
                                     xnp, qnb, eps_rel, k, th.get<uint32_t>(),
-                                    hp.get<float>(), cd.get<int32_t>(), cc.get<uint32_t>(), Cg, s))
+                                    hp.get<float>(), cd.get<int32_t>(), cc.get<uint32_t>(), Cg, s,
+                                    Xb_ix ? perm_ix : nullptr))
                 return fail(NRLSH_ECUDA, "tensor map encoding failed");
         } else {
             // pilot: certified lower bound of the k-th best score from a strided sample
@@ -957,7 +969,7 @@ nrlsh_status nrlsh_index_exact_topk(const nrlsh_index *ix, const float *queries,
                                     void *cuda_stream) {
     if (!ix) return fail(NRLSH_EINVAL, "index is NULL");
     return exact_impl(ix->X, ix->n, ix->d, queries, nq, k, nullptr, 0, out_ids, out_scores,
-                      cuda_stream, ix->Xb, ix->xnorm);
+                      cuda_stream, ix->Xb, ix->xnorm_pos, ix->perm);
 }
 
 nrlsh_status nrlsh_index_exact_topk_seeded(const nrlsh_index *ix, const float *queries,
@@ -967,7 +979,7 @@ nrlsh_status nrlsh_index_exact_topk_seeded(const nrlsh_index *ix, const float *q
     if (!ix) return fail(NRLSH_EINVAL, "index is NULL");
     if (!seed_ids) return fail(NRLSH_EINVAL, "seed_ids is NULL");
     return exact_impl(ix->X, ix->n, ix->d, queries, nq, k, seed_ids, seed_k, out_ids, out_scores,
-                      cuda_stream, ix->Xb, ix->xnorm);
+                      cuda_stream, ix->Xb, ix->xnorm_pos, ix->perm);
 }
 
 // ------------------------------------------------------------------ hooks
@@ -1007,8 +1019,6 @@ nrlsh_status nrlsh_set_codes(nrlsh_index *ix, const uint32_t *codes) {
     if (!ix || !codes) return fail(NRLSH_EINVAL, "bad argument");
     cudaError_t e = cudaMemcpy(ix->codes, codes, (size_t)ix->n * ix->W * 4, cudaMemcpyDefault);
     if (e) return cuda_fail(e, "set codes");
-    launch_codes_by_id(ix, nullptr);
-    if ((e = cudaDeviceSynchronize())) return cuda_fail(e, "set codes (item order)");
     if (ix->samp_codes) {   // keep the pilot sample in step with the codes
         launch_gather_sample(ix, pilot_stride(ix->n), ix->samp_codes, ix->samp_part, nullptr);
         if ((e = cudaDeviceSynchronize())) return cuda_fail(e, "set codes (sample)");

@@ -814,14 +814,15 @@ __global__ void __launch_bounds__(256) k3_codes_simt(
 void launch_item_codes(const float *X, int64_t n, int d, const double *norm2,
                        const uint8_t *part, const double *V, const float *Apad, int L, int W,
                        const int32_t *pos_of_id, uint32_t *codes, void *Xb, int dpb,
-                       float *xnorm, float *Xpad, int dpad, cudaStream_t s) {
+                       float *xnorm, float *Xpad, int dpad, cudaStream_t s,
+                       const int32_t *perm) {
     if (codes_tc_supported(d, W)) {
         launch_item_codes_tc(X, n, d, norm2, part, V, Apad, L, W, pos_of_id, codes, Xb, dpb, Xpad,
                              dpad, s);
         return;
     }
     // SIMT path: the row copies in separate passes
-    if (Xb) launch_bf16_prep(X, n, d, dpb, Xb, xnorm, s);
+    if (Xb) launch_bf16_prep(X, n, d, dpb, Xb, nullptr, s, perm);
     if (Xpad) {
         cudaMemcpy2DAsync(Xpad, (size_t)dpad * 4, X, (size_t)d * 4, (size_t)d * 4, (size_t)n,
                           cudaMemcpyDeviceToDevice, s);

@@ -51,7 +51,7 @@ struct CodesArgs {
     const float *Apad;       // [(d+1) x N]
     const int32_t *pos_of_id;
     uint32_t *codes;         // [n x N/32], partition order
-    __nv_bfloat16 *Xb;       // optional bf16 row copy [n x dpb] (the converters have the rows)
+    __nv_bfloat16 *Xb;       // optional bf16 row copy [n x dpb], PARTITION order (row pos_of_id[i])
     int dpb;
     float *Xpad;             // optional fp32 row copy [n x dpad], 16-byte rows (re-rank gathers)
     int dpad;
@@ -137,7 +137,7 @@ __device__ __forceinline__ void conv_store_bf16(const CodesArgs &a, int64_t tile
         const int rr = 16 * w + j * rpi + l / lpr;
         const int64_t i = tile * CT_M + rr;
         if (i >= a.n) continue;
-        __nv_bfloat16 *dst = a.Xb + i * a.dpb + col;
+        __nv_bfloat16 *dst = a.Xb + (int64_t)__ldg(a.pos_of_id + i) * a.dpb + col;
         if (VEC == 4) {
             const __nv_bfloat162 p0 = __floats2bfloat162_rn(v[j * 4 + 0], v[j * 4 + 1]);
             const __nv_bfloat162 p1 = __floats2bfloat162_rn(v[j * 4 + 2], v[j * 4 + 3]);

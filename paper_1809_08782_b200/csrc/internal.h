@@ -25,20 +25,19 @@ struct nrlsh_index {
     float *X_owned = nullptr;
     float *Xpad = nullptr;      // fp32 rows [n x dpad], dpad = d rounded up to 4 (16-byte rows),
     int32_t dpad = 0;           //   only when d % 4 != 0: the re-rank's gather source
-    void *Xb = nullptr;         // bf16 rows [n x dpb], dpb = d rounded up to 8 (16-byte rows):
-    int32_t dpb = 0;            //   the GT tensor-core operand and the re-rank's filter pass
-    float *xnorm = nullptr;     // [n rounded up to 256] |x| rounded up (0 past n)
+    void *Xb = nullptr;         // bf16 rows [n x dpb], dpb = d rounded up to 8 (16-byte rows),
+    int32_t dpb = 0;            //   PARTITION order: the tensor-core filter's B operand
+    float *xnorm = nullptr;     // [n rounded up to 256] |x| rounded up (0 past n), item order
+    float *xnorm_pos = nullptr; // the same in partition order (the filter's |x| tiles)
 
     double *norm2 = nullptr;      // [n] item order
     int32_t *perm = nullptr;      // [n] position -> id
     int32_t *pos_of_id = nullptr; // [n] id -> position
     uint8_t *part_of_id = nullptr;  // [n rounded up to 256] (0 past n)
-    uint8_t *part_of_pos = nullptr; // [n]
+    uint8_t *part_of_pos = nullptr; // [n rounded up to 256] (0 past n)
     int64_t *offsets_d = nullptr;   // [m+1]
     double *V_d = nullptr;          // [m]
     uint32_t *codes = nullptr;      // [n x W], partition order
-    uint32_t *codes_id = nullptr;   // [n rounded up to 256 x W], item order (0 past n): the
-                                    //   tensor-core re-rank's membership test
     float *A = nullptr;             // [(d+1) x L] row-major (as generated)
     float *Apad = nullptr;          // [(d+1) x 32W], zero columns >= L
     uint16_t *R_d = nullptr;        // [m x (L+1)]
@@ -95,7 +94,8 @@ int partition_scatter(const double *norm2, const uint8_t *part_of_id, int64_t n,
 void launch_item_codes(const float *X, int64_t n, int d, const double *norm2,
                        const uint8_t *part_of_id, const double *V_d, const float *Apad,
                        int L, int W, const int32_t *pos_of_id, uint32_t *codes, void *Xb,
-                       int dpb, float *xnorm, float *Xpad, int dpad, cudaStream_t s);
+                       int dpb, float *xnorm, float *Xpad, int dpad, cudaStream_t s,
+                       const int32_t *perm);
 
 // K3 on tcgen05 (codes_tc.cu); the SIMT kernel above covers the other shapes
 bool codes_tc_supported(int d, int W);
@@ -165,7 +165,7 @@ void launch_rerank_bf(const float *X, int d, int ldx, const void *Xb, int dpb, c
                       const float *Q, int Qb, const int32_t *cand, int64_t ncand, int64_t cand_ld,
                       const uint32_t *ncand_per_q, int k, unsigned long long *partial,
                       int64_t *out_ids, float *out_scores, unsigned long long *nexact,
-                      cudaStream_t s);
+                      cudaStream_t s, const int32_t *xb_row = nullptr);
 
 // select split in two passes (query_kernels.cu): mode 1 = bound (B, pk, per-sub-dataset
 // candidate counts), mode 2 = emit the candidates outside dense sub-datasets
@@ -186,8 +186,8 @@ void launch_dense_merge(const unsigned long long *partial, int S, int k, const i
                         const float *g_sc, int Qb, int64_t *out_ids, float *out_scores,
                         cudaStream_t s);
 
-// item-order copy of the codes (codes_id[i] = codes[pos_of_id[i]])
-void launch_codes_by_id(const nrlsh_index *ix, cudaStream_t s);
+// dst[p] = src[idx[p]] for p < n
+void launch_gather_f32(const float *src, const int32_t *idx, int64_t n, float *dst, cudaStream_t s);
 // theta_glob[q] = orderable image of out_scores[q][k-1] when that slot holds an item
 void launch_theta_from_topk(const int64_t *ids, const float *scores, int Qb, int k,
                             uint32_t *theta_glob, cudaStream_t s);
@@ -214,23 +214,32 @@ void launch_gt_seed_theta(const float *X, int64_t n, int d, const float *Q, int 
                           uint32_t *theta_glob, cudaStream_t s);
 // tensor-core ground truth (tc_kernels.cu)
 void launch_bf16_prep(const float *X, int64_t n, int d, int dp, void *Xb, float *xnorm,
-                      cudaStream_t s);
+                      cudaStream_t s, const int32_t *perm = nullptr);
 bool gt_tc_supported(int d, int k);
 size_t gt_heap_bytes(int k);
 // Candidate membership for the tensor-core re-rank (the select's rule): item i is a
 // candidate of query q iff r = R[part(i)][h(q,i)] < B_q or (r == B_q and pos(i) <= pk_q)
+// (Xb rows are partition positions here; only the tiles of sub-datasets holding a
+// candidate of a query pair are streamed for it)
 struct GtMember {
-    const uint32_t *codes_id;   // [npad x W] item order
-    const uint8_t *part_id;     // [npad]
-    const int32_t *pos_of_id;   // [n]
+    const uint32_t *codes;      // [npad x W] partition order
+    const uint8_t *part;        // [npad] sub-dataset of each position
+    const int64_t *offsets;     // [m+1] (device)
+    int m;
     const uint16_t *R;          // [m x (L+1)]
     int L, W;
     const uint32_t *qcodes;     // [Qb x W]
     const uint32_t *sel_B, *sel_pk;   // [Qb]
+    int32_t *tile_ws;           // gt_tile_ws_bytes(n, Qb) of scratch for the tile lists
+    unsigned long long *pairs;  // optional: += (query, row) pairs multiplied
 };
+size_t gt_tile_ws_bytes(int64_t n, int Qb);
+// Xb / xnorm rows in any order: perm[row] = item id written to the survivor lists
+// (nullptr: rows are ids)
 int launch_gt_filter_tc(const void *Xb, int64_t n, int d, int dp, const void *Qb16, int Qb,
                         const float *xnorm, const float *qnorm, float eps_rel, int k,
                         uint32_t *theta_glob, float *heap, int32_t *cand, uint32_t *cnt,
-                        int64_t C, cudaStream_t s, const GtMember *member = nullptr);
+                        int64_t C, cudaStream_t s, const int32_t *perm = nullptr,
+                        const GtMember *member = nullptr);
 
 }  // namespace nrlsh

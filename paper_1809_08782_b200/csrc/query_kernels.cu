@@ -678,25 +678,15 @@ void launch_select_seeds(const nrlsh_index *ix, int Qb, int64_t Tq, const unsign
 }
 
 // ------------------------------------------------------- tensor-core re-rank helpers
-template <int W>
-__global__ void codes_by_id(const uint32_t *__restrict__ codes, const int32_t *__restrict__ pos_of_id,
-                            int64_t n, uint32_t *__restrict__ out) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        uint32_t c[W];
-        load_code<W>(codes, pos_of_id[i], c);
-#pragma unroll
-        for (int w = 0; w < W; ++w) out[i * W + w] = c[w];
-    }
+__global__ void gather_f32(const float *__restrict__ src, const int32_t *__restrict__ idx, int64_t n,
+                           float *__restrict__ dst) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+         p += (int64_t)gridDim.x * blockDim.x)
+        dst[p] = src[idx[p]];
 }
 
-void launch_codes_by_id(const nrlsh_index *ix, cudaStream_t s) {
-    const int grid = grid_for(ix->n, 256, 4096);
-    switch (ix->W) {
-        case 1: codes_by_id<1><<<grid, 256, 0, s>>>(ix->codes, ix->pos_of_id, ix->n, ix->codes_id); break;
-        case 2: codes_by_id<2><<<grid, 256, 0, s>>>(ix->codes, ix->pos_of_id, ix->n, ix->codes_id); break;
-        default: codes_by_id<4><<<grid, 256, 0, s>>>(ix->codes, ix->pos_of_id, ix->n, ix->codes_id); break;
-    }
+void launch_gather_f32(const float *src, const int32_t *idx, int64_t n, float *dst, cudaStream_t s) {
+    gather_f32<<<grid_for(n, 256, 4096), 256, 0, s>>>(src, idx, n, dst);
     note_launch();
 }
 
@@ -1111,7 +1101,8 @@ __global__ void __launch_bounds__(kRrThreads) k8_rerank_bf(
     const int32_t *__restrict__ cand, int64_t cand_ld, int64_t ncand,
     const uint32_t *__restrict__ ncand_per_q, int k, int cap, int64_t slice,
     unsigned long long *__restrict__ partial, int64_t *__restrict__ out_ids,
-    float *__restrict__ out_scores, unsigned long long *__restrict__ nexact) {
+    float *__restrict__ out_scores, unsigned long long *__restrict__ nexact,
+    const int32_t *__restrict__ xb_row) {
     extern __shared__ __align__(16) unsigned long long rr_smem[];
     unsigned long long *buf = rr_smem;                       // [cap]
     float *sq = reinterpret_cast<float *>(buf + cap);        // [dpad] fp32 q
@@ -1161,7 +1152,8 @@ __global__ void __launch_bounds__(kRrThreads) k8_rerank_bf(
             const int id = __shfl_sync(NR_FULL, myid, st * 4 + grp);
             const float xn = __shfl_sync(NR_FULL, myxn, st * 4 + grp);
             float sa = 0.f;
-            if (id >= 0) sa = row_dot_bf<NB>(Xb + (int64_t)id * dpb, sqb, sub, nchunk);
+            if (id >= 0)   // (Xb rows are partition positions: xb_row = pos_of_id)
+                sa = row_dot_bf<NB>(Xb + (int64_t)(xb_row ? __ldg(xb_row + id) : id) * dpb, sqb, sub, nchunk);
             sa += __shfl_xor_sync(NR_FULL, sa, 1);
             sa += __shfl_xor_sync(NR_FULL, sa, 2);
             sa += __shfl_xor_sync(NR_FULL, sa, 4);
@@ -1312,7 +1304,7 @@ void launch_rerank_bf(const float *X, int d, int ldx, const void *Xb, int dpb, c
                       const float *Q, int Qb, const int32_t *cand, int64_t ncand, int64_t cand_ld,
                       const uint32_t *ncand_per_q, int k, unsigned long long *partial,
                       int64_t *out_ids, float *out_scores, unsigned long long *nexact,
-                      cudaStream_t s) {
+                      cudaStream_t s, const int32_t *xb_row) {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     const int64_t rounds = std::max<int64_t>(1, (ncand + kRrRound - 1) / kRrRound);
@@ -1338,7 +1330,7 @@ void launch_rerank_bf(const float *X, int d, int ldx, const void *Xb, int dpb, c
                              (int)sm);                                                          \
         k8_rerank_bf<V, B><<<grid, kRrThreads, sm, s>>>(                                        \
             X, ldx, d, (const uint16_t *)Xb, dpb, xnorm, eps, Q, cand, cand_ld, ncand,        \
-            ncand_per_q, k, cap, slice, pp, out_ids, out_scores, nexact);                       \
+            ncand_per_q, k, cap, slice, pp, out_ids, out_scores, nexact, xb_row);               \
     } while (0)
 #define NR_RB_V(V)                                                   \
     switch (nb) {                                                    \

@@ -26,13 +26,15 @@
 namespace nrlsh {
 
 // ------------------------------------------------------------ operand prep
-// fp32 rows -> bf16 rows padded to dp (multiple of 8) + fp32 |row| rounded up.
+// fp32 rows -> bf16 rows padded to dp (multiple of 8) + fp32 |row| rounded up;
+// with perm, output row i is input row perm[i].
 __global__ void bf16_prep(const float *__restrict__ X, int64_t n, int d, int dp,
-                          __nv_bfloat16 *__restrict__ Xb, float *__restrict__ xnorm) {
+                          __nv_bfloat16 *__restrict__ Xb, float *__restrict__ xnorm,
+                          const int32_t *__restrict__ perm) {
     const int lane = threadIdx.x & 31;
     for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < n;
          i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-        const float *src = X + i * (int64_t)d;
+        const float *src = X + (perm ? (int64_t)perm[i] : i) * (int64_t)d;
         __nv_bfloat16 *dst = Xb + i * (int64_t)dp;
         double s = 0.0;
         for (int k = lane; k < dp; k += 32) {
@@ -42,16 +44,16 @@ __global__ void bf16_prep(const float *__restrict__ X, int64_t n, int d, int dp,
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(NR_FULL, s, o);
-        if (lane == 0) xnorm[i] = __double2float_ru(sqrt(s) * (1.0 + 0x1p-50));   // upper bound
+        if (lane == 0 && xnorm) xnorm[i] = __double2float_ru(sqrt(s) * (1.0 + 0x1p-50));   // upper bound
     }
 }
 
 void launch_bf16_prep(const float *X, int64_t n, int d, int dp, void *Xb, float *xnorm,
-                      cudaStream_t s) {
+                      cudaStream_t s, const int32_t *perm) {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     bf16_prep<<<grid_for(n * 32, 256, sms * 16), 256, 0, s>>>(X, n, d, dp, (__nv_bfloat16 *)Xb,
-                                                             xnorm);
+                                                             xnorm, perm);
     note_launch();
 }
 
@@ -137,14 +139,34 @@ struct GtArgs {
     // candidate-membership mode (the tensor-core re-rank): survivors must also be
     // candidates of their query; the running bound is over candidates only
     int member;
-    const uint32_t *codes_id;
-    const uint8_t *part_id;
-    const int32_t *pos_of_id;
+    const uint32_t *codes;  // [npad x W] in the row order of Xb (partition order)
+    const uint8_t *part;    // [npad]
     const uint16_t *R;
     int L, W;
     const uint32_t *qcodes;
     const uint32_t *sel_B, *sel_pk;
+    const int32_t *perm;    // row -> item id of the survivors (nullptr: identity)
+    // per query-pair tile lists (member mode: only tiles of sub-datasets holding a
+    // candidate of the pair's queries); nullptr: every tile
+    const int32_t *tlist;   // [nqp x tstride] tile indices
+    const int32_t *tcount;  // [nqp]
+    int64_t tstride;
+    int64_t split_tiles;    // tiles per split without lists
+    int64_t ntiles;
 };
+
+// Unit (query pair qp, split sp) takes every nsplit-th tile starting at sp: rows in
+// partition order sort by norm, and the high-norm tiles (where the filter keeps the
+// most) spread over all splits instead of loading the last few.  v = 0..count-1
+// indexes the unit's tiles; the CTAs of the other pairs of a split read the same ones.
+__device__ __forceinline__ int64_t gt_unit_count(const GtArgs &a, int qp, int sp) {
+    const int64_t c = a.tlist ? (int64_t)a.tcount[qp] : a.ntiles;
+    return c > sp ? (c - sp + a.nsplit - 1) / a.nsplit : 0;
+}
+__device__ __forceinline__ int64_t gt_tile_row0(const GtArgs &a, int qp, int sp, int64_t v, int nt) {
+    const int64_t e = sp + v * a.nsplit;
+    return (a.tlist ? (int64_t)__ldg(a.tlist + qp * a.tstride + e) : e) * nt;
+}
 
 __device__ __forceinline__ float fmax3f(float a, float b, float c) {
     float r;
@@ -268,19 +290,20 @@ struct GtEpiRow {
                     if (jj == j) s_j = __uint_as_float(hh ? r1[jj] : r0[jj]);
                 const float x = xn[col];
                 if (__fmaf_ru(x, qe, s_j) < theta) continue;   // exact re-test
-                const int64_t i = i0 + col;
+                const int64_t i = i0 + col;   // row of Xb
                 if (i >= a->n) continue;
-                if (a->member) {   // candidate of q? (the select's rule)
+                if (a->member) {   // candidate of q? (the select's rule; rows are positions)
                     const uint32_t *cw = scode + col * a->W;
                     int hq = 0;
 #pragma unroll
                     for (int w = 0; w < 4; ++w)
                         if (w < a->W) hq += __popc(cw[w] ^ qcw[w]);
                     const uint32_t r = __ldg(a->R + spart[col] * (a->L + 1) + hq);
-                    if (!(r < Bq || (r == Bq && (uint32_t)__ldg(a->pos_of_id + i) <= pkq))) continue;
+                    if (!(r < Bq || (r == Bq && (uint32_t)i <= pkq))) continue;
                 }
                 if (sleft == 0) { sbase = atomicAdd(&a->cnt[q], 16u); sleft = 16; }
-                if (sbase + (16 - sleft) < a->C) cl[sbase + (16 - sleft)] = (int32_t)i;
+                if (sbase + (16 - sleft) < a->C)
+                    cl[sbase + (16 - sleft)] = a->perm ? __ldg(a->perm + i) : (int32_t)i;
                 --sleft;
                 const float lb = __fmaf_rd(-x, qe, s_j);
                 const int k = a->k;
@@ -328,7 +351,6 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
     constexpr int GT_N = NT;                     // items per tile
     constexpr int GT_B_BLK = NT * 128;           // one K block of a tile
     constexpr int NBUF = 512 / (GT_QB * NT);     // TMEM accumulator buffers per block
-    auto gt_tile_at = [&](int64_t ib, int64_t jt) -> int64_t { return ib + jt * GT_N; };
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
     uint8_t *sA = smem;                                        // QB x kblocks x 16 KB
@@ -372,8 +394,7 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
         uint32_t g = 0, ul = 0;
         for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++ul) {
             const int qp = u % a.nqp, sp = u / a.nqp;
-            const int64_t ib = (int64_t)sp * a.split_items;
-            const int64_t ie = min(a.n, ib + a.split_items);
+            const int64_t v0 = 0, v1 = gt_unit_count(a, qp, sp);
             // query blocks of this pair that hold any query (a block wholly past Qb
             // is neither loaded nor multiplied)
             const int nh = min(GT_QB, (a.Qb - qp * GT_QB * GT_M + GT_M - 1) / GT_M);
@@ -383,11 +404,10 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
                 for (int kb = 0; kb < a.kblocks; ++kb)
                     tc::tma_load_2d(sA + (h * a.kblocks + kb) * GT_A_BLK, &tmQ, a_full, kb * GT_KB,
                                     (qp * GT_QB + h) * GT_M);
-            const int64_t ntu = (ie - ib + GT_N - 1) / GT_N;
-            for (int64_t jt = 0; jt < ntu; ++jt) {
-                const int64_t i0 = gt_tile_at(ib, jt);
-                if (a.prefetch > 0 && jt + a.prefetch < ntu) {
-                    const int64_t ip = gt_tile_at(ib, jt + a.prefetch);
+            for (int64_t v = v0; v < v1; ++v) {
+                const int64_t i0 = gt_tile_row0(a, qp, sp, v, GT_N);
+                if (a.prefetch > 0 && v + a.prefetch < v1) {
+                    const int64_t ip = gt_tile_row0(a, qp, sp, v + a.prefetch, GT_N);
                     for (int kb = 0; kb < a.kblocks; ++kb) tc::tma_prefetch_2d(&tmX, kb * GT_KB, (int)ip);
                 }
                 for (int kb = 0; kb < a.kblocks; ++kb, ++g) {
@@ -405,11 +425,10 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
         for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++ul) {
             const int qp = u % a.nqp, sp = u / a.nqp;
             const int nh = min(GT_QB, (a.Qb - qp * GT_QB * GT_M + GT_M - 1) / GT_M);
-            const int64_t ib = (int64_t)sp * a.split_items;
-            const int64_t ie = min(a.n, ib + a.split_items);
+            const int64_t v0 = 0, v1 = gt_unit_count(a, qp, sp);
             tc::mbar_wait(a_full, ul & 1);
             tc::tc_fence_after();
-            for (int64_t i0 = ib; i0 < ie; i0 += GT_N, ++t) {
+            for (int64_t v = v0; v < v1; ++v, ++t) {
                 const uint32_t buf = t % NBUF, tr = t / NBUF;
                 for (int kb = 0; kb < a.kblocks; ++kb, ++g) {
                     const uint32_t s = g % a.stages, r = g / a.stages;
@@ -442,19 +461,17 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
         // copies into the tile's buffer once both epilogue groups released it
         uint32_t t = 0;
         for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
-            const int sp = u / a.nqp;
-            const int64_t ib = (int64_t)sp * a.split_items;
-            const int64_t ie = min(a.n, ib + a.split_items);
-            const int64_t ntu = (ie - ib + GT_N - 1) / GT_N;
-            for (int64_t jt = 0; jt < ntu; ++jt, ++t) {
-                const int64_t i0 = gt_tile_at(ib, jt);
+            const int qp = u % a.nqp, sp = u / a.nqp;
+            const int64_t v0 = 0, v1 = gt_unit_count(a, qp, sp);
+            for (int64_t v = v0; v < v1; ++v, ++t) {
+                const int64_t i0 = gt_tile_row0(a, qp, sp, v, GT_N);
                 const uint32_t b = t & 1, tr = t >> 1;
                 tc::mbar_wait(&xempty[b], (tr & 1) ^ 1);
                 tc::mbar_arrive_expect_tx(&xfull[b], GT_N * 4 + (a.member ? GT_N * (a.W * 4 + 1) : 0));
                 tc::bulk_load(sxn + b * GT_N, a.xnorm + i0, GT_N * 4, &xfull[b]);
-                if (a.member) {   // the tile's codes and sub-datasets (item order)
-                    tc::bulk_load(scode + b * GT_N * 4, a.codes_id + i0 * a.W, GT_N * a.W * 4, &xfull[b]);
-                    tc::bulk_load(spart + b * GT_N, a.part_id + i0, GT_N, &xfull[b]);
+                if (a.member) {   // the tile's codes and sub-datasets
+                    tc::bulk_load(scode + b * GT_N * 4, a.codes + i0 * a.W, GT_N * a.W * 4, &xfull[b]);
+                    tc::bulk_load(spart + b * GT_N, a.part + i0, GT_N, &xfull[b]);
                 }
             }
         }
@@ -470,16 +487,14 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
             const int qp = u % a.nqp, sp = u / a.nqp;
             const int nh = min(GT_QB, (a.Qb - qp * GT_QB * GT_M + GT_M - 1) / GT_M);
             const bool hact = h < nh;   // this group's block holds queries in this unit
-            const int64_t ib = (int64_t)sp * a.split_items;
-            const int64_t ie = min(a.n, ib + a.split_items);
+            const int64_t v0 = 0, v1 = gt_unit_count(a, qp, sp);
             const int q = (qp * GT_QB + h) * GT_M + row;
             // heap of this CTA's query row (CTAs of other item splits keep their own)
             er.begin(a, q, hact && q < a.Qb,
                      a.heap_smem ? sheap + (h * GT_M + row) * a.k
                                  : a.heap + ((int64_t)(blockIdx.x * 2 + h) * GT_M + row) * a.k);
-            const int64_t ntu = (ie - ib + GT_N - 1) / GT_N;
-            for (int64_t jt = 0; jt < ntu; ++jt, ++t) {
-                const int64_t i0 = gt_tile_at(ib, jt);
+            for (int64_t v = v0; v < v1; ++v, ++t) {
+                const int64_t i0 = gt_tile_row0(a, qp, sp, v, GT_N);
                 const uint32_t b = t & 1;
                 const float *xn = sxn + b * GT_N;
                 uint32_t o_next = 0;
@@ -659,8 +674,8 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
                 tc::mbar_arrive_expect_tx(&xfull[b], GP_PN * 4 + (a.member ? GP_PN * (a.W * 4 + 1) : 0));
                 tc::bulk_load(sxn + b * GP_PN, a.xnorm + i0, GP_PN * 4, &xfull[b]);
                 if (a.member) {
-                    tc::bulk_load(scode + b * GP_PN * 4, a.codes_id + i0 * a.W, GP_PN * a.W * 4, &xfull[b]);
-                    tc::bulk_load(spart + b * GP_PN, a.part_id + i0, GP_PN, &xfull[b]);
+                    tc::bulk_load(scode + b * GP_PN * 4, a.codes + i0 * a.W, GP_PN * a.W * 4, &xfull[b]);
+                    tc::bulk_load(spart + b * GP_PN, a.part + i0, GP_PN, &xfull[b]);
                 }
             }
         }
@@ -737,6 +752,61 @@ size_t gt_heap_bytes(int k) {
     return (size_t)sms * 2 * GT_M * k * 4;
 }
 
+// Tile lists of the member mode: for query pair g, the NT-row tiles (partition
+// order) overlapping a sub-dataset j with R[j][0] <= B_q for some query q of the
+// pair (j holds candidates of q only then: R[j][h] grows with h).
+__global__ void __launch_bounds__(256) gt_tile_lists(const uint16_t *__restrict__ R, int L, int m,
+                                                     const uint8_t *__restrict__ part, int64_t n,
+                                                     const uint32_t *__restrict__ sel_B, int Qb, int nt,
+                                                     int32_t *__restrict__ list, int64_t stride,
+                                                     int32_t *__restrict__ count,
+                                                     unsigned long long *__restrict__ pairs) {
+    __shared__ uint32_t act[257];
+    __shared__ uint32_t ws[32];
+    __shared__ uint32_t s_base;
+    const int g = blockIdx.x;
+    const int q0 = g * 2 * GT_M, q1 = min(Qb, q0 + 2 * GT_M);
+    for (int j = threadIdx.x; j < m; j += blockDim.x) {
+        const uint32_t r0 = R[j * (L + 1)];
+        uint32_t on = 0;
+        for (int q = q0; q < q1 && !on; ++q) on = r0 <= sel_B[q];
+        act[j] = on;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {   // inclusive prefix count, act[j+1] = #active in [0, j]
+        uint32_t c = 0;
+        for (int j = 0; j < m; ++j) { const uint32_t v = act[j]; act[j] = c; c += v; }
+        act[m] = c;
+        s_base = 0;
+    }
+    __syncthreads();
+    const int64_t ntiles = (n + nt - 1) / nt;
+    for (int64_t t0 = 0; t0 < ntiles; t0 += blockDim.x) {
+        const int64_t t = t0 + threadIdx.x;
+        uint32_t on = 0;
+        if (t < ntiles) {
+            const int j0 = part[t * nt], j1 = part[min(n - 1, t * nt + nt - 1)];
+            on = act[j1 + 1] - act[j0] > 0;
+        }
+        uint32_t tot;
+        const uint32_t ex = block_excl_scan(on, ws, &tot);
+        if (on) list[g * stride + s_base + ex] = (int32_t)t;
+        __syncthreads();
+        if (threadIdx.x == 0) s_base += tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        count[g] = (int32_t)s_base;
+        // (query, item) pairs the filter multiplies for this pair's real queries
+        if (pairs) atomicAdd(pairs, (unsigned long long)s_base * nt * (unsigned long long)(q1 - q0));
+    }
+}
+
+size_t gt_tile_ws_bytes(int64_t n, int Qb) {
+    const int64_t ng = (Qb + 2 * GT_M - 1) / (2 * GT_M);
+    return (size_t)(ng * (1 + (n + 127) / 128) + 4) * 4;
+}
+
 static int gt_pick_nt(int kb) {
     if (getenv("NRLSH_GT_NT") && atoi(getenv("NRLSH_GT_NT")) == 128) return 128;
     return gt_tc_smem_bytes(256, kb, 3, 0) <= 227 * 1024 ? 256 : 128;
@@ -752,7 +822,7 @@ bool gt_tc_supported(int d, int k) {
 int launch_gt_filter_tc(const void *Xb, int64_t n, int d, int dp, const void *Qb16, int Qb,
                         const float *xnorm, const float *qnorm, float eps_rel, int k,
                         uint32_t *theta_glob, float *heap, int32_t *cand, uint32_t *cnt, int64_t C,
-                        cudaStream_t s, const GtMember *mb) {
+                        cudaStream_t s, const int32_t *perm, const GtMember *mb) {
     const int kblocks = (dp + GT_KB - 1) / GT_KB;
     const int NT = gt_pick_nt(kblocks);
     CUtensorMap tq, tx;
@@ -779,10 +849,13 @@ int launch_gt_filter_tc(const void *Xb, int64_t n, int d, int dp, const void *Qb
     a.dbg = getenv("NRLSH_GT_DBG") ? atoi(getenv("NRLSH_GT_DBG")) : 0;
     a.prefetch = getenv("NRLSH_GT_PREFETCH") ? atoi(getenv("NRLSH_GT_PREFETCH")) : GT_PREFETCH;
     a.member = mb != nullptr;
-    a.codes_id = mb ? mb->codes_id : nullptr;
-    a.part_id = mb ? mb->part_id : nullptr;
-    a.pos_of_id = mb ? mb->pos_of_id : nullptr;
+    a.codes = mb ? mb->codes : nullptr;
+    a.part = mb ? mb->part : nullptr;
     a.R = mb ? mb->R : nullptr;
+    a.perm = perm;
+    a.tlist = nullptr;
+    a.tcount = nullptr;
+    a.tstride = 0;
     a.L = mb ? mb->L : 0;
     a.W = mb ? mb->W : 1;
     a.qcodes = mb ? mb->qcodes : nullptr;
@@ -792,7 +865,7 @@ int launch_gt_filter_tc(const void *Xb, int64_t n, int d, int dp, const void *Qb
     // CTA-pair kernel: opt-in (NRLSH_GT_PAIR=1) — correct, but measured slower than
     // the single-CTA N=256 kernel on c4 (0.84 vs 0.72 ms per 1024 queries: ~6.7K
     // cycles per pair tile against 1.3K of MMA work)
-    const bool use_pair = Qb > GT_M && getenv("NRLSH_GT_PAIR") && atoi(getenv("NRLSH_GT_PAIR")) == 1 &&
+    const bool use_pair = Qb > GT_M && !mb && getenv("NRLSH_GT_PAIR") && atoi(getenv("NRLSH_GT_PAIR")) == 1 &&
                           gp_smem_bytes(kblocks, 4, 0) <= 227 * 1024;
     if (use_pair) {
         CUtensorMap tq2, tx2;
@@ -847,8 +920,21 @@ int launch_gt_filter_tc(const void *Xb, int64_t n, int d, int dp, const void *Qb
     const int64_t ntiles = (n + NT - 1) / NT;
     int nsplit = std::max(1, sms / a.nqp);     // one unit per CTA: no tail wave
     nsplit = (int)std::min<int64_t>(nsplit, ntiles);
-    a.split_items = ((ntiles + nsplit - 1) / nsplit) * NT;
+    a.split_tiles = (ntiles + nsplit - 1) / nsplit;
+    a.split_items = a.split_tiles * NT;
     a.nsplit = (int)((n + a.split_items - 1) / a.split_items);
+    a.ntiles = ntiles;
+    if (mb && mb->tile_ws && !getenv("NRLSH_RERANK_TC_ALLTILES")) {
+        // member mode: per query pair, only the tiles of sub-datasets with candidates
+        a.tcount = mb->tile_ws;
+        a.tstride = ntiles;
+        a.tlist = mb->tile_ws + a.nqp + 4;
+        a.nsplit = nsplit;
+        gt_tile_lists<<<a.nqp, 256, 0, s>>>(mb->R, mb->L, mb->m, mb->part, n, mb->sel_B, Qb, NT,
+                                            const_cast<int32_t *>(a.tlist), a.tstride,
+                                            const_cast<int32_t *>(a.tcount), mb->pairs);
+        note_launch();
+    }
     // deepest ring that fits, with the heaps in smem if they fit too
     const int smax = NT == 256 ? 6 : GT_MAX_STAGES;
     a.stages = 3;
