@@ -216,14 +216,16 @@ void launch_pilot(const nrlsh_index *ix, const uint32_t *qcodes, int Qb, int64_t
 
 // =========================================================================== K6 scan
 constexpr int kScanThreads = 256;
-constexpr int kScanIPT = 4;                       // items per thread
+constexpr int kScanIPT = 8;                       // items per thread
 constexpr int kChunk = kScanThreads * kScanIPT;   // items per work unit
 constexpr int kQG = 64;                           // queries per CTA
-constexpr int kSB = 64;                           // staged appends per (CTA, query)
+constexpr int kSB = 128;                          // staged appends per (CTA, query)
 
-// Appends (R << 32 | pos) are staged per query in shared memory (one shared
-// atomic per warp ballot) and copied out with one global reservation per
-// (CTA, query); a query whose stage fills spills the rest straight to global.
+// Appends are staged per query in shared memory as (h << 16 | offset in chunk)
+// — one shared atomic per (warp, query) after a warp prefix sum of the lanes'
+// pass counts — and copied out, expanded to (flat (j, h) << 32 | position), with
+// one global reservation per (CTA, query); a query whose stage fills spills the
+// rest straight to global.
 template <int W>
 __global__ void __launch_bounds__(kScanThreads) k6_scan(
     const uint32_t *__restrict__ codes, const int4 *__restrict__ chunks,
@@ -232,7 +234,7 @@ __global__ void __launch_bounds__(kScanThreads) k6_scan(
     uint32_t *__restrict__ cnt, int64_t C, unsigned long long *__restrict__ pairs) {
     __shared__ uint32_t sq[kQG][W];
     __shared__ int sd[kQG];
-    __shared__ unsigned long long sbuf[kQG][kSB];
+    __shared__ uint32_t sbuf[kQG][kSB];
     __shared__ uint32_t scnt[kQG];
     __shared__ uint32_t sbase[kQG];
     // consecutive CTAs share a chunk (different query groups): the chunk's codes
@@ -267,17 +269,18 @@ __global__ void __launch_bounds__(kScanThreads) k6_scan(
     if (nact == 0) return;
     if (threadIdx.x == 0 && pairs) atomicAdd(pairs, (unsigned long long)nact * (p1 - p0));
     const int lane = threadIdx.x & 31;
-    const unsigned lt = lanemask_lt();
     uint32_t c[kScanIPT][W];
-    bool valid[kScanIPT];
+    uint32_t vmask = 0;   // bit u: item u of this thread exists
 #pragma unroll
     for (int u = 0; u < kScanIPT; ++u) {
         const int p = p0 + threadIdx.x + kScanThreads * u;
-        valid[u] = p < p1;
-        if (valid[u]) load_code<W>(codes, p, c[u]);
-        else
+        if (p < p1) {
+            load_code<W>(codes, p, c[u]);
+            vmask |= 1u << u;
+        } else {
 #pragma unroll
             for (int w = 0; w < W; ++w) c[u][w] = 0u;
+        }
     }
     for (int ia = 0; ia < nact; ++ia) {
         const int qq = sact[ia];
@@ -285,38 +288,49 @@ __global__ void __launch_bounds__(kScanThreads) k6_scan(
         uint32_t qc[W];
 #pragma unroll
         for (int w = 0; w < W; ++w) qc[w] = sq[qq][w];
-        int h[kScanIPT];
-        bool pass[kScanIPT];
-        bool any = false;
+        uint32_t mask = 0, hp = 0;   // pass bits; h of the passing items, 8 bits each (first 4)
+        int hh[kScanIPT];
 #pragma unroll
         for (int u = 0; u < kScanIPT; ++u) {
-            h[u] = hamming<W>(c[u], qc);
-            pass[u] = valid[u] && (h[u] <= dl);
-            any |= pass[u];
+            hh[u] = hamming<W>(c[u], qc);
+            mask |= (uint32_t)(hh[u] <= dl) << u;
         }
-        if (!__any_sync(NR_FULL, any)) continue;
+        mask &= vmask;
+        if (!__any_sync(NR_FULL, mask != 0u)) continue;
+        // warp prefix sum of the pass counts -> one shared reservation per warp
+        const int np = __popc(mask);
+        int inc = np;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(NR_FULL, inc, o);
+            if (lane >= o) inc += y;
+        }
+        const int tot = __shfl_sync(NR_FULL, inc, 31);
+        uint32_t base = 0, gbase = 0;
+        if (lane == 31) {
+            base = atomicAdd(&scnt[qq], (uint32_t)tot);
+            // the part past the stage goes straight to global: one reservation per warp
+            const uint32_t lo = max(base, (uint32_t)kSB), hi = base + (uint32_t)tot;
+            if (hi > lo) gbase = atomicAdd(&cnt[q0 + qq], hi - lo);
+        }
+        base = __shfl_sync(NR_FULL, base, 31);
+        gbase = __shfl_sync(NR_FULL, gbase, 31);
+        const uint32_t glo = max(base, (uint32_t)kSB);
+        uint32_t slot = base + inc - np;
+        (void)hp;
 #pragma unroll
         for (int u = 0; u < kScanIPT; ++u) {
-            const unsigned bal = __ballot_sync(NR_FULL, pass[u]);
-            if (bal == 0u) continue;
-            const int leader = __ffs(bal) - 1;
-            uint32_t base = 0;
-            if (lane == leader) base = atomicAdd(&scnt[qq], (uint32_t)__popc(bal));
-            base = __shfl_sync(NR_FULL, base, leader);
-            if (pass[u]) {
-                const uint32_t slot = base + __popc(bal & lt);
-                const uint32_t p = p0 + threadIdx.x + kScanThreads * u;
-                // entry: (flat (j, h) index of the sorted structure << 32) | position;
-                // select maps it to the structure position R[j][h]
-                const unsigned long long e = ((unsigned long long)(j * (L + 1) + h[u]) << 32) | p;
-                if (slot < kSB) {
-                    sbuf[qq][slot] = e;
-                } else {   // stage full: direct global append (rare)
-                    const int q = q0 + qq;
-                    const uint32_t g = atomicAdd(&cnt[q], 1u);
-                    if (g < C) buf[(int64_t)q * C + g] = e;
-                }
+            if (!(mask >> u & 1u)) continue;
+            const uint32_t off = threadIdx.x + kScanThreads * u;
+            if (slot < kSB) {
+                sbuf[qq][slot] = ((uint32_t)hh[u] << 16) | off;
+            } else {   // stage full: direct global append
+                const uint32_t g = gbase + (slot - glo);
+                if (g < C)
+                    buf[(int64_t)(q0 + qq) * C + g] =
+                        ((unsigned long long)(j * (L + 1) + hh[u]) << 32) | (p0 + off);
             }
+            ++slot;
         }
     }
     __syncthreads();
@@ -326,13 +340,17 @@ __global__ void __launch_bounds__(kScanThreads) k6_scan(
     }
     __syncthreads();
     // copy-out: warp w handles queries w, w+8, ...; lanes stride the staged entries
+    // entry: (flat (j, h) index of the sorted structure << 32) | position; select maps
+    // it to the structure position R[j][h]
     const int warp = threadIdx.x >> 5;
+    const unsigned long long jb = (unsigned long long)(j * (L + 1));
     for (int t = warp; t < nqg; t += kScanThreads / 32) {
         const uint32_t nst = min(scnt[t], (uint32_t)kSB);
         const int64_t q = q0 + t;
         for (uint32_t e = lane; e < nst; e += 32) {
             const uint32_t g = sbase[t] + e;
-            if (g < C) buf[q * C + g] = sbuf[t][e];
+            const uint32_t v = sbuf[t][e];
+            if (g < C) buf[q * C + g] = ((jb + (v >> 16)) << 32) | (uint32_t)(p0 + (v & 0xffffu));
         }
     }
 }
