@@ -142,7 +142,7 @@ void free_index(nrlsh_index *ix) {
     void *ps[] = {ix->X_owned, ix->Xpad, ix->Xb, ix->xnorm, ix->norm2, ix->perm, ix->pos_of_id, ix->part_of_id,
                   ix->part_of_pos, ix->offsets_d, ix->V_d, ix->codes, ix->A, ix->Apad,
                   ix->R_d, ix->chunks_d, ix->order_d, ix->samp_codes, ix->samp_part,
-                  ix->tiles_d, ix->xnorm_pos};
+                  ix->tiles_d, ix->xnorm_pos, ix->tile_xmax};
     // pool-backed (cudaMallocAsync at build); the index may have been used on any stream
     cudaDeviceSynchronize();
     for (void *p : ps)
@@ -300,6 +300,7 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
     cudaMemsetAsync(ix->part_of_pos + n, 0, (size_t)(npad - n), s);
     NR_ALLOC(ix->xnorm_pos, (size_t)npad * 4);
     cudaMemsetAsync(ix->xnorm_pos + n, 0, (size_t)(npad - n) * 4, s);
+    NR_ALLOC(ix->tile_xmax, (size_t)((n + 127) / 128) * 4);
     NR_ALLOC(ix->offsets_d, (size_t)(m + 1) * 8);
     NR_ALLOC(ix->V_d, (size_t)m * 8);
     NR_ALLOC(ix->codes, (size_t)n * W * 4);
@@ -389,6 +390,7 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
     {
         ProfScope p(SLOT_CODES, s);
         launch_gather_f32(ix->xnorm, ix->perm, n, ix->xnorm_pos, s);
+        launch_tile_xmax128(ix->xnorm_pos, n, ix->tile_xmax, s);
     }
     // compacted pilot sample (query-time pilots read it contiguously)
     {
@@ -403,6 +405,17 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
     }
     e = cudaStreamSynchronize(s);
     if (e) return cuda_fail(e, "codes");
+    {   // first-pass split of the filter's tiles: the ~2% of largest |x|
+        const int64_t nt = (n + 127) / 128;
+        if (nt >= 64) {
+            std::vector<float> xm((size_t)nt);
+            if ((e = cudaMemcpy(xm.data(), ix->tile_xmax, (size_t)nt * 4, cudaMemcpyDeviceToHost)))
+                return cuda_fail(e, "tile xmax");
+            const int64_t r = nt - std::max<int64_t>(1, nt / 50);
+            std::nth_element(xm.begin(), xm.begin() + r, xm.end());
+            ix->tile_xsplit = xm[(size_t)r];
+        }
+    }
     prof_collect();
     e = cudaGetLastError();
     if (e) return cuda_fail(e, "build launch");
@@ -607,8 +620,11 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
     mb.R = ix->R_d;
     mb.L = ix->L;
     mb.W = ix->W;
-    mb.tile_ws = use_rtc ? rtl.get<int32_t>() : nullptr;
-    mb.pairs = (unsigned long long *)(fl.get<int>() + 8);
+    GtTiles tls;
+    tls.xmax128 = ix->tile_xmax;
+    tls.ws = use_rtc ? rtl.get<int32_t>() : nullptr;
+    tls.pairs = (unsigned long long *)(fl.get<int>() + 8);
+    tls.xsplit = ix->tile_xsplit;
     const int init_flags[10] = {INT_MAX, INT_MAX, 0, 0, 0, 0, 0, 0, 0, 0};
     cudaMemcpyAsync(fl.p, init_flags, 40, cudaMemcpyHostToDevice, s);
     unsigned long long *pairs = (unsigned long long *)(fl.get<int>() + 4);
@@ -645,7 +661,7 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
             if (launch_gt_filter_tc(ix->Xb, n, ix->d, ix->dpb, rqb.p, Qb, ix->xnorm_pos,
                                     rqn.get<float>(), gt_eps_rel(ix->dpb), k, rth.get<uint32_t>(),
                                     rhp.get<float>(), rcd.get<int32_t>(), rcc.get<uint32_t>(), Cg,
-                                    s, ix->perm, &mb))
+                                    s, ix->perm, &mb, &tls))
                 return fail(NRLSH_ECUDA, "tensor map encoding failed");
             // exact fp32 re-rank of the surviving candidates (same arithmetic as the
             // gather path: identical scores and order)
@@ -814,7 +830,8 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
                                int64_t nq, int32_t k, const int64_t *seed_ids, int32_t seed_k,
                                int64_t *out_ids, float *out_scores, void *cuda_stream,
                                const void *Xb_ix = nullptr, const float *xnorm_ix = nullptr,
-                               const int32_t *perm_ix = nullptr) {
+                               const int32_t *perm_ix = nullptr,
+                               const float *tile_xmax_ix = nullptr, float xsplit_ix = 0.f) {
     if (!items || !queries || !out_ids || !out_scores) return fail(NRLSH_EINVAL, "NULL argument");
     if (seed_ids && (seed_k < 1 || seed_k > 1024))
         return fail(NRLSH_EINVAL, "seed_k must be in [1, 1024]");
@@ -848,7 +865,7 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
                               : std::min<int64_t>(n, std::max<int64_t>(4 * (int64_t)S * k + 4096, 2 * k));
     int Qmax = (int)std::min<int64_t>(1024, nq);
     while (Qmax > 64 && (int64_t)Qmax * (ns * 4 + Cg * 8) > ((int64_t)2500 << 20)) Qmax >>= 1;
-    DBuf xn, qn, ss, lb, tid, tsc, cc, cd, cs, xb, qb, th, pt, hp;
+    DBuf xn, qn, ss, lb, tid, tsc, cc, cd, cs, xb, qb, th, pt, hp, tw;
     const int64_t npad = (n + 255) / 256 * 256;   // |x| padded: the tc kernel bulk-loads 1 KB tiles
     if (xn.alloc((size_t)npad * 4, s) || qn.alloc((size_t)nq * 4, s) ||
         ss.alloc((size_t)Qmax * ns * 4, s) || lb.alloc((size_t)Qmax * 4, s) ||
@@ -862,7 +879,8 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
     const float *xnp = xnorm_ix;
     if (use_tc) {
         if ((!Xbp && xb.alloc((size_t)n * dp * 2, s)) || qb.alloc((size_t)nq * dp * 2, s) ||
-            hp.alloc(gt_heap_bytes(k), s))
+            hp.alloc(gt_heap_bytes(k), s) ||
+            (Xb_ix && tile_xmax_ix && tw.alloc(gt_tile_ws_bytes(n, Qmax), s)))
             return fail(NRLSH_ENOMEM, "exact_topk bf16 workspace");
         ProfScope p(SLOT_GT_NORMS, s);
         if (!Xbp) {
@@ -877,6 +895,13 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
         launch_vec_norms(X, n, d, xn.get<float>(), s);
         launch_vec_norms(Q, nq, d, qn.get<float>(), s);
     }
+    // rows in partition order (the index's): per query pair, only the tiles whose
+    // largest |x| can reach the pair's seeded bound (GtTiles)
+    GtTiles gtl;
+    gtl.xmax128 = tile_xmax_ix;
+    gtl.ws = tw.get<int32_t>();
+    gtl.pairs = nullptr;
+    gtl.xsplit = xsplit_ix;
     std::vector<uint32_t> hcnt(Qmax);
     for (int64_t q0 = 0; q0 < nq; q0 += Qmax) {
         const int Qb = (int)std::min<int64_t>(Qmax, nq - q0);
@@ -897,7 +922,8 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
             if (launch_gt_filter_tc(Xbp, n, d, dp, (const uint16_t *)qb.p + q0 * dp, Qb,
                                     xnp, qnb, eps_rel, k, th.get<uint32_t>(),
                                     hp.get<float>(), cd.get<int32_t>(), cc.get<uint32_t>(), Cg, s,
-                                    Xb_ix ? perm_ix : nullptr))
+                                    Xb_ix ? perm_ix : nullptr, nullptr,
+                                    (Xb_ix && tile_xmax_ix) ? &gtl : nullptr))
                 return fail(NRLSH_ECUDA, "tensor map encoding failed");
         } else {
             // pilot: certified lower bound of the k-th best score from a strided sample
@@ -969,7 +995,8 @@ nrlsh_status nrlsh_index_exact_topk(const nrlsh_index *ix, const float *queries,
                                     void *cuda_stream) {
     if (!ix) return fail(NRLSH_EINVAL, "index is NULL");
     return exact_impl(ix->X, ix->n, ix->d, queries, nq, k, nullptr, 0, out_ids, out_scores,
-                      cuda_stream, ix->Xb, ix->xnorm_pos, ix->perm);
+                      cuda_stream, ix->Xb, ix->xnorm_pos, ix->perm, ix->tile_xmax,
+                      ix->tile_xsplit);
 }
 
 nrlsh_status nrlsh_index_exact_topk_seeded(const nrlsh_index *ix, const float *queries,
@@ -979,7 +1006,8 @@ nrlsh_status nrlsh_index_exact_topk_seeded(const nrlsh_index *ix, const float *q
     if (!ix) return fail(NRLSH_EINVAL, "index is NULL");
     if (!seed_ids) return fail(NRLSH_EINVAL, "seed_ids is NULL");
     return exact_impl(ix->X, ix->n, ix->d, queries, nq, k, seed_ids, seed_k, out_ids, out_scores,
-                      cuda_stream, ix->Xb, ix->xnorm_pos, ix->perm);
+                      cuda_stream, ix->Xb, ix->xnorm_pos, ix->perm, ix->tile_xmax,
+                      ix->tile_xsplit);
 }
 
 // ------------------------------------------------------------------ hooks

@@ -29,6 +29,8 @@ struct nrlsh_index {
     int32_t dpb = 0;            //   PARTITION order: the tensor-core filter's B operand
     float *xnorm = nullptr;     // [n rounded up to 256] |x| rounded up (0 past n), item order
     float *xnorm_pos = nullptr; // the same in partition order (the filter's |x| tiles)
+    float *tile_xmax = nullptr; // [ceil(n/128)] largest xnorm_pos of each 128-row tile
+    float tile_xsplit = 0.f;    // xmax above which ~2% of those tiles lie (first filter pass)
 
     double *norm2 = nullptr;      // [n] item order
     int32_t *perm = nullptr;      // [n] position -> id
@@ -230,16 +232,26 @@ struct GtMember {
     int L, W;
     const uint32_t *qcodes;     // [Qb x W]
     const uint32_t *sel_B, *sel_pk;   // [Qb]
-    int32_t *tile_ws;           // gt_tile_ws_bytes(n, Qb) of scratch for the tile lists
+};
+// Tile pruning for rows in partition order (the index's Xb): per query pair, only
+// the NT-row tiles that can hold an answer are streamed — not the tiles whose
+// largest |x| keeps |q||x| (1 + 2 eps) below every query's starting bound theta_q
+// (Cauchy-Schwarz: such rows fail the filter's screen at that bound), and, in
+// member mode, not the tiles of sub-datasets without a candidate of the pair.
+struct GtTiles {
+    const float *xmax128;       // [ceil(n/128)] largest |x| (rounded up) per 128-row tile
+    int32_t *ws;                // gt_tile_ws_bytes(n, Qb) of scratch for the lists
     unsigned long long *pairs;  // optional: += (query, row) pairs multiplied
+    float xsplit;               // > 0: two passes, tiles with xmax >= xsplit first
 };
 size_t gt_tile_ws_bytes(int64_t n, int Qb);
+void launch_tile_xmax128(const float *xnorm_pos, int64_t n, float *out, cudaStream_t s);
 // Xb / xnorm rows in any order: perm[row] = item id written to the survivor lists
 // (nullptr: rows are ids)
 int launch_gt_filter_tc(const void *Xb, int64_t n, int d, int dp, const void *Qb16, int Qb,
                         const float *xnorm, const float *qnorm, float eps_rel, int k,
                         uint32_t *theta_glob, float *heap, int32_t *cand, uint32_t *cnt,
                         int64_t C, cudaStream_t s, const int32_t *perm = nullptr,
-                        const GtMember *member = nullptr);
+                        const GtMember *member = nullptr, const GtTiles *tiles = nullptr);
 
 }  // namespace nrlsh

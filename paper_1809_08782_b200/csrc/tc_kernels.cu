@@ -227,6 +227,8 @@ struct GtEpiRow {
         }
     }
     __device__ __forceinline__ void end() {
+        // publish the final bound (a later pass over the remaining tiles starts from it)
+        if (vq && hs == a->k && hp[0] > pub) atomicMax(&a->theta_glob[q], float_order(hp[0]));
         for (; sleft > 0; --sleft)
             if (sbase + (16 - sleft) < a->C) cl[sbase + (16 - sleft)] = -1;
     }
@@ -752,54 +754,106 @@ size_t gt_heap_bytes(int k) {
     return (size_t)sms * 2 * GT_M * k * 4;
 }
 
-// Tile lists of the member mode: for query pair g, the NT-row tiles (partition
-// order) overlapping a sub-dataset j with R[j][0] <= B_q for some query q of the
+// Tile lists (rows in partition order): for query pair g, the NT-row tiles that can
+// hold an answer of one of its queries.  A tile is skipped if its largest |x| is
+// below tau_g = min_q theta_q / (|q| (1 + eps2)) (every row then has
+// s~ + eps|q||x| <= |q||x|(1 + 2 eps) < theta_q <= the in-kernel bound, so the
+// filter's screen drops it anyway; tau = 0 while some theta_q is unset), and in
+// member mode if it overlaps no sub-dataset j with R[j][0] <= B_q for some q of the
 // pair (j holds candidates of q only then: R[j][h] grows with h).
+// (grid: x = chunks of 1024 tiles, y = query pairs; list order is arbitrary — the
+// filter's splits interleave the list anyway; count[] must be zeroed beforehand)
 __global__ void __launch_bounds__(256) gt_tile_lists(const uint16_t *__restrict__ R, int L, int m,
                                                      const uint8_t *__restrict__ part, int64_t n,
                                                      const uint32_t *__restrict__ sel_B, int Qb, int nt,
+                                                     const float *__restrict__ xmax128,
+                                                     const uint32_t *__restrict__ theta_glob,
+                                                     const float *__restrict__ qnorm, double eps2,
+                                                     float xsplit, int phase,
                                                      int32_t *__restrict__ list, int64_t stride,
                                                      int32_t *__restrict__ count,
                                                      unsigned long long *__restrict__ pairs) {
     __shared__ uint32_t act[257];
-    __shared__ uint32_t ws[32];
-    __shared__ uint32_t s_base;
-    const int g = blockIdx.x;
+    __shared__ uint32_t sB[2 * GT_M];
+    __shared__ float s_tau;
+    __shared__ uint32_t s_found;
+    const int g = blockIdx.y;
     const int q0 = g * 2 * GT_M, q1 = min(Qb, q0 + 2 * GT_M);
-    for (int j = threadIdx.x; j < m; j += blockDim.x) {
-        const uint32_t r0 = R[j * (L + 1)];
-        uint32_t on = 0;
-        for (int q = q0; q < q1 && !on; ++q) on = r0 <= sel_B[q];
-        act[j] = on;
+    // tau_g: min over the pair's queries (a thread per query; warp + smem min)
+    float tq = INFINITY;
+    for (int q = q0 + threadIdx.x; q < q1; q += blockDim.x) {
+        const uint32_t o = theta_glob[q];
+        const float th = o ? float_unorder(o) : -INFINITY;
+        // rounded down in double: tau never exceeds the exact threshold
+        const double t = th > 0.f ? (double)th / ((double)qnorm[q] * (1.0 + eps2) * (1.0 + 0x1p-20)) : 0.0;
+        tq = fminf(tq, __double2float_rd(t));
+        if (R) sB[q - q0] = sel_B[q];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tq = fminf(tq, __shfl_xor_sync(NR_FULL, tq, o));
+    if (threadIdx.x == 0) { s_tau = INFINITY; s_found = 0; }
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) atomicMin((int *)&s_tau, __float_as_int(fmaxf(tq, 0.f)));   // (>= 0: int order)
+    if (R) {
+        for (int j = threadIdx.x; j < m; j += blockDim.x) {
+            const uint32_t r0 = R[j * (L + 1)];
+            uint32_t on = 0;
+            for (int i = 0; i < q1 - q0 && !on; ++i) on = r0 <= sB[i];
+            act[j] = on;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {   // exclusive prefix count, act[j+1] - act[j0] = #active in [j0, j]
+            uint32_t c = 0;
+            for (int j = 0; j < m; ++j) { const uint32_t v = act[j]; act[j] = c; c += v; }
+            act[m] = c;
+        }
     }
     __syncthreads();
-    if (threadIdx.x == 0) {   // inclusive prefix count, act[j+1] = #active in [0, j]
-        uint32_t c = 0;
-        for (int j = 0; j < m; ++j) { const uint32_t v = act[j]; act[j] = c; c += v; }
-        act[m] = c;
-        s_base = 0;
-    }
-    __syncthreads();
+    const float tau = s_tau;
     const int64_t ntiles = (n + nt - 1) / nt;
-    for (int64_t t0 = 0; t0 < ntiles; t0 += blockDim.x) {
-        const int64_t t = t0 + threadIdx.x;
-        uint32_t on = 0;
-        if (t < ntiles) {
+    const int64_t n128 = (n + 127) / 128;
+    const int lane = threadIdx.x & 31;
+    for (int64_t t = (int64_t)blockIdx.x * 1024 + threadIdx.x; t < min(ntiles, (int64_t)(blockIdx.x + 1) * 1024);
+         t += blockDim.x) {
+        const int64_t a0 = t * (nt / 128);
+        float xm = xmax128[a0];
+        if (nt == 256 && a0 + 1 < n128) xm = fmaxf(xm, xmax128[a0 + 1]);
+        bool on = xm >= tau && (phase == 0 || (phase == 1) == (xm >= xsplit));
+        if (R && on) {
             const int j0 = part[t * nt], j1 = part[min(n - 1, t * nt + nt - 1)];
             on = act[j1 + 1] - act[j0] > 0;
         }
-        uint32_t tot;
-        const uint32_t ex = block_excl_scan(on, ws, &tot);
-        if (on) list[g * stride + s_base + ex] = (int32_t)t;
-        __syncthreads();
-        if (threadIdx.x == 0) s_base += tot;
-        __syncthreads();
+        const unsigned bal = __ballot_sync(__activemask(), on);
+        int base = 0;
+        if (lane == __ffs(__activemask()) - 1 && bal) base = atomicAdd(&count[g], __popc(bal));
+        base = __shfl_sync(__activemask(), base, __ffs(__activemask()) - 1);
+        if (on) list[g * stride + base + __popc(bal & lanemask_lt())] = (int32_t)t;
+        if (lane == 0) atomicAdd(&s_found, (uint32_t)__popc(bal));
     }
-    if (threadIdx.x == 0) {
-        count[g] = (int32_t)s_base;
-        // (query, item) pairs the filter multiplies for this pair's real queries
-        if (pairs) atomicAdd(pairs, (unsigned long long)s_base * nt * (unsigned long long)(q1 - q0));
+    __syncthreads();
+    // (query, item) pairs the filter multiplies for this pair's real queries
+    if (threadIdx.x == 0 && pairs && s_found)
+        atomicAdd(pairs, (unsigned long long)s_found * nt * (unsigned long long)(q1 - q0));
+}
+
+__global__ void tile_xmax128(const float *__restrict__ xn, int64_t n, float *__restrict__ out) {
+    const int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (t * 128 >= n) return;
+    float m = 0.f;
+    for (int e = lane; e < 128; e += 32) {
+        const int64_t i = t * 128 + e;
+        if (i < n) m = fmaxf(m, xn[i]);
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(NR_FULL, m, o));
+    if (lane == 0) out[t] = m;
+}
+
+void launch_tile_xmax128(const float *xnorm_pos, int64_t n, float *out, cudaStream_t s) {
+    const int64_t nt = (n + 127) / 128;
+    tile_xmax128<<<(unsigned)((nt * 32 + 255) / 256), 256, 0, s>>>(xnorm_pos, n, out);
+    note_launch();
 }
 
 size_t gt_tile_ws_bytes(int64_t n, int Qb) {
@@ -822,7 +876,8 @@ bool gt_tc_supported(int d, int k) {
 int launch_gt_filter_tc(const void *Xb, int64_t n, int d, int dp, const void *Qb16, int Qb,
                         const float *xnorm, const float *qnorm, float eps_rel, int k,
                         uint32_t *theta_glob, float *heap, int32_t *cand, uint32_t *cnt, int64_t C,
-                        cudaStream_t s, const int32_t *perm, const GtMember *mb) {
+                        cudaStream_t s, const int32_t *perm, const GtMember *mb,
+                        const GtTiles *tl) {
     const int kblocks = (dp + GT_KB - 1) / GT_KB;
     const int NT = gt_pick_nt(kblocks);
     CUtensorMap tq, tx;
@@ -865,7 +920,7 @@ int launch_gt_filter_tc(const void *Xb, int64_t n, int d, int dp, const void *Qb
     // CTA-pair kernel: opt-in (NRLSH_GT_PAIR=1) — correct, but measured slower than
     // the single-CTA N=256 kernel on c4 (0.84 vs 0.72 ms per 1024 queries: ~6.7K
     // cycles per pair tile against 1.3K of MMA work)
-    const bool use_pair = Qb > GT_M && !mb && getenv("NRLSH_GT_PAIR") && atoi(getenv("NRLSH_GT_PAIR")) == 1 &&
+    const bool use_pair = Qb > GT_M && !mb && !tl && getenv("NRLSH_GT_PAIR") && atoi(getenv("NRLSH_GT_PAIR")) == 1 &&
                           gp_smem_bytes(kblocks, 4, 0) <= 227 * 1024;
     if (use_pair) {
         CUtensorMap tq2, tx2;
@@ -924,16 +979,16 @@ int launch_gt_filter_tc(const void *Xb, int64_t n, int d, int dp, const void *Qb
     a.split_items = a.split_tiles * NT;
     a.nsplit = (int)((n + a.split_items - 1) / a.split_items);
     a.ntiles = ntiles;
-    if (mb && mb->tile_ws && !getenv("NRLSH_RERANK_TC_ALLTILES")) {
-        // member mode: per query pair, only the tiles of sub-datasets with candidates
-        a.tcount = mb->tile_ws;
+    const bool lists = tl && tl->ws && !getenv("NRLSH_GT_ALLTILES");
+    // two passes when the rows are norm-sorted tiles: the tiles of largest |x| first
+    // (their scores lift theta close to its final value), then the rest, pruned
+    // against the lifted theta
+    const int npass = lists && tl->xsplit > 0.f && !getenv("NRLSH_GT_ONEPASS") ? 2 : 1;
+    if (lists) {
+        a.tcount = tl->ws;
         a.tstride = ntiles;
-        a.tlist = mb->tile_ws + a.nqp + 4;
+        a.tlist = tl->ws + a.nqp + 4;
         a.nsplit = nsplit;
-        gt_tile_lists<<<a.nqp, 256, 0, s>>>(mb->R, mb->L, mb->m, mb->part, n, mb->sel_B, Qb, NT,
-                                            const_cast<int32_t *>(a.tlist), a.tstride,
-                                            const_cast<int32_t *>(a.tcount), mb->pairs);
-        note_launch();
     }
     // deepest ring that fits, with the heaps in smem if they fit too
     const int smax = NT == 256 ? 6 : GT_MAX_STAGES;
@@ -951,14 +1006,26 @@ int launch_gt_filter_tc(const void *Xb, int64_t n, int d, int dp, const void *Qb
     }
     const size_t sm = gt_tc_smem_bytes(NT, kblocks, a.stages, a.heap_smem ? k : 0);
     const int grid = std::min(sms, a.nqp * a.nsplit);
-    if (NT == 256) {
-        cudaFuncSetAttribute(gt_filter_tc<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        gt_filter_tc<256><<<grid, GT_THREADS, sm, s>>>(tq, tx, a);
-    } else {
-        cudaFuncSetAttribute(gt_filter_tc<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        gt_filter_tc<128><<<grid, GT_THREADS, sm, s>>>(tq, tx, a);
+    for (int pass = 0; pass < npass; ++pass) {
+        if (lists) {   // per query pair, only the tiles that can hold an answer (GtTiles)
+            cudaMemsetAsync(const_cast<int32_t *>(a.tcount), 0, (size_t)a.nqp * 4, s);
+            gt_tile_lists<<<dim3((unsigned)((ntiles + 1023) / 1024), a.nqp), 256, 0, s>>>(mb ? mb->R : nullptr, mb ? mb->L : 0, mb ? mb->m : 0,
+                                                mb ? mb->part : nullptr, n, mb ? mb->sel_B : nullptr,
+                                                Qb, NT, tl->xmax128, theta_glob, qnorm, 2.0 * eps_rel,
+                                                tl->xsplit, npass == 1 ? 0 : pass + 1,
+                                                const_cast<int32_t *>(a.tlist), a.tstride,
+                                                const_cast<int32_t *>(a.tcount), tl->pairs);
+            note_launch();
+        }
+        if (NT == 256) {
+            cudaFuncSetAttribute(gt_filter_tc<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            gt_filter_tc<256><<<grid, GT_THREADS, sm, s>>>(tq, tx, a);
+        } else {
+            cudaFuncSetAttribute(gt_filter_tc<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            gt_filter_tc<128><<<grid, GT_THREADS, sm, s>>>(tq, tx, a);
+        }
+        note_launch();
     }
-    note_launch();
     return 0;
 }
 

@@ -608,3 +608,30 @@ def test_exact_topk_cta_pair_kernel(name, n, nq, k, monkeypatch):
     for qi in (0, nq - 1):
         ids, s = oracle.exact_topk(X, Q[qi], k)
         assert_topk_match(b[qi].cpu().numpy(), sb[qi].cpu().numpy(), ids, s, X, Q[qi])
+
+
+@pytest.mark.parametrize("case", [("c4", 300_000, 32, 64, 128), ("scale", 70_000, 16, 128, 256),
+                                  ("c3", 40_000, 64, 64, 64)], ids=_ids)
+def test_tile_pruning_is_exact(built, case, monkeypatch):
+    """Tile pruning of the tensor-core filter (tiles whose largest |x| cannot reach a
+    query pair's seeded bound are not streamed; Cauchy-Schwarz) changes nothing: the
+    index's seeded ground truth and the tensor-core re-rank equal their unpruned runs
+    bit for bit (ids and fp32 scores), at budgets from tiny to all of n."""
+    cfg, X, Q, Xd, idx, orc = built(*case)
+    P = _P()
+    n = X.shape[0]
+    Qd = torch.from_numpy(np.concatenate([Q] * (300 // len(Q) + 1))[:300]).cuda()   # > 1 pair
+    seeds, _ = idx.query(Qd, cfg.k, max(cfg.k, n // 100))
+    for k in (1, cfg.k, 50):
+        monkeypatch.delenv("NRLSH_GT_ALLTILES", raising=False)
+        a, sa = idx.exact_topk(Qd, k, seed_ids=seeds)
+        monkeypatch.setenv("NRLSH_GT_ALLTILES", "1")
+        b, sb = idx.exact_topk(Qd, k, seed_ids=seeds)
+        assert torch.equal(a, b) and torch.equal(sa.view(torch.int32), sb.view(torch.int32)), k
+    monkeypatch.setenv("NRLSH_RERANK_TC", "1")
+    for T in (max(1, n // 100), n // 3):
+        monkeypatch.delenv("NRLSH_GT_ALLTILES", raising=False)
+        a, sa = idx.query(Qd, cfg.k, T)
+        monkeypatch.setenv("NRLSH_GT_ALLTILES", "1")
+        b, sb = idx.query(Qd, cfg.k, T)
+        assert torch.equal(a, b) and torch.equal(sa.view(torch.int32), sb.view(torch.int32)), T
