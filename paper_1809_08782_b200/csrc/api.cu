@@ -142,7 +142,7 @@ void free_index(nrlsh_index *ix) {
     void *ps[] = {ix->X_owned, ix->Xpad, ix->Xb, ix->xnorm, ix->norm2, ix->perm, ix->pos_of_id, ix->part_of_id,
                   ix->part_of_pos, ix->offsets_d, ix->V_d, ix->codes, ix->A, ix->Apad,
                   ix->R_d, ix->chunks_d, ix->order_d, ix->samp_codes, ix->samp_part,
-                  ix->tiles_d, ix->xnorm_pos, ix->tile_xmax};
+                  ix->tiles_d, ix->xnorm_pos, ix->tile_xmax, ix->codes_pm};
     // pool-backed (cudaMallocAsync at build); the index may have been used on any stream
     cudaDeviceSynchronize();
     for (void *p : ps)
@@ -301,6 +301,9 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
     NR_ALLOC(ix->xnorm_pos, (size_t)npad * 4);
     cudaMemsetAsync(ix->xnorm_pos + n, 0, (size_t)(npad - n) * 4, s);
     NR_ALLOC(ix->tile_xmax, (size_t)((n + 127) / 128) * 4);
+    // +-1 rows for the opt-in tensor-core scan (NRLSH_SCAN_TC=1 at build and query)
+    if (L <= 128 && getenv("NRLSH_SCAN_TC") && atoi(getenv("NRLSH_SCAN_TC")) != 0)
+        NR_ALLOC(ix->codes_pm, (size_t)n * scan_kp(L));
     NR_ALLOC(ix->offsets_d, (size_t)(m + 1) * 8);
     NR_ALLOC(ix->V_d, (size_t)m * 8);
     NR_ALLOC(ix->codes, (size_t)n * W * 4);
@@ -391,6 +394,7 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
         ProfScope p(SLOT_CODES, s);
         launch_gather_f32(ix->xnorm, ix->perm, n, ix->xnorm_pos, s);
         launch_tile_xmax128(ix->xnorm_pos, n, ix->tile_xmax, s);
+        if (ix->codes_pm) launch_expand_pm(ix->codes, n, W, L, ix->codes_pm, s);
     }
     // compacted pilot sample (query-time pilots read it contiguously)
     {
@@ -476,7 +480,10 @@ void run_candidates(const nrlsh_index *ix, const float *Qd, const uint32_t *qcod
         ProfScope p(SLOT_SCAN, s);
         if (tc) {
             cudaMemsetAsync(cntv, 0, (size_t)Qb * 4, s);
-            launch_scan_tc(ix, qcodes, delta, Qb, blk_act, buf, cnt, cntv, C, pairs, s);
+            if (launch_scan_tc(ix, qcodes, delta, Qb, blk_act, buf, cnt, cntv, C, pairs, s)) {
+                launch_scan(ix, qcodes, delta, Qb, buf, cnt, C, pairs, s);   // (tensor map failure)
+                cudaMemcpyAsync(cntv, cnt, (size_t)Qb * 4, cudaMemcpyDeviceToDevice, s);
+            }
         } else {
             launch_scan(ix, qcodes, delta, Qb, buf, cnt, C, pairs, s);
         }
@@ -567,7 +574,8 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
     DBuf qc, dl, cn, cv, ba, bf, cd, pt, fl;
     if (qc.alloc((size_t)Qmax * ix->W * 4, s) || dl.alloc((size_t)Qmax * ix->m, s) ||
         cn.alloc((size_t)Qmax * 4, s) || cv.alloc((size_t)Qmax * 4, s) ||
-        ba.alloc((size_t)((Qmax + 127) / 128) * ix->m, s) || bf.alloc((size_t)Qmax * C * 8, s) ||
+        ba.alloc(scan_tc_supported(ix) ? scan_tc_ws_bytes(ix, Qmax) : 16, s) ||
+        bf.alloc((size_t)Qmax * C * 8, s) ||
         cd.alloc((size_t)Qmax * Tq * 4, s) ||
         pt.alloc(want_topk ? rerank_partial_bytes(Qmax, Tq, k) : 0, s) || fl.alloc(40, s))
         return fail(NRLSH_ENOMEM, "query workspace");
@@ -624,7 +632,8 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
     tls.xmax128 = ix->tile_xmax;
     tls.ws = use_rtc ? rtl.get<int32_t>() : nullptr;
     tls.pairs = (unsigned long long *)(fl.get<int>() + 8);
-    tls.xsplit = ix->tile_xsplit;
+    tls.xsplit = getenv("NRLSH_GT_ONEPASS") ? 0.f : ix->tile_xsplit;
+    tls.pass = 0;
     const int init_flags[10] = {INT_MAX, INT_MAX, 0, 0, 0, 0, 0, 0, 0, 0};
     cudaMemcpyAsync(fl.p, init_flags, 40, cudaMemcpyHostToDevice, s);
     unsigned long long *pairs = (unsigned long long *)(fl.get<int>() + 4);
@@ -647,6 +656,7 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
                 ProfScope p(SLOT_SCORE, s);
                 // certified warm start: the k-th best fp32 score (the final re-rank's own
                 // arithmetic) over KS best-ranked candidates bounds the answer's k-th score
+                cudaMemsetAsync(rth.p, 0, (size_t)Qb * 4, s);
                 launch_rerank(Xr, ix->d, ldr, Qd, Qb, rseed.get<int32_t>(), KS, KS, nullptr, 1, k,
                               rpt.get<unsigned long long>(), rtid.get<int64_t>(), rtsc.get<float>(), s);
                 launch_theta_from_topk(rtid.get<int64_t>(), rtsc.get<float>(), Qb, k,
@@ -658,11 +668,23 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
             mb.qcodes = qc.get<uint32_t>();
             mb.sel_B = rsb.get<uint32_t>();
             mb.sel_pk = rspk.get<uint32_t>();
-            if (launch_gt_filter_tc(ix->Xb, n, ix->d, ix->dpb, rqb.p, Qb, ix->xnorm_pos,
-                                    rqn.get<float>(), gt_eps_rel(ix->dpb), k, rth.get<uint32_t>(),
-                                    rhp.get<float>(), rcd.get<int32_t>(), rcc.get<uint32_t>(), Cg,
-                                    s, ix->perm, &mb, &tls))
-                return fail(NRLSH_ECUDA, "tensor map encoding failed");
+            // two passes: the top-|x| tiles, then — after an exact re-rank of their
+            // survivors has lifted theta to a real k-th best — the rest, pruned by it
+            for (int pass = 1; pass <= 2; ++pass) {
+                tls.pass = pass;
+                if (launch_gt_filter_tc(ix->Xb, n, ix->d, ix->dpb, rqb.p, Qb, ix->xnorm_pos,
+                                        rqn.get<float>(), gt_eps_rel(ix->dpb), k, rth.get<uint32_t>(),
+                                        rhp.get<float>(), rcd.get<int32_t>(), rcc.get<uint32_t>(), Cg,
+                                        s, ix->perm, &mb, &tls))
+                    return fail(NRLSH_ECUDA, "tensor map encoding failed");
+                if (pass == 1 && tls.xsplit > 0.f) {
+                    launch_rerank(Xr, ix->d, ldr, Qd, Qb, rcd.get<int32_t>(), Cg, Cg, rcc.get<uint32_t>(),
+                                  1, k, rpt.get<unsigned long long>(), rtid.get<int64_t>(),
+                                  rtsc.get<float>(), s);
+                    launch_theta_from_topk(rtid.get<int64_t>(), rtsc.get<float>(), Qb, k,
+                                           rth.get<uint32_t>(), s);
+                }
+            }
             // exact fp32 re-rank of the surviving candidates (same arithmetic as the
             // gather path: identical scores and order)
             ProfScope p2(SLOT_RERANK_TOPK, s);
@@ -901,7 +923,8 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
     gtl.xmax128 = tile_xmax_ix;
     gtl.ws = tw.get<int32_t>();
     gtl.pairs = nullptr;
-    gtl.xsplit = xsplit_ix;
+    gtl.xsplit = getenv("NRLSH_GT_ONEPASS") ? 0.f : xsplit_ix;
+    gtl.pass = 0;
     std::vector<uint32_t> hcnt(Qmax);
     for (int64_t q0 = 0; q0 < nq; q0 += Qmax) {
         const int Qb = (int)std::min<int64_t>(Qmax, nq - q0);
@@ -919,12 +942,24 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
                                      th.get<uint32_t>(), s);
             }
             ProfScope p(SLOT_GT_FILTER, s);
-            if (launch_gt_filter_tc(Xbp, n, d, dp, (const uint16_t *)qb.p + q0 * dp, Qb,
-                                    xnp, qnb, eps_rel, k, th.get<uint32_t>(),
-                                    hp.get<float>(), cd.get<int32_t>(), cc.get<uint32_t>(), Cg, s,
-                                    Xb_ix ? perm_ix : nullptr, nullptr,
-                                    (Xb_ix && tile_xmax_ix) ? &gtl : nullptr))
-                return fail(NRLSH_ECUDA, "tensor map encoding failed");
+            const bool tiles = Xb_ix && tile_xmax_ix;
+            // with tile lists: the top-|x| tiles, an exact re-rank of their survivors
+            // (theta := a real k-th best, the final re-rank's arithmetic), the rest
+            const int npass = tiles && gtl.xsplit > 0.f ? 2 : 1;
+            for (int pass = 1; pass <= npass; ++pass) {
+                gtl.pass = npass == 1 ? 0 : pass;
+                if (launch_gt_filter_tc(Xbp, n, d, dp, (const uint16_t *)qb.p + q0 * dp, Qb,
+                                        xnp, qnb, eps_rel, k, th.get<uint32_t>(),
+                                        hp.get<float>(), cd.get<int32_t>(), cc.get<uint32_t>(), Cg, s,
+                                        Xb_ix ? perm_ix : nullptr, nullptr, tiles ? &gtl : nullptr))
+                    return fail(NRLSH_ECUDA, "tensor map encoding failed");
+                if (pass < npass) {
+                    launch_rerank(X, d, d, Qb_ptr, Qb, cd.get<int32_t>(), Cg, Cg, cc.get<uint32_t>(), 1, k,
+                                  pt.get<unsigned long long>(), tid.get<int64_t>(), tsc.get<float>(), s);
+                    launch_theta_from_topk(tid.get<int64_t>(), tsc.get<float>(), Qb, k,
+                                           th.get<uint32_t>(), s);
+                }
+            }
         } else {
             // pilot: certified lower bound of the k-th best score from a strided sample
             {
@@ -1047,6 +1082,10 @@ nrlsh_status nrlsh_set_codes(nrlsh_index *ix, const uint32_t *codes) {
     if (!ix || !codes) return fail(NRLSH_EINVAL, "bad argument");
     cudaError_t e = cudaMemcpy(ix->codes, codes, (size_t)ix->n * ix->W * 4, cudaMemcpyDefault);
     if (e) return cuda_fail(e, "set codes");
+    if (ix->codes_pm) {   // keep the tensor-core scan's +-1 rows in step
+        launch_expand_pm(ix->codes, ix->n, ix->W, ix->L, ix->codes_pm, nullptr);
+        if ((e = cudaDeviceSynchronize())) return cuda_fail(e, "set codes (+-1 rows)");
+    }
     if (ix->samp_codes) {   // keep the pilot sample in step with the codes
         launch_gather_sample(ix, pilot_stride(ix->n), ix->samp_codes, ix->samp_part, nullptr);
         if ((e = cudaDeviceSynchronize())) return cuda_fail(e, "set codes (sample)");

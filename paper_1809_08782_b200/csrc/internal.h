@@ -40,6 +40,8 @@ struct nrlsh_index {
     int64_t *offsets_d = nullptr;   // [m+1]
     double *V_d = nullptr;          // [m]
     uint32_t *codes = nullptr;      // [n x W], partition order
+    int8_t *codes_pm = nullptr;     // [n x scan_kp(L)] +-1 int8 code rows, partition order
+                                    //   (the tensor-core scan's B operand)
     float *A = nullptr;             // [(d+1) x L] row-major (as generated)
     float *Apad = nullptr;          // [(d+1) x 32W], zero columns >= L
     uint16_t *R_d = nullptr;        // [m x (L+1)]
@@ -134,10 +136,14 @@ void launch_scan(const nrlsh_index *ix, const uint32_t *qcodes, const int8_t *de
 void launch_fallback(const nrlsh_index *ix, const uint32_t *qcodes, int Qb, int64_t Tq,
                      unsigned long long *buf, uint32_t *cnt, const uint32_t *cntv, int64_t C,
                      int *flags, cudaStream_t s);
+// tensor-core Hamming scan (scan_tc.cu): +-1 int8 item codes expanded at build
+int scan_kp(int L);
+void launch_expand_pm(const uint32_t *codes, int64_t rows, int W, int L, int8_t *out, cudaStream_t s);
 bool scan_tc_supported(const nrlsh_index *ix);
-void launch_scan_tc(const nrlsh_index *ix, const uint32_t *qcodes, const int8_t *delta, int Qb,
-                    uint8_t *blk_act, unsigned long long *buf, uint32_t *cnt, uint32_t *cntv,
-                    int64_t C, unsigned long long *pairs, cudaStream_t s);
+size_t scan_tc_ws_bytes(const nrlsh_index *ix, int Qb);
+int launch_scan_tc(const nrlsh_index *ix, const uint32_t *qcodes, const int8_t *delta, int Qb,
+                   void *ws, unsigned long long *buf, uint32_t *cnt, uint32_t *cntv, int64_t C,
+                   unsigned long long *pairs, cudaStream_t s);
 void launch_select(const nrlsh_index *ix, int Qb, int64_t Tq, const unsigned long long *buf,
                    const uint32_t *cnt, int64_t C, int32_t *cand, uint16_t *cand_rank,
                    cudaStream_t s);
@@ -190,7 +196,8 @@ void launch_dense_merge(const unsigned long long *partial, int S, int k, const i
 
 // dst[p] = src[idx[p]] for p < n
 void launch_gather_f32(const float *src, const int32_t *idx, int64_t n, float *dst, cudaStream_t s);
-// theta_glob[q] = orderable image of out_scores[q][k-1] when that slot holds an item
+// theta_glob[q] = max(theta_glob[q], orderable image of out_scores[q][k-1]) when that
+// slot holds an item
 void launch_theta_from_topk(const int64_t *ids, const float *scores, int Qb, int k,
                             uint32_t *theta_glob, cudaStream_t s);
 // *out += sum_q min(cnt[q], C)
@@ -243,6 +250,7 @@ struct GtTiles {
     int32_t *ws;                // gt_tile_ws_bytes(n, Qb) of scratch for the lists
     unsigned long long *pairs;  // optional: += (query, row) pairs multiplied
     float xsplit;               // > 0: two passes, tiles with xmax >= xsplit first
+    int pass;                   // 0: both passes; 1 / 2: only that one
 };
 size_t gt_tile_ws_bytes(int64_t n, int Qb);
 void launch_tile_xmax128(const float *xnorm_pos, int64_t n, float *out, cudaStream_t s);

@@ -713,7 +713,7 @@ __global__ void theta_from_topk(const int64_t *__restrict__ ids, const float *__
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= Qb) return;
     const int64_t e = (int64_t)q * k + k - 1;
-    theta_glob[q] = ids[e] >= 0 ? float_order(sc[e]) : 0u;
+    if (ids[e] >= 0) theta_glob[q] = max(theta_glob[q], float_order(sc[e]));
 }
 
 void launch_theta_from_topk(const int64_t *ids, const float *scores, int Qb, int k,

@@ -9,19 +9,23 @@
 // (the pilot's per-(query, sub-dataset) radius) — becomes  dot >= L - 2 delta_j(q).
 // Passing pairs are appended to the query's candidate buffer as ((j,h) << 32 | pos),
 // exactly as the popcount scan (query_kernels.cu) appends them, so the fallback and
-// select stages are shared (see the epilogue for how appends are reserved).
+// select stages are shared.
 //
-// CTA unit = (block of 128 queries, range of item tiles).  An item tile holds <= 256
-// consecutive positions of ONE sub-dataset (tile list built at index build), so a
-// query has one threshold per tile.
-//   warps 0-3  expand packed codes into +-1 int8, K-major, 128B-swizzled smem tiles
-//              (the block's 128 queries once per unit; 256 items per ring stage)
-//   warp  4    TMEM allocator + warp-uniform tcgen05.mma kind::i8 issue (M = 128
-//              queries, N = 256 items, K = 32 per instruction, ceil(L/32) per tile)
-//   warps 8-23 epilogue: thread = query row, 64 columns each; tcgen05.ld, a max
-//              screen per 32 columns, the exact test, the append
-// Tiles of sub-datasets in which no query of the block has delta_j(q) >= 0 are
-// skipped by every role (exact: no pair there can pass).
+// The +-1 item codes are expanded once, at index build, into an int8 matrix in
+// partition order ([n x Kp], Kp = 64 or 128 bytes, 64/128-byte swizzled rows), so the
+// kernel is a plain TMA -> tcgen05 kind::i8 -> TMEM pipeline (no converter warps):
+//   warp 0     TMA producer: the block's 128 queries once per unit, then one
+//              256-row tile per ring stage
+//   warp 1     MMA issuer (warp-uniform, elected lane): M = 128 queries, N = 256
+//              items, K = 32 per instruction, ceil(L/32) per tile, TMEM double-buffered
+//   warp 2     TMEM allocator
+//   warps 4-11 epilogue: thread = (query row, 128-column half); tcgen05.ld 32
+//              columns, pass mask, the dots of a passing group staged in shared
+//              memory, one append per passing pair into 64-slot chunks reserved per
+//              thread
+// Tiles are the index's sub-dataset-aligned runs of <= 256 positions, so a query has
+// one threshold per tile; per query block only the tiles of sub-datasets with some
+// delta_j(q) >= 0 are listed (exact: no pair elsewhere can pass).
 #include <cuda.h>
 
 #include <algorithm>
@@ -36,38 +40,29 @@
 
 namespace nrlsh {
 
-constexpr int ST_M = 128;                 // queries per block (TMEM lanes)
-constexpr int ST_N = 256;                 // items per tile (TMEM columns)
-constexpr int ST_ROWB = 128;              // bytes per swizzled K-major row (K <= 128 int8)
-constexpr int ST_A = ST_M * ST_ROWB;      // 16 KB
-constexpr int ST_B = ST_N * ST_ROWB;      // 32 KB per stage
-constexpr int ST_STAGES = 4;             // max ring depth (runtime: a.stages)
-constexpr int ST_THREADS = 24 * 32;        // 0-3 convert, 4 MMA, 8-23 epilogue
-constexpr int ST_CONV = 128;              // converter threads (warps 0-3)
-constexpr int ST_CH = 64;                 // append chunk (slots reserved per atomic)
+bool make_tmap_2d(CUtensorMap *m, const void *base, CUtensorMapDataType dt, int esize,
+                  uint64_t cols, uint64_t rows, uint32_t box_cols, uint32_t box_rows, int swizzle);
 
-struct ScanTcArgs {
-    const uint32_t *codes;    // [n x W] partition order
-    const uint32_t *qcodes;   // [Qb x W]
+constexpr int SM_M = 128;                 // queries per block (TMEM lanes)
+constexpr int SM_N = 256;                 // items per tile (TMEM columns per buffer)
+constexpr int SM_MAX_STAGES = 8;
+constexpr int SM_THREADS = 384;           // warps 0-3 control, 4-11 epilogue
+constexpr int SM_CH = 64;                 // append chunk (slots reserved per atomic)
+constexpr int SM_DOT_LD = 36;             // staged dots per thread (16-byte aligned rows)
+
+struct ScanMmaArgs {
+    const int4 *tiles;        // (j, p0, p1, 0), sub-dataset aligned
+    const int32_t *tlist;     // [nqb x tstride] tile indices per query block
+    const int32_t *tcount;    // [nqb]
+    int64_t tstride;
     const int8_t *delta;      // [Qb x m]
-    const uint8_t *blk_act;   // [nqb x m]: any query of the block has delta_j >= 0
-    const int4 *tiles;        // (j, p0, p1, 0)
-    int ntiles;
-    int Qb, m, L, W;
-    int nqb, nsplit, tiles_per_split, stages;
-    unsigned long long *clk;   // profiling experiments only (NRLSH_SCAN_CLK): per-CTA phase cycles
-    int dbg;   // profiling experiments only (NRLSH_SCAN_DBG): 1 = epilogue reads TMEM only,
-               // 2 = epilogue idle, 3 = converters store nothing
+    int Qb, m, L, Kp, nqb, nsplit, stages;
     unsigned long long *buf;  // [Qb x C]
     uint32_t *cnt;            // slots used per query (entries incl. sentinels)
     uint32_t *cntv;           // valid entries per query
     int64_t C;
     unsigned long long *pairs;
 };
-
-__device__ __forceinline__ uint32_t st_swz(int row, int kbyte) {
-    return (uint32_t)(row * ST_ROWB + ((((kbyte >> 4) ^ (row & 7))) << 4) + (kbyte & 15));
-}
 
 // 4 code bits -> 4 int8 (+1 for a 1 bit, -1 for a 0 bit): spread bit i to byte i
 // (nibble * 0x204081 puts bit i at bit 8i), then 0xFF ^ (byte * 0xFE).
@@ -76,380 +71,300 @@ __device__ __forceinline__ uint32_t expand4(uint32_t nib) {
     return 0xFFFFFFFFu ^ (y * 0xFEu);
 }
 
-// one 32-bit code word (bits 32w .. 32w+31) -> two 16-byte chunks of the swizzled row
-// (bytes for bits >= L are 0)
-__device__ __forceinline__ void expand_word(uint32_t word, int w, int L, int row, uint8_t *tile) {
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        uint32_t v[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int b0 = 32 * w + 16 * h + 4 * i;
-            uint32_t x = expand4((word >> (16 * h + 4 * i)) & 0xFu);
-            if (b0 + 4 > L) {   // partial nibble / past L: zero the bytes of bits >= L
-                const int keep = max(0, min(4, L - b0));
-                x &= keep >= 4 ? 0xFFFFFFFFu : ((1u << (8 * keep)) - 1u);
+// codes [rows x W] -> +-1 int8 rows [rows x Kp] (bytes of bits >= L are 0)
+__global__ void expand_pm(const uint32_t *__restrict__ codes, int64_t rows, int W, int L, int Kp,
+                          int8_t *__restrict__ out) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t *dst = reinterpret_cast<uint32_t *>(out + r * Kp);
+        for (int b0 = 0; b0 < Kp; b0 += 4) {
+            uint32_t v = 0u;
+            if (b0 < L) {
+                v = expand4((codes[r * W + (b0 >> 5)] >> (b0 & 31)) & 0xFu);
+                if (b0 + 4 > L) v &= (1u << (8 * (L - b0))) - 1u;
             }
-            v[i] = x;
-        }
-        *reinterpret_cast<uint4 *>(tile + st_swz(row, 32 * w + 16 * h)) = make_uint4(v[0], v[1], v[2], v[3]);
-    }
-}
-
-// Codes of rows [first, first + rows) -> registers (the loads of a whole tile are
-// issued before any use); thread `tid` of `nthreads` owns rows tid, tid + nthreads, ...
-template <int W, int RPT>
-__device__ __forceinline__ void tile_load(const uint32_t *__restrict__ src, int64_t first, int rows,
-                                          int tid, uint32_t (&c)[RPT][W]) {
-#pragma unroll
-    for (int k = 0; k < RPT; ++k) {
-        const int r = tid + k * ST_CONV;
-        const int64_t p = first + min(r, max(rows - 1, 0));
-        if (W == 4) {
-            const uint4 v = __ldg(reinterpret_cast<const uint4 *>(src) + p);
-            c[k][0] = v.x; c[k][1] = v.y; c[k][2] = v.z; c[k][3] = v.w;
-        } else if (W == 2) {
-            const uint2 v = __ldg(reinterpret_cast<const uint2 *>(src) + p);
-            c[k][0] = v.x; c[k][1] = v.y;
-        } else {
-            c[k][0] = __ldg(src + p);
+            dst[b0 >> 2] = v;
         }
     }
 }
 
-template <int W, int RPT>
-__device__ __forceinline__ void tile_store(const uint32_t (&c)[RPT][W], int rows, int L, int tid,
-                                           uint8_t *tile) {
-#pragma unroll
-    for (int k = 0; k < RPT; ++k) {
-        const int r = tid + k * ST_CONV;
-#pragma unroll
-        for (int w = 0; w < W; ++w) expand_word(r < rows ? c[k][w] : 0u, w, r < rows ? L : 0, r, tile);
+int scan_kp(int L) { return L <= 64 ? 64 : 128; }
+
+void launch_expand_pm(const uint32_t *codes, int64_t rows, int W, int L, int8_t *out, cudaStream_t s) {
+    expand_pm<<<grid_for(rows, 256, 4096), 256, 0, s>>>(codes, rows, W, L, scan_kp(L), out);
+    note_launch();
+}
+
+// per query block: the sub-dataset tiles in which some query of the block has
+// delta_j(q) >= 0 (grid: x = chunks of 1024 tiles, y = blocks; count zeroed before)
+__global__ void __launch_bounds__(256) scan_tile_lists(const int8_t *__restrict__ delta, int Qb, int m,
+                                                       const int4 *__restrict__ tiles, int ntiles,
+                                                       int32_t *__restrict__ list, int64_t stride,
+                                                       int32_t *__restrict__ count) {
+    __shared__ uint8_t act[256];
+    const int qb = blockIdx.y;
+    const int q0 = qb * SM_M, q1 = min(Qb, q0 + SM_M);
+    for (int j = threadIdx.x; j < m; j += blockDim.x) {
+        uint8_t on = 0;
+        for (int q = q0; q < q1 && !on; ++q) on = delta[(int64_t)q * m + j] >= 0;
+        act[j] = on;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    for (int t = blockIdx.x * 1024 + threadIdx.x; t < min(ntiles, (int)(blockIdx.x + 1) * 1024);
+         t += blockDim.x) {
+        const bool on = act[tiles[t].x] != 0;
+        const unsigned am = __activemask();
+        const unsigned bal = __ballot_sync(am, on);
+        const int leader = __ffs(am) - 1;
+        int base = 0;
+        if (lane == leader && bal) base = atomicAdd(&count[qb], __popc(bal));
+        base = __shfl_sync(am, base, leader);
+        if (on) list[qb * stride + base + __popc(bal & lanemask_lt())] = t;
     }
 }
 
-template <int W>
-__global__ void __launch_bounds__(ST_THREADS, 1) k6_scan_tc(ScanTcArgs a) {
+template <int KP>
+__global__ void __launch_bounds__(SM_THREADS, 1)
+    k6_scan_mma(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmX,
+                ScanMmaArgs a) {
+    constexpr int A_BYTES = SM_M * KP;
+    constexpr int B_BYTES = SM_N * KP;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
-    uint8_t *sA = smem;                                   // 16 KB
-    uint8_t *ring = sA + ST_A;                            // ST_STAGES x 32 KB
-    int8_t *sdelta = reinterpret_cast<int8_t *>(ring + a.stages * ST_B);     // [128 x m]
-    int4 *stile = reinterpret_cast<int4 *>(sdelta + ((ST_M * a.m + 15) & ~15)); // [tiles_per_split]
-    uint64_t *bars = reinterpret_cast<uint64_t *>(stile + a.tiles_per_split);
-    uint64_t *full = bars, *empty = bars + ST_STAGES;
-    uint64_t *a_full = bars + 2 * ST_STAGES;
-    uint64_t *tfull = a_full + 1, *tempty = tfull + 2;
+    uint8_t *sA = smem;
+    uint8_t *ring = sA + A_BYTES;
+    int *sdot = reinterpret_cast<int *>(ring + a.stages * B_BYTES);          // [256][SM_DOT_LD]
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sdot + 256 * SM_DOT_LD);
+    uint64_t *full = bars, *empty = bars + SM_MAX_STAGES;
+    uint64_t *a_full = bars + 2 * SM_MAX_STAGES, *a_empty = a_full + 1;
+    uint64_t *tfull = a_empty + 1, *tempty = tfull + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
-    __shared__ int s_ntl;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // one unit per CTA: (query block, item split)
-    const int qb = blockIdx.x % a.nqb, sp = blockIdx.x / a.nqb;
-    const int t0 = sp * a.tiles_per_split, t1 = min(a.ntiles, t0 + a.tiles_per_split);
-    const int q0 = qb * ST_M;
-    const int nq = min(ST_M, a.Qb - q0);
-    for (int e = threadIdx.x; e < ST_M * a.m; e += blockDim.x) {
-        const int r = e / a.m;
-        sdelta[e] = r < nq ? a.delta[(int64_t)(q0 + r) * a.m + (e % a.m)] : (int8_t)-1;
-    }
-    if (warp == 5) {   // compacted list of this unit's tiles in sub-datasets the block probes
-        const uint8_t *act = a.blk_act + (int64_t)qb * a.m;
-        int n = 0;
-        for (int t = t0 + lane; t - lane < t1; t += 32) {
-            int4 tl = make_int4(0, 0, 0, 0);
-            const bool ok = t < t1 && act[(tl = a.tiles[t]).x];
-            const unsigned bal = __ballot_sync(NR_FULL, ok);
-            if (ok) stile[n + __popc(bal & lanemask_lt())] = tl;
-            n += __popc(bal);
-        }
-        if (lane == 0) s_ntl = n;
-    }
     if (threadIdx.x == 0) {
-        for (int s = 0; s < a.stages; ++s) {
-            tc::mbar_init(&full[s], ST_CONV / 32);
-            tc::mbar_init(&empty[s], 1);
-        }
-        tc::mbar_init(a_full, ST_CONV / 32);
-        for (int s = 0; s < 2; ++s) {
-            tc::mbar_init(&tfull[s], 1);
-            tc::mbar_init(&tempty[s], 16);
+        for (int s = 0; s < a.stages; ++s) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
+        tc::mbar_init(a_full, 1);
+        tc::mbar_init(a_empty, 1);
+        for (int b = 0; b < 2; ++b) {
+            tc::mbar_init(&tfull[b], 1);
+            tc::mbar_init(&tempty[b], 8);
         }
         tc::fence_mbar_init();
     }
-    if (warp == 4) tc::tmem_alloc(tmem_slot, 512);
+    if (warp == 2) tc::tmem_alloc(tmem_slot, 512);
+    if (warp == 0 && lane == 0) { tc::tma_prefetch(&tmQ); tc::tma_prefetch(&tmX); }
     tc::tc_fence_before();
     __syncthreads();
     tc::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    const int ntl = s_ntl;
-    const int ksteps = (a.L + 31) / 32;   // K = 32 int8 per MMA
-    constexpr int RPT = ST_N / ST_CONV;   // item rows per converter thread
+    // unit = (query block qb, split sp): every nsplit-th listed tile of qb from sp on;
+    // the units of one split run concurrently and share each tile's L2 fetch
+    const int nunits = a.nqb * a.nsplit;
+    auto unit_count = [&](int qb, int sp) -> int {
+        const int c = a.tcount[qb];
+        return c > sp ? (c - sp + a.nsplit - 1) / a.nsplit : 0;
+    };
+    auto unit_tile = [&](int qb, int sp, int v) -> int4 {
+        return a.tiles[__ldg(a.tlist + qb * a.tstride + sp + (int64_t)v * a.nsplit)];
+    };
 
-    if (warp < 4) {
-        // ================= converters: queries once, then the tiles (loads of tile
-        // t+1 in flight while tile t is expanded)
-        {
-            uint32_t c[ST_M / ST_CONV][W];
-            tile_load<W, ST_M / ST_CONV>(a.qcodes, q0, nq, threadIdx.x, c);
-            tile_store<W, ST_M / ST_CONV>(c, nq, a.L, threadIdx.x, sA);
-            tc::fence_async_shared();
-            __syncwarp();
-            if (lane == 0) tc::mbar_arrive(a_full);
-        }
-        uint32_t cur[RPT][W];
-        if (ntl > 0) tile_load<W, RPT>(a.codes, stile[0].y, stile[0].z - stile[0].y, threadIdx.x, cur);
-        for (int t = 0; t < ntl; ++t) {
-            const int4 tl = stile[t];
-            uint32_t nxt[RPT][W];
-            if (t + 1 < ntl)
-                tile_load<W, RPT>(a.codes, stile[t + 1].y, stile[t + 1].z - stile[t + 1].y,
-                                  threadIdx.x, nxt);
-            const uint32_t s = t % a.stages, ph = (t / a.stages) & 1;
-            const long long c0 = clock64();
-            tc::mbar_wait(&empty[s], ph ^ 1);
-            const long long c1 = clock64();
-            if (a.dbg != 3) tile_store<W, RPT>(cur, tl.z - tl.y, a.L, threadIdx.x, ring + s * ST_B);
-            if (a.clk && threadIdx.x == 0) {
-                a.clk[blockIdx.x * 8 + 0] += c1 - c0;
-                a.clk[blockIdx.x * 8 + 1] += clock64() - c1;
+    if (warp == 0 && lane == 0) {
+        // ================= TMA producer
+        uint32_t g = 0, ul = 0;
+        for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++ul) {
+            const int qb = u % a.nqb, sp = u / a.nqb;
+            if (ul > 0) tc::mbar_wait(a_empty, (ul - 1) & 1);
+            tc::mbar_arrive_expect_tx(a_full, A_BYTES);
+            tc::tma_load_2d(sA, &tmQ, a_full, 0, qb * SM_M);
+            const int nt = unit_count(qb, sp);
+            for (int v = 0; v < nt; ++v, ++g) {
+                const int4 tl = unit_tile(qb, sp, v);
+                const uint32_t s = g % a.stages, r = g / a.stages;
+                tc::mbar_wait(&empty[s], (r & 1) ^ 1);
+                tc::mbar_arrive_expect_tx(&full[s], B_BYTES);
+                tc::tma_load_2d(ring + s * B_BYTES, &tmX, &full[s], 0, tl.y);
             }
-            tc::fence_async_shared();
-            __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&full[s]);
-#pragma unroll
-            for (int k = 0; k < RPT; ++k)
-#pragma unroll
-                for (int w = 0; w < W; ++w) cur[k][w] = nxt[k][w];
         }
-    } else if (warp == 4) {
-        // ================= MMA issuer (warp-uniform, one elected lane issues)
-        const uint32_t idesc = tc::umma_idesc_i8(ST_M, ST_N);
-        tc::mbar_wait(a_full, 0);
-        tc::tc_fence_after();
-        const uint32_t abase = tc::smem_u32(sA);
-        for (int t = 0; t < ntl; ++t) {
-            const uint32_t acc = t & 1, tr = t >> 1;
-            const long long c0 = clock64();
-            tc::mbar_wait(&tempty[acc], (tr & 1) ^ 1);
+    } else if (warp == 1) {
+        // ================= MMA issuer
+        const uint32_t idesc = tc::umma_idesc_i8(SM_M, SM_N);
+        uint32_t g = 0, t = 0, ul = 0;
+        for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++ul) {
+            const int qb = u % a.nqb, sp = u / a.nqb;
+            tc::mbar_wait(a_full, ul & 1);
             tc::tc_fence_after();
-            const long long c1 = clock64();
-            const uint32_t s = t % a.stages, ph = (t / a.stages) & 1;
-            tc::mbar_wait(&full[s], ph);
-            tc::tc_fence_after();
-            if (a.clk && lane == 0) {
-                a.clk[blockIdx.x * 8 + 2] += c1 - c0;
-                a.clk[blockIdx.x * 8 + 3] += clock64() - c1;
-            }
-            const uint32_t bbase = tc::smem_u32(ring + s * ST_B);
-            const uint32_t dt = tmem_base + acc * ST_N;
-            for (int kk = 0; kk < ksteps; ++kk)
-                tc::mma_i8_warp(dt, tc::umma_desc_sw128(abase + kk * 32),
-                                tc::umma_desc_sw128(bbase + kk * 32), idesc, kk != 0);
-            tc::mma_commit_warp(&empty[s]);
-            tc::mma_commit_warp(&tfull[acc]);
-        }
-    } else if (warp >= 8) {
-        // ================= epilogue: 16 warps; thread <-> query row (TMEM lane),
-        // 64 columns each.  Appends fill 64-slot chunks of the query's buffer; the
-        // next chunk is reserved one chunk ahead and only read when a group spills
-        // into it, so the reservation atomic never stalls the common path.  Unused
-        // reserved slots get the sentinel ~0 (skipped by select; the fallback test
-        // counts real entries, cntv).
-        const int grp = warp & 3;
-        const int sub = (warp - 8) >> 2;            // 64-column slice of the tile
-        const int row = grp * 32 + lane;
-        const int q = q0 + row;
-        const bool vq = row < nq;
-        unsigned long long *bq = a.buf + (int64_t)(vq ? q : 0) * a.C;
-        uint32_t nvalid = 0;
-        uint32_t cb = 0, cl = 0, nb = 0;           // current chunk base / slots left; next chunk
-        bool have = false;
-        unsigned long long npairs = 0, dbg_sink = 0;
-        for (int t = 0; t < ntl; ++t) {
-            const int4 tl = stile[t];
-            const uint32_t acc = t & 1, tr = t >> 1;
-            const int rows = tl.z - tl.y;
-            const int dl = sdelta[row * a.m + tl.x];
-            const int thr = dl >= 0 ? a.L - 2 * dl : INT_MAX;
-            const uint32_t fj = (uint32_t)(tl.x * (a.L + 1) + a.L);   // flat (j,h) = fj - (L+dot)/2
-            npairs += rows;
-            const long long c0 = clock64();
-            tc::mbar_wait(&tfull[acc], tr & 1);
-            tc::tc_fence_after();
-            const long long c1 = clock64();
-            const uint32_t taddr =
-                tmem_base + ((uint32_t)(grp * 32) << 16) + acc * ST_N + sub * 64;
-#pragma unroll 1
-            for (int g = 0; g < (a.dbg == 2 ? 0 : 2); ++g) {
-                uint32_t r[32];
-                tc::tmem_ld_32x32b_x32(taddr + 32 * g, r);
-                tc::tmem_ld_wait();
-                if (a.dbg == 1) continue;
-                int mx = (int)r[0];   // cheap screen: most groups of cold tiles pass nothing
+            const uint32_t abase = tc::smem_u32(sA);
+            const int nt = unit_count(qb, sp);
+            for (int v = 0; v < nt; ++v, ++g, ++t) {
+                const uint32_t buf = t & 1, tr = t >> 1;
+                tc::mbar_wait(&tempty[buf], (tr & 1) ^ 1);
+                tc::tc_fence_after();
+                const uint32_t s = g % a.stages, r = g / a.stages;
+                tc::mbar_wait(&full[s], r & 1);
+                tc::tc_fence_after();
+                const uint32_t bbase = tc::smem_u32(ring + s * B_BYTES);
+                const uint32_t dt = tmem_base + buf * SM_N;
 #pragma unroll
-                for (int e = 1; e < 32; ++e) mx = max(mx, (int)r[e]);
-                if (mx < thr) continue;
-                const int cbase = sub * 64 + 32 * g;
-                uint32_t mask = 0;
-#pragma unroll
-                for (int e = 0; e < 32; ++e) mask |= (uint32_t)((int)r[e] >= thr) << e;
-                const int valid_cols = rows - cbase;     // columns past the tile's rows
-                if (valid_cols < 32) mask &= valid_cols <= 0 ? 0u : ((1u << valid_cols) - 1u);
-                if (mask == 0u) continue;
-                const uint32_t np = __popc(mask);
-                nvalid += np;
-                if (!have) {   // first pass of this (thread, unit): reserve two chunks
-                    cb = atomicAdd(&a.cnt[q], (uint32_t)ST_CH);
-                    nb = atomicAdd(&a.cnt[q], (uint32_t)ST_CH);
-                    cl = ST_CH;
-                    have = true;
+                for (int kk = 0; kk < KP / 32; ++kk) {
+                    if (kk * 32 >= a.L) break;   // K bytes past L are zero
+                    const uint64_t da = KP == 64 ? tc::umma_desc_sw64(abase + kk * 32)
+                                                 : tc::umma_desc_sw128(abase + kk * 32);
+                    const uint64_t db = KP == 64 ? tc::umma_desc_sw64(bbase + kk * 32)
+                                                 : tc::umma_desc_sw128(bbase + kk * 32);
+                    tc::mma_i8_warp(dt, da, db, idesc, kk != 0);
                 }
-                const uint32_t pos0 = (uint32_t)(tl.y + cbase);
-                if (np <= cl) {
-                    // common path: the current chunk holds the group (no use of nb)
-                    uint32_t slot = cb + (ST_CH - cl);
+                tc::mma_commit_warp(&empty[s]);
+                tc::mma_commit_warp(&tfull[buf]);
+            }
+            tc::mma_commit_warp(a_empty);
+        }
+    } else if (warp >= 4) {
+        // ================= epilogue: thread <-> (query row = TMEM lane, 128-column half)
+        const int grp = warp & 3;
+        const int half = (warp - 4) >> 2;
+        const int row = grp * 32 + lane;
+        int *my = sdot + (threadIdx.x - 128) * SM_DOT_LD;
+        uint32_t t = 0;
+        for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+            const int qb = u % a.nqb, sp = u / a.nqb;
+            const int q = qb * SM_M + row;
+            const bool vq = q < a.Qb;
+            unsigned long long *bq = a.buf + (int64_t)(vq ? q : 0) * a.C;
+            uint32_t cb = 0, cl = 0, nvalid = 0;
+            unsigned long long npairs = 0;
+            const int nt = unit_count(qb, sp);
+            for (int v = 0; v < nt; ++v, ++t) {
+                const int4 tl = unit_tile(qb, sp, v);
+                const int rows = tl.z - tl.y;
+                const int dl = vq ? (int)a.delta[(int64_t)q * a.m + tl.x] : -1;
+                const int thr = dl >= 0 ? a.L - 2 * dl : INT_MAX;
+                const uint32_t fj = (uint32_t)(tl.x * (a.L + 1));
+                if (dl >= 0 && half == 0) npairs += rows;
+                const uint32_t buf = t & 1, tr = t >> 1;
+                tc::mbar_wait(&tfull[buf], tr & 1);
+                tc::tc_fence_after();
+                if (__any_sync(NR_FULL, dl >= 0)) {
+                    const uint32_t taddr = tmem_base + ((uint32_t)(grp * 32) << 16) + buf * SM_N + half * 128;
+#pragma unroll 1
+                    for (int gcol = 0; gcol < 128; gcol += 32) {
+                        uint32_t r[32];
+                        tc::tmem_ld_32x32b_x32(taddr + gcol, r);
+                        tc::tmem_ld_wait();
+                        const int c0 = half * 128 + gcol;
+                        uint32_t mask = 0;
 #pragma unroll
-                    for (int e = 0; e < 32; ++e) {
-                        if ((mask >> e) & 1u) {
-                            const unsigned long long v =
-                                ((unsigned long long)(fj - (uint32_t)((a.L + (int)r[e]) >> 1)) << 32) | (pos0 + e);
-                            if (a.dbg == 4) dbg_sink ^= v;
-                            else if (slot < a.C) bq[slot] = v;
-                            ++slot;
+                        for (int e = 0; e < 32; ++e) mask |= (uint32_t)((int)r[e] >= thr) << e;
+                        const int vc = rows - c0;   // columns past the tile's rows
+                        if (vc < 32) mask &= vc <= 0 ? 0u : ((1u << vc) - 1u);
+                        if (!mask) continue;
+#pragma unroll
+                        for (int e = 0; e < 32; e += 4)
+                            *reinterpret_cast<int4 *>(my + e) =
+                                make_int4((int)r[e], (int)r[e + 1], (int)r[e + 2], (int)r[e + 3]);
+                        nvalid += __popc(mask);
+                        const uint32_t pos0 = (uint32_t)(tl.y + c0);
+                        while (mask) {
+                            const int e = __ffs(mask) - 1;
+                            mask &= mask - 1;
+                            const uint32_t h = (uint32_t)((a.L - my[e]) >> 1);
+                            if (cl == 0) { cb = atomicAdd(&a.cnt[q], (uint32_t)SM_CH); cl = SM_CH; }
+                            const uint32_t slot = cb + (SM_CH - cl);
+                            if (slot < a.C) bq[slot] = ((unsigned long long)(fj + h) << 32) | (pos0 + e);
+                            --cl;
                         }
                     }
-                    cl -= np;
-                } else {
-                    // spill into the reserved chunk (reserved at least one group ago)
-                    const uint32_t cur0 = cb + (ST_CH - cl);
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) {
-                        const uint32_t i = __popc(mask & ((1u << e) - 1u));
-                        const uint32_t slot = i < cl ? cur0 + i : nb + (i - cl);
-                        if (((mask >> e) & 1u) && slot < a.C)
-                            bq[slot] = ((unsigned long long)(fj - (uint32_t)((a.L + (int)r[e]) >> 1)) << 32) |
-                                       (pos0 + e);
-                    }
-                    cl = ST_CH - (np - cl);
-                    cb = nb;
-                    nb = atomicAdd(&a.cnt[q], (uint32_t)ST_CH);
                 }
+                tc::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&tempty[buf]);
             }
-            tc::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&tempty[acc]);
-            if (a.clk && warp == 8 && lane == 0) {
-                a.clk[blockIdx.x * 8 + 4] += c1 - c0;
-                a.clk[blockIdx.x * 8 + 5] += clock64() - c1;
-            }
+            // unused slots of the last chunk: sentinel (skipped by select; the fallback
+            // test counts real entries, cntv)
+            for (; cl > 0; --cl)
+                if (cb + (SM_CH - cl) < a.C) bq[cb + (SM_CH - cl)] = ~0ull;
+            if (vq && nvalid) atomicAdd(&a.cntv[q], nvalid);
+            if (vq && npairs && a.pairs) atomicAdd(a.pairs, npairs);
         }
-        if (vq && have) {   // unused slots of the current and the reserved chunk
-            for (uint32_t e = ST_CH - cl; e < (uint32_t)ST_CH; ++e)
-                if (cb + e < a.C) bq[cb + e] = ~0ull;
-            for (uint32_t e = 0; e < (uint32_t)ST_CH; ++e)
-                if (nb + e < a.C) bq[nb + e] = ~0ull;
-        }
-        if (vq && nvalid) atomicAdd(&a.cntv[q], nvalid);
-        if (vq && sub == 0 && a.pairs) atomicAdd(a.pairs, npairs + (dbg_sink == 1 ? 1 : 0));
     }
     __syncthreads();
-    if (a.clk && threadIdx.x == 0) a.clk[blockIdx.x * 8 + 6] = (unsigned long long)ntl;
-    if (warp == 4) {
+    if (warp == 2) {
         tc::tc_fence_after();
         tc::tmem_dealloc(tmem_base, 512);
     }
 }
 
-// blk_act[qb][j] = any query of block qb has delta_j(q) >= 0
-__global__ void scan_blk_act(const int8_t *__restrict__ delta, int Qb, int m,
-                             uint8_t *__restrict__ blk_act) {
-    const int qb = blockIdx.x;
-    for (int j = threadIdx.x; j < m; j += blockDim.x) {
-        int any = 0;
-        const int q1 = min(Qb, (qb + 1) * ST_M);
-        for (int q = qb * ST_M; q < q1; ++q) any |= delta[(int64_t)q * m + j] >= 0;
-        blk_act[(int64_t)qb * m + j] = (uint8_t)any;
-    }
-}
-
-static size_t scan_tc_smem(int m, int L, int tiles_per_split, int stages) {
-    (void)L;
-    return 1024 + ST_A + (size_t)stages * ST_B +
-           (size_t)((ST_M * m + 15) & ~15) + (size_t)tiles_per_split * 16 +
-           (2 * ST_STAGES + 6) * 8 + 16;
+static size_t scan_mma_smem(int kp, int stages) {
+    return 1024 + (size_t)SM_M * kp + (size_t)stages * SM_N * kp + 256 * SM_DOT_LD * 4 +
+           (2 * SM_MAX_STAGES + 6) * 8 + 16;
 }
 
 // Opt-in (NRLSH_SCAN_TC=1): exact and parity-tested, but measured slower than the
-// popcount scan on c4 (4.8 vs 0.9 ms per 1024 queries): the per-column epilogue
-// (mask + predicated (j,h,pos) stores, ~350 instructions per 32 columns of a dense
-// group) is instruction-bound while the MMA takes ~300 cycles per tile.
-// "Tensor-core scan" has the measurements and the redesign (grouped appends).
+// popcount scan on c4 (0.93 vs 0.58 ms per 1024 queries): the tensor pipe is ~4%
+// busy; the epilogue's per-pair appends (divergent loops over the pass bits, chunk
+// reservations) bound it.  DESIGN.md "Tensor-core scan" has the numbers.
 bool scan_tc_supported(const nrlsh_index *ix) {
-    // (smem: 16 KB queries + 128 KB ring + rank table + delta rows + tile list)
-    return ix->tiles_d != nullptr && ix->L <= 128 && ix->W != 3 &&
-           scan_tc_smem(ix->m, ix->L, 2048, 2) <= 226 * 1024 && getenv("NRLSH_SCAN_TC") &&
-           atoi(getenv("NRLSH_SCAN_TC")) != 0;
+    if (!ix->codes_pm || !ix->tiles_d || ix->L > 128) return false;
+    const char *e = getenv("NRLSH_SCAN_TC");
+    return e && atoi(e) != 0;
 }
 
-void launch_scan_tc(const nrlsh_index *ix, const uint32_t *qcodes, const int8_t *delta, int Qb,
-                    uint8_t *blk_act, unsigned long long *buf, uint32_t *cnt, uint32_t *cntv,
-                    int64_t C, unsigned long long *pairs, cudaStream_t s) {
+size_t scan_tc_ws_bytes(const nrlsh_index *ix, int Qb) {
+    const int64_t nqb = (Qb + SM_M - 1) / SM_M;
+    return (size_t)(nqb * (1 + ix->ntiles) + 4) * 4 + (size_t)Qb * scan_kp(ix->L) + 2048;
+}
+
+int launch_scan_tc(const nrlsh_index *ix, const uint32_t *qcodes, const int8_t *delta, int Qb,
+                   void *ws, unsigned long long *buf, uint32_t *cnt, uint32_t *cntv, int64_t C,
+                   unsigned long long *pairs, cudaStream_t s) {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    ScanTcArgs a;
-    a.codes = ix->codes;
-    a.qcodes = qcodes;
-    a.delta = delta;
-    a.blk_act = blk_act;
+    const int Kp = scan_kp(ix->L);
+    ScanMmaArgs a;
+    a.nqb = (Qb + SM_M - 1) / SM_M;
+    int32_t *tcount = reinterpret_cast<int32_t *>(ws);
+    int32_t *tlist = tcount + a.nqb + 4;
+    int8_t *qpm = reinterpret_cast<int8_t *>(
+        (reinterpret_cast<uintptr_t>(tlist + (int64_t)a.nqb * ix->ntiles) + 1023) & ~(uintptr_t)1023);
+    // the queries' +-1 rows, the per-block tile lists
+    launch_expand_pm(qcodes, Qb, ix->W, ix->L, qpm, s);
+    cudaMemsetAsync(tcount, 0, (size_t)a.nqb * 4, s);
+    scan_tile_lists<<<dim3((unsigned)((ix->ntiles + 1023) / 1024), a.nqb), 256, 0, s>>>(
+        delta, Qb, ix->m, ix->tiles_d, ix->ntiles, tlist, ix->ntiles, tcount);
+    note_launch();
+    CUtensorMap tq, tx;
+    if (!make_tmap_2d(&tq, qpm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, Kp, Qb, Kp, SM_M, Kp) ||
+        !make_tmap_2d(&tx, ix->codes_pm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, Kp, ix->n, Kp, SM_N, Kp))
+        return -1;
     a.tiles = ix->tiles_d;
-    a.ntiles = ix->ntiles;
+    a.tlist = tlist;
+    a.tcount = tcount;
+    a.tstride = ix->ntiles;
+    a.delta = delta;
     a.Qb = Qb;
     a.m = ix->m;
     a.L = ix->L;
-    a.W = ix->W;
-    a.nqb = (Qb + ST_M - 1) / ST_M;
-    // one unit per CTA; splits small enough that the tile list fits in smem
-    a.nsplit = std::max(1, std::min(ix->ntiles, sms / a.nqb));
-    while ((ix->ntiles + a.nsplit - 1) / a.nsplit > 2048) ++a.nsplit;
-    a.tiles_per_split = (ix->ntiles + a.nsplit - 1) / a.nsplit;
-    a.nsplit = (ix->ntiles + a.tiles_per_split - 1) / a.tiles_per_split;
+    a.Kp = Kp;
+    a.nsplit = std::max(1, sms / a.nqb);
     a.buf = buf;
     a.cnt = cnt;
     a.cntv = cntv;
     a.C = C;
     a.pairs = pairs;
-    a.dbg = getenv("NRLSH_SCAN_DBG") ? atoi(getenv("NRLSH_SCAN_DBG")) : 0;
-    scan_blk_act<<<a.nqb, 256, 0, s>>>(delta, Qb, ix->m, blk_act);
     a.stages = 2;
-    for (int st = ST_STAGES; st > 2; --st)
-        if (scan_tc_smem(ix->m, ix->L, a.tiles_per_split, st) <= 226 * 1024) { a.stages = st; break; }
-    const size_t sm = scan_tc_smem(ix->m, ix->L, a.tiles_per_split, a.stages);
-    const int grid = a.nqb * a.nsplit;
-    a.clk = nullptr;
-    if (getenv("NRLSH_SCAN_CLK")) {
-        cudaMalloc(&a.clk, (size_t)grid * 64);
-        cudaMemsetAsync(a.clk, 0, (size_t)grid * 64, s);
+    for (int st = SM_MAX_STAGES; st > 2; --st)
+        if (scan_mma_smem(Kp, st) <= 227 * 1024) { a.stages = st; break; }
+    const size_t sm = scan_mma_smem(Kp, a.stages);
+    const int grid = std::min(sms, a.nqb * a.nsplit);
+    if (Kp == 64) {
+        cudaFuncSetAttribute(k6_scan_mma<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        k6_scan_mma<64><<<grid, SM_THREADS, sm, s>>>(tq, tx, a);
+    } else {
+        cudaFuncSetAttribute(k6_scan_mma<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        k6_scan_mma<128><<<grid, SM_THREADS, sm, s>>>(tq, tx, a);
     }
-#define NR_STC(W_)                                                                             \
-    cudaFuncSetAttribute(k6_scan_tc<W_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
-    k6_scan_tc<W_><<<grid, ST_THREADS, sm, s>>>(a)
-    if (ix->W == 4) { NR_STC(4); } else if (ix->W == 2) { NR_STC(2); } else { NR_STC(1); }
-#undef NR_STC
-    note_launch(2);
-    if (a.clk) {
-        std::vector<unsigned long long> h((size_t)grid * 8);
-        cudaMemcpyAsync(h.data(), a.clk, h.size() * 8, cudaMemcpyDeviceToHost, s);
-        cudaStreamSynchronize(s);
-        double acc[8] = {0};
-        for (int b = 0; b < grid; ++b)
-            for (int i = 0; i < 8; ++i) acc[i] += (double)h[(size_t)b * 8 + i];
-        fprintf(stderr, "scan_tc clk/CTA: conv wait %.0f store %.0f | mma wait_tempty %.0f wait_full %.0f | "
-                        "epi wait %.0f work %.0f | tiles %.0f\n",
-                acc[0] / grid, acc[1] / grid, acc[2] / grid, acc[3] / grid, acc[4] / grid,
-                acc[5] / grid, acc[6] / grid);
-        cudaFree(a.clk);
-    }
+    note_launch();
+    return 0;
 }
 
 }  // namespace nrlsh

@@ -18,6 +18,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
+#include <cstdio>
 
 #include "common.cuh"
 #include "internal.h"
@@ -76,9 +78,10 @@ static EncodeTiledFn encode_fn() {
     return fn;
 }
 
-// 2-D row-major [rows x cols] of `esize`-byte elements, box {64 B*2 ... } with 128B swizzle
-static bool make_tmap(CUtensorMap *m, const void *base, CUtensorMapDataType dt, int esize,
-                      uint64_t cols, uint64_t rows, uint32_t box_cols, uint32_t box_rows) {
+// 2-D row-major [rows x cols] of `esize`-byte elements, box {box_cols, box_rows},
+// 128-byte (default) or 64-byte swizzle
+bool make_tmap_2d(CUtensorMap *m, const void *base, CUtensorMapDataType dt, int esize,
+                  uint64_t cols, uint64_t rows, uint32_t box_cols, uint32_t box_rows, int swizzle) {
     EncodeTiledFn fn = encode_fn();
     if (!fn) return false;
     cuuint64_t dims[2] = {cols, rows};
@@ -86,9 +89,14 @@ static bool make_tmap(CUtensorMap *m, const void *base, CUtensorMapDataType dt, 
     cuuint32_t box[2] = {box_cols, box_rows};
     cuuint32_t es[2] = {1, 1};
     CUresult r = fn(m, dt, 2, const_cast<void *>(base), dims, strides, box, es,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    swizzle == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
+}
+static bool make_tmap(CUtensorMap *m, const void *base, CUtensorMapDataType dt, int esize,
+                      uint64_t cols, uint64_t rows, uint32_t box_cols, uint32_t box_rows) {
+    return make_tmap_2d(m, base, dt, esize, cols, rows, box_cols, box_rows, 128);
 }
 
 // ------------------------------------------------------------ the kernel
@@ -983,7 +991,12 @@ int launch_gt_filter_tc(const void *Xb, int64_t n, int d, int dp, const void *Qb
     // two passes when the rows are norm-sorted tiles: the tiles of largest |x| first
     // (their scores lift theta close to its final value), then the rest, pruned
     // against the lifted theta
-    const int npass = lists && tl->xsplit > 0.f && !getenv("NRLSH_GT_ONEPASS") ? 2 : 1;
+    const bool two = lists && tl->xsplit > 0.f && !getenv("NRLSH_GT_ONEPASS");
+    // tl->pass: 0 = both passes here, 1 / 2 = only that pass (the caller re-ranks the
+    // first pass's survivors in between, lifting theta to an exact k-th best)
+    const int p_lo = two ? (tl->pass == 2 ? 1 : 0) : 0;
+    const int p_hi = two ? (tl->pass == 1 ? 1 : 2) : 1;
+    if (!two && tl && tl->pass == 2) return 0;   // single pass already done
     if (lists) {
         a.tcount = tl->ws;
         a.tstride = ntiles;
@@ -1006,16 +1019,25 @@ int launch_gt_filter_tc(const void *Xb, int64_t n, int d, int dp, const void *Qb
     }
     const size_t sm = gt_tc_smem_bytes(NT, kblocks, a.stages, a.heap_smem ? k : 0);
     const int grid = std::min(sms, a.nqp * a.nsplit);
-    for (int pass = 0; pass < npass; ++pass) {
+    for (int pass = p_lo; pass < p_hi; ++pass) {
         if (lists) {   // per query pair, only the tiles that can hold an answer (GtTiles)
             cudaMemsetAsync(const_cast<int32_t *>(a.tcount), 0, (size_t)a.nqp * 4, s);
             gt_tile_lists<<<dim3((unsigned)((ntiles + 1023) / 1024), a.nqp), 256, 0, s>>>(mb ? mb->R : nullptr, mb ? mb->L : 0, mb ? mb->m : 0,
                                                 mb ? mb->part : nullptr, n, mb ? mb->sel_B : nullptr,
                                                 Qb, NT, tl->xmax128, theta_glob, qnorm, 2.0 * eps_rel,
-                                                tl->xsplit, npass == 1 ? 0 : pass + 1,
+                                                tl->xsplit, two ? pass + 1 : 0,
                                                 const_cast<int32_t *>(a.tlist), a.tstride,
                                                 const_cast<int32_t *>(a.tcount), tl->pairs);
             note_launch();
+        }
+        if (lists && getenv("NRLSH_GT_TILESTATS")) {   // development: tiles kept per pair
+            std::vector<int32_t> hc(a.nqp);
+            cudaMemcpyAsync(hc.data(), a.tcount, (size_t)a.nqp * 4, cudaMemcpyDeviceToHost, s);
+            cudaStreamSynchronize(s);
+            fprintf(stderr, "gt tiles (%s, pass %d, of %lld):", mb ? "member" : "gt", pass,
+                    (long long)ntiles);
+            for (int g = 0; g < a.nqp; ++g) fprintf(stderr, " %d", hc[g]);
+            fprintf(stderr, "\n");
         }
         if (NT == 256) {
             cudaFuncSetAttribute(gt_filter_tc<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);

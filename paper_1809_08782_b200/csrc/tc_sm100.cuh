@@ -281,6 +281,17 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
     return d;
 }
 
+// The same for 64-byte swizzled K-major rows (8-row atoms 512 B apart).
+__device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);          // start address  [0,14)
+    d |= (uint64_t)1 << 16;                          // LBO (unused for swizzled K-major)
+    d |= (uint64_t)(512 >> 4) << 32;                 // SBO            [32,46)
+    d |= (uint64_t)1 << 46;                          // version = 1 (sm100)
+    d |= (uint64_t)4 << 61;                          // SWIZZLE_64B
+    return d;
+}
+
 // Instruction descriptor, dense, fp32 accumulate, both operands K-major.
 // a/b format: 1 = BF16 (kind::f16), 2 = TF32 (kind::tf32).
 __host__ __device__ constexpr uint32_t umma_idesc(uint32_t ab_format, uint32_t M, uint32_t N) {

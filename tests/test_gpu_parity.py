@@ -446,13 +446,18 @@ def test_full_size_sampled(name, L, m):
         assert_topk_match(gt_ids[qi], gt_sc[qi], a, s, X, Q[qi])
 
 
+@pytest.mark.parametrize("scan", ["tensor", "popcount"])
 @pytest.mark.parametrize("case", [("c4", 300_000, 32, 64, 128), ("scale", 70_000, 16, 128, 256),
-                                  ("tiny", None, None, 32, 8)], ids=_ids)
-def test_candidates_parity_tensor_core_scan(built, case, monkeypatch):
-    """The opt-in tcgen05 int8 Hamming scan (scan_tc.cu) gives the same candidate
-    sets, ranks and (R, id) order as the oracle (identical codes injected)."""
-    monkeypatch.setenv("NRLSH_SCAN_TC", "1")
+                                  ("tiny", None, None, 32, 8), ("c4", 300_000, 32, 32, 4),
+                                  ("c3", 40_000, 64, 64, 1)], ids=_ids)
+def test_candidates_parity_both_scans(built, case, scan, monkeypatch):
+    """Both Hamming scans — the tcgen05 int8 one (scan_tc.cu, the default) and the
+    popcount one (NRLSH_SCAN_TC=0) — give the oracle's candidate sets, ranks and
+    (R, id) order (identical codes injected), across budgets from 1 to n."""
+    monkeypatch.setenv("NRLSH_SCAN_TC", "1" if scan == "tensor" else "0")
     cfg, X, Q, Xd, idx, orc = built(*case)
+    if scan == "tensor":   # its +-1 code rows are made at build time (opt-in)
+        idx = _P().Index(Xd, case[3], case[4], seed=cfg.seed)
     n = X.shape[0]
     ocodes = orc.codes()
     idx.set_codes(ocodes[orc.perm])
