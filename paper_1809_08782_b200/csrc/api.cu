@@ -608,7 +608,7 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
     const int64_t Cg = getenv("NRLSH_RERANK_TC_CAP")
                            ? std::max<int64_t>(16, atoll(getenv("NRLSH_RERANK_TC_CAP")))
                            : std::min<int64_t>(n, std::max<int64_t>(16384, 256 * (int64_t)k));
-    DBuf rsb, rspk, rseed, rtid, rtsc, rth, rqb, rqn, rhp, rcd, rcc, rov, rovn, rpt, rtl;
+    DBuf rsb, rspk, rseed, rtid, rtsc, rth, rqb, rqn, rhp, rcd, rcc, rov, rovn, rpt, rtl, rqp;
     if (use_rtc &&
         (rsb.alloc((size_t)Qmax * 4, s) || rspk.alloc((size_t)Qmax * 4, s) ||
          rseed.alloc((size_t)Qmax * KS * 4, s) || rtid.alloc((size_t)Qmax * k * 8, s) ||
@@ -617,7 +617,7 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
          rhp.alloc(gt_heap_bytes(k), s) || rcd.alloc((size_t)Qmax * Cg * 4, s) ||
          rcc.alloc((size_t)Qmax * 4, s) || rov.alloc((size_t)nq * 8, s) || rovn.alloc(4, s) ||
          rpt.alloc(std::max(rerank_partial_bytes(Qmax, Cg, k), rerank_partial_bytes(Qmax, KS, k)), s) ||
-         rtl.alloc(gt_tile_ws_bytes(n, Qmax), s)))
+         rtl.alloc(gt_tile_ws_bytes(n, Qmax), s) || rqp.alloc((size_t)Qmax * 4, s)))
         return fail(NRLSH_ENOMEM, "query workspace (tensor-core re-rank)");
     if (use_rtc) cudaMemsetAsync(rovn.p, 0, 4, s);
     GtMember mb;
@@ -632,8 +632,11 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
     tls.xmax128 = ix->tile_xmax;
     tls.ws = use_rtc ? rtl.get<int32_t>() : nullptr;
     tls.pairs = (unsigned long long *)(fl.get<int>() + 8);
-    tls.xsplit = getenv("NRLSH_GT_ONEPASS") ? 0.f : ix->tile_xsplit;
+    // one pass for the re-rank (two measured slower: 0.50 vs 0.43 ms per 1024 queries
+    // on c4, the candidates' k-th best stays low after the top tiles)
+    tls.xsplit = getenv("NRLSH_RERANK_TWOPASS") ? ix->tile_xsplit : 0.f;
     tls.pass = 0;
+    tls.qperm = nullptr;
     const int init_flags[10] = {INT_MAX, INT_MAX, 0, 0, 0, 0, 0, 0, 0, 0};
     cudaMemcpyAsync(fl.p, init_flags, 40, cudaMemcpyHostToDevice, s);
     unsigned long long *pairs = (unsigned long long *)(fl.get<int>() + 4);
@@ -663,7 +666,13 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
                                        rth.get<uint32_t>(), s);
             }
             ProfScope p(SLOT_RERANK, s);
-            launch_bf16_prep(Qd, Qb, ix->d, ix->dpb, rqb.p, rqn.get<float>(), s);
+            // bf16 query rows in descending theta/|q| (pairs of similar bound prune alike)
+            // (opt-in NRLSH_GT_SORT=1: measured slower on c4 — the filter's time does not
+            // track its tile count at these sizes)
+            const bool sorted = Qb <= 4096 && getenv("NRLSH_GT_SORT");
+            if (sorted) launch_sort_by_bound(Qd, ix->d, Qb, rth.get<uint32_t>(), rqp.get<int32_t>(), s);
+            tls.qperm = sorted ? rqp.get<int32_t>() : nullptr;
+            launch_bf16_prep(Qd, Qb, ix->d, ix->dpb, rqb.p, rqn.get<float>(), s, tls.qperm);
             cudaMemsetAsync(rcc.p, 0, (size_t)Qb * 4, s);
             mb.qcodes = qc.get<uint32_t>();
             mb.sel_B = rsb.get<uint32_t>();
@@ -887,7 +896,7 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
                               : std::min<int64_t>(n, std::max<int64_t>(4 * (int64_t)S * k + 4096, 2 * k));
     int Qmax = (int)std::min<int64_t>(1024, nq);
     while (Qmax > 64 && (int64_t)Qmax * (ns * 4 + Cg * 8) > ((int64_t)2500 << 20)) Qmax >>= 1;
-    DBuf xn, qn, ss, lb, tid, tsc, cc, cd, cs, xb, qb, th, pt, hp, tw;
+    DBuf xn, qn, ss, lb, tid, tsc, cc, cd, cs, xb, qb, th, pt, hp, tw, gqp, gqb, gqn;
     const int64_t npad = (n + 255) / 256 * 256;   // |x| padded: the tc kernel bulk-loads 1 KB tiles
     if (xn.alloc((size_t)npad * 4, s) || qn.alloc((size_t)nq * 4, s) ||
         ss.alloc((size_t)Qmax * ns * 4, s) || lb.alloc((size_t)Qmax * 4, s) ||
@@ -902,7 +911,9 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
     if (use_tc) {
         if ((!Xbp && xb.alloc((size_t)n * dp * 2, s)) || qb.alloc((size_t)nq * dp * 2, s) ||
             hp.alloc(gt_heap_bytes(k), s) ||
-            (Xb_ix && tile_xmax_ix && tw.alloc(gt_tile_ws_bytes(n, Qmax), s)))
+            (Xb_ix && tile_xmax_ix &&
+             (tw.alloc(gt_tile_ws_bytes(n, Qmax), s) || gqp.alloc((size_t)Qmax * 4, s) ||
+              gqb.alloc((size_t)Qmax * dp * 2, s) || gqn.alloc((size_t)Qmax * 4, s))))
             return fail(NRLSH_ENOMEM, "exact_topk bf16 workspace");
         ProfScope p(SLOT_GT_NORMS, s);
         if (!Xbp) {
@@ -925,6 +936,7 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
     gtl.pairs = nullptr;
     gtl.xsplit = getenv("NRLSH_GT_ONEPASS") ? 0.f : xsplit_ix;
     gtl.pass = 0;
+    gtl.qperm = nullptr;
     std::vector<uint32_t> hcnt(Qmax);
     for (int64_t q0 = 0; q0 < nq; q0 += Qmax) {
         const int Qb = (int)std::min<int64_t>(Qmax, nq - q0);
@@ -943,13 +955,24 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
             }
             ProfScope p(SLOT_GT_FILTER, s);
             const bool tiles = Xb_ix && tile_xmax_ix;
+            // bf16 query rows of this batch in descending theta/|q| (tile lists only)
+            const void *qrows = (const uint16_t *)qb.p + q0 * dp;
+            const float *qnrows = qnb;
+            gtl.qperm = nullptr;
+            if (tiles && seed_ids && Qb <= 4096 && getenv("NRLSH_GT_SORT")) {
+                launch_sort_by_bound(Qb_ptr, d, Qb, th.get<uint32_t>(), gqp.get<int32_t>(), s);
+                launch_bf16_prep(Qb_ptr, Qb, d, dp, gqb.p, gqn.get<float>(), s, gqp.get<int32_t>());
+                gtl.qperm = gqp.get<int32_t>();
+                qrows = gqb.p;
+                qnrows = gqn.get<float>();
+            }
             // with tile lists: the top-|x| tiles, an exact re-rank of their survivors
             // (theta := a real k-th best, the final re-rank's arithmetic), the rest
             const int npass = tiles && gtl.xsplit > 0.f ? 2 : 1;
             for (int pass = 1; pass <= npass; ++pass) {
                 gtl.pass = npass == 1 ? 0 : pass;
-                if (launch_gt_filter_tc(Xbp, n, d, dp, (const uint16_t *)qb.p + q0 * dp, Qb,
-                                        xnp, qnb, eps_rel, k, th.get<uint32_t>(),
+                if (launch_gt_filter_tc(Xbp, n, d, dp, qrows, Qb,
+                                        xnp, qnrows, eps_rel, k, th.get<uint32_t>(),
                                         hp.get<float>(), cd.get<int32_t>(), cc.get<uint32_t>(), Cg, s,
                                         Xb_ix ? perm_ix : nullptr, nullptr, tiles ? &gtl : nullptr))
                     return fail(NRLSH_ECUDA, "tensor map encoding failed");

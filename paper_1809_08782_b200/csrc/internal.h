@@ -251,7 +251,15 @@ struct GtTiles {
     unsigned long long *pairs;  // optional: += (query, row) pairs multiplied
     float xsplit;               // > 0: two passes, tiles with xmax >= xsplit first
     int pass;                   // 0: both passes; 1 / 2: only that one
+    const int32_t *qperm;       // optional: row r of the bf16 queries / qnorm is query
+                                //   qperm[r] (queries sorted by theta/|q|: pairs of similar
+                                //   bound prune alike); theta, lists and member data stay
+                                //   in query order
 };
+// qperm[0..Qb) = the queries in descending theta_q / |q| (theta_glob orderable
+// images, 0 = unset); one CTA, Qb <= 4096
+void launch_sort_by_bound(const float *Q, int d, int Qb, const uint32_t *theta_glob,
+                          int32_t *qperm, cudaStream_t s);
 size_t gt_tile_ws_bytes(int64_t n, int Qb);
 void launch_tile_xmax128(const float *xnorm_pos, int64_t n, float *out, cudaStream_t s);
 // Xb / xnorm rows in any order: perm[row] = item id written to the survivor lists

@@ -1062,9 +1062,11 @@ __global__ void __launch_bounds__(kRrThreads) k8_rerank(
     }
     __syncthreads();
     const int c = (int)s_cnt;
-    for (int e = c + threadIdx.x; e < cap; e += blockDim.x) buf[e] = ~0ull;
+    int np2 = 2;   // sort only the collected entries (padded to a power of two)
+    while (np2 < c) np2 <<= 1;
+    for (int e = c + threadIdx.x; e < np2; e += blockDim.x) buf[e] = ~0ull;
     __syncthreads();
-    bitonic_sort_smem(buf, cap);
+    bitonic_sort_smem(buf, np2);
     if (partial) {
         unsigned long long *pp = partial + ((int64_t)q * gridDim.y + blockIdx.y) * k;
         for (int t = threadIdx.x; t < k; t += blockDim.x) pp[t] = t < c ? buf[t] : ~0ull;

@@ -154,6 +154,7 @@ struct GtArgs {
     const uint32_t *qcodes;
     const uint32_t *sel_B, *sel_pk;
     const int32_t *perm;    // row -> item id of the survivors (nullptr: identity)
+    const int32_t *qperm;   // query row -> original query index (nullptr: identity)
     // per query-pair tile lists (member mode: only tiles of sub-datasets holding a
     // candidate of the pair's queries); nullptr: every tile
     const int32_t *tlist;   // [nqp x tstride] tile indices
@@ -205,11 +206,13 @@ struct GtEpiRow {
         theta = th;
         thr_adj = th - fabsf(th) * 2.384185791015625e-7f;   // 2^-22
     }
-    __device__ __forceinline__ void begin(const GtArgs &args, int q_, bool vq_, float *heap_) {
+    // qrow: the query's row of the (possibly bound-sorted) bf16 query matrix and of
+    // qnorm; everything else is indexed by the original query index q = qperm[qrow]
+    __device__ __forceinline__ void begin(const GtArgs &args, int qrow, bool vq_, float *heap_) {
         a = &args;
-        q = q_;
         vq = vq_;
-        qe = vq ? args.eps_rel * args.qnorm[q] : 0.f;
+        q = vq && args.qperm ? __ldg(args.qperm + qrow) : qrow;
+        qe = vq ? args.eps_rel * args.qnorm[qrow] : 0.f;
         theta = -INFINITY;
         thr_adj = -INFINITY;
         pub = -INFINITY;
@@ -509,7 +512,7 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
                 const float *xn = sxn + b * GT_N;
                 uint32_t o_next = 0;
                 const bool share = er.vq && ((t & 3) == 0);
-                if (share) o_next = *((volatile uint32_t *)&a.theta_glob[q]);   // consumed below
+                if (share) o_next = *((volatile uint32_t *)&a.theta_glob[er.q]);   // consumed below
                 tc::mbar_wait(&xfull[b], (t >> 1) & 1);
                 const uint32_t buf = t % NBUF, tr = t / NBUF;
                 tc::mbar_wait(&tfull[buf * GT_QB + h], tr & 1);
@@ -709,7 +712,7 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
                 const float *xn = sxn + b * GP_PN;
                 uint32_t o_next = 0;
                 const bool share = er.vq && ((t & 3) == 0);
-                if (share) o_next = *((volatile uint32_t *)&a.theta_glob[q]);
+                if (share) o_next = *((volatile uint32_t *)&a.theta_glob[er.q]);
                 tc::mbar_wait(&xfull[b], tr & 1);
                 tc::mbar_wait_cluster(&tfull[b], tr & 1);
                 tc::tc_fence_after();
@@ -780,7 +783,8 @@ __global__ void __launch_bounds__(256) gt_tile_lists(const uint16_t *__restrict_
                                                      float xsplit, int phase,
                                                      int32_t *__restrict__ list, int64_t stride,
                                                      int32_t *__restrict__ count,
-                                                     unsigned long long *__restrict__ pairs) {
+                                                     unsigned long long *__restrict__ pairs,
+                                                     const int32_t *__restrict__ qperm) {
     __shared__ uint32_t act[257];
     __shared__ uint32_t sB[2 * GT_M];
     __shared__ float s_tau;
@@ -789,13 +793,14 @@ __global__ void __launch_bounds__(256) gt_tile_lists(const uint16_t *__restrict_
     const int q0 = g * 2 * GT_M, q1 = min(Qb, q0 + 2 * GT_M);
     // tau_g: min over the pair's queries (a thread per query; warp + smem min)
     float tq = INFINITY;
-    for (int q = q0 + threadIdx.x; q < q1; q += blockDim.x) {
-        const uint32_t o = theta_glob[q];
+    for (int q = q0 + threadIdx.x; q < q1; q += blockDim.x) {   // q: query row
+        const int qo = qperm ? qperm[q] : q;
+        const uint32_t o = theta_glob[qo];
         const float th = o ? float_unorder(o) : -INFINITY;
         // rounded down in double: tau never exceeds the exact threshold
         const double t = th > 0.f ? (double)th / ((double)qnorm[q] * (1.0 + eps2) * (1.0 + 0x1p-20)) : 0.0;
         tq = fminf(tq, __double2float_rd(t));
-        if (R) sB[q - q0] = sel_B[q];
+        if (R) sB[q - q0] = sel_B[qo];
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) tq = fminf(tq, __shfl_xor_sync(NR_FULL, tq, o));
@@ -842,6 +847,51 @@ __global__ void __launch_bounds__(256) gt_tile_lists(const uint16_t *__restrict_
     // (query, item) pairs the filter multiplies for this pair's real queries
     if (threadIdx.x == 0 && pairs && s_found)
         atomicAdd(pairs, (unsigned long long)s_found * nt * (unsigned long long)(q1 - q0));
+}
+
+// queries in descending theta_q / |q| (unset theta last): grouping queries of similar
+// bound into the filter's 256-query pairs makes each pair's pruning bound (its
+// minimum) tight for all but the last pair
+__global__ void __launch_bounds__(1024) sort_by_bound(const float *__restrict__ Q, int d, int Qb,
+                                                      const uint32_t *__restrict__ theta,
+                                                      int32_t *__restrict__ qperm) {
+    extern __shared__ unsigned long long keys[];
+    int np2 = 2;
+    while (np2 < Qb) np2 <<= 1;
+    for (int i = threadIdx.x; i < np2; i += blockDim.x) {
+        unsigned long long key = ~0ull;
+        if (i < Qb) {
+            float ss = 0.f;
+            for (int e = 0; e < d; ++e) ss = fmaf(Q[(int64_t)i * d + e], Q[(int64_t)i * d + e], ss);
+            const uint32_t o = theta[i];
+            const float th = o ? float_unorder(o) : 0.f;
+            const float kf = (th > 0.f && ss > 0.f) ? th / sqrtf(ss) : 0.f;
+            key = ((unsigned long long)(~float_order(kf)) << 32) | (uint32_t)i;
+        }
+        keys[i] = key;
+    }
+    __syncthreads();
+    for (int size = 2; size <= np2; size <<= 1)
+        for (int st = size >> 1; st > 0; st >>= 1) {
+            for (int t = threadIdx.x; t < np2; t += blockDim.x) {
+                const int o = t ^ st;
+                if (o > t) {
+                    const bool up = (t & size) == 0;
+                    const unsigned long long x = keys[t], y = keys[o];
+                    if ((x > y) == up) { keys[t] = y; keys[o] = x; }
+                }
+            }
+            __syncthreads();
+        }
+    for (int i = threadIdx.x; i < Qb; i += blockDim.x) qperm[i] = (int32_t)(uint32_t)keys[i];
+}
+
+void launch_sort_by_bound(const float *Q, int d, int Qb, const uint32_t *theta_glob,
+                          int32_t *qperm, cudaStream_t s) {
+    int np2 = 2;
+    while (np2 < Qb) np2 <<= 1;
+    sort_by_bound<<<1, 1024, (size_t)np2 * 8, s>>>(Q, d, Qb, theta_glob, qperm);
+    note_launch();
 }
 
 __global__ void tile_xmax128(const float *__restrict__ xn, int64_t n, float *__restrict__ out) {
@@ -916,6 +966,7 @@ int launch_gt_filter_tc(const void *Xb, int64_t n, int d, int dp, const void *Qb
     a.part = mb ? mb->part : nullptr;
     a.R = mb ? mb->R : nullptr;
     a.perm = perm;
+    a.qperm = tl ? tl->qperm : nullptr;
     a.tlist = nullptr;
     a.tcount = nullptr;
     a.tstride = 0;
@@ -1027,7 +1078,7 @@ int launch_gt_filter_tc(const void *Xb, int64_t n, int d, int dp, const void *Qb
                                                 Qb, NT, tl->xmax128, theta_glob, qnorm, 2.0 * eps_rel,
                                                 tl->xsplit, two ? pass + 1 : 0,
                                                 const_cast<int32_t *>(a.tlist), a.tstride,
-                                                const_cast<int32_t *>(a.tcount), tl->pairs);
+                                                const_cast<int32_t *>(a.tcount), tl->pairs, a.qperm);
             note_launch();
         }
         if (lists && getenv("NRLSH_GT_TILESTATS")) {   // development: tiles kept per pair
