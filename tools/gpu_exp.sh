@@ -1,4 +1,5 @@
 mkdir -p gpurun_out
-(timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -2
-timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench.log 2>&1; echo bench rc=$?
+(timeout 900 python -m pytest tests -x -q -m gpu -k "candidates or coarse or fallback or query_parity" 2>&1 | tail -2
+timeout 300 python tools/run_stage.py query --reps 3 2>&1 | tail -1
+timeout 300 python tools/run_stage.py query --bits 32 --reps 3 2>&1 | tail -1
 ) > gpurun_out/exp.log 2>&1
