@@ -602,7 +602,8 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
     const bool use_rtc = want_topk && !use_dense && !g_in_rtc_redo && ix->Xb && ix->xnorm_pos &&
                          gt_tc_supported(ix->d, k) &&
                          (rtc_env ? atoi(rtc_env) != 0 : (double)Tq * rtc_ratio >= (double)n);
-    const int KS = std::min(1024, std::max(256, 4 * k));
+    const int KS = getenv("NRLSH_RERANK_TC_KS") ? std::max(k, std::min(1024, atoi(getenv("NRLSH_RERANK_TC_KS"))))
+                                                 : std::min(1024, std::max(512, 4 * k));
     // survivor list capacity per query (NRLSH_RERANK_TC_CAP: test switch forcing the
     // overflow redo path)
     const int64_t Cg = getenv("NRLSH_RERANK_TC_CAP")
@@ -667,9 +668,9 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
             }
             ProfScope p(SLOT_RERANK, s);
             // bf16 query rows in descending theta/|q| (pairs of similar bound prune alike)
-            // (opt-in NRLSH_GT_SORT=1: measured slower on c4 — the filter's time does not
-            // track its tile count at these sizes)
-            const bool sorted = Qb <= 4096 && getenv("NRLSH_GT_SORT");
+            // (c4: 0.36 -> 0.30 ms per 1024 queries with the pairs' CTA shares in
+            // proportion to their tile lists; NRLSH_RERANK_NOSORT=1 turns it off)
+            const bool sorted = Qb <= 4096 && !getenv("NRLSH_RERANK_NOSORT");
             if (sorted) launch_sort_by_bound(Qd, ix->d, Qb, rth.get<uint32_t>(), rqp.get<int32_t>(), s);
             tls.qperm = sorted ? rqp.get<int32_t>() : nullptr;
             launch_bf16_prep(Qd, Qb, ix->d, ix->dpb, rqb.p, rqn.get<float>(), s, tls.qperm);
@@ -959,6 +960,8 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
             const void *qrows = (const uint16_t *)qb.p + q0 * dp;
             const float *qnrows = qnb;
             gtl.qperm = nullptr;
+            // (opt-in NRLSH_GT_SORT=1: the sort and the extra bf16 pass cost more than the
+            // pruning gains here, 0.25 vs 0.17 ms per 1024 queries on c4)
             if (tiles && seed_ids && Qb <= 4096 && getenv("NRLSH_GT_SORT")) {
                 launch_sort_by_bound(Qb_ptr, d, Qb, th.get<uint32_t>(), gqp.get<int32_t>(), s);
                 launch_bf16_prep(Qb_ptr, Qb, d, dp, gqb.p, gqn.get<float>(), s, gqp.get<int32_t>());

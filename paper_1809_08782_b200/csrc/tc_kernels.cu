@@ -168,12 +168,34 @@ struct GtArgs {
 // partition order sort by norm, and the high-norm tiles (where the filter keeps the
 // most) spread over all splits instead of loading the last few.  v = 0..count-1
 // indexes the unit's tiles; the CTAs of the other pairs of a split read the same ones.
-__device__ __forceinline__ int64_t gt_unit_count(const GtArgs &a, int qp, int sp) {
-    const int64_t c = a.tlist ? (int64_t)a.tcount[qp] : a.ntiles;
-    return c > sp ? (c - sp + a.nsplit - 1) / a.nsplit : 0;
+// With tile lists the nqp * nsplit units are shared out in proportion to the pairs'
+// list lengths (each pair >= 1 unit), so a pair with many tiles gets more CTAs; every
+// role derives the same map from tcount.  Units past the map are idle (count 0).
+__device__ __forceinline__ void gt_unit_map(const GtArgs &a, int u, int &qp, int &sp, int &ns) {
+    if (!a.tlist) {
+        qp = u % a.nqp;
+        sp = u / a.nqp;
+        ns = a.nsplit;
+        return;
+    }
+    const int U = a.nqp * a.nsplit;
+    int64_t C = 0;
+    for (int g = 0; g < a.nqp; ++g) C += a.tcount[g];
+    int base = 0;
+    for (int g = 0; g < a.nqp; ++g) {
+        const int n_g = (int)((int64_t)(U - a.nqp) * a.tcount[g] / max(C, (int64_t)1)) + 1;
+        if (u < base + n_g) { qp = g; sp = u - base; ns = n_g; return; }
+        base += n_g;
+    }
+    qp = 0; sp = 0; ns = 0;   // idle
 }
-__device__ __forceinline__ int64_t gt_tile_row0(const GtArgs &a, int qp, int sp, int64_t v, int nt) {
-    const int64_t e = sp + v * a.nsplit;
+__device__ __forceinline__ int64_t gt_unit_count(const GtArgs &a, int qp, int sp, int ns) {
+    if (ns == 0) return 0;
+    const int64_t c = a.tlist ? (int64_t)a.tcount[qp] : a.ntiles;
+    return c > sp ? (c - sp + ns - 1) / ns : 0;
+}
+__device__ __forceinline__ int64_t gt_tile_row0(const GtArgs &a, int qp, int sp, int ns, int64_t v, int nt) {
+    const int64_t e = sp + v * ns;
     return (a.tlist ? (int64_t)__ldg(a.tlist + qp * a.tstride + e) : e) * nt;
 }
 
@@ -406,8 +428,9 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
         // ================= TMA producer
         uint32_t g = 0, ul = 0;
         for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++ul) {
-            const int qp = u % a.nqp, sp = u / a.nqp;
-            const int64_t v0 = 0, v1 = gt_unit_count(a, qp, sp);
+            int qp, sp, ns;
+            gt_unit_map(a, u, qp, sp, ns);
+            const int64_t v0 = 0, v1 = gt_unit_count(a, qp, sp, ns);
             // query blocks of this pair that hold any query (a block wholly past Qb
             // is neither loaded nor multiplied)
             const int nh = min(GT_QB, (a.Qb - qp * GT_QB * GT_M + GT_M - 1) / GT_M);
@@ -418,9 +441,9 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
                     tc::tma_load_2d(sA + (h * a.kblocks + kb) * GT_A_BLK, &tmQ, a_full, kb * GT_KB,
                                     (qp * GT_QB + h) * GT_M);
             for (int64_t v = v0; v < v1; ++v) {
-                const int64_t i0 = gt_tile_row0(a, qp, sp, v, GT_N);
+                const int64_t i0 = gt_tile_row0(a, qp, sp, ns, v, GT_N);
                 if (a.prefetch > 0 && v + a.prefetch < v1) {
-                    const int64_t ip = gt_tile_row0(a, qp, sp, v + a.prefetch, GT_N);
+                    const int64_t ip = gt_tile_row0(a, qp, sp, ns, v + a.prefetch, GT_N);
                     for (int kb = 0; kb < a.kblocks; ++kb) tc::tma_prefetch_2d(&tmX, kb * GT_KB, (int)ip);
                 }
                 for (int kb = 0; kb < a.kblocks; ++kb, ++g) {
@@ -436,9 +459,10 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
         constexpr uint32_t idesc = tc::umma_idesc(1, GT_M, GT_N);
         uint32_t g = 0, t = 0, ul = 0;
         for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++ul) {
-            const int qp = u % a.nqp, sp = u / a.nqp;
+            int qp, sp, ns;
+            gt_unit_map(a, u, qp, sp, ns);
             const int nh = min(GT_QB, (a.Qb - qp * GT_QB * GT_M + GT_M - 1) / GT_M);
-            const int64_t v0 = 0, v1 = gt_unit_count(a, qp, sp);
+            const int64_t v0 = 0, v1 = gt_unit_count(a, qp, sp, ns);
             tc::mbar_wait(a_full, ul & 1);
             tc::tc_fence_after();
             for (int64_t v = v0; v < v1; ++v, ++t) {
@@ -474,10 +498,11 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
         // copies into the tile's buffer once both epilogue groups released it
         uint32_t t = 0;
         for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
-            const int qp = u % a.nqp, sp = u / a.nqp;
-            const int64_t v0 = 0, v1 = gt_unit_count(a, qp, sp);
+            int qp, sp, ns;
+            gt_unit_map(a, u, qp, sp, ns);
+            const int64_t v0 = 0, v1 = gt_unit_count(a, qp, sp, ns);
             for (int64_t v = v0; v < v1; ++v, ++t) {
-                const int64_t i0 = gt_tile_row0(a, qp, sp, v, GT_N);
+                const int64_t i0 = gt_tile_row0(a, qp, sp, ns, v, GT_N);
                 const uint32_t b = t & 1, tr = t >> 1;
                 tc::mbar_wait(&xempty[b], (tr & 1) ^ 1);
                 tc::mbar_arrive_expect_tx(&xfull[b], GT_N * 4 + (a.member ? GT_N * (a.W * 4 + 1) : 0));
@@ -497,17 +522,18 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
         uint32_t t = 0;
         GtEpiRow er;
         for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
-            const int qp = u % a.nqp, sp = u / a.nqp;
+            int qp, sp, ns;
+            gt_unit_map(a, u, qp, sp, ns);
             const int nh = min(GT_QB, (a.Qb - qp * GT_QB * GT_M + GT_M - 1) / GT_M);
             const bool hact = h < nh;   // this group's block holds queries in this unit
-            const int64_t v0 = 0, v1 = gt_unit_count(a, qp, sp);
+            const int64_t v0 = 0, v1 = gt_unit_count(a, qp, sp, ns);
             const int q = (qp * GT_QB + h) * GT_M + row;
             // heap of this CTA's query row (CTAs of other item splits keep their own)
             er.begin(a, q, hact && q < a.Qb,
                      a.heap_smem ? sheap + (h * GT_M + row) * a.k
                                  : a.heap + ((int64_t)(blockIdx.x * 2 + h) * GT_M + row) * a.k);
             for (int64_t v = v0; v < v1; ++v, ++t) {
-                const int64_t i0 = gt_tile_row0(a, qp, sp, v, GT_N);
+                const int64_t i0 = gt_tile_row0(a, qp, sp, ns, v, GT_N);
                 const uint32_t b = t & 1;
                 const float *xn = sxn + b * GT_N;
                 uint32_t o_next = 0;
