@@ -897,15 +897,17 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
                               : std::min<int64_t>(n, std::max<int64_t>(4 * (int64_t)S * k + 4096, 2 * k));
     int Qmax = (int)std::min<int64_t>(1024, nq);
     while (Qmax > 64 && (int64_t)Qmax * (ns * 4 + Cg * 8) > ((int64_t)2500 << 20)) Qmax >>= 1;
-    DBuf xn, qn, ss, lb, tid, tsc, cc, cd, cs, xb, qb, th, pt, hp, tw, gqp, gqb, gqn;
+    DBuf xn, qn, ss, lb, tid, tsc, cc, cd, cs, xb, qb, th, pt, hp, tw, gqp, gqb, gqn, gst, gov;
     const int64_t npad = (n + 255) / 256 * 256;   // |x| padded: the tc kernel bulk-loads 1 KB tiles
     if (xn.alloc((size_t)npad * 4, s) || qn.alloc((size_t)nq * 4, s) ||
         ss.alloc((size_t)Qmax * ns * 4, s) || lb.alloc((size_t)Qmax * 4, s) ||
         tid.alloc((size_t)Qmax * k * 8, s) || tsc.alloc((size_t)Qmax * k * 4, s) ||
         cc.alloc((size_t)Qmax * 4, s) || cd.alloc((size_t)Qmax * Cg * 4, s) ||
         cs.alloc((size_t)Qmax * Cg * 4, s) || th.alloc((size_t)Qmax * 4, s) ||
-        pt.alloc(std::max(rerank_partial_bytes(Qmax, Cg, k), rerank_partial_bytes(1, n, k)), s))
+        pt.alloc(std::max(rerank_partial_bytes(Qmax, Cg, k), rerank_partial_bytes(1, n, k)), s) ||
+        gst.alloc(32, s) || gov.alloc((size_t)nq * 8, s))
         return fail(NRLSH_ENOMEM, "exact_topk workspace");
+    cudaMemsetAsync(gst.p, 0, 32, s);
     // bf16 item rows and |x|: the index's (written by its build), else prepared here
     const void *Xbp = Xb_ix;
     const float *xnp = xnorm_ix;
@@ -938,7 +940,6 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
     gtl.xsplit = getenv("NRLSH_GT_ONEPASS") ? 0.f : xsplit_ix;
     gtl.pass = 0;
     gtl.qperm = nullptr;
-    std::vector<uint32_t> hcnt(Qmax);
     for (int64_t q0 = 0; q0 < nq; q0 += Qmax) {
         const int Qb = (int)std::min<int64_t>(Qmax, nq - q0);
         const float *Qb_ptr = Q + q0 * d;
@@ -1007,17 +1008,27 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
             launch_rerank(X, d, d, Qb_ptr, Qb, cd.get<int32_t>(), Cg, Cg, cc.get<uint32_t>(), 1, k,
                           pt.get<unsigned long long>(), oid, osc, s);
         }
-        // overflowing queries (rare): exact scoring of every item
-        cudaMemcpyAsync(hcnt.data(), cc.p, (size_t)Qb * 4, cudaMemcpyDeviceToHost, s);
+        // survivor statistics and overflowing queries, collected on the device (no
+        // host round trip per sub-batch)
+        launch_count_stats(cc.get<uint32_t>(), Qb, gst.get<unsigned long long>(), s);
+        launch_collect_overflow(cc.get<uint32_t>(), Qb, Cg, q0, gov.get<int64_t>(),
+                                (uint32_t *)(gst.get<unsigned long long>() + 2), s);
+    }
+    {   // overflowing queries (rare): exact scoring of every item
+        unsigned long long hst[3];
+        cudaMemcpyAsync(hst, gst.p, 24, cudaMemcpyDeviceToHost, s);
         if ((e = cudaStreamSynchronize(s))) return cuda_fail(e, "exact_topk");
-        for (int qi = 0; qi < Qb; ++qi) {
-            g_last_gt_max_cand = std::max<int64_t>(g_last_gt_max_cand, hcnt[qi]);
-            g_last_gt_sum_cand += hcnt[qi];
-            if (hcnt[qi] <= (uint32_t)Cg) continue;
-            ++g_last_gt_overflow;
-            launch_rerank(X, d, d, Qb_ptr + (int64_t)qi * d, 1, nullptr, n, n, nullptr, 1, k,
-                          pt.get<unsigned long long>(), oid + (int64_t)qi * k,
-                          osc + (int64_t)qi * k, s);
+        g_last_gt_max_cand = (int64_t)hst[0];
+        g_last_gt_sum_cand = (int64_t)hst[1];
+        const uint32_t nov = (uint32_t)hst[2];
+        g_last_gt_overflow = nov;
+        if (nov) {
+            std::vector<int64_t> ql(nov);
+            cudaMemcpy(ql.data(), gov.p, (size_t)nov * 8, cudaMemcpyDeviceToHost);
+            for (int64_t qi : ql)
+                launch_rerank(X, d, d, Q + qi * d, 1, nullptr, n, n, nullptr, 1, k,
+                              pt.get<unsigned long long>(), (int64_t *)oi.dev + qi * k,
+                              (float *)os.dev + qi * k, s);
         }
     }
     if ((e = oi.finish(s)) || (e = os.finish(s))) return cuda_fail(e, "copy results");

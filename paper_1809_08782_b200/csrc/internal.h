@@ -203,6 +203,8 @@ void launch_theta_from_topk(const int64_t *ids, const float *scores, int Qb, int
 // *out += sum_q min(cnt[q], C)
 void launch_sum_counts(const uint32_t *cnt, int Qb, int64_t C, unsigned long long *out,
                        cudaStream_t s);
+// out[0] = max(out[0], max_q cnt[q]); out[1] += sum_q cnt[q]
+void launch_count_stats(const uint32_t *cnt, int Qb, unsigned long long *out, cudaStream_t s);
 // appends q0 + q to list (count at *n) for every q with cnt[q] > C
 void launch_collect_overflow(const uint32_t *cnt, int Qb, int64_t C, int64_t q0, int64_t *list,
                              uint32_t *n, cudaStream_t s);

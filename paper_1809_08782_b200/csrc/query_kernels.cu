@@ -188,6 +188,10 @@ void launch_pilot(const nrlsh_index *ix, const uint32_t *qcodes, int Qb, int64_t
     double target = (double)Tq;
     if (stride > 1) target += 4.0 * sqrt((double)Tq * stride) + stride;
     uint32_t need = (uint32_t)ceil(target / stride);
+    // a few sampled items make a noisy bound: with T tiny the sampled count at the
+    // bound is a handful and a query now and then under-shoots into the (slow) exact
+    // fallback; 16 sampled items keep that rare at little extra scan cost
+    if (stride > 1 && need < 16) need = 16;
     if (need < 1) need = 1;
     const int NR = ix->m * (ix->L + 1);
     const size_t sm = (size_t)NR * 4;
@@ -740,6 +744,29 @@ __global__ void sum_counts(const uint32_t *__restrict__ cnt, int Qb, int64_t C,
 void launch_sum_counts(const uint32_t *cnt, int Qb, int64_t C, unsigned long long *out,
                        cudaStream_t s) {
     sum_counts<<<1, 256, 0, s>>>(cnt, Qb, C, out);
+    note_launch();
+}
+
+__global__ void count_stats(const uint32_t *__restrict__ cnt, int Qb,
+                            unsigned long long *__restrict__ out) {
+    unsigned long long mx = 0, sm = 0;
+    for (int q = threadIdx.x; q < Qb; q += blockDim.x) {
+        mx = max(mx, (unsigned long long)cnt[q]);
+        sm += cnt[q];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        mx = max(mx, __shfl_xor_sync(NR_FULL, mx, o));
+        sm += __shfl_xor_sync(NR_FULL, sm, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(out, mx);
+        atomicAdd(out + 1, sm);
+    }
+}
+
+void launch_count_stats(const uint32_t *cnt, int Qb, unsigned long long *out, cudaStream_t s) {
+    count_stats<<<1, 256, 0, s>>>(cnt, Qb, out);
     note_launch();
 }
 
