@@ -400,9 +400,12 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
     {
         const int stride = pilot_stride(n);
         if (stride > 1) {
-            ix->nsamp = (n + stride - 1) / stride;
+            // (interleaved slots: 32 columns of ceil(samples / 32); unused slots get
+            // sub-dataset 255, which no histogram bin takes)
+            ix->nsamp = ((n + stride - 1) / stride + 31) / 32 * 32;
             NR_ALLOC(ix->samp_codes, (size_t)ix->nsamp * W * 4);
             NR_ALLOC(ix->samp_part, (size_t)ix->nsamp);
+            cudaMemsetAsync(ix->samp_part, 0xff, (size_t)ix->nsamp, s);
             ProfScope p(SLOT_CODES, s);
             launch_gather_sample(ix.get(), stride, ix->samp_codes, ix->samp_part, s);
         }

@@ -88,12 +88,13 @@ __device__ __forceinline__ void load_code(const uint32_t *__restrict__ codes, in
 // count reaches `need` (in histogram units).  Returns r (NR-1 if never reached)
 // and the count strictly before r in *cum_lt.  Lanes holding the same bin add
 // once (match_any), which turns most shared atomics of a warp into one.
-template <int W>
+template <int W, bool AGG = true>
 __device__ void hist_and_bound(const uint32_t *__restrict__ codes,
                                const uint8_t *__restrict__ part, int64_t ns,
                                const uint32_t (&qc)[W], int L, int NR,
                                const int32_t *__restrict__ order, uint32_t *hist, uint32_t need,
-                               uint32_t *ws, int *sB, uint32_t *sLt) {
+                               uint32_t *ws, int *sB, uint32_t *sLt, int64_t per = 0,
+                               int64_t ns_real = 0) {
     for (int e = threadIdx.x; e < NR; e += blockDim.x) hist[e] = 0u;
     if (threadIdx.x == 0) { *sB = NR - 1; *sLt = 0u; }
     __syncthreads();
@@ -101,13 +102,18 @@ __device__ void hist_and_bound(const uint32_t *__restrict__ codes,
     for (int64_t b0 = 0; b0 < ns; b0 += blockDim.x) {
         const int64_t t = b0 + threadIdx.x;
         int bin = -1;
-        if (t < ns) {
+        // (interleaved sample: slot t holds sample (t % per) * 32 + t / per, if any)
+        if (t < ns && (per == 0 || (t % per) * 32 + t / per < ns_real)) {
             uint32_t c[W];
             load_code<W>(codes, t, c);
             bin = (int)part[t] * (L + 1) + hamming<W>(c, qc);
         }
-        const unsigned peers = __match_any_sync(NR_FULL, bin);
-        if (bin >= 0 && lane == __ffs(peers) - 1) atomicAdd(&hist[bin], (uint32_t)__popc(peers));
+        if (AGG) {
+            const unsigned peers = __match_any_sync(NR_FULL, bin);
+            if (bin >= 0 && lane == __ffs(peers) - 1) atomicAdd(&hist[bin], (uint32_t)__popc(peers));
+        } else if (bin >= 0) {
+            atomicAdd(&hist[bin], 1u);
+        }
     }
     __syncthreads();
     const int seg = (NR + blockDim.x - 1) / blockDim.x;
@@ -134,12 +140,16 @@ template <int W>
 __global__ void gather_sample(const uint32_t *__restrict__ codes, const uint8_t *__restrict__ part,
                               int64_t ns, int stride, uint32_t *__restrict__ sc,
                               uint8_t *__restrict__ sp) {
+    // sample t (position t * stride) goes to slot (t % 32) * per + t / 32: the 32
+    // slots a warp reads together come from positions ~n/32 apart
+    const int64_t per = (ns + 31) / 32;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ns;
          t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t p = t * stride;
+        const int64_t slot = (t % 32) * per + t / 32;
 #pragma unroll
-        for (int w = 0; w < W; ++w) sc[t * W + w] = codes[p * W + w];
-        sp[t] = part[p];
+        for (int w = 0; w < W; ++w) sc[slot * W + w] = codes[p * W + w];
+        sp[slot] = part[p];
     }
 }
 
@@ -161,7 +171,7 @@ __global__ void __launch_bounds__(1024) k6_pilot(
     const uint32_t *__restrict__ codes, const uint8_t *__restrict__ part_of_pos, int64_t n,
     const uint32_t *__restrict__ qcodes, int L, int m,
     const int32_t *__restrict__ order, const uint16_t *__restrict__ R, uint32_t need,
-    int8_t *__restrict__ delta, uint32_t *__restrict__ cnt) {
+    int8_t *__restrict__ delta, uint32_t *__restrict__ cnt, int interleaved, int64_t ns_real) {
     extern __shared__ uint32_t hist[];
     __shared__ uint32_t ws[32];
     __shared__ int sB;
@@ -171,7 +181,13 @@ __global__ void __launch_bounds__(1024) k6_pilot(
     uint32_t qc[W];
 #pragma unroll
     for (int w = 0; w < W; ++w) qc[w] = qcodes[q * W + w];
-    hist_and_bound<W>(codes, part_of_pos, n, qc, L, NR, order, hist, need, ws, &sB, &sLt);
+    // the compacted sample is stored interleaved (neighbouring slots from distant
+    // sub-datasets), so a warp's bins rarely collide and plain shared atomics beat
+    // the match_any aggregation the full-data fallback needs
+    if (interleaved)
+        hist_and_bound<W, false>(codes, part_of_pos, n, qc, L, NR, order, hist, need, ws, &sB, &sLt,
+                                 n / 32, ns_real);
+    else hist_and_bound<W>(codes, part_of_pos, n, qc, L, NR, order, hist, need, ws, &sB, &sLt);
     const int B = sB;
     for (int j = threadIdx.x; j < m; j += blockDim.x) {
         int c = 0;
@@ -204,15 +220,15 @@ void launch_pilot(const nrlsh_index *ix, const uint32_t *qcodes, int Qb, int64_t
     switch (ix->W) {
         case 1:
             cudaFuncSetAttribute(k6_pilot<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            k6_pilot<1><<<Qb, 1024, sm, s>>>(sc, sp, ns, qcodes, ix->L, ix->m, order, ix->R_d, need, delta, cnt);
+            k6_pilot<1><<<Qb, 1024, sm, s>>>(sc, sp, ns, qcodes, ix->L, ix->m, order, ix->R_d, need, delta, cnt, cmp, (ix->n + stride - 1) / stride);
             break;
         case 2:
             cudaFuncSetAttribute(k6_pilot<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            k6_pilot<2><<<Qb, 1024, sm, s>>>(sc, sp, ns, qcodes, ix->L, ix->m, order, ix->R_d, need, delta, cnt);
+            k6_pilot<2><<<Qb, 1024, sm, s>>>(sc, sp, ns, qcodes, ix->L, ix->m, order, ix->R_d, need, delta, cnt, cmp, (ix->n + stride - 1) / stride);
             break;
         default:
             cudaFuncSetAttribute(k6_pilot<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            k6_pilot<4><<<Qb, 1024, sm, s>>>(sc, sp, ns, qcodes, ix->L, ix->m, order, ix->R_d, need, delta, cnt);
+            k6_pilot<4><<<Qb, 1024, sm, s>>>(sc, sp, ns, qcodes, ix->L, ix->m, order, ix->R_d, need, delta, cnt, cmp, (ix->n + stride - 1) / stride);
             break;
     }
     note_launch();
