@@ -55,7 +55,10 @@ def parse():
     ap.add_argument("--nq", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-latency", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--sweep-m", action="store_true",
+                    help="with --sweep: m in {1,32,64,128,256} at the paper's bit accounting")
     ap.add_argument("--sweep", default=None,
                     help="comma-separated configs: per probe budget queries/s and recall@k "
                          "(no driver line; writes --sweep-out)")
@@ -163,7 +166,12 @@ def roofline_for(slot, ms_total, count, info, peaks, peaks_src):
                 "achieved": ach / 1e12, "peak": POPC_PEAK_PER_S / 1e12, "unit": "TPOPC/s",
                 "frac": ach / POPC_PEAK_PER_S, "traffic": traffic,
                 "peak_source": "tools/ubench.cu measured POPC rate (profiles/r01/ubench_popc.txt)",
-                "logical_pairs_per_s": nq * n / (ms_total / 1e3)}
+                "logical_pairs_per_s": nq * n * steps / (ms_total / 1e3),
+                # SURVEY §8(d) "code-scan GB/s": code bytes compared (all n items per query)
+                # and the codes actually scanned (skipped sub-datasets excluded), per second
+                "code_scan_logical_gbs": nq * n * steps * L / 8 / (ms_total / 1e3) / 1e9,
+                "code_scan_actual_gbs": info["scanned_pairs"] * L / 8 / (ms_total / 1e3) / 1e9,
+                "dram_gbs": (traffic / per_launch_s / 1e9) if traffic else None}
     if slot == "gt_filter" or (slot == "rerank" and info.get("rerank_path") == "tensor"):
         # one bf16 pass over every item per query; the re-rank's member-mode pass
         # multiplies only the tiles of sub-datasets holding candidates (its own count)
@@ -392,6 +400,35 @@ def run_native(args):
     rec = float(np.mean([len(set(a.tolist()) & set(b.tolist())) / k for a, b in zip(ids_h, gid_h)]))
 
     # -------- end to end through the public API with HOST buffers (pinned)
+    # latency mode: 1 and 2 queries per call, index resident; the scan
+    # is then bound by streaming the codes of the probed sub-datasets from HBM
+    latency = []
+    if not args.no_latency:
+        idx = P.Index(Xd, L, m, seed=cfg.seed, query_batch=cfg.query_batch)
+        for nql in (1, 2):
+            Ql = Qd[:nql].contiguous()
+            for _ in range(3):
+                idx.query(Ql, k, T)
+            P.profile_read(reset=True)
+            P.profile_enable(True)
+            ts = []
+            for _ in range(20):
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                idx.query(Ql, k, T)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            P.profile_enable(False)
+            pr = P.profile_read(reset=True)
+            qs = P.last_query_stats()
+            scan_ms = pr["scan"][0] / max(1, pr["scan"][1])
+            latency.append({"nq": nql, "ms_median": float(np.median(ts)),
+                            "scan_ms": scan_ms,
+                            "code_scan_actual_gbs": qs["scanned_pairs"] * L / 8 / (scan_ms / 1e3) / 1e9,
+                            "code_scan_logical_gbs": nql * cfg.n * L / 8 / (scan_ms / 1e3) / 1e9})
+        idx.close()
     e2e = None
     if not args.no_e2e:
         Xh = torch.from_numpy(X).pin_memory()
@@ -459,6 +496,7 @@ def run_native(args):
         "stage_ms_per_step": stage,
         "roofline": roof, "scan_roofline": scan_roof, "other_rooflines": others,
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+        "latency_mode": latency,
         "clocks": clocks,
         "notes": {"input_gen_s": t_gen, "peaks": peaks_src,
                   "step_ms_all": ms, "rerank_path": rerank_path,
@@ -470,15 +508,23 @@ def run_native(args):
         dist.destroy_process_group()
 
 
-def _sweep_plan(cfg):
-    """(code_bits, num_parts, budgets) runs of a config: its stated budgets plus the
-    paper's 2^i probe grid (Fig. 2 x-axis) where BASELINE.json asks
-    for recall curves (c3, c4)."""
+def _sweep_plan(cfg, m_sweep=False):
+    """(code_bits, num_parts, budgets, index_bits_in_budget) runs of a config: its
+    stated budgets plus the paper's 2^i probe grid (Fig. 2 x-axis)
+    where BASELINE.json asks for recall curves (c3, c4).  m_sweep (SURVEY §8(f)
+    NEXT-1): m = 1 (SIMPLE-LSH) against m in {32, 64, 128, 256} at the paper's bit
+    accounting, L_h = code_bits - ceil(log2 m)."""
+    Ts = sorted(set(cfg.budget_list()) | set(t for t in cfg.extra_T if t <= cfg.n))
     runs = []
+    if m_sweep:
+        for L in cfg.code_bits:
+            for m in (1, 32, 64, 128, 256):
+                if m <= cfg.n:
+                    runs.append((L, m, Ts, True))
+        return runs
     for L in cfg.code_bits:
         for m in cfg.num_parts:
-            Ts = sorted(set(cfg.budget_list()) | set(t for t in cfg.extra_T if t <= cfg.n))
-            runs.append((L, m, Ts))
+            runs.append((L, m, Ts, False))
     return runs
 
 
@@ -497,11 +543,12 @@ def run_sweep(args):
         Qd = torch.from_numpy(Q).to(dev)
         k = cfg.k
         gt = None
-        for L, m, Ts in _sweep_plan(cfg):
+        for L, m, Ts, ibits in _sweep_plan(cfg, args.sweep_m):
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            idx = P.Index(Xd, L, m, seed=cfg.seed, query_batch=cfg.query_batch)
+            idx = P.Index(Xd, L, m, seed=cfg.seed, query_batch=cfg.query_batch,
+                          index_bits_in_budget=ibits)
             e1.record()
             torch.cuda.synchronize()
             build_ms = e0.elapsed_time(e1)
@@ -521,6 +568,7 @@ def run_sweep(args):
                 rec = float(np.mean([len(set(a.tolist()) & set(b.tolist())) / k
                                      for a, b in zip(ids, gt)]))
                 row = {"config": name, "n": cfg.n, "d": cfg.d, "code_bits": L, "num_parts": m,
+                       "hash_bits": idx.hash_bits, "index_bits_in_budget": ibits,
                        "nq": len(Q), "k": k, "probe_budget": int(T), "budget_frac": T / cfg.n,
                        "queries_per_s": len(Q) / (float(np.median(ms)) / 1e3),
                        "query_ms": float(np.median(ms)), "recall_at_k": rec,
