@@ -464,7 +464,7 @@ void run_candidates(const nrlsh_index *ix, const float *Qd, const uint32_t *qcod
                     unsigned long long *buf, int32_t *cand, uint16_t *cand_rank, int *flags,
                     unsigned long long *pairs, cudaStream_t s, uint32_t *sel_B = nullptr,
                     uint32_t *sel_pk = nullptr, uint32_t *cnt_part = nullptr,
-                    int32_t *seeds = nullptr, int ks = 0) {
+                    int32_t *seeds = nullptr, int ks = 0, void *fb_ws = nullptr) {
     if (qcodes_in) {
         cudaMemcpyAsync(qcodes, qcodes_in + qbase * ix->W, (size_t)Qb * ix->W * 4,
                         cudaMemcpyDeviceToDevice, s);
@@ -493,7 +493,7 @@ void run_candidates(const nrlsh_index *ix, const float *Qd, const uint32_t *qcod
     }
     {
         ProfScope p(SLOT_FALLBACK, s);
-        launch_fallback(ix, qcodes, Qb, Tq, buf, cnt, tc ? cntv : cnt, C, flags, s);
+        launch_fallback(ix, qcodes, Qb, Tq, buf, cnt, tc ? cntv : cnt, C, flags, fb_ws, s);
     }
     {
         ProfScope p(SLOT_SELECT, s);
@@ -574,14 +574,16 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
         if ((e = oc.init(cand_out, (size_t)nq * Tq * 4, s))) return cuda_fail(e, "cand_ids");
         if (rank_out && (e = orr.init(rank_out, (size_t)nq * Tq * 2, s))) return cuda_fail(e, "cand_rank");
     }
-    DBuf qc, dl, cn, cv, ba, bf, cd, pt, fl;
+    DBuf qc, dl, cn, cv, ba, bf, cd, pt, fl, fbw;
     if (qc.alloc((size_t)Qmax * ix->W * 4, s) || dl.alloc((size_t)Qmax * ix->m, s) ||
         cn.alloc((size_t)Qmax * 4, s) || cv.alloc((size_t)Qmax * 4, s) ||
         ba.alloc(scan_tc_supported(ix) ? scan_tc_ws_bytes(ix, Qmax) : 16, s) ||
         bf.alloc((size_t)Qmax * C * 8, s) ||
         cd.alloc((size_t)Qmax * Tq * 4, s) ||
-        pt.alloc(want_topk ? rerank_partial_bytes(Qmax, Tq, k) : 0, s) || fl.alloc(40, s))
+        pt.alloc(want_topk ? rerank_partial_bytes(Qmax, Tq, k) : 0, s) || fl.alloc(40, s) ||
+        fbw.alloc(fallback_ws_bytes(ix), s))
         return fail(NRLSH_ENOMEM, "query workspace");
+    cudaMemsetAsync(fbw.p, 0, fallback_ws_bytes(ix), s);   // (histogram rows stay zero between uses)
     // dense re-rank of the sub-datasets most of whose pairs are candidates (rerank_dense.cu)
     const float *Xr = ix->Xpad ? ix->Xpad : ix->X;
     const int ldr = ix->Xpad ? ix->dpad : ix->d;
@@ -657,7 +659,7 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
                        use_dense ? sb.get<uint32_t>() : (use_rtc ? rsb.get<uint32_t>() : nullptr),
                        use_dense ? spk.get<uint32_t>() : (use_rtc ? rspk.get<uint32_t>() : nullptr),
                        use_dense ? cpart.get<uint32_t>() : nullptr,
-                       use_rtc ? rseed.get<int32_t>() : nullptr, KS);
+                       use_rtc ? rseed.get<int32_t>() : nullptr, KS, fbw.p);
         if (use_rtc) {
             {
                 ProfScope p(SLOT_SCORE, s);

@@ -133,9 +133,12 @@ void launch_scan(const nrlsh_index *ix, const uint32_t *qcodes, const int8_t *de
                  unsigned long long *pairs, cudaStream_t s);
 // cntv: entries of the buffer that are real (the tensor-core scan pads append
 // chunks with ~0 sentinels); == cnt for the popcount scan
+// ws: fallback_ws_bytes() of zeroed scratch for the all-SM re-do of failed queries
+// (nullptr: one CTA per failed query only)
+size_t fallback_ws_bytes(const nrlsh_index *ix);
 void launch_fallback(const nrlsh_index *ix, const uint32_t *qcodes, int Qb, int64_t Tq,
-                     unsigned long long *buf, uint32_t *cnt, const uint32_t *cntv, int64_t C,
-                     int *flags, cudaStream_t s);
+                     unsigned long long *buf, uint32_t *cnt, uint32_t *cntv, int64_t C,
+                     int *flags, void *ws, cudaStream_t s);
 // tensor-core Hamming scan (scan_tc.cu): +-1 int8 item codes expanded at build
 int scan_kp(int L);
 void launch_expand_pm(const uint32_t *codes, int64_t rows, int W, int L, int8_t *out, cudaStream_t s);

@@ -405,7 +405,7 @@ __global__ void __launch_bounds__(1024) k6_fallback(
     const int q = blockIdx.x;
     const uint32_t c0 = cnt[q], cv = cntv[q];
     if (cv >= (uint64_t)Tq && c0 <= (uint64_t)C) return;
-    if (threadIdx.x == 0) atomicAdd(&flags[2], 1);
+    if (threadIdx.x == 0 && flags) atomicAdd(&flags[2], 1);
     const int NR = m * (L + 1);
     uint32_t qc[W];
 #pragma unroll
@@ -438,24 +438,195 @@ __global__ void __launch_bounds__(1024) k6_fallback(
     if (threadIdx.x == 0) cnt[q] = (uint32_t)Tq;
 }
 
+// ---------------------------------------------------------------- parallel fallback
+// Queries whose pilot bound under- or overshot are re-done exactly by all SMs at once
+// (the one-CTA-per-query k6_fallback takes ~4.5 ms for a query on c4): an exact
+// histogram of the structure positions over all n items (slices of n per CTA,
+// flushed to a per-query global histogram), the exact bound B, then every item with
+// R <= B appended — the select resolves the ties at B as usual (the buffer holds
+// them: count(< B) < T and the cell at B is at most one sub-dataset, C covers both).
+// Persistent grids over a device-side list of the failed queries: nothing to do
+// costs three near-empty launches.
+constexpr int kFbSlices = 32;
+constexpr int kFbMax = 64;   // failed queries handled per sub-batch this way
+
+__global__ void fb_list(const uint32_t *__restrict__ cnt, const uint32_t *__restrict__ cntv, int Qb,
+                        int64_t Tq, int64_t C, int32_t *__restrict__ fl, uint32_t *__restrict__ nf,
+                        int *__restrict__ flags) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= Qb) return;
+    const uint32_t v = cntv ? cntv[q] : cnt[q];
+    if ((uint64_t)v >= (uint64_t)Tq && (uint64_t)cnt[q] <= (uint64_t)C) return;
+    atomicAdd(&flags[2], 1);   // counted here; the serial kernel then counts nothing
+    const uint32_t i = atomicAdd(nf, 1u);
+    if (i < (uint32_t)kFbMax) fl[i] = q;
+}
+
+template <int W>
+__global__ void __launch_bounds__(1024) fb_hist(const uint32_t *__restrict__ codes,
+                                                const uint8_t *__restrict__ part, int64_t n,
+                                                const uint32_t *__restrict__ qcodes, int L, int NR,
+                                                const uint16_t *__restrict__ R,
+                                                const int32_t *__restrict__ fl, const uint32_t *__restrict__ nf,
+                                                uint32_t *__restrict__ ghist) {
+    extern __shared__ uint32_t hist[];
+    const int nfl = (int)min(*nf, (uint32_t)kFbMax);
+    const int lane = threadIdx.x & 31;
+    for (int w = blockIdx.x; w < nfl * kFbSlices; w += gridDim.x) {
+        const int fi = w / kFbSlices, sl = w % kFbSlices;
+        const int q = fl[fi];
+        uint32_t qc[W];
+#pragma unroll
+        for (int k = 0; k < W; ++k) qc[k] = qcodes[q * W + k];
+        for (int e = threadIdx.x; e < NR; e += blockDim.x) hist[e] = 0u;
+        __syncthreads();
+        const int64_t p0 = n * sl / kFbSlices, p1 = n * (sl + 1) / kFbSlices;
+        for (int64_t b0 = p0; b0 < p1; b0 += blockDim.x) {
+            const int64_t p = b0 + threadIdx.x;
+            int r = -1;
+            if (p < p1) {
+                uint32_t c[W];
+                load_code<W>(codes, p, c);
+                r = R[part[p] * (L + 1) + hamming<W>(c, qc)];
+            }
+            const unsigned peers = __match_any_sync(NR_FULL, r);
+            if (r >= 0 && lane == __ffs(peers) - 1) atomicAdd(&hist[r], (uint32_t)__popc(peers));
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < NR; e += blockDim.x)
+            if (hist[e]) atomicAdd(&ghist[(int64_t)fi * NR + e], hist[e]);
+        __syncthreads();
+    }
+}
+
+// exact bound per failed query; clears its histogram row and its buffer counters
+__global__ void __launch_bounds__(1024) fb_bound(const int32_t *__restrict__ fl,
+                                                 const uint32_t *__restrict__ nf, int NR, int64_t Tq,
+                                                 uint32_t *__restrict__ ghist, uint32_t *__restrict__ Bout,
+                                                 uint32_t *__restrict__ cnt, uint32_t *__restrict__ cntv) {
+    __shared__ uint32_t ws[32];
+    __shared__ int sB;
+    const int nfl = (int)min(*nf, (uint32_t)kFbMax);
+    for (int fi = blockIdx.x; fi < nfl; fi += gridDim.x) {
+        uint32_t *h = ghist + (int64_t)fi * NR;
+        if (threadIdx.x == 0) sB = NR - 1;
+        __syncthreads();
+        const int seg = (NR + blockDim.x - 1) / blockDim.x;
+        const int r0 = threadIdx.x * seg, r1 = min(NR, r0 + seg);
+        uint32_t loc = 0;
+        for (int r = r0; r < r1; ++r) loc += h[r];
+        uint32_t tot;
+        const uint32_t ex = block_excl_scan(loc, ws, &tot);
+        if (ex < (uint64_t)Tq && ex + loc >= (uint64_t)Tq) {
+            uint32_t cc = ex;
+            for (int r = r0; r < r1; ++r) {
+                if (cc + h[r] >= (uint64_t)Tq) { sB = r; break; }
+                cc += h[r];
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            Bout[fi] = (uint32_t)sB;
+            cnt[fl[fi]] = 0u;
+            if (cntv) cntv[fl[fi]] = 0u;
+        }
+        for (int r = threadIdx.x; r < NR; r += blockDim.x) h[r] = 0u;
+        __syncthreads();
+    }
+}
+
+template <int W>
+__global__ void __launch_bounds__(1024) fb_take(const uint32_t *__restrict__ codes,
+                                                const uint8_t *__restrict__ part, int64_t n,
+                                                const uint32_t *__restrict__ qcodes, int L,
+                                                const uint16_t *__restrict__ R,
+                                                const int32_t *__restrict__ fl, const uint32_t *__restrict__ nf,
+                                                const uint32_t *__restrict__ Bq,
+                                                unsigned long long *__restrict__ buf, uint32_t *__restrict__ cnt,
+                                                uint32_t *__restrict__ cntv, int64_t C) {
+    const int nfl = (int)min(*nf, (uint32_t)kFbMax);
+    const int lane = threadIdx.x & 31;
+    for (int w = blockIdx.x; w < nfl * kFbSlices; w += gridDim.x) {
+        const int fi = w / kFbSlices, sl = w % kFbSlices;
+        const int q = fl[fi];
+        const uint32_t B = Bq[fi];
+        uint32_t qc[W];
+#pragma unroll
+        for (int k = 0; k < W; ++k) qc[k] = qcodes[q * W + k];
+        const int64_t p0 = n * sl / kFbSlices, p1 = n * (sl + 1) / kFbSlices;
+        uint32_t mine = 0;
+        for (int64_t b0 = p0; b0 < p1; b0 += blockDim.x) {
+            const int64_t p = b0 + threadIdx.x;
+            bool take = false;
+            uint32_t f = 0;
+            if (p < p1) {
+                uint32_t c[W];
+                load_code<W>(codes, p, c);
+                f = part[p] * (L + 1) + hamming<W>(c, qc);
+                take = R[f] <= B;
+            }
+            const unsigned bal = __ballot_sync(NR_FULL, take);
+            if (!bal) continue;
+            uint32_t base = 0;
+            if (lane == 0) base = atomicAdd(&cnt[q], (uint32_t)__popc(bal));
+            base = __shfl_sync(NR_FULL, base, 0);
+            if (take) {
+                const uint32_t slot = base + __popc(bal & lanemask_lt());
+                if (slot < C) buf[(int64_t)q * C + slot] = ((unsigned long long)f << 32) | (uint32_t)p;
+                ++mine;
+            }
+        }
+        if (mine && cntv) atomicAdd(&cntv[q], mine);
+    }
+}
+
+size_t fallback_ws_bytes(const nrlsh_index *ix) {
+    return ((size_t)kFbMax * ix->m * (ix->L + 1) + 2 * kFbMax + 64) * 4;
+}
+
 void launch_fallback(const nrlsh_index *ix, const uint32_t *qcodes, int Qb, int64_t Tq,
-                     unsigned long long *buf, uint32_t *cnt, const uint32_t *cntv, int64_t C,
-                     int *flags, cudaStream_t s) {
+                     unsigned long long *buf, uint32_t *cnt, uint32_t *cntv, int64_t C,
+                     int *flags, void *ws, cudaStream_t s) {
     const int NR = ix->m * (ix->L + 1);
+    const bool par = ws && !getenv("NRLSH_FALLBACK_SERIAL");
+    if (par) {
+        uint32_t *cv_sep = cntv != cnt ? cntv : nullptr;   // (popcount scan: cntv is cnt)
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+        uint32_t *ghist = reinterpret_cast<uint32_t *>(ws);   // [kFbMax x NR], zero between uses
+        int32_t *fl = reinterpret_cast<int32_t *>(ghist + (size_t)kFbMax * NR);
+        uint32_t *Bq = reinterpret_cast<uint32_t *>(fl + kFbMax);
+        uint32_t *nf = Bq + kFbMax;
+        cudaMemsetAsync(nf, 0, 4, s);
+        fb_list<<<(Qb + 255) / 256, 256, 0, s>>>(cnt, cv_sep, Qb, Tq, C, fl, nf, flags);
+        const size_t sm = (size_t)NR * 4;
+#define NR_FB(W_)                                                                                   \
+        cudaFuncSetAttribute(fb_hist<W_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);    \
+        fb_hist<W_><<<sms, 1024, sm, s>>>(ix->codes, ix->part_of_pos, ix->n, qcodes, ix->L, NR,     \
+                                          ix->R_d, fl, nf, ghist);                                  \
+        fb_bound<<<sms, 1024, 0, s>>>(fl, nf, NR, Tq, ghist, Bq, cnt, cv_sep);                      \
+        fb_take<W_><<<sms, 1024, 0, s>>>(ix->codes, ix->part_of_pos, ix->n, qcodes, ix->L, ix->R_d, \
+                                         fl, nf, Bq, buf, cnt, cv_sep, C)
+        if (ix->W == 1) { NR_FB(1); } else if (ix->W == 2) { NR_FB(2); } else { NR_FB(4); }
+#undef NR_FB
+        note_launch(4);
+        // the serial kernel below still counts every failed query (flags[2]) and
+        // handles any beyond kFbMax; the ones done here now pass its test
+    }
     const size_t sm = (size_t)NR * 4;
     const int32_t *order = ix->order_d;
     switch (ix->W) {
         case 1:
             cudaFuncSetAttribute(k6_fallback<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            k6_fallback<1><<<Qb, 1024, sm, s>>>(ix->codes, ix->part_of_pos, ix->n, qcodes, ix->L, ix->m, order, ix->R_d, Tq, buf, cnt, cntv, C, flags);
+            k6_fallback<1><<<Qb, 1024, sm, s>>>(ix->codes, ix->part_of_pos, ix->n, qcodes, ix->L, ix->m, order, ix->R_d, Tq, buf, cnt, cntv, C, par ? nullptr : flags);
             break;
         case 2:
             cudaFuncSetAttribute(k6_fallback<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            k6_fallback<2><<<Qb, 1024, sm, s>>>(ix->codes, ix->part_of_pos, ix->n, qcodes, ix->L, ix->m, order, ix->R_d, Tq, buf, cnt, cntv, C, flags);
+            k6_fallback<2><<<Qb, 1024, sm, s>>>(ix->codes, ix->part_of_pos, ix->n, qcodes, ix->L, ix->m, order, ix->R_d, Tq, buf, cnt, cntv, C, par ? nullptr : flags);
             break;
         default:
             cudaFuncSetAttribute(k6_fallback<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            k6_fallback<4><<<Qb, 1024, sm, s>>>(ix->codes, ix->part_of_pos, ix->n, qcodes, ix->L, ix->m, order, ix->R_d, Tq, buf, cnt, cntv, C, flags);
+            k6_fallback<4><<<Qb, 1024, sm, s>>>(ix->codes, ix->part_of_pos, ix->n, qcodes, ix->L, ix->m, order, ix->R_d, Tq, buf, cnt, cntv, C, par ? nullptr : flags);
             break;
     }
     note_launch();

@@ -349,18 +349,25 @@ def test_uniform_scheme_and_bit_accounting():
         assert np.array_equal(g[o], oid) and np.array_equal(r[o], ork)
 
 
-def test_forced_fallback_path(built, monkeypatch):
+@pytest.mark.parametrize("mode", ["parallel", "serial", "parallel+serial"])
+def test_forced_fallback_path(built, mode, monkeypatch):
     """The exact fallback (taken when the pilot bound under/overflows) gives the
-    same candidates as the oracle; forced for every query via a test switch."""
+    same candidates as the oracle; forced for every query via a test switch.  Modes:
+    the all-SM re-do (up to 64 failed queries per sub-batch), the one-CTA-per-query
+    kernel, and both (100 failed queries: 64 + 36)."""
     cfg, X, Q, Xd, idx, orc = built("c4", 300_000, 32, 32, 128)
     monkeypatch.setenv("NRLSH_TEST_FORCE_FALLBACK", "1")
+    if mode == "serial":
+        monkeypatch.setenv("NRLSH_FALLBACK_SERIAL", "1")
     P = _P()
     ocodes = orc.codes()
     idx.set_codes(ocodes[orc.perm])
-    qc = oracle.query_codes(Q[:6], orc.A)
+    nq = 100 if mode == "parallel+serial" else 6
+    Qm = np.concatenate([Q] * (nq // len(Q) + 1))[:nq]
+    qc = oracle.query_codes(Qm, orc.A)
     gid, grk = idx.candidates(2000, qcodes=torch.from_numpy(qc.view(np.int32)).cuda())
-    assert P.last_query_stats()["fallback_queries"] == 6
-    for qi in range(6):
+    assert P.last_query_stats()["fallback_queries"] == nq
+    for qi in ([0, 1, 63, 64, 99] if nq == 100 else range(6)):
         oid, ork = oracle.candidates(ocodes, orc.part, qc[qi], orc.R, 2000)
         g = gid[qi].cpu().numpy()
         r = grk[qi].cpu().numpy().view(np.uint16)
