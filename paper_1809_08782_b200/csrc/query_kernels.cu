@@ -375,11 +375,239 @@ __global__ void __launch_bounds__(kScanThreads) k6_scan(
     }
 }
 
+// ------------------------------------------------------------------ K6 on IMMA
+// The same scan with the Hamming distances from the legacy warp-level int8 tensor
+// instruction (mma.sync m16n8k32 s8, native IMMA on sm_100a; measured 1,550 MAC/clk/SM
+// = 3x the pair rate of two POPCs): a code bit b is s_b = +1 / -1 (bit 1 / 0), so
+// sum_b s_b(q) s_b(x) = 32W - 2h exactly (the zero bits past L agree), and one
+// 32-bit code word is one K = 32 step.
+// The +-1 operand fragments are built in registers straight from the packed code
+// words (a nibble -> 4 bytes, expand4), so nothing is expanded in memory.
+// CTA = (chunk of <= 2048 positions of one sub-dataset, group of 64 queries), as the
+// popcount scan; the group's active queries (delta_j >= 0) form tiles of 16 rows;
+// a warp unit = (query tile, span of 256 positions = 32 n8 tiles): a thread holds the
+// pass bits of its two rows (g, g+8) for its two columns of every n8 tile (64 bits
+// per row), then the 4 lanes of a row reserve the row's stage slots with one shared
+// atomic (and the global overflow with one more) and write their entries, h taken
+// again with POPC for the passing pairs only.
+__device__ __forceinline__ uint32_t expand4_pm(uint32_t nib) {
+    const uint32_t y = (nib * 0x00204081u) & 0x01010101u;
+    return 0xFFFFFFFFu ^ (y * 0xFEu);   // bit i -> byte i: +1 (0x01) or -1 (0xFF)
+}
+
+constexpr int kQGI = 128;    // queries per CTA (IMMA scan): more active rows per tile
+constexpr int kSBI = 48;     // staged appends per (CTA, query)
+constexpr int kTPU = 4;      // query tiles (of 16 rows) per warp unit: one B expansion feeds 4 MMAs
+
+template <int W>
+__global__ void __launch_bounds__(kScanThreads) k6_scan_imma(
+    const uint32_t *__restrict__ codes, const int4 *__restrict__ chunks,
+    const uint32_t *__restrict__ qcodes, const int8_t *__restrict__ delta, int Qb, int m,
+    int L, unsigned long long *__restrict__ buf, uint32_t *__restrict__ cnt, int64_t C,
+    unsigned long long *__restrict__ pairs) {
+    __shared__ uint32_t sq[kQGI][W];
+    __shared__ int sthr[kQGI];
+    __shared__ uint32_t sbuf[kQGI][kSBI];
+    __shared__ uint32_t scnt[kQGI];
+    __shared__ uint32_t sbase[kQGI];
+    __shared__ int sact[kQGI];
+    __shared__ int s_nact;
+    __shared__ uint32_t scode[kScanThreads / 32][128 * W];   // a warp unit's span of codes
+    const int ngroups = (Qb + kQGI - 1) / kQGI;
+    const int4 ch = chunks[blockIdx.x / ngroups];
+    const int j = ch.x, p0 = ch.y, p1 = ch.z;
+    const int q0 = (blockIdx.x % ngroups) * kQGI;
+    const int nqg = min(kQGI, Qb - q0);
+    if (threadIdx.x < 32) {       // warp 0 compacts the group's active queries
+        int base = 0;
+        for (int t0 = 0; t0 < kQGI; t0 += 32) {
+            const int t = t0 + threadIdx.x;
+            int dl = -1;
+            if (t < nqg) {
+                dl = delta[(int64_t)(q0 + t) * m + j];
+#pragma unroll
+                for (int w = 0; w < W; ++w) sq[t][w] = qcodes[(int64_t)(q0 + t) * W + w];
+            }
+            scnt[t] = 0;
+            const unsigned bal = __ballot_sync(NR_FULL, dl >= 0);
+            if (dl >= 0) {
+                const int slot = base + __popc(bal & lanemask_lt());
+                sact[slot] = t;
+                // bits >= L are 0 in both codes, so they add +1 each: dot = 32 W - 2h,
+                // and h <= delta  <=>  dot >= 32 W - 2 delta
+                sthr[slot] = 32 * W - 2 * dl;
+            }
+            base += __popc(bal);
+        }
+        if (threadIdx.x == 0) s_nact = base;
+    }
+    __syncthreads();
+    const int nact = s_nact;
+    if (nact == 0) return;
+    if (threadIdx.x == 0 && pairs) atomicAdd(pairs, (unsigned long long)nact * (p1 - p0));
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const int nqt = (nact + 15) >> 4;
+    const int ntg = (nqt + kTPU - 1) / kTPU;           // tile groups
+    constexpr int kSpan = 128;                         // positions per warp unit (16 n8 tiles)
+    const int nspan = (p1 - p0 + kSpan - 1) / kSpan;
+    for (int u = warp; u < ntg * nspan; u += kScanThreads / 32) {
+        const int tg = u % ntg, sp = u / ntg;
+        const int qt0 = tg * kTPU, nt = min(kTPU, nqt - qt0);
+        uint32_t a[kTPU][W][4];
+        int th[kTPU][2];
+#pragma unroll
+        for (int x = 0; x < kTPU; ++x) {
+            const int r0 = (qt0 + x) * 16 + g, r1 = r0 + 8;
+            const bool v0 = x < nt && r0 < nact, v1 = x < nt && r1 < nact;
+            const int qq0 = v0 ? sact[r0] : 0, qq1 = v1 ? sact[r1] : 0;
+            th[x][0] = v0 ? sthr[r0] : INT_MAX;
+            th[x][1] = v1 ? sthr[r1] : INT_MAX;
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+                const uint32_t c0 = v0 ? sq[qq0][w] : 0u, c1 = v1 ? sq[qq1][w] : 0u;
+                a[x][w][0] = expand4_pm((c0 >> (4 * t)) & 0xFu);
+                a[x][w][1] = expand4_pm((c1 >> (4 * t)) & 0xFu);
+                a[x][w][2] = expand4_pm((c0 >> (16 + 4 * t)) & 0xFu);
+                a[x][w][3] = expand4_pm((c1 >> (16 + 4 * t)) & 0xFu);
+            }
+        }
+        const int sb = p0 + sp * kSpan;                // first position of the span
+        const int se = min(p1, sb + kSpan);
+        uint32_t *wc = scode[warp];
+        __syncwarp();
+        for (int e = lane; e < kSpan; e += 32) {       // the span's codes, coalesced, to smem
+            uint32_t cw[W];
+            if (sb + e < se) load_code<W>(codes, sb + e, cw);
+            else
+#pragma unroll
+                for (int w = 0; w < W; ++w) cw[w] = 0u;
+#pragma unroll
+            for (int w = 0; w < W; ++w) wc[e * W + w] = cw[w];
+        }
+        __syncwarp();
+        uint32_t mk[kTPU][2];                          // bit 2k + c: n8 tile k, column 2t + c
+#pragma unroll
+        for (int x = 0; x < kTPU; ++x) mk[x][0] = mk[x][1] = 0u;
+#pragma unroll 2
+        for (int k = 0; k < kSpan / 8; ++k) {
+            uint32_t iw[W];                             // B column (item k * 8 + g)
+#pragma unroll
+            for (int w = 0; w < W; ++w) iw[w] = wc[(k * 8 + g) * W + w];
+            uint32_t b[W][2];
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+                b[w][0] = expand4_pm((iw[w] >> (4 * t)) & 0xFu);
+                b[w][1] = expand4_pm((iw[w] >> (16 + 4 * t)) & 0xFu);
+            }
+            const int pc = sb + k * 8 + 2 * t;          // C columns of this lane: pc, pc + 1
+            const uint32_t ok = (uint32_t)(pc < se) | ((uint32_t)(pc + 1 < se) << 1);
+            // (all kTPU tiles unconditionally: independent MMAs in flight; the rows of
+            // missing tiles have threshold INT_MAX and never pass)
+#pragma unroll
+            for (int x = 0; x < kTPU; ++x) {
+                int c[4] = {0, 0, 0, 0};
+#pragma unroll
+                for (int w = 0; w < W; ++w)
+                    asm volatile(
+                        "mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+                        : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+                        : "r"(a[x][w][0]), "r"(a[x][w][1]), "r"(a[x][w][2]), "r"(a[x][w][3]),
+                          "r"(b[w][0]), "r"(b[w][1]));
+                const uint32_t f0 = ((uint32_t)(c[0] >= th[x][0]) | ((uint32_t)(c[1] >= th[x][0]) << 1)) & ok;
+                const uint32_t f1 = ((uint32_t)(c[2] >= th[x][1]) | ((uint32_t)(c[3] >= th[x][1]) << 1)) & ok;
+                mk[x][0] |= f0 << (2 * k);
+                mk[x][1] |= f1 << (2 * k);
+            }
+        }
+        // appends: per row, the 4 lanes of the group reserve together
+#pragma unroll
+        for (int x = 0; x < kTPU; ++x) {
+            if (x >= nt) break;
+#pragma unroll
+            for (int rr = 0; rr < 2; ++rr) {
+                const int r = (qt0 + x) * 16 + g + 8 * rr;
+                const uint32_t mm = mk[x][rr];
+                const int np = __popc(mm);
+                int inc = np;
+                {
+                    const int y1 = __shfl_up_sync(NR_FULL, inc, 1);
+                    if (t >= 1) inc += y1;
+                    const int y2 = __shfl_up_sync(NR_FULL, inc, 2);
+                    if (t >= 2) inc += y2;
+                }
+                const int tot = __shfl_sync(NR_FULL, inc, (lane & ~3) + 3);
+                const int qq = r < nact ? sact[r] : 0;
+                uint32_t base = 0, gbase = 0;
+                if (t == 3 && tot > 0) {
+                    base = atomicAdd(&scnt[qq], (uint32_t)tot);
+                    const uint32_t lo = max(base, (uint32_t)kSBI), hi = base + (uint32_t)tot;
+                    if (hi > lo) gbase = atomicAdd(&cnt[q0 + qq], hi - lo);
+                }
+                base = __shfl_sync(NR_FULL, base, (lane & ~3) + 3);
+                gbase = __shfl_sync(NR_FULL, gbase, (lane & ~3) + 3);
+                if (!np) continue;
+                const uint32_t glo = max(base, (uint32_t)kSBI);
+                uint32_t slot = base + (uint32_t)(inc - np);
+                uint32_t qc[W];
+#pragma unroll
+                for (int w = 0; w < W; ++w) qc[w] = sq[qq][w];
+                uint32_t mb = mm;
+                while (mb) {
+                    const int bb = __ffs(mb) - 1;
+                    mb &= mb - 1;
+                    const int e = (bb >> 1) * 8 + 2 * t + (bb & 1);
+                    const int pos = sb + e;
+                    uint32_t iw[W];
+#pragma unroll
+                    for (int w = 0; w < W; ++w) iw[w] = wc[e * W + w];
+                    const int h = hamming<W>(iw, qc);
+                    const uint32_t off = (uint32_t)(pos - p0);
+                    if (slot < kSBI) {
+                        sbuf[qq][slot] = ((uint32_t)h << 16) | off;
+                    } else {
+                        const uint32_t gg = gbase + (slot - glo);
+                        if (gg < C)
+                            buf[(int64_t)(q0 + qq) * C + gg] = ((unsigned long long)(j * (L + 1) + h) << 32) | (uint32_t)pos;
+                    }
+                    ++slot;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    for (int tq = threadIdx.x; tq < nqg; tq += blockDim.x) {
+        const uint32_t nst = min(scnt[tq], (uint32_t)kSBI);
+        sbase[tq] = nst ? atomicAdd(&cnt[q0 + tq], nst) : 0u;
+    }
+    __syncthreads();
+    const unsigned long long jb = (unsigned long long)(j * (L + 1));
+    for (int tq = warp; tq < nqg; tq += kScanThreads / 32) {
+        const uint32_t nst = min(scnt[tq], (uint32_t)kSBI);
+        const int64_t q = q0 + tq;
+        for (uint32_t e = lane; e < nst; e += 32) {
+            const uint32_t gg = sbase[tq] + e;
+            const uint32_t v = sbuf[tq][e];
+            if (gg < C) buf[q * C + gg] = ((jb + (v >> 16)) << 32) | (uint32_t)(p0 + (v & 0xffffu));
+        }
+    }
+}
+
 void launch_scan(const nrlsh_index *ix, const uint32_t *qcodes, const int8_t *delta, int Qb,
                  unsigned long long *buf, uint32_t *cnt, int64_t C, unsigned long long *pairs,
                  cudaStream_t s) {
     const int64_t ngroups = (Qb + kQG - 1) / kQG;
     const unsigned grid = (unsigned)(ix->nchunks * ngroups);
+    if (getenv("NRLSH_SCAN_IMMA") && atoi(getenv("NRLSH_SCAN_IMMA")) != 0) {
+        const unsigned gridi = (unsigned)(ix->nchunks * ((Qb + kQGI - 1) / kQGI));
+        switch (ix->W) {
+            case 1: k6_scan_imma<1><<<gridi, kScanThreads, 0, s>>>(ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->L, buf, cnt, C, pairs); break;
+            case 2: k6_scan_imma<2><<<gridi, kScanThreads, 0, s>>>(ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->L, buf, cnt, C, pairs); break;
+            default: k6_scan_imma<4><<<gridi, kScanThreads, 0, s>>>(ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->L, buf, cnt, C, pairs); break;
+        }
+        note_launch();
+        return;
+    }
     switch (ix->W) {
         case 1: k6_scan<1><<<grid, kScanThreads, 0, s>>>(ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs); break;
         case 2: k6_scan<2><<<grid, kScanThreads, 0, s>>>(ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs); break;
