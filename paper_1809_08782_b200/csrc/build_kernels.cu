@@ -123,11 +123,29 @@ __global__ void __launch_bounds__(128) k1_norms_bulk(const float *__restrict__ X
             const float *row = src + (size_t)min(r, rows - 1) * d;
             const int lag = skew * lane;
             double s = 0.0;
-            for (int step = 0; step < d + 31 * skew; ++step) {
-                const int k = step - lag;
-                if (k >= 0 && k < d) {
-                    const double v = (double)row[k];
-                    s = __fma_rn(v, v, s);        // v*v is exact: one rounding, as s + v*v
+            // k ascending (the oracle's order); v*v is exact, so each step rounds once,
+            // as s + v*v.  Lane l runs l steps behind lane 0 when d is even (bank skew);
+            // the middle section, where every lane has a valid k, is unrolled so its
+            // shared-memory loads issue ahead of the dependent fma chain.
+            if (skew && d >= 32) {
+                for (int step = 0; step < 31; ++step) {
+                    const int k = step - lag;
+                    if (k >= 0) { const double v = (double)row[k]; s = __fma_rn(v, v, s); }
+                }
+                const float *p = row + 31 - lag;
+#pragma unroll 8
+                for (int t = 0; t < d - 31; ++t) { const double v = (double)p[t]; s = __fma_rn(v, v, s); }
+                for (int step = d; step < d + 31; ++step) {
+                    const int k = step - lag;
+                    if (k < d) { const double v = (double)row[k]; s = __fma_rn(v, v, s); }
+                }
+            } else if (!skew) {
+#pragma unroll 8
+                for (int k = 0; k < d; ++k) { const double v = (double)row[k]; s = __fma_rn(v, v, s); }
+            } else {
+                for (int step = 0; step < d + 31; ++step) {
+                    const int k = step - lag;
+                    if (k >= 0 && k < d) { const double v = (double)row[k]; s = __fma_rn(v, v, s); }
                 }
             }
             if (r < rows) {

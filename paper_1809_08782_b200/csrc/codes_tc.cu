@@ -15,9 +15,9 @@
 // (|x - X_big - tf32(X_small)| < 2^-20 |x|), far inside the 1e-5 parity band.
 //
 // CTA (persistent, one per SM): tile = 128 items (TMEM lanes) x N = 32W columns.
-//   warps 0-7  convert: coalesced loads of X (next K-block prefetched in
-//              registers), split, store both halves into 128B-swizzled K-major
-//              smem K-blocks (32 tf32 wide), ring of CT_STAGES stages
+//   warps 0-7  convert: coalesced cp.async loads of X into per-thread raw
+//              slots (up to 3 K-blocks ahead), split, store both halves into
+//              128B-swizzled K-major smem K-blocks (32 tf32 wide), ring of stages
 //   warp  8    TMEM allocator + single-thread tcgen05.mma issuer
 //   warps 9-12 epilogue: tcgen05.ld the accumulator row, add A_d t_i, sign, pack,
 //              scatter the W code words to pos_of_id[i]
@@ -43,7 +43,7 @@ constexpr int CT_THREADS = 13 * 32;
 struct CodesArgs {
     const float *X;
     int64_t n;
-    int d, KB, L, N, stages;
+    int d, KB, L, N, stages, raw;   // raw: cp.async slots per converter thread (lookahead raw-1)
     int64_t ntiles;
     const double *norm2;
     const uint8_t *part;
@@ -61,34 +61,67 @@ __device__ __forceinline__ uint32_t swz(int row, int kbyte) {
     return (uint32_t)(row * 128 + ((((kbyte >> 4) ^ (row & 7))) << 4) + (kbyte & 15));
 }
 
+// Loads go through cp.async (zero-filled past n and d) into a per-thread raw slot
+// ring: RAW K-blocks in flight per SM without holding them in registers.
+constexpr int CT_RAW_SLOT = CT_CONV * 16 * 4;   // 16 KB: 16 floats per converter thread
+
 template <int VEC>
-__device__ __forceinline__ void conv_load(const CodesArgs &a, int64_t tile, int kb, int w, int l,
-                                          float (&v)[16]) {
-    constexpr int lpr = VEC == 4 ? 8 : (VEC == 2 ? 16 : 32);   // lanes per 128-byte row
-    constexpr int rpi = 32 / lpr;                               // rows per instruction
-    constexpr int ni = 16 / rpi;                                // instructions per K-block
+__device__ __forceinline__ void conv_issue(const CodesArgs &a, int64_t tile, int kb, int w, int l,
+                                           uint8_t *slot, int32_t *posr) {
+    // with the first K-block of a tile, the warp's 16 rows' partition positions (the
+    // bf16 copy's destination rows; read back by the warp only)
+    if (kb == 0 && a.Xb && l < 16) {
+        const int64_t i = tile * CT_M + 16 * w + l;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4, 4;" ::"r"(tc::smem_u32(posr + 16 * w + l)),
+                     "l"(a.pos_of_id + (i < a.n ? i : a.n - 1))
+                     : "memory");
+    }
+    constexpr int lpr = VEC == 4 ? 8 : (VEC == 2 ? 16 : 32);
+    constexpr int rpi = 32 / lpr;
+    constexpr int ni = 16 / rpi;
     const int col = kb * CT_KB + (l % lpr) * VEC;
     const int cc = min(col, a.d - VEC);
+    const int tid = w * 32 + l;
 #pragma unroll
     for (int j = 0; j < ni; ++j) {
         const int rr = 16 * w + j * rpi + l / lpr;
         const int64_t i = tile * CT_M + rr;
         const int64_t ic = i < a.n ? i : a.n - 1;
         const float *p = a.X + ic * a.d + cc;
-        float t[VEC];
-        if (VEC == 4) {
-            const float4 q = __ldg(reinterpret_cast<const float4 *>(p));
-            t[0] = q.x; t[1] = q.y; t[2] = q.z; t[3] = q.w;
-        } else if (VEC == 2) {
-            const float2 q = __ldg(reinterpret_cast<const float2 *>(p));
-            t[0] = q.x; t[1] = q.y;
-        } else {
-            t[0] = __ldg(p);
-        }
-        const bool ok = (i < a.n) && (col < a.d);
-#pragma unroll
-        for (int e = 0; e < VEC; ++e) v[j * VEC + e] = ok ? t[e] : 0.f;
+        const uint32_t dst = tc::smem_u32(slot + (size_t)(j * CT_CONV + tid) * VEC * 4);
+        const int nb = ((i < a.n) && (col < a.d)) ? VEC * 4 : 0;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(dst), "l"(p), "n"(VEC * 4),
+                     "r"(nb)
+                     : "memory");
     }
+}
+
+template <int VEC>
+__device__ __forceinline__ void conv_read(const uint8_t *slot, int w, int l, float (&v)[16]) {
+    constexpr int lpr = VEC == 4 ? 8 : (VEC == 2 ? 16 : 32);
+    constexpr int rpi = 32 / lpr;
+    constexpr int ni = 16 / rpi;
+    const int tid = w * 32 + l;
+#pragma unroll
+    for (int j = 0; j < ni; ++j) {
+        const float *q = reinterpret_cast<const float *>(slot + (size_t)(j * CT_CONV + tid) * VEC * 4);
+        if (VEC == 4) {
+            const float4 t = *reinterpret_cast<const float4 *>(q);
+            v[j * 4] = t.x; v[j * 4 + 1] = t.y; v[j * 4 + 2] = t.z; v[j * 4 + 3] = t.w;
+        } else if (VEC == 2) {
+            const float2 t = *reinterpret_cast<const float2 *>(q);
+            v[j * 2] = t.x; v[j * 2 + 1] = t.y;
+        } else {
+            v[j] = q[0];
+        }
+    }
+}
+
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait(int la) {
+    if (la >= 3) asm volatile("cp.async.wait_group 3;" ::: "memory");
+    else if (la == 2) asm volatile("cp.async.wait_group 2;" ::: "memory");
+    else asm volatile("cp.async.wait_group 1;" ::: "memory");
 }
 
 template <int VEC>
@@ -126,7 +159,7 @@ __device__ __forceinline__ void conv_store(uint8_t *stage, int w, int l, const f
 // bf16 copy of the converter's slice of the rows (columns < dpb; zeros past d)
 template <int VEC>
 __device__ __forceinline__ void conv_store_bf16(const CodesArgs &a, int64_t tile, int kb, int w, int l,
-                                                const float (&v)[16]) {
+                                                const float (&v)[16], const int32_t *posr) {
     constexpr int lpr = VEC == 4 ? 8 : (VEC == 2 ? 16 : 32);
     constexpr int rpi = 32 / lpr;
     constexpr int ni = 16 / rpi;
@@ -137,7 +170,7 @@ __device__ __forceinline__ void conv_store_bf16(const CodesArgs &a, int64_t tile
         const int rr = 16 * w + j * rpi + l / lpr;
         const int64_t i = tile * CT_M + rr;
         if (i >= a.n) continue;
-        __nv_bfloat16 *dst = a.Xb + (int64_t)__ldg(a.pos_of_id + i) * a.dpb + col;
+        __nv_bfloat16 *dst = a.Xb + (int64_t)posr[rr] * a.dpb + col;
         if (VEC == 4) {
             const __nv_bfloat162 p0 = __floats2bfloat162_rn(v[j * 4 + 0], v[j * 4 + 1]);
             const __nv_bfloat162 p1 = __floats2bfloat162_rn(v[j * 4 + 2], v[j * 4 + 3]);
@@ -167,8 +200,9 @@ __device__ __forceinline__ void conv_store_pad(const CodesArgs &a, int64_t tile,
         const int64_t i = tile * CT_M + rr;
         if (i >= a.n) continue;
         float *dst = a.Xpad + i * a.dpad + col;
-#pragma unroll
-        for (int e = 0; e < VEC; ++e) dst[e] = v[j * VEC + e];
+        if (VEC == 4) *reinterpret_cast<float4 *>(dst) = make_float4(v[j * 4], v[j * 4 + 1], v[j * 4 + 2], v[j * 4 + 3]);
+        else if (VEC == 2) *reinterpret_cast<float2 *>(dst) = make_float2(v[j * 2], v[j * 2 + 1]);
+        else dst[0] = v[j];
     }
 }
 
@@ -177,12 +211,14 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k3_codes_tc(CodesArgs a) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
     uint8_t *ring = smem;                                        // stages x 32 KB
-    uint8_t *Bs = ring + a.stages * CT_STAGE;                    // KB x N x 128 B
+    uint8_t *rawr = ring + a.stages * CT_STAGE;                  // raw x 16 KB
+    uint8_t *Bs = rawr + (size_t)a.raw * CT_RAW_SLOT;            // KB x N x 128 B
     float *Ad = reinterpret_cast<float *>(Bs + (size_t)a.KB * a.N * 128);   // [N]
     uint64_t *bars = reinterpret_cast<uint64_t *>(Ad + a.N);
     uint64_t *full = bars, *empty = bars + a.stages;
     uint64_t *tfull = bars + 2 * a.stages, *tempty = tfull + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+    int32_t *posr = reinterpret_cast<int32_t *>(tempty + 4);     // [4][CT_M], ring by tile
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int N = a.N;
@@ -216,28 +252,44 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k3_codes_tc(CodesArgs a) {
 
     if (warp < 8) {
         // ================= converters
+        // K-block g of this CTA = (tile blockIdx.x + (g / KB) gridDim.x, kb g % KB);
+        // issue and consume cursors advance incrementally (no 64-bit divisions)
+        const int64_t my_tiles =
+            a.ntiles > (int64_t)blockIdx.x ? (a.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+        const int64_t G = my_tiles * a.KB;
+        const int la = a.raw - 1;
+        int64_t i_tile = blockIdx.x, issued = 0;
+        int i_kb = 0, i_ti = 0, i_slot = 0;
+        auto issue = [&]() {
+            if (issued < G) {
+                conv_issue<VEC>(a, i_tile, i_kb, warp, lane, rawr + (size_t)i_slot * CT_RAW_SLOT,
+                                posr + (i_ti & 3) * CT_M);
+                if (++i_kb == a.KB) { i_kb = 0; i_tile += gridDim.x; ++i_ti; }
+                if (++i_slot == a.raw) i_slot = 0;
+            }
+            ++issued;
+            cp_async_commit();   // (empty groups keep the group count uniform)
+        };
+        for (int g = 0; g < la; ++g) issue();
         int64_t tile = blockIdx.x;
-        int kb = 0;
-        float cur[16];
-        if (tile < a.ntiles) conv_load<VEC>(a, tile, 0, warp, lane, cur);
-        for (uint32_t g = 0; tile < a.ntiles; ++g) {
-            int64_t ntile = tile;
-            int nkb = kb + 1;
-            if (nkb == a.KB) { nkb = 0; ntile += gridDim.x; }
-            float nxt[16];
-            if (ntile < a.ntiles) conv_load<VEC>(a, ntile, nkb, warp, lane, nxt);
-            const uint32_t s = g % a.stages, ph = (g / a.stages) & 1;
+        int kb = 0, ti = 0, rslot = 0;
+        uint32_t s = 0, ph = 0;
+        for (int64_t g = 0; g < G; ++g) {
+            issue();               // into the slot this thread emptied at g - 1
+            cp_async_wait(la);     // this thread's copies for K-block g have landed
+            __syncwarp();          // (and the warp's positions of the tile's rows)
+            float cur[16];
+            conv_read<VEC>(rawr + (size_t)rslot * CT_RAW_SLOT, warp, lane, cur);
             tc::mbar_wait(&empty[s], ph ^ 1);
             conv_store<VEC>(ring + s * CT_STAGE, warp, lane, cur);
-            if (a.Xb) conv_store_bf16<VEC>(a, tile, kb, warp, lane, cur);
+            if (a.Xb) conv_store_bf16<VEC>(a, tile, kb, warp, lane, cur, posr + (ti & 3) * CT_M);
             if (a.Xpad) conv_store_pad<VEC>(a, tile, kb, warp, lane, cur);
             tc::fence_async_shared();
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&full[s]);
-#pragma unroll
-            for (int e = 0; e < 16; ++e) cur[e] = nxt[e];
-            tile = ntile;
-            kb = nkb;
+            if (++kb == a.KB) { kb = 0; tile += gridDim.x; ++ti; }
+            if (++rslot == a.raw) rslot = 0;
+            if (++s == (uint32_t)a.stages) { s = 0; ph ^= 1; }
         }
     } else if (warp == 8) {
         if (lane == 0) {
@@ -327,16 +379,25 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k3_codes_tc(CodesArgs a) {
     }
 }
 
-static size_t codes_tc_smem(int KB, int N, int stages) {
-    return 1024 + (size_t)stages * CT_STAGE + (size_t)KB * N * 128 + (size_t)N * 4 +
-           (2 * stages + 4) * 8 + 16;
+static size_t codes_tc_smem(int KB, int N, int stages, int raw) {
+    return 1024 + (size_t)stages * CT_STAGE + (size_t)raw * CT_RAW_SLOT + (size_t)KB * N * 128 +
+           (size_t)N * 4 + (2 * stages + 4) * 8 + 32 + 4 * CT_M * 4;
+}
+
+// (MMA stages, raw slots): most loads in flight first (raw 4 = 48 KB ahead per SM),
+// then MMA stages
+static void codes_tc_config(int d, int N, int &stages, int &raw) {
+    const int KB = (d + CT_KB - 1) / CT_KB;
+    const int opts[][2] = {{3, 4}, {2, 4}, {2, 3}, {2, 2}};
+    for (const auto &o : opts)
+        if (codes_tc_smem(KB, N, o[0], o[1]) <= 227 * 1024) { stages = o[0]; raw = o[1]; return; }
+    stages = raw = 0;
 }
 
 static int codes_tc_stages(int d, int N) {
-    const int KB = (d + CT_KB - 1) / CT_KB;
-    for (int st = 4; st >= 2; --st)
-        if (codes_tc_smem(KB, N, st) <= 227 * 1024) return st;
-    return 0;
+    int st, raw;
+    codes_tc_config(d, N, st, raw);
+    return st;
 }
 
 bool codes_tc_supported(int d, int W) {
@@ -356,7 +417,7 @@ void launch_item_codes_tc(const float *X, int64_t n, int d, const double *norm2,
     a.KB = (d + CT_KB - 1) / CT_KB;
     a.L = L;
     a.N = 32 * W;
-    a.stages = codes_tc_stages(d, a.N);
+    codes_tc_config(d, a.N, a.stages, a.raw);
     a.ntiles = (n + CT_M - 1) / CT_M;
     a.norm2 = norm2;
     a.part = part;
@@ -368,7 +429,7 @@ void launch_item_codes_tc(const float *X, int64_t n, int d, const double *norm2,
     a.dpb = dpb;
     a.Xpad = Xpad;
     a.dpad = dpad;
-    const size_t sm = codes_tc_smem(a.KB, a.N, a.stages);
+    const size_t sm = codes_tc_smem(a.KB, a.N, a.stages, a.raw);
     const int grid = (int)std::min<int64_t>(sms, a.ntiles);
     const int vec = (d % 4 == 0) ? 4 : ((d % 2 == 0) ? 2 : 1);
 #define NR_CT(V)                                                                               \
