@@ -104,11 +104,11 @@ __global__ void __launch_bounds__(256) scan_tile_lists(const int8_t *__restrict_
     __shared__ uint8_t act[256];
     const int qb = blockIdx.y;
     const int q0 = qb * SM_M, q1 = min(Qb, q0 + SM_M);
-    for (int j = threadIdx.x; j < m; j += blockDim.x) {
-        uint8_t on = 0;
-        for (int q = q0; q < q1 && !on; ++q) on = delta[(int64_t)q * m + j] >= 0;
-        act[j] = on;
-    }
+    for (int j = threadIdx.x; j < m; j += blockDim.x) act[j] = 0;
+    __syncthreads();
+    const int nv = (q1 - q0) * m;   // the block's delta rows, read coalesced
+    for (int e = threadIdx.x; e < nv; e += blockDim.x)
+        if (delta[(int64_t)q0 * m + e] >= 0) act[e % m] = 1;
     __syncthreads();
     const int lane = threadIdx.x & 31;
     for (int t = blockIdx.x * 1024 + threadIdx.x; t < min(ntiles, (int)(blockIdx.x + 1) * 1024);
