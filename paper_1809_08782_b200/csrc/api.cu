@@ -868,7 +868,8 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
                                int64_t *out_ids, float *out_scores, void *cuda_stream,
                                const void *Xb_ix = nullptr, const float *xnorm_ix = nullptr,
                                const int32_t *perm_ix = nullptr,
-                               const float *tile_xmax_ix = nullptr, float xsplit_ix = 0.f) {
+                               const float *tile_xmax_ix = nullptr, float xsplit_ix = 0.f,
+                               const float *Xpad_ix = nullptr, int dpad_ix = 0) {
     if (!items || !queries || !out_ids || !out_scores) return fail(NRLSH_EINVAL, "NULL argument");
     if (seed_ids && (seed_k < 1 || seed_k > 1024))
         return fail(NRLSH_EINVAL, "seed_k must be in [1, 1024]");
@@ -890,6 +891,9 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
     if ((e = os.init(out_scores, (size_t)nq * k * 4, s))) return cuda_fail(e, "out_scores");
     const float *X = (const float *)Xs.dev;
     const float *Q = (const float *)Qs.dev;
+    // exact re-ranks read the index's 16-byte-aligned row copy when it has one
+    const float *Xr = Xpad_ix ? Xpad_ix : X;
+    const int ldr = Xpad_ix ? dpad_ix : d;
     const bool use_tc = gt_tc_supported(d, k) && !getenv("NRLSH_GT_SIMT");
     const int dp = (d + 7) / 8 * 8;
     // certified error bound of fl(q.x) relative to |q||x|:
@@ -986,7 +990,7 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
                                         Xb_ix ? perm_ix : nullptr, nullptr, tiles ? &gtl : nullptr))
                     return fail(NRLSH_ECUDA, "tensor map encoding failed");
                 if (pass < npass) {
-                    launch_rerank(X, d, d, Qb_ptr, Qb, cd.get<int32_t>(), Cg, Cg, cc.get<uint32_t>(), 1, k,
+                    launch_rerank(Xr, d, ldr, Qb_ptr, Qb, cd.get<int32_t>(), Cg, Cg, cc.get<uint32_t>(), 1, k,
                                   pt.get<unsigned long long>(), tid.get<int64_t>(), tsc.get<float>(), s);
                     launch_theta_from_topk(tid.get<int64_t>(), tsc.get<float>(), Qb, k,
                                            th.get<uint32_t>(), s);
@@ -1010,7 +1014,7 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
         }
         {
             ProfScope p(SLOT_SCORE, s);
-            launch_rerank(X, d, d, Qb_ptr, Qb, cd.get<int32_t>(), Cg, Cg, cc.get<uint32_t>(), 1, k,
+            launch_rerank(Xr, d, ldr, Qb_ptr, Qb, cd.get<int32_t>(), Cg, Cg, cc.get<uint32_t>(), 1, k,
                           pt.get<unsigned long long>(), oid, osc, s);
         }
         // survivor statistics and overflowing queries, collected on the device (no
@@ -1031,7 +1035,7 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
             std::vector<int64_t> ql(nov);
             cudaMemcpy(ql.data(), gov.p, (size_t)nov * 8, cudaMemcpyDeviceToHost);
             for (int64_t qi : ql)
-                launch_rerank(X, d, d, Q + qi * d, 1, nullptr, n, n, nullptr, 1, k,
+                launch_rerank(Xr, d, ldr, Q + qi * d, 1, nullptr, n, n, nullptr, 1, k,
                               pt.get<unsigned long long>(), (int64_t *)oi.dev + qi * k,
                               (float *)os.dev + qi * k, s);
         }
@@ -1073,7 +1077,7 @@ nrlsh_status nrlsh_index_exact_topk(const nrlsh_index *ix, const float *queries,
     if (!ix) return fail(NRLSH_EINVAL, "index is NULL");
     return exact_impl(ix->X, ix->n, ix->d, queries, nq, k, nullptr, 0, out_ids, out_scores,
                       cuda_stream, ix->Xb, ix->xnorm_pos, ix->perm, ix->tile_xmax,
-                      ix->tile_xsplit);
+                      ix->tile_xsplit, ix->Xpad, ix->dpad);
 }
 
 nrlsh_status nrlsh_index_exact_topk_seeded(const nrlsh_index *ix, const float *queries,
@@ -1084,7 +1088,7 @@ nrlsh_status nrlsh_index_exact_topk_seeded(const nrlsh_index *ix, const float *q
     if (!seed_ids) return fail(NRLSH_EINVAL, "seed_ids is NULL");
     return exact_impl(ix->X, ix->n, ix->d, queries, nq, k, seed_ids, seed_k, out_ids, out_scores,
                       cuda_stream, ix->Xb, ix->xnorm_pos, ix->perm, ix->tile_xmax,
-                      ix->tile_xsplit);
+                      ix->tile_xsplit, ix->Xpad, ix->dpad);
 }
 
 // ------------------------------------------------------------------ hooks

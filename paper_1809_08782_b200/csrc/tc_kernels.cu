@@ -884,17 +884,22 @@ __global__ void __launch_bounds__(1024) sort_by_bound(const float *__restrict__ 
     extern __shared__ unsigned long long keys[];
     int np2 = 2;
     while (np2 < Qb) np2 <<= 1;
-    for (int i = threadIdx.x; i < np2; i += blockDim.x) {
+    // a warp per query row (coalesced); the key only orders the pairs (any |q|
+    // rounding is fine)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int i = warp; i < np2; i += nw) {
         unsigned long long key = ~0ull;
         if (i < Qb) {
             float ss = 0.f;
-            for (int e = 0; e < d; ++e) ss = fmaf(Q[(int64_t)i * d + e], Q[(int64_t)i * d + e], ss);
+            for (int e = lane; e < d; e += 32) ss = fmaf(Q[(int64_t)i * d + e], Q[(int64_t)i * d + e], ss);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
             const uint32_t o = theta[i];
             const float th = o ? float_unorder(o) : 0.f;
             const float kf = (th > 0.f && ss > 0.f) ? th / sqrtf(ss) : 0.f;
             key = ((unsigned long long)(~float_order(kf)) << 32) | (uint32_t)i;
         }
-        keys[i] = key;
+        if (lane == 0) keys[i] = key;
     }
     __syncthreads();
     for (int size = 2; size <= np2; size <<= 1)
