@@ -99,20 +99,40 @@ __device__ void hist_and_bound(const uint32_t *__restrict__ codes,
     if (threadIdx.x == 0) { *sB = NR - 1; *sLt = 0u; }
     __syncthreads();
     const int lane = threadIdx.x & 31;
-    for (int64_t b0 = 0; b0 < ns; b0 += blockDim.x) {
-        const int64_t t = b0 + threadIdx.x;
-        int bin = -1;
-        // (interleaved sample: slot t holds sample (t % per) * 32 + t / per, if any)
-        if (t < ns && (per == 0 || (t % per) * 32 + t / per < ns_real)) {
-            uint32_t c[W];
-            load_code<W>(codes, t, c);
-            bin = (int)part[t] * (L + 1) + hamming<W>(c, qc);
-        }
-        if (AGG) {
+    if (AGG) {
+        for (int64_t b0 = 0; b0 < ns; b0 += blockDim.x) {
+            const int64_t t = b0 + threadIdx.x;
+            int bin = -1;
+            if (t < ns) {
+                uint32_t c[W];
+                load_code<W>(codes, t, c);
+                bin = (int)part[t] * (L + 1) + hamming<W>(c, qc);
+            }
             const unsigned peers = __match_any_sync(NR_FULL, bin);
             if (bin >= 0 && lane == __ffs(peers) - 1) atomicAdd(&hist[bin], (uint32_t)__popc(peers));
-        } else if (bin >= 0) {
-            atomicAdd(&hist[bin], 1u);
+        }
+    } else {
+        // (interleaved sample: slot t holds sample (t % per) * 32 + t / per, if any;
+        // slots fit 32 bits.)  PU slots' loads are issued before their atomics.
+        const uint32_t per32 = (uint32_t)per, nsr = (uint32_t)ns_real;
+        constexpr int PU = 4;
+        for (int64_t b0 = 0; b0 < ns; b0 += PU * (int64_t)blockDim.x) {
+            uint32_t c[PU][W];
+            int pt[PU];
+#pragma unroll
+            for (int u = 0; u < PU; ++u) {
+                const int64_t t = b0 + (int64_t)u * blockDim.x + threadIdx.x;
+                const uint32_t t32 = (uint32_t)t;
+                const bool ok = t < ns && (per32 == 0 || (t32 % per32) * 32u + t32 / per32 < nsr);
+                pt[u] = -1;
+                if (ok) {
+                    load_code<W>(codes, t, c[u]);
+                    pt[u] = (int)part[t];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < PU; ++u)
+                if (pt[u] >= 0) atomicAdd(&hist[pt[u] * (L + 1) + hamming<W>(c[u], qc)], 1u);
         }
     }
     __syncthreads();
