@@ -902,6 +902,29 @@ __global__ void __launch_bounds__(1024) sort_by_bound(const float *__restrict__ 
         if (lane == 0) keys[i] = key;
     }
     __syncthreads();
+    if (np2 <= (int)blockDim.x) {
+        // one key per thread (blockDim.x, a power of two, keys padded): the stages
+        // with partner distance < 32 exchange through shuffles, the rest through smem
+        const int P = blockDim.x, i = threadIdx.x;
+        unsigned long long v = i < np2 ? keys[i] : ~0ull;
+        __syncthreads();
+        for (int size = 2; size <= P; size <<= 1)
+            for (int st = size >> 1; st > 0; st >>= 1) {
+                unsigned long long o;
+                if (st < 32) {
+                    o = __shfl_xor_sync(0xffffffffu, v, st);
+                } else {
+                    keys[i] = v;
+                    __syncthreads();
+                    o = keys[i ^ st];
+                    __syncthreads();
+                }
+                const bool up = (i & size) == 0, lower = (i & st) == 0;
+                v = (lower == up) ? (v < o ? v : o) : (v < o ? o : v);
+            }
+        if (i < Qb) qperm[i] = (int32_t)(uint32_t)v;
+        return;
+    }
     for (int size = 2; size <= np2; size <<= 1)
         for (int st = size >> 1; st > 0; st >>= 1) {
             for (int t = threadIdx.x; t < np2; t += blockDim.x) {
@@ -921,7 +944,7 @@ void launch_sort_by_bound(const float *Q, int d, int Qb, const uint32_t *theta_g
                           int32_t *qperm, cudaStream_t s) {
     int np2 = 2;
     while (np2 < Qb) np2 <<= 1;
-    sort_by_bound<<<1, 1024, (size_t)np2 * 8, s>>>(Q, d, Qb, theta_glob, qperm);
+    sort_by_bound<<<1, 1024, (size_t)std::max(np2, 1024) * 8, s>>>(Q, d, Qb, theta_glob, qperm);
     note_launch();
 }
 
