@@ -648,3 +648,58 @@ def test_tile_pruning_is_exact(built, case, monkeypatch):
         monkeypatch.setenv("NRLSH_GT_ALLTILES", "1")
         b, sb = idx.query(Qd, cfg.k, T)
         assert torch.equal(a, b) and torch.equal(sa.view(torch.int32), sb.view(torch.int32)), T
+
+
+# ------------------------------------------------------------------ unusual shapes
+ODD = [   # (n, d, L, m): odd d (scalar loads, unskewed norm chain), partial code words
+          # (L = 17, 50, 100), tiny d, d beyond the bf16 filters' range, ragged n
+    (12_345, 37, 17, 7),
+    (9_999, 150, 100, 5),
+    (7_777, 64, 50, 9),
+    (5_000, 2, 64, 3),
+    (3_001, 301, 128, 61),
+    (2_000, 513, 32, 10),
+]
+
+
+@pytest.mark.parametrize("shape", ODD, ids=_ids)
+def test_odd_shapes_parity(shape):
+    """Build, query (oracle codes injected) and exact top-k parity on shapes off the
+    configs' grid: every kernel's scalar / ragged / fallback variant."""
+    from dataclasses import replace
+    n, d, L, m = shape
+    P = _P()
+    cfg = replace(workloads.CONFIGS["c2"], name=f"odd{n}x{d}", n=n, d=d, nq=12)
+    X = workloads.make_items(cfg)
+    Q = workloads.make_queries(cfg)
+    Xd = torch.from_numpy(X).cuda()
+    idx = P.Index(Xd, L, m, seed=3)
+    orc = oracle.OracleIndex(X, idx.hash_bits, m, seed=3)
+    norm2, perm, offsets, V = idx.partition()
+    assert np.array_equal(norm2.view(np.uint64), orc.norm2.view(np.uint64))
+    assert np.array_equal(perm, orc.perm)
+    assert np.array_equal(offsets, orc.offsets)
+    assert np.array_equal(V, orc.V)
+    assert np.array_equal(idx.projection(), orc.A)
+    assert np.array_equal(idx.rank_table(), orc.R)
+    ocodes, z = orc.codes(want_z=True)
+    assert_codes_match(idx.codes()[np.argsort(perm, kind="stable")], ocodes, z, idx.hash_bits)
+    idx.set_codes(ocodes[orc.perm])
+    Qd = torch.from_numpy(Q).cuda()
+    gq = idx.query_codes(Qd).cpu().numpy().view(np.uint32)
+    oq = oracle.query_codes(Q, orc.A)
+    k = 10
+    for T in (1, 37, (n + 99) // 100, n // 3, n):
+        ids, sc = idx.query(Qd, k, T)
+        ids, sc = ids.cpu().numpy(), sc.cpu().numpy()
+        for qi in range(len(Q)):
+            if not np.array_equal(gq[qi], oq[qi]):
+                continue
+            a, s = oracle.query(X, ocodes, orc.part, orc.R, orc.A, Q[qi], T, k)
+            assert_topk_match(ids[qi], sc[qi], a, s, X, Q[qi])
+    gi, gs = P.exact_topk(Xd, Qd, k)
+    gi, gs = gi.cpu().numpy(), gs.cpu().numpy()
+    for qi in range(len(Q)):
+        a, s = oracle.exact_topk(X, Q[qi], k)
+        assert_topk_match(gi[qi], gs[qi], a, s, X, Q[qi])
+    idx.close()
