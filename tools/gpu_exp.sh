@@ -1,9 +1,5 @@
 mkdir -p gpurun_out
-(timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -2
-for ko in 0 1; do echo "KB_OUTER=$ko"; if [ $ko = 1 ]; then export NRLSH_GT_KB_OUTER=1; fi
+(timeout 900 python -m pytest tests -x -q -m gpu -k "candidates or query or rerank" 2>&1 | tail -2
 timeout 300 python tools/run_stage.py query --reps 3 2>&1 | tail -1
-timeout 300 python tools/run_stage.py gtseed --reps 3 2>&1 | tail -1
-done
-unset NRLSH_GT_KB_OUTER
-timeout 600 python bench.py --no-latency --no-cpu-baseline 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['value'], d['recall_at_10'], {k:round(v['ms_per_step'],3) for k,v in d['stage_ms_per_step'].items()}, d['e2e']['ms_per_step'])"
+NRLSH_RERANK_TC=0 timeout 300 python tools/run_stage.py query --reps 3 2>&1 | tail -1
 ) > gpurun_out/exp.log 2>&1
