@@ -319,14 +319,10 @@ struct GtEpiRow {
                 const int j = __ffs(m) - 1;
                 m &= m - 1;
                 const int col = c + 32 * hh + j;
-                float s_j = 0.f;
-#pragma unroll
-                for (int jj = 0; jj < 32; ++jj)
-                    if (jj == j) s_j = __uint_as_float(hh ? r1[jj] : r0[jj]);
-                const float x = xn[col];
-                if (__fmaf_ru(x, qe, s_j) < theta) continue;   // exact re-test
                 const int64_t i = i0 + col;   // row of Xb
                 if (i >= a->n) continue;
+                // (member mode: the candidate test first — most hits of a re-rank are
+                // not candidates of q, and it needs no score)
                 if (a->member) {   // candidate of q? (the select's rule; rows are positions)
                     const uint32_t *cw = scode + col * a->W;
                     int hq = 0;
@@ -336,6 +332,12 @@ struct GtEpiRow {
                     const uint32_t r = __ldg(a->R + spart[col] * (a->L + 1) + hq);
                     if (!(r < Bq || (r == Bq && (uint32_t)i <= pkq))) continue;
                 }
+                float s_j = 0.f;
+#pragma unroll
+                for (int jj = 0; jj < 32; ++jj)
+                    if (jj == j) s_j = __uint_as_float(hh ? r1[jj] : r0[jj]);
+                const float x = xn[col];
+                if (__fmaf_ru(x, qe, s_j) < theta) continue;   // exact re-test
                 if (sleft == 0) { sbase = atomicAdd(&a->cnt[q], 16u); sleft = 16; }
                 if (sbase + (16 - sleft) < a->C)
                     cl[sbase + (16 - sleft)] = a->perm ? __ldg(a->perm + i) : (int32_t)i;
