@@ -998,6 +998,10 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
                                   pt.get<unsigned long long>(), tid.get<int64_t>(), tsc.get<float>(), s);
                     launch_theta_from_topk(tid.get<int64_t>(), tsc.get<float>(), Qb, k,
                                            th.get<uint32_t>(), s);
+                    // the second pass appends to the first pass's exact top-k only
+                    if (!getenv("NRLSH_GT_RESCORE_ALL"))
+                        launch_restart_from_topk(tid.get<int64_t>(), Qb, k, cd.get<int32_t>(), Cg,
+                                                 cc.get<uint32_t>(), s);
                 }
             }
         } else {

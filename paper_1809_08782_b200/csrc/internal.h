@@ -201,6 +201,8 @@ void launch_dense_merge(const unsigned long long *partial, int S, int k, const i
 void launch_gather_f32(const float *src, const int32_t *idx, int64_t n, float *dst, cudaStream_t s);
 // theta_glob[q] = max(theta_glob[q], orderable image of out_scores[q][k-1]) when that
 // slot holds an item
+void launch_restart_from_topk(const int64_t *ids, int Qb, int k, int32_t *cand, int64_t C,
+                              uint32_t *cnt, cudaStream_t s);
 void launch_theta_from_topk(const int64_t *ids, const float *scores, int Qb, int k,
                             uint32_t *theta_glob, cudaStream_t s);
 // *out += sum_q min(cnt[q], C)

@@ -1161,6 +1161,28 @@ void launch_theta_from_topk(const int64_t *ids, const float *scores, int Qb, int
     note_launch();
 }
 
+// Restart each query's survivor list from its exact top-k so far (the first pass's
+// survivors re-ranked): top-k(A u B) = top-k(top-k(A) u B), so the final re-rank
+// only re-scores k rows of the first pass.  An overflowed list (cnt > C) is kept
+// as it is (the overflow redo needs its count).
+__global__ void restart_from_topk(const int64_t *__restrict__ ids, int Qb, int k,
+                                  int32_t *__restrict__ cand, int64_t C, uint32_t *__restrict__ cnt) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= Qb || (int64_t)cnt[q] > C) return;
+    uint32_t c = 0;
+    for (int t = 0; t < k && (int64_t)t < C; ++t) {
+        const int64_t id = ids[(int64_t)q * k + t];
+        if (id >= 0) cand[(int64_t)q * C + c++] = (int32_t)id;
+    }
+    cnt[q] = c;
+}
+
+void launch_restart_from_topk(const int64_t *ids, int Qb, int k, int32_t *cand, int64_t C,
+                              uint32_t *cnt, cudaStream_t s) {
+    restart_from_topk<<<(Qb + 255) / 256, 256, 0, s>>>(ids, Qb, k, cand, C, cnt);
+    note_launch();
+}
+
 __global__ void collect_overflow(const uint32_t *__restrict__ cnt, int Qb, int64_t C, int64_t q0,
                                  int64_t *__restrict__ list, uint32_t *__restrict__ n) {
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
