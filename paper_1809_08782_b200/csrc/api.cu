@@ -412,13 +412,16 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
     }
     e = cudaStreamSynchronize(s);
     if (e) return cuda_fail(e, "codes");
-    {   // first-pass split of the filter's tiles: the ~2% of largest |x|
+    {   // first-pass split of the filter's tiles: the 1/800 (at least 16) with the
+        // largest |x| (c4: 0.15 vs 0.18 ms per 1024 seeded queries at 1/50, 0.37 vs
+        // 0.74 unseeded; the first pass's exact k-th best then prunes every other tile)
         const int64_t nt = (n + 127) / 128;
         if (nt >= 64) {
             std::vector<float> xm((size_t)nt);
             if ((e = cudaMemcpy(xm.data(), ix->tile_xmax, (size_t)nt * 4, cudaMemcpyDeviceToHost)))
                 return cuda_fail(e, "tile xmax");
-            const int64_t r = nt - std::max<int64_t>(1, nt / 50);
+            const int64_t div = getenv("NRLSH_GT_SPLIT_DIV") ? std::max(2, atoi(getenv("NRLSH_GT_SPLIT_DIV"))) : 800;
+            const int64_t r = nt - std::min<int64_t>(nt - 1, std::max<int64_t>(16, nt / div));
             std::nth_element(xm.begin(), xm.begin() + r, xm.end());
             ix->tile_xsplit = xm[(size_t)r];
         }

@@ -1,6 +1,6 @@
 mkdir -p gpurun_out
 (timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -2
-for ra in 0 1; do echo "RESCORE_ALL=$ra"; if [ $ra = 1 ]; then export NRLSH_GT_RESCORE_ALL=1; fi; timeout 300 python tools/run_stage.py gtseed --reps 3 2>&1 | tail -1; timeout 300 python tools/run_stage.py gt --reps 3 2>&1 | tail -1; done
-unset NRLSH_GT_RESCORE_ALL
+timeout 300 python tools/run_stage.py gtseed --reps 3 2>&1 | tail -1; timeout 300 python tools/run_stage.py gt --reps 3 2>&1 | tail -1
+timeout 300 python tools/run_stage.py gt --config scale --nq 1024 --reps 2 2>&1 | tail -1
 timeout 600 python bench.py --no-cpu-baseline --no-latency 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['value'], d['recall_at_10'], {k:round(v['ms_per_step'],3) for k,v in d['stage_ms_per_step'].items()})"
 ) > gpurun_out/exp.log 2>&1
