@@ -1,6 +1,3 @@
 mkdir -p gpurun_out
-(timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -2
-timeout 300 python tools/run_stage.py gtseed --reps 3 2>&1 | tail -1; timeout 300 python tools/run_stage.py gt --reps 3 2>&1 | tail -1
-timeout 300 python tools/run_stage.py gt --config scale --nq 1024 --reps 2 2>&1 | tail -1
-timeout 600 python bench.py --no-cpu-baseline --no-latency 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['value'], d['recall_at_10'], {k:round(v['ms_per_step'],3) for k,v in d['stage_ms_per_step'].items()})"
+(for dv in 50 200 800; do echo "DIV=$dv"; export NRLSH_GT_SPLIT_DIV=$dv; timeout 300 python tools/run_stage.py gt --config scale --nq 1024 --reps 2 2>&1 | tail -1; timeout 300 python tools/run_stage.py gtseed --config scale --nq 1024 --reps 2 2>&1 | tail -1; timeout 300 python tools/run_stage.py gt --config c3 --nq 1024 --reps 2 2>&1 | tail -1; done
 ) > gpurun_out/exp.log 2>&1
