@@ -705,6 +705,8 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
                                   rtsc.get<float>(), s);
                     launch_theta_from_topk(rtid.get<int64_t>(), rtsc.get<float>(), Qb, k,
                                            rth.get<uint32_t>(), s);
+                    launch_restart_from_topk(rtid.get<int64_t>(), Qb, k, rcd.get<int32_t>(), Cg,
+                                             rcc.get<uint32_t>(), s);
                 }
             }
             // exact fp32 re-rank of the surviving candidates (same arithmetic as the
