@@ -880,29 +880,32 @@ __global__ void __launch_bounds__(256) gt_tile_lists(const uint16_t *__restrict_
 // queries in descending theta_q / |q| (unset theta last): grouping queries of similar
 // bound into the filter's 256-query pairs makes each pair's pruning bound (its
 // minimum) tight for all but the last pair
-__global__ void __launch_bounds__(1024) sort_by_bound(const float *__restrict__ Q, int d, int Qb,
-                                                      const uint32_t *__restrict__ theta,
-                                                      int32_t *__restrict__ qperm) {
+// sort key of each query, theta_q / |q| descending (a warp per query row, all SMs;
+// the key only orders the pairs, so any |q| rounding is fine), written over qperm
+__global__ void __launch_bounds__(256) bound_keys(const float *__restrict__ Q, int d, int Qb,
+                                                  const uint32_t *__restrict__ theta,
+                                                  uint32_t *__restrict__ key_out) {
+    const int lane = threadIdx.x & 31;
+    const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (i >= Qb) return;
+    float ss = 0.f;
+    for (int e = lane; e < d; e += 32) ss = fmaf(Q[(int64_t)i * d + e], Q[(int64_t)i * d + e], ss);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if (lane == 0) {
+        const uint32_t o = theta[i];
+        const float th = o ? float_unorder(o) : 0.f;
+        const float kf = (th > 0.f && ss > 0.f) ? th / sqrtf(ss) : 0.f;
+        key_out[i] = ~float_order(kf);
+    }
+}
+
+__global__ void __launch_bounds__(1024) sort_by_bound(int Qb, int32_t *__restrict__ qperm) {
     extern __shared__ unsigned long long keys[];
     int np2 = 2;
     while (np2 < Qb) np2 <<= 1;
-    // a warp per query row (coalesced); the key only orders the pairs (any |q|
-    // rounding is fine)
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int i = warp; i < np2; i += nw) {
-        unsigned long long key = ~0ull;
-        if (i < Qb) {
-            float ss = 0.f;
-            for (int e = lane; e < d; e += 32) ss = fmaf(Q[(int64_t)i * d + e], Q[(int64_t)i * d + e], ss);
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-            const uint32_t o = theta[i];
-            const float th = o ? float_unorder(o) : 0.f;
-            const float kf = (th > 0.f && ss > 0.f) ? th / sqrtf(ss) : 0.f;
-            key = ((unsigned long long)(~float_order(kf)) << 32) | (uint32_t)i;
-        }
-        if (lane == 0) keys[i] = key;
-    }
+    for (int i = threadIdx.x; i < np2; i += blockDim.x)
+        keys[i] = i < Qb ? ((unsigned long long)(uint32_t)qperm[i] << 32) | (uint32_t)i : ~0ull;
     __syncthreads();
     if (np2 <= (int)blockDim.x) {
         // one key per thread (blockDim.x, a power of two, keys padded): the stages
@@ -946,7 +949,9 @@ void launch_sort_by_bound(const float *Q, int d, int Qb, const uint32_t *theta_g
                           int32_t *qperm, cudaStream_t s) {
     int np2 = 2;
     while (np2 < Qb) np2 <<= 1;
-    sort_by_bound<<<1, 1024, (size_t)std::max(np2, 1024) * 8, s>>>(Q, d, Qb, theta_glob, qperm);
+    bound_keys<<<(Qb + 7) / 8, 256, 0, s>>>(Q, d, Qb, theta_glob, reinterpret_cast<uint32_t *>(qperm));
+    note_launch();
+    sort_by_bound<<<1, 1024, (size_t)std::max(np2, 1024) * 8, s>>>(Qb, qperm);
     note_launch();
 }
 
