@@ -135,27 +135,38 @@ __global__ void __launch_bounds__(256) gt_seed_theta(const float *__restrict__ X
     const int q = blockIdx.x;
     const float *qp = Q + (int64_t)q * d;
     const int np2 = ks <= 1 ? 1 : 1 << (32 - __clz(ks - 1));
-    for (int t = threadIdx.x; t < np2; t += blockDim.x) {
+    // a warp per seed, lanes over the dimensions (32 partial FMA chains and a 5-level
+    // tree: an error bound below the sequential chain's, which eps_rel covers)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int t = warp; t < np2; t += nw) {
         int64_t id = t < ks ? seeds[(int64_t)q * ks + t] : -1;
         if (id >= n) id = -1;
         // duplicates count once: keep the first occurrence only
-        for (int u = 0; u < t && id >= 0; ++u)
-            if (seeds[(int64_t)q * ks + u] == id) id = -1;
+        bool dup = false;
+        for (int u = lane; u < t && id >= 0; u += 32) dup |= seeds[(int64_t)q * ks + u] == id;
+        if (__any_sync(0xffffffffu, dup)) id = -1;
         float lb = -INFINITY;
-        if (id >= 0) {
+        if (id >= 0) {   // (warp-uniform)
             const float *xp = X + id * d;
             float acc = 0.f;
             double xx = 0.0;
-            for (int j = 0; j < d; ++j) {
+            for (int j = lane; j < d; j += 32) {
                 const float xv = __ldg(xp + j);
                 acc = fmaf(__ldg(qp + j), xv, acc);
                 xx += (double)xv * (double)xv;
             }
-            const float xn = __double2float_ru(sqrt(xx));
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                xx += __shfl_xor_sync(0xffffffffu, xx, o);
+            }
+            const float xn = __double2float_ru(sqrt(xx) * (1.0 + 0x1p-50));
             lb = __fsub_rd(acc, __fmul_ru(__fmul_ru(eps_rel, qnorm[q]), xn));
         }
-        lbs[t] = lb;
-        sid[t] = id;
+        if (lane == 0) {
+            lbs[t] = lb;
+            sid[t] = id;
+        }
     }
     __syncthreads();
     // sort descending
