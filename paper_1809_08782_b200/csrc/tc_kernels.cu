@@ -802,6 +802,8 @@ size_t gt_heap_bytes(int k) {
 // pair (j holds candidates of q only then: R[j][h] grows with h).
 // (grid: x = chunks of 1024 tiles, y = query pairs; list order is arbitrary — the
 // filter's splits interleave the list anyway; count[] must be zeroed beforehand)
+constexpr int kTlChunk = 256;   // tiles per list-building CTA (one per thread)
+
 __global__ void __launch_bounds__(256) gt_tile_lists(const uint16_t *__restrict__ R, int L, int m,
                                                      const uint8_t *__restrict__ part, int64_t n,
                                                      const uint32_t *__restrict__ sel_B, int Qb, int nt,
@@ -854,7 +856,7 @@ __global__ void __launch_bounds__(256) gt_tile_lists(const uint16_t *__restrict_
     const int64_t ntiles = (n + nt - 1) / nt;
     const int64_t n128 = (n + 127) / 128;
     const int lane = threadIdx.x & 31;
-    for (int64_t t = (int64_t)blockIdx.x * 1024 + threadIdx.x; t < min(ntiles, (int64_t)(blockIdx.x + 1) * 1024);
+    for (int64_t t = (int64_t)blockIdx.x * kTlChunk + threadIdx.x; t < min(ntiles, (int64_t)(blockIdx.x + 1) * kTlChunk);
          t += blockDim.x) {
         const int64_t a0 = t * (nt / 128);
         float xm = xmax128[a0];
@@ -1134,7 +1136,7 @@ int launch_gt_filter_tc(const void *Xb, int64_t n, int d, int dp, const void *Qb
     for (int pass = p_lo; pass < p_hi; ++pass) {
         if (lists) {   // per query pair, only the tiles that can hold an answer (GtTiles)
             cudaMemsetAsync(const_cast<int32_t *>(a.tcount), 0, (size_t)a.nqp * 4, s);
-            gt_tile_lists<<<dim3((unsigned)((ntiles + 1023) / 1024), a.nqp), 256, 0, s>>>(mb ? mb->R : nullptr, mb ? mb->L : 0, mb ? mb->m : 0,
+            gt_tile_lists<<<dim3((unsigned)((ntiles + kTlChunk - 1) / kTlChunk), a.nqp), 256, 0, s>>>(mb ? mb->R : nullptr, mb ? mb->L : 0, mb ? mb->m : 0,
                                                 mb ? mb->part : nullptr, n, mb ? mb->sel_B : nullptr,
                                                 Qb, NT, tl->xmax128, theta_glob, qnorm, 2.0 * eps_rel,
                                                 tl->xsplit, two ? pass + 1 : 0,
