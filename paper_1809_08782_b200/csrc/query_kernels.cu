@@ -899,7 +899,7 @@ __global__ void __launch_bounds__(1024) k7_select(
     __shared__ uint32_t ws[32];
     __shared__ uint32_t h256[256];
     __shared__ int sB, s_bseed;
-    __shared__ uint32_t sLt, s_out, s_pfx, s_kth;
+    __shared__ uint32_t sLt, s_out, s_pfx, s_kth, s_seed;
     const int q = blockIdx.x;
     const int64_t c = min((int64_t)cnt[q], C);
     const unsigned long long *b = buf + (int64_t)q * C;
@@ -986,11 +986,23 @@ __global__ void __launch_bounds__(1024) k7_select(
     __syncthreads();
     uint32_t *teq = hist;   // the histogram is dead once B and n_eq are known
     const bool in_smem = need_eq < n_eq && n_eq <= (uint32_t)tie_cap;
+    // the seeds ride along with the tie gather when they all rank before B (they then
+    // need no tie cut-off): one pass over the buffer fewer
+    const uint32_t Bsd = (uint32_t)s_bseed;
+    const bool merge_seeds = mode == 1 && seeds && in_smem && Bsd < B;
+    if (threadIdx.x == 0) s_seed = 0;
+    __syncthreads();
     if (in_smem) {
         for (int64_t e = threadIdx.x; e < c; e += blockDim.x) {
             const unsigned long long v = b[e];
             const uint32_t f = (uint32_t)(v >> 32);
-            if (f < (uint32_t)NR && sRt[f] == B) teq[atomicAdd(&s_out, 1u)] = (uint32_t)v;
+            if (f >= (uint32_t)NR) continue;
+            const uint32_t r = sRt[f];
+            if (r == B) teq[atomicAdd(&s_out, 1u)] = (uint32_t)v;
+            else if (merge_seeds && r <= Bsd) {
+                const uint32_t slot = atomicAdd(&s_seed, 1u);
+                if (slot < (uint32_t)ks) seeds[(int64_t)q * ks + slot] = perm[(uint32_t)v];
+            }
         }
         __syncthreads();
         for (int shift = 24; shift >= 0; shift -= 8) {
@@ -1061,7 +1073,10 @@ __global__ void __launch_bounds__(1024) k7_select(
     const uint32_t pk = s_pfx;
     if (mode == 1) {
         if (threadIdx.x == 0) { sel_B[q] = B; sel_pk[q] = pk; }
-        if (seeds) {   // up to ks candidates among the best-ranked structure positions
+        if (seeds && merge_seeds) {   // (gathered with the ties)
+            for (uint32_t t = min(s_seed, (uint32_t)ks) + threadIdx.x; t < (uint32_t)ks; t += blockDim.x)
+                seeds[(int64_t)q * ks + t] = -1;
+        } else if (seeds) {   // up to ks candidates among the best-ranked structure positions
             if (threadIdx.x == 0) s_out = 0;
             __syncthreads();
             const uint32_t Bs = (uint32_t)s_bseed;
