@@ -168,8 +168,10 @@ void launch_norms(const float *X, int64_t n, int d, double *norm2, unsigned long
     const int ld = (d % 2 == 1) ? d : d + 1;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    int RT = 64;   // two stages of <= 100 KB: >= 2 CTAs (>= 128 summing threads) per SM
-    while (RT > 32 && (size_t)2 * RT * d * 4 > 100 * 1024) RT >>= 1;
+    // rows per tile: two stages of <= 120 KB, a multiple of 32, at most 96 (c4,
+    // d = 150: 96 rows, one CTA per SM, 0.30 ms; 64 rows, two CTAs, 0.385 ms)
+    int RT = (int)std::min<int64_t>(96, std::max<int64_t>(32, (120 * 1024 / (8 * (int64_t)d)) / 32 * 32));
+    if (getenv("NRLSH_NORMS_RT")) RT = std::max(32, std::min(128, atoi(getenv("NRLSH_NORMS_RT")) / 32 * 32));
     if (((uintptr_t)X & 15u) == 0 && (size_t)2 * RT * d * 4 <= 200 * 1024 && !getenv("NRLSH_NORMS_OLD")) {
         const size_t sm = (size_t)2 * RT * d * 4;
         cudaFuncSetAttribute(k1_norms_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
