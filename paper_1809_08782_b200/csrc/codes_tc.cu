@@ -26,6 +26,8 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "internal.h"
@@ -384,11 +386,18 @@ static size_t codes_tc_smem(int KB, int N, int stages, int raw) {
            (size_t)N * 4 + (2 * stages + 4) * 8 + 32 + 4 * CT_M * 4;
 }
 
-// (MMA stages, raw slots): most loads in flight first (raw 4 = 48 KB ahead per SM),
-// then MMA stages
+// (MMA stages, raw slots): two MMA stages and up to 4 raw slots (48 KB of loads in
+// flight per SM).  A third MMA stage measured slower (c4: 1.16 vs 0.85 ms) — the
+// shared-memory carve-out it takes comes out of L1, which the cp.async loads and
+// the row-copy stores go through.
 static void codes_tc_config(int d, int N, int &stages, int &raw) {
     const int KB = (d + CT_KB - 1) / CT_KB;
-    const int opts[][2] = {{3, 4}, {2, 4}, {2, 3}, {2, 2}};
+    if (getenv("NRLSH_CODES_CFG")) {   // experiments: "stages,raw"
+        int st = 0, rw = 0;
+        if (sscanf(getenv("NRLSH_CODES_CFG"), "%d,%d", &st, &rw) == 2 && st >= 2 && rw >= 2 && rw <= 4 &&
+            codes_tc_smem(KB, N, st, rw) <= 227 * 1024) { stages = st; raw = rw; return; }
+    }
+    const int opts[][2] = {{2, 4}, {2, 3}, {2, 2}};
     for (const auto &o : opts)
         if (codes_tc_smem(KB, N, o[0], o[1]) <= 227 * 1024) { stages = o[0]; raw = o[1]; return; }
     stages = raw = 0;
