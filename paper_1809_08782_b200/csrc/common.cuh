@@ -10,6 +10,36 @@
 
 namespace nrlsh {
 
+// Programmatic dependent launch: a kernel launched with launch_pdl may start (its
+// CTAs scheduled, prologue run) while the previous kernel on the stream drains;
+// it must call pdl_wait() before touching anything that kernel wrote (the wait
+// returns once the predecessor has completed and its writes are visible).
+// NRLSH_NO_PDL=1 launches plainly (A/B experiments).
+__device__ __forceinline__ void pdl_wait() {
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 900)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t s, Args... args) {
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
+
 constexpr int kMaxParts = 256;     // uint8 partition ids
 constexpr int kMaxWords = 4;       // code_bits <= 128
 

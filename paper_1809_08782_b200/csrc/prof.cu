@@ -1,3 +1,4 @@
+#include <cstdlib>
 // prof.cu — per-kernel-class CUDA-event timing and launch counting (the
 // library's own tracing; used by bench.py to time the dominant kernel live on
 // the stream it is launched on).
@@ -25,6 +26,10 @@ static double g_ms[kNumSlots];
 static long long g_cnt[kNumSlots];
 
 void note_launch(int k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+bool pdl_enabled() {
+    static const bool on = !(getenv("NRLSH_NO_PDL") && atoi(getenv("NRLSH_NO_PDL")) != 0);
+    return on;
+}
 long long launch_count() { return g_launches.load(); }
 
 static cudaEvent_t get_event() {

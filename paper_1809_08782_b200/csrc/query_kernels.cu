@@ -646,6 +646,7 @@ __global__ void __launch_bounds__(1024) k6_fallback(
     const uint16_t *__restrict__ R, int64_t Tq, unsigned long long *__restrict__ buf,
     uint32_t *__restrict__ cnt, const uint32_t *__restrict__ cntv, int64_t C,
     int *__restrict__ flags) {
+    pdl_wait();
     extern __shared__ uint32_t hist[];
     __shared__ uint32_t ws[32];
     __shared__ int sB;
@@ -701,6 +702,7 @@ constexpr int kFbMax = 64;   // failed queries handled per sub-batch this way
 __global__ void fb_list(const uint32_t *__restrict__ cnt, const uint32_t *__restrict__ cntv, int Qb,
                         int64_t Tq, int64_t C, int32_t *__restrict__ fl, uint32_t *__restrict__ nf,
                         int *__restrict__ flags) {
+    pdl_wait();
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= Qb) return;
     const uint32_t v = cntv ? cntv[q] : cnt[q];
@@ -717,6 +719,7 @@ __global__ void __launch_bounds__(1024) fb_hist(const uint32_t *__restrict__ cod
                                                 const uint16_t *__restrict__ R,
                                                 const int32_t *__restrict__ fl, const uint32_t *__restrict__ nf,
                                                 uint32_t *__restrict__ ghist) {
+    pdl_wait();
     extern __shared__ uint32_t hist[];
     const int nfl = (int)min(*nf, (uint32_t)kFbMax);
     const int lane = threadIdx.x & 31;
@@ -752,6 +755,7 @@ __global__ void __launch_bounds__(1024) fb_bound(const int32_t *__restrict__ fl,
                                                  const uint32_t *__restrict__ nf, int NR, int64_t Tq,
                                                  uint32_t *__restrict__ ghist, uint32_t *__restrict__ Bout,
                                                  uint32_t *__restrict__ cnt, uint32_t *__restrict__ cntv) {
+    pdl_wait();
     __shared__ uint32_t ws[32];
     __shared__ int sB;
     const int nfl = (int)min(*nf, (uint32_t)kFbMax);
@@ -792,6 +796,7 @@ __global__ void __launch_bounds__(1024) fb_take(const uint32_t *__restrict__ cod
                                                 const uint32_t *__restrict__ Bq,
                                                 unsigned long long *__restrict__ buf, uint32_t *__restrict__ cnt,
                                                 uint32_t *__restrict__ cntv, int64_t C) {
+    pdl_wait();
     const int nfl = (int)min(*nf, (uint32_t)kFbMax);
     const int lane = threadIdx.x & 31;
     for (int w = blockIdx.x; w < nfl * kFbSlices; w += gridDim.x) {
@@ -846,14 +851,14 @@ void launch_fallback(const nrlsh_index *ix, const uint32_t *qcodes, int Qb, int6
         uint32_t *Bq = reinterpret_cast<uint32_t *>(fl + kFbMax);
         uint32_t *nf = Bq + kFbMax;
         cudaMemsetAsync(nf, 0, 4, s);
-        fb_list<<<(Qb + 255) / 256, 256, 0, s>>>(cnt, cv_sep, Qb, Tq, C, fl, nf, flags);
+        launch_pdl(fb_list, dim3((Qb + 255) / 256), dim3(256), 0, s, cnt, cv_sep, Qb, Tq, C, fl, nf, flags);
         const size_t sm = (size_t)NR * 4;
 #define NR_FB(W_)                                                                                   \
         cudaFuncSetAttribute(fb_hist<W_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);    \
-        fb_hist<W_><<<sms, 1024, sm, s>>>(ix->codes, ix->part_of_pos, ix->n, qcodes, ix->L, NR,     \
+        launch_pdl(fb_hist<W_>, dim3(sms), dim3(1024), sm, s, ix->codes, ix->part_of_pos, ix->n, qcodes, ix->L, NR,     \
                                           ix->R_d, fl, nf, ghist);                                  \
-        fb_bound<<<sms, 1024, 0, s>>>(fl, nf, NR, Tq, ghist, Bq, cnt, cv_sep);                      \
-        fb_take<W_><<<sms, 1024, 0, s>>>(ix->codes, ix->part_of_pos, ix->n, qcodes, ix->L, ix->R_d, \
+        launch_pdl(fb_bound, dim3(sms), dim3(1024), 0, s, fl, nf, NR, Tq, ghist, Bq, cnt, cv_sep);                      \
+        launch_pdl(fb_take<W_>, dim3(sms), dim3(1024), 0, s, ix->codes, ix->part_of_pos, ix->n, qcodes, ix->L, ix->R_d, \
                                          fl, nf, Bq, buf, cnt, cv_sep, C)
         if (ix->W == 1) { NR_FB(1); } else if (ix->W == 2) { NR_FB(2); } else { NR_FB(4); }
 #undef NR_FB
@@ -866,15 +871,15 @@ void launch_fallback(const nrlsh_index *ix, const uint32_t *qcodes, int Qb, int6
     switch (ix->W) {
         case 1:
             cudaFuncSetAttribute(k6_fallback<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            k6_fallback<1><<<Qb, 1024, sm, s>>>(ix->codes, ix->part_of_pos, ix->n, qcodes, ix->L, ix->m, order, ix->R_d, Tq, buf, cnt, cntv, C, par ? nullptr : flags);
+            launch_pdl(k6_fallback<1>, dim3(Qb), dim3(1024), sm, s, ix->codes, ix->part_of_pos, ix->n, qcodes, ix->L, ix->m, order, ix->R_d, Tq, buf, cnt, cntv, C, par ? nullptr : flags);
             break;
         case 2:
             cudaFuncSetAttribute(k6_fallback<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            k6_fallback<2><<<Qb, 1024, sm, s>>>(ix->codes, ix->part_of_pos, ix->n, qcodes, ix->L, ix->m, order, ix->R_d, Tq, buf, cnt, cntv, C, par ? nullptr : flags);
+            launch_pdl(k6_fallback<2>, dim3(Qb), dim3(1024), sm, s, ix->codes, ix->part_of_pos, ix->n, qcodes, ix->L, ix->m, order, ix->R_d, Tq, buf, cnt, cntv, C, par ? nullptr : flags);
             break;
         default:
             cudaFuncSetAttribute(k6_fallback<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            k6_fallback<4><<<Qb, 1024, sm, s>>>(ix->codes, ix->part_of_pos, ix->n, qcodes, ix->L, ix->m, order, ix->R_d, Tq, buf, cnt, cntv, C, par ? nullptr : flags);
+            launch_pdl(k6_fallback<4>, dim3(Qb), dim3(1024), sm, s, ix->codes, ix->part_of_pos, ix->n, qcodes, ix->L, ix->m, order, ix->R_d, Tq, buf, cnt, cntv, C, par ? nullptr : flags);
             break;
     }
     note_launch();
@@ -1164,6 +1169,7 @@ void launch_gather_f32(const float *src, const int32_t *idx, int64_t n, float *d
 
 __global__ void theta_from_topk(const int64_t *__restrict__ ids, const float *__restrict__ sc, int Qb,
                                 int k, uint32_t *__restrict__ theta_glob) {
+    pdl_wait();
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= Qb) return;
     const int64_t e = (int64_t)q * k + k - 1;
@@ -1172,7 +1178,7 @@ __global__ void theta_from_topk(const int64_t *__restrict__ ids, const float *__
 
 void launch_theta_from_topk(const int64_t *ids, const float *scores, int Qb, int k,
                             uint32_t *theta_glob, cudaStream_t s) {
-    theta_from_topk<<<(Qb + 255) / 256, 256, 0, s>>>(ids, scores, Qb, k, theta_glob);
+    launch_pdl(theta_from_topk, dim3((Qb + 255) / 256), dim3(256), 0, s, ids, scores, Qb, k, theta_glob);
     note_launch();
 }
 
@@ -1200,12 +1206,14 @@ void launch_restart_from_topk(const int64_t *ids, int Qb, int k, int32_t *cand, 
 
 __global__ void collect_overflow(const uint32_t *__restrict__ cnt, int Qb, int64_t C, int64_t q0,
                                  int64_t *__restrict__ list, uint32_t *__restrict__ n) {
+    pdl_wait();
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q < Qb && (int64_t)cnt[q] > C) list[atomicAdd(n, 1u)] = q0 + q;
 }
 
 __global__ void sum_counts(const uint32_t *__restrict__ cnt, int Qb, int64_t C,
                            unsigned long long *__restrict__ out) {
+    pdl_wait();
     unsigned long long v = 0;
     for (int q = threadIdx.x; q < Qb; q += blockDim.x) v += (unsigned long long)min((int64_t)cnt[q], C);
 #pragma unroll
@@ -1215,7 +1223,7 @@ __global__ void sum_counts(const uint32_t *__restrict__ cnt, int Qb, int64_t C,
 
 void launch_sum_counts(const uint32_t *cnt, int Qb, int64_t C, unsigned long long *out,
                        cudaStream_t s) {
-    sum_counts<<<1, 256, 0, s>>>(cnt, Qb, C, out);
+    launch_pdl(sum_counts, dim3(1), dim3(256), 0, s, cnt, Qb, C, out);
     note_launch();
 }
 
@@ -1244,7 +1252,7 @@ void launch_count_stats(const uint32_t *cnt, int Qb, unsigned long long *out, cu
 
 void launch_collect_overflow(const uint32_t *cnt, int Qb, int64_t C, int64_t q0, int64_t *list,
                              uint32_t *n, cudaStream_t s) {
-    collect_overflow<<<(Qb + 255) / 256, 256, 0, s>>>(cnt, Qb, C, q0, list, n);
+    launch_pdl(collect_overflow, dim3((Qb + 255) / 256), dim3(256), 0, s, cnt, Qb, C, q0, list, n);
     note_launch();
 }
 
@@ -1501,6 +1509,7 @@ __global__ void __launch_bounds__(kRrThreads) k8_rerank(
     const uint32_t *__restrict__ ncand_per_q, int stride, int k, int cap, int64_t slice,
     unsigned long long *__restrict__ partial, int64_t *__restrict__ out_ids,
     float *__restrict__ out_scores) {
+    pdl_wait();
     extern __shared__ __align__(16) unsigned long long rr_smem[];
     unsigned long long *buf = rr_smem;                       // [cap]
     float *sq = reinterpret_cast<float *>(buf + cap);        // [dpad]
@@ -1737,6 +1746,7 @@ __global__ void __launch_bounds__(256) k8_rerank_merge(const unsigned long long 
                                                        int gy, int k, int np2,
                                                        int64_t *__restrict__ out_ids,
                                                        float *__restrict__ out_scores) {
+    pdl_wait();
     extern __shared__ unsigned long long mk[];
     const int q = blockIdx.x;
     const int tot = gy * k;
@@ -1792,7 +1802,7 @@ void launch_rerank(const float *X, int d, int ldx, const float *Q, int Qb, const
     do {                                                                                       \
         cudaFuncSetAttribute(k8_rerank<V, N>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
                              (int)sm);                                                         \
-        k8_rerank<V, N><<<grid, kRrThreads, sm, s>>>(X, ldx, d, Q, cand, cand_ld, ncand,       \
+        launch_pdl(k8_rerank<V, N>, dim3(grid), dim3(kRrThreads), sm, s, X, ldx, d, Q, cand, cand_ld, ncand,       \
                                                      ncand_per_q, stride, k, cap, slice, pp,   \
                                                      out_ids, out_scores);                     \
     } while (0)
@@ -1813,7 +1823,7 @@ void launch_rerank(const float *X, int d, int ldx, const float *Q, int Qb, const
     if (gy > 1) {
         const int np2 = pow2_at_least((int64_t)gy * k);
         cudaFuncSetAttribute(k8_rerank_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, np2 * 8);
-        k8_rerank_merge<<<Qb, 256, (size_t)np2 * 8, s>>>(partial, gy, k, np2, out_ids, out_scores);
+        launch_pdl(k8_rerank_merge, dim3(Qb), dim3(256), (size_t)np2 * 8, s, partial, gy, k, np2, out_ids, out_scores);
         note_launch();
     }
 }
@@ -1863,7 +1873,7 @@ void launch_rerank_bf(const float *X, int d, int ldx, const void *Xb, int dpb, c
     if (gy > 1) {
         const int np2 = pow2_at_least((int64_t)gy * k);
         cudaFuncSetAttribute(k8_rerank_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, np2 * 8);
-        k8_rerank_merge<<<Qb, 256, (size_t)np2 * 8, s>>>(partial, gy, k, np2, out_ids, out_scores);
+        launch_pdl(k8_rerank_merge, dim3(Qb), dim3(256), (size_t)np2 * 8, s, partial, gy, k, np2, out_ids, out_scores);
         note_launch();
     }
 }

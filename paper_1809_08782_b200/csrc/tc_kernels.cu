@@ -33,6 +33,7 @@ namespace nrlsh {
 __global__ void bf16_prep(const float *__restrict__ X, int64_t n, int d, int dp,
                           __nv_bfloat16 *__restrict__ Xb, float *__restrict__ xnorm,
                           const int32_t *__restrict__ perm) {
+    pdl_wait();
     const int lane = threadIdx.x & 31;
     for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < n;
          i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
@@ -54,7 +55,7 @@ void launch_bf16_prep(const float *X, int64_t n, int d, int dp, void *Xb, float 
                       cudaStream_t s, const int32_t *perm) {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    bf16_prep<<<grid_for(n * 32, 256, sms * 16), 256, 0, s>>>(X, n, d, dp, (__nv_bfloat16 *)Xb,
+    launch_pdl(bf16_prep, dim3(grid_for(n * 32, 256, sms * 16)), dim3(256), 0, s, X, n, d, dp, (__nv_bfloat16 *)Xb,
                                                              xnorm, perm);
     note_launch();
 }
@@ -815,6 +816,7 @@ __global__ void __launch_bounds__(256) gt_tile_lists(const uint16_t *__restrict_
                                                      int32_t *__restrict__ count,
                                                      unsigned long long *__restrict__ pairs,
                                                      const int32_t *__restrict__ qperm) {
+    pdl_wait();
     __shared__ uint32_t act[257];
     __shared__ uint32_t sB[2 * GT_M];
     __shared__ float s_tau;
@@ -887,6 +889,7 @@ __global__ void __launch_bounds__(256) gt_tile_lists(const uint16_t *__restrict_
 __global__ void __launch_bounds__(256) bound_keys(const float *__restrict__ Q, int d, int Qb,
                                                   const uint32_t *__restrict__ theta,
                                                   uint32_t *__restrict__ key_out) {
+    pdl_wait();
     const int lane = threadIdx.x & 31;
     const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (i >= Qb) return;
@@ -903,6 +906,7 @@ __global__ void __launch_bounds__(256) bound_keys(const float *__restrict__ Q, i
 }
 
 __global__ void __launch_bounds__(1024) sort_by_bound(int Qb, int32_t *__restrict__ qperm) {
+    pdl_wait();
     extern __shared__ unsigned long long keys[];
     int np2 = 2;
     while (np2 < Qb) np2 <<= 1;
@@ -951,9 +955,9 @@ void launch_sort_by_bound(const float *Q, int d, int Qb, const uint32_t *theta_g
                           int32_t *qperm, cudaStream_t s) {
     int np2 = 2;
     while (np2 < Qb) np2 <<= 1;
-    bound_keys<<<(Qb + 7) / 8, 256, 0, s>>>(Q, d, Qb, theta_glob, reinterpret_cast<uint32_t *>(qperm));
+    launch_pdl(bound_keys, dim3((Qb + 7) / 8), dim3(256), 0, s, Q, d, Qb, theta_glob, reinterpret_cast<uint32_t *>(qperm));
     note_launch();
-    sort_by_bound<<<1, 1024, (size_t)std::max(np2, 1024) * 8, s>>>(Qb, qperm);
+    launch_pdl(sort_by_bound, dim3(1), dim3(1024), (size_t)std::max(np2, 1024) * 8, s, Qb, qperm);
     note_launch();
 }
 
@@ -1136,7 +1140,7 @@ int launch_gt_filter_tc(const void *Xb, int64_t n, int d, int dp, const void *Qb
     for (int pass = p_lo; pass < p_hi; ++pass) {
         if (lists) {   // per query pair, only the tiles that can hold an answer (GtTiles)
             cudaMemsetAsync(const_cast<int32_t *>(a.tcount), 0, (size_t)a.nqp * 4, s);
-            gt_tile_lists<<<dim3((unsigned)((ntiles + kTlChunk - 1) / kTlChunk), a.nqp), 256, 0, s>>>(mb ? mb->R : nullptr, mb ? mb->L : 0, mb ? mb->m : 0,
+            launch_pdl(gt_tile_lists, dim3(dim3((unsigned)((ntiles + kTlChunk - 1) / kTlChunk), a.nqp)), dim3(256), 0, s, mb ? mb->R : nullptr, mb ? mb->L : 0, mb ? mb->m : 0,
                                                 mb ? mb->part : nullptr, n, mb ? mb->sel_B : nullptr,
                                                 Qb, NT, tl->xmax128, theta_glob, qnorm, 2.0 * eps_rel,
                                                 tl->xsplit, two ? pass + 1 : 0,
