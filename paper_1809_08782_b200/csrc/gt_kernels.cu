@@ -130,6 +130,7 @@ __global__ void __launch_bounds__(256) gt_seed_theta(const float *__restrict__ X
                                                      const int64_t *__restrict__ seeds, int ks,
                                                      int k, float eps_rel,
                                                      uint32_t *__restrict__ theta_glob) {
+    pdl_wait();
     __shared__ float lbs[1024];
     __shared__ int64_t sid[1024];
     const int q = blockIdx.x;
@@ -191,7 +192,7 @@ __global__ void __launch_bounds__(256) gt_seed_theta(const float *__restrict__ X
 void launch_gt_seed_theta(const float *X, int64_t n, int d, const float *Q, int Qb,
                           const float *qnorm, const int64_t *seeds, int ks, int k, float eps_rel,
                           uint32_t *theta_glob, cudaStream_t s) {
-    gt_seed_theta<<<Qb, 256, 0, s>>>(X, n, d, Q, qnorm, seeds, ks, k, eps_rel, theta_glob);
+    launch_pdl(gt_seed_theta, dim3(Qb), dim3(256), 0, s, X, n, d, Q, qnorm, seeds, ks, k, eps_rel, theta_glob);
     note_launch();
 }
 

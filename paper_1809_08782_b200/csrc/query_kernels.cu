@@ -31,6 +31,7 @@ __global__ void __launch_bounds__(32 * W) k5_qcodes(const float *__restrict__ Q,
                                                     const float *__restrict__ Apad, int L,
                                                     uint32_t *__restrict__ qcodes,
                                                     int *__restrict__ flags, int64_t qbase) {
+    pdl_wait();
     extern __shared__ float sq[];
     const int64_t q = blockIdx.x;
     const float *qp = Q + q * (int64_t)d;
@@ -59,9 +60,9 @@ void launch_qcodes(const float *Q, int64_t nq, int d, const float *Apad, int L, 
                    uint32_t *qcodes, int *flags, int64_t qbase, cudaStream_t s) {
     const size_t sm = (size_t)d * 4;
     switch (W) {
-        case 1: k5_qcodes<1><<<(int)nq, 32, sm, s>>>(Q, d, Apad, L, qcodes, flags, qbase); break;
-        case 2: k5_qcodes<2><<<(int)nq, 64, sm, s>>>(Q, d, Apad, L, qcodes, flags, qbase); break;
-        default: k5_qcodes<4><<<(int)nq, 128, sm, s>>>(Q, d, Apad, L, qcodes, flags, qbase); break;
+        case 1: launch_pdl(k5_qcodes<1>, dim3((int)nq), dim3(32), sm, s, Q, d, Apad, L, qcodes, flags, qbase); break;
+        case 2: launch_pdl(k5_qcodes<2>, dim3((int)nq), dim3(64), sm, s, Q, d, Apad, L, qcodes, flags, qbase); break;
+        default: launch_pdl(k5_qcodes<4>, dim3((int)nq), dim3(128), sm, s, Q, d, Apad, L, qcodes, flags, qbase); break;
     }
     note_launch();
 }
@@ -192,6 +193,7 @@ __global__ void __launch_bounds__(1024) k6_pilot(
     const uint32_t *__restrict__ qcodes, int L, int m,
     const int32_t *__restrict__ order, const uint16_t *__restrict__ R, uint32_t need,
     int8_t *__restrict__ delta, uint32_t *__restrict__ cnt, int interleaved, int64_t ns_real) {
+    pdl_wait();
     extern __shared__ uint32_t hist[];
     __shared__ uint32_t ws[32];
     __shared__ int sB;
@@ -240,15 +242,15 @@ void launch_pilot(const nrlsh_index *ix, const uint32_t *qcodes, int Qb, int64_t
     switch (ix->W) {
         case 1:
             cudaFuncSetAttribute(k6_pilot<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            k6_pilot<1><<<Qb, 1024, sm, s>>>(sc, sp, ns, qcodes, ix->L, ix->m, order, ix->R_d, need, delta, cnt, cmp, (ix->n + stride - 1) / stride);
+            launch_pdl(k6_pilot<1>, dim3(Qb), dim3(1024), sm, s, sc, sp, ns, qcodes, ix->L, ix->m, order, ix->R_d, need, delta, cnt, cmp, (ix->n + stride - 1) / stride);
             break;
         case 2:
             cudaFuncSetAttribute(k6_pilot<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            k6_pilot<2><<<Qb, 1024, sm, s>>>(sc, sp, ns, qcodes, ix->L, ix->m, order, ix->R_d, need, delta, cnt, cmp, (ix->n + stride - 1) / stride);
+            launch_pdl(k6_pilot<2>, dim3(Qb), dim3(1024), sm, s, sc, sp, ns, qcodes, ix->L, ix->m, order, ix->R_d, need, delta, cnt, cmp, (ix->n + stride - 1) / stride);
             break;
         default:
             cudaFuncSetAttribute(k6_pilot<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            k6_pilot<4><<<Qb, 1024, sm, s>>>(sc, sp, ns, qcodes, ix->L, ix->m, order, ix->R_d, need, delta, cnt, cmp, (ix->n + stride - 1) / stride);
+            launch_pdl(k6_pilot<4>, dim3(Qb), dim3(1024), sm, s, sc, sp, ns, qcodes, ix->L, ix->m, order, ix->R_d, need, delta, cnt, cmp, (ix->n + stride - 1) / stride);
             break;
     }
     note_launch();
@@ -272,6 +274,7 @@ __global__ void __launch_bounds__(kScanThreads) k6_scan(
     const uint32_t *__restrict__ qcodes, const int8_t *__restrict__ delta, int Qb, int m,
     const uint16_t *__restrict__ R, int L, unsigned long long *__restrict__ buf,
     uint32_t *__restrict__ cnt, int64_t C, unsigned long long *__restrict__ pairs) {
+    pdl_wait();
     __shared__ uint32_t sq[kQG][W];
     __shared__ int sd[kQG];
     __shared__ uint32_t sbuf[kQG][kSB];
@@ -629,9 +632,9 @@ void launch_scan(const nrlsh_index *ix, const uint32_t *qcodes, const int8_t *de
         return;
     }
     switch (ix->W) {
-        case 1: k6_scan<1><<<grid, kScanThreads, 0, s>>>(ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs); break;
-        case 2: k6_scan<2><<<grid, kScanThreads, 0, s>>>(ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs); break;
-        default: k6_scan<4><<<grid, kScanThreads, 0, s>>>(ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs); break;
+        case 1: launch_pdl(k6_scan<1>, dim3(grid), dim3(kScanThreads), 0, s, ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs); break;
+        case 2: launch_pdl(k6_scan<2>, dim3(grid), dim3(kScanThreads), 0, s, ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs); break;
+        default: launch_pdl(k6_scan<4>, dim3(grid), dim3(kScanThreads), 0, s, ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs); break;
     }
     note_launch();
 }
@@ -899,6 +902,7 @@ __global__ void __launch_bounds__(1024) k7_select(
     uint32_t *__restrict__ sel_pk, uint32_t *__restrict__ cnt_part,
     const uint8_t *__restrict__ dense, uint32_t *__restrict__ ncand_out,
     int32_t *__restrict__ seeds, int ks) {
+    pdl_wait();
     extern __shared__ uint32_t hist[];   // [max(NR, tie_cap)] + R copy [NR] (uint16)
     uint16_t *sRt = reinterpret_cast<uint16_t *>(hist + tie_cap);
     __shared__ uint32_t ws[32];
@@ -1123,7 +1127,7 @@ void launch_select(const nrlsh_index *ix, int Qb, int64_t Tq, const unsigned lon
     const int tie_cap = std::max(NR, 16384);
     const size_t sm = (size_t)tie_cap * 4 + (size_t)NR * 2;
     cudaFuncSetAttribute(k7_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k7_select<<<Qb, 1024, sm, s>>>(buf, cnt, C, Tq, NR, tie_cap, ix->R_d, ix->perm, cand, cand_rank,
+    launch_pdl(k7_select, dim3(Qb), dim3(1024), sm, s, buf, cnt, C, Tq, NR, tie_cap, ix->R_d, ix->perm, cand, cand_rank,
                                    0, ix->L, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0);
     note_launch();
 }
@@ -1137,7 +1141,7 @@ void launch_select_split(const nrlsh_index *ix, int Qb, int64_t Tq, const unsign
     const int tie_cap = std::max(NR, 16384);
     const size_t sm = (size_t)tie_cap * 4 + (size_t)NR * 2;
     cudaFuncSetAttribute(k7_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k7_select<<<Qb, 1024, sm, s>>>(buf, cnt, C, Tq, NR, tie_cap, ix->R_d, ix->perm, cand, nullptr,
+    launch_pdl(k7_select, dim3(Qb), dim3(1024), sm, s, buf, cnt, C, Tq, NR, tie_cap, ix->R_d, ix->perm, cand, nullptr,
                                    mode, ix->L, sel_B, sel_pk, cnt_part, dense, ncand_out, nullptr, 0);
     note_launch();
 }
@@ -1149,7 +1153,7 @@ void launch_select_seeds(const nrlsh_index *ix, int Qb, int64_t Tq, const unsign
     const int tie_cap = std::max(NR, 16384);
     const size_t sm = (size_t)tie_cap * 4 + (size_t)NR * 2;
     cudaFuncSetAttribute(k7_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k7_select<<<Qb, 1024, sm, s>>>(buf, cnt, C, Tq, NR, tie_cap, ix->R_d, ix->perm, nullptr, nullptr,
+    launch_pdl(k7_select, dim3(Qb), dim3(1024), sm, s, buf, cnt, C, Tq, NR, tie_cap, ix->R_d, ix->perm, nullptr, nullptr,
                                    1, ix->L, sel_B, sel_pk, nullptr, nullptr, nullptr, seeds, ks);
     note_launch();
 }

@@ -425,6 +425,7 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
     __syncthreads();
     tc::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    pdl_wait();   // (the prologue above overlaps the previous kernel's tail)
     const int nunits = a.nqp * a.nsplit;
 
     if (warp == 0 && lane == 0) {
@@ -1159,10 +1160,10 @@ int launch_gt_filter_tc(const void *Xb, int64_t n, int d, int dp, const void *Qb
         }
         if (NT == 256) {
             cudaFuncSetAttribute(gt_filter_tc<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            gt_filter_tc<256><<<grid, GT_THREADS, sm, s>>>(tq, tx, a);
+            launch_pdl(gt_filter_tc<256>, dim3(grid), dim3(GT_THREADS), sm, s, tq, tx, a);
         } else {
             cudaFuncSetAttribute(gt_filter_tc<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            gt_filter_tc<128><<<grid, GT_THREADS, sm, s>>>(tq, tx, a);
+            launch_pdl(gt_filter_tc<128>, dim3(grid), dim3(GT_THREADS), sm, s, tq, tx, a);
         }
         note_launch();
     }
