@@ -672,11 +672,11 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
                 ProfScope p(SLOT_SCORE, s);
                 // certified warm start: the k-th best fp32 score (the final re-rank's own
                 // arithmetic) over KS best-ranked candidates bounds the answer's k-th score
-                cudaMemsetAsync(rth.p, 0, (size_t)Qb * 4, s);
                 launch_rerank(Xr, ix->d, ldr, Qd, Qb, rseed.get<int32_t>(), KS, KS, nullptr, 1, k,
                               rpt.get<unsigned long long>(), rtid.get<int64_t>(), rtsc.get<float>(), s);
+                // (assigns theta and zeroes the survivor counts: no memset nodes)
                 launch_theta_from_topk(rtid.get<int64_t>(), rtsc.get<float>(), Qb, k,
-                                       rth.get<uint32_t>(), s);
+                                       rth.get<uint32_t>(), s, true, rcc.get<uint32_t>());
             }
             ProfScope p(SLOT_RERANK, s);
             // bf16 query rows in descending theta/|q| (pairs of similar bound prune alike)
@@ -686,7 +686,6 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
             if (sorted) launch_sort_by_bound(Qd, ix->d, Qb, rth.get<uint32_t>(), rqp.get<int32_t>(), s);
             tls.qperm = sorted ? rqp.get<int32_t>() : nullptr;
             launch_bf16_prep(Qd, Qb, ix->d, ix->dpb, rqb.p, rqn.get<float>(), s, tls.qperm);
-            cudaMemsetAsync(rcc.p, 0, (size_t)Qb * 4, s);
             mb.qcodes = qc.get<uint32_t>();
             mb.sel_B = rsb.get<uint32_t>();
             mb.sel_pk = rspk.get<uint32_t>();

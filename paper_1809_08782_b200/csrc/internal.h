@@ -203,8 +203,11 @@ void launch_gather_f32(const float *src, const int32_t *idx, int64_t n, float *d
 // slot holds an item
 void launch_restart_from_topk(const int64_t *ids, int Qb, int k, int32_t *cand, int64_t C,
                               uint32_t *cnt, cudaStream_t s);
+// theta_glob[q] := (assign ? : max with) the order key of the k-th score (0 if none);
+// zero_cnt, if given, is zeroed per query on the way (saves a memset node)
 void launch_theta_from_topk(const int64_t *ids, const float *scores, int Qb, int k,
-                            uint32_t *theta_glob, cudaStream_t s);
+                            uint32_t *theta_glob, cudaStream_t s, bool assign = false,
+                            uint32_t *zero_cnt = nullptr);
 // *out += sum_q min(cnt[q], C)
 void launch_sum_counts(const uint32_t *cnt, int Qb, int64_t C, unsigned long long *out,
                        cudaStream_t s);

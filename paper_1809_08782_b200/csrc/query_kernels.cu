@@ -1172,17 +1172,21 @@ void launch_gather_f32(const float *src, const int32_t *idx, int64_t n, float *d
 }
 
 __global__ void theta_from_topk(const int64_t *__restrict__ ids, const float *__restrict__ sc, int Qb,
-                                int k, uint32_t *__restrict__ theta_glob) {
+                                int k, uint32_t *__restrict__ theta_glob, int assign,
+                                uint32_t *__restrict__ zero_cnt) {
     pdl_wait();
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= Qb) return;
     const int64_t e = (int64_t)q * k + k - 1;
-    if (ids[e] >= 0) theta_glob[q] = max(theta_glob[q], float_order(sc[e]));
+    const uint32_t o = ids[e] >= 0 ? float_order(sc[e]) : 0u;
+    theta_glob[q] = assign ? o : max(theta_glob[q], o);
+    if (zero_cnt) zero_cnt[q] = 0u;
 }
 
 void launch_theta_from_topk(const int64_t *ids, const float *scores, int Qb, int k,
-                            uint32_t *theta_glob, cudaStream_t s) {
-    launch_pdl(theta_from_topk, dim3((Qb + 255) / 256), dim3(256), 0, s, ids, scores, Qb, k, theta_glob);
+                            uint32_t *theta_glob, cudaStream_t s, bool assign, uint32_t *zero_cnt) {
+    launch_pdl(theta_from_topk, dim3((Qb + 255) / 256), dim3(256), 0, s, ids, scores, Qb, k, theta_glob,
+               (int)assign, zero_cnt);
     note_launch();
 }
 
