@@ -963,14 +963,16 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
         const float *qnb = qn.get<float>() + q0;
         int64_t *oid = (int64_t *)oi.dev + q0 * k;
         float *osc = (float *)os.dev + q0 * k;
-        cudaMemsetAsync(cc.p, 0, (size_t)Qb * 4, s);
+        // (the seeded bound kernel assigns theta and zeroes the survivor counts itself)
+        if (!(use_tc && seed_ids)) cudaMemsetAsync(cc.p, 0, (size_t)Qb * 4, s);
         if (use_tc) {
-            cudaMemsetAsync(th.p, 0, (size_t)Qb * 4, s);
             if (seed_ids) {
                 ProfScope p(SLOT_GT_NORMS, s);
                 launch_gt_seed_theta(X, n, d, Qb_ptr, Qb, qnb, (const int64_t *)Ss.dev + q0 * seed_k,
                                      seed_k, k, (float)(1.25 * (d + 2) * std::ldexp(1.0, -24)),
-                                     th.get<uint32_t>(), s);
+                                     th.get<uint32_t>(), s, cc.get<uint32_t>());
+            } else {
+                cudaMemsetAsync(th.p, 0, (size_t)Qb * 4, s);
             }
             ProfScope p(SLOT_GT_FILTER, s);
             const bool tiles = Xb_ix && tile_xmax_ix;

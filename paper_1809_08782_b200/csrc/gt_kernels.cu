@@ -129,7 +129,8 @@ __global__ void __launch_bounds__(256) gt_seed_theta(const float *__restrict__ X
                                                      const float *__restrict__ qnorm,
                                                      const int64_t *__restrict__ seeds, int ks,
                                                      int k, float eps_rel,
-                                                     uint32_t *__restrict__ theta_glob) {
+                                                     uint32_t *__restrict__ theta_glob,
+                                                     uint32_t *__restrict__ zero_cnt) {
     pdl_wait();
     __shared__ float lbs[1024];
     __shared__ int64_t sid[1024];
@@ -186,13 +187,15 @@ __global__ void __launch_bounds__(256) gt_seed_theta(const float *__restrict__ X
     if (threadIdx.x == 0) {
         const float th = (k <= np2) ? lbs[k - 1] : -INFINITY;
         theta_glob[q] = (th > -INFINITY) ? float_order(th) : 0u;
+        if (zero_cnt) zero_cnt[q] = 0u;   // (the survivor count, instead of a memset node)
     }
 }
 
 void launch_gt_seed_theta(const float *X, int64_t n, int d, const float *Q, int Qb,
                           const float *qnorm, const int64_t *seeds, int ks, int k, float eps_rel,
-                          uint32_t *theta_glob, cudaStream_t s) {
-    launch_pdl(gt_seed_theta, dim3(Qb), dim3(256), 0, s, X, n, d, Q, qnorm, seeds, ks, k, eps_rel, theta_glob);
+                          uint32_t *theta_glob, cudaStream_t s, uint32_t *zero_cnt) {
+    launch_pdl(gt_seed_theta, dim3(Qb), dim3(256), 0, s, X, n, d, Q, qnorm, seeds, ks, k, eps_rel, theta_glob,
+               zero_cnt);
     note_launch();
 }
 

@@ -230,7 +230,7 @@ void launch_gt_filter(const float *X, int64_t n, int d, const float *Q, int Qb,
 int scan_chunk_items();
 void launch_gt_seed_theta(const float *X, int64_t n, int d, const float *Q, int Qb,
                           const float *qnorm, const int64_t *seeds, int ks, int k, float eps_rel,
-                          uint32_t *theta_glob, cudaStream_t s);
+                          uint32_t *theta_glob, cudaStream_t s, uint32_t *zero_cnt = nullptr);
 // tensor-core ground truth (tc_kernels.cu)
 void launch_bf16_prep(const float *X, int64_t n, int d, int dp, void *Xb, float *xnorm,
                       cudaStream_t s, const int32_t *perm = nullptr);
