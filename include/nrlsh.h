@@ -172,7 +172,7 @@ nrlsh_status nrlsh_last_rerank_stats(int64_t *rescored_fp32);
                                keeping survivors that pass the select's candidate
                                rule, then the same fp32 re-rank of the survivors
                                (default when probe_budget >= n / 300 and a
-                               sub-batch holds >= 128 queries);
+                               sub-batch's queries x probe_budget >= 1.28 n);
      NRLSH_RERANK_DENSE        dense SIMT re-rank of hot sub-datasets (opt-in);
      NRLSH_RERANK_GATHER_BF16  gather with a certified bf16 pre-pass (opt-in).
    overflow_redone: queries whose tensor-core survivor list overflowed and were

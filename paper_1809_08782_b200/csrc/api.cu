@@ -604,16 +604,19 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
     // tensor-core re-rank (tc_kernels.cu member mode): a bf16 GEMM pass over the
     // tiles of the sub-datasets holding candidates, certified filter, keeping only
     // candidates; chosen when the candidate budget is a large enough share of n
-    // (measured on c4: break-even near T = n / 300) and the sub-batch holds enough
-    // queries to share the item tiles (c4, T = 1%: the gather path wins below ~128
-    // queries, 0.27 vs 0.39 ms for one) — NRLSH_RERANK_TC=0/1 forces it
+    // (measured on c4: break-even near T = n / 300) and the sub-batch's gather would
+    // touch at least ~1.28 n rows (Qmax T >= 1.28 n: the filter streams the items
+    // once for all its queries; c4, T = 1%: the gather path wins below ~128 queries,
+    // 0.27 vs 0.39 ms for one, while at T = 45% even 64 queries want the filter)
+    // — NRLSH_RERANK_TC=0/1 forces it
     const char *rtc_env = getenv("NRLSH_RERANK_TC");
     const double rtc_ratio = getenv("NRLSH_RERANK_TC_RATIO") ? atof(getenv("NRLSH_RERANK_TC_RATIO")) : 300.0;
-    const int rtc_minq = getenv("NRLSH_RERANK_TC_MINQ") ? atoi(getenv("NRLSH_RERANK_TC_MINQ")) : 128;
+    const double rtc_qt = getenv("NRLSH_RERANK_TC_QT") ? atof(getenv("NRLSH_RERANK_TC_QT")) : 1.28;
     const bool use_rtc = want_topk && !use_dense && !g_in_rtc_redo && ix->Xb && ix->xnorm_pos &&
                          gt_tc_supported(ix->d, k) &&
                          (rtc_env ? atoi(rtc_env) != 0
-                                  : (double)Tq * rtc_ratio >= (double)n && Qmax >= rtc_minq);
+                                  : (double)Tq * rtc_ratio >= (double)n &&
+                                        (double)Qmax * (double)Tq >= rtc_qt * (double)n);
     const int KS = getenv("NRLSH_RERANK_TC_KS") ? std::max(k, std::min(1024, atoi(getenv("NRLSH_RERANK_TC_KS"))))
                                                  : std::min(1024, std::max(512, 4 * k));
     // survivor list capacity per query (NRLSH_RERANK_TC_CAP: test switch forcing the
