@@ -57,6 +57,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-latency", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-scale", dest="scale", action="store_false",
+                    help="skip the scale (configs[4]) sub-record")
+    ap.add_argument("--scale-steps", type=int, default=3)
     ap.add_argument("--sweep-m", action="store_true",
                     help="with --sweep: m in {1,32,64,128,256} at the paper's bit accounting")
     ap.add_argument("--sweep", default=None,
@@ -175,7 +178,8 @@ def roofline_for(slot, ms_total, count, info, peaks, peaks_src):
     if slot == "gt_filter" or (slot == "rerank" and info.get("rerank_path") == "tensor"):
         # one bf16 pass over every item per query; the re-rank's member-mode pass
         # multiplies only the tiles of sub-datasets holding candidates (its own count)
-        pairs = nq * n if slot == "gt_filter" else info["rerank_filter_pairs"]
+        # the pairs each filter actually multiplied (tile pruning skips the rest)
+        pairs = info["gt_filter_pairs"] if slot == "gt_filter" else info["rerank_filter_pairs"]
         fl = 2.0 * pairs * d * steps / count
         ach = fl / per_launch_s
         if slot == "rerank":
@@ -324,6 +328,125 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def measure_path(P, torch, cfg, L, m, T, Xd, Qd, steps, warmup, stream, flush, dist=None):
+    """Time `steps` whole steps (build + query batch + exact ground truth), each
+    phase bracketed by CUDA events on the launching stream; per-stage device time
+    from the library's own events; the work counters the rooflines need."""
+    k = cfg.k
+
+    def step(ev=None):
+        if ev:
+            ev[0].record(stream)
+        idx = P.Index(Xd, L, m, seed=cfg.seed, query_batch=cfg.query_batch)
+        if ev:
+            ev[1].record(stream)
+        ids, sc = idx.query(Qd, k, T)
+        qstats = P.last_query_stats()
+        rinfo = P.last_rerank_path()
+        if ev:
+            ev[2].record(stream)
+        # ground truth, warm-started from the LSH answers (certified; the result
+        # does not depend on the seeds — tests/test_gpu_parity.py)
+        gid, gsc = idx.exact_topk(Qd, k, seed_ids=ids)
+        gstats = P.last_exact_stats()
+        if ev:
+            ev[3].record(stream)
+        idx.close()
+        return ids, gid, qstats, rinfo, gstats
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    P.profile_read(reset=True)
+    P.profile_enable(True)
+    launches0 = P.launch_count()
+    acc = {"scanned_pairs": 0, "buffer_entries": 0, "fallback_queries": 0, "rerank_filter_pairs": 0,
+           "rerank_overflow": 0, "gt_filter_pairs": 0, "gt_survivors": 0}
+    evs = []
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for _ in range(steps):
+        flush.zero_()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ids, gid, qstats, rinfo, gstats = step(ev)
+        evs.append(ev)
+        acc["scanned_pairs"] += qstats["scanned_pairs"]
+        acc["buffer_entries"] += qstats["buffer_entries"]
+        acc["fallback_queries"] += qstats["fallback_queries"]
+        acc["rerank_filter_pairs"] += rinfo["filter_pairs"]
+        acc["rerank_overflow"] += rinfo["overflow_redone"]
+        acc["gt_filter_pairs"] += gstats["filter_pairs"]
+        acc["gt_survivors"] += gstats["sum_survivors"]
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    launches = P.launch_count() - launches0
+    P.profile_enable(False)
+    prof = P.profile_read(reset=True)
+    ms = [e[0].elapsed_time(e[3]) for e in evs]
+    ids_h, gid_h = ids.cpu().numpy(), gid.cpu().numpy()
+    rec = float(np.mean([len(set(a.tolist()) & set(b.tolist())) / k for a, b in zip(ids_h, gid_h)]))
+    rec10 = float(np.mean([len(set(a[:10].tolist()) & set(b[:10].tolist())) / 10
+                           for a, b in zip(ids_h, gid_h)]))
+    return {"ms_all": ms, "ms_step": float(np.mean(ms)),
+            "build_ms": float(np.mean([e[0].elapsed_time(e[1]) for e in evs])),
+            "query_ms": float(np.mean([e[1].elapsed_time(e[2]) for e in evs])),
+            "gt_ms": float(np.mean([e[2].elapsed_time(e[3]) for e in evs])),
+            "prof": prof, "launches": launches, "acc": acc, "recall_at_k": rec,
+            "recall_at_10": rec10, "rerank_path": rinfo["path"]}
+
+
+def rooflines(r, cfg, L, m, nq, T, steps, peaks, peaks_src):
+    """SURVEY.md §8(d) rooflines from one measure_path() result: the dominant
+    kernel, every stage's own, and the build / query totals."""
+    prof, acc = r["prof"], r["acc"]
+    W = 1 if L <= 32 else (2 if L <= 64 else 4)
+    info = {"n": cfg.n, "d": cfg.d, "L": L, "W": W, "nq": nq, "T": T, "k": cfg.k, "m": m,
+            "scanned_pairs": acc["scanned_pairs"], "traffic": load_traffic(), "steps": steps,
+            "rerank_path": r["rerank_path"], "rerank_filter_pairs": acc["rerank_filter_pairs"],
+            "gt_filter_pairs": acc["gt_filter_pairs"],
+            "score_bytes": float(nq) * T * cfg.d * 4.0 * steps, "gt_tensor": True}
+    live = {n_: v for n_, v in prof.items() if v[1] > 0}
+    dom = max(live.items(), key=lambda x: x[1][0])
+    roof = roofline_for(dom[0], dom[1][0], dom[1][1], info, peaks, peaks_src)
+    scan_roof = roofline_for("scan", *prof["scan"], info, peaks, peaks_src) if prof["scan"][1] else None
+    others = {s_: roofline_for(s_, *prof[s_], info, peaks, peaks_src)
+              for s_ in ("gt_filter", "rerank", "codes", "norms") if prof.get(s_, (0, 0))[1]}
+    hbm = peaks["hbm_gbs"] * 1e9
+    bf16 = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")) * 1e12
+    n, d = cfg.n, cfg.d
+    # build (Alg. 1): X read twice (exact ranks precede hashing) + codes + ~32 B/item
+    # of keys / permutation (SURVEY §8(d))
+    b_bytes = 2.0 * n * d * 4 + n * L / 8.0 + 32.0 * n
+    build_dev = sum(prof.get(s_, (0, 0))[0] for s_ in ("norms", "partition", "scatter", "codes")) / steps
+    build = {"bound": "hbm", "algorithmic_bytes": b_bytes, "t_roof_ms": b_bytes / hbm * 1e3,
+             "t_measured_ms": r["build_ms"], "frac": b_bytes / hbm * 1e3 / r["build_ms"],
+             "t_device_stages_ms": build_dev, "frac_device_stages": b_bytes / hbm * 1e3 / build_dev,
+             "peak_gbs": peaks["hbm_gbs"], "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peaks_src})"}
+    # query (SURVEY §8(d)): t_codes + max(popc, hbm)_scan + t_select + t_rerank
+    nsub = -(-nq // cfg.query_batch)
+    t_codes = 2.0 * nq * d * L / FFMA_PEAK_FLOPS
+    t_scan_hbm = nsub * n * W * 4.0 / hbm
+    t_sel = acc["buffer_entries"] / steps * 8.0 / hbm
+    def q_roof(pairs, rr_pairs):
+        t_scan = max(pairs * W / POPC_PEAK_PER_S, t_scan_hbm)
+        t_rr = rr_pairs * 2.0 * d / bf16
+        t = t_codes + t_scan + t_sel + t_rr
+        return {"t_roof_ms": t * 1e3, "frac": t * 1e3 / r["query_ms"],
+                "terms_ms": {"codes": t_codes * 1e3, "scan": t_scan * 1e3, "select": t_sel * 1e3,
+                             "rerank": t_rr * 1e3}}
+    query = {"t_measured_ms": r["query_ms"],
+             # every (query, item) pair scanned; every probed candidate scored on the tensor pipe
+             "logical": q_roof(float(nq) * n, float(nq) * T),
+             # the pairs the scan evaluated after exact sub-dataset skipping, the pairs
+             # the re-rank's filter multiplied
+             "actual": q_roof(acc["scanned_pairs"] / steps, acc["rerank_filter_pairs"] / steps),
+             "peaks": {"popc_per_s": POPC_PEAK_PER_S, "hbm_gbs": peaks["hbm_gbs"],
+                       "bf16_tflops": bf16 / 1e12, "ffma_tflops": FFMA_PEAK_FLOPS / 1e12}}
+    return roof, scan_roof, others, build, query
+
+
 def run_native(args):
     import torch
     world, rank, local = dist_setup(args)
@@ -348,56 +471,13 @@ def run_native(args):
     stream = torch.cuda.current_stream()
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
 
-    def step():
-        idx = P.Index(Xd, L, m, seed=cfg.seed, query_batch=cfg.query_batch)
-        ids, sc = idx.query(Qd, k, T)
-        qstats = P.last_query_stats()
-        # ground truth, warm-started from the LSH answers (certified; the result
-        # does not depend on the seeds — tests/test_gpu_parity.py)
-        gid, gsc = idx.exact_topk(Qd, k, seed_ids=ids)
-        idx.close()
-        return ids, gid, qstats
-
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-
     sampler = ClockSampler(local)
-    P.profile_read(reset=True)
-    P.profile_enable(True)
-    launches0 = P.launch_count()
-    scanned = 0
-    evs = []
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
     sampler.start()
-    for _ in range(args.steps):
-        flush.zero_()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        ids, gid, qstats = step()
-        e1.record(stream)
-        evs.append((e0, e1))
-        scanned += qstats["scanned_pairs"]
-    torch.cuda.synchronize()
-    rinfo = P.last_rerank_path()
-    rerank_path = rinfo["path"]
-    if dist:
-        dist.barrier()
+    r = measure_path(P, torch, cfg, L, m, T, Xd, Qd, args.steps, args.warmup, stream, flush, dist)
     clocks = sampler.stop()
-    launches = P.launch_count() - launches0
-    P.profile_enable(False)
-    prof = P.profile_read(reset=True)
-    ms = [a.elapsed_time(b) for a, b in evs]
-    ms_step = float(np.mean(ms))
-    ms_step = max_over_ranks(ms_step, dist, dev)
+    ms_step = max_over_ranks(r["ms_step"], dist, dev)
     value = whole_job_rate(nq, world, ms_step)
-
-    ids_h = ids.cpu().numpy()
-    gid_h = gid.cpu().numpy()
-    rec = float(np.mean([len(set(a.tolist()) & set(b.tolist())) / k for a, b in zip(ids_h, gid_h)]))
+    prof = r["prof"]
 
     # -------- end to end through the public API with HOST buffers (pinned)
     # latency mode: 1 and 2 queries per call, index resident; the scan
@@ -455,6 +535,7 @@ def run_native(args):
                "h2d_bytes_per_step": int(X.nbytes + 2 * Q.nbytes),
                "d2h_bytes_per_step": int(2 * (oid.numel() * 8 + osc.numel() * 4)),
                "ms_per_step": e2, "ms_all": e2e_ms}
+        del Xh, Qh
 
     if rank != 0:
         if dist:
@@ -464,16 +545,36 @@ def run_native(args):
     peaks, peaks_src = load_peaks()
     stage = {name: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps}
              for name, v in prof.items() if v[1] > 0}
-    W = 1 if L <= 32 else (2 if L <= 64 else 4)
-    info = {"n": cfg.n, "d": cfg.d, "L": L, "W": W, "nq": nq, "T": T, "k": k, "m": m,
-            "scanned_pairs": scanned, "traffic": load_traffic(), "steps": args.steps,
-            "rerank_path": rerank_path, "rerank_filter_pairs": rinfo["filter_pairs"],
-            "score_bytes": float(nq) * T * cfg.d * 4.0 * args.steps, "gt_tensor": True}
-    dom = max(((n_, v) for n_, v in prof.items() if v[1] > 0), key=lambda x: x[1][0])
-    roof = roofline_for(dom[0], dom[1][0], dom[1][1], info, peaks, peaks_src)
-    scan_roof = roofline_for("scan", *prof["scan"], info, peaks, peaks_src) if prof["scan"][1] else None
-    others = {s_: roofline_for(s_, *prof[s_], info, peaks, peaks_src)
-              for s_ in ("gt_filter", "rerank", "codes", "norms") if prof.get(s_, (0, 0))[1]}
+    roof, scan_roof, others, build_roof, query_roof = rooflines(r, cfg, L, m, nq, T, args.steps,
+                                                                peaks, peaks_src)
+
+    # -------- scale (BASELINE configs[4]) in the same run: a sub-record, not the headline
+    scale = None
+    if args.scale and world == 1 and cfg.name != "scale":
+        del Xd, Qd
+        torch.cuda.empty_cache()
+        scfg = workloads.CONFIGS["scale"]
+        sL, sm_ = scfg.code_bits[-1], scfg.num_parts[0]
+        sT = max(scfg.budget_list())
+        sX = torch.from_numpy(workloads.make_items(scfg)).to(dev)
+        sQ = torch.from_numpy(workloads.make_queries(scfg)).to(dev)
+        rs = measure_path(P, torch, scfg, sL, sm_, sT, sX, sQ, args.scale_steps, 2, stream, flush)
+        sroof, sscan, sothers, sbuild, squery = rooflines(rs, scfg, sL, sm_, scfg.nq, sT,
+                                                          args.scale_steps, peaks, peaks_src)
+        scale = {"workload": f"scale: n={scfg.n:,} d={scfg.d} {scfg.norm_law} norms, {sL}-bit codes, "
+                             f"m={sm_}, {scfg.nq:,} queries (sub-batches of {scfg.query_batch}), "
+                             f"top-{scfg.k}, T={sT:,}",
+                 "value": scfg.nq / (rs["ms_step"] / 1e3), "unit": "queries/s",
+                 "ms_per_step": rs["ms_step"], "steps": args.scale_steps, "warmup": 2,
+                 "build_ms": rs["build_ms"], "query_ms": rs["query_ms"], "gt_ms": rs["gt_ms"],
+                 "recall_at_100": rs["recall_at_k"], "recall_at_10": rs["recall_at_10"],
+                 "scan_frac": sscan["frac"] if sscan else None, "build_frac": sbuild["frac"],
+                 "build_roofline": sbuild, "query_roofline": squery, "roofline": sroof,
+                 "stage_ms_per_step": {nm: v[0] / args.scale_steps for nm, v in rs["prof"].items()
+                                       if v[1] > 0},
+                 "counters": rs["acc"]}
+        del sX, sQ
+        torch.cuda.empty_cache()
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:
@@ -492,16 +593,18 @@ def run_native(args):
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u32 codes / f32 scores",
         "data": "synthetic", "config": desc,
-        "recall_at_10": rec,
+        "recall_at_10": r["recall_at_10"],
         "stage_ms_per_step": stage,
+        "phase_ms_per_step": {"build": r["build_ms"], "query": r["query_ms"], "ground_truth": r["gt_ms"]},
         "roofline": roof, "scan_roofline": scan_roof, "other_rooflines": others,
-        "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+        "build_roofline": build_roof, "query_roofline": query_roof,
+        "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(r["launches"]),
         "latency_mode": latency,
+        "scale": scale,
         "clocks": clocks,
         "notes": {"input_gen_s": t_gen, "peaks": peaks_src,
-                  "step_ms_all": ms, "rerank_path": rerank_path,
-                  "rerank_filter_pairs_per_step": rinfo["filter_pairs"],
-                  "rerank_overflow_redone": rinfo["overflow_redone"]},
+                  "step_ms_all": r["ms_all"], "rerank_path": r["rerank_path"],
+                  "counters_per_step": {k_: v / args.steps for k_, v in r["acc"].items()}},
     }
     print(json.dumps(line), flush=True)
     if dist:

@@ -149,10 +149,11 @@ nrlsh_status nrlsh_query_candidates(const nrlsh_index *index, const float *queri
                                     int32_t *cand_ids, uint16_t *cand_rank, void *cuda_stream);
 /* Statistics of the last nrlsh_query / nrlsh_query_candidates on this thread:
    queries that took the exact fallback (pilot bound under/overflowed), kernels
-   launched, and (query, item) pairs the Hamming scan actually evaluated (pairs of
-   sub-datasets whose radius delta_j(q) < 0 are skipped exactly). Any may be NULL. */
+   launched, (query, item) pairs the Hamming scan actually evaluated (pairs of
+   sub-datasets whose radius delta_j(q) < 0 are skipped exactly), and candidate-
+   buffer entries the top-T select read (8 bytes each). Any may be NULL. */
 nrlsh_status nrlsh_last_query_stats(int64_t *fallback_queries, int64_t *kernel_launches,
-                                    int64_t *scanned_pairs);
+                                    int64_t *scanned_pairs, int64_t *buffer_entries);
 
 /* Candidates of the last nrlsh_query on this thread that the re-rank rescored in
    fp32 after a certified bf16 pass (the others provably could not enter the
@@ -211,9 +212,12 @@ nrlsh_status nrlsh_index_exact_topk_seeded(const nrlsh_index *index, const float
                                            void *cuda_stream);
 
 /* Statistics of the last exact top-k on this thread: the largest and the total
-   number of filter survivors per query (re-scored exactly), and the number of
-   queries whose survivors overflowed the buffer (answered by a full exact scan). */
-nrlsh_status nrlsh_last_exact_stats(int64_t *max_cand, int64_t *sum_cand, int64_t *overflow);
+   number of filter survivors per query (re-scored exactly), the number of
+   queries whose survivors overflowed the buffer (answered by a full exact scan),
+   and the (query, item) pairs the tensor-core filter multiplied (nq * n without
+   the index's tile pruning).  Any may be NULL. */
+nrlsh_status nrlsh_last_exact_stats(int64_t *max_cand, int64_t *sum_cand, int64_t *overflow,
+                                    int64_t *filter_pairs);
 
 /* ---- tracing ------------------------------------------------------------
    With profiling on, every kernel class is bracketed by CUDA events recorded on

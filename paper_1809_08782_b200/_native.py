@@ -84,7 +84,7 @@ def lib():
         L.nrlsh_query_codes.restype = st
         L.nrlsh_query_candidates.argtypes = [p, p, p, i64, i64, p, p, p]
         L.nrlsh_query_candidates.restype = st
-        L.nrlsh_last_query_stats.argtypes = [p, p, p]
+        L.nrlsh_last_query_stats.argtypes = [p, p, p, p]
         L.nrlsh_last_query_stats.restype = st
         L.nrlsh_index_exact_topk.argtypes = [p, p, i64, i32, p, p, p]
         L.nrlsh_index_exact_topk.restype = st
@@ -102,7 +102,7 @@ def lib():
         L.nrlsh_last_rerank_stats.restype = st
         L.nrlsh_last_rerank_path.argtypes = [p, p, p]
         L.nrlsh_last_rerank_path.restype = st
-        L.nrlsh_last_exact_stats.argtypes = [p, p, p]
+        L.nrlsh_last_exact_stats.argtypes = [p, p, p, p]
         L.nrlsh_last_exact_stats.restype = st
         L.nrlsh_launch_count.argtypes = []
         L.nrlsh_launch_count.restype = C.c_int64
@@ -124,6 +124,41 @@ def _ptr(a):
         return C.c_void_p(a.ctypes.data)
     assert a.is_contiguous()
     return C.c_void_p(a.data_ptr())
+
+
+_NP_OF = {"float32": np.float32, "int64": np.int64, "int32": np.int32, "uint32": np.uint32,
+          "uint16": np.uint16}
+
+
+def _want(a, name, dtypes, shape=None, device=None):
+    """Validate an array before its raw pointer crosses the ABI (which cannot check
+    dtype, width or device itself): C-contiguous, one of `dtypes` (numpy names;
+    int32/uint32 and int16/uint16 are interchangeable bit containers), `shape` (None
+    entries are free), and for torch tensors on the index's device (or the host)."""
+    if a is None:
+        raise ValueError(f"{name} is None")
+    if isinstance(a, np.ndarray):
+        dt = a.dtype.name
+        if not a.flags["C_CONTIGUOUS"]:
+            raise ValueError(f"{name} must be C-contiguous")
+    else:
+        dt = str(a.dtype).replace("torch.", "")
+        if not a.is_contiguous():
+            raise ValueError(f"{name} must be contiguous")
+        if device is not None and a.is_cuda and a.device != device:
+            raise ValueError(f"{name} is on {a.device}, the index on {device}")
+    alias = {"int32": "uint32", "uint32": "int32", "int16": "uint16", "uint16": "int16"}
+    if dt not in dtypes and alias.get(dt) not in dtypes:
+        raise TypeError(f"{name} must be {'/'.join(dtypes)}, got {dt}")
+    if shape is not None:
+        got = tuple(a.shape)
+        if len(got) != len(shape) or any(w is not None and g != w for g, w in zip(got, shape)):
+            raise ValueError(f"{name} must have shape {shape} (None = any), got {got}")
+    return a
+
+
+def _dev_of(a):
+    return None if isinstance(a, np.ndarray) or not a.is_cuda else a.device
 
 
 def _stream(stream):
@@ -154,7 +189,9 @@ class Index:
 
     def __init__(self, items, code_bits, num_parts, seed=0, eps=0.01, scheme="percentile",
                  index_bits_in_budget=False, query_batch=0, stream=None):
+        _want(items, "items", ("float32",), (None, None))
         self._items = items
+        self._device = _dev_of(items)
         opt = Options()
         lib().nrlsh_default_options(C.byref(opt))
         opt.eps = float(eps)
@@ -186,11 +223,14 @@ class Index:
 
     # -------------------------------------------------------------- query
     def query(self, queries, k, probe_budget, out_ids=None, out_scores=None, stream=None):
+        _want(queries, "queries", ("float32",), (None, self.d), self._device)
         nq = queries.shape[0]
         if out_ids is None:
             out_ids = _empty_like_io(queries, (nq, k), np.int64, _torch_dtype("int64"))
         if out_scores is None:
             out_scores = _empty_like_io(queries, (nq, k), np.float32, _torch_dtype("float32"))
+        _want(out_ids, "out_ids", ("int64",), (nq, k), self._device)
+        _want(out_scores, "out_scores", ("float32",), (nq, k), self._device)
         _check(lib().nrlsh_query(self._h, _ptr(queries), nq, int(k), int(probe_budget),
                                  _ptr(out_ids), _ptr(out_scores), _stream(stream)))
         return out_ids, out_scores
@@ -199,11 +239,16 @@ class Index:
         """Ground truth against the index's own items (no re-staging of host items).
         seed_ids [nq x ks] int64 (optional): warm-start ids, e.g. query()'s answers;
         the result does not depend on them."""
+        _want(queries, "queries", ("float32",), (None, self.d), self._device)
         nq = queries.shape[0]
         if out_ids is None:
             out_ids = _empty_like_io(queries, (nq, k), np.int64, _torch_dtype("int64"))
         if out_scores is None:
             out_scores = _empty_like_io(queries, (nq, k), np.float32, _torch_dtype("float32"))
+        _want(out_ids, "out_ids", ("int64",), (nq, k), self._device)
+        _want(out_scores, "out_scores", ("float32",), (nq, k), self._device)
+        if seed_ids is not None:
+            _want(seed_ids, "seed_ids", ("int64",), (nq, None), self._device)
         if seed_ids is None:
             _check(lib().nrlsh_index_exact_topk(self._h, _ptr(queries), nq, int(k), _ptr(out_ids),
                                                 _ptr(out_scores), _stream(stream)))
@@ -214,6 +259,7 @@ class Index:
         return out_ids, out_scores
 
     def query_codes(self, queries, stream=None):
+        _want(queries, "queries", ("float32",), (None, self.d), self._device)
         nq = queries.shape[0]
         out = _empty_like_io(queries, (nq, self.words), np.uint32, _torch_dtype("int32"))
         _check(lib().nrlsh_query_codes(self._h, _ptr(queries), nq, _ptr(out), _stream(stream)))
@@ -221,6 +267,12 @@ class Index:
 
     def candidates(self, probe_budget, queries=None, qcodes=None, stream=None):
         ref = queries if queries is not None else qcodes
+        if queries is not None:
+            _want(queries, "queries", ("float32",), (None, self.d), self._device)
+        if qcodes is not None:
+            _want(qcodes, "qcodes", ("uint32",), (None, self.words), self._device)
+            if queries is not None and queries.shape[0] != qcodes.shape[0]:
+                raise ValueError("queries and qcodes disagree on nq")
         nq = ref.shape[0]
         T = min(int(probe_budget), self.n)
         ids = _empty_like_io(ref, (nq, T), np.int32, _torch_dtype("int32"))
@@ -267,12 +319,19 @@ def _torch_dtype(name):
 
 
 def exact_topk(items, queries, k, out_ids=None, out_scores=None, stream=None, seed_ids=None):
+    _want(items, "items", ("float32",), (None, None))
     n, d = items.shape
+    dev = _dev_of(items)
+    _want(queries, "queries", ("float32",), (None, d), dev)
     nq = queries.shape[0]
     if out_ids is None:
         out_ids = _empty_like_io(queries, (nq, k), np.int64, _torch_dtype("int64"))
     if out_scores is None:
         out_scores = _empty_like_io(queries, (nq, k), np.float32, _torch_dtype("float32"))
+    _want(out_ids, "out_ids", ("int64",), (nq, k), dev)
+    _want(out_scores, "out_scores", ("float32",), (nq, k), dev)
+    if seed_ids is not None:
+        _want(seed_ids, "seed_ids", ("int64",), (nq, None), dev)
     if seed_ids is None:
         _check(lib().nrlsh_exact_topk(_ptr(items), n, d, _ptr(queries), nq, int(k), _ptr(out_ids),
                                       _ptr(out_scores), _stream(stream)))
@@ -302,15 +361,17 @@ def last_rerank_path():
 
 
 def last_query_stats():
-    a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
-    _check(lib().nrlsh_last_query_stats(C.byref(a), C.byref(b), C.byref(c)))
-    return {"fallback_queries": a.value, "kernel_launches": b.value, "scanned_pairs": c.value}
+    a, b, c, e = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
+    _check(lib().nrlsh_last_query_stats(C.byref(a), C.byref(b), C.byref(c), C.byref(e)))
+    return {"fallback_queries": a.value, "kernel_launches": b.value, "scanned_pairs": c.value,
+            "buffer_entries": e.value}
 
 
 def last_exact_stats():
-    a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
-    _check(lib().nrlsh_last_exact_stats(C.byref(a), C.byref(b), C.byref(c)))
-    return {"max_survivors": a.value, "sum_survivors": b.value, "overflow_queries": c.value}
+    a, b, c, e = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
+    _check(lib().nrlsh_last_exact_stats(C.byref(a), C.byref(b), C.byref(c), C.byref(e)))
+    return {"max_survivors": a.value, "sum_survivors": b.value, "overflow_queries": c.value,
+            "filter_pairs": e.value}
 
 
 def profile_enable(on=True):

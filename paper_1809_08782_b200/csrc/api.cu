@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -21,6 +22,8 @@ thread_local std::string g_last_error;
 thread_local int64_t g_last_fallbacks = 0;
 thread_local int64_t g_last_launches = 0;
 thread_local int64_t g_last_pairs = 0;
+thread_local int64_t g_last_entries = 0;       // candidate-buffer entries the select read
+thread_local int64_t g_last_gt_pairs = 0;      // (query, item) pairs the exact filter multiplied
 thread_local int64_t g_last_rescored = 0;
 thread_local int64_t g_last_rtc_overflow = 0;   // tensor-core re-rank: queries redone by gather
 thread_local int64_t g_last_rtc = 0;            // 1 if the last query used the tensor-core re-rank
@@ -56,23 +59,10 @@ struct DBuf {
     ~DBuf() { if (p) cudaFreeAsync(p, s); }
     cudaError_t alloc(size_t bytes, cudaStream_t st) {
         s = st;
-        return cudaMallocAsync(&p, bytes ? bytes : 16, st);
+        return dmalloc(&p, bytes ? bytes : 16, st);
     }
     template <class T> T *get() const { return (T *)p; }
 };
-
-void configure_pool() {
-    static bool done = false;
-    if (done) return;
-    done = true;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thr = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-}
 
 // -------------------------------------------------------------- projection
 // Documented generator (include/nrlsh.h): SplitMix64 at counter c, two 53-bit
@@ -187,6 +177,35 @@ struct OutBuf {
 }  // namespace
 
 namespace nrlsh {
+// Stream-ordered allocations come from a private pool per device (not the
+// process-wide default pool a PyTorch allocator in the same process may rely on).
+// It keeps up to 8 GiB of freed memory cached across calls (query workspaces are
+// ~2.5 GB and are reallocated every call) and returns the rest to the driver at
+// the next synchronisation.
+cudaError_t dmalloc(void **p, size_t bytes, cudaStream_t s) {
+    static std::mutex mu;
+    static cudaMemPool_t pools[128] = {};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e) return e;
+    if (dev < 0 || dev >= 128) return cudaErrorInvalidDevice;
+    cudaMemPool_t pool;
+    {
+        std::lock_guard<std::mutex> g(mu);
+        if (!pools[dev]) {
+            cudaMemPoolProps pr = {};
+            pr.allocType = cudaMemAllocationTypePinned;
+            pr.location.type = cudaMemLocationTypeDevice;
+            pr.location.id = dev;
+            if ((e = cudaMemPoolCreate(&pools[dev], &pr))) { pools[dev] = nullptr; return e; }
+            uint64_t thr = 8ull << 30;
+            cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        pool = pools[dev];
+    }
+    return cudaMallocFromPoolAsync(p, bytes, pool, s);
+}
+
 int pilot_stride(int64_t n) {
     if (n <= (1 << 18)) return 1;                 // exact histogram: no fallback needed
     // ~32,768 sampled positions (stride capped at 64; NRLSH_PILOT_SAMPLES overrides for
@@ -248,7 +267,6 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
         return fail(NRLSH_EINVAL, "hash bits L_h must be in [1,64] or [97,128] (got " +
                                       std::to_string(L) + ")");
     cudaStream_t s = (cudaStream_t)cuda_stream;
-    configure_pool();
 
     std::unique_ptr<nrlsh_index, void (*)(nrlsh_index *)> ix(new nrlsh_index(), free_index);
     ix->n = n;
@@ -266,7 +284,7 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
 
 #define NR_ALLOC(ptr, bytes)                                                      \
     do {                                                                          \
-        cudaError_t e_ = cudaMallocAsync((void **)&(ptr), (bytes) ? (bytes) : 16, s); \
+        cudaError_t e_ = dmalloc((void **)&(ptr), (bytes) ? (bytes) : 16, s); \
         if (e_ != cudaSuccess) { cudaGetLastError(); return fail(NRLSH_ENOMEM, "cudaMalloc " #ptr); } \
     } while (0)
 
@@ -467,7 +485,8 @@ void run_candidates(const nrlsh_index *ix, const float *Qd, const uint32_t *qcod
                     unsigned long long *buf, int32_t *cand, uint16_t *cand_rank, int *flags,
                     unsigned long long *pairs, cudaStream_t s, uint32_t *sel_B = nullptr,
                     uint32_t *sel_pk = nullptr, uint32_t *cnt_part = nullptr,
-                    int32_t *seeds = nullptr, int ks = 0, void *fb_ws = nullptr) {
+                    int32_t *seeds = nullptr, int ks = 0, void *fb_ws = nullptr,
+                    unsigned long long *entries = nullptr) {
     if (qcodes_in) {
         cudaMemcpyAsync(qcodes, qcodes_in + qbase * ix->W, (size_t)Qb * ix->W * 4,
                         cudaMemcpyDeviceToDevice, s);
@@ -497,6 +516,8 @@ void run_candidates(const nrlsh_index *ix, const float *Qd, const uint32_t *qcod
     {
         ProfScope p(SLOT_FALLBACK, s);
         launch_fallback(ix, qcodes, Qb, Tq, buf, cnt, tc ? cntv : cnt, C, flags, fb_ws, s);
+        // buffer entries the select reads (statistics: the select's HBM roofline)
+        if (entries) launch_sum_counts(tc ? cntv : cnt, Qb, C, entries, s);
     }
     {
         ProfScope p(SLOT_SELECT, s);
@@ -546,7 +567,6 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
     if (want_topk && !queries) return fail(NRLSH_EINVAL, "queries is NULL");
     if (want_topk && !out_scores) return fail(NRLSH_EINVAL, "out_scores is NULL");
     cudaStream_t s = (cudaStream_t)cuda_stream;
-    configure_pool();
     const int64_t n = ix->n;
     const int64_t Tq = std::min<int64_t>(probe_budget, n);
     const int stride = pilot_stride(n);
@@ -583,7 +603,7 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
         ba.alloc(scan_tc_supported(ix) ? scan_tc_ws_bytes(ix, Qmax) : 16, s) ||
         bf.alloc((size_t)Qmax * C * 8, s) ||
         cd.alloc((size_t)Qmax * Tq * 4, s) ||
-        pt.alloc(want_topk ? rerank_partial_bytes(Qmax, Tq, k) : 0, s) || fl.alloc(40, s) ||
+        pt.alloc(want_topk ? rerank_partial_bytes(Qmax, Tq, k) : 0, s) || fl.alloc(48, s) ||
         fbw.alloc(fallback_ws_bytes(ix), s))
         return fail(NRLSH_ENOMEM, "query workspace");
     cudaMemsetAsync(fbw.p, 0, fallback_ws_bytes(ix), s);   // (histogram rows stay zero between uses)
@@ -653,8 +673,8 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
     tls.xsplit = getenv("NRLSH_RERANK_TWOPASS") ? ix->tile_xsplit : 0.f;
     tls.pass = 0;
     tls.qperm = nullptr;
-    const int init_flags[10] = {INT_MAX, INT_MAX, 0, 0, 0, 0, 0, 0, 0, 0};
-    cudaMemcpyAsync(fl.p, init_flags, 40, cudaMemcpyHostToDevice, s);
+    const int init_flags[12] = {INT_MAX, INT_MAX, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyAsync(fl.p, init_flags, 48, cudaMemcpyHostToDevice, s);
     unsigned long long *pairs = (unsigned long long *)(fl.get<int>() + 4);
     const long long launches0 = launch_count();
     for (int64_t q0 = 0; q0 < nq; q0 += Qmax) {
@@ -669,7 +689,8 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
                        use_dense ? sb.get<uint32_t>() : (use_rtc ? rsb.get<uint32_t>() : nullptr),
                        use_dense ? spk.get<uint32_t>() : (use_rtc ? rspk.get<uint32_t>() : nullptr),
                        use_dense ? cpart.get<uint32_t>() : nullptr,
-                       use_rtc ? rseed.get<int32_t>() : nullptr, KS, fbw.p);
+                       use_rtc ? rseed.get<int32_t>() : nullptr, KS, fbw.p,
+                       (unsigned long long *)(fl.get<int>() + 10));
         if (use_rtc) {
             {
                 ProfScope p(SLOT_SCORE, s);
@@ -764,16 +785,20 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
         if ((e = cudaStreamSynchronize(s))) return cuda_fail(e, "query (re-rank overflow)");
         g_last_rtc_overflow = nov;
         if (nov) {
-            std::vector<int64_t> ql(nov);
-            cudaMemcpy(ql.data(), rov.p, (size_t)nov * 8, cudaMemcpyDeviceToHost);
+            // one gather-path call over all overflowed queries: gather their rows,
+            // re-rank, scatter the answers back (the list is on the device)
+            DBuf qr, ri, rs;
+            if (qr.alloc((size_t)nov * ix->d * 4, s) || ri.alloc((size_t)nov * k * 8, s) ||
+                rs.alloc((size_t)nov * k * 4, s))
+                return fail(NRLSH_ENOMEM, "re-rank overflow workspace");
+            launch_move_rows(Qs.dev, rov.get<int64_t>(), (int)nov, (size_t)ix->d * 4, qr.p, false, s);
             g_in_rtc_redo = true;
-            for (int64_t qi : ql) {
-                const nrlsh_status st = query_impl(
-                    ix, (const float *)Qs.dev + qi * ix->d, nullptr, 1, k, probe_budget,
-                    (int64_t *)oi.dev + qi * k, (float *)os.dev + qi * k, nullptr, nullptr, s);
-                if (st != NRLSH_OK) { g_in_rtc_redo = false; return st; }
-            }
+            const nrlsh_status st = query_impl(ix, qr.get<float>(), nullptr, nov, k, probe_budget,
+                                               ri.get<int64_t>(), rs.get<float>(), nullptr, nullptr, s);
             g_in_rtc_redo = false;
+            if (st != NRLSH_OK) return st;
+            launch_move_rows(ri.p, rov.get<int64_t>(), (int)nov, (size_t)k * 8, oi.dev, true, s);
+            launch_move_rows(rs.p, rov.get<int64_t>(), (int)nov, (size_t)k * 4, os.dev, true, s);
         }
     } else if (!g_in_rtc_redo) {
         g_last_rtc_overflow = 0;
@@ -785,8 +810,8 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
         if ((e = oc.finish(s))) return cuda_fail(e, "copy candidates");
         if (rank_out && (e = orr.finish(s))) return cuda_fail(e, "copy ranks");
     }
-    int hflags[10];
-    cudaMemcpyAsync(hflags, fl.p, 40, cudaMemcpyDeviceToHost, s);
+    int hflags[12];
+    cudaMemcpyAsync(hflags, fl.p, 48, cudaMemcpyDeviceToHost, s);
     e = cudaStreamSynchronize(s);
     if (e) return cuda_fail(e, "query");
     e = cudaGetLastError();
@@ -799,6 +824,8 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
     g_last_pairs = (int64_t)pr;
     std::memcpy(&pr, hflags + 6, 8);
     g_last_rescored = (int64_t)pr;
+    std::memcpy(&pr, hflags + 10, 8);
+    g_last_entries = (int64_t)pr;
     std::memcpy(&pr, hflags + 8, 8);
     if (!g_in_rtc_redo) g_last_rtc_pairs = (int64_t)pr;
     if (!g_in_rtc_redo)
@@ -829,7 +856,6 @@ nrlsh_status nrlsh_query_codes(const nrlsh_index *ix, const float *queries, int6
                                uint32_t *qcodes, void *cuda_stream) {
     if (!ix || !queries || !qcodes || nq < 1) return fail(NRLSH_EINVAL, "bad argument");
     cudaStream_t s = (cudaStream_t)cuda_stream;
-    configure_pool();
     Staged Qs;
     cudaError_t e = Qs.in(queries, (size_t)nq * ix->d * 4, s);
     if (e) return cuda_fail(e, "stage queries");
@@ -866,7 +892,8 @@ nrlsh_status nrlsh_last_rerank_path(int32_t *path, int64_t *overflow_redone,
 }
 
 nrlsh_status nrlsh_last_query_stats(int64_t *fallback_queries, int64_t *kernel_launches,
-                                    int64_t *scanned_pairs) {
+                                    int64_t *scanned_pairs, int64_t *buffer_entries) {
+    if (buffer_entries) *buffer_entries = g_last_entries;
     if (fallback_queries) *fallback_queries = g_last_fallbacks;
     if (kernel_launches) *kernel_launches = g_last_launches;
     if (scanned_pairs) *scanned_pairs = g_last_pairs;
@@ -889,8 +916,7 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
     if (nq < 1) return fail(NRLSH_EINVAL, "nq must be >= 1");
     if (k < 1 || k > 1024) return fail(NRLSH_EINVAL, "k must be in [1, 1024]");
     cudaStream_t s = (cudaStream_t)cuda_stream;
-    configure_pool();
-    g_last_gt_max_cand = g_last_gt_sum_cand = g_last_gt_overflow = 0;
+    g_last_gt_max_cand = g_last_gt_sum_cand = g_last_gt_overflow = g_last_gt_pairs = 0;
     cudaError_t e;
     Staged Xs, Qs;
     if ((e = Xs.in(items, (size_t)n * d * 4, s))) return cuda_fail(e, "stage items");
@@ -925,9 +951,9 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
         cc.alloc((size_t)Qmax * 4, s) || cd.alloc((size_t)Qmax * Cg * 4, s) ||
         cs.alloc((size_t)Qmax * Cg * 4, s) || th.alloc((size_t)Qmax * 4, s) ||
         pt.alloc(std::max(rerank_partial_bytes(Qmax, Cg, k), rerank_partial_bytes(1, n, k)), s) ||
-        gst.alloc(32, s) || gov.alloc((size_t)nq * 8, s))
+        gst.alloc(40, s) || gov.alloc((size_t)nq * 8, s))
         return fail(NRLSH_ENOMEM, "exact_topk workspace");
-    cudaMemsetAsync(gst.p, 0, 32, s);
+    cudaMemsetAsync(gst.p, 0, 40, s);
     // bf16 item rows and |x|: the index's (written by its build), else prepared here
     const void *Xbp = Xb_ix;
     const float *xnp = xnorm_ix;
@@ -956,7 +982,7 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
     GtTiles gtl;
     gtl.xmax128 = tile_xmax_ix;
     gtl.ws = tw.get<int32_t>();
-    gtl.pairs = nullptr;
+    gtl.pairs = gst.get<unsigned long long>() + 4;   // (query, item) pairs multiplied
     gtl.xsplit = getenv("NRLSH_GT_ONEPASS") ? 0.f : xsplit_ix;
     gtl.pass = 0;
     gtl.qperm = nullptr;
@@ -1041,9 +1067,11 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
                                 (uint32_t *)(gst.get<unsigned long long>() + 2), s);
     }
     {   // overflowing queries (rare): exact scoring of every item
-        unsigned long long hst[3];
-        cudaMemcpyAsync(hst, gst.p, 24, cudaMemcpyDeviceToHost, s);
+        unsigned long long hst[5];
+        cudaMemcpyAsync(hst, gst.p, 40, cudaMemcpyDeviceToHost, s);
         if ((e = cudaStreamSynchronize(s))) return cuda_fail(e, "exact_topk");
+        // without tile lists the filter multiplies every (query, item) pair
+        g_last_gt_pairs = (Xb_ix && tile_xmax_ix && use_tc) ? (int64_t)hst[4] : (int64_t)(nq * n);
         g_last_gt_max_cand = (int64_t)hst[0];
         g_last_gt_sum_cand = (int64_t)hst[1];
         const uint32_t nov = (uint32_t)hst[2];
@@ -1066,7 +1094,9 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
     return NRLSH_OK;
 }
 
-nrlsh_status nrlsh_last_exact_stats(int64_t *max_cand, int64_t *sum_cand, int64_t *overflow) {
+nrlsh_status nrlsh_last_exact_stats(int64_t *max_cand, int64_t *sum_cand, int64_t *overflow,
+                                    int64_t *filter_pairs) {
+    if (filter_pairs) *filter_pairs = g_last_gt_pairs;
     if (max_cand) *max_cand = g_last_gt_max_cand;
     if (sum_cand) *sum_cand = g_last_gt_sum_cand;
     if (overflow) *overflow = g_last_gt_overflow;

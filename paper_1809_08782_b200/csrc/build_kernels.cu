@@ -450,7 +450,7 @@ struct DevBuf {
     template <class T> T *get() { return (T *)p; }
     cudaError_t alloc(size_t bytes) {
         if (p) { cudaFreeAsync(p, s); p = nullptr; }
-        return cudaMallocAsync(&p, bytes ? bytes : 16, s);
+        return dmalloc(&p, bytes ? bytes : 16, s);
     }
 };
 }  // namespace

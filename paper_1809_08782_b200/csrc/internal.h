@@ -62,6 +62,9 @@ struct nrlsh_index {
 
 namespace nrlsh {
 
+// stream-ordered device allocation from the library's private per-device pool
+cudaError_t dmalloc(void **p, size_t bytes, cudaStream_t s);
+
 // ---------------------------------------------------------------- tracing
 enum ProfSlot { SLOT_NORMS = 0, SLOT_PARTITION, SLOT_SCATTER, SLOT_CODES, SLOT_QCODES,
                 SLOT_PILOT, SLOT_SCAN, SLOT_FALLBACK, SLOT_SELECT, SLOT_SCORE, SLOT_TOPK,
@@ -197,6 +200,10 @@ void launch_dense_merge(const unsigned long long *partial, int S, int k, const i
                         const float *g_sc, int Qb, int64_t *out_ids, float *out_scores,
                         cudaStream_t s);
 
+// row gather (dst row r = src row idx[r]) or scatter (dst row idx[r] = src row r);
+// row_bytes a multiple of 4
+void launch_move_rows(const void *src, const int64_t *idx, int nrows, size_t row_bytes, void *dst,
+                      bool scatter, cudaStream_t s);
 // dst[p] = src[idx[p]] for p < n
 void launch_gather_f32(const float *src, const int32_t *idx, int64_t n, float *dst, cudaStream_t s);
 // theta_glob[q] = max(theta_glob[q], orderable image of out_scores[q][k-1]) when that

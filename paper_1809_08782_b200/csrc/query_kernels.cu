@@ -1171,6 +1171,24 @@ void launch_gather_f32(const float *src, const int32_t *idx, int64_t n, float *d
     note_launch();
 }
 
+// rows idx[r] of src -> row r of dst (scatter: row r of src -> row idx[r] of dst);
+// rows of `words` 32-bit words
+__global__ void move_rows(const uint32_t *__restrict__ src, const int64_t *__restrict__ idx, int nrows,
+                          int64_t words, uint32_t *__restrict__ dst, int scatter) {
+    for (int r = blockIdx.x; r < nrows; r += gridDim.x) {
+        const int64_t a = scatter ? r : idx[r], b = scatter ? idx[r] : r;
+        for (int64_t w = threadIdx.x; w < words; w += blockDim.x) dst[b * words + w] = src[a * words + w];
+    }
+}
+
+void launch_move_rows(const void *src, const int64_t *idx, int nrows, size_t row_bytes, void *dst,
+                      bool scatter, cudaStream_t s) {
+    if (nrows <= 0) return;
+    move_rows<<<std::min(nrows, 4096), 128, 0, s>>>((const uint32_t *)src, idx, nrows,
+                                                     (int64_t)(row_bytes / 4), (uint32_t *)dst, scatter);
+    note_launch();
+}
+
 __global__ void theta_from_topk(const int64_t *__restrict__ ids, const float *__restrict__ sc, int Qb,
                                 int k, uint32_t *__restrict__ theta_glob, int assign,
                                 uint32_t *__restrict__ zero_cnt) {

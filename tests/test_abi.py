@@ -68,3 +68,25 @@ def test_no_oracle_in_product_path():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 txt = open(os.path.join(dp, f)).read()
                 assert "import oracle" not in txt and "liboracle" not in txt, f
+
+
+def test_binding_validates_arrays_before_the_abi():
+    """The ABI takes raw pointers and cannot check dtype, width or shape: the binding
+    rejects a wrong dtype, a wrong row width or a wrong output shape before any call."""
+    import numpy as np
+    import paper_1809_08782_b200 as P
+    X = np.ones((8, 3), np.float32)
+    with pytest.raises(TypeError):
+        P.exact_topk(X.astype(np.float64), X, 2)
+    with pytest.raises(ValueError):
+        P.exact_topk(X, np.ones((2, 4), np.float32), 2)              # width != d
+    with pytest.raises(TypeError):
+        P.exact_topk(X, X[:2], 2, out_ids=np.empty((2, 2), np.int32))
+    with pytest.raises(ValueError):
+        P.exact_topk(X, X[:2], 2, out_ids=np.empty((2, 3), np.int64))
+    with pytest.raises(ValueError):
+        P.exact_topk(X, X[:2], 2, seed_ids=np.zeros((3, 2), np.int64))
+    with pytest.raises(ValueError):
+        P.exact_topk(np.asfortranarray(X), X[:2], 2)
+    with pytest.raises(TypeError):
+        P.Index(X.astype(np.float16), 32, 1)

@@ -87,12 +87,23 @@ def assert_topk_match(ids, scores, ref_ids, ref_scores, X, q, rtol=1e-4):
     assert np.all(np.abs(exact - s_ref) <= tol), (ids, ref_ids)
 
 
+def band_mask(gq, oq, frac=0.9):
+    """Queries whose GPU and oracle query codes agree (a query bit inside the 1e-5
+    band may differ, and then the probe order may legitimately differ).  At least
+    `frac` of the queries must be comparable, so a test cannot pass by skipping."""
+    same = np.array([np.array_equal(a, b) for a, b in zip(gq, oq)])
+    assert same.mean() >= frac, f"only {same.sum()} of {len(same)} query codes agree"
+    return same
+
+
 # ------------------------------------------------------------------ configs
 SMALL = [
     ("tiny", None, None, 32, 8),
     ("c2", None, 200, 64, 32),
     ("c3", 40_000, 64, 64, 64),
     ("c3", 40_000, 64, 64, 1),
+    ("c3", None, 64, 64, 64),        # c3 at its full n (Yahoo!Music-shaped, PAPER:1072)
+    ("c3", None, 64, 64, 1),         #   and plain SIMPLE-LSH on it (PAPER:1077)
     ("c4", 300_000, 32, 32, 128),    # pilot stride > 1 (n > 2^18)
     ("c4", 300_000, 32, 64, 128),
     ("scale", 70_000, 16, 128, 256),
@@ -184,11 +195,12 @@ def test_query_parity(built, case):
     gq = idx.query_codes(Qd).cpu().numpy().view(np.uint32)
     oq = oracle.query_codes(Q[:nq], orc.A)
     k = cfg.k
+    same = band_mask(gq, oq)
     for T in [t for t in _budgets(cfg, n) if t <= n][:5] + [n]:
         ids, sc = idx.query(Qd, k, T)
         ids, sc = ids.cpu().numpy(), sc.cpu().numpy()
         for qi in range(nq):
-            if not np.array_equal(gq[qi], oq[qi]):
+            if not same[qi]:
                 continue     # a query bit inside the 1e-5 band: different probe order allowed
             a, s = oracle.query(X, ocodes, orc.part, orc.R, orc.A, Q[qi], T, k)
             assert_topk_match(ids[qi], sc[qi], a, s, X, Q[qi])
@@ -397,6 +409,81 @@ def test_errors():
     assert e.value.code == "EINVAL"
 
 
+# ------------------------------------------------------- the bench's re-rank path
+def _headline_rerank_check(P, cfg, X, Q, idx, ocodes, part, R, A, L):
+    """The path bench.py times, at full size: the default re-rank selection with
+    more than one sub-batch (a ragged last one) and several 256-query pairs per
+    sub-batch — at c4 the tensor-core member-mode filter with bound-sorted query
+    pairs, proportional CTA shares and tile pruning (Alg. 2 l.6).  Every
+    query's ids and fp32 scores equal the gather path's bit for bit, and sampled
+    queries equal the oracle's answer (the oracle's codes are injected)."""
+    n = X.shape[0]
+    if cfg.name == "c4":
+        T, nqh = cfg.T((1, 100)), cfg.query_batch + 300       # the bench's T; 1024 + 300
+    else:
+        T, nqh = n // 200, 1100                                 # T >= n/300: the tensor path
+    Qh = np.ascontiguousarray(Q[:nqh])
+    Qd = torch.from_numpy(Qh).cuda()
+    os.environ.pop("NRLSH_RERANK_TC", None)
+    ti, ts = idx.query(Qd, cfg.k, T)
+    info = P.last_rerank_path()
+    assert info["path"] == "tensor", info
+    assert info["filter_pairs"] > 0
+    try:
+        os.environ["NRLSH_RERANK_TC"] = "0"
+        gi, gs = idx.query(Qd, cfg.k, T)
+        assert P.last_rerank_path()["path"] == "gather"
+    finally:
+        os.environ.pop("NRLSH_RERANK_TC", None)
+    assert torch.equal(gi, ti)
+    assert torch.equal(gs.view(torch.int32), ts.view(torch.int32))
+    ti, ts = ti.cpu().numpy(), ts.cpu().numpy()
+    gq = idx.query_codes(Qd).cpu().numpy().view(np.uint32)
+    qc = oracle.query_codes(Qh, A)
+    rng = np.random.default_rng(2)
+    sample = sorted(set([0, 255, 256, cfg.query_batch - 1, cfg.query_batch, nqh - 1]
+                        + rng.choice(nqh, 14, replace=False).tolist()))
+    same = band_mask(gq[sample], qc[sample], 0.8)
+    for s_, qi in zip(same, sample):
+        if s_:
+            a, sc = oracle.query(X, ocodes, part, R, A, Qh[qi], T, cfg.k)
+            assert_topk_match(ti[qi], ts[qi], a, sc, X, Qh[qi])
+
+
+def test_rerank_path_selection(built, monkeypatch):
+    """The automatic re-rank rule (api.cu): the tensor-core filter iff T >= n/300 and
+    a full sub-batch's Qmax * T >= 1.28 n; both sides of each threshold."""
+    cfg, X, Q, Xd, idx, orc = built("c4", 300_000, 32, 64, 128)
+    P = _P()
+    monkeypatch.delenv("NRLSH_RERANK_TC", raising=False)
+    n = X.shape[0]
+    Qrep = np.ascontiguousarray(np.concatenate([Q] * 20)[:600])
+    assert n == 300_000            # n / 300 = 1000; 1.28 n = 384,000
+    for nq, T, want in [(500, 1000, "tensor"), (500, 999, "gather"), (384, 1000, "tensor"),
+                        (383, 1000, "gather"), (300, 1280, "tensor"), (300, 1279, "gather"),
+                        (1, n, "gather"), (600, 10, "gather")]:
+        idx.query(torch.from_numpy(Qrep[:nq]).cuda(), 10, T)
+        assert P.last_rerank_path()["path"] == want, (nq, T)
+
+
+@pytest.mark.parametrize("nq", [513, 700])
+def test_rerank_tensor_multi_pair_matches_gather(built, nq, monkeypatch):
+    """Several 256-query pairs per sub-batch with a ragged last pair, under the
+    automatic selection (bound-sorted pairs, proportional CTA shares, pruning):
+    bit-identical to the gather path at T = n/100 and n/3."""
+    cfg, X, Q, Xd, idx, orc = built("c4", 300_000, 32, 64, 128)
+    P = _P()
+    n = X.shape[0]
+    Qd = torch.from_numpy(np.ascontiguousarray(np.concatenate([Q] * 25)[:nq])).cuda()
+    for T in (n // 100, n // 3):
+        monkeypatch.delenv("NRLSH_RERANK_TC", raising=False)
+        ti, ts = idx.query(Qd, cfg.k, T)
+        assert P.last_rerank_path()["path"] == "tensor", T
+        monkeypatch.setenv("NRLSH_RERANK_TC", "0")
+        gi, gs = idx.query(Qd, cfg.k, T)
+        assert torch.equal(gi, ti) and torch.equal(gs.view(torch.int32), ts.view(torch.int32)), T
+
+
 # ------------------------------------------------------- full (BASELINE) sizes
 @pytest.mark.parametrize("name,L,m", [("c4", 64, 128), ("c4", 32, 128), ("scale", 128, 256)])
 def test_full_size_sampled(name, L, m):
@@ -442,10 +529,12 @@ def test_full_size_sampled(name, L, m):
     gq = idx.query_codes(Qd).cpu().numpy().view(np.uint32)
     ids, sc = idx.query(Qd, cfg.k, T)
     ids, sc = ids.cpu().numpy(), sc.cpu().numpy()
+    same = band_mask(gq, qc, 0.8)
     for qi in range(len(qs)):
-        if np.array_equal(gq[qi], qc[qi]):
+        if same[qi]:
             a, s = oracle.query(X, ocodes, part, R, A, qs[qi], T, cfg.k)
             assert_topk_match(ids[qi], sc[qi], a, s, X, qs[qi])
+    _headline_rerank_check(P, cfg, X, Q, idx, ocodes, part, R, A, L)
     gt_ids, gt_sc = P.exact_topk(Xd, torch.from_numpy(Q[:3]).cuda(), cfg.k)
     gt_ids, gt_sc = gt_ids.cpu().numpy(), gt_sc.cpu().numpy()
     for qi in range(3):
@@ -458,8 +547,8 @@ def test_full_size_sampled(name, L, m):
                                   ("tiny", None, None, 32, 8), ("c4", 300_000, 32, 32, 4),
                                   ("c3", 40_000, 64, 64, 1)], ids=_ids)
 def test_candidates_parity_both_scans(built, case, scan, monkeypatch):
-    """Both Hamming scans — the tcgen05 int8 one (scan_tc.cu, the default) and the
-    popcount one (NRLSH_SCAN_TC=0) — give the oracle's candidate sets, ranks and
+    """The Hamming scans — the popcount one (the default), the tcgen05 int8 one
+    (scan_tc.cu, NRLSH_SCAN_TC=1) and the warp-level IMMA one — give the oracle's candidate sets, ranks and
     (R, id) order (identical codes injected), across budgets from 1 to n."""
     monkeypatch.setenv("NRLSH_SCAN_TC", "1" if scan == "tensor" else "0")
     monkeypatch.setenv("NRLSH_SCAN_IMMA", "1" if scan == "imma" else "0")
@@ -520,11 +609,12 @@ def test_dense_rerank_path(built, case, monkeypatch):
     Qd = torch.from_numpy(Q[:nq]).cuda()
     gq = idx.query_codes(Qd).cpu().numpy().view(np.uint32)
     oq = oracle.query_codes(Q[:nq], orc.A)
+    same = band_mask(gq, oq)
     for T in sorted(set([cfg.k, (n + 99) // 100, n // 7, n])):
         ids, sc = idx.query(Qd, cfg.k, T)
         ids, sc = ids.cpu().numpy(), sc.cpu().numpy()
         for qi in range(nq):
-            if not np.array_equal(gq[qi], oq[qi]):
+            if not same[qi]:
                 continue
             a, s = oracle.query(X, ocodes, orc.part, orc.R, orc.A, Q[qi], T, cfg.k)
             assert_topk_match(ids[qi], sc[qi], a, s, X, Q[qi])
@@ -542,11 +632,12 @@ def test_small_last_sub_batch_large_budget(built):
     idx.set_codes(ocodes[orc.perm])
     gq = idx.query_codes(Qd).cpu().numpy().view(np.uint32)
     oq = oracle.query_codes(Qbig, orc.A)
+    same = band_mask(gq, oq)
     for T in (1777, n // 2):
         ids, sc = idx.query(Qd, cfg.k, T)
         ids, sc = ids.cpu().numpy(), sc.cpu().numpy()
         for qi in list(range(1024, 1033)) + [0, 511]:
-            if not np.array_equal(gq[qi], oq[qi]):
+            if not same[qi]:
                 continue
             a, s = oracle.query(X, ocodes, orc.part, orc.R, orc.A, Qbig[qi], T, cfg.k)
             assert_topk_match(ids[qi], sc[qi], a, s, X, Qbig[qi])
@@ -689,11 +780,12 @@ def test_odd_shapes_parity(shape):
     gq = idx.query_codes(Qd).cpu().numpy().view(np.uint32)
     oq = oracle.query_codes(Q, orc.A)
     k = 10
+    same = band_mask(gq, oq, 0.75)
     for T in (1, 37, (n + 99) // 100, n // 3, n):
         ids, sc = idx.query(Qd, k, T)
         ids, sc = ids.cpu().numpy(), sc.cpu().numpy()
         for qi in range(len(Q)):
-            if not np.array_equal(gq[qi], oq[qi]):
+            if not same[qi]:
                 continue
             a, s = oracle.query(X, ocodes, orc.part, orc.R, orc.A, Q[qi], T, k)
             assert_topk_match(ids[qi], sc[qi], a, s, X, Q[qi])

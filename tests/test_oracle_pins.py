@@ -137,6 +137,60 @@ def test_partition_uniform_spec_example():
     assert part.tolist() == g["part"]
 
 
+def test_partition_uniform_ranges_are_on_the_norm_not_its_square():
+    """Fig. 3(a) / PAPER:1365 split the 2-norm range into equal-width intervals.
+    Norms [0, 3, 4, 5], m = 2: the interval width is 2.5, so {0} | {3, 4, 5}; an
+    equal-width split of ||x||^2 (width 12.5 over [0, 25]) would give {0, 3} | {4, 5}."""
+    nv = np.array([0.0, 3.0, 4.0, 5.0]) ** 2
+    part, perm, offsets, V = oracle.partition(nv, 2, scheme="uniform")
+    assert part.tolist() == [0, 1, 1, 1]
+    assert offsets.tolist() == [0, 1, 4]
+    assert V.tolist() == [0.0, 25.0]
+
+
+def test_partition_uniform_interior_boundaries():
+    """An item exactly on an interior boundary u_j = lo + j (hi - lo) / m opens
+    sub-dataset j (half-open [u_j, u_{j+1})); the maximum norm closes the last one
+    (reading Q19).  All values here are exact in binary."""
+    part, _, offsets, V = oracle.partition(np.array([1.0, 2.0, 3.0, 5.0]) ** 2, 2, scheme="uniform")
+    assert part.tolist() == [0, 0, 1, 1]                 # 3 = lo + (hi - lo) / 2
+    part, _, offsets, V = oracle.partition(np.arange(5.0) ** 2, 4, scheme="uniform")
+    assert part.tolist() == [0, 1, 2, 3, 3]              # 1, 2, 3 on boundaries; 4 = max
+    assert offsets.tolist() == [0, 1, 2, 3, 5]
+    assert V.tolist() == [0.0, 1.0, 4.0, 16.0]
+    # empty sub-datasets are allowed (SPEC:367); their V is 0
+    part, _, offsets, V = oracle.partition(np.array([1.0, 1.1, 9.0, 10.0]) ** 2, 4, scheme="uniform")
+    assert part.tolist() == [0, 0, 3, 3] and offsets.tolist() == [0, 2, 2, 2, 4]
+    assert V[1] == 0.0 and V[2] == 0.0
+    # all norms equal: one non-empty range (hi == lo)
+    part, _, offsets, _ = oracle.partition(np.full(6, 2.0), 3, scheme="uniform")
+    assert part.tolist() == [0] * 6 and offsets.tolist() == [0, 6, 6, 6]
+
+
+@pytest.mark.parametrize("m", [1, 3, 7, 32, 256])
+def test_partition_uniform_matches_brute_force_edges(m):
+    """Brute force, written independently: explicit edges lo + (hi - lo) k / m and
+    a search for the interval of every norm (numpy searchsorted), on long-tailed
+    norms; perm = ids grouped by interval, ascending id; V = max norm^2 per interval."""
+    rng = _rng(11 + m)
+    r = np.exp(rng.normal(0.0, 1.0, 20_000))
+    nv = r * r
+    part, perm, offsets, V = oracle.partition(nv, m, scheme="uniform")
+    rr = np.sqrt(nv)
+    lo, hi = rr.min(), rr.max()
+    edges = lo + (hi - lo) * np.arange(m + 1) / m
+    ref = np.clip(np.searchsorted(edges, rr, side="right") - 1, 0, m - 1)
+    near = np.min(np.abs(rr[:, None] - edges[None, 1:-1]), axis=1) < 1e-12 * hi if m > 1 \
+        else np.zeros(len(rr), bool)
+    assert near.sum() <= 2
+    assert np.array_equal(part[~near], ref[~near])
+    assert np.array_equal(perm, np.argsort(part, kind="stable"))
+    assert np.array_equal(offsets, np.concatenate([[0], np.cumsum(np.bincount(part, minlength=m))]))
+    for j in range(m):
+        sel = nv[part == j]
+        assert V[j] == (sel.max() if len(sel) else 0.0)
+
+
 # -------------------------------------------------------------- P3 transform
 def test_transform_spec_examples():
     for g in _gold("spec_examples.json")["transform"]:
