@@ -82,6 +82,17 @@ def _declare(L):
     L.orc_query.argtypes = [_p, _i64, _i32, _p, _p, _p, _i32, _p, _i32, _p, _i64, _i32,
                             _p, _p]
     L.orc_query.restype = C.c_int
+    L.orc_projection_pp.argtypes = [_u64, _i32, _i32, _i32, _p]
+    L.orc_projection_pp.restype = None
+    L.orc_item_codes_pp.argtypes = [_p, _i64, _i32, _p, _p, _p, _p, _i32, _p, _p]
+    L.orc_item_codes_pp.restype = C.c_int
+    L.orc_query_codes_pp.argtypes = [_p, _i64, _i32, _p, _i32, _i32, _p, _p]
+    L.orc_query_codes_pp.restype = C.c_int
+    L.orc_candidates_pp.argtypes = [_p, _p, _i64, _i32, _p, _p, _i32, _i64, _p, _p]
+    L.orc_candidates_pp.restype = _i64
+    L.orc_query_pp.argtypes = [_p, _i64, _i32, _p, _p, _p, _i32, _p, _i32, _p, _i64, _i32,
+                               _p, _p]
+    L.orc_query_pp.restype = C.c_int
 
 
 def _c(a, dtype):
@@ -256,11 +267,98 @@ def query(X, codes, part, R, A, q, T, k):
     return ids, sc
 
 
+# ---------------------------------------- per-sub-dataset projections (NEXT-4)
+def projection_pp(seed, m, rows, L):
+    """A_all [m, rows, L]: A_j from seed ^ j (SPEC:453)."""
+    A = np.empty((m, rows, L), np.float32)
+    lib().orc_projection_pp(C.c_uint64(seed & 0xFFFFFFFFFFFFFFFF), m, rows, L, _ptr(A))
+    return A
+
+
+def item_codes_pp(X, part, V, norm2_, A_all, want_z=False):
+    X = _c(X, np.float32)
+    n, d = X.shape
+    A_all = _c(A_all, np.float32)
+    L = A_all.shape[2]
+    assert A_all.shape[1] == d + 1
+    codes = np.empty((n, (L + 31) // 32), np.uint32)
+    z = np.empty((n, L), np.float64) if want_z else None
+    rc = lib().orc_item_codes_pp(_ptr(X), n, d, _ptr(_c(part, np.int32)), _ptr(_c(V, np.float64)),
+                                 _ptr(_c(norm2_, np.float64)), _ptr(A_all), L, _ptr(codes),
+                                 _ptr(z) if z is not None else None)
+    _check(rc, "item_codes_pp")
+    return (codes, z) if want_z else codes
+
+
+def item_codes_pp_parallel(X, part, V, norm2_, A_all, threads=None, chunk=1 << 15):
+    from concurrent.futures import ThreadPoolExecutor
+    X = _c(X, np.float32)
+    n = X.shape[0]
+    L = A_all.shape[2]
+    out = np.empty((n, (L + 31) // 32), np.uint32)
+    part = _c(part, np.int32)
+    nv = _c(norm2_, np.float64)
+
+    def work(r0):
+        r1 = min(n, r0 + chunk)
+        out[r0:r1] = item_codes_pp(X[r0:r1], part[r0:r1], V, nv[r0:r1], A_all)
+
+    with ThreadPoolExecutor(max_workers=threads or os.cpu_count()) as ex:
+        list(ex.map(work, range(0, n, chunk)))
+    return out
+
+
+def query_codes_pp(Q, A_all, want_z=False):
+    """qcodes [nq, m, W] (and z [nq, m, L])."""
+    Q = _c(Q, np.float32)
+    nq, d = Q.shape
+    A_all = _c(A_all, np.float32)
+    m, L = A_all.shape[0], A_all.shape[2]
+    W = (L + 31) // 32
+    qc = np.empty((nq, m, W), np.uint32)
+    z = np.empty((nq, m, L), np.float64) if want_z else None
+    rc = lib().orc_query_codes_pp(_ptr(Q), nq, d, _ptr(A_all), m, L, _ptr(qc),
+                                  _ptr(z) if z is not None else None)
+    _check(rc, "query_codes_pp")
+    return (qc, z) if want_z else qc
+
+
+def candidates_pp(codes, part, qcodes_m, R, T):
+    """qcodes_m [m, W]: the query's code under each sub-index's projection."""
+    codes = _c(codes, np.uint32)
+    n, W = codes.shape
+    R = _c(R, np.uint16)
+    m, L = R.shape[0], R.shape[1] - 1
+    Tp = min(int(T), n)
+    ids = np.empty(Tp, np.int32)
+    rk = np.empty(Tp, np.uint16)
+    got = lib().orc_candidates_pp(_ptr(codes), _ptr(_c(part, np.int32)), n, L,
+                                  _ptr(_c(qcodes_m, np.uint32)), _ptr(R), m, int(T),
+                                  _ptr(ids), _ptr(rk))
+    _check(got, "candidates_pp")
+    return ids[:got], rk[:got]
+
+
+def query_pp(X, codes, part, R, A_all, q, T, k):
+    X = _c(X, np.float32)
+    n, d = X.shape
+    R = _c(R, np.uint16)
+    L = R.shape[1] - 1
+    ids = np.empty(k, np.int64)
+    sc = np.empty(k, np.float64)
+    rc = lib().orc_query_pp(_ptr(X), n, d, _ptr(_c(codes, np.uint32)), _ptr(_c(part, np.int32)),
+                            _ptr(R), R.shape[0], _ptr(_c(A_all, np.float32)), L,
+                            _ptr(_c(q, np.float32)), int(T), int(k), _ptr(ids), _ptr(sc))
+    _check(rc, "query_pp")
+    return ids, sc
+
+
 # ------------------------------------------------------------- whole index
 class OracleIndex:
     """Alg. 1 end to end on the CPU (D1-D5, D8-D9)."""
 
-    def __init__(self, X, code_bits, num_parts, seed, eps=0.01, scheme="percentile"):
+    def __init__(self, X, code_bits, num_parts, seed, eps=0.01, scheme="percentile",
+                 proj="shared"):
         self.X = _c(X, np.float32)
         n, d = self.X.shape
         self.L = int(code_bits)
@@ -269,11 +367,31 @@ class OracleIndex:
         self.norm2 = norm2(self.X)
         self.part, self.perm, self.offsets, self.V = partition(self.norm2, self.m, scheme)
         self.U = np.sqrt(self.V)
+        self.proj = proj
         self.A = projection(seed, d + 1, self.L)
+        # per-sub-dataset projections (A_all[j] = A_j; A_all[0] == A)
+        self.A_all = projection_pp(seed, self.m, d + 1, self.L) if proj == "per_partition" else None
         self.R, self.order = rank_table(self.U, self.L, self.eps)
 
     def codes(self, want_z=False):
+        if self.proj == "per_partition":
+            return item_codes_pp(self.X, self.part, self.V, self.norm2, self.A_all, want_z=want_z)
         return item_codes(self.X, self.part, self.V, self.norm2, self.A, want_z=want_z)
+
+    def query_codes(self, Q, want_z=False):
+        if self.proj == "per_partition":
+            return query_codes_pp(Q, self.A_all, want_z=want_z)
+        return query_codes(Q, self.A, want_z=want_z)
+
+    def candidates(self, codes, qcode, T):
+        if self.proj == "per_partition":
+            return candidates_pp(codes, self.part, qcode, self.R, T)
+        return candidates(codes, self.part, qcode, self.R, T)
+
+    def query(self, codes, q, T, k):
+        if self.proj == "per_partition":
+            return query_pp(self.X, codes, self.part, self.R, self.A_all, q, T, k)
+        return query(self.X, codes, self.part, self.R, self.A, q, T, k)
 
 
 def recall_at_k(ret_ids, true_ids):

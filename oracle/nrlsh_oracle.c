@@ -494,3 +494,116 @@ int orc_query(const float *X, int64_t n, int32_t d, const uint32_t *codes,
     free(crk);
     return rc;
 }
+
+/* ================================================================== */
+/* Per-sub-dataset projections (reading Q4).  */
+/* Alg. 1 l.7 "Apply SIMPLE-LSH to build index I_j for S_j"           */
+/* (PAPER:155), "building a hash index for each sub-dataset            */
+/* independently": sub-index j draws its own projection A_j, */
+/* from the documented generator with seed_j = seed XOR j (SPEC:453,   */
+/* "seed (+) j"), so A_0 is the shared projection and m = 1 is plain   */
+/* SIMPLE-LSH again.  The query is hashed once per sub-index            */
+/* ("hash q once per sub-index"), and an item of S_j is      */
+/* compared with the query's code under A_j.                           */
+/* A_all: m blocks of (d+1) x L, block j = A_j.                         */
+/* ================================================================== */
+void orc_projection_pp(uint64_t seed, int32_t m, int32_t rows, int32_t L, float *A_all)
+{
+    for (int32_t j = 0; j < m; ++j)
+        orc_projection(seed ^ (uint64_t)j, rows, L, A_all + (int64_t)j * rows * L);
+}
+
+/* D5 with A := A_{j(i)}: each item is hashed by its own sub-index.      */
+int orc_item_codes_pp(const float *X, int64_t n, int32_t d,
+                      const int32_t *part, const double *V, const double *norm2,
+                      const float *A_all, int32_t L, uint32_t *codes, double *z)
+{
+    if (L < 1) return ORC_EINVAL;
+    int32_t W = (L + 31) / 32;
+    for (int64_t i = 0; i < n; ++i) {
+        const float *Aj = A_all + (int64_t)part[i] * (d + 1) * L;
+        int rc = orc_item_codes(X + i * (int64_t)d, 1, d, part + i, V, norm2 + i, Aj, L,
+                                codes + i * W, z ? z + i * (int64_t)L : NULL);
+        if (rc) return rc;
+    }
+    return ORC_OK;
+}
+
+/* D6 once per sub-index: qcodes [nq x m x W], z [nq x m x L].          */
+int orc_query_codes_pp(const float *Q, int64_t nq, int32_t d, const float *A_all,
+                       int32_t m, int32_t L, uint32_t *qcodes, double *z)
+{
+    if (L < 1 || m < 1) return ORC_EINVAL;
+    int32_t W = (L + 31) / 32;
+    for (int64_t i = 0; i < nq; ++i)
+        for (int32_t j = 0; j < m; ++j) {
+            int rc = orc_query_codes(Q + i * (int64_t)d, 1, d, A_all + (int64_t)j * (d + 1) * L, L,
+                                     qcodes + (i * m + j) * W,
+                                     z ? z + (i * m + j) * (int64_t)L : NULL);
+            if (rc) return rc;
+        }
+    return ORC_OK;
+}
+
+/* D10 with per-sub-index query codes: qcodes [m x W]; item i is compared */
+/* with the query's code of its own sub-dataset, qcodes[part[i]].         */
+int64_t orc_candidates_pp(const uint32_t *codes, const int32_t *part, int64_t n,
+                          int32_t L, const uint32_t *qcodes, const uint16_t *R,
+                          int32_t m, int64_t T, int32_t *cand_ids,
+                          uint16_t *cand_rank)
+{
+    if (L < 1 || T < 1) return ORC_EINVAL;
+    int32_t W = (L + 31) / 32;
+    int64_t nent = (int64_t)m * (L + 1);
+    int64_t Tp = T < n ? T : n;
+    int64_t *start = (int64_t *)calloc((size_t)nent + 1, sizeof(int64_t));
+    int64_t *fill = (int64_t *)malloc(sizeof(int64_t) * (size_t)nent);
+    int32_t *key = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
+    int32_t *items = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
+    if (!start || !fill || !key || !items) {
+        free(start); free(fill); free(key); free(items);
+        return ORC_ENOMEM;
+    }
+    for (int64_t i = 0; i < n; ++i) {
+        int32_t h = orc_hamming(codes + i * W, qcodes + (int64_t)part[i] * W, W);
+        key[i] = (int32_t)R[(int64_t)part[i] * (L + 1) + h];
+        start[key[i] + 1] += 1;
+    }
+    for (int64_t p = 0; p < nent; ++p) start[p + 1] += start[p];
+    for (int64_t p = 0; p < nent; ++p) fill[p] = start[p];
+    for (int64_t i = 0; i < n; ++i) items[fill[key[i]]++] = (int32_t)i;
+    int64_t taken = 0;
+    for (int64_t p = 0; p < nent && taken < Tp; ++p) {
+        for (int64_t e = start[p]; e < start[p + 1] && taken < Tp; ++e) {
+            cand_ids[taken] = items[e];
+            cand_rank[taken] = (uint16_t)p;
+            ++taken;
+        }
+    }
+    free(start); free(fill); free(key); free(items);
+    return taken;
+}
+
+/* One whole query with per-sub-index projections.                       */
+int orc_query_pp(const float *X, int64_t n, int32_t d, const uint32_t *codes,
+                 const int32_t *part, const uint16_t *R, int32_t m,
+                 const float *A_all, int32_t L, const float *q, int64_t T,
+                 int32_t k, int64_t *out_ids, double *out_scores)
+{
+    if (L > 256 || m < 1) return ORC_EINVAL;
+    int32_t W = (L + 31) / 32;
+    uint32_t *qc = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)m * W);
+    int64_t Tp = T < n ? T : n;
+    int32_t *cid = (int32_t *)malloc(sizeof(int32_t) * (size_t)Tp);
+    uint16_t *crk = (uint16_t *)malloc(sizeof(uint16_t) * (size_t)Tp);
+    if (!qc || !cid || !crk) { free(qc); free(cid); free(crk); return ORC_ENOMEM; }
+    int rc = orc_query_codes_pp(q, 1, d, A_all, m, L, qc, NULL);
+    if (!rc) {
+        int64_t got = orc_candidates_pp(codes, part, n, L, qc, R, m, T, cid, crk);
+        rc = got < 0 ? (int)got : orc_rerank(X, n, d, q, cid, got, k, out_ids, out_scores);
+    }
+    free(qc);
+    free(cid);
+    free(crk);
+    return rc;
+}

@@ -506,3 +506,105 @@ def test_range_beats_simple_on_long_tail():
             r.append(len(set(a) & set(b)) / 10)
         rec[m] = np.mean(r)
     assert rec[16] >= rec[1] - 0.05
+
+
+# --------------------------- NEXT-4: per-sub-dataset projections (reading Q4)
+def test_pp_one_partition_is_the_shared_projection():
+    """seed_j = seed XOR j, so A_0 is the shared A and m = 1 is plain
+    SIMPLE-LSH: codes, query codes, candidates and answers equal the shared-A path."""
+    cfg = workloads.scaled(workloads.CONFIGS["tiny"], 1500, 6)
+    X = workloads.make_items(cfg)
+    Q = workloads.make_queries(cfg)
+    a = oracle.OracleIndex(X, 32, 1, seed=13)
+    b = oracle.OracleIndex(X, 32, 1, seed=13, proj="per_partition")
+    assert np.array_equal(b.A_all[0], a.A)
+    ca, cb = a.codes(), b.codes()
+    assert np.array_equal(ca, cb)
+    qa, qb = a.query_codes(Q), b.query_codes(Q)
+    assert np.array_equal(qa, qb[:, 0, :])
+    for qi in range(len(Q)):
+        assert np.array_equal(a.candidates(ca, qa[qi], 200)[0], b.candidates(cb, qb[qi], 200)[0])
+        assert np.array_equal(a.query(ca, Q[qi], 200, 10)[0], b.query(cb, Q[qi], 200, 10)[0])
+
+
+def test_pp_projections_are_independent_gaussians():
+    """Each A_j is i.i.d. N(0, 1) (Eq. (4)) and A_j, A_j' are
+    uncorrelated (independent hash families per sub-index)."""
+    from scipy import stats
+    A = oracle.projection_pp(99, 3, 65, 512).astype(np.float64)
+    for j in range(3):
+        assert stats.kstest(A[j].ravel(), "norm").pvalue > 1e-3
+        assert np.array_equal(A[j], oracle.projection(99 ^ j, 65, 512))
+    for j, jj in ((0, 1), (1, 2), (0, 2)):
+        r = np.corrcoef(A[j].ravel(), A[jj].ravel())[0, 1]
+        assert abs(r) < 4.0 / math.sqrt(A[j].size)
+
+
+def test_pp_collision_law_per_sub_index():
+    """Within sub-index j the bits of P(x) and P(q) = [q; 0] under A_j agree with
+    probability 1 - acos(q.x/(U_j|q|))/pi (Eq. (4)); a query
+    code taken under another sub-index's projection agrees with probability 1/2
+    (independent hyperplanes) — so an item must be compared with the query's code
+    of its own sub-index."""
+    L = 1 << 16
+    m = 2
+    A_all = oracle.projection_pp(31, m, 3, L)
+    X = np.array([[0.6, 0.0], [0.0, 0.9], [0.3, 0.3], [0.5, -0.5]], np.float32)
+    part = np.array([0, 0, 1, 1], np.int32)
+    nv = oracle.norm2(X)
+    V = np.array([nv[:2].max(), nv[2:].max()])
+    codes = oracle.item_codes_pp(X, part, V, nv, A_all)
+    q = np.array([[1.0, 0.0]], np.float32)
+    qc = oracle.query_codes_pp(q, A_all)[0]            # [m, W]
+    for i in range(4):
+        j = part[i]
+        p = 1.0 - math.acos(float(X[i, 0]) / math.sqrt(V[j])) / math.pi
+        sig = math.sqrt(p * (1 - p) / L)
+        agree = (L - oracle.hamming(codes[i], qc[j])) / L
+        assert abs(agree - p) < 4 * sig, (i, agree, p)
+        other = (L - oracle.hamming(codes[i], qc[1 - j])) / L
+        assert abs(other - 0.5) < 4 * math.sqrt(0.25 / L), (i, other)
+
+
+@pytest.mark.parametrize("L,m", [(32, 8), (64, 5), (17, 3)])
+def test_pp_candidates_match_sorted_keys(L, m):
+    """D10 with per-sub-index query codes, against a brute-force sort of all keys
+    (R[j(i)][popc(code_i ^ qcode_q[j(i)])], i) written here with numpy."""
+    cfg = workloads.scaled(workloads.CONFIGS["tiny"], 2500, 4)
+    X = workloads.make_items(cfg)[:, :24]
+    Q = workloads.make_queries(cfg)[:, :24]
+    idx = oracle.OracleIndex(X, L, m, seed=7, proj="per_partition")
+    codes = idx.codes()
+    qc = idx.query_codes(Q)
+    for qi in range(4):
+        h = _popcount_np(codes ^ qc[qi][idx.part])
+        key = idx.R[idx.part, h].astype(np.int64)
+        order = np.lexsort((np.arange(len(X)), key))
+        for T in (1, 40, 900, 2500, 4000):
+            ids, rk = idx.candidates(codes, qc[qi], T)
+            t = min(T, len(X))
+            assert np.array_equal(ids, order[:t])
+            assert np.array_equal(rk.astype(np.int64), key[order[:t]])
+
+
+def test_pp_codes_use_each_items_own_projection():
+    """Every item's per-sub-index code equals the shared-A oracle code of that item
+    computed with A := A_{j(i)} (D5 applied sub-index by sub-index), and the
+    query codes equal the shared-A query codes under each A_j."""
+    cfg = workloads.scaled(workloads.CONFIGS["c2"], 900, 5)
+    X = workloads.make_items(cfg)[:, :40]
+    Q = workloads.make_queries(cfg)[:, :40]
+    idx = oracle.OracleIndex(X, 64, 6, seed=3, proj="per_partition")
+    codes = idx.codes()
+    for j in range(6):
+        sel = idx.part == j
+        ref = oracle.item_codes(X[sel], idx.part[sel], idx.V, idx.norm2[sel], idx.A_all[j])
+        assert np.array_equal(codes[sel], ref)
+    qc = idx.query_codes(Q)
+    for j in range(6):
+        assert np.array_equal(qc[:, j, :], oracle.query_codes(Q, idx.A_all[j]))
+    # T = n: every item is probed, so the answer is the brute-force top-k (SPEC:426)
+    for qi in range(len(Q)):
+        a, _ = idx.query(codes, Q[qi], len(X), 10)
+        b, _ = oracle.exact_topk(X, Q[qi], 10)
+        assert np.array_equal(a, b)
