@@ -66,6 +66,12 @@ def parse():
                     help="comma-separated configs: per probe budget queries/s and recall@k "
                          "(no driver line; writes --sweep-out)")
     ap.add_argument("--sweep-out", default=None)
+    ap.add_argument("--proj", default="shared", choices=["shared", "per_partition"],
+                    help="sub-index projections (DESIGN.md reading Q4; NEXT-4)")
+    ap.add_argument("--scheme", default="percentile", choices=["percentile", "uniform"],
+                    help="partitioning (Alg. 1 l.4; uniform = Fig. 3(a), NEXT-2)")
+    ap.add_argument("--sweep-parts", default=None,
+                    help="with --sweep: comma-separated m values instead of the config's")
     return ap.parse_args()
 
 
@@ -646,12 +652,17 @@ def run_sweep(args):
         Qd = torch.from_numpy(Q).to(dev)
         k = cfg.k
         gt = None
-        for L, m, Ts, ibits in _sweep_plan(cfg, args.sweep_m):
+        plan = _sweep_plan(cfg, args.sweep_m)
+        if args.sweep_parts:
+            ms = [int(v) for v in args.sweep_parts.split(",")]
+            Ts0, ib0 = plan[0][2], plan[0][3]
+            plan = [(L, m_, Ts0, ib0) for L in cfg.code_bits for m_ in ms]
+        for L, m, Ts, ibits in plan:
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             idx = P.Index(Xd, L, m, seed=cfg.seed, query_batch=cfg.query_batch,
-                          index_bits_in_budget=ibits)
+                          index_bits_in_budget=ibits, proj=args.proj, scheme=args.scheme)
             e1.record()
             torch.cuda.synchronize()
             build_ms = e0.elapsed_time(e1)
@@ -671,6 +682,7 @@ def run_sweep(args):
                 rec = float(np.mean([len(set(a.tolist()) & set(b.tolist())) / k
                                      for a, b in zip(ids, gt)]))
                 row = {"config": name, "n": cfg.n, "d": cfg.d, "code_bits": L, "num_parts": m,
+                       "proj": args.proj, "scheme": args.scheme,
                        "hash_bits": idx.hash_bits, "index_bits_in_budget": ibits,
                        "nq": len(Q), "k": k, "probe_budget": int(T), "budget_frac": T / cfg.n,
                        "queries_per_s": len(Q) / (float(np.median(ms)) / 1e3),

@@ -43,6 +43,13 @@ typedef enum {
 enum { NRLSH_SCHEME_PERCENTILE = 0, /* Alg. 1 l.4             */
        NRLSH_SCHEME_UNIFORM = 1 };  /* equal-width norm ranges */
 
+/* Hash functions of the sub-indexes ("Apply SIMPLE-LSH to build index I_j for S_j",
+   Alg. 1 l.7).  SHARED: one projection A for every sub-dataset (one
+   query code per query).  PER_PARTITION: sub-index j draws its own A_j with seed
+   seed XOR j, so A_0 = A; the query is hashed once per sub-index and an
+   item of S_j is compared with the query's code under A_j. */
+enum { NRLSH_PROJ_SHARED = 0, NRLSH_PROJ_PER_PARTITION = 1 };
+
 typedef struct nrlsh_options {
     double eps;            /* metric adjustment of PAPER:215, 0 <= eps < 1; default 0.01 */
     int32_t scheme;        /* NRLSH_SCHEME_*; default PERCENTILE                        */
@@ -50,7 +57,9 @@ typedef struct nrlsh_options {
                                      (PAPER:1075), so L_h = code_bits - ceil(log2 m);
                                      0 (default): all code_bits are SRP hash bits         */
     int32_t query_batch;   /* queries per internal sub-batch; 0 -> 1024                  */
-    int32_t reserved;
+    int32_t proj;          /* NRLSH_PROJ_*; default SHARED.  PER_PARTITION needs the
+                              tensor-core code kernel's shapes (d <= 512, L_h <= 128,
+                              ceil(L_h/32) != 3), else NRLSH_ENOTIMPL                  */
 } nrlsh_options;
 
 /* Fill *opt with the defaults above. */
@@ -75,7 +84,8 @@ void nrlsh_default_options(nrlsh_options *opt);
  *            in 1, 2 or 4 32-bit words.
  * num_parts  m, 1 <= m <= min(n, 256) (percentile) / 256 (uniform).
  * seed       seeds the projection matrix A [(d+1) x L_h] (one A shared by all
- *            sub-datasets, reading Q4): entry e = k*L_h + b is
+ *            sub-datasets, reading Q4; with opt->proj = PER_PARTITION
+ *            sub-dataset j uses the same generator with seed XOR j): entry e = k*L_h + b is
  *            g = sqrt(-2 ln u1) cos(2 pi u2) with u1 = ((s(2e) >> 11) + 1) 2^-53,
  *            u2 = (s(2e+1) >> 11) 2^-53, s(c) = SplitMix64 output at counter c
  *            (z = seed + (c+1)*0x9E3779B97F4A7C15, then the standard mix), rounded
@@ -120,16 +130,20 @@ nrlsh_status nrlsh_exact_topk(const float *items, int64_t n, int32_t d,
 void nrlsh_free(nrlsh_index *index);
 const char *nrlsh_last_error(void);
 
-/* Index geometry: n, d, L_h (hash bits), m, words per code (ceil(L_h/32)). */
+/* Index geometry: n, d, L_h (hash bits), m, words per code (ceil(L_h/32)).
+   (nrlsh_get_proj gives the projection mode.) */
 nrlsh_status nrlsh_get_info(const nrlsh_index *index, int64_t *n, int32_t *d,
                             int32_t *hash_bits, int32_t *num_parts, int32_t *words);
+
+/* Projection mode of the index: NRLSH_PROJ_SHARED or NRLSH_PROJ_PER_PARTITION. */
+nrlsh_status nrlsh_get_proj(const nrlsh_index *index, int32_t *proj);
 
 /* ---- parity / test hooks (copies; pointers may be host or device) ------- */
 /* norm2 fp64 [n] (item-id order), perm int32 [n] (ids grouped by sub-dataset,
    ascending id within), offsets int64 [m+1], V fp64 [m] = U_j^2. Any may be NULL. */
 nrlsh_status nrlsh_get_partition(const nrlsh_index *index, double *norm2, int32_t *perm,
                                  int64_t *offsets, double *V);
-/* A fp32 [(d+1) x L_h] row-major. */
+/* A fp32 [(d+1) x L_h] row-major; PER_PARTITION: m such blocks, block j = A_j. */
 nrlsh_status nrlsh_get_projection(const nrlsh_index *index, float *A);
 /* R uint16 [m x (L_h+1)]: position of (j, h) in the sorted structure. */
 nrlsh_status nrlsh_get_rank_table(const nrlsh_index *index, uint16_t *R);
@@ -137,13 +151,15 @@ nrlsh_status nrlsh_get_rank_table(const nrlsh_index *index, uint16_t *R);
 nrlsh_status nrlsh_get_codes(const nrlsh_index *index, uint32_t *codes);
 /* overwrite the codes (same layout) — lets tests inject the oracle's codes. */
 nrlsh_status nrlsh_set_codes(nrlsh_index *index, const uint32_t *codes);
-/* query codes uint32 [nq x words] of P(q) = [q; 0]. */
+/* query codes uint32 [nq x words] of P(q) = [q; 0]; PER_PARTITION: [nq x m x words],
+   the code of q under each sub-index's projection A_j. */
 nrlsh_status nrlsh_query_codes(const nrlsh_index *index, const float *queries, int64_t nq,
                                uint32_t *qcodes, void *cuda_stream);
 /* The probed candidates of each query (a prefix of the probing order, exactly
    min(T,n) per query, in unspecified order): cand_ids int32 [nq x T'] and their
    positions in the sorted structure cand_rank uint16 [nq x T'].  qcodes may be
-   NULL (computed from queries) or injected (then queries may be NULL). */
+   NULL (computed from queries) or injected (then queries may be NULL), laid out as
+   nrlsh_query_codes returns them. */
 nrlsh_status nrlsh_query_candidates(const nrlsh_index *index, const float *queries,
                                     const uint32_t *qcodes, int64_t nq, int64_t probe_budget,
                                     int32_t *cand_ids, uint16_t *cand_rank, void *cuda_stream);

@@ -25,7 +25,7 @@ EXPORTS = [
     "nrlsh_query_codes", "nrlsh_query_candidates", "nrlsh_last_query_stats",
     "nrlsh_index_exact_topk", "nrlsh_exact_topk_seeded", "nrlsh_index_exact_topk_seeded",
     "nrlsh_last_rerank_stats", "nrlsh_last_rerank_path", "nrlsh_profile_enable", "nrlsh_profile_read",
-    "nrlsh_profile_slot_name", "nrlsh_launch_count", "nrlsh_last_exact_stats",
+    "nrlsh_profile_slot_name", "nrlsh_launch_count", "nrlsh_last_exact_stats", "nrlsh_get_proj",
 ]
 
 
@@ -38,7 +38,7 @@ class NrlshError(RuntimeError):
 
 class Options(C.Structure):
     _fields_ = [("eps", C.c_double), ("scheme", C.c_int32), ("index_bits_in_budget", C.c_int32),
-                ("query_batch", C.c_int32), ("reserved", C.c_int32)]
+                ("query_batch", C.c_int32), ("proj", C.c_int32)]
 
 
 _lib = None
@@ -70,6 +70,8 @@ def lib():
         L.nrlsh_last_error.restype = C.c_char_p
         L.nrlsh_get_info.argtypes = [p, p, p, p, p, p]
         L.nrlsh_get_info.restype = st
+        L.nrlsh_get_proj.argtypes = [p, p]
+        L.nrlsh_get_proj.restype = st
         L.nrlsh_get_partition.argtypes = [p, p, p, p, p]
         L.nrlsh_get_partition.restype = st
         L.nrlsh_get_projection.argtypes = [p, p]
@@ -188,7 +190,7 @@ class Index:
     """An nrlsh_index handle (Alg. 1).  Keeps the item buffer alive (borrowed)."""
 
     def __init__(self, items, code_bits, num_parts, seed=0, eps=0.01, scheme="percentile",
-                 index_bits_in_budget=False, query_batch=0, stream=None):
+                 index_bits_in_budget=False, query_batch=0, stream=None, proj="shared"):
         _want(items, "items", ("float32",), (None, None))
         self._items = items
         self._device = _dev_of(items)
@@ -198,6 +200,7 @@ class Index:
         opt.scheme = {"percentile": 0, "uniform": 1}[scheme]
         opt.index_bits_in_budget = 1 if index_bits_in_budget else 0
         opt.query_batch = int(query_batch)
+        opt.proj = {"shared": 0, "per_partition": 1}[proj]
         n, d = items.shape
         h = C.c_void_p()
         _check(lib().nrlsh_build_ex(_ptr(items), n, d, int(code_bits), int(num_parts),
@@ -209,6 +212,14 @@ class Index:
                                     C.byref(w)))
         self.n, self.d, self.hash_bits, self.num_parts, self.words = (
             ni.value, di.value, hb.value, npart.value, w.value)
+        pj = C.c_int32()
+        _check(lib().nrlsh_get_proj(h, C.byref(pj)))
+        self.proj = "per_partition" if pj.value == 1 else "shared"
+        # query codes per query: one, or one per sub-index (A_j)
+        self.qm = self.num_parts if self.proj == "per_partition" else 1
+
+    def _qshape(self, nq):
+        return (nq, self.qm, self.words) if self.qm > 1 else (nq, self.words)
 
     def close(self):
         if getattr(self, "_h", None):
@@ -261,7 +272,7 @@ class Index:
     def query_codes(self, queries, stream=None):
         _want(queries, "queries", ("float32",), (None, self.d), self._device)
         nq = queries.shape[0]
-        out = _empty_like_io(queries, (nq, self.words), np.uint32, _torch_dtype("int32"))
+        out = _empty_like_io(queries, self._qshape(nq), np.uint32, _torch_dtype("int32"))
         _check(lib().nrlsh_query_codes(self._h, _ptr(queries), nq, _ptr(out), _stream(stream)))
         return out
 
@@ -270,7 +281,7 @@ class Index:
         if queries is not None:
             _want(queries, "queries", ("float32",), (None, self.d), self._device)
         if qcodes is not None:
-            _want(qcodes, "qcodes", ("uint32",), (None, self.words), self._device)
+            _want(qcodes, "qcodes", ("uint32",), self._qshape(None), self._device)
             if queries is not None and queries.shape[0] != qcodes.shape[0]:
                 raise ValueError("queries and qcodes disagree on nq")
         nq = ref.shape[0]
@@ -293,7 +304,9 @@ class Index:
         return norm2, perm, offsets, V
 
     def projection(self):
-        A = np.empty((self.d + 1, self.hash_bits), np.float32)
+        """A [(d+1) x L_h]; per-sub-dataset projections: [m x (d+1) x L_h], A[j] = A_j."""
+        shp = (self.d + 1, self.hash_bits)
+        A = np.empty(((self.qm,) + shp) if self.qm > 1 else shp, np.float32)
         _check(lib().nrlsh_get_projection(self._h, _ptr(A)))
         return A
 

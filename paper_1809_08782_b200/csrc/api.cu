@@ -132,7 +132,7 @@ void free_index(nrlsh_index *ix) {
     void *ps[] = {ix->X_owned, ix->Xpad, ix->Xb, ix->xnorm, ix->norm2, ix->perm, ix->pos_of_id, ix->part_of_id,
                   ix->part_of_pos, ix->offsets_d, ix->V_d, ix->codes, ix->A, ix->Apad,
                   ix->R_d, ix->chunks_d, ix->order_d, ix->samp_codes, ix->samp_part,
-                  ix->tiles_d, ix->xnorm_pos, ix->tile_xmax, ix->codes_pm};
+                  ix->tiles_d, ix->xnorm_pos, ix->tile_xmax, ix->codes_pm, ix->ctiles_d};
     // pool-backed (cudaMallocAsync at build); the index may have been used on any stream
     cudaDeviceSynchronize();
     for (void *p : ps)
@@ -225,7 +225,7 @@ void nrlsh_default_options(nrlsh_options *opt) {
     opt->scheme = NRLSH_SCHEME_PERCENTILE;
     opt->index_bits_in_budget = 0;
     opt->query_batch = 0;
-    opt->reserved = 0;
+    opt->proj = NRLSH_PROJ_SHARED;
 }
 
 const char *nrlsh_last_error(void) { return g_last_error.c_str(); }
@@ -253,6 +253,8 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
     if (!(o.eps >= 0.0 && o.eps < 1.0)) return fail(NRLSH_EINVAL, "eps must be in [0, 1)");
     if (o.scheme != NRLSH_SCHEME_PERCENTILE && o.scheme != NRLSH_SCHEME_UNIFORM)
         return fail(NRLSH_EINVAL, "unknown partition scheme");
+    if (o.proj != NRLSH_PROJ_SHARED && o.proj != NRLSH_PROJ_PER_PARTITION)
+        return fail(NRLSH_EINVAL, "unknown projection mode");
     if (num_parts < 1 || num_parts > kMaxParts)
         return fail(NRLSH_EINVAL, "num_parts must be in [1, 256]");
     if (o.scheme == NRLSH_SCHEME_PERCENTILE && (int64_t)num_parts > n)
@@ -279,6 +281,11 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
     ix->eps = o.eps;
     ix->scheme = o.scheme;
     ix->query_batch = o.query_batch > 0 ? o.query_batch : 1024;
+    ix->proj = o.proj;
+    ix->QM = o.proj == NRLSH_PROJ_PER_PARTITION ? num_parts : 1;
+    if (ix->QM > 1 && !codes_tc_supported(d, words_for(L)))
+        return fail(NRLSH_ENOTIMPL, "per-sub-dataset projections need the tensor-core code kernel's "
+                                    "shapes (d <= 512, ceil(L_h/32) != 3)");
     cudaGetDevice(&ix->device);
     const int m = num_parts, W = ix->W;
 
@@ -303,8 +310,12 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
     // filter pass (half the bytes of the fp32 rows it then gathers only for survivors)
     // rows of d % 4 != 0 floats are only 4- or 8-byte aligned: a 16-byte-aligned padded
     // fp32 copy (written by the codes pass) lets the re-rank gather with 16-byte loads
+    // (opt-in NRLSH_XPAD=1: a 16-byte-aligned fp32 row copy for the re-rank's gathers
+    // when 4 does not divide d — measured a wash on c4: the codes pass saves 0.17 ms
+    // without it, the 8-byte-load gathers lose about as much)
     ix->dpad = (d + 3) / 4 * 4;
-    if (ix->dpad != d && !getenv("NRLSH_NO_XPAD")) NR_ALLOC(ix->Xpad, (size_t)n * ix->dpad * 4);
+    if (ix->dpad != d && getenv("NRLSH_XPAD") && atoi(getenv("NRLSH_XPAD")) != 0)
+        NR_ALLOC(ix->Xpad, (size_t)n * ix->dpad * 4);
     ix->dpb = (d + 7) / 8 * 8;
     const int64_t npad = (n + 255) / 256 * 256;
     NR_ALLOC(ix->Xb, (size_t)n * ix->dpb * 2);
@@ -320,7 +331,7 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
     cudaMemsetAsync(ix->xnorm_pos + n, 0, (size_t)(npad - n) * 4, s);
     NR_ALLOC(ix->tile_xmax, (size_t)((n + 127) / 128) * 4);
     // +-1 rows for the opt-in tensor-core scan (NRLSH_SCAN_TC=1 at build and query)
-    if (L <= 128 && getenv("NRLSH_SCAN_TC") && atoi(getenv("NRLSH_SCAN_TC")) != 0)
+    if (L <= 128 && ix->QM == 1 && getenv("NRLSH_SCAN_TC") && atoi(getenv("NRLSH_SCAN_TC")) != 0)
         NR_ALLOC(ix->codes_pm, (size_t)n * scan_kp(L));
     NR_ALLOC(ix->offsets_d, (size_t)(m + 1) * 8);
     NR_ALLOC(ix->V_d, (size_t)m * 8);
@@ -367,11 +378,18 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
     ix->U.resize(m);
     for (int j = 0; j < m; ++j) ix->U[j] = std::sqrt(ix->V[j]);
 
-    // K4 (host): projection and the sorted (U_j, l) structure
-    make_projection(seed, d + 1, L, ix->A_h);
-    std::vector<float> Apad((size_t)(d + 1) * 32 * W, 0.f);
-    for (int k = 0; k <= d; ++k)
-        for (int b = 0; b < L; ++b) Apad[(size_t)k * 32 * W + b] = ix->A_h[(size_t)k * L + b];
+    // K4 (host): projection(s) and the sorted (U_j, l) structure
+    const int QM = ix->QM;
+    const size_t ablk = (size_t)(d + 1) * L, pblk = (size_t)(d + 1) * 32 * W;
+    ix->A_h.resize(QM * ablk);
+    std::vector<float> Apad(QM * pblk, 0.f);
+    for (int j = 0; j < QM; ++j) {   // A_j from seed XOR j (A_0 = the shared A)
+        std::vector<float> Aj;
+        make_projection(seed ^ (uint64_t)j, d + 1, L, Aj);
+        std::copy(Aj.begin(), Aj.end(), ix->A_h.begin() + j * ablk);
+        for (int k = 0; k <= d; ++k)
+            for (int b = 0; b < L; ++b) Apad[j * pblk + (size_t)k * 32 * W + b] = Aj[(size_t)k * L + b];
+    }
     std::vector<int32_t> order;
     make_rank_table(ix->U, L, ix->eps, ix->R_h, order);
     // scan work units: chunks of <= scan_chunk_items() positions inside one sub-dataset
@@ -387,6 +405,17 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
         for (int64_t p = ix->offsets[j]; p < ix->offsets[j + 1]; p += 256)
             tiles.push_back(make_int4(j, (int)p, (int)std::min<int64_t>(p + 256, ix->offsets[j + 1]), 0));
     ix->ntiles = (int32_t)tiles.size();
+    // per-sub-dataset projections: the code kernel's tiles of <= 128 positions of one j
+    std::vector<int4> ctiles;
+    if (QM > 1)
+        for (int j = 0; j < m; ++j)
+            for (int64_t p = ix->offsets[j]; p < ix->offsets[j + 1]; p += 128)
+                ctiles.push_back(make_int4(j, (int)p, (int)std::min<int64_t>(p + 128, ix->offsets[j + 1]), 0));
+    ix->nctiles = (int32_t)ctiles.size();
+    if (QM > 1) {
+        NR_ALLOC(ix->ctiles_d, ctiles.size() * sizeof(int4));
+        cudaMemcpyAsync(ix->ctiles_d, ctiles.data(), ctiles.size() * sizeof(int4), cudaMemcpyHostToDevice, s);
+    }
     NR_ALLOC(ix->A, ix->A_h.size() * 4);
     NR_ALLOC(ix->Apad, Apad.size() * 4);
     NR_ALLOC(ix->R_d, ix->R_h.size() * 2);
@@ -403,9 +432,14 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
     // K3: codes
     {
         ProfScope p(SLOT_CODES, s);
-        launch_item_codes(ix->X, n, d, ix->norm2, ix->part_of_id, ix->V_d, ix->Apad, L, W,
-                          ix->pos_of_id, ix->codes, ix->Xb, ix->dpb, ix->xnorm, ix->Xpad,
-                          ix->dpad, s, ix->perm);
+        if (QM > 1)
+            launch_item_codes_tc(ix->X, n, d, ix->norm2, ix->part_of_id, ix->V_d, ix->Apad, L, W,
+                                 ix->pos_of_id, ix->codes, ix->Xb, ix->dpb, ix->Xpad, ix->dpad, s,
+                                 ix->ctiles_d, ix->nctiles, ix->perm);
+        else
+            launch_item_codes(ix->X, n, d, ix->norm2, ix->part_of_id, ix->V_d, ix->Apad, L, W,
+                              ix->pos_of_id, ix->codes, ix->Xb, ix->dpb, ix->xnorm, ix->Xpad,
+                              ix->dpad, s, ix->perm);
     }
     // |x| in partition order (the tensor-core filter's tiles)
     {
@@ -488,11 +522,11 @@ void run_candidates(const nrlsh_index *ix, const float *Qd, const uint32_t *qcod
                     int32_t *seeds = nullptr, int ks = 0, void *fb_ws = nullptr,
                     unsigned long long *entries = nullptr) {
     if (qcodes_in) {
-        cudaMemcpyAsync(qcodes, qcodes_in + qbase * ix->W, (size_t)Qb * ix->W * 4,
+        cudaMemcpyAsync(qcodes, qcodes_in + qbase * ix->QM * ix->W, (size_t)Qb * ix->QM * ix->W * 4,
                         cudaMemcpyDeviceToDevice, s);
     } else {
         ProfScope p(SLOT_QCODES, s);
-        launch_qcodes(Qd, Qb, ix->d, ix->Apad, ix->L, ix->W, qcodes, flags, qbase, s);
+        launch_qcodes(Qd, Qb, ix->d, ix->Apad, ix->L, ix->W, qcodes, flags, qbase, s, ix->QM);
     }
     {
         ProfScope p(SLOT_PILOT, s);
@@ -585,7 +619,7 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
         if (e) return cuda_fail(e, "stage queries");
     }
     if (qcodes_user) {
-        e = QCs.in(qcodes_user, (size_t)nq * ix->W * 4, s);
+        e = QCs.in(qcodes_user, (size_t)nq * ix->QM * ix->W * 4, s);
         if (e) return cuda_fail(e, "stage qcodes");
     }
     OutBuf oi, os, oc, orr;
@@ -598,7 +632,7 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
         if (rank_out && (e = orr.init(rank_out, (size_t)nq * Tq * 2, s))) return cuda_fail(e, "cand_rank");
     }
     DBuf qc, dl, cn, cv, ba, bf, cd, pt, fl, fbw;
-    if (qc.alloc((size_t)Qmax * ix->W * 4, s) || dl.alloc((size_t)Qmax * ix->m, s) ||
+    if (qc.alloc((size_t)Qmax * ix->QM * ix->W * 4, s) || dl.alloc((size_t)Qmax * ix->m, s) ||
         cn.alloc((size_t)Qmax * 4, s) || cv.alloc((size_t)Qmax * 4, s) ||
         ba.alloc(scan_tc_supported(ix) ? scan_tc_ws_bytes(ix, Qmax) : 16, s) ||
         bf.alloc((size_t)Qmax * C * 8, s) ||
@@ -610,7 +644,7 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
     // dense re-rank of the sub-datasets most of whose pairs are candidates (rerank_dense.cu)
     const float *Xr = ix->Xpad ? ix->Xpad : ix->X;
     const int ldr = ix->Xpad ? ix->dpad : ix->d;
-    const bool use_dense = want_topk && dense_rerank_supported(ldr, ix->W, k);
+    const bool use_dense = want_topk && ix->QM == 1 && dense_rerank_supported(ldr, ix->W, k);
     const int S = use_dense ? dense_splits(Qmax) : 0;
     DBuf sb, spk, cpart, dmask, dinf, nco, gid, gsc, dpart;
     if (use_dense &&
@@ -664,6 +698,7 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
     mb.R = ix->R_d;
     mb.L = ix->L;
     mb.W = ix->W;
+    mb.qm = ix->QM;
     GtTiles tls;
     tls.xmax128 = ix->tile_xmax;
     tls.ws = use_rtc ? rtl.get<int32_t>() : nullptr;
@@ -860,7 +895,7 @@ nrlsh_status nrlsh_query_codes(const nrlsh_index *ix, const float *queries, int6
     cudaError_t e = Qs.in(queries, (size_t)nq * ix->d * 4, s);
     if (e) return cuda_fail(e, "stage queries");
     OutBuf oq;
-    if ((e = oq.init(qcodes, (size_t)nq * ix->W * 4, s))) return cuda_fail(e, "qcodes");
+    if ((e = oq.init(qcodes, (size_t)nq * ix->QM * ix->W * 4, s))) return cuda_fail(e, "qcodes");
     DBuf fl;
     if (fl.alloc(16, s)) return fail(NRLSH_ENOMEM, "flags");
     const int init_flags[4] = {INT_MAX, INT_MAX, 0, 0};
@@ -868,7 +903,7 @@ nrlsh_status nrlsh_query_codes(const nrlsh_index *ix, const float *queries, int6
     for (int64_t q0 = 0; q0 < nq; q0 += 65535) {
         const int Qb = (int)std::min<int64_t>(65535, nq - q0);
         launch_qcodes((const float *)Qs.dev + q0 * ix->d, Qb, ix->d, ix->Apad, ix->L, ix->W,
-                      (uint32_t *)oq.dev + q0 * ix->W, fl.get<int>(), q0, s);
+                      (uint32_t *)oq.dev + q0 * ix->QM * ix->W, fl.get<int>(), q0, s, ix->QM);
     }
     if ((e = oq.finish(s))) return cuda_fail(e, "copy qcodes");
     int hflags[4];
@@ -1159,6 +1194,12 @@ nrlsh_status nrlsh_get_partition(const nrlsh_index *ix, double *norm2, int32_t *
 nrlsh_status nrlsh_get_projection(const nrlsh_index *ix, float *A) {
     if (!ix || !A) return fail(NRLSH_EINVAL, "bad argument");
     return copy_out(A, ix->A, ix->A_h.size() * 4);
+}
+
+nrlsh_status nrlsh_get_proj(const nrlsh_index *ix, int32_t *proj) {
+    if (!ix || !proj) return fail(NRLSH_EINVAL, "bad argument");
+    *proj = ix->proj;
+    return NRLSH_OK;
 }
 
 nrlsh_status nrlsh_get_rank_table(const nrlsh_index *ix, uint16_t *R) {

@@ -57,7 +57,40 @@ struct CodesArgs {
     int dpb;
     float *Xpad;             // optional fp32 row copy [n x dpad], 16-byte rows (re-rank gathers)
     int dpad;
+    // per-sub-dataset projections (reading Q4, NEXT-4): items in partition
+    // order, tile t = ctiles[t] = (j, p0, p1) of <= 128 positions of sub-dataset j,
+    // projected by A_j = Apad + j (d+1) N; each CTA takes a contiguous run of tiles, so
+    // the resident B operand is reloaded only when j changes
+    const int4 *ctiles;      // nullptr: shared A, tiles of 128 consecutive items
+    const int32_t *perm;     // position -> item id
 };
+
+// tile sequence of a CTA: shared A — tiles blockIdx.x + t gridDim.x; per-sub-dataset
+// A_j — the contiguous run [lo, hi)
+__device__ __forceinline__ void ct_range(const CodesArgs &a, int64_t &lo, int64_t &hi) {
+    if (a.ctiles) {
+        lo = a.ntiles * blockIdx.x / gridDim.x;
+        hi = a.ntiles * (blockIdx.x + 1) / gridDim.x;
+    } else {
+        lo = blockIdx.x;
+        hi = a.ntiles;
+    }
+}
+__device__ __forceinline__ int64_t ct_step(const CodesArgs &a) { return a.ctiles ? 1 : gridDim.x; }
+
+// row rr of tile `tile`: item id (i < 0: past the tile / past n) and destination position
+__device__ __forceinline__ void ct_row(const CodesArgs &a, int64_t tile, int rr, int64_t &i, int64_t &pos) {
+    if (a.ctiles) {
+        const int4 t = __ldg(a.ctiles + tile);
+        const int64_t p = (int64_t)t.y + rr;
+        if (p < t.z) { pos = p; i = __ldg(a.perm + p); }
+        else { pos = -1; i = -1; }
+    } else {
+        i = tile * CT_M + rr;
+        if (i >= a.n) i = -1;
+        pos = -1;   // (shared A: pos_of_id[i], read where needed)
+    }
+}
 
 __device__ __forceinline__ uint32_t swz(int row, int kbyte) {
     return (uint32_t)(row * 128 + ((((kbyte >> 4) ^ (row & 7))) << 4) + (kbyte & 15));
@@ -73,10 +106,16 @@ __device__ __forceinline__ void conv_issue(const CodesArgs &a, int64_t tile, int
     // with the first K-block of a tile, the warp's 16 rows' partition positions (the
     // bf16 copy's destination rows; read back by the warp only)
     if (kb == 0 && a.Xb && l < 16) {
-        const int64_t i = tile * CT_M + 16 * w + l;
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4, 4;" ::"r"(tc::smem_u32(posr + 16 * w + l)),
-                     "l"(a.pos_of_id + (i < a.n ? i : a.n - 1))
-                     : "memory");
+        if (a.ctiles) {   // destination rows are the positions themselves
+            int64_t i, pos;
+            ct_row(a, tile, 16 * w + l, i, pos);
+            posr[16 * w + l] = (int32_t)pos;
+        } else {
+            const int64_t i = tile * CT_M + 16 * w + l;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, 4;" ::"r"(tc::smem_u32(posr + 16 * w + l)),
+                         "l"(a.pos_of_id + (i < a.n ? i : a.n - 1))
+                         : "memory");
+        }
     }
     constexpr int lpr = VEC == 4 ? 8 : (VEC == 2 ? 16 : 32);
     constexpr int rpi = 32 / lpr;
@@ -87,11 +126,12 @@ __device__ __forceinline__ void conv_issue(const CodesArgs &a, int64_t tile, int
 #pragma unroll
     for (int j = 0; j < ni; ++j) {
         const int rr = 16 * w + j * rpi + l / lpr;
-        const int64_t i = tile * CT_M + rr;
-        const int64_t ic = i < a.n ? i : a.n - 1;
+        int64_t i, pos;
+        ct_row(a, tile, rr, i, pos);
+        const int64_t ic = i >= 0 ? i : 0;
         const float *p = a.X + ic * a.d + cc;
         const uint32_t dst = tc::smem_u32(slot + (size_t)(j * CT_CONV + tid) * VEC * 4);
-        const int nb = ((i < a.n) && (col < a.d)) ? VEC * 4 : 0;
+        const int nb = ((i >= 0) && (col < a.d)) ? VEC * 4 : 0;
         asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(dst), "l"(p), "n"(VEC * 4),
                      "r"(nb)
                      : "memory");
@@ -170,9 +210,9 @@ __device__ __forceinline__ void conv_store_bf16(const CodesArgs &a, int64_t tile
 #pragma unroll
     for (int j = 0; j < ni; ++j) {
         const int rr = 16 * w + j * rpi + l / lpr;
-        const int64_t i = tile * CT_M + rr;
-        if (i >= a.n) continue;
-        __nv_bfloat16 *dst = a.Xb + (int64_t)posr[rr] * a.dpb + col;
+        const int32_t prow = posr[rr];
+        if (a.ctiles ? prow < 0 : tile * CT_M + rr >= a.n) continue;
+        __nv_bfloat16 *dst = a.Xb + (int64_t)prow * a.dpb + col;
         if (VEC == 4) {
             const __nv_bfloat162 p0 = __floats2bfloat162_rn(v[j * 4 + 0], v[j * 4 + 1]);
             const __nv_bfloat162 p1 = __floats2bfloat162_rn(v[j * 4 + 2], v[j * 4 + 3]);
@@ -199,8 +239,9 @@ __device__ __forceinline__ void conv_store_pad(const CodesArgs &a, int64_t tile,
 #pragma unroll
     for (int j = 0; j < ni; ++j) {
         const int rr = 16 * w + j * rpi + l / lpr;
-        const int64_t i = tile * CT_M + rr;
-        if (i >= a.n) continue;
+        int64_t i, pos;
+        ct_row(a, tile, rr, i, pos);
+        if (i < 0) continue;
         float *dst = a.Xpad + i * a.dpad + col;
         if (VEC == 4) *reinterpret_cast<float4 *>(dst) = make_float4(v[j * 4], v[j * 4 + 1], v[j * 4 + 2], v[j * 4 + 3]);
         else if (VEC == 2) *reinterpret_cast<float2 *>(dst) = make_float2(v[j * 2], v[j * 2 + 1]);
@@ -221,18 +262,25 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k3_codes_tc(CodesArgs a) {
     uint64_t *tfull = bars + 2 * a.stages, *tempty = tfull + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
     int32_t *posr = reinterpret_cast<int32_t *>(tempty + 4);     // [4][CT_M], ring by tile
+    uint64_t *bdone = reinterpret_cast<uint64_t *>(posr + 4 * CT_M);   // MMAs drained (B reload)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int N = a.N;
-    // resident B operand (A^T, K-major, swizzled) and A_d
-    for (int e = threadIdx.x; e < a.KB * N * CT_KB; e += blockDim.x) {
-        const int kb = e / (N * CT_KB), rem = e % (N * CT_KB);
-        const int b = rem / CT_KB, k = rem % CT_KB;
-        const int kg = kb * CT_KB + k;
-        const float v = kg < a.d ? a.Apad[(size_t)kg * N + b] : 0.f;
-        *reinterpret_cast<float *>(Bs + (size_t)kb * N * 128 + swz(b, k * 4)) = v;
+    // resident B operand (A^T, K-major, swizzled) and A_d (shared A; per-sub-dataset
+    // projections load A_j in the MMA warp when the tile's j changes)
+    auto load_B = [&](const float *Aj, int t0, int nt) {
+        for (int e = t0; e < a.KB * N * CT_KB; e += nt) {
+            const int kb = e / (N * CT_KB), rem = e % (N * CT_KB);
+            const int b = rem / CT_KB, k = rem % CT_KB;
+            const int kg = kb * CT_KB + k;
+            const float v = kg < a.d ? Aj[(size_t)kg * N + b] : 0.f;
+            *reinterpret_cast<float *>(Bs + (size_t)kb * N * 128 + swz(b, k * 4)) = v;
+        }
+    };
+    if (!a.ctiles) {
+        load_B(a.Apad, threadIdx.x, blockDim.x);
+        for (int b = threadIdx.x; b < N; b += blockDim.x) Ad[b] = a.Apad[(size_t)a.d * N + b];
     }
-    for (int b = threadIdx.x; b < N; b += blockDim.x) Ad[b] = a.Apad[(size_t)a.d * N + b];
     tc::fence_async_shared();
     if (threadIdx.x == 0) {
         for (int s = 0; s < a.stages; ++s) {
@@ -243,6 +291,7 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k3_codes_tc(CodesArgs a) {
             tc::mbar_init(&tfull[s], 1);
             tc::mbar_init(&tempty[s], 4);
         }
+        tc::mbar_init(bdone, 1);
         tc::fence_mbar_init();
     }
     const uint32_t tcols = N <= 16 ? 32 : (2 * N <= 64 ? 64 : (2 * N <= 128 ? 128 : 256));
@@ -256,24 +305,26 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k3_codes_tc(CodesArgs a) {
         // ================= converters
         // K-block g of this CTA = (tile blockIdx.x + (g / KB) gridDim.x, kb g % KB);
         // issue and consume cursors advance incrementally (no 64-bit divisions)
-        const int64_t my_tiles =
-            a.ntiles > (int64_t)blockIdx.x ? (a.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+        int64_t tlo, thi;
+        ct_range(a, tlo, thi);
+        const int64_t tst = ct_step(a);
+        const int64_t my_tiles = thi > tlo ? (thi - 1 - tlo) / tst + 1 : 0;
         const int64_t G = my_tiles * a.KB;
         const int la = a.raw - 1;
-        int64_t i_tile = blockIdx.x, issued = 0;
+        int64_t i_tile = tlo, issued = 0;
         int i_kb = 0, i_ti = 0, i_slot = 0;
         auto issue = [&]() {
             if (issued < G) {
                 conv_issue<VEC>(a, i_tile, i_kb, warp, lane, rawr + (size_t)i_slot * CT_RAW_SLOT,
                                 posr + (i_ti & 3) * CT_M);
-                if (++i_kb == a.KB) { i_kb = 0; i_tile += gridDim.x; ++i_ti; }
+                if (++i_kb == a.KB) { i_kb = 0; i_tile += tst; ++i_ti; }
                 if (++i_slot == a.raw) i_slot = 0;
             }
             ++issued;
             cp_async_commit();   // (empty groups keep the group count uniform)
         };
         for (int g = 0; g < la; ++g) issue();
-        int64_t tile = blockIdx.x;
+        int64_t tile = tlo;
         int kb = 0, ti = 0, rslot = 0;
         uint32_t s = 0, ph = 0;
         for (int64_t g = 0; g < G; ++g) {
@@ -289,16 +340,38 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k3_codes_tc(CodesArgs a) {
             tc::fence_async_shared();
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&full[s]);
-            if (++kb == a.KB) { kb = 0; tile += gridDim.x; ++ti; }
+            if (++kb == a.KB) { kb = 0; tile += tst; ++ti; }
             if (++rslot == a.raw) rslot = 0;
             if (++s == (uint32_t)a.stages) { s = 0; ph ^= 1; }
         }
     } else if (warp == 8) {
-        if (lane == 0) {
-            // ================= MMA issuer
+        {
+            // ================= MMA issuer (lane 0); per-sub-dataset projections: the
+            // warp reloads B = A_j^T when the tile's sub-dataset changes, after every
+            // MMA issued so far has completed
             const uint32_t idesc = tc::umma_idesc(2, CT_M, N);
-            uint32_t g = 0, t = 0;
-            for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++t) {
+            uint32_t g = 0, t = 0, nb = 0;
+            int curj = -1;
+            int64_t tlo, thi;
+            ct_range(a, tlo, thi);
+            const int64_t tst = ct_step(a);
+            for (int64_t tile = tlo; tile < thi; tile += tst, ++t) {
+                if (a.ctiles) {
+                    const int j = __ldg(a.ctiles + tile).x;
+                    if (j != curj) {
+                        if (t > 0) {
+                            if (lane == 0) tc::mma_commit(bdone);
+                            __syncwarp();
+                            tc::mbar_wait(bdone, nb & 1);
+                            ++nb;
+                        }
+                        load_B(a.Apad + (size_t)j * (a.d + 1) * N, lane, 32);
+                        tc::fence_async_shared();
+                        __syncwarp();
+                        curj = j;
+                    }
+                }
+                if (lane != 0) continue;
                 const uint32_t acc = t & 1, tr = t >> 1;
                 tc::mbar_wait(&tempty[acc], (tr & 1) ^ 1);
                 tc::tc_fence_after();
@@ -328,12 +401,17 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k3_codes_tc(CodesArgs a) {
         const int row = qd * 32 + lane;
         const int W = N / 32;
         uint32_t t = 0;
-        for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++t) {
+        int64_t tlo, thi;
+        ct_range(a, tlo, thi);
+        const int64_t tst = ct_step(a);
+        for (int64_t tile = tlo; tile < thi; tile += tst, ++t) {
             const uint32_t acc = t & 1, tr = t >> 1;
-            const int64_t i = tile * CT_M + row;
-            const bool valid = i < a.n;
+            int64_t i, pos = 0;
+            ct_row(a, tile, row, i, pos);
+            const bool valid = i >= 0;
+            // A_d of the tile's projection
+            const float *Adj = a.ctiles ? a.Apad + ((size_t)__ldg(a.ctiles + tile).x * (a.d + 1) + a.d) * N : Ad;
             float tt = 0.f;
-            int64_t pos = 0;
             if (valid) {
                 const double Vj = a.V[a.part[i]];
                 if (Vj == 0.0) tt = 1.f;
@@ -341,7 +419,7 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k3_codes_tc(CodesArgs a) {
                     const double df = Vj - a.norm2[i];
                     tt = (float)sqrt(df > 0.0 ? df : 0.0);
                 }
-                pos = a.pos_of_id[i];
+                if (!a.ctiles) pos = a.pos_of_id[i];
             }
             tc::mbar_wait(&tfull[acc], tr & 1);
             tc::tc_fence_after();
@@ -357,7 +435,7 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k3_codes_tc(CodesArgs a) {
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
                         const int b = c * 32 + j;
-                        const float y = fmaf(Ad[b], tt, __uint_as_float(r[j]));
+                        const float y = fmaf(Adj[b], tt, __uint_as_float(r[j]));
                         wd |= (uint32_t)(b < a.L && y >= 0.f) << j;
                     }
                     words[c] = wd;
@@ -383,7 +461,7 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k3_codes_tc(CodesArgs a) {
 
 static size_t codes_tc_smem(int KB, int N, int stages, int raw) {
     return 1024 + (size_t)stages * CT_STAGE + (size_t)raw * CT_RAW_SLOT + (size_t)KB * N * 128 +
-           (size_t)N * 4 + (2 * stages + 4) * 8 + 32 + 4 * CT_M * 4;
+           (size_t)N * 4 + (2 * stages + 4) * 8 + 32 + 4 * CT_M * 4 + 16;
 }
 
 // (MMA stages, raw slots): two MMA stages and up to 4 raw slots (48 KB of loads in
@@ -416,7 +494,8 @@ bool codes_tc_supported(int d, int W) {
 void launch_item_codes_tc(const float *X, int64_t n, int d, const double *norm2,
                           const uint8_t *part, const double *V, const float *Apad, int L, int W,
                           const int32_t *pos_of_id, uint32_t *codes, void *Xb, int dpb,
-                          float *Xpad, int dpad, cudaStream_t s) {
+                          float *Xpad, int dpad, cudaStream_t s, const int4 *ctiles, int nctiles,
+                          const int32_t *perm) {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     CodesArgs a;
@@ -427,7 +506,9 @@ void launch_item_codes_tc(const float *X, int64_t n, int d, const double *norm2,
     a.L = L;
     a.N = 32 * W;
     codes_tc_config(d, a.N, a.stages, a.raw);
-    a.ntiles = (n + CT_M - 1) / CT_M;
+    a.ctiles = ctiles;
+    a.perm = perm;
+    a.ntiles = ctiles ? nctiles : (n + CT_M - 1) / CT_M;
     a.norm2 = norm2;
     a.part = part;
     a.V = V;

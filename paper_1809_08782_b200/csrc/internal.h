@@ -18,6 +18,8 @@ struct nrlsh_index {
     uint64_t seed = 0;
     double eps = 0.01;
     int32_t scheme = NRLSH_SCHEME_PERCENTILE;
+    int32_t proj = NRLSH_PROJ_SHARED;
+    int32_t QM = 1;             // query codes per query: 1 (shared A) or m (per-sub-dataset A_j)
     int32_t query_batch = 1024;
     int device = 0;
 
@@ -42,8 +44,10 @@ struct nrlsh_index {
     uint32_t *codes = nullptr;      // [n x W], partition order
     int8_t *codes_pm = nullptr;     // [n x scan_kp(L)] +-1 int8 code rows, partition order
                                     //   (the tensor-core scan's B operand)
-    float *A = nullptr;             // [(d+1) x L] row-major (as generated)
-    float *Apad = nullptr;          // [(d+1) x 32W], zero columns >= L
+    float *A = nullptr;             // [QM x (d+1) x L] row-major (as generated; block j = A_j)
+    float *Apad = nullptr;          // [QM x (d+1) x 32W], zero columns >= L
+    int4 *ctiles_d = nullptr;       // per-sub-dataset projections: code-kernel tiles
+    int32_t nctiles = 0;            //   (j, p0, p1): <= 128 positions of one sub-dataset
     uint16_t *R_d = nullptr;        // [m x (L+1)]
     int4 *chunks_d = nullptr;       // scan work units (j, pos0, pos1, 0)
     int4 *tiles_d = nullptr;        // tensor-core scan tiles: <= 256 positions of one j
@@ -106,10 +110,14 @@ void launch_item_codes(const float *X, int64_t n, int d, const double *norm2,
 
 // K3 on tcgen05 (codes_tc.cu); the SIMT kernel above covers the other shapes
 bool codes_tc_supported(int d, int W);
+// (ctiles != nullptr: per-sub-dataset projections — items are processed in partition
+//  order, tile t = (j, p0, p1) uses A_j = Apad + j (d+1) 32W; perm maps positions to ids)
 void launch_item_codes_tc(const float *X, int64_t n, int d, const double *norm2,
                           const uint8_t *part_of_id, const double *V_d, const float *Apad,
                           int L, int W, const int32_t *pos_of_id, uint32_t *codes, void *Xb,
-                          int dpb, float *Xpad, int dpad, cudaStream_t s);
+                          int dpb, float *Xpad, int dpad, cudaStream_t s,
+                          const int4 *ctiles = nullptr, int nctiles = 0,
+                          const int32_t *perm = nullptr);
 
 // ---------------------------------------------------------------- query
 struct QueryWS {
@@ -124,8 +132,10 @@ struct QueryWS {
     int64_t C;          // buffer capacity per query
 };
 
+// qcodes [nq x QM x W]: QM = 1 (Apad = A) or m (Apad = [m x (d+1) x 32W], code j under A_j)
 void launch_qcodes(const float *Q, int64_t nq, int d, const float *Apad, int L, int W,
-                   uint32_t *qcodes, int *flags, int64_t q_index_base, cudaStream_t s);
+                   uint32_t *qcodes, int *flags, int64_t q_index_base, cudaStream_t s,
+                   int QM = 1);
 int pilot_stride(int64_t n);
 void launch_gather_sample(const nrlsh_index *ix, int stride, uint32_t *sc, uint8_t *sp,
                           cudaStream_t s);
@@ -254,7 +264,8 @@ struct GtMember {
     int m;
     const uint16_t *R;          // [m x (L+1)]
     int L, W;
-    const uint32_t *qcodes;     // [Qb x W]
+    const uint32_t *qcodes;     // [Qb x QM x W]
+    int qm;                     // QM: 1, or m (a query's code under each A_j)
     const uint32_t *sel_B, *sel_pk;   // [Qb]
 };
 // Tile pruning for rows in partition order (the index's Xb): per query pair, only

@@ -56,8 +56,86 @@ __global__ void __launch_bounds__(32 * W) k5_qcodes(const float *__restrict__ Q,
     if ((threadIdx.x & 31) == 0) qcodes[q * W + (threadIdx.x >> 5)] = word;
 }
 
+// Per-sub-dataset projections (reading Q4, NEXT-4): the code of q under
+// every A_j, qcodes[(q QM + j) W + w].  CTA = (64 queries, sub-index j): k-chunks of
+// A_j [64 x 32W] and of the queries [64 x 64] staged in shared memory; thread =
+// (column b, a slice of the queries); sign bits packed by warp ballots (lanes are
+// consecutive columns).  The j = 0 CTAs also flag zero / non-finite queries.
+constexpr int kQpT = 64;   // queries per CTA
+constexpr int kQpK = 32;   // k per staged chunk
+template <int W>
+__global__ void __launch_bounds__(256) k5_qcodes_pp(const float *__restrict__ Q, int64_t nq, int d,
+                                                    const float *__restrict__ Apad, int L, int QM,
+                                                    uint32_t *__restrict__ qcodes,
+                                                    int *__restrict__ flags, int64_t qbase) {
+    pdl_wait();
+    constexpr int NC = 32 * W;                 // columns
+    constexpr int QPT = kQpT * NC / 256;       // queries per thread
+    __shared__ float As[kQpK][NC];
+    __shared__ float Qs[kQpT][kQpK + 1];
+    __shared__ int sbad[kQpT], snz[kQpT];
+    const int j = blockIdx.y;
+    const int64_t q0 = (int64_t)blockIdx.x * kQpT;
+    const int col = threadIdx.x % NC, qs0 = (threadIdx.x / NC) * QPT;
+    const float *Aj = Apad + (int64_t)j * (d + 1) * NC;
+    if (threadIdx.x < kQpT) { sbad[threadIdx.x] = 0; snz[threadIdx.x] = 0; }
+    float acc[QPT];
+#pragma unroll
+    for (int u = 0; u < QPT; ++u) acc[u] = 0.f;
+    for (int k0 = 0; k0 < d; k0 += kQpK) {
+        __syncthreads();
+        for (int e = threadIdx.x; e < kQpK * NC; e += 256) {
+            const int k = e / NC, b = e % NC;
+            As[k][b] = k0 + k < d ? Aj[(int64_t)(k0 + k) * NC + b] : 0.f;
+        }
+        for (int e = threadIdx.x; e < kQpT * kQpK; e += 256) {
+            const int qi = e / kQpK, k = e % kQpK;
+            float v = 0.f;
+            if (q0 + qi < nq && k0 + k < d) {
+                v = Q[(q0 + qi) * d + k0 + k];
+                if (j == 0) {
+                    if (!isfinite(v)) sbad[qi] = 1;
+                    if (v != 0.f) snz[qi] = 1;
+                }
+            }
+            Qs[qi][k] = v;
+        }
+        __syncthreads();
+        const int kn = min(kQpK, d - k0);
+        for (int k = 0; k < kn; ++k) {   // k ascending: the fp32 FMA chain of k5_qcodes
+            const float a = As[k][col];
+#pragma unroll
+            for (int u = 0; u < QPT; ++u) acc[u] = fmaf(a, Qs[qs0 + u][k], acc[u]);
+        }
+    }
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int u = 0; u < QPT; ++u) {
+        const int64_t q = q0 + qs0 + u;
+        const unsigned word = __ballot_sync(NR_FULL, col < L && acc[u] >= 0.f);
+        if (lane == 0 && q < nq) qcodes[(q * QM + j) * W + col / 32] = word;
+    }
+    if (j == 0) {
+        __syncthreads();
+        if (threadIdx.x < kQpT && q0 + threadIdx.x < nq) {
+            if (sbad[threadIdx.x]) atomicMin(&flags[1], (int)(qbase + q0 + threadIdx.x));
+            else if (!snz[threadIdx.x]) atomicMin(&flags[0], (int)(qbase + q0 + threadIdx.x));
+        }
+    }
+}
+
 void launch_qcodes(const float *Q, int64_t nq, int d, const float *Apad, int L, int W,
-                   uint32_t *qcodes, int *flags, int64_t qbase, cudaStream_t s) {
+                   uint32_t *qcodes, int *flags, int64_t qbase, cudaStream_t s, int QM) {
+    if (QM > 1) {
+        const dim3 grid((unsigned)((nq + kQpT - 1) / kQpT), (unsigned)QM);
+        switch (W) {
+            case 1: launch_pdl(k5_qcodes_pp<1>, grid, dim3(256), 0, s, Q, nq, d, Apad, L, QM, qcodes, flags, qbase); break;
+            case 2: launch_pdl(k5_qcodes_pp<2>, grid, dim3(256), 0, s, Q, nq, d, Apad, L, QM, qcodes, flags, qbase); break;
+            default: launch_pdl(k5_qcodes_pp<4>, grid, dim3(256), 0, s, Q, nq, d, Apad, L, QM, qcodes, flags, qbase); break;
+        }
+        note_launch();
+        return;
+    }
     const size_t sm = (size_t)d * 4;
     switch (W) {
         case 1: launch_pdl(k5_qcodes<1>, dim3((int)nq), dim3(32), sm, s, Q, d, Apad, L, qcodes, flags, qbase); break;
@@ -83,6 +161,15 @@ __device__ __forceinline__ void load_code(const uint32_t *__restrict__ codes, in
     }
 }
 
+// Hamming distance to a query code held in (shared) memory
+template <int W>
+__device__ __forceinline__ int hamming_at(const uint32_t (&c)[W], const uint32_t *q) {
+    int h = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) h += __popc(c[w] ^ q[w]);
+    return h;
+}
+
 // Histogram of (j, h) over the ns sample entries (codes[t], part[t]) into smem
 // `hist` [m*(L+1)] (the sample is every position, or the index's compacted
 // strided sample); then the smallest structure position r whose cumulative
@@ -95,7 +182,7 @@ __device__ void hist_and_bound(const uint32_t *__restrict__ codes,
                                const uint32_t (&qc)[W], int L, int NR,
                                const int32_t *__restrict__ order, uint32_t *hist, uint32_t need,
                                uint32_t *ws, int *sB, uint32_t *sLt, int64_t per = 0,
-                               int64_t ns_real = 0) {
+                               int64_t ns_real = 0, const uint32_t *sqc = nullptr) {
     for (int e = threadIdx.x; e < NR; e += blockDim.x) hist[e] = 0u;
     if (threadIdx.x == 0) { *sB = NR - 1; *sLt = 0u; }
     __syncthreads();
@@ -107,7 +194,8 @@ __device__ void hist_and_bound(const uint32_t *__restrict__ codes,
             if (t < ns) {
                 uint32_t c[W];
                 load_code<W>(codes, t, c);
-                bin = (int)part[t] * (L + 1) + hamming<W>(c, qc);
+                const int pj = (int)part[t];
+                bin = pj * (L + 1) + (sqc ? hamming_at<W>(c, sqc + pj * W) : hamming<W>(c, qc));
             }
             const unsigned peers = __match_any_sync(NR_FULL, bin);
             if (bin >= 0 && lane == __ffs(peers) - 1) atomicAdd(&hist[bin], (uint32_t)__popc(peers));
@@ -133,7 +221,10 @@ __device__ void hist_and_bound(const uint32_t *__restrict__ codes,
             }
 #pragma unroll
             for (int u = 0; u < PU; ++u)
-                if (pt[u] >= 0) atomicAdd(&hist[pt[u] * (L + 1) + hamming<W>(c[u], qc)], 1u);
+                if (pt[u] >= 0)
+                    atomicAdd(&hist[pt[u] * (L + 1) +
+                                    (sqc ? hamming_at<W>(c[u], sqc + pt[u] * W) : hamming<W>(c[u], qc))],
+                              1u);
         }
     }
     __syncthreads();
@@ -192,9 +283,10 @@ __global__ void __launch_bounds__(1024) k6_pilot(
     const uint32_t *__restrict__ codes, const uint8_t *__restrict__ part_of_pos, int64_t n,
     const uint32_t *__restrict__ qcodes, int L, int m,
     const int32_t *__restrict__ order, const uint16_t *__restrict__ R, uint32_t need,
-    int8_t *__restrict__ delta, uint32_t *__restrict__ cnt, int interleaved, int64_t ns_real) {
+    int8_t *__restrict__ delta, uint32_t *__restrict__ cnt, int interleaved, int64_t ns_real,
+    int QM) {
     pdl_wait();
-    extern __shared__ uint32_t hist[];
+    extern __shared__ uint32_t hist[];   // [NR] (+ [QM x W] query codes, per-sub-dataset A_j)
     __shared__ uint32_t ws[32];
     __shared__ int sB;
     __shared__ uint32_t sLt;
@@ -202,14 +294,19 @@ __global__ void __launch_bounds__(1024) k6_pilot(
     const int NR = m * (L + 1);
     uint32_t qc[W];
 #pragma unroll
-    for (int w = 0; w < W; ++w) qc[w] = qcodes[q * W + w];
+    for (int w = 0; w < W; ++w) qc[w] = qcodes[(int64_t)q * QM * W + w];
+    uint32_t *sqc = nullptr;
+    if (QM > 1) {
+        sqc = hist + NR;
+        for (int e = threadIdx.x; e < QM * W; e += blockDim.x) sqc[e] = qcodes[(int64_t)q * QM * W + e];
+    }
     // the compacted sample is stored interleaved (neighbouring slots from distant
     // sub-datasets), so a warp's bins rarely collide and plain shared atomics beat
     // the match_any aggregation the full-data fallback needs
     if (interleaved)
         hist_and_bound<W, false>(codes, part_of_pos, n, qc, L, NR, order, hist, need, ws, &sB, &sLt,
-                                 n / 32, ns_real);
-    else hist_and_bound<W>(codes, part_of_pos, n, qc, L, NR, order, hist, need, ws, &sB, &sLt);
+                                 n / 32, ns_real, sqc);
+    else hist_and_bound<W>(codes, part_of_pos, n, qc, L, NR, order, hist, need, ws, &sB, &sLt, 0, 0, sqc);
     const int B = sB;
     for (int j = threadIdx.x; j < m; j += blockDim.x) {
         int c = 0;
@@ -232,7 +329,7 @@ void launch_pilot(const nrlsh_index *ix, const uint32_t *qcodes, int Qb, int64_t
     if (stride > 1 && need < 16) need = 16;
     if (need < 1) need = 1;
     const int NR = ix->m * (ix->L + 1);
-    const size_t sm = (size_t)NR * 4;
+    const size_t sm = (size_t)NR * 4 + (ix->QM > 1 ? (size_t)ix->QM * ix->W * 4 : 0);
     const int32_t *order = ix->order_d;
     // the strided sample p = t * stride, compacted at build time (or every position)
     const bool cmp = stride > 1 && ix->samp_codes;
@@ -242,15 +339,15 @@ void launch_pilot(const nrlsh_index *ix, const uint32_t *qcodes, int Qb, int64_t
     switch (ix->W) {
         case 1:
             cudaFuncSetAttribute(k6_pilot<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            launch_pdl(k6_pilot<1>, dim3(Qb), dim3(1024), sm, s, sc, sp, ns, qcodes, ix->L, ix->m, order, ix->R_d, need, delta, cnt, cmp, (ix->n + stride - 1) / stride);
+            launch_pdl(k6_pilot<1>, dim3(Qb), dim3(1024), sm, s, sc, sp, ns, qcodes, ix->L, ix->m, order, ix->R_d, need, delta, cnt, cmp, (ix->n + stride - 1) / stride, ix->QM);
             break;
         case 2:
             cudaFuncSetAttribute(k6_pilot<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            launch_pdl(k6_pilot<2>, dim3(Qb), dim3(1024), sm, s, sc, sp, ns, qcodes, ix->L, ix->m, order, ix->R_d, need, delta, cnt, cmp, (ix->n + stride - 1) / stride);
+            launch_pdl(k6_pilot<2>, dim3(Qb), dim3(1024), sm, s, sc, sp, ns, qcodes, ix->L, ix->m, order, ix->R_d, need, delta, cnt, cmp, (ix->n + stride - 1) / stride, ix->QM);
             break;
         default:
             cudaFuncSetAttribute(k6_pilot<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            launch_pdl(k6_pilot<4>, dim3(Qb), dim3(1024), sm, s, sc, sp, ns, qcodes, ix->L, ix->m, order, ix->R_d, need, delta, cnt, cmp, (ix->n + stride - 1) / stride);
+            launch_pdl(k6_pilot<4>, dim3(Qb), dim3(1024), sm, s, sc, sp, ns, qcodes, ix->L, ix->m, order, ix->R_d, need, delta, cnt, cmp, (ix->n + stride - 1) / stride, ix->QM);
             break;
     }
     note_launch();
@@ -273,7 +370,7 @@ __global__ void __launch_bounds__(kScanThreads) k6_scan(
     const uint32_t *__restrict__ codes, const int4 *__restrict__ chunks,
     const uint32_t *__restrict__ qcodes, const int8_t *__restrict__ delta, int Qb, int m,
     const uint16_t *__restrict__ R, int L, unsigned long long *__restrict__ buf,
-    uint32_t *__restrict__ cnt, int64_t C, unsigned long long *__restrict__ pairs) {
+    uint32_t *__restrict__ cnt, int64_t C, unsigned long long *__restrict__ pairs, int QM) {
     pdl_wait();
     __shared__ uint32_t sq[kQG][W];
     __shared__ int sd[kQG];
@@ -297,7 +394,8 @@ __global__ void __launch_bounds__(kScanThreads) k6_scan(
             if (t < nqg) {
                 dl = delta[(int64_t)(q0 + t) * m + j];
 #pragma unroll
-                for (int w = 0; w < W; ++w) sq[t][w] = qcodes[(int64_t)(q0 + t) * W + w];
+                for (int w = 0; w < W; ++w)   // (per-sub-dataset A_j: the code under A_j)
+                    sq[t][w] = qcodes[((int64_t)(q0 + t) * QM + (QM > 1 ? j : 0)) * W + w];
             }
             sd[t] = dl;
             scnt[t] = 0;
@@ -398,243 +496,15 @@ __global__ void __launch_bounds__(kScanThreads) k6_scan(
     }
 }
 
-// ------------------------------------------------------------------ K6 on IMMA
-// The same scan with the Hamming distances from the legacy warp-level int8 tensor
-// instruction (mma.sync m16n8k32 s8, native IMMA on sm_100a; measured 1,550 MAC/clk/SM
-// = 3x the pair rate of two POPCs): a code bit b is s_b = +1 / -1 (bit 1 / 0), so
-// sum_b s_b(q) s_b(x) = 32W - 2h exactly (the zero bits past L agree), and one
-// 32-bit code word is one K = 32 step.
-// The +-1 operand fragments are built in registers straight from the packed code
-// words (a nibble -> 4 bytes, expand4), so nothing is expanded in memory.
-// CTA = (chunk of <= 2048 positions of one sub-dataset, group of 64 queries), as the
-// popcount scan; the group's active queries (delta_j >= 0) form tiles of 16 rows;
-// a warp unit = (query tile, span of 256 positions = 32 n8 tiles): a thread holds the
-// pass bits of its two rows (g, g+8) for its two columns of every n8 tile (64 bits
-// per row), then the 4 lanes of a row reserve the row's stage slots with one shared
-// atomic (and the global overflow with one more) and write their entries, h taken
-// again with POPC for the passing pairs only.
-__device__ __forceinline__ uint32_t expand4_pm(uint32_t nib) {
-    const uint32_t y = (nib * 0x00204081u) & 0x01010101u;
-    return 0xFFFFFFFFu ^ (y * 0xFEu);   // bit i -> byte i: +1 (0x01) or -1 (0xFF)
-}
-
-constexpr int kQGI = 128;    // queries per CTA (IMMA scan): more active rows per tile
-constexpr int kSBI = 48;     // staged appends per (CTA, query)
-constexpr int kTPU = 4;      // query tiles (of 16 rows) per warp unit: one B expansion feeds 4 MMAs
-
-template <int W>
-__global__ void __launch_bounds__(kScanThreads) k6_scan_imma(
-    const uint32_t *__restrict__ codes, const int4 *__restrict__ chunks,
-    const uint32_t *__restrict__ qcodes, const int8_t *__restrict__ delta, int Qb, int m,
-    int L, unsigned long long *__restrict__ buf, uint32_t *__restrict__ cnt, int64_t C,
-    unsigned long long *__restrict__ pairs) {
-    __shared__ uint32_t sq[kQGI][W];
-    __shared__ int sthr[kQGI];
-    __shared__ uint32_t sbuf[kQGI][kSBI];
-    __shared__ uint32_t scnt[kQGI];
-    __shared__ uint32_t sbase[kQGI];
-    __shared__ int sact[kQGI];
-    __shared__ int s_nact;
-    __shared__ uint32_t scode[kScanThreads / 32][128 * W];   // a warp unit's span of codes
-    const int ngroups = (Qb + kQGI - 1) / kQGI;
-    const int4 ch = chunks[blockIdx.x / ngroups];
-    const int j = ch.x, p0 = ch.y, p1 = ch.z;
-    const int q0 = (blockIdx.x % ngroups) * kQGI;
-    const int nqg = min(kQGI, Qb - q0);
-    if (threadIdx.x < 32) {       // warp 0 compacts the group's active queries
-        int base = 0;
-        for (int t0 = 0; t0 < kQGI; t0 += 32) {
-            const int t = t0 + threadIdx.x;
-            int dl = -1;
-            if (t < nqg) {
-                dl = delta[(int64_t)(q0 + t) * m + j];
-#pragma unroll
-                for (int w = 0; w < W; ++w) sq[t][w] = qcodes[(int64_t)(q0 + t) * W + w];
-            }
-            scnt[t] = 0;
-            const unsigned bal = __ballot_sync(NR_FULL, dl >= 0);
-            if (dl >= 0) {
-                const int slot = base + __popc(bal & lanemask_lt());
-                sact[slot] = t;
-                // bits >= L are 0 in both codes, so they add +1 each: dot = 32 W - 2h,
-                // and h <= delta  <=>  dot >= 32 W - 2 delta
-                sthr[slot] = 32 * W - 2 * dl;
-            }
-            base += __popc(bal);
-        }
-        if (threadIdx.x == 0) s_nact = base;
-    }
-    __syncthreads();
-    const int nact = s_nact;
-    if (nact == 0) return;
-    if (threadIdx.x == 0 && pairs) atomicAdd(pairs, (unsigned long long)nact * (p1 - p0));
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int g = lane >> 2, t = lane & 3;
-    const int nqt = (nact + 15) >> 4;
-    const int ntg = (nqt + kTPU - 1) / kTPU;           // tile groups
-    constexpr int kSpan = 128;                         // positions per warp unit (16 n8 tiles)
-    const int nspan = (p1 - p0 + kSpan - 1) / kSpan;
-    for (int u = warp; u < ntg * nspan; u += kScanThreads / 32) {
-        const int tg = u % ntg, sp = u / ntg;
-        const int qt0 = tg * kTPU, nt = min(kTPU, nqt - qt0);
-        uint32_t a[kTPU][W][4];
-        int th[kTPU][2];
-#pragma unroll
-        for (int x = 0; x < kTPU; ++x) {
-            const int r0 = (qt0 + x) * 16 + g, r1 = r0 + 8;
-            const bool v0 = x < nt && r0 < nact, v1 = x < nt && r1 < nact;
-            const int qq0 = v0 ? sact[r0] : 0, qq1 = v1 ? sact[r1] : 0;
-            th[x][0] = v0 ? sthr[r0] : INT_MAX;
-            th[x][1] = v1 ? sthr[r1] : INT_MAX;
-#pragma unroll
-            for (int w = 0; w < W; ++w) {
-                const uint32_t c0 = v0 ? sq[qq0][w] : 0u, c1 = v1 ? sq[qq1][w] : 0u;
-                a[x][w][0] = expand4_pm((c0 >> (4 * t)) & 0xFu);
-                a[x][w][1] = expand4_pm((c1 >> (4 * t)) & 0xFu);
-                a[x][w][2] = expand4_pm((c0 >> (16 + 4 * t)) & 0xFu);
-                a[x][w][3] = expand4_pm((c1 >> (16 + 4 * t)) & 0xFu);
-            }
-        }
-        const int sb = p0 + sp * kSpan;                // first position of the span
-        const int se = min(p1, sb + kSpan);
-        uint32_t *wc = scode[warp];
-        __syncwarp();
-        for (int e = lane; e < kSpan; e += 32) {       // the span's codes, coalesced, to smem
-            uint32_t cw[W];
-            if (sb + e < se) load_code<W>(codes, sb + e, cw);
-            else
-#pragma unroll
-                for (int w = 0; w < W; ++w) cw[w] = 0u;
-#pragma unroll
-            for (int w = 0; w < W; ++w) wc[e * W + w] = cw[w];
-        }
-        __syncwarp();
-        uint32_t mk[kTPU][2];                          // bit 2k + c: n8 tile k, column 2t + c
-#pragma unroll
-        for (int x = 0; x < kTPU; ++x) mk[x][0] = mk[x][1] = 0u;
-#pragma unroll 2
-        for (int k = 0; k < kSpan / 8; ++k) {
-            uint32_t iw[W];                             // B column (item k * 8 + g)
-#pragma unroll
-            for (int w = 0; w < W; ++w) iw[w] = wc[(k * 8 + g) * W + w];
-            uint32_t b[W][2];
-#pragma unroll
-            for (int w = 0; w < W; ++w) {
-                b[w][0] = expand4_pm((iw[w] >> (4 * t)) & 0xFu);
-                b[w][1] = expand4_pm((iw[w] >> (16 + 4 * t)) & 0xFu);
-            }
-            const int pc = sb + k * 8 + 2 * t;          // C columns of this lane: pc, pc + 1
-            const uint32_t ok = (uint32_t)(pc < se) | ((uint32_t)(pc + 1 < se) << 1);
-            // (all kTPU tiles unconditionally: independent MMAs in flight; the rows of
-            // missing tiles have threshold INT_MAX and never pass)
-#pragma unroll
-            for (int x = 0; x < kTPU; ++x) {
-                int c[4] = {0, 0, 0, 0};
-#pragma unroll
-                for (int w = 0; w < W; ++w)
-                    asm volatile(
-                        "mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
-                        : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
-                        : "r"(a[x][w][0]), "r"(a[x][w][1]), "r"(a[x][w][2]), "r"(a[x][w][3]),
-                          "r"(b[w][0]), "r"(b[w][1]));
-                const uint32_t f0 = ((uint32_t)(c[0] >= th[x][0]) | ((uint32_t)(c[1] >= th[x][0]) << 1)) & ok;
-                const uint32_t f1 = ((uint32_t)(c[2] >= th[x][1]) | ((uint32_t)(c[3] >= th[x][1]) << 1)) & ok;
-                mk[x][0] |= f0 << (2 * k);
-                mk[x][1] |= f1 << (2 * k);
-            }
-        }
-        // appends: per row, the 4 lanes of the group reserve together
-#pragma unroll
-        for (int x = 0; x < kTPU; ++x) {
-            if (x >= nt) break;
-#pragma unroll
-            for (int rr = 0; rr < 2; ++rr) {
-                const int r = (qt0 + x) * 16 + g + 8 * rr;
-                const uint32_t mm = mk[x][rr];
-                const int np = __popc(mm);
-                int inc = np;
-                {
-                    const int y1 = __shfl_up_sync(NR_FULL, inc, 1);
-                    if (t >= 1) inc += y1;
-                    const int y2 = __shfl_up_sync(NR_FULL, inc, 2);
-                    if (t >= 2) inc += y2;
-                }
-                const int tot = __shfl_sync(NR_FULL, inc, (lane & ~3) + 3);
-                const int qq = r < nact ? sact[r] : 0;
-                uint32_t base = 0, gbase = 0;
-                if (t == 3 && tot > 0) {
-                    base = atomicAdd(&scnt[qq], (uint32_t)tot);
-                    const uint32_t lo = max(base, (uint32_t)kSBI), hi = base + (uint32_t)tot;
-                    if (hi > lo) gbase = atomicAdd(&cnt[q0 + qq], hi - lo);
-                }
-                base = __shfl_sync(NR_FULL, base, (lane & ~3) + 3);
-                gbase = __shfl_sync(NR_FULL, gbase, (lane & ~3) + 3);
-                if (!np) continue;
-                const uint32_t glo = max(base, (uint32_t)kSBI);
-                uint32_t slot = base + (uint32_t)(inc - np);
-                uint32_t qc[W];
-#pragma unroll
-                for (int w = 0; w < W; ++w) qc[w] = sq[qq][w];
-                uint32_t mb = mm;
-                while (mb) {
-                    const int bb = __ffs(mb) - 1;
-                    mb &= mb - 1;
-                    const int e = (bb >> 1) * 8 + 2 * t + (bb & 1);
-                    const int pos = sb + e;
-                    uint32_t iw[W];
-#pragma unroll
-                    for (int w = 0; w < W; ++w) iw[w] = wc[e * W + w];
-                    const int h = hamming<W>(iw, qc);
-                    const uint32_t off = (uint32_t)(pos - p0);
-                    if (slot < kSBI) {
-                        sbuf[qq][slot] = ((uint32_t)h << 16) | off;
-                    } else {
-                        const uint32_t gg = gbase + (slot - glo);
-                        if (gg < C)
-                            buf[(int64_t)(q0 + qq) * C + gg] = ((unsigned long long)(j * (L + 1) + h) << 32) | (uint32_t)pos;
-                    }
-                    ++slot;
-                }
-            }
-        }
-    }
-    __syncthreads();
-    for (int tq = threadIdx.x; tq < nqg; tq += blockDim.x) {
-        const uint32_t nst = min(scnt[tq], (uint32_t)kSBI);
-        sbase[tq] = nst ? atomicAdd(&cnt[q0 + tq], nst) : 0u;
-    }
-    __syncthreads();
-    const unsigned long long jb = (unsigned long long)(j * (L + 1));
-    for (int tq = warp; tq < nqg; tq += kScanThreads / 32) {
-        const uint32_t nst = min(scnt[tq], (uint32_t)kSBI);
-        const int64_t q = q0 + tq;
-        for (uint32_t e = lane; e < nst; e += 32) {
-            const uint32_t gg = sbase[tq] + e;
-            const uint32_t v = sbuf[tq][e];
-            if (gg < C) buf[q * C + gg] = ((jb + (v >> 16)) << 32) | (uint32_t)(p0 + (v & 0xffffu));
-        }
-    }
-}
-
 void launch_scan(const nrlsh_index *ix, const uint32_t *qcodes, const int8_t *delta, int Qb,
                  unsigned long long *buf, uint32_t *cnt, int64_t C, unsigned long long *pairs,
                  cudaStream_t s) {
     const int64_t ngroups = (Qb + kQG - 1) / kQG;
     const unsigned grid = (unsigned)(ix->nchunks * ngroups);
-    if (getenv("NRLSH_SCAN_IMMA") && atoi(getenv("NRLSH_SCAN_IMMA")) != 0) {
-        const unsigned gridi = (unsigned)(ix->nchunks * ((Qb + kQGI - 1) / kQGI));
-        switch (ix->W) {
-            case 1: k6_scan_imma<1><<<gridi, kScanThreads, 0, s>>>(ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->L, buf, cnt, C, pairs); break;
-            case 2: k6_scan_imma<2><<<gridi, kScanThreads, 0, s>>>(ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->L, buf, cnt, C, pairs); break;
-            default: k6_scan_imma<4><<<gridi, kScanThreads, 0, s>>>(ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->L, buf, cnt, C, pairs); break;
-        }
-        note_launch();
-        return;
-    }
     switch (ix->W) {
-        case 1: launch_pdl(k6_scan<1>, dim3(grid), dim3(kScanThreads), 0, s, ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs); break;
-        case 2: launch_pdl(k6_scan<2>, dim3(grid), dim3(kScanThreads), 0, s, ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs); break;
-        default: launch_pdl(k6_scan<4>, dim3(grid), dim3(kScanThreads), 0, s, ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs); break;
+        case 1: launch_pdl(k6_scan<1>, dim3(grid), dim3(kScanThreads), 0, s, ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs, ix->QM); break;
+        case 2: launch_pdl(k6_scan<2>, dim3(grid), dim3(kScanThreads), 0, s, ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs, ix->QM); break;
+        default: launch_pdl(k6_scan<4>, dim3(grid), dim3(kScanThreads), 0, s, ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs, ix->QM); break;
     }
     note_launch();
 }
@@ -648,9 +518,9 @@ __global__ void __launch_bounds__(1024) k6_fallback(
     const uint32_t *__restrict__ qcodes, int L, int m, const int32_t *__restrict__ order,
     const uint16_t *__restrict__ R, int64_t Tq, unsigned long long *__restrict__ buf,
     uint32_t *__restrict__ cnt, const uint32_t *__restrict__ cntv, int64_t C,
-    int *__restrict__ flags) {
+    int *__restrict__ flags, int QM) {
     pdl_wait();
-    extern __shared__ uint32_t hist[];
+    extern __shared__ uint32_t hist[];   // [NR] (+ [QM x W] query codes)
     __shared__ uint32_t ws[32];
     __shared__ int sB;
     __shared__ uint32_t sLt, s_out, s_eq;
@@ -661,8 +531,14 @@ __global__ void __launch_bounds__(1024) k6_fallback(
     const int NR = m * (L + 1);
     uint32_t qc[W];
 #pragma unroll
-    for (int w = 0; w < W; ++w) qc[w] = qcodes[q * W + w];
-    hist_and_bound<W>(codes, part_of_pos, n, qc, L, NR, order, hist, (uint32_t)Tq, ws, &sB, &sLt);
+    for (int w = 0; w < W; ++w) qc[w] = qcodes[(int64_t)q * QM * W + w];
+    uint32_t *sqc = nullptr;
+    if (QM > 1) {
+        sqc = hist + NR;
+        for (int e = threadIdx.x; e < QM * W; e += blockDim.x) sqc[e] = qcodes[(int64_t)q * QM * W + e];
+    }
+    hist_and_bound<W>(codes, part_of_pos, n, qc, L, NR, order, hist, (uint32_t)Tq, ws, &sB, &sLt, 0, 0,
+                      sqc);
     const int B = sB;
     const uint32_t need_eq = (uint32_t)Tq - sLt;
     // R[j][h] lookup straight from the structure (global, cached)
@@ -674,7 +550,8 @@ __global__ void __launch_bounds__(1024) k6_fallback(
         if (p < n) {
             uint32_t c[W];
             load_code<W>(codes, p, c);
-            f = part_of_pos[p] * (L + 1) + hamming<W>(c, qc);
+            const int pj = part_of_pos[p];
+            f = pj * (L + 1) + (sqc ? hamming_at<W>(c, sqc + pj * W) : hamming<W>(c, qc));
             r = R[f];
         }
         const uint32_t lt = r < B, eq = r == B;
@@ -721,7 +598,7 @@ __global__ void __launch_bounds__(1024) fb_hist(const uint32_t *__restrict__ cod
                                                 const uint32_t *__restrict__ qcodes, int L, int NR,
                                                 const uint16_t *__restrict__ R,
                                                 const int32_t *__restrict__ fl, const uint32_t *__restrict__ nf,
-                                                uint32_t *__restrict__ ghist) {
+                                                uint32_t *__restrict__ ghist, int QM) {
     pdl_wait();
     extern __shared__ uint32_t hist[];
     const int nfl = (int)min(*nf, (uint32_t)kFbMax);
@@ -731,7 +608,8 @@ __global__ void __launch_bounds__(1024) fb_hist(const uint32_t *__restrict__ cod
         const int q = fl[fi];
         uint32_t qc[W];
 #pragma unroll
-        for (int k = 0; k < W; ++k) qc[k] = qcodes[q * W + k];
+        for (int k = 0; k < W; ++k) qc[k] = qcodes[(int64_t)q * QM * W + k];
+        const uint32_t *qall = qcodes + (int64_t)q * QM * W;
         for (int e = threadIdx.x; e < NR; e += blockDim.x) hist[e] = 0u;
         __syncthreads();
         const int64_t p0 = n * sl / kFbSlices, p1 = n * (sl + 1) / kFbSlices;
@@ -741,7 +619,8 @@ __global__ void __launch_bounds__(1024) fb_hist(const uint32_t *__restrict__ cod
             if (p < p1) {
                 uint32_t c[W];
                 load_code<W>(codes, p, c);
-                r = R[part[p] * (L + 1) + hamming<W>(c, qc)];
+                const int pj = part[p];
+                r = R[pj * (L + 1) + (QM > 1 ? hamming_at<W>(c, qall + pj * W) : hamming<W>(c, qc))];
             }
             const unsigned peers = __match_any_sync(NR_FULL, r);
             if (r >= 0 && lane == __ffs(peers) - 1) atomicAdd(&hist[r], (uint32_t)__popc(peers));
@@ -798,7 +677,7 @@ __global__ void __launch_bounds__(1024) fb_take(const uint32_t *__restrict__ cod
                                                 const int32_t *__restrict__ fl, const uint32_t *__restrict__ nf,
                                                 const uint32_t *__restrict__ Bq,
                                                 unsigned long long *__restrict__ buf, uint32_t *__restrict__ cnt,
-                                                uint32_t *__restrict__ cntv, int64_t C) {
+                                                uint32_t *__restrict__ cntv, int64_t C, int QM) {
     pdl_wait();
     const int nfl = (int)min(*nf, (uint32_t)kFbMax);
     const int lane = threadIdx.x & 31;
@@ -808,7 +687,8 @@ __global__ void __launch_bounds__(1024) fb_take(const uint32_t *__restrict__ cod
         const uint32_t B = Bq[fi];
         uint32_t qc[W];
 #pragma unroll
-        for (int k = 0; k < W; ++k) qc[k] = qcodes[q * W + k];
+        for (int k = 0; k < W; ++k) qc[k] = qcodes[(int64_t)q * QM * W + k];
+        const uint32_t *qall = qcodes + (int64_t)q * QM * W;
         const int64_t p0 = n * sl / kFbSlices, p1 = n * (sl + 1) / kFbSlices;
         uint32_t mine = 0;
         for (int64_t b0 = p0; b0 < p1; b0 += blockDim.x) {
@@ -818,7 +698,8 @@ __global__ void __launch_bounds__(1024) fb_take(const uint32_t *__restrict__ cod
             if (p < p1) {
                 uint32_t c[W];
                 load_code<W>(codes, p, c);
-                f = part[p] * (L + 1) + hamming<W>(c, qc);
+                const int pj = part[p];
+                f = pj * (L + 1) + (QM > 1 ? hamming_at<W>(c, qall + pj * W) : hamming<W>(c, qc));
                 take = R[f] <= B;
             }
             const unsigned bal = __ballot_sync(NR_FULL, take);
@@ -856,33 +737,34 @@ void launch_fallback(const nrlsh_index *ix, const uint32_t *qcodes, int Qb, int6
         cudaMemsetAsync(nf, 0, 4, s);
         launch_pdl(fb_list, dim3((Qb + 255) / 256), dim3(256), 0, s, cnt, cv_sep, Qb, Tq, C, fl, nf, flags);
         const size_t sm = (size_t)NR * 4;
+        const int QM = ix->QM;
 #define NR_FB(W_)                                                                                   \
         cudaFuncSetAttribute(fb_hist<W_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);    \
         launch_pdl(fb_hist<W_>, dim3(sms), dim3(1024), sm, s, ix->codes, ix->part_of_pos, ix->n, qcodes, ix->L, NR,     \
-                                          ix->R_d, fl, nf, ghist);                                  \
+                                          ix->R_d, fl, nf, ghist, QM);                              \
         launch_pdl(fb_bound, dim3(sms), dim3(1024), 0, s, fl, nf, NR, Tq, ghist, Bq, cnt, cv_sep);                      \
         launch_pdl(fb_take<W_>, dim3(sms), dim3(1024), 0, s, ix->codes, ix->part_of_pos, ix->n, qcodes, ix->L, ix->R_d, \
-                                         fl, nf, Bq, buf, cnt, cv_sep, C)
+                                         fl, nf, Bq, buf, cnt, cv_sep, C, QM)
         if (ix->W == 1) { NR_FB(1); } else if (ix->W == 2) { NR_FB(2); } else { NR_FB(4); }
 #undef NR_FB
         note_launch(4);
         // the serial kernel below still counts every failed query (flags[2]) and
         // handles any beyond kFbMax; the ones done here now pass its test
     }
-    const size_t sm = (size_t)NR * 4;
+    const size_t sm = (size_t)NR * 4 + (ix->QM > 1 ? (size_t)ix->QM * ix->W * 4 : 0);
     const int32_t *order = ix->order_d;
     switch (ix->W) {
         case 1:
             cudaFuncSetAttribute(k6_fallback<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            launch_pdl(k6_fallback<1>, dim3(Qb), dim3(1024), sm, s, ix->codes, ix->part_of_pos, ix->n, qcodes, ix->L, ix->m, order, ix->R_d, Tq, buf, cnt, cntv, C, par ? nullptr : flags);
+            launch_pdl(k6_fallback<1>, dim3(Qb), dim3(1024), sm, s, ix->codes, ix->part_of_pos, ix->n, qcodes, ix->L, ix->m, order, ix->R_d, Tq, buf, cnt, cntv, C, par ? nullptr : flags, ix->QM);
             break;
         case 2:
             cudaFuncSetAttribute(k6_fallback<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            launch_pdl(k6_fallback<2>, dim3(Qb), dim3(1024), sm, s, ix->codes, ix->part_of_pos, ix->n, qcodes, ix->L, ix->m, order, ix->R_d, Tq, buf, cnt, cntv, C, par ? nullptr : flags);
+            launch_pdl(k6_fallback<2>, dim3(Qb), dim3(1024), sm, s, ix->codes, ix->part_of_pos, ix->n, qcodes, ix->L, ix->m, order, ix->R_d, Tq, buf, cnt, cntv, C, par ? nullptr : flags, ix->QM);
             break;
         default:
             cudaFuncSetAttribute(k6_fallback<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            launch_pdl(k6_fallback<4>, dim3(Qb), dim3(1024), sm, s, ix->codes, ix->part_of_pos, ix->n, qcodes, ix->L, ix->m, order, ix->R_d, Tq, buf, cnt, cntv, C, par ? nullptr : flags);
+            launch_pdl(k6_fallback<4>, dim3(Qb), dim3(1024), sm, s, ix->codes, ix->part_of_pos, ix->n, qcodes, ix->L, ix->m, order, ix->R_d, Tq, buf, cnt, cntv, C, par ? nullptr : flags, ix->QM);
             break;
     }
     note_launch();

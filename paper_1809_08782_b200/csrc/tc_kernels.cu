@@ -152,7 +152,8 @@ struct GtArgs {
     const uint8_t *part;    // [npad]
     const uint16_t *R;
     int L, W;
-    const uint32_t *qcodes;
+    const uint32_t *qcodes; // [Qb x qm x W]
+    int qm;                 // 1, or m (per-sub-dataset projections: q's code under A_j)
     const uint32_t *sel_B, *sel_pk;
     const int32_t *perm;    // row -> item id of the survivors (nullptr: identity)
     const int32_t *qperm;   // query row -> original query index (nullptr: identity)
@@ -254,7 +255,7 @@ struct GtEpiRow {
             if (args.member) {
 #pragma unroll
                 for (int w = 0; w < 4; ++w)
-                    if (w < args.W) qcw[w] = args.qcodes[(int64_t)q * args.W + w];
+                    if (w < args.W) qcw[w] = args.qcodes[(int64_t)q * args.qm * args.W + w];
                 Bq = args.sel_B[q];
                 pkq = args.sel_pk[q];
             }
@@ -327,9 +328,16 @@ struct GtEpiRow {
                 if (a->member) {   // candidate of q? (the select's rule; rows are positions)
                     const uint32_t *cw = scode + col * a->W;
                     int hq = 0;
+                    if (a->qm > 1) {   // the query's code under the item's sub-index A_j
+                        const uint32_t *qj = a->qcodes + ((int64_t)q * a->qm + spart[col]) * a->W;
 #pragma unroll
-                    for (int w = 0; w < 4; ++w)
-                        if (w < a->W) hq += __popc(cw[w] ^ qcw[w]);
+                        for (int w = 0; w < 4; ++w)
+                            if (w < a->W) hq += __popc(cw[w] ^ __ldg(qj + w));
+                    } else {
+#pragma unroll
+                        for (int w = 0; w < 4; ++w)
+                            if (w < a->W) hq += __popc(cw[w] ^ qcw[w]);
+                    }
                     const uint32_t r = __ldg(a->R + spart[col] * (a->L + 1) + hq);
                     if (!(r < Bq || (r == Bq && (uint32_t)i <= pkq))) continue;
                 }
@@ -1041,6 +1049,7 @@ int launch_gt_filter_tc(const void *Xb, int64_t n, int d, int dp, const void *Qb
     a.L = mb ? mb->L : 0;
     a.W = mb ? mb->W : 1;
     a.qcodes = mb ? mb->qcodes : nullptr;
+    a.qm = mb ? mb->qm : 1;
     a.sel_B = mb ? mb->sel_B : nullptr;
     a.sel_pk = mb ? mb->sel_pk : nullptr;
     if (mb && (mb->W < 1 || mb->W > 4)) return -1;

@@ -441,7 +441,8 @@ def _headline_rerank_check(P, cfg, X, Q, idx, ocodes, part, R, A, L):
     gq = idx.query_codes(Qd).cpu().numpy().view(np.uint32)
     qc = oracle.query_codes(Qh, A)
     rng = np.random.default_rng(2)
-    sample = sorted(set([0, 255, 256, cfg.query_batch - 1, cfg.query_batch, nqh - 1]
+    sample = sorted(set([q for q in (0, 255, 256, 1023, 1024, cfg.query_batch - 1,
+                                     cfg.query_batch, nqh - 1) if q < nqh]
                         + rng.choice(nqh, 14, replace=False).tolist()))
     same = band_mask(gq[sample], qc[sample], 0.8)
     for s_, qi in zip(same, sample):
@@ -542,16 +543,15 @@ def test_full_size_sampled(name, L, m):
         assert_topk_match(gt_ids[qi], gt_sc[qi], a, s, X, Q[qi])
 
 
-@pytest.mark.parametrize("scan", ["tensor", "popcount", "imma"])
+@pytest.mark.parametrize("scan", ["tensor", "popcount"])
 @pytest.mark.parametrize("case", [("c4", 300_000, 32, 64, 128), ("scale", 70_000, 16, 128, 256),
                                   ("tiny", None, None, 32, 8), ("c4", 300_000, 32, 32, 4),
                                   ("c3", 40_000, 64, 64, 1)], ids=_ids)
 def test_candidates_parity_both_scans(built, case, scan, monkeypatch):
-    """The Hamming scans — the popcount one (the default), the tcgen05 int8 one
-    (scan_tc.cu, NRLSH_SCAN_TC=1) and the warp-level IMMA one — give the oracle's candidate sets, ranks and
+    """Both Hamming scans — the popcount one (the default) and the tcgen05 int8 one
+    (scan_tc.cu, NRLSH_SCAN_TC=1) — give the oracle's candidate sets, ranks and
     (R, id) order (identical codes injected), across budgets from 1 to n."""
     monkeypatch.setenv("NRLSH_SCAN_TC", "1" if scan == "tensor" else "0")
-    monkeypatch.setenv("NRLSH_SCAN_IMMA", "1" if scan == "imma" else "0")
     cfg, X, Q, Xd, idx, orc = built(*case)
     if scan == "tensor":   # its +-1 code rows are made at build time (opt-in)
         idx = _P().Index(Xd, case[3], case[4], seed=cfg.seed)
@@ -795,3 +795,123 @@ def test_odd_shapes_parity(shape):
         a, s = oracle.exact_topk(X, Q[qi], k)
         assert_topk_match(gi[qi], gs[qi], a, s, X, Q[qi])
     idx.close()
+
+
+# ------------------------------------- NEXT-4: per-sub-dataset projections A_j
+PP_CASES = [("tiny", None, 40, 32, 8), ("c3", 40_000, 40, 64, 64), ("c4", 300_000, 32, 64, 128),
+            ("scale", 70_000, 16, 128, 256), ("c2", None, 40, 50, 7)]
+
+
+@pytest.fixture(scope="session")
+def built_pp():
+    cache = {}
+
+    def get(name, n, nq, L, m):
+        key = (name, n, nq, L, m)
+        if key not in cache:
+            P = _P()
+            cfg, X, Q = dataset(workloads.CONFIGS[name], n, nq)
+            Xd = torch.from_numpy(X).cuda()
+            idx = P.Index(Xd, L, m, seed=cfg.seed + 5, proj="per_partition")
+            orc = oracle.OracleIndex(X, idx.hash_bits, m, seed=cfg.seed + 5, proj="per_partition")
+            cache[key] = (cfg, X, Q[:nq], Xd, idx, orc)
+        return cache[key]
+    return get
+
+
+@pytest.mark.parametrize("case", PP_CASES, ids=_ids)
+def test_pp_build_and_codes_parity(built_pp, case):
+    """Alg. 1 l.7 with an independent projection per sub-index (PAPER:155, PAPER:6;
+    A_j from seed XOR j): every A_j, the partition, the rank table and
+    every item code (band-exempt) and query code under every A_j match the oracle."""
+    cfg, X, Q, Xd, idx, orc = built_pp(*case)
+    assert idx.proj == "per_partition" and idx.qm == case[4]
+    A = idx.projection()
+    assert A.shape == orc.A_all.shape and np.array_equal(A, orc.A_all)
+    _, perm, offsets, V = idx.partition()
+    assert np.array_equal(perm, orc.perm) and np.array_equal(V, orc.V)
+    assert np.array_equal(idx.rank_table(), orc.R)
+    ocodes, z = orc.codes(want_z=True)
+    assert_codes_match(idx.codes()[np.argsort(perm, kind="stable")], ocodes, z, idx.hash_bits)
+    g = idx.query_codes(torch.from_numpy(Q).cuda()).cpu().numpy().view(np.uint32)
+    oq, oz = orc.query_codes(Q, want_z=True)
+    assert g.shape == oq.shape
+    m, W = oq.shape[1], oq.shape[2]
+    assert_codes_match(g.reshape(-1, W), oq.reshape(-1, W), oz.reshape(-1, oz.shape[2]), idx.hash_bits)
+
+
+@pytest.mark.parametrize("case", PP_CASES, ids=_ids)
+def test_pp_candidates_and_query_parity(built_pp, case):
+    """Identical codes injected: candidate sets, structure positions and (R, id)
+    order, and the end-to-end answers equal the oracle's at budgets from 1 to n."""
+    cfg, X, Q, Xd, idx, orc = built_pp(*case)
+    n = X.shape[0]
+    ocodes = orc.codes()
+    idx.set_codes(ocodes[orc.perm])
+    qc = orc.query_codes(Q)
+    nq = min(len(Q), 12)
+    qcd = torch.from_numpy(np.ascontiguousarray(qc[:nq]).view(np.int32)).cuda()
+    for T in _budgets(cfg, n):
+        gid, grk = idx.candidates(T, qcodes=qcd)
+        gid, grk = gid.cpu().numpy(), grk.cpu().numpy().view(np.uint16)
+        for qi in range(nq):
+            oid, ork = orc.candidates(ocodes, qc[qi], T)
+            o = np.lexsort((gid[qi], grk[qi]))
+            assert np.array_equal(gid[qi][o], oid), (T, qi)
+            assert np.array_equal(grk[qi][o], ork), (T, qi)
+    Qd = torch.from_numpy(Q[:nq]).cuda()
+    gq = idx.query_codes(Qd).cpu().numpy().view(np.uint32)
+    same = band_mask(gq, qc[:nq], 0.75)
+    for T in sorted({1, 37, max(1, n // 100), n // 3, n}):
+        ids, sc = idx.query(Qd, cfg.k, T)
+        ids, sc = ids.cpu().numpy(), sc.cpu().numpy()
+        for qi in range(nq):
+            if same[qi]:
+                a, s = orc.query(ocodes, Q[qi], T, cfg.k)
+                assert_topk_match(ids[qi], sc[qi], a, s, X, Q[qi])
+
+
+def test_pp_one_sub_dataset_equals_shared():
+    """m = 1: A_0 is the shared projection, so codes, query codes and answers are
+    identical to the shared-A index (plain SIMPLE-LSH either way)."""
+    P = _P()
+    cfg, X, Q = dataset(workloads.CONFIGS["c2"], None, 40)
+    Xd, Qd = torch.from_numpy(X).cuda(), torch.from_numpy(Q[:40]).cuda()
+    a = P.Index(Xd, 64, 1, seed=2)
+    b = P.Index(Xd, 64, 1, seed=2, proj="per_partition")
+    assert np.array_equal(a.codes(), b.codes())
+    assert torch.equal(a.query_codes(Qd), b.query_codes(Qd).reshape(40, -1))
+    for T in (50, 1777):
+        ia, sa = a.query(Qd, 10, T)
+        ib, sb = b.query(Qd, 10, T)
+        assert torch.equal(ia, ib) and torch.equal(sa, sb)
+
+
+@pytest.mark.parametrize("case", [("c4", 300_000, 32, 64, 128), ("c3", 40_000, 40, 64, 64)], ids=_ids)
+def test_pp_rerank_tensor_and_fallback(built_pp, case, monkeypatch):
+    """The tensor-core re-rank (member test with the query's code under the item's
+    A_j) equals the gather path bit for bit over several query pairs; the forced
+    exact fallback gives the oracle's candidates."""
+    cfg, X, Q, Xd, idx, orc = built_pp(*case)
+    P = _P()
+    n = X.shape[0]
+    Qd = torch.from_numpy(np.ascontiguousarray(np.concatenate([Q] * 20)[:600])).cuda()
+    for T in (n // 100, n // 3):
+        monkeypatch.setenv("NRLSH_RERANK_TC", "1")
+        ti, ts = idx.query(Qd, cfg.k, T)
+        assert P.last_rerank_path()["path"] == "tensor"
+        monkeypatch.setenv("NRLSH_RERANK_TC", "0")
+        gi, gs = idx.query(Qd, cfg.k, T)
+        assert torch.equal(gi, ti) and torch.equal(gs.view(torch.int32), ts.view(torch.int32)), T
+    monkeypatch.delenv("NRLSH_RERANK_TC")
+    ocodes = orc.codes()
+    idx.set_codes(ocodes[orc.perm])
+    qc = orc.query_codes(Q[:6])
+    monkeypatch.setenv("NRLSH_TEST_FORCE_FALLBACK", "1")
+    gid, grk = idx.candidates(2000, qcodes=torch.from_numpy(np.ascontiguousarray(qc).view(np.int32)).cuda())
+    assert P.last_query_stats()["fallback_queries"] == 6
+    for qi in range(6):
+        oid, ork = orc.candidates(ocodes, qc[qi], 2000)
+        g, r = gid[qi].cpu().numpy(), grk[qi].cpu().numpy().view(np.uint16)
+        o = np.lexsort((g, r))
+        assert np.array_equal(g[o], oid) and np.array_equal(r[o], ork)
