@@ -337,7 +337,7 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
         NR_ALLOC(ix->codes_pm, (size_t)n * scan_kp(L));
     NR_ALLOC(ix->offsets_d, (size_t)(m + 1) * 8);
     NR_ALLOC(ix->V_d, (size_t)m * 8);
-    NR_ALLOC(ix->codes, (size_t)n * W * 4);
+    NR_ALLOC(ix->codes, (size_t)n * W * 4 + 64);   // (+64: the scan's aligned bulk copies)
 
     // K1: norms + finite check
     DBuf bad;
@@ -421,16 +421,14 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
             tiles.push_back(make_int4(j, (int)p, (int)std::min<int64_t>(p + 256, ix->offsets[j + 1]), 0));
     ix->ntiles = (int32_t)tiles.size();
     // per-sub-dataset projections: the code kernel's tiles of <= 128 positions of one j
+    // (also the tensor-core scan's item tiles)
     std::vector<int4> ctiles;
-    if (QM > 1)
-        for (int j = 0; j < m; ++j)
+    for (int j = 0; j < m; ++j)
             for (int64_t p = ix->offsets[j]; p < ix->offsets[j + 1]; p += 128)
                 ctiles.push_back(make_int4(j, (int)p, (int)std::min<int64_t>(p + 128, ix->offsets[j + 1]), 0));
     ix->nctiles = (int32_t)ctiles.size();
-    if (QM > 1) {
-        NR_ALLOC(ix->ctiles_d, ctiles.size() * sizeof(int4));
-        cudaMemcpyAsync(ix->ctiles_d, ctiles.data(), ctiles.size() * sizeof(int4), cudaMemcpyHostToDevice, s);
-    }
+    NR_ALLOC(ix->ctiles_d, ctiles.size() * sizeof(int4));
+    cudaMemcpyAsync(ix->ctiles_d, ctiles.data(), ctiles.size() * sizeof(int4), cudaMemcpyHostToDevice, s);
     NR_ALLOC(ix->A, ix->A_h.size() * 4);
     NR_ALLOC(ix->Apad, Apad.size() * 4);
     NR_ALLOC(ix->R_d, ix->R_h.size() * 2);
@@ -549,24 +547,22 @@ void run_candidates(const nrlsh_index *ix, const float *Qd, const uint32_t *qcod
     }
     if (getenv("NRLSH_TEST_FORCE_FALLBACK"))   // test switch: empty pilot bound -> fallback
         cudaMemsetAsync(delta, 0xff, (size_t)Qb * ix->m, s);
-    const bool tc = scan_tc_supported(ix);
+    bool tc = scan_tc_supported(ix);
     {
         ProfScope p(SLOT_SCAN, s);
+        // (both scans append the same entries — the tensor-core one with ~0 sentinels
+        // counted in cnt, real entries in cntv; a tensor-map failure falls back)
         if (tc) {
             cudaMemsetAsync(cntv, 0, (size_t)Qb * 4, s);
-            if (launch_scan_tc(ix, qcodes, delta, Qb, blk_act, buf, cnt, cntv, C, pairs, s)) {
-                launch_scan(ix, qcodes, delta, Qb, buf, cnt, C, pairs, s);   // (tensor map failure)
-                cudaMemcpyAsync(cntv, cnt, (size_t)Qb * 4, cudaMemcpyDeviceToDevice, s);
-            }
-        } else {
-            launch_scan(ix, qcodes, delta, Qb, buf, cnt, C, pairs, s);
+            if (launch_scan_tc(ix, qcodes, delta, Qb, blk_act, buf, cnt, cntv, C, pairs, s)) tc = false;
         }
+        if (!tc) launch_scan(ix, qcodes, delta, Qb, buf, cnt, C, pairs, s);
     }
     {
         ProfScope p(SLOT_FALLBACK, s);
         launch_fallback(ix, qcodes, Qb, Tq, buf, cnt, tc ? cntv : cnt, C, flags, fb_ws, s);
         // buffer entries the select reads (statistics: the select's HBM roofline)
-        if (entries) launch_sum_counts(tc ? cntv : cnt, Qb, C, entries, s);
+        if (entries) launch_sum_counts(cnt, Qb, C, entries, s);
     }
     {
         ProfScope p(SLOT_SELECT, s);
@@ -621,8 +617,9 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
     const int stride = pilot_stride(n);
     int64_t max_part = 0;
     for (int j = 0; j < ix->m; ++j) max_part = std::max(max_part, ix->offsets[j + 1] - ix->offsets[j]);
-    const int64_t C = buffer_capacity(Tq, stride, n, max_part);
+    int64_t C = buffer_capacity(Tq, stride, n, max_part);
     int Qmax = (int)std::min<int64_t>(ix->query_batch, nq);
+    if (scan_tc_supported(ix)) C += scan_tc_slack(Qmax);   // (its runs' unused tails)
     // keep the candidate buffers bounded (~2.5 GB)
     const int64_t per_q = C * 8 + Tq * 10;
     while (Qmax > 64 && (int64_t)Qmax * per_q > (int64_t)2500 << 20) Qmax >>= 1;

@@ -157,6 +157,7 @@ int scan_kp(int L);
 void launch_expand_pm(const uint32_t *codes, int64_t rows, int W, int L, int8_t *out, cudaStream_t s);
 bool scan_tc_supported(const nrlsh_index *ix);
 size_t scan_tc_ws_bytes(const nrlsh_index *ix, int Qb);
+int64_t scan_tc_slack(int Qmax);   // buffer slots per query the tensor-core scan may fill with sentinels
 int launch_scan_tc(const nrlsh_index *ix, const uint32_t *qcodes, const int8_t *delta, int Qb,
                    void *ws, unsigned long long *buf, uint32_t *cnt, uint32_t *cntv, int64_t C,
                    unsigned long long *pairs, cudaStream_t s);
@@ -289,6 +290,8 @@ struct GtTiles {
 void launch_sort_by_bound(const float *Q, int d, int Qb, const uint32_t *theta_glob,
                           int32_t *qperm, cudaStream_t s);
 size_t gt_tile_ws_bytes(int64_t n, int Qb);
+// qperm in: uint32 keys per query; out: queries in ascending (key, index) order (Qb <= 4096)
+void launch_sort_keys(int Qb, int32_t *qperm, cudaStream_t s);
 void launch_tile_xmax128(const float *xnorm_pos, int64_t n, float *out, cudaStream_t s);
 // Xb / xnorm rows in any order: perm[row] = item id written to the survivor lists
 // (nullptr: rows are ids)

@@ -95,6 +95,22 @@ bool make_tmap_2d(CUtensorMap *m, const void *base, CUtensorMapDataType dt, int 
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
+// 1-D tensor of n elements, box of `box` elements (any start element; out of range
+// reads as zero)
+bool make_tmap_1d(CUtensorMap *m, const void *base, CUtensorMapDataType dt, int esize, uint64_t n,
+                  uint32_t box) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return false;
+    (void)esize;
+    cuuint64_t dims[1] = {n};
+    cuuint64_t strides[1] = {0};
+    cuuint32_t bx[1] = {box};
+    cuuint32_t es[1] = {1};
+    CUresult r = fn(m, dt, 1, const_cast<void *>(base), dims, strides, bx, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
 static bool make_tmap(CUtensorMap *m, const void *base, CUtensorMapDataType dt, int esize,
                       uint64_t cols, uint64_t rows, uint32_t box_cols, uint32_t box_rows) {
     return make_tmap_2d(m, base, dt, esize, cols, rows, box_cols, box_rows, 128);
@@ -958,6 +974,14 @@ __global__ void __launch_bounds__(1024) sort_by_bound(int Qb, int32_t *__restric
             __syncthreads();
         }
     for (int i = threadIdx.x; i < Qb; i += blockDim.x) qperm[i] = (int32_t)(uint32_t)keys[i];
+}
+
+// qperm in: uint32 keys per query; out: the queries in ascending (key, index) order
+void launch_sort_keys(int Qb, int32_t *qperm, cudaStream_t s) {
+    int np2 = 2;
+    while (np2 < Qb) np2 <<= 1;
+    launch_pdl(sort_by_bound, dim3(1), dim3(1024), (size_t)std::max(np2, 1024) * 8, s, Qb, qperm);
+    note_launch();
 }
 
 void launch_sort_by_bound(const float *Q, int d, int Qb, const uint32_t *theta_glob,
