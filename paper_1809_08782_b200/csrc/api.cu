@@ -283,6 +283,7 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
     ix->eps = o.eps;
     ix->scheme = o.scheme;
     ix->query_batch = o.query_batch > 0 ? o.query_batch : 1024;
+    if (getenv("NRLSH_QUERY_BATCH")) ix->query_batch = std::max(1, atoi(getenv("NRLSH_QUERY_BATCH")));   // (experiments)
     ix->proj = o.proj;
     ix->QM = o.proj == NRLSH_PROJ_PER_PARTITION ? num_parts : 1;
     if (ix->QM > 1 && !codes_tc_supported(d, words_for(L)))
@@ -339,54 +340,102 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
     NR_ALLOC(ix->V_d, (size_t)m * 8);
     NR_ALLOC(ix->codes, (size_t)n * W * 4 + 64);   // (+64: the scan's aligned bulk copies)
 
-    // K1: norms + finite check
-    DBuf bad;
-    if (bad.alloc(8, s)) return fail(NRLSH_ENOMEM, "cudaMallocAsync");
-    cudaMemsetAsync(bad.p, 0xff, 8, s);
-    {
-        ProfScope p(SLOT_NORMS, s);
-        launch_norms(ix->X, n, d, ix->norm2, bad.get<unsigned long long>(), ix->Xb, ix->dpb,
-                     ix->xnorm, s);
-    }
-    unsigned long long badidx = 0;
-    cudaMemcpyAsync(&badidx, bad.p, 8, cudaMemcpyDeviceToHost, s);
-    cudaError_t e = cudaStreamSynchronize(s);
-    if (e) return cuda_fail(e, "norms");
-    if (badidx != ~0ull)
-        return fail(NRLSH_ENONFINITE, "non-finite item at index " + std::to_string(badidx));
-
-    // K2: partition + stable scatter
-    std::string err;
-    int rc;
-    {
-        ProfScope p(SLOT_PARTITION, s);
-        rc = (o.scheme == NRLSH_SCHEME_PERCENTILE)
-                 ? partition_percentile(ix->norm2, n, m, ix->part_of_id, s, &err)
-                 : partition_uniform(ix->norm2, n, m, ix->part_of_id, s, &err);
-    }
-    if (rc) return fail((nrlsh_status)rc, err);
-    {
-        ProfScope p(SLOT_SCATTER, s);
-        rc = partition_scatter(ix->norm2, ix->part_of_id, n, m, ix->perm, ix->pos_of_id,
-                               ix->part_of_pos, ix->offsets_d, ix->V_d, s, &err);
-    }
-    if (rc) return fail((nrlsh_status)rc, err);
-    ix->offsets.resize(m + 1);
-    ix->V.resize(m);
-    cudaMemcpyAsync(ix->offsets.data(), ix->offsets_d, (size_t)(m + 1) * 8, cudaMemcpyDeviceToHost, s);
-    cudaMemcpyAsync(ix->V.data(), ix->V_d, (size_t)m * 8, cudaMemcpyDeviceToHost, s);
-    e = cudaStreamSynchronize(s);
-    if (e) return cuda_fail(e, "partition readback");
-    ix->U.resize(m);
-    for (int j = 0; j < m; ++j) ix->U[j] = std::sqrt(ix->V[j]);
-
-    // K4 (host): projection(s) and the sorted (U_j, l) structure
+    // One host round trip: the device steps of Alg. 1 are enqueued ahead of the host
+    // work that depends on them.  Stream order: norms, partition, scatter, the
+    // read-back of (offsets, V, flags) [event], codes and the |x| tiles; meanwhile the
+    // host generates the projection (before the codes are enqueued) and, once the
+    // event fires, builds its tables while the codes kernel runs.
     const int QM = ix->QM;
     const size_t ablk = (size_t)(d + 1) * L, pblk = (size_t)(d + 1) * 32 * W;
-    ix->A_h.resize(QM * ablk);
-    std::vector<float> Apad(QM * pblk, 0.f);
-    {   // A_j from seed XOR j (A_0 = the shared A); per-sub-dataset projections are
-        // m independent draws, generated on up to 16 host threads
+    NR_ALLOC(ix->A, (size_t)QM * ablk * 4);
+    NR_ALLOC(ix->Apad, (size_t)QM * pblk * 4);
+    // build flags: [0] first non-finite item (~0: none), [1] large percentile group,
+    // [2] the filter's first-pass |x| split (float bits)
+    DBuf res;
+    if (res.alloc(32, s)) return fail(NRLSH_ENOMEM, "cudaMallocAsync");
+    const unsigned long long res0[4] = {~0ull, 0ull, 0ull, 0ull};
+    cudaMemcpyAsync(res.p, res0, 32, cudaMemcpyHostToDevice, s);
+    unsigned long long *resd = res.get<unsigned long long>();
+    const int64_t ntx = (n + 127) / 128;   // 128-row |x| tiles
+    ix->offsets.resize(m + 1);
+    ix->V.resize(m);
+    // pinned read-back area (a D2H copy into pageable memory would block the host):
+    // [offsets (m+1) | V (m) | flags (4)], thread-local and grown on demand
+    thread_local void *pin = nullptr;
+    thread_local size_t pin_bytes = 0;
+    const size_t need = (size_t)(2 * m + 1) * 8 + 32;
+    if (pin_bytes < need) {
+        if (pin) cudaFreeHost(pin);
+        pin = nullptr;
+        pin_bytes = 0;
+        if (cudaMallocHost(&pin, std::max<size_t>(need, 8192)) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(NRLSH_ENOMEM, "pinned read-back buffer");
+        }
+        pin_bytes = std::max<size_t>(need, 8192);
+    }
+    int64_t *h_off = reinterpret_cast<int64_t *>(pin);
+    double *h_V = reinterpret_cast<double *>(h_off + m + 1);
+    unsigned long long *hres = reinterpret_cast<unsigned long long *>(h_V + m);
+    cudaEvent_t ev_part;
+    cudaEventCreateWithFlags(&ev_part, cudaEventDisableTiming);
+    std::unique_ptr<CUevent_st, cudaError_t (*)(cudaEvent_t)> ev_guard(ev_part, cudaEventDestroy);
+    auto partition_steps = [&](bool fast) -> nrlsh_status {
+        std::string err;
+        int rc;
+        if (fast) {   // K1: norms + finite check
+            ProfScope p(SLOT_NORMS, s);
+            launch_norms(ix->X, n, d, ix->norm2, resd, ix->Xb, ix->dpb, ix->xnorm, s);
+        }
+        {   // K2: percentile (or uniform) partition
+            ProfScope p(SLOT_PARTITION, s);
+            if (o.scheme != NRLSH_SCHEME_PERCENTILE)
+                rc = partition_uniform(ix->norm2, n, m, ix->part_of_id, s, &err);
+            else if (fast)
+                rc = partition_percentile_fast(ix->norm2, n, m, ix->part_of_id,
+                                               reinterpret_cast<unsigned int *>(resd + 1), s, &err);
+            else
+                rc = partition_percentile(ix->norm2, n, m, ix->part_of_id, s, &err);
+        }
+        if (rc) return fail((nrlsh_status)rc, err);
+        {   // stable scatter: perm, positions, offsets, V
+            ProfScope p(SLOT_SCATTER, s);
+            rc = partition_scatter(ix->norm2, ix->part_of_id, n, m, ix->perm, ix->pos_of_id,
+                                   ix->part_of_pos, ix->offsets_d, ix->V_d, s, &err);
+        }
+        if (rc) return fail((nrlsh_status)rc, err);
+        cudaMemcpyAsync(h_off, ix->offsets_d, (size_t)(m + 1) * 8, cudaMemcpyDeviceToHost, s);
+        cudaMemcpyAsync(h_V, ix->V_d, (size_t)m * 8, cudaMemcpyDeviceToHost, s);
+        cudaMemcpyAsync(hres, res.p, 16, cudaMemcpyDeviceToHost, s);
+        cudaEventRecord(ev_part, s);
+        return NRLSH_OK;
+    };
+    auto code_steps = [&]() {
+        ProfScope p(SLOT_CODES, s);
+        // K3: codes (shared A: every input is on the device already)
+        if (QM == 1)
+            launch_item_codes(ix->X, n, d, ix->norm2, ix->part_of_id, ix->V_d, ix->Apad, L, W,
+                              ix->pos_of_id, ix->codes, ix->Xb, ix->dpb, ix->xnorm, ix->Xpad,
+                              ix->dpad, s, ix->perm);
+        // |x| in partition order (the tensor-core filter's tiles) and the first-pass split
+        // of those tiles: the 1/800 (at least 16) with the largest |x| (c4: 0.15 vs 0.18 ms
+        // per 1024 seeded queries at 1/50, 0.37 vs 0.74 unseeded; the first pass's exact
+        // k-th best then prunes every other tile)
+        launch_gather_f32(ix->xnorm, ix->perm, n, ix->xnorm_pos, s);
+        launch_tile_xmax128(ix->xnorm_pos, n, ix->tile_xmax, s);
+        if (ntx >= 64) {
+            const int64_t div = getenv("NRLSH_GT_SPLIT_DIV") ? std::max(2, atoi(getenv("NRLSH_GT_SPLIT_DIV"))) : 800;
+            const int64_t r = ntx - std::min<int64_t>(ntx - 1, std::max<int64_t>(16, ntx / div));
+            launch_select_kth_float(ix->tile_xmax, ntx, r, reinterpret_cast<float *>(resd + 2), s);
+        }
+    };
+    nrlsh_status st = partition_steps(true);
+    if (st) return st;
+    {   // K4a (host, overlapped with the partition): A_j from seed XOR j (A_0 = the
+        // shared A); per-sub-dataset projections are m independent draws, on up to 16
+        // host threads
+        ix->A_h.resize(QM * ablk);
+        std::vector<float> Apad(QM * pblk, 0.f);
         auto gen = [&](int j0, int j1) {
             for (int j = j0; j < j1; ++j) {
                 std::vector<float> Aj;
@@ -404,7 +453,26 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
             for (int t = 0; t < nt; ++t) th.emplace_back(gen, QM * t / nt, QM * (t + 1) / nt);
             for (auto &t : th) t.join();
         }
+        // (pageable sources: staged before the calls return)
+        cudaMemcpyAsync(ix->A, ix->A_h.data(), ix->A_h.size() * 4, cudaMemcpyHostToDevice, s);
+        cudaMemcpyAsync(ix->Apad, Apad.data(), Apad.size() * 4, cudaMemcpyHostToDevice, s);
     }
+    code_steps();
+    cudaError_t e = cudaEventSynchronize(ev_part);
+    if (e) return cuda_fail(e, "build");
+    if (hres[0] != ~0ull)
+        return fail(NRLSH_ENONFINITE, "non-finite item at index " + std::to_string(hres[0]));
+    if (hres[1]) {   // (ties or duplicates: a boundary group needs the multi-level select)
+        if ((st = partition_steps(false))) return st;
+        code_steps();
+        if ((e = cudaEventSynchronize(ev_part))) return cuda_fail(e, "build");
+    }
+    std::copy(h_off, h_off + m + 1, ix->offsets.begin());
+    std::copy(h_V, h_V + m, ix->V.begin());
+    ix->U.resize(m);
+    for (int j = 0; j < m; ++j) ix->U[j] = std::sqrt(ix->V[j]);
+
+    // K4b (host): the sorted (U_j, l) structure and the work lists
     std::vector<int32_t> order;
     make_rank_table(ix->U, L, ix->eps, ix->R_h, order);
     // scan work units: chunks of <= scan_chunk_items() positions inside one sub-dataset
@@ -420,49 +488,33 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
         for (int64_t p = ix->offsets[j]; p < ix->offsets[j + 1]; p += 256)
             tiles.push_back(make_int4(j, (int)p, (int)std::min<int64_t>(p + 256, ix->offsets[j + 1]), 0));
     ix->ntiles = (int32_t)tiles.size();
-    // per-sub-dataset projections: the code kernel's tiles of <= 128 positions of one j
-    // (also the tensor-core scan's item tiles)
+    // tiles of <= 128 positions of one sub-dataset: the code kernel's with per-sub-
+    // dataset projections, the (opt-in) tensor-core scan's items
     std::vector<int4> ctiles;
     for (int j = 0; j < m; ++j)
-            for (int64_t p = ix->offsets[j]; p < ix->offsets[j + 1]; p += 128)
-                ctiles.push_back(make_int4(j, (int)p, (int)std::min<int64_t>(p + 128, ix->offsets[j + 1]), 0));
+        for (int64_t p = ix->offsets[j]; p < ix->offsets[j + 1]; p += 128)
+            ctiles.push_back(make_int4(j, (int)p, (int)std::min<int64_t>(p + 128, ix->offsets[j + 1]), 0));
     ix->nctiles = (int32_t)ctiles.size();
     NR_ALLOC(ix->ctiles_d, ctiles.size() * sizeof(int4));
-    cudaMemcpyAsync(ix->ctiles_d, ctiles.data(), ctiles.size() * sizeof(int4), cudaMemcpyHostToDevice, s);
-    NR_ALLOC(ix->A, ix->A_h.size() * 4);
-    NR_ALLOC(ix->Apad, Apad.size() * 4);
     NR_ALLOC(ix->R_d, ix->R_h.size() * 2);
     NR_ALLOC(ix->order_d, order.size() * 4);
     NR_ALLOC(ix->chunks_d, chunks.size() * sizeof(int4));
     NR_ALLOC(ix->tiles_d, tiles.size() * sizeof(int4));
-    cudaMemcpyAsync(ix->A, ix->A_h.data(), ix->A_h.size() * 4, cudaMemcpyHostToDevice, s);
-    cudaMemcpyAsync(ix->Apad, Apad.data(), Apad.size() * 4, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(ix->ctiles_d, ctiles.data(), ctiles.size() * sizeof(int4), cudaMemcpyHostToDevice, s);
     cudaMemcpyAsync(ix->R_d, ix->R_h.data(), ix->R_h.size() * 2, cudaMemcpyHostToDevice, s);
     cudaMemcpyAsync(ix->order_d, order.data(), order.size() * 4, cudaMemcpyHostToDevice, s);
     cudaMemcpyAsync(ix->chunks_d, chunks.data(), chunks.size() * sizeof(int4), cudaMemcpyHostToDevice, s);
     cudaMemcpyAsync(ix->tiles_d, tiles.data(), tiles.size() * sizeof(int4), cudaMemcpyHostToDevice, s);
-
-    // K3: codes
-    {
+    if (QM > 1) {   // K3 with per-sub-dataset projections: partition-ordered tiles
         ProfScope p(SLOT_CODES, s);
-        if (QM > 1)
-            launch_item_codes_tc(ix->X, n, d, ix->norm2, ix->part_of_id, ix->V_d, ix->Apad, L, W,
-                                 ix->pos_of_id, ix->codes, ix->Xb, ix->dpb, ix->Xpad, ix->dpad, s,
-                                 ix->ctiles_d, ix->nctiles, ix->perm);
-        else
-            launch_item_codes(ix->X, n, d, ix->norm2, ix->part_of_id, ix->V_d, ix->Apad, L, W,
-                              ix->pos_of_id, ix->codes, ix->Xb, ix->dpb, ix->xnorm, ix->Xpad,
-                              ix->dpad, s, ix->perm);
+        launch_item_codes_tc(ix->X, n, d, ix->norm2, ix->part_of_id, ix->V_d, ix->Apad, L, W,
+                             ix->pos_of_id, ix->codes, ix->Xb, ix->dpb, ix->Xpad, ix->dpad, s,
+                             ix->ctiles_d, ix->nctiles, ix->perm);
     }
-    // |x| in partition order (the tensor-core filter's tiles)
     {
         ProfScope p(SLOT_CODES, s);
-        launch_gather_f32(ix->xnorm, ix->perm, n, ix->xnorm_pos, s);
-        launch_tile_xmax128(ix->xnorm_pos, n, ix->tile_xmax, s);
         if (ix->codes_pm) launch_expand_pm(ix->codes, n, W, L, ix->codes_pm, s);
-    }
-    // compacted pilot sample (query-time pilots read it contiguously)
-    {
+        // compacted pilot sample (query-time pilots read it contiguously)
         const int stride = pilot_stride(n);
         if (stride > 1) {
             // (interleaved slots: 32 columns of ceil(samples / 32); unused slots get
@@ -471,25 +523,17 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
             NR_ALLOC(ix->samp_codes, (size_t)ix->nsamp * W * 4);
             NR_ALLOC(ix->samp_part, (size_t)ix->nsamp);
             cudaMemsetAsync(ix->samp_part, 0xff, (size_t)ix->nsamp, s);
-            ProfScope p(SLOT_CODES, s);
             launch_gather_sample(ix.get(), stride, ix->samp_codes, ix->samp_part, s);
         }
     }
+    cudaMemcpyAsync(hres + 2, resd + 2, 8, cudaMemcpyDeviceToHost, s);
     e = cudaStreamSynchronize(s);
     if (e) return cuda_fail(e, "codes");
-    {   // first-pass split of the filter's tiles: the 1/800 (at least 16) with the
-        // largest |x| (c4: 0.15 vs 0.18 ms per 1024 seeded queries at 1/50, 0.37 vs
-        // 0.74 unseeded; the first pass's exact k-th best then prunes every other tile)
-        const int64_t nt = (n + 127) / 128;
-        if (nt >= 64) {
-            std::vector<float> xm((size_t)nt);
-            if ((e = cudaMemcpy(xm.data(), ix->tile_xmax, (size_t)nt * 4, cudaMemcpyDeviceToHost)))
-                return cuda_fail(e, "tile xmax");
-            const int64_t div = getenv("NRLSH_GT_SPLIT_DIV") ? std::max(2, atoi(getenv("NRLSH_GT_SPLIT_DIV"))) : 800;
-            const int64_t r = nt - std::min<int64_t>(nt - 1, std::max<int64_t>(16, nt / div));
-            std::nth_element(xm.begin(), xm.begin() + r, xm.end());
-            ix->tile_xsplit = xm[(size_t)r];
-        }
+    {
+        float xs;
+        const uint32_t xb = (uint32_t)hres[2];
+        std::memcpy(&xs, &xb, 4);
+        ix->tile_xsplit = ntx >= 64 ? xs : 0.f;
     }
     prof_collect();
     e = cudaGetLastError();

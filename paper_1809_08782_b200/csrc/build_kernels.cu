@@ -440,6 +440,56 @@ __global__ void __launch_bounds__(1024) sel_resolve_small(
     }
 }
 
+// Device-decided resolution of the level-0 groups (no host round trip): block g
+// sorts group g if it exists and is small; a larger group sets *large (the host then
+// redoes the partition with the multi-level path).
+__global__ void __launch_bounds__(1024) sel_resolve_dev(
+    const SelGroup *__restrict__ groups, const int64_t *__restrict__ meta,
+    const uint64_t *__restrict__ keys, const uint32_t *__restrict__ ids, int64_t n, int m,
+    uint8_t *__restrict__ part, unsigned int *__restrict__ large) {
+    __shared__ uint64_t sk[kSmallGroup];
+    __shared__ uint32_t si[kSmallGroup];
+    if ((int64_t)blockIdx.x >= meta[0]) return;
+    const SelGroup g = groups[blockIdx.x];
+    const int cnt = (int)g.count;
+    if (g.count > (uint32_t)kSmallGroup) {
+        if (threadIdx.x == 0) atomicOr(large, 1u);
+        return;
+    }
+    int np2 = 1;
+    while (np2 < cnt) np2 <<= 1;
+    for (int t = threadIdx.x; t < np2; t += blockDim.x) {
+        if (t < cnt) {
+            sk[t] = keys[g.cand_off + t];
+            si[t] = ids[g.cand_off + t];
+        } else {
+            sk[t] = ~0ull;
+            si[t] = 0xffffffffu;
+        }
+    }
+    __syncthreads();
+    for (int size = 2; size <= np2; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int t = threadIdx.x; t < np2; t += blockDim.x) {
+                const int o = t ^ stride;
+                if (o > t) {
+                    const bool up = ((t & size) == 0);
+                    const bool gt = (sk[t] > sk[o]) || (sk[t] == sk[o] && si[t] > si[o]);
+                    if (gt == up) {
+                        uint64_t tk = sk[t]; sk[t] = sk[o]; sk[o] = tk;
+                        uint32_t ti = si[t]; si[t] = si[o]; si[o] = ti;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int t = threadIdx.x; t < cnt; t += blockDim.x) {
+        const int64_t r = g.base + t;
+        part[si[t]] = (uint8_t)((r * m) / n);
+    }
+}
+
 namespace {
 // stream-ordered scratch (memory pool): no device-wide synchronisation on free
 struct DevBuf {
@@ -454,6 +504,45 @@ struct DevBuf {
     }
 };
 }  // namespace
+
+// One level of the exact multi-select, decided on the device: the first digit's
+// histogram, the boundary groups, direct assignment outside them and an in-smem sort
+// of each group (<= kSmallGroup items; continuous norms — every BASELINE config —
+// leave only such groups).  No host synchronisation; *large (device) is set when a
+// group is larger, and the caller then runs partition_percentile.
+int partition_percentile_fast(const double *norm2, int64_t n, int m, uint8_t *part,
+                              unsigned int *large, cudaStream_t s, std::string *err) {
+    if (m == 1) {
+        cudaMemsetAsync(part, 0, (size_t)n, s);
+        return 0;
+    }
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const SelLevel lv = kLevels[0];
+    const int64_t nbins = 1ll << lv.width;
+    DevBuf H(s), P(s), TS(s), G(s), META(s), FILL(s), KB(s), IB(s);
+    if (H.alloc(nbins * 4) || P.alloc(nbins * 4) || TS.alloc(4096 * 4) ||
+        G.alloc(sizeof(SelGroup) * kMaxGroups) || META.alloc(16) || FILL.alloc(kMaxGroups * 4) ||
+        KB.alloc((size_t)n * 8) || IB.alloc((size_t)n * 4)) {
+        *err = "partition: cudaMalloc failed";
+        return NRLSH_ENOMEM;
+    }
+    cudaMemsetAsync(H.p, 0, nbins * 4, s);
+    cudaMemsetAsync(FILL.p, 0, kMaxGroups * 4, s);
+    const int grid = grid_for(n, 256, sms * 16);
+    sel_hist<true><<<grid, 256, 0, s>>>(norm2, nullptr, nullptr, n, lv.shift, lv.width, H.get<uint32_t>());
+    scan_excl(H.get<uint32_t>(), P.get<uint32_t>(), nbins, TS.get<uint32_t>(), s);
+    sel_locate<<<1, kMaxParts, 0, s>>>(H.get<uint32_t>(), P.get<uint32_t>(), nbins, 0, n, n, m,
+                                       G.get<SelGroup>(), META.get<int64_t>());
+    sel_classify<true><<<grid, 256, 0, s>>>(norm2, nullptr, nullptr, n, lv.shift, lv.width,
+                                            P.get<uint32_t>(), (int64_t)0, n, m, G.get<SelGroup>(),
+                                            META.get<int64_t>(), FILL.get<uint32_t>(),
+                                            KB.get<uint64_t>(), IB.get<uint32_t>(), part);
+    sel_resolve_dev<<<kMaxGroups, 1024, 0, s>>>(G.get<SelGroup>(), META.get<int64_t>(), KB.get<uint64_t>(),
+                                               IB.get<uint32_t>(), n, m, part, large);
+    note_launch(nbins > 4096 ? 8 : 6);
+    return 0;
+}
 
 int partition_percentile(const double *norm2, int64_t n, int m, uint8_t *part, cudaStream_t s,
                          std::string *err) {
@@ -566,6 +655,40 @@ int partition_percentile(const double *norm2, int64_t n, int m, uint8_t *part, c
     return 0;
 }
 
+// ------------------------------------------------------------- k-th of non-negative floats
+// One CTA: 4 radix passes of 8 bits over the IEEE bit patterns (monotone for x >= 0).
+__global__ void __launch_bounds__(1024) select_kth_float(const float *__restrict__ v, int64_t nt, int64_t r,
+                                                         float *__restrict__ out) {
+    __shared__ uint32_t hist[256];
+    __shared__ uint32_t s_prefix, s_r;
+    if (threadIdx.x == 0) { s_prefix = 0u; s_r = (uint32_t)r; }
+    for (int pass = 0; pass < 4; ++pass) {
+        const int shift = 24 - 8 * pass;
+        const uint32_t pmask = pass == 0 ? 0u : (0xFFFFFFFFu << (shift + 8));
+        for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0u;
+        __syncthreads();
+        const uint32_t prefix = s_prefix;
+        for (int64_t i = threadIdx.x; i < nt; i += blockDim.x) {
+            const uint32_t b = __float_as_uint(v[i]);
+            if ((b & pmask) == prefix) atomicAdd(&hist[(b >> shift) & 255u], 1u);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t rr = s_r, d = 0;
+            while (d < 255 && hist[d] <= rr) { rr -= hist[d]; ++d; }
+            s_r = rr;
+            s_prefix = prefix | (d << shift);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = __uint_as_float(s_prefix);
+}
+
+void launch_select_kth_float(const float *v, int64_t nt, int64_t r, float *out, cudaStream_t s) {
+    select_kth_float<<<1, 1024, 0, s>>>(v, nt, r, out);
+    note_launch();
+}
+
 // ------------------------------------------------------------- uniform (NEXT-2)
 __global__ void minmax_bits(const double *__restrict__ norm2, int64_t n,
                             unsigned long long *__restrict__ mm) {
@@ -622,11 +745,6 @@ int partition_uniform(const double *norm2, int64_t n, int m, uint8_t *part, cuda
     note_launch(2);
     uniform_assign<<<grid_for(n, 256, 4096), 256, 0, s>>>(norm2, n, m,
                                                          mm.get<unsigned long long>(), part);
-    cudaError_t e = cudaStreamSynchronize(s);
-    if (e != cudaSuccess) {
-        *err = std::string("partition: ") + cudaGetErrorString(e);
-        return NRLSH_ECUDA;
-    }
     return 0;
 }
 

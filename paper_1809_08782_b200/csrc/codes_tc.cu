@@ -67,8 +67,9 @@ struct CodesArgs {
 
 // tile sequence of a CTA: shared A — tiles blockIdx.x + t gridDim.x; per-sub-dataset
 // A_j — the contiguous run [lo, hi)
+template <bool PP>
 __device__ __forceinline__ void ct_range(const CodesArgs &a, int64_t &lo, int64_t &hi) {
-    if (a.ctiles) {
+    if (PP) {
         lo = a.ntiles * blockIdx.x / gridDim.x;
         hi = a.ntiles * (blockIdx.x + 1) / gridDim.x;
     } else {
@@ -76,11 +77,13 @@ __device__ __forceinline__ void ct_range(const CodesArgs &a, int64_t &lo, int64_
         hi = a.ntiles;
     }
 }
-__device__ __forceinline__ int64_t ct_step(const CodesArgs &a) { return a.ctiles ? 1 : gridDim.x; }
+template <bool PP>
+__device__ __forceinline__ int64_t ct_step(const CodesArgs &a) { return PP ? 1 : gridDim.x; }
 
 // row rr of tile `tile`: item id (i < 0: past the tile / past n) and destination position
+template <bool PP>
 __device__ __forceinline__ void ct_row(const CodesArgs &a, int64_t tile, int rr, int64_t &i, int64_t &pos) {
-    if (a.ctiles) {
+    if (PP) {
         const int4 t = __ldg(a.ctiles + tile);
         const int64_t p = (int64_t)t.y + rr;
         if (p < t.z) { pos = p; i = __ldg(a.perm + p); }
@@ -100,15 +103,15 @@ __device__ __forceinline__ uint32_t swz(int row, int kbyte) {
 // ring: RAW K-blocks in flight per SM without holding them in registers.
 constexpr int CT_RAW_SLOT = CT_CONV * 16 * 4;   // 16 KB: 16 floats per converter thread
 
-template <int VEC>
+template <int VEC, bool PP>
 __device__ __forceinline__ void conv_issue(const CodesArgs &a, int64_t tile, int kb, int w, int l,
                                            uint8_t *slot, int32_t *posr) {
     // with the first K-block of a tile, the warp's 16 rows' partition positions (the
     // bf16 copy's destination rows; read back by the warp only)
     if (kb == 0 && a.Xb && l < 16) {
-        if (a.ctiles) {   // destination rows are the positions themselves
+        if (PP) {   // destination rows are the positions themselves
             int64_t i, pos;
-            ct_row(a, tile, 16 * w + l, i, pos);
+            ct_row<PP>(a, tile, 16 * w + l, i, pos);
             posr[16 * w + l] = (int32_t)pos;
         } else {
             const int64_t i = tile * CT_M + 16 * w + l;
@@ -127,7 +130,7 @@ __device__ __forceinline__ void conv_issue(const CodesArgs &a, int64_t tile, int
     for (int j = 0; j < ni; ++j) {
         const int rr = 16 * w + j * rpi + l / lpr;
         int64_t i, pos;
-        ct_row(a, tile, rr, i, pos);
+        ct_row<PP>(a, tile, rr, i, pos);
         const int64_t ic = i >= 0 ? i : 0;
         const float *p = a.X + ic * a.d + cc;
         const uint32_t dst = tc::smem_u32(slot + (size_t)(j * CT_CONV + tid) * VEC * 4);
@@ -138,7 +141,7 @@ __device__ __forceinline__ void conv_issue(const CodesArgs &a, int64_t tile, int
     }
 }
 
-template <int VEC>
+template <int VEC, bool PP>
 __device__ __forceinline__ void conv_read(const uint8_t *slot, int w, int l, float (&v)[16]) {
     constexpr int lpr = VEC == 4 ? 8 : (VEC == 2 ? 16 : 32);
     constexpr int rpi = 32 / lpr;
@@ -166,7 +169,7 @@ __device__ __forceinline__ void cp_async_wait(int la) {
     else asm volatile("cp.async.wait_group 1;" ::: "memory");
 }
 
-template <int VEC>
+template <int VEC, bool PP>
 __device__ __forceinline__ void conv_store(uint8_t *stage, int w, int l, const float (&v)[16]) {
     constexpr int lpr = VEC == 4 ? 8 : (VEC == 2 ? 16 : 32);
     constexpr int rpi = 32 / lpr;
@@ -199,7 +202,7 @@ __device__ __forceinline__ void conv_store(uint8_t *stage, int w, int l, const f
 
 
 // bf16 copy of the converter's slice of the rows (columns < dpb; zeros past d)
-template <int VEC>
+template <int VEC, bool PP>
 __device__ __forceinline__ void conv_store_bf16(const CodesArgs &a, int64_t tile, int kb, int w, int l,
                                                 const float (&v)[16], const int32_t *posr) {
     constexpr int lpr = VEC == 4 ? 8 : (VEC == 2 ? 16 : 32);
@@ -211,7 +214,7 @@ __device__ __forceinline__ void conv_store_bf16(const CodesArgs &a, int64_t tile
     for (int j = 0; j < ni; ++j) {
         const int rr = 16 * w + j * rpi + l / lpr;
         const int32_t prow = posr[rr];
-        if (a.ctiles ? prow < 0 : tile * CT_M + rr >= a.n) continue;
+        if (PP ? prow < 0 : tile * CT_M + rr >= a.n) continue;
         __nv_bfloat16 *dst = a.Xb + (int64_t)prow * a.dpb + col;
         if (VEC == 4) {
             const __nv_bfloat162 p0 = __floats2bfloat162_rn(v[j * 4 + 0], v[j * 4 + 1]);
@@ -228,7 +231,7 @@ __device__ __forceinline__ void conv_store_bf16(const CodesArgs &a, int64_t tile
     }
 }
 
-template <int VEC>
+template <int VEC, bool PP>
 __device__ __forceinline__ void conv_store_pad(const CodesArgs &a, int64_t tile, int kb, int w, int l,
                                                const float (&v)[16]) {
     constexpr int lpr = VEC == 4 ? 8 : (VEC == 2 ? 16 : 32);
@@ -240,7 +243,7 @@ __device__ __forceinline__ void conv_store_pad(const CodesArgs &a, int64_t tile,
     for (int j = 0; j < ni; ++j) {
         const int rr = 16 * w + j * rpi + l / lpr;
         int64_t i, pos;
-        ct_row(a, tile, rr, i, pos);
+        ct_row<PP>(a, tile, rr, i, pos);
         if (i < 0) continue;
         float *dst = a.Xpad + i * a.dpad + col;
         if (VEC == 4) *reinterpret_cast<float4 *>(dst) = make_float4(v[j * 4], v[j * 4 + 1], v[j * 4 + 2], v[j * 4 + 3]);
@@ -249,7 +252,7 @@ __device__ __forceinline__ void conv_store_pad(const CodesArgs &a, int64_t tile,
     }
 }
 
-template <int VEC>
+template <int VEC, bool PP>
 __global__ void __launch_bounds__(CT_THREADS, 1) k3_codes_tc(CodesArgs a) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
@@ -277,7 +280,7 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k3_codes_tc(CodesArgs a) {
             *reinterpret_cast<float *>(Bs + (size_t)kb * N * 128 + swz(b, k * 4)) = v;
         }
     };
-    if (!a.ctiles) {
+    if (!PP) {
         load_B(a.Apad, threadIdx.x, blockDim.x);
         for (int b = threadIdx.x; b < N; b += blockDim.x) Ad[b] = a.Apad[(size_t)a.d * N + b];
     }
@@ -306,8 +309,8 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k3_codes_tc(CodesArgs a) {
         // K-block g of this CTA = (tile blockIdx.x + (g / KB) gridDim.x, kb g % KB);
         // issue and consume cursors advance incrementally (no 64-bit divisions)
         int64_t tlo, thi;
-        ct_range(a, tlo, thi);
-        const int64_t tst = ct_step(a);
+        ct_range<PP>(a, tlo, thi);
+        const int64_t tst = ct_step<PP>(a);
         const int64_t my_tiles = thi > tlo ? (thi - 1 - tlo) / tst + 1 : 0;
         const int64_t G = my_tiles * a.KB;
         const int la = a.raw - 1;
@@ -315,7 +318,7 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k3_codes_tc(CodesArgs a) {
         int i_kb = 0, i_ti = 0, i_slot = 0;
         auto issue = [&]() {
             if (issued < G) {
-                conv_issue<VEC>(a, i_tile, i_kb, warp, lane, rawr + (size_t)i_slot * CT_RAW_SLOT,
+                conv_issue<VEC, PP>(a, i_tile, i_kb, warp, lane, rawr + (size_t)i_slot * CT_RAW_SLOT,
                                 posr + (i_ti & 3) * CT_M);
                 if (++i_kb == a.KB) { i_kb = 0; i_tile += tst; ++i_ti; }
                 if (++i_slot == a.raw) i_slot = 0;
@@ -332,11 +335,11 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k3_codes_tc(CodesArgs a) {
             cp_async_wait(la);     // this thread's copies for K-block g have landed
             __syncwarp();          // (and the warp's positions of the tile's rows)
             float cur[16];
-            conv_read<VEC>(rawr + (size_t)rslot * CT_RAW_SLOT, warp, lane, cur);
+            conv_read<VEC, PP>(rawr + (size_t)rslot * CT_RAW_SLOT, warp, lane, cur);
             tc::mbar_wait(&empty[s], ph ^ 1);
-            conv_store<VEC>(ring + s * CT_STAGE, warp, lane, cur);
-            if (a.Xb) conv_store_bf16<VEC>(a, tile, kb, warp, lane, cur, posr + (ti & 3) * CT_M);
-            if (a.Xpad) conv_store_pad<VEC>(a, tile, kb, warp, lane, cur);
+            conv_store<VEC, PP>(ring + s * CT_STAGE, warp, lane, cur);
+            if (a.Xb) conv_store_bf16<VEC, PP>(a, tile, kb, warp, lane, cur, posr + (ti & 3) * CT_M);
+            if (a.Xpad) conv_store_pad<VEC, PP>(a, tile, kb, warp, lane, cur);
             tc::fence_async_shared();
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&full[s]);
@@ -353,10 +356,10 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k3_codes_tc(CodesArgs a) {
             uint32_t g = 0, t = 0, nb = 0;
             int curj = -1;
             int64_t tlo, thi;
-            ct_range(a, tlo, thi);
-            const int64_t tst = ct_step(a);
+            ct_range<PP>(a, tlo, thi);
+            const int64_t tst = ct_step<PP>(a);
             for (int64_t tile = tlo; tile < thi; tile += tst, ++t) {
-                if (a.ctiles) {
+                if (PP) {
                     const int j = __ldg(a.ctiles + tile).x;
                     if (j != curj) {
                         if (t > 0) {
@@ -402,15 +405,15 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k3_codes_tc(CodesArgs a) {
         const int W = N / 32;
         uint32_t t = 0;
         int64_t tlo, thi;
-        ct_range(a, tlo, thi);
-        const int64_t tst = ct_step(a);
+        ct_range<PP>(a, tlo, thi);
+        const int64_t tst = ct_step<PP>(a);
         for (int64_t tile = tlo; tile < thi; tile += tst, ++t) {
             const uint32_t acc = t & 1, tr = t >> 1;
             int64_t i, pos = 0;
-            ct_row(a, tile, row, i, pos);
+            ct_row<PP>(a, tile, row, i, pos);
             const bool valid = i >= 0;
             // A_d of the tile's projection
-            const float *Adj = a.ctiles ? a.Apad + ((size_t)__ldg(a.ctiles + tile).x * (a.d + 1) + a.d) * N : Ad;
+            const float *Adj = PP ? a.Apad + ((size_t)__ldg(a.ctiles + tile).x * (a.d + 1) + a.d) * N : Ad;
             float tt = 0.f;
             if (valid) {
                 const double Vj = a.V[a.part[i]];
@@ -419,7 +422,7 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k3_codes_tc(CodesArgs a) {
                     const double df = Vj - a.norm2[i];
                     tt = (float)sqrt(df > 0.0 ? df : 0.0);
                 }
-                if (!a.ctiles) pos = a.pos_of_id[i];
+                if (!PP) pos = a.pos_of_id[i];
             }
             tc::mbar_wait(&tfull[acc], tr & 1);
             tc::tc_fence_after();
@@ -522,10 +525,14 @@ void launch_item_codes_tc(const float *X, int64_t n, int d, const double *norm2,
     const size_t sm = codes_tc_smem(a.KB, a.N, a.stages, a.raw);
     const int grid = (int)std::min<int64_t>(sms, a.ntiles);
     const int vec = (d % 4 == 0) ? 4 : ((d % 2 == 0) ? 2 : 1);
-#define NR_CT(V)                                                                               \
-    cudaFuncSetAttribute(k3_codes_tc<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
-    k3_codes_tc<V><<<grid, CT_THREADS, sm, s>>>(a)
-    if (vec == 4) { NR_CT(4); } else if (vec == 2) { NR_CT(2); } else { NR_CT(1); }
+#define NR_CT(V, PP_)                                                                            \
+    cudaFuncSetAttribute(k3_codes_tc<V, PP_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+    k3_codes_tc<V, PP_><<<grid, CT_THREADS, sm, s>>>(a)
+    if (ctiles) {
+        if (vec == 4) { NR_CT(4, true); } else if (vec == 2) { NR_CT(2, true); } else { NR_CT(1, true); }
+    } else {
+        if (vec == 4) { NR_CT(4, false); } else if (vec == 2) { NR_CT(2, false); } else { NR_CT(1, false); }
+    }
 #undef NR_CT
     note_launch();
 }

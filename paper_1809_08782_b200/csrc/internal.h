@@ -93,6 +93,13 @@ void launch_norms(const float *X, int64_t n, int d, double *norm2, unsigned long
 // K2 (percentile): fills part_of_id.  Host-orchestrated; may synchronise `s`.
 int partition_percentile(const double *norm2, int64_t n, int m, uint8_t *part_of_id,
                          cudaStream_t s, std::string *err);
+// level 0 + in-smem group sorts, decided on the device (no host sync); sets *large
+// (device flag) when a boundary group exceeds the in-smem sort: then run the above
+int partition_percentile_fast(const double *norm2, int64_t n, int m, uint8_t *part_of_id,
+                              unsigned int *large, cudaStream_t s, std::string *err);
+// largest-|x| threshold of the filter's first pass: the r-th smallest of nt tile
+// maxima (non-negative floats), radix-selected by one CTA into *out
+void launch_select_kth_float(const float *v, int64_t nt, int64_t r, float *out, cudaStream_t s);
 int partition_uniform(const double *norm2, int64_t n, int m, uint8_t *part_of_id,
                       cudaStream_t s, std::string *err);
 // stable scatter by sub-dataset: perm, pos_of_id, part_of_pos, offsets, V

@@ -355,16 +355,23 @@ void launch_pilot(const nrlsh_index *ix, const uint32_t *qcodes, int Qb, int64_t
 
 // =========================================================================== K6 scan
 constexpr int kScanThreads = 256;
-constexpr int kScanIPT = 8;                       // items per thread
+// items per thread (a work unit = one CTA's chunk of 256 x IPT positions of one
+// sub-dataset), queries per CTA, staged appends per (CTA, query)
+#ifndef NRLSH_SCAN_IPT
+#define NRLSH_SCAN_IPT 8
+#endif
+constexpr int kScanIPT = NRLSH_SCAN_IPT;
 constexpr int kChunk = kScanThreads * kScanIPT;   // items per work unit
-constexpr int kQG = 64;                           // queries per CTA
-constexpr int kSB = 128;                          // staged appends per (CTA, query)
+constexpr int kQG = kScanIPT >= 16 ? 32 : 64;     // queries per CTA
+constexpr int kSB = kScanIPT >= 16 ? 256 : 128;   // staged appends per (CTA, query)
 
 // Appends are staged per query in shared memory as (h << 16 | offset in chunk)
 // — one shared atomic per (warp, query) after a warp prefix sum of the lanes'
 // pass counts — and copied out, expanded to (flat (j, h) << 32 | position), with
 // one global reservation per (CTA, query); a query whose stage fills spills the
-// rest straight to global.
+// rest straight to global.  The CTA's active queries (delta_j(q) >= 0) are packed
+// as (code words, radius, index) records read with one 16-byte shared load per
+// word pair, and a thread's pass bits are the sign bits of delta - h (funnel shifts).
 template <int W>
 __global__ void __launch_bounds__(kScanThreads) k6_scan(
     const uint32_t *__restrict__ codes, const int4 *__restrict__ chunks,
@@ -372,8 +379,8 @@ __global__ void __launch_bounds__(kScanThreads) k6_scan(
     const uint16_t *__restrict__ R, int L, unsigned long long *__restrict__ buf,
     uint32_t *__restrict__ cnt, int64_t C, unsigned long long *__restrict__ pairs, int QM) {
     pdl_wait();
-    __shared__ uint32_t sq[kQG][W];
-    __shared__ int sd[kQG];
+    constexpr int RW = W <= 2 ? 4 : 8;             // record words: codes, radius, query
+    __shared__ __align__(16) uint32_t srec[kQG][RW];
     __shared__ uint32_t sbuf[kQG][kSB];
     __shared__ uint32_t scnt[kQG];
     __shared__ uint32_t sbase[kQG];
@@ -384,23 +391,23 @@ __global__ void __launch_bounds__(kScanThreads) k6_scan(
     const int j = ch.x, p0 = ch.y, p1 = ch.z;
     const int q0 = (blockIdx.x % ngroups) * kQG;
     const int nqg = min(kQG, Qb - q0);
-    __shared__ int sact[kQG];     // compacted list of the queries with delta_j(q) >= 0
     __shared__ int s_nact;
-    if (threadIdx.x < 32) {       // warp 0 compacts the group's active queries
+    if (threadIdx.x < 32) {       // warp 0 packs the group's active queries
         int base = 0;
         for (int t0 = 0; t0 < kQG; t0 += 32) {
             const int t = t0 + threadIdx.x;
             int dl = -1;
-            if (t < nqg) {
-                dl = delta[(int64_t)(q0 + t) * m + j];
+            if (t < nqg) dl = delta[(int64_t)(q0 + t) * m + j];
+            if (t < kQG) scnt[t] = 0;
+            const unsigned bal = __ballot_sync(NR_FULL, dl >= 0);
+            if (dl >= 0) {
+                uint32_t *r = srec[base + __popc(bal & lanemask_lt())];
 #pragma unroll
                 for (int w = 0; w < W; ++w)   // (per-sub-dataset A_j: the code under A_j)
-                    sq[t][w] = qcodes[((int64_t)(q0 + t) * QM + (QM > 1 ? j : 0)) * W + w];
+                    r[w] = qcodes[((int64_t)(q0 + t) * QM + (QM > 1 ? j : 0)) * W + w];
+                r[W] = (uint32_t)dl;
+                r[W + 1] = (uint32_t)t;
             }
-            sd[t] = dl;
-            scnt[t] = 0;
-            const unsigned bal = __ballot_sync(NR_FULL, dl >= 0);
-            if (dl >= 0) sact[base + __popc(bal & lanemask_lt())] = t;
             base += __popc(bal);
         }
         if (threadIdx.x == 0) s_nact = base;
@@ -424,19 +431,22 @@ __global__ void __launch_bounds__(kScanThreads) k6_scan(
         }
     }
     for (int ia = 0; ia < nact; ++ia) {
-        const int qq = sact[ia];
-        const int dl = sd[qq];
+        uint32_t rec[RW];
+        *reinterpret_cast<uint4 *>(rec) = *reinterpret_cast<const uint4 *>(srec[ia]);
+        if (RW == 8) *reinterpret_cast<uint4 *>(rec + 4) = *reinterpret_cast<const uint4 *>(srec[ia] + 4);
+        const int dl = (int)rec[W];
+        const int qq = (int)rec[W + 1];
         uint32_t qc[W];
 #pragma unroll
-        for (int w = 0; w < W; ++w) qc[w] = sq[qq][w];
-        uint32_t mask = 0, hp = 0;   // pass bits; h of the passing items, 8 bits each (first 4)
+        for (int w = 0; w < W; ++w) qc[w] = rec[w];
         int hh[kScanIPT];
+        uint32_t fail = 0;   // bit u: h_u > delta (the sign of delta - h_u)
 #pragma unroll
-        for (int u = 0; u < kScanIPT; ++u) {
+        for (int u = kScanIPT - 1; u >= 0; --u) {
             hh[u] = hamming<W>(c[u], qc);
-            mask |= (uint32_t)(hh[u] <= dl) << u;
+            fail = __funnelshift_l((uint32_t)(dl - hh[u]), fail, 1);
         }
-        mask &= vmask;
+        const uint32_t mask = ~fail & vmask;
         if (!__any_sync(NR_FULL, mask != 0u)) continue;
         // warp prefix sum of the pass counts -> one shared reservation per warp
         const int np = __popc(mask);
@@ -458,7 +468,6 @@ __global__ void __launch_bounds__(kScanThreads) k6_scan(
         gbase = __shfl_sync(NR_FULL, gbase, 31);
         const uint32_t glo = max(base, (uint32_t)kSB);
         uint32_t slot = base + inc - np;
-        (void)hp;
 #pragma unroll
         for (int u = 0; u < kScanIPT; ++u) {
             if (!(mask >> u & 1u)) continue;
