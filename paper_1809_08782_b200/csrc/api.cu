@@ -133,7 +133,8 @@ void free_index(nrlsh_index *ix) {
     void *ps[] = {ix->X_owned, ix->Xpad, ix->Xb, ix->xnorm, ix->norm2, ix->perm, ix->pos_of_id, ix->part_of_id,
                   ix->part_of_pos, ix->offsets_d, ix->V_d, ix->codes, ix->A, ix->Apad,
                   ix->R_d, ix->chunks_d, ix->order_d, ix->samp_codes, ix->samp_part,
-                  ix->tiles_d, ix->xnorm_pos, ix->tile_xmax, ix->codes_pm, ix->ctiles_d};
+                  ix->tiles_d, ix->xnorm_pos, ix->tile_xmax, ix->codes_pm, ix->ctiles_d,
+                  ix->bs_planes, ix->bs_gdesc, ix->bs_chunks};
     // pool-backed (cudaMallocAsync at build); the index may have been used on any stream
     cudaDeviceSynchronize();
     for (void *p : ps)
@@ -495,6 +496,30 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
         for (int64_t p = ix->offsets[j]; p < ix->offsets[j + 1]; p += 128)
             ctiles.push_back(make_int4(j, (int)p, (int)std::min<int64_t>(p + 128, ix->offsets[j + 1]), 0));
     ix->nctiles = (int32_t)ctiles.size();
+    // bit-sliced scan (L <= 64): groups of 32 positions per sub-dataset, work units of
+    // scan_bs_groups_per_chunk() groups
+    std::vector<int2> gdesc;
+    std::vector<int4> bchunks;
+    const bool want_bs = L <= 64 && QM == 1 && getenv("NRLSH_SCAN_BS") && atoi(getenv("NRLSH_SCAN_BS")) != 0;
+    if (want_bs) {
+        const int GPC = scan_bs_groups_per_chunk();
+        for (int j = 0; j < m; ++j) {
+            const int64_t gs = (int64_t)gdesc.size();
+            for (int64_t p = ix->offsets[j]; p < ix->offsets[j + 1]; p += 32)
+                gdesc.push_back(make_int2((int)p, (int)std::min<int64_t>(32, ix->offsets[j + 1] - p)));
+            const int64_t ge = (int64_t)gdesc.size();
+            for (int64_t gg = gs; gg < ge; gg += GPC)
+                bchunks.push_back(make_int4(j, (int)gg, (int)std::min<int64_t>(gg + GPC, ge),
+                                            (int)(ix->offsets[j] + 32 * (gg - gs))));
+        }
+        ix->bs_G = (int64_t)gdesc.size();
+        ix->bs_nchunks = (int32_t)bchunks.size();
+        NR_ALLOC(ix->bs_gdesc, gdesc.size() * sizeof(int2));
+        NR_ALLOC(ix->bs_chunks, bchunks.size() * sizeof(int4));
+        NR_ALLOC(ix->bs_planes, (size_t)32 * W * ix->bs_G * 4);
+        cudaMemcpyAsync(ix->bs_gdesc, gdesc.data(), gdesc.size() * sizeof(int2), cudaMemcpyHostToDevice, s);
+        cudaMemcpyAsync(ix->bs_chunks, bchunks.data(), bchunks.size() * sizeof(int4), cudaMemcpyHostToDevice, s);
+    }
     NR_ALLOC(ix->ctiles_d, ctiles.size() * sizeof(int4));
     NR_ALLOC(ix->R_d, ix->R_h.size() * 2);
     NR_ALLOC(ix->order_d, order.size() * 4);
@@ -514,6 +539,7 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
     {
         ProfScope p(SLOT_CODES, s);
         if (ix->codes_pm) launch_expand_pm(ix->codes, n, W, L, ix->codes_pm, s);
+        if (ix->bs_planes) launch_transpose_groups(ix->codes, ix->bs_gdesc, ix->bs_G, W, ix->bs_planes, s);
         // compacted pilot sample (query-time pilots read it contiguously)
         const int stride = pilot_stride(n);
         if (stride > 1) {
@@ -600,7 +626,10 @@ void run_candidates(const nrlsh_index *ix, const float *Qd, const uint32_t *qcod
             cudaMemsetAsync(cntv, 0, (size_t)Qb * 4, s);
             if (launch_scan_tc(ix, qcodes, delta, Qb, blk_act, buf, cnt, cntv, C, pairs, s)) tc = false;
         }
-        if (!tc) launch_scan(ix, qcodes, delta, Qb, buf, cnt, C, pairs, s);
+        if (!tc) {
+            if (scan_bs_supported(ix)) launch_scan_bs(ix, qcodes, delta, Qb, buf, cnt, C, pairs, s, blk_act);
+            else launch_scan(ix, qcodes, delta, Qb, buf, cnt, C, pairs, s);
+        }
     }
     {
         ProfScope p(SLOT_FALLBACK, s);
@@ -690,7 +719,8 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
     DBuf qc, dl, cn, cv, ba, bf, cd, pt, fl, fbw;
     if (qc.alloc((size_t)Qmax * ix->QM * ix->W * 4, s) || dl.alloc((size_t)Qmax * ix->m, s) ||
         cn.alloc((size_t)Qmax * 4, s) || cv.alloc((size_t)Qmax * 4, s) ||
-        ba.alloc(scan_tc_supported(ix) ? scan_tc_ws_bytes(ix, Qmax) : 16, s) ||
+        ba.alloc(scan_tc_supported(ix) ? scan_tc_ws_bytes(ix, Qmax)
+                                       : (scan_bs_supported(ix) ? scan_bs_ws_bytes(ix, Qmax) : 16), s) ||
         bf.alloc((size_t)Qmax * C * 8, s) ||
         cd.alloc((size_t)Qmax * Tq * 4, s) ||
         pt.alloc(want_topk ? rerank_partial_bytes(Qmax, Tq, k) : 0, s) || fl.alloc(48, s) ||
@@ -1275,6 +1305,10 @@ nrlsh_status nrlsh_set_codes(nrlsh_index *ix, const uint32_t *codes) {
     if (ix->codes_pm) {   // keep the tensor-core scan's +-1 rows in step
         launch_expand_pm(ix->codes, ix->n, ix->W, ix->L, ix->codes_pm, nullptr);
         if ((e = cudaDeviceSynchronize())) return cuda_fail(e, "set codes (+-1 rows)");
+    }
+    if (ix->bs_planes) {   // keep the bit-sliced planes in step with the codes
+        launch_transpose_groups(ix->codes, ix->bs_gdesc, ix->bs_G, ix->W, ix->bs_planes, nullptr);
+        if ((e = cudaDeviceSynchronize())) return cuda_fail(e, "set codes (planes)");
     }
     if (ix->samp_codes) {   // keep the pilot sample in step with the codes
         launch_gather_sample(ix, pilot_stride(ix->n), ix->samp_codes, ix->samp_part, nullptr);

@@ -54,6 +54,11 @@ struct nrlsh_index {
     int32_t ntiles = 0;
     int32_t *order_d = nullptr;     // [m*(L+1)] structure position -> j*(L+1)+h
     int32_t nchunks = 0;
+    uint32_t *bs_planes = nullptr;  // bit-sliced scan (L <= 64): [32W x bs_G] planes of the
+    int64_t bs_G = 0;               //   groups of 32 positions of one sub-dataset
+    int2 *bs_gdesc = nullptr;       //   [bs_G] (first position, items)
+    int4 *bs_chunks = nullptr;      //   work units (j, g0, g1, first position)
+    int32_t bs_nchunks = 0;
     uint32_t *samp_codes = nullptr; // pilot sample: codes of positions t * stride (compacted)
     uint8_t *samp_part = nullptr;
     int64_t nsamp = 0;
@@ -151,6 +156,15 @@ void launch_pilot(const nrlsh_index *ix, const uint32_t *qcodes, int Qb, int64_t
 void launch_scan(const nrlsh_index *ix, const uint32_t *qcodes, const int8_t *delta, int Qb,
                  unsigned long long *buf, uint32_t *cnt, int64_t C,
                  unsigned long long *pairs, cudaStream_t s);
+// bit-sliced scan (scan_bs.cu): codes of <= 64 bits, same appends as launch_scan
+int scan_bs_groups_per_chunk();
+bool scan_bs_supported(const nrlsh_index *ix);
+void launch_transpose_groups(const uint32_t *codes, const int2 *gdesc, int64_t G, int W, uint32_t *planes,
+                             cudaStream_t s);
+size_t scan_bs_ws_bytes(const nrlsh_index *ix, int Qb);
+void launch_scan_bs(const nrlsh_index *ix, const uint32_t *qcodes, const int8_t *delta, int Qb,
+                    unsigned long long *buf, uint32_t *cnt, int64_t C, unsigned long long *pairs,
+                    cudaStream_t s, void *ws);
 // cntv: entries of the buffer that are real (the tensor-core scan pads append
 // chunks with ~0 sentinels); == cnt for the popcount scan
 // ws: fallback_ws_bytes() of zeroed scratch for the all-SM re-do of failed queries

@@ -543,17 +543,21 @@ def test_full_size_sampled(name, L, m):
         assert_topk_match(gt_ids[qi], gt_sc[qi], a, s, X, Q[qi])
 
 
-@pytest.mark.parametrize("scan", ["tensor", "popcount"])
+@pytest.mark.parametrize("scan", ["tensor", "popcount", "bitsliced"])
 @pytest.mark.parametrize("case", [("c4", 300_000, 32, 64, 128), ("scale", 70_000, 16, 128, 256),
                                   ("tiny", None, None, 32, 8), ("c4", 300_000, 32, 32, 4),
                                   ("c3", 40_000, 64, 64, 1)], ids=_ids)
 def test_candidates_parity_both_scans(built, case, scan, monkeypatch):
-    """Both Hamming scans — the popcount one (the default) and the tcgen05 int8 one
-    (scan_tc.cu, NRLSH_SCAN_TC=1) — give the oracle's candidate sets, ranks and
+    """The Hamming scans — the popcount one (the default), the tcgen05 int8 one
+    (scan_tc.cu, NRLSH_SCAN_TC=1) and the bit-sliced one (scan_bs.cu, NRLSH_SCAN_BS=1)
+    — give the oracle's candidate sets, ranks and
     (R, id) order (identical codes injected), across budgets from 1 to n."""
     monkeypatch.setenv("NRLSH_SCAN_TC", "1" if scan == "tensor" else "0")
+    monkeypatch.setenv("NRLSH_SCAN_BS", "1" if scan == "bitsliced" else "0")
     cfg, X, Q, Xd, idx, orc = built(*case)
-    if scan == "tensor":   # its +-1 code rows are made at build time (opt-in)
+    if scan == "bitsliced" and case[3] > 64:
+        pytest.skip("the bit-sliced scan covers codes of <= 64 bits")
+    if scan != "popcount":   # their code layouts are made at build time (opt-in)
         idx = _P().Index(Xd, case[3], case[4], seed=cfg.seed)
     n = X.shape[0]
     ocodes = orc.codes()
