@@ -792,7 +792,7 @@ __global__ void __launch_bounds__(1024) k7_select(
     uint16_t *__restrict__ cand_rank, int mode, int L, uint32_t *__restrict__ sel_B,
     uint32_t *__restrict__ sel_pk, uint32_t *__restrict__ cnt_part,
     const uint8_t *__restrict__ dense, uint32_t *__restrict__ ncand_out,
-    int32_t *__restrict__ seeds, int ks) {
+    int32_t *__restrict__ seeds, int ks, const int32_t *__restrict__ order) {
     pdl_wait();
     extern __shared__ uint32_t hist[];   // [max(NR, tie_cap)] + R copy [NR] (uint16)
     uint16_t *sRt = reinterpret_cast<uint16_t *>(hist + tie_cap);
@@ -825,11 +825,12 @@ __global__ void __launch_bounds__(1024) k7_select(
     for (int e = threadIdx.x; e < NR; e += blockDim.x) { hist[e] = 0u; sRt[e] = R[e]; }
     if (threadIdx.x == 0) { sB = NR - 1; sLt = 0; s_out = 0; s_bseed = NR - 1; }
     __syncthreads();
-    // entries carry the flat (j, h) index; R maps it to the structure position
-    // (~0 = unused append slot of the tensor-core scan)
+    // entries carry the flat (j, h) index f; the histogram is kept per f (one shared
+    // atomic per entry, no R lookup), and the bound walks the structure through its
+    // inverse order[] (~0 = unused append slot of the tensor-core scan)
     for (int64_t e = threadIdx.x; e < c; e += blockDim.x) {
         const uint32_t f = (uint32_t)(b[e] >> 32);
-        if (f < (uint32_t)NR) atomicAdd(&hist[sRt[f]], 1u);
+        if (f < (uint32_t)NR) atomicAdd(&hist[f], 1u);
     }
     __syncthreads();
     const uint32_t need = (uint32_t)Tq;
@@ -837,44 +838,40 @@ __global__ void __launch_bounds__(1024) k7_select(
         const int seg = (NR + blockDim.x - 1) / blockDim.x;
         const int r0 = threadIdx.x * seg, r1 = min(NR, r0 + seg);
         uint32_t loc = 0;
-        for (int r = r0; r < r1; ++r) loc += hist[r];
+        for (int r = r0; r < r1; ++r) loc += hist[__ldg(order + r)];
         uint32_t tot;
         const uint32_t ex = block_excl_scan(loc, ws, &tot);
         if (ex < need && ex + loc >= need) {
             uint32_t cc = ex;
             for (int r = r0; r < r1; ++r) {
-                if (cc + hist[r] >= need) { sB = r; sLt = cc; break; }
-                cc += hist[r];
+                const uint32_t hr = hist[__ldg(order + r)];
+                if (cc + hr >= need) { sB = r; sLt = cc; break; }
+                cc += hr;
             }
         }
-        __syncthreads();
-    }
-    if (seeds) {   // structure position holding the ks-th best-ranked entry
-        const int seg = (NR + blockDim.x - 1) / blockDim.x;
-        const int r0 = threadIdx.x * seg, r1 = min(NR, r0 + seg);
-        uint32_t loc = 0;
-        for (int r = r0; r < r1; ++r) loc += hist[r];
-        uint32_t tot;
-        const uint32_t ex = block_excl_scan(loc, ws, &tot);
-        if (ex < (uint32_t)ks && ex + loc >= (uint32_t)ks) {
-            uint32_t cc = ex;
-            for (int r = r0; r < r1; ++r) {
-                if (cc + hist[r] >= (uint32_t)ks) { s_bseed = r; break; }
-                cc += hist[r];
+        if (seeds) {   // structure position holding the ks-th best-ranked entry
+            if (ex < (uint32_t)ks && ex + loc >= (uint32_t)ks) {
+                uint32_t cc = ex;
+                for (int r = r0; r < r1; ++r) {
+                    const uint32_t hr = hist[__ldg(order + r)];
+                    if (cc + hr >= (uint32_t)ks) { s_bseed = r; break; }
+                    cc += hr;
+                }
             }
         }
         __syncthreads();
     }
     const uint32_t B = (uint32_t)sB;
+    const uint32_t fB = (uint32_t)__ldg(order + B);   // the flat (j, h) cell at the bound
     const uint32_t need_eq = need - sLt;
-    const uint32_t n_eq = hist[B];
+    const uint32_t n_eq = hist[fB];
     if (cnt_part) {   // the query's candidates per sub-dataset (hist is still intact here)
         const int m = NR / (L + 1);
         for (int j = threadIdx.x; j < m; j += blockDim.x) {
             uint32_t cj = 0;
             for (int h = 0; h <= L; ++h) {
-                const uint32_t r = sRt[j * (L + 1) + h];
-                cj += r < B ? hist[r] : (r == B ? min(need_eq, n_eq) : 0u);
+                const uint32_t f = j * (L + 1) + h, r = sRt[f];
+                cj += r < B ? hist[f] : (r == B ? min(need_eq, n_eq) : 0u);
             }
             if (cj) atomicAdd(&cnt_part[j], cj);
         }
@@ -897,9 +894,8 @@ __global__ void __launch_bounds__(1024) k7_select(
             const unsigned long long v = b[e];
             const uint32_t f = (uint32_t)(v >> 32);
             if (f >= (uint32_t)NR) continue;
-            const uint32_t r = sRt[f];
-            if (r == B) teq[atomicAdd(&s_out, 1u)] = (uint32_t)v;
-            else if (merge_seeds && r <= Bsd) {
+            if (f == fB) teq[atomicAdd(&s_out, 1u)] = (uint32_t)v;
+            else if (merge_seeds && sRt[f] <= Bsd) {
                 const uint32_t slot = atomicAdd(&s_seed, 1u);
                 if (slot < (uint32_t)ks) seeds[(int64_t)q * ks + slot] = perm[(uint32_t)v];
             }
@@ -951,7 +947,7 @@ __global__ void __launch_bounds__(1024) k7_select(
             for (int64_t e = threadIdx.x; e < c; e += blockDim.x) {
                 const unsigned long long v = b[e];
                 const uint32_t f = (uint32_t)(v >> 32);
-                if (f >= (uint32_t)NR || sRt[f] != B) continue;
+                if (f != fB) continue;
                 const uint32_t pos = (uint32_t)v;
                 if (shift < 24 && (pos >> (shift + 8)) != (pfx >> (shift + 8))) continue;
                 atomicAdd(&h256[(pos >> shift) & 255u], 1u);
@@ -1019,7 +1015,7 @@ void launch_select(const nrlsh_index *ix, int Qb, int64_t Tq, const unsigned lon
     const size_t sm = (size_t)tie_cap * 4 + (size_t)NR * 2;
     cudaFuncSetAttribute(k7_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     launch_pdl(k7_select, dim3(Qb), dim3(1024), sm, s, buf, cnt, C, Tq, NR, tie_cap, ix->R_d, ix->perm, cand, cand_rank,
-                                   0, ix->L, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0);
+                                   0, ix->L, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0, ix->order_d);
     note_launch();
 }
 
@@ -1033,7 +1029,7 @@ void launch_select_split(const nrlsh_index *ix, int Qb, int64_t Tq, const unsign
     const size_t sm = (size_t)tie_cap * 4 + (size_t)NR * 2;
     cudaFuncSetAttribute(k7_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     launch_pdl(k7_select, dim3(Qb), dim3(1024), sm, s, buf, cnt, C, Tq, NR, tie_cap, ix->R_d, ix->perm, cand, nullptr,
-                                   mode, ix->L, sel_B, sel_pk, cnt_part, dense, ncand_out, nullptr, 0);
+                                   mode, ix->L, sel_B, sel_pk, cnt_part, dense, ncand_out, nullptr, 0, ix->order_d);
     note_launch();
 }
 
@@ -1045,7 +1041,7 @@ void launch_select_seeds(const nrlsh_index *ix, int Qb, int64_t Tq, const unsign
     const size_t sm = (size_t)tie_cap * 4 + (size_t)NR * 2;
     cudaFuncSetAttribute(k7_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     launch_pdl(k7_select, dim3(Qb), dim3(1024), sm, s, buf, cnt, C, Tq, NR, tie_cap, ix->R_d, ix->perm, nullptr, nullptr,
-                                   1, ix->L, sel_B, sel_pk, nullptr, nullptr, nullptr, seeds, ks);
+                                   1, ix->L, sel_B, sel_pk, nullptr, nullptr, nullptr, seeds, ks, ix->order_d);
     note_launch();
 }
 
