@@ -696,6 +696,7 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
     int64_t C = buffer_capacity(Tq, stride, n, max_part);
     int Qmax = (int)std::min<int64_t>(ix->query_batch, nq);
     if (scan_tc_supported(ix)) C += scan_tc_slack(Qmax);   // (its runs' unused tails)
+    C = (C + 1) & ~(int64_t)1;   // even: 16-byte-aligned buffer rows (the select's paired loads)
     // keep the candidate buffers bounded (~2.5 GB)
     const int64_t per_q = C * 8 + Tq * 10;
     while (Qmax > 64 && (int64_t)Qmax * per_q > (int64_t)2500 << 20) Qmax >>= 1;

@@ -828,9 +828,36 @@ __global__ void __launch_bounds__(1024) k7_select(
     // entries carry the flat (j, h) index f; the histogram is kept per f (one shared
     // atomic per entry, no R lookup), and the bound walks the structure through its
     // inverse order[] (~0 = unused append slot of the tensor-core scan)
-    for (int64_t e = threadIdx.x; e < c; e += blockDim.x) {
-        const uint32_t f = (uint32_t)(b[e] >> 32);
-        if (f < (uint32_t)NR) atomicAdd(&hist[f], 1u);
+    if ((C & 1) == 0) {   // 8 entries in flight per thread: 16-byte loads of entry pairs
+        const int64_t c2 = c / 2;
+        const ulonglong2 *b2 = reinterpret_cast<const ulonglong2 *>(b);
+        int64_t e2 = threadIdx.x;
+        for (; e2 + 3 * (int64_t)blockDim.x < c2; e2 += 4 * (int64_t)blockDim.x) {
+            ulonglong2 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = b2[e2 + u * (int64_t)blockDim.x];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t f0 = (uint32_t)(v[u].x >> 32), f1 = (uint32_t)(v[u].y >> 32);
+                if (f0 < (uint32_t)NR) atomicAdd(&hist[f0], 1u);
+                if (f1 < (uint32_t)NR) atomicAdd(&hist[f1], 1u);
+            }
+        }
+        for (; e2 < c2; e2 += blockDim.x) {
+            const ulonglong2 v = b2[e2];
+            const uint32_t f0 = (uint32_t)(v.x >> 32), f1 = (uint32_t)(v.y >> 32);
+            if (f0 < (uint32_t)NR) atomicAdd(&hist[f0], 1u);
+            if (f1 < (uint32_t)NR) atomicAdd(&hist[f1], 1u);
+        }
+        if ((c & 1) && threadIdx.x == 0) {
+            const uint32_t f = (uint32_t)(b[c - 1] >> 32);
+            if (f < (uint32_t)NR) atomicAdd(&hist[f], 1u);
+        }
+    } else {
+        for (int64_t e = threadIdx.x; e < c; e += blockDim.x) {
+            const uint32_t f = (uint32_t)(b[e] >> 32);
+            if (f < (uint32_t)NR) atomicAdd(&hist[f], 1u);
+        }
     }
     __syncthreads();
     const uint32_t need = (uint32_t)Tq;
@@ -890,15 +917,34 @@ __global__ void __launch_bounds__(1024) k7_select(
     if (threadIdx.x == 0) s_seed = 0;
     __syncthreads();
     if (in_smem) {
-        for (int64_t e = threadIdx.x; e < c; e += blockDim.x) {
-            const unsigned long long v = b[e];
+        auto take = [&](unsigned long long v) {
             const uint32_t f = (uint32_t)(v >> 32);
-            if (f >= (uint32_t)NR) continue;
+            if (f >= (uint32_t)NR) return;
             if (f == fB) teq[atomicAdd(&s_out, 1u)] = (uint32_t)v;
             else if (merge_seeds && sRt[f] <= Bsd) {
                 const uint32_t slot = atomicAdd(&s_seed, 1u);
                 if (slot < (uint32_t)ks) seeds[(int64_t)q * ks + slot] = perm[(uint32_t)v];
             }
+        };
+        if ((C & 1) == 0) {   // (paired 16-byte loads, 8 entries in flight per thread)
+            const int64_t c2 = c / 2;
+            const ulonglong2 *b2 = reinterpret_cast<const ulonglong2 *>(b);
+            int64_t e2 = threadIdx.x;
+            for (; e2 + 3 * (int64_t)blockDim.x < c2; e2 += 4 * (int64_t)blockDim.x) {
+                ulonglong2 v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) v[u] = b2[e2 + u * (int64_t)blockDim.x];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) { take(v[u].x); take(v[u].y); }
+            }
+            for (; e2 < c2; e2 += blockDim.x) {
+                const ulonglong2 v = b2[e2];
+                take(v.x);
+                take(v.y);
+            }
+            if ((c & 1) && threadIdx.x == 0) take(b[c - 1]);
+        } else {
+            for (int64_t e = threadIdx.x; e < c; e += blockDim.x) take(b[e]);
         }
         __syncthreads();
         for (int shift = 24; shift >= 0; shift -= 8) {
