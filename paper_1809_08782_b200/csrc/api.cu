@@ -420,7 +420,7 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
         if (QM == 1)
             launch_item_codes(ix->X, n, d, ix->norm2, ix->part_of_id, ix->V_d, ix->Apad, L, W,
                               ix->pos_of_id, ix->codes, ix->Xb, ix->dpb, ix->xnorm, ix->Xpad,
-                              ix->dpad, s, ix->perm);
+                              ix->dpad, s, ix->perm, m);
         // |x| in partition order (the tensor-core filter's tiles) and the first-pass split
         // of those tiles: the 1/800 (at least 16) with the largest |x| (c4: 0.15 vs 0.18 ms
         // per 1024 seeded queries at 1/50, 0.37 vs 0.74 unseeded; the first pass's exact

@@ -953,10 +953,10 @@ void launch_item_codes(const float *X, int64_t n, int d, const double *norm2,
                        const uint8_t *part, const double *V, const float *Apad, int L, int W,
                        const int32_t *pos_of_id, uint32_t *codes, void *Xb, int dpb,
                        float *xnorm, float *Xpad, int dpad, cudaStream_t s,
-                       const int32_t *perm) {
+                       const int32_t *perm, int m) {
     if (codes_tc_supported(d, W)) {
         launch_item_codes_tc(X, n, d, norm2, part, V, Apad, L, W, pos_of_id, codes, Xb, dpb, Xpad,
-                             dpad, s);
+                             dpad, s, nullptr, 0, nullptr, m);
         return;
     }
     // SIMT path: the row copies in separate passes

@@ -118,7 +118,7 @@ void launch_item_codes(const float *X, int64_t n, int d, const double *norm2,
                        const uint8_t *part_of_id, const double *V_d, const float *Apad,
                        int L, int W, const int32_t *pos_of_id, uint32_t *codes, void *Xb,
                        int dpb, float *xnorm, float *Xpad, int dpad, cudaStream_t s,
-                       const int32_t *perm);
+                       const int32_t *perm, int m);
 
 // K3 on tcgen05 (codes_tc.cu); the SIMT kernel above covers the other shapes
 bool codes_tc_supported(int d, int W);
@@ -129,7 +129,7 @@ void launch_item_codes_tc(const float *X, int64_t n, int d, const double *norm2,
                           int L, int W, const int32_t *pos_of_id, uint32_t *codes, void *Xb,
                           int dpb, float *Xpad, int dpad, cudaStream_t s,
                           const int4 *ctiles = nullptr, int nctiles = 0,
-                          const int32_t *perm = nullptr);
+                          const int32_t *perm = nullptr, int m = 0);
 
 // ---------------------------------------------------------------- query
 struct QueryWS {

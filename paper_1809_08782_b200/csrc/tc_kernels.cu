@@ -80,7 +80,7 @@ static EncodeTiledFn encode_fn() {
 }
 
 // 2-D row-major [rows x cols] of `esize`-byte elements, box {box_cols, box_rows},
-// 128-byte (default) or 64-byte swizzle
+// 128-byte (default), 64-byte or (0) no swizzle
 bool make_tmap_2d(CUtensorMap *m, const void *base, CUtensorMapDataType dt, int esize,
                   uint64_t cols, uint64_t rows, uint32_t box_cols, uint32_t box_rows, int swizzle) {
     EncodeTiledFn fn = encode_fn();
@@ -91,7 +91,8 @@ bool make_tmap_2d(CUtensorMap *m, const void *base, CUtensorMapDataType dt, int 
     cuuint32_t es[2] = {1, 1};
     CUresult r = fn(m, dt, 2, const_cast<void *>(base), dims, strides, box, es,
                     CU_TENSOR_MAP_INTERLEAVE_NONE,
-                    swizzle == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                    swizzle == 0 ? CU_TENSOR_MAP_SWIZZLE_NONE
+                                 : (swizzle == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B),
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
