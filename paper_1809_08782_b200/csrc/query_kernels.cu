@@ -377,7 +377,8 @@ __global__ void __launch_bounds__(kScanThreads) k6_scan(
     const uint32_t *__restrict__ codes, const int4 *__restrict__ chunks,
     const uint32_t *__restrict__ qcodes, const int8_t *__restrict__ delta, int Qb, int m,
     const uint16_t *__restrict__ R, int L, unsigned long long *__restrict__ buf,
-    uint32_t *__restrict__ cnt, int64_t C, unsigned long long *__restrict__ pairs, int QM) {
+    uint32_t *__restrict__ cnt, int64_t C, unsigned long long *__restrict__ pairs, int QM,
+    int probe = 0) {
     pdl_wait();
     constexpr int RW = W <= 2 ? 4 : 8;             // record words: codes, radius, query
     __shared__ __align__(16) uint32_t srec[kQG][RW];
@@ -415,8 +416,9 @@ __global__ void __launch_bounds__(kScanThreads) k6_scan(
     __syncthreads();
     const int nact = s_nact;
     if (nact == 0) return;
-    if (threadIdx.x == 0 && pairs) atomicAdd(pairs, (unsigned long long)nact * (p1 - p0));
+    if (threadIdx.x == 0 && pairs && !probe) atomicAdd(pairs, (unsigned long long)nact * (p1 - p0));
     const int lane = threadIdx.x & 31;
+    uint32_t nprobe = 0;   // (probe: the XOR/POPC/threshold work alone, no appends)
     uint32_t c[kScanIPT][W];
     uint32_t vmask = 0;   // bit u: item u of this thread exists
 #pragma unroll
@@ -447,6 +449,7 @@ __global__ void __launch_bounds__(kScanThreads) k6_scan(
             fail = __funnelshift_l((uint32_t)(dl - hh[u]), fail, 1);
         }
         const uint32_t mask = ~fail & vmask;
+        if (probe) { nprobe += __popc(mask); continue; }
         if (!__any_sync(NR_FULL, mask != 0u)) continue;
         // warp prefix sum of the pass counts -> one shared reservation per warp
         const int np = __popc(mask);
@@ -483,6 +486,10 @@ __global__ void __launch_bounds__(kScanThreads) k6_scan(
             ++slot;
         }
     }
+    if (probe) {
+        if (nprobe) atomicAdd((unsigned int *)pairs, nprobe);
+        return;
+    }
     __syncthreads();
     for (int t = threadIdx.x; t < nqg; t += blockDim.x) {
         const uint32_t nst = min(scnt[t], (uint32_t)kSB);
@@ -511,11 +518,21 @@ void launch_scan(const nrlsh_index *ix, const uint32_t *qcodes, const int8_t *de
     const int64_t ngroups = (Qb + kQG - 1) / kQG;
     const unsigned grid = (unsigned)(ix->nchunks * ngroups);
     switch (ix->W) {
-        case 1: launch_pdl(k6_scan<1>, dim3(grid), dim3(kScanThreads), 0, s, ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs, ix->QM); break;
-        case 2: launch_pdl(k6_scan<2>, dim3(grid), dim3(kScanThreads), 0, s, ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs, ix->QM); break;
-        default: launch_pdl(k6_scan<4>, dim3(grid), dim3(kScanThreads), 0, s, ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs, ix->QM); break;
+        case 1: launch_pdl(k6_scan<1>, dim3(grid), dim3(kScanThreads), 0, s, ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs, ix->QM, 0); break;
+        case 2: launch_pdl(k6_scan<2>, dim3(grid), dim3(kScanThreads), 0, s, ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs, ix->QM, 0); break;
+        default: launch_pdl(k6_scan<4>, dim3(grid), dim3(kScanThreads), 0, s, ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs, ix->QM, 0); break;
     }
     note_launch();
+    if (getenv("NRLSH_SCAN_PROBE")) {   // experiment: time the scan without its appends
+        static unsigned long long *dummy = nullptr;
+        if (!dummy) cudaMalloc(&dummy, 8);
+        ProfScope p(SLOT_OTHER, s);
+        switch (ix->W) {
+            case 1: k6_scan<1><<<grid, kScanThreads, 0, s>>>(ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, dummy, ix->QM, 1); break;
+            case 2: k6_scan<2><<<grid, kScanThreads, 0, s>>>(ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, dummy, ix->QM, 1); break;
+            default: k6_scan<4><<<grid, kScanThreads, 0, s>>>(ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, dummy, ix->QM, 1); break;
+        }
+    }
 }
 
 int scan_chunk_items() { return kChunk; }
