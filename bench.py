@@ -168,12 +168,18 @@ def roofline_for(slot, ms_total, count, info, peaks, peaks_src):
     traffic = info.get("traffic", {}).get(slot)
     if slot == "scan":
         # L/32 POPC per (query, item) pair the scan must evaluate;
-        # pairs of sub-datasets whose radius is < 0 are skipped exactly.
-        ops = info["scanned_pairs"] * W / count
+        # pairs of sub-datasets whose radius is < 0 are skipped exactly.  POPCs issued:
+        # W per pair, minus the W/2 the one-POPC-per-word-pair lower bound saves on the
+        # pairs it decides alone, plus W/2 on the pairs where it ran and did not
+        ops = (info["scanned_pairs"] * W - info["lb_decided_pairs"] * W
+               + info["lb_pairs"] * (W // 2)) / count
         ach = ops / per_launch_s
         return {"bound": "alu", "kernel": "k6_scan (XOR+POPC Hamming scan + metric filter)",
                 "achieved": ach / 1e12, "peak": POPC_PEAK_PER_S / 1e12, "unit": "TPOPC/s",
                 "frac": ach / POPC_PEAK_PER_S, "traffic": traffic,
+                "popc_per_pair": ops * count / max(1, info["scanned_pairs"]),
+                "pairs_decided_per_s": info["scanned_pairs"] / (ms_total / 1e3),
+                "pairs_decided_frac": info["scanned_pairs"] * W / (ms_total / 1e3) / POPC_PEAK_PER_S,
                 "peak_source": "tools/ubench.cu measured POPC rate (profiles/r01/ubench_popc.txt)",
                 "logical_pairs_per_s": nq * n * steps / (ms_total / 1e3),
                 # SURVEY §8(d) "code-scan GB/s": code bytes compared (all n items per query)
@@ -348,6 +354,7 @@ def measure_path(P, torch, cfg, L, m, T, Xd, Qd, steps, warmup, stream, flush, d
             ev[1].record(stream)
         ids, sc = idx.query(Qd, k, T)
         qstats = P.last_query_stats()
+        qstats.update(P.last_scan_stats())
         rinfo = P.last_rerank_path()
         if ev:
             ev[2].record(stream)
@@ -366,7 +373,8 @@ def measure_path(P, torch, cfg, L, m, T, Xd, Qd, steps, warmup, stream, flush, d
     P.profile_read(reset=True)
     P.profile_enable(True)
     launches0 = P.launch_count()
-    acc = {"scanned_pairs": 0, "buffer_entries": 0, "fallback_queries": 0, "rerank_filter_pairs": 0,
+    acc = {"scanned_pairs": 0, "lb_pairs": 0, "lb_decided_pairs": 0, "buffer_entries": 0,
+           "fallback_queries": 0, "rerank_filter_pairs": 0,
            "rerank_overflow": 0, "gt_filter_pairs": 0, "gt_survivors": 0}
     evs = []
     if dist:
@@ -378,6 +386,8 @@ def measure_path(P, torch, cfg, L, m, T, Xd, Qd, steps, warmup, stream, flush, d
         ids, gid, qstats, rinfo, gstats = step(ev)
         evs.append(ev)
         acc["scanned_pairs"] += qstats["scanned_pairs"]
+        acc["lb_pairs"] += qstats["bound_pairs"]
+        acc["lb_decided_pairs"] += qstats["bound_decided_pairs"]
         acc["buffer_entries"] += qstats["buffer_entries"]
         acc["fallback_queries"] += qstats["fallback_queries"]
         acc["rerank_filter_pairs"] += rinfo["filter_pairs"]
@@ -398,6 +408,7 @@ def measure_path(P, torch, cfg, L, m, T, Xd, Qd, steps, warmup, stream, flush, d
     return {"ms_all": ms, "ms_step": float(np.mean(ms)),
             "build_ms": float(np.mean([e[0].elapsed_time(e[1]) for e in evs])),
             "query_ms": float(np.mean([e[1].elapsed_time(e[2]) for e in evs])),
+            "query_ms_all": [e[1].elapsed_time(e[2]) for e in evs],
             "gt_ms": float(np.mean([e[2].elapsed_time(e[3]) for e in evs])),
             "prof": prof, "launches": launches, "acc": acc, "recall_at_k": rec,
             "recall_at_10": rec10, "rerank_path": rinfo["path"]}
@@ -409,7 +420,8 @@ def rooflines(r, cfg, L, m, nq, T, steps, peaks, peaks_src):
     prof, acc = r["prof"], r["acc"]
     W = 1 if L <= 32 else (2 if L <= 64 else 4)
     info = {"n": cfg.n, "d": cfg.d, "L": L, "W": W, "nq": nq, "T": T, "k": cfg.k, "m": m,
-            "scanned_pairs": acc["scanned_pairs"], "traffic": load_traffic(), "steps": steps,
+            "scanned_pairs": acc["scanned_pairs"], "lb_pairs": acc["lb_pairs"],
+            "lb_decided_pairs": acc["lb_decided_pairs"], "traffic": load_traffic(), "steps": steps,
             "rerank_path": r["rerank_path"], "rerank_filter_pairs": acc["rerank_filter_pairs"],
             "gt_filter_pairs": acc["gt_filter_pairs"],
             "score_bytes": float(nq) * T * cfg.d * 4.0 * steps, "gt_tensor": True}
@@ -435,8 +447,8 @@ def rooflines(r, cfg, L, m, nq, T, steps, peaks, peaks_src):
     t_codes = 2.0 * nq * d * L / FFMA_PEAK_FLOPS
     t_scan_hbm = nsub * n * W * 4.0 / hbm
     t_sel = acc["buffer_entries"] / steps * 8.0 / hbm
-    def q_roof(pairs, rr_pairs):
-        t_scan = max(pairs * W / POPC_PEAK_PER_S, t_scan_hbm)
+    def q_roof(popcs, rr_pairs):
+        t_scan = max(popcs / POPC_PEAK_PER_S, t_scan_hbm)
         t_rr = rr_pairs * 2.0 * d / bf16
         t = t_codes + t_scan + t_sel + t_rr
         return {"t_roof_ms": t * 1e3, "frac": t * 1e3 / r["query_ms"],
@@ -444,10 +456,12 @@ def rooflines(r, cfg, L, m, nq, T, steps, peaks, peaks_src):
                              "rerank": t_rr * 1e3}}
     query = {"t_measured_ms": r["query_ms"],
              # every (query, item) pair scanned; every probed candidate scored on the tensor pipe
-             "logical": q_roof(float(nq) * n, float(nq) * T),
-             # the pairs the scan evaluated after exact sub-dataset skipping, the pairs
-             # the re-rank's filter multiplied
-             "actual": q_roof(acc["scanned_pairs"] / steps, acc["rerank_filter_pairs"] / steps),
+             "logical": q_roof(float(nq) * n * W, float(nq) * T),
+             # the POPCs the scan issued after exact sub-dataset skipping and the lower
+             # bound, the pairs the re-rank's filter multiplied
+             "actual": q_roof((acc["scanned_pairs"] * W - acc["lb_decided_pairs"] * W
+                               + acc["lb_pairs"] * (W // 2)) / steps,
+                              acc["rerank_filter_pairs"] / steps),
              "peaks": {"popc_per_s": POPC_PEAK_PER_S, "hbm_gbs": peaks["hbm_gbs"],
                        "bf16_tflops": bf16 / 1e12, "ffma_tflops": FFMA_PEAK_FLOPS / 1e12}}
     return roof, scan_roof, others, build, query
@@ -571,8 +585,8 @@ def run_native(args):
                              f"m={sm_}, {scfg.nq:,} queries (sub-batches of {scfg.query_batch}), "
                              f"top-{scfg.k}, T={sT:,}",
                  "value": scfg.nq / (rs["ms_step"] / 1e3), "unit": "queries/s",
-                 "ms_per_step": rs["ms_step"], "steps": args.scale_steps, "warmup": 2,
-                 "build_ms": rs["build_ms"], "query_ms": rs["query_ms"], "gt_ms": rs["gt_ms"],
+                 "ms_per_step": rs["ms_step"], "ms_all": rs["ms_all"], "steps": args.scale_steps,
+                 "warmup": 2, "query_ms_all": rs["query_ms_all"], "build_ms": rs["build_ms"], "query_ms": rs["query_ms"], "gt_ms": rs["gt_ms"],
                  "recall_at_100": rs["recall_at_k"], "recall_at_10": rs["recall_at_10"],
                  "scan_frac": sscan["frac"] if sscan else None, "build_frac": sbuild["frac"],
                  "build_roofline": sbuild, "query_roofline": squery, "roofline": sroof,

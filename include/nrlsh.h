@@ -171,11 +171,18 @@ nrlsh_status nrlsh_query_candidates(const nrlsh_index *index, const float *queri
 nrlsh_status nrlsh_last_query_stats(int64_t *fallback_queries, int64_t *kernel_launches,
                                     int64_t *scanned_pairs, int64_t *buffer_entries);
 
+/* Of the last nrlsh_query's scanned pairs on this thread (codes of >= 64 bits): the
+   pairs on which the scan first evaluated the lower bound h >= sum over word pairs
+   of popcount((x_a ^ q_a) | (x_b ^ q_b)) (radii delta_j(q) up to 16 for 64-bit
+   codes, 37 for 128-bit codes), and the pairs that bound decided alone (a warp's
+   256 items all above the radius: no exact distance needed, the same candidates as
+   without it).  Either may be NULL. */
+nrlsh_status nrlsh_last_scan_stats(int64_t *bound_pairs, int64_t *bound_decided_pairs);
+
 /* Candidates of the last nrlsh_query on this thread that the re-rank rescored in
    fp32 after a certified bf16 pass (the others provably could not enter the
    top-k; the answer is the same as rescoring all of them): the tensor-core
-   re-rank's survivor slots, or the opt-in bf16 gather pre-pass's survivors;
-   0 for the plain gather path. */
+   re-rank's survivor slots; 0 for the plain gather path. */
 nrlsh_status nrlsh_last_rerank_stats(int64_t *rescored_fp32);
 
 /* Which implementation re-ranked the last nrlsh_query on this thread (all return
@@ -189,16 +196,12 @@ nrlsh_status nrlsh_last_rerank_stats(int64_t *rescored_fp32);
                                keeping survivors that pass the select's candidate
                                rule, then the same fp32 re-rank of the survivors
                                (default when probe_budget >= n / 300 and a
-                               sub-batch's queries x probe_budget >= 1.28 n);
-     NRLSH_RERANK_DENSE        dense SIMT re-rank of hot sub-datasets (opt-in);
-     NRLSH_RERANK_GATHER_BF16  gather with a certified bf16 pre-pass (opt-in).
+                               sub-batch's queries x probe_budget >= 1.28 n).
    overflow_redone: queries whose tensor-core survivor list overflowed and were
    re-ranked by the gather path instead; filter_pairs: (query, item) pairs the
    tensor-core filter multiplied (0 on the other paths).  Any pointer may be NULL. */
 #define NRLSH_RERANK_GATHER 0
 #define NRLSH_RERANK_TENSOR 1
-#define NRLSH_RERANK_DENSE 2
-#define NRLSH_RERANK_GATHER_BF16 3
 nrlsh_status nrlsh_last_rerank_path(int32_t *path, int64_t *overflow_redone,
                                     int64_t *filter_pairs);
 

@@ -2,6 +2,7 @@
 // launch orchestration, and the two small host-side steps of the build (the
 // seeded projection matrix and the sorted (U_j, l) structure of PAPER:217).
 #include <algorithm>
+#include <chrono>
 #include <climits>
 #include <cmath>
 #include <cstdio>
@@ -24,6 +25,8 @@ thread_local int64_t g_last_fallbacks = 0;
 thread_local int64_t g_last_launches = 0;
 thread_local int64_t g_last_pairs = 0;
 thread_local int64_t g_last_entries = 0;       // candidate-buffer entries the select read
+thread_local int64_t g_last_lb_pairs = 0;       // pairs the scan's lower bound ran on
+thread_local int64_t g_last_lb_skipped = 0;     // ... and decided alone
 thread_local int64_t g_last_gt_pairs = 0;      // (query, item) pairs the exact filter multiplied
 thread_local int64_t g_last_rescored = 0;
 thread_local int64_t g_last_rtc_overflow = 0;   // tensor-core re-rank: queries redone by gather
@@ -133,8 +136,7 @@ void free_index(nrlsh_index *ix) {
     void *ps[] = {ix->X_owned, ix->Xpad, ix->Xb, ix->xnorm, ix->norm2, ix->perm, ix->pos_of_id, ix->part_of_id,
                   ix->part_of_pos, ix->offsets_d, ix->V_d, ix->codes, ix->A, ix->Apad,
                   ix->R_d, ix->chunks_d, ix->order_d, ix->samp_codes, ix->samp_part,
-                  ix->tiles_d, ix->xnorm_pos, ix->tile_xmax, ix->codes_pm, ix->ctiles_d,
-                  ix->bs_planes, ix->bs_gdesc, ix->bs_chunks};
+                  ix->xnorm_pos, ix->tile_xmax, ix->ctiles_d, ix->codes_pm};
     // pool-backed (cudaMallocAsync at build); the index may have been used on any stream
     cudaDeviceSynchronize();
     for (void *p : ps)
@@ -275,6 +277,14 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
         return fail(NRLSH_EINVAL, "hash bits L_h must be in [1,64] or [97,128] (got " +
                                       std::to_string(L) + ")");
     cudaStream_t s = (cudaStream_t)cuda_stream;
+    // (NRLSH_BUILD_TRACE=1: host timestamps of the build's phases on stderr)
+    const bool trace = getenv("NRLSH_BUILD_TRACE") != nullptr;
+    const auto t_start = std::chrono::steady_clock::now();
+    auto tr = [&](const char *what) {
+        if (trace)
+            fprintf(stderr, "[build] %8.1f us  %s\n",
+                    std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_start).count(), what);
+    };
 
     std::unique_ptr<nrlsh_index, void (*)(nrlsh_index *)> ix(new nrlsh_index(), free_index);
     ix->n = n;
@@ -311,6 +321,7 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
         if (e) return cuda_fail(e, "copy items");
         ix->X = ix->X_owned;
     }
+    tr("args");
     NR_ALLOC(ix->norm2, (size_t)n * 8);
     // bf16 rows (16-byte aligned, zero-padded to dpb) and |x| rounded up, written by the
     // norms pass: the ground truth's tensor-core operand and the re-rank's certified
@@ -337,28 +348,30 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
     NR_ALLOC(ix->xnorm_pos, (size_t)npad * 4);
     cudaMemsetAsync(ix->xnorm_pos + n, 0, (size_t)(npad - n) * 4, s);
     NR_ALLOC(ix->tile_xmax, (size_t)((n + 127) / 128) * 4);
-    // +-1 rows for the opt-in tensor-core scan (NRLSH_SCAN_TC=1 at build and query)
+    // +-1 rows for the opt-in tensor-core scan (NEXT-3; NRLSH_SCAN_TC=1 at build and query)
     if (L <= 128 && ix->QM == 1 && getenv("NRLSH_SCAN_TC") && atoi(getenv("NRLSH_SCAN_TC")) != 0)
         NR_ALLOC(ix->codes_pm, (size_t)n * scan_kp(L));
     NR_ALLOC(ix->offsets_d, (size_t)(m + 1) * 8);
     NR_ALLOC(ix->V_d, (size_t)m * 8);
-    NR_ALLOC(ix->codes, (size_t)n * W * 4 + 64);   // (+64: the scan's aligned bulk copies)
+    NR_ALLOC(ix->codes, (size_t)n * W * 4 + 1024);   // (+1 KB: the scans' aligned reads past the end)
 
     // One host round trip: the device steps of Alg. 1 are enqueued ahead of the host
     // work that depends on them.  Stream order: norms, partition, scatter, the
     // read-back of (offsets, V, flags) [event], codes and the |x| tiles; meanwhile the
     // host generates the projection (before the codes are enqueued) and, once the
     // event fires, builds its tables while the codes kernel runs.
+    tr("allocs");
     const int QM = ix->QM;
     const size_t ablk = (size_t)(d + 1) * L, pblk = (size_t)(d + 1) * 32 * W;
     NR_ALLOC(ix->A, (size_t)QM * ablk * 4);
     NR_ALLOC(ix->Apad, (size_t)QM * pblk * 4);
     // build flags: [0] first non-finite item (~0: none), [1] large percentile group,
     // [2] the filter's first-pass |x| split (float bits)
+    // [4], [5] the smallest positive and largest norm2 bits (the percentile select's window)
     DBuf res;
-    if (res.alloc(32, s)) return fail(NRLSH_ENOMEM, "cudaMallocAsync");
-    const unsigned long long res0[4] = {~0ull, 0ull, 0ull, 0ull};
-    cudaMemcpyAsync(res.p, res0, 32, cudaMemcpyHostToDevice, s);
+    if (res.alloc(48, s)) return fail(NRLSH_ENOMEM, "cudaMallocAsync");
+    const unsigned long long res0[6] = {~0ull, 0ull, 0ull, 0ull, ~0ull, 0ull};
+    cudaMemcpyAsync(res.p, res0, 48, cudaMemcpyHostToDevice, s);
     unsigned long long *resd = res.get<unsigned long long>();
     const int64_t ntx = (n + 127) / 128;   // 128-row |x| tiles
     ix->offsets.resize(m + 1);
@@ -387,9 +400,10 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
     auto partition_steps = [&](bool fast) -> nrlsh_status {
         std::string err;
         int rc;
+        bool have_mm = false;
         if (fast) {   // K1: norms + finite check
             ProfScope p(SLOT_NORMS, s);
-            launch_norms(ix->X, n, d, ix->norm2, resd, ix->Xb, ix->dpb, ix->xnorm, s);
+            have_mm = launch_norms(ix->X, n, d, ix->norm2, resd, ix->Xb, ix->dpb, ix->xnorm, s, resd + 4);
         }
         {   // K2: percentile (or uniform) partition
             ProfScope p(SLOT_PARTITION, s);
@@ -397,7 +411,8 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
                 rc = partition_uniform(ix->norm2, n, m, ix->part_of_id, s, &err);
             else if (fast)
                 rc = partition_percentile_fast(ix->norm2, n, m, ix->part_of_id,
-                                               reinterpret_cast<unsigned int *>(resd + 1), s, &err);
+                                               reinterpret_cast<unsigned int *>(resd + 1), s, &err,
+                                               have_mm ? resd + 4 : nullptr);
             else
                 rc = partition_percentile(ix->norm2, n, m, ix->part_of_id, s, &err);
         }
@@ -433,8 +448,10 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
             launch_select_kth_float(ix->tile_xmax, ntx, r, reinterpret_cast<float *>(resd + 2), s);
         }
     };
+    tr("pinned/event");
     nrlsh_status st = partition_steps(true);
     if (st) return st;
+    tr("partition enqueued");
     {   // K4a (host, overlapped with the partition): A_j from seed XOR j (A_0 = the
         // shared A); per-sub-dataset projections are m independent draws, on up to 16
         // host threads
@@ -461,9 +478,12 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
         cudaMemcpyAsync(ix->A, ix->A_h.data(), ix->A_h.size() * 4, cudaMemcpyHostToDevice, s);
         cudaMemcpyAsync(ix->Apad, Apad.data(), Apad.size() * 4, cudaMemcpyHostToDevice, s);
     }
+    tr("projection");
     code_steps();
+    tr("codes enqueued");
     cudaError_t e = cudaEventSynchronize(ev_part);
     if (e) return cuda_fail(e, "build");
+    tr("partition done (event)");
     if (hres[0] != ~0ull)
         return fail(NRLSH_ENONFINITE, "non-finite item at index " + std::to_string(hres[0]));
     if (hres[1]) {   // (ties or duplicates: a boundary group needs the multi-level select)
@@ -486,12 +506,6 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
         for (int64_t p = ix->offsets[j]; p < ix->offsets[j + 1]; p += CH)
             chunks.push_back(make_int4(j, (int)p, (int)std::min<int64_t>(p + CH, ix->offsets[j + 1]), 0));
     ix->nchunks = (int32_t)chunks.size();
-    // tensor-core scan tiles: <= 256 consecutive positions inside one sub-dataset
-    std::vector<int4> tiles;
-    for (int j = 0; j < m; ++j)
-        for (int64_t p = ix->offsets[j]; p < ix->offsets[j + 1]; p += 256)
-            tiles.push_back(make_int4(j, (int)p, (int)std::min<int64_t>(p + 256, ix->offsets[j + 1]), 0));
-    ix->ntiles = (int32_t)tiles.size();
     // tiles of <= 128 positions of one sub-dataset: the code kernel's with per-sub-
     // dataset projections, the (opt-in) tensor-core scan's items
     std::vector<int4> ctiles;
@@ -499,40 +513,14 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
         for (int64_t p = ix->offsets[j]; p < ix->offsets[j + 1]; p += 128)
             ctiles.push_back(make_int4(j, (int)p, (int)std::min<int64_t>(p + 128, ix->offsets[j + 1]), 0));
     ix->nctiles = (int32_t)ctiles.size();
-    // bit-sliced scan (L <= 64): groups of 32 positions per sub-dataset, work units of
-    // scan_bs_groups_per_chunk() groups
-    std::vector<int2> gdesc;
-    std::vector<int4> bchunks;
-    const bool want_bs = L <= 64 && QM == 1 && getenv("NRLSH_SCAN_BS") && atoi(getenv("NRLSH_SCAN_BS")) != 0;
-    if (want_bs) {
-        const int GPC = scan_bs_groups_per_chunk();
-        for (int j = 0; j < m; ++j) {
-            const int64_t gs = (int64_t)gdesc.size();
-            for (int64_t p = ix->offsets[j]; p < ix->offsets[j + 1]; p += 32)
-                gdesc.push_back(make_int2((int)p, (int)std::min<int64_t>(32, ix->offsets[j + 1] - p)));
-            const int64_t ge = (int64_t)gdesc.size();
-            for (int64_t gg = gs; gg < ge; gg += GPC)
-                bchunks.push_back(make_int4(j, (int)gg, (int)std::min<int64_t>(gg + GPC, ge),
-                                            (int)(ix->offsets[j] + 32 * (gg - gs))));
-        }
-        ix->bs_G = (int64_t)gdesc.size();
-        ix->bs_nchunks = (int32_t)bchunks.size();
-        NR_ALLOC(ix->bs_gdesc, gdesc.size() * sizeof(int2));
-        NR_ALLOC(ix->bs_chunks, bchunks.size() * sizeof(int4));
-        NR_ALLOC(ix->bs_planes, (size_t)32 * W * ix->bs_G * 4);
-        cudaMemcpyAsync(ix->bs_gdesc, gdesc.data(), gdesc.size() * sizeof(int2), cudaMemcpyHostToDevice, s);
-        cudaMemcpyAsync(ix->bs_chunks, bchunks.data(), bchunks.size() * sizeof(int4), cudaMemcpyHostToDevice, s);
-    }
     NR_ALLOC(ix->ctiles_d, ctiles.size() * sizeof(int4));
     NR_ALLOC(ix->R_d, ix->R_h.size() * 2);
     NR_ALLOC(ix->order_d, order.size() * 4);
     NR_ALLOC(ix->chunks_d, chunks.size() * sizeof(int4));
-    NR_ALLOC(ix->tiles_d, tiles.size() * sizeof(int4));
     cudaMemcpyAsync(ix->ctiles_d, ctiles.data(), ctiles.size() * sizeof(int4), cudaMemcpyHostToDevice, s);
     cudaMemcpyAsync(ix->R_d, ix->R_h.data(), ix->R_h.size() * 2, cudaMemcpyHostToDevice, s);
     cudaMemcpyAsync(ix->order_d, order.data(), order.size() * 4, cudaMemcpyHostToDevice, s);
     cudaMemcpyAsync(ix->chunks_d, chunks.data(), chunks.size() * sizeof(int4), cudaMemcpyHostToDevice, s);
-    cudaMemcpyAsync(ix->tiles_d, tiles.data(), tiles.size() * sizeof(int4), cudaMemcpyHostToDevice, s);
     if (QM > 1) {   // K3 with per-sub-dataset projections: partition-ordered tiles
         ProfScope p(SLOT_CODES, s);
         launch_item_codes_tc(ix->X, n, d, ix->norm2, ix->part_of_id, ix->V_d, ix->Apad, L, W,
@@ -542,22 +530,22 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
     {
         ProfScope p(SLOT_CODES, s);
         if (ix->codes_pm) launch_expand_pm(ix->codes, n, W, L, ix->codes_pm, s);
-        if (ix->bs_planes) launch_transpose_groups(ix->codes, ix->bs_gdesc, ix->bs_G, W, ix->bs_planes, s);
         // compacted pilot sample (query-time pilots read it contiguously)
         const int stride = pilot_stride(n);
         if (stride > 1) {
-            // (interleaved slots: 32 columns of ceil(samples / 32); unused slots get
-            // sub-dataset 255, which no histogram bin takes)
+            // (interleaved slots: 32 columns of ceil(samples / 32) positions ~n/32
+            // apart; the pilot skips the slots past the sample)
             ix->nsamp = ((n + stride - 1) / stride + 31) / 32 * 32;
             NR_ALLOC(ix->samp_codes, (size_t)ix->nsamp * W * 4);
             NR_ALLOC(ix->samp_part, (size_t)ix->nsamp);
-            cudaMemsetAsync(ix->samp_part, 0xff, (size_t)ix->nsamp, s);
             launch_gather_sample(ix.get(), stride, ix->samp_codes, ix->samp_part, s);
         }
     }
+    tr("tables enqueued");
     cudaMemcpyAsync(hres + 2, resd + 2, 8, cudaMemcpyDeviceToHost, s);
     e = cudaStreamSynchronize(s);
     if (e) return cuda_fail(e, "codes");
+    tr("done (stream sync)");
     {
         float xs;
         const uint32_t xb = (uint32_t)hres[2];
@@ -601,10 +589,10 @@ int64_t buffer_capacity(int64_t Tq, int stride, int64_t n, int64_t max_part) {
 // The candidate pipeline for one sub-batch; leaves cand [Qb x Tq] (item ids).
 void run_candidates(const nrlsh_index *ix, const float *Qd, const uint32_t *qcodes_in, int Qb,
                     int64_t qbase, int64_t Tq, int stride, int64_t C, uint32_t *qcodes,
-                    int8_t *delta, uint32_t *cnt, uint32_t *cntv, uint8_t *blk_act,
+                    int8_t *delta, uint32_t *cnt, uint32_t *cntv, void *scan_ws,
                     unsigned long long *buf, int32_t *cand, uint16_t *cand_rank, int *flags,
                     unsigned long long *pairs, cudaStream_t s, uint32_t *sel_B = nullptr,
-                    uint32_t *sel_pk = nullptr, uint32_t *cnt_part = nullptr,
+                    uint32_t *sel_pk = nullptr,
                     int32_t *seeds = nullptr, int ks = 0, void *fb_ws = nullptr,
                     unsigned long long *entries = nullptr) {
     if (qcodes_in) {
@@ -627,12 +615,9 @@ void run_candidates(const nrlsh_index *ix, const float *Qd, const uint32_t *qcod
         // counted in cnt, real entries in cntv; a tensor-map failure falls back)
         if (tc) {
             cudaMemsetAsync(cntv, 0, (size_t)Qb * 4, s);
-            if (launch_scan_tc(ix, qcodes, delta, Qb, blk_act, buf, cnt, cntv, C, pairs, s)) tc = false;
+            if (launch_scan_tc(ix, qcodes, delta, Qb, scan_ws, buf, cnt, cntv, C, pairs, s)) tc = false;
         }
-        if (!tc) {
-            if (scan_bs_supported(ix)) launch_scan_bs(ix, qcodes, delta, Qb, buf, cnt, C, pairs, s, blk_act);
-            else launch_scan(ix, qcodes, delta, Qb, buf, cnt, C, pairs, s);
-        }
+        if (!tc) launch_scan(ix, qcodes, delta, Qb, buf, cnt, C, pairs, s, pairs + 4);
     }
     {
         ProfScope p(SLOT_FALLBACK, s);
@@ -644,10 +629,6 @@ void run_candidates(const nrlsh_index *ix, const float *Qd, const uint32_t *qcod
         ProfScope p(SLOT_SELECT, s);
         if (seeds) {   // bound pass + seed members (the tensor-core re-rank)
             launch_select_seeds(ix, Qb, Tq, buf, cnt, C, sel_B, sel_pk, seeds, ks, s);
-        } else if (sel_B) {   // bound pass only (the dense re-rank path emits later)
-            cudaMemsetAsync(cnt_part, 0, (size_t)ix->m * 4, s);
-            launch_select_split(ix, Qb, Tq, buf, cnt, C, 1, sel_B, sel_pk, cnt_part, nullptr,
-                                nullptr, nullptr, s);
         } else {
             launch_select(ix, Qb, Tq, buf, cnt, C, cand, cand_rank, s);
         }
@@ -723,28 +704,14 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
     DBuf qc, dl, cn, cv, ba, bf, cd, pt, fl, fbw;
     if (qc.alloc((size_t)Qmax * ix->QM * ix->W * 4, s) || dl.alloc((size_t)Qmax * ix->m, s) ||
         cn.alloc((size_t)Qmax * 4, s) || cv.alloc((size_t)Qmax * 4, s) ||
-        ba.alloc(scan_tc_supported(ix) ? scan_tc_ws_bytes(ix, Qmax)
-                                       : (scan_bs_supported(ix) ? scan_bs_ws_bytes(ix, Qmax) : 16), s) ||
-        bf.alloc((size_t)Qmax * C * 8, s) ||
+        ba.alloc(scan_tc_supported(ix) ? scan_tc_ws_bytes(ix, Qmax) : 16, s) || bf.alloc((size_t)Qmax * C * 8, s) ||
         cd.alloc((size_t)Qmax * Tq * 4, s) ||
-        pt.alloc(want_topk ? rerank_partial_bytes(Qmax, Tq, k) : 0, s) || fl.alloc(48, s) ||
+        pt.alloc(want_topk ? rerank_partial_bytes(Qmax, Tq, k) : 0, s) || fl.alloc(64, s) ||
         fbw.alloc(fallback_ws_bytes(ix), s))
         return fail(NRLSH_ENOMEM, "query workspace");
     cudaMemsetAsync(fbw.p, 0, fallback_ws_bytes(ix), s);   // (histogram rows stay zero between uses)
-    // dense re-rank of the sub-datasets most of whose pairs are candidates (rerank_dense.cu)
     const float *Xr = ix->Xpad ? ix->Xpad : ix->X;
     const int ldr = ix->Xpad ? ix->dpad : ix->d;
-    const bool use_dense = want_topk && ix->QM == 1 && dense_rerank_supported(ldr, ix->W, k);
-    const int S = use_dense ? dense_splits(Qmax) : 0;
-    DBuf sb, spk, cpart, dmask, dinf, nco, gid, gsc, dpart;
-    if (use_dense &&
-        (sb.alloc((size_t)Qmax * 4, s) || spk.alloc((size_t)Qmax * 4, s) ||
-         cpart.alloc((size_t)ix->m * 4, s) || dmask.alloc((size_t)ix->m, s) ||
-         dinf.alloc((size_t)(2 * ix->m + 2) * 4, s) || nco.alloc((size_t)Qmax * 4, s) ||
-         gid.alloc((size_t)Qmax * k * 8, s) || gsc.alloc((size_t)Qmax * k * 4, s) ||
-         dpart.alloc((size_t)Qmax * S * k * 8, s)))
-        return fail(NRLSH_ENOMEM, "query workspace (dense re-rank)");
-    const float dense_frac = getenv("NRLSH_DENSE_FRAC") ? (float)atof(getenv("NRLSH_DENSE_FRAC")) : 0.10f;
     // tensor-core re-rank (tc_kernels.cu member mode): a bf16 GEMM pass over the
     // tiles of the sub-datasets holding candidates, certified filter, keeping only
     // candidates; chosen when the candidate budget is a large enough share of n
@@ -756,7 +723,7 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
     const char *rtc_env = getenv("NRLSH_RERANK_TC");
     const double rtc_ratio = getenv("NRLSH_RERANK_TC_RATIO") ? atof(getenv("NRLSH_RERANK_TC_RATIO")) : 300.0;
     const double rtc_qt = getenv("NRLSH_RERANK_TC_QT") ? atof(getenv("NRLSH_RERANK_TC_QT")) : 1.28;
-    const bool use_rtc = want_topk && !use_dense && !g_in_rtc_redo && ix->Xb && ix->xnorm_pos &&
+    const bool use_rtc = want_topk && !g_in_rtc_redo && ix->Xb && ix->xnorm_pos &&
                          gt_tc_supported(ix->d, k) &&
                          (rtc_env ? atoi(rtc_env) != 0
                                   : (double)Tq * rtc_ratio >= (double)n &&
@@ -798,8 +765,10 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
     tls.xsplit = getenv("NRLSH_RERANK_TWOPASS") ? ix->tile_xsplit : 0.f;
     tls.pass = 0;
     tls.qperm = nullptr;
-    const int init_flags[12] = {INT_MAX, INT_MAX, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-    cudaMemcpyAsync(fl.p, init_flags, 48, cudaMemcpyHostToDevice, s);
+    // [0, 1] non-finite / zero query, [2] fallbacks, [4:5] scanned pairs, [6:7] re-scored,
+    // [8:9] filter pairs, [10:11] buffer entries, [12:13] / [14:15] lower-bound pairs
+    const int init_flags[16] = {INT_MAX, INT_MAX, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyAsync(fl.p, init_flags, 64, cudaMemcpyHostToDevice, s);
     unsigned long long *pairs = (unsigned long long *)(fl.get<int>() + 4);
     const long long launches0 = launch_count();
     for (int64_t q0 = 0; q0 < nq; q0 += Qmax) {
@@ -809,11 +778,10 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
         uint16_t *crank = (cand_out && rank_out) ? (uint16_t *)orr.dev + q0 * Tq : nullptr;
         run_candidates(ix, Qd, qcodes_user ? (const uint32_t *)QCs.dev : nullptr, Qb, q0, Tq,
                        stride, C, qc.get<uint32_t>(), dl.get<int8_t>(), cn.get<uint32_t>(),
-                       cv.get<uint32_t>(), ba.get<uint8_t>(), bf.get<unsigned long long>(), cand,
+                       cv.get<uint32_t>(), ba.p, bf.get<unsigned long long>(), cand,
                        crank, fl.get<int>(), pairs, s,
-                       use_dense ? sb.get<uint32_t>() : (use_rtc ? rsb.get<uint32_t>() : nullptr),
-                       use_dense ? spk.get<uint32_t>() : (use_rtc ? rspk.get<uint32_t>() : nullptr),
-                       use_dense ? cpart.get<uint32_t>() : nullptr,
+                       use_rtc ? rsb.get<uint32_t>() : nullptr,
+                       use_rtc ? rspk.get<uint32_t>() : nullptr,
                        use_rtc ? rseed.get<int32_t>() : nullptr, KS, fbw.p,
                        (unsigned long long *)(fl.get<int>() + 10));
         if (use_rtc) {
@@ -867,41 +835,11 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
                                     rovn.get<uint32_t>(), s);
             // survivors re-scored in fp32 (incl. the unused slots of their last chunk)
             launch_sum_counts(rcc.get<uint32_t>(), Qb, Cg, (unsigned long long *)(fl.get<int>() + 6), s);
-        } else if (use_dense) {
-            {
-                ProfScope p(SLOT_SELECT, s);
-                launch_dense_decide(cpart.get<uint32_t>(), ix->offsets_d, ix->m, Qb, dense_frac,
-                                    dmask.get<uint8_t>(), dinf.get<int32_t>(), s);
-                launch_select_split(ix, Qb, Tq, bf.get<unsigned long long>(), cn.get<uint32_t>(),
-                                    C, 2, sb.get<uint32_t>(), spk.get<uint32_t>(), nullptr,
-                                    dmask.get<uint8_t>(), cand, nco.get<uint32_t>(), s);
-            }
-            {
-                ProfScope p(SLOT_RERANK, s);
-                launch_rerank(Xr, ix->d, ldr, Qd, Qb, cand, Tq, Tq, nco.get<uint32_t>(), 1, k,
-                              pt.get<unsigned long long>(), gid.get<int64_t>(), gsc.get<float>(),
-                              s);
-            }
-            ProfScope p(SLOT_RERANK_TOPK, s);
-            launch_rerank_dense(Xr, ldr, ix->d, Qd, qc.get<uint32_t>(), sb.get<uint32_t>(),
-                                spk.get<uint32_t>(), ix, Qb, k, dinf.get<int32_t>(),
-                                dpart.get<unsigned long long>(), S, s);
-            launch_dense_merge(dpart.get<unsigned long long>(), S, k, gid.get<int64_t>(),
-                               gsc.get<float>(), Qb, (int64_t *)oi.dev + q0 * k,
-                               (float *)os.dev + q0 * k, s);
         } else if (want_topk) {
             ProfScope p(SLOT_RERANK, s);
-            if (ix->Xb && getenv("NRLSH_RERANK_BF16"))
-                launch_rerank_bf(ix->Xpad ? ix->Xpad : ix->X, ix->d, ix->Xpad ? ix->dpad : ix->d,
-                                 ix->Xb, ix->dpb, ix->xnorm, Qd, Qb, cand, Tq, Tq,
-                                 nullptr, k, pt.get<unsigned long long>(),
-                                 (int64_t *)oi.dev + q0 * k, (float *)os.dev + q0 * k,
-                                 (unsigned long long *)(fl.get<int>() + 6), s, ix->pos_of_id);
-            else
-                launch_rerank(ix->Xpad ? ix->Xpad : ix->X, ix->d, ix->Xpad ? ix->dpad : ix->d, Qd,
-                              Qb, cand, Tq, Tq, nullptr, 1, k,
-                              pt.get<unsigned long long>(), (int64_t *)oi.dev + q0 * k,
-                              (float *)os.dev + q0 * k, s);
+            launch_rerank(Xr, ix->d, ldr, Qd, Qb, cand, Tq, Tq, nullptr, 1, k,
+                          pt.get<unsigned long long>(), (int64_t *)oi.dev + q0 * k,
+                          (float *)os.dev + q0 * k, s);
         }
     }
     if (use_rtc) {   // queries whose survivor list overflowed (rare): the gather path
@@ -935,8 +873,8 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
         if ((e = oc.finish(s))) return cuda_fail(e, "copy candidates");
         if (rank_out && (e = orr.finish(s))) return cuda_fail(e, "copy ranks");
     }
-    int hflags[12];
-    cudaMemcpyAsync(hflags, fl.p, 48, cudaMemcpyDeviceToHost, s);
+    int hflags[16];
+    cudaMemcpyAsync(hflags, fl.p, 64, cudaMemcpyDeviceToHost, s);
     e = cudaStreamSynchronize(s);
     if (e) return cuda_fail(e, "query");
     e = cudaGetLastError();
@@ -951,13 +889,14 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
     g_last_rescored = (int64_t)pr;
     std::memcpy(&pr, hflags + 10, 8);
     g_last_entries = (int64_t)pr;
+    std::memcpy(&pr, hflags + 12, 8);
+    g_last_lb_pairs = (int64_t)pr;
+    std::memcpy(&pr, hflags + 14, 8);
+    g_last_lb_skipped = (int64_t)pr;
     std::memcpy(&pr, hflags + 8, 8);
     if (!g_in_rtc_redo) g_last_rtc_pairs = (int64_t)pr;
     if (!g_in_rtc_redo)
-        g_last_rtc = use_rtc ? NRLSH_RERANK_TENSOR
-                             : (use_dense ? NRLSH_RERANK_DENSE
-                                          : (ix->Xb && getenv("NRLSH_RERANK_BF16") ? NRLSH_RERANK_GATHER_BF16
-                                                                               : NRLSH_RERANK_GATHER));
+        g_last_rtc = use_rtc ? NRLSH_RERANK_TENSOR : NRLSH_RERANK_GATHER;
     return check_flags(hflags);
 }
 
@@ -1022,6 +961,12 @@ nrlsh_status nrlsh_last_query_stats(int64_t *fallback_queries, int64_t *kernel_l
     if (fallback_queries) *fallback_queries = g_last_fallbacks;
     if (kernel_launches) *kernel_launches = g_last_launches;
     if (scanned_pairs) *scanned_pairs = g_last_pairs;
+    return NRLSH_OK;
+}
+
+nrlsh_status nrlsh_last_scan_stats(int64_t *bound_pairs, int64_t *bound_decided_pairs) {
+    if (bound_pairs) *bound_pairs = g_last_lb_pairs;
+    if (bound_decided_pairs) *bound_decided_pairs = g_last_lb_skipped;
     return NRLSH_OK;
 }
 
@@ -1309,10 +1254,6 @@ nrlsh_status nrlsh_set_codes(nrlsh_index *ix, const uint32_t *codes) {
     if (ix->codes_pm) {   // keep the tensor-core scan's +-1 rows in step
         launch_expand_pm(ix->codes, ix->n, ix->W, ix->L, ix->codes_pm, nullptr);
         if ((e = cudaDeviceSynchronize())) return cuda_fail(e, "set codes (+-1 rows)");
-    }
-    if (ix->bs_planes) {   // keep the bit-sliced planes in step with the codes
-        launch_transpose_groups(ix->codes, ix->bs_gdesc, ix->bs_G, ix->W, ix->bs_planes, nullptr);
-        if ((e = cudaDeviceSynchronize())) return cuda_fail(e, "set codes (planes)");
     }
     if (ix->samp_codes) {   // keep the pilot sample in step with the codes
         launch_gather_sample(ix, pilot_stride(ix->n), ix->samp_codes, ix->samp_part, nullptr);

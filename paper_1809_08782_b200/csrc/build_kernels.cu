@@ -84,8 +84,11 @@ __global__ void __launch_bounds__(128) k1_norms_bulk(const float *__restrict__ X
                                                      int RT, double *__restrict__ norm2,
                                                      unsigned long long *__restrict__ bad,
                                                      __nv_bfloat16 *__restrict__ Xb, int dpb,
-                                                     float *__restrict__ xnorm) {
+                                                     float *__restrict__ xnorm,
+                                                     unsigned long long *__restrict__ mm) {
     extern __shared__ __align__(128) float nbuf[];       // [2][RT * d]
+    // (mm: smallest positive and largest key bits, for the percentile select's window)
+    unsigned long long klo = ~0ull, khi = 0ull;
     __shared__ __align__(8) uint64_t full[2];
     const int64_t ntiles = (n + RT - 1) / RT;
     const int skew = (d % 2 == 0) ? 1 : 0;
@@ -150,6 +153,9 @@ __global__ void __launch_bounds__(128) k1_norms_bulk(const float *__restrict__ X
             }
             if (r < rows) {
                 norm2[r0 + r] = s;
+                const unsigned long long kb = (unsigned long long)__double_as_longlong(s);
+                if (kb != 0ull) klo = kb < klo ? kb : klo;
+                khi = kb > khi ? kb : khi;
                 if (!isfinite(s)) atomicMin(bad, (unsigned long long)(r0 + r));
                 // |x| rounded up (with a 2^-50 margin over the fp64 sum's rounding):
                 // an upper bound for the certified bf16 filters
@@ -161,10 +167,22 @@ __global__ void __launch_bounds__(128) k1_norms_bulk(const float *__restrict__ X
         if (threadIdx.x == 0 && tile + 2 * (int64_t)gridDim.x < ntiles)
             issue(tile + 2 * (int64_t)gridDim.x, st);
     }
+    if (mm) {
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long l2 = __shfl_xor_sync(NR_FULL, klo, o);
+            const unsigned long long h2 = __shfl_xor_sync(NR_FULL, khi, o);
+            klo = l2 < klo ? l2 : klo;
+            khi = h2 > khi ? h2 : khi;
+        }
+        if (lane == 0) {
+            if (klo != ~0ull) atomicMin(&mm[0], klo);
+            atomicMax(&mm[1], khi);
+        }
+    }
 }
 
-void launch_norms(const float *X, int64_t n, int d, double *norm2, unsigned long long *bad,
-                  void *Xb, int dpb, float *xnorm, cudaStream_t s) {
+bool launch_norms(const float *X, int64_t n, int d, double *norm2, unsigned long long *bad,
+                  void *Xb, int dpb, float *xnorm, cudaStream_t s, unsigned long long *mm) {
     const int ld = (d % 2 == 1) ? d : d + 1;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -178,9 +196,9 @@ void launch_norms(const float *X, int64_t n, int d, double *norm2, unsigned long
         const int64_t ntiles = (n + RT - 1) / RT;
         const int per_sm = std::max(1, (int)((227 * 1024) / (sm + 1024)));
         const int grid = (int)std::min<int64_t>(ntiles, (int64_t)sms * per_sm);
-        k1_norms_bulk<<<grid, RT, sm, s>>>(X, n, d, RT, norm2, bad, nullptr, dpb, xnorm);
+        k1_norms_bulk<<<grid, RT, sm, s>>>(X, n, d, RT, norm2, bad, nullptr, dpb, xnorm, mm);
         note_launch();
-        return;
+        return mm != nullptr;
     }
     const size_t lim = 200 * 1024;
     if ((size_t)256 * ld * 4 <= lim / 2) {
@@ -199,6 +217,7 @@ void launch_norms(const float *X, int64_t n, int d, double *norm2, unsigned long
         k1_norms_direct<<<grid_for(n, 256, sms * 8), 256, 0, s>>>(X, n, d, norm2, bad);
     }
     note_launch();
+    return false;
 }
 
 // =========================================================================== K2
@@ -505,42 +524,260 @@ struct DevBuf {
 };
 }  // namespace
 
+// ---------------------------------------------------------------- windowed level 0
+// The device-decided level 0 bins the fp64 key by its bits above `shift` relative to
+// the smallest positive key (zeros, the only keys below it, go to bin 0 — the binning
+// stays monotone).  shift >= 40 (12 mantissa bits: ~80 items per bin at the mode of a
+// lognormal(0, 1) norm law on 2.3M items) is raised until the keys' range fits
+// 2^kWinBits bins, so the histogram is 1 MB instead of the 2^24 bins of a fixed digit.
+constexpr int kWinBits = 18;
+constexpr int kWinFinePerCoarse = 1024;
+constexpr int kWinCoarse = (1 << kWinBits) / kWinFinePerCoarse;   // 256
+
+__device__ __forceinline__ void win_params(const unsigned long long *mm, int &shift,
+                                           unsigned long long &base) {
+    unsigned long long lo = mm[0], hi = mm[1];
+    if (lo == ~0ull) lo = 0ull;   // (no positive key)
+    if (hi < lo) hi = lo;
+    int sh = 40;
+    while (((hi >> sh) - (lo >> sh)) >= (1ull << kWinBits)) ++sh;
+    shift = sh;
+    base = lo >> sh;
+}
+
+__device__ __forceinline__ uint32_t win_bin(unsigned long long key, int shift, unsigned long long base) {
+    const unsigned long long b = key >> shift;
+    return b < base ? 0u : (uint32_t)(b - base);
+}
+
+// mm[0] = smallest positive key (init ~0), mm[1] = largest key (init 0)
+__global__ void win_minmax(const double *__restrict__ norm2, int64_t n, unsigned long long *__restrict__ mm) {
+    unsigned long long lo = ~0ull, hi = 0ull;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long b = (unsigned long long)__double_as_longlong(norm2[i]);
+        if (b != 0ull) lo = b < lo ? b : lo;
+        hi = b > hi ? b : hi;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long l2 = __shfl_xor_sync(NR_FULL, lo, o);
+        const unsigned long long h2 = __shfl_xor_sync(NR_FULL, hi, o);
+        lo = l2 < lo ? l2 : lo;
+        hi = h2 > hi ? h2 : hi;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (lo != ~0ull) atomicMin(&mm[0], lo);
+        atomicMax(&mm[1], hi);
+    }
+}
+
+// fine histogram H [2^kWinBits] (global atomics; keys in item order are spread over
+// the bins, so a warp's atomics rarely collide)
+__global__ void __launch_bounds__(256) win_hist(const double *__restrict__ norm2, int64_t n,
+                                                const unsigned long long *__restrict__ mm,
+                                                uint32_t *__restrict__ H) {
+    int shift;
+    unsigned long long base;
+    win_params(mm, shift, base);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(&H[win_bin((unsigned long long)__double_as_longlong(norm2[i]), shift, base)], 1u);
+}
+
+// coarse sums: CTA c adds the kWinFinePerCoarse fine counts of coarse bin c
+__global__ void __launch_bounds__(256) win_coarse(const uint32_t *__restrict__ H, uint32_t *__restrict__ Hc) {
+    __shared__ uint32_t ws[32];
+    const uint4 v = reinterpret_cast<const uint4 *>(H + (size_t)blockIdx.x * kWinFinePerCoarse)[threadIdx.x];
+    uint32_t tot;
+    block_excl_scan(v.x + v.y + v.z + v.w, ws, &tot);
+    if (threadIdx.x == 0) Hc[blockIdx.x] = tot;
+}
+
+// One CTA of 1024 threads.  Boundary j (first rank b_j = ceil(j n / m)) lies in the
+// coarse bin whose prefix brackets b_j and, inside it, in the fine bin a warp finds
+// by a prefix over the coarse bin's 1024 fine counts.  The bins a boundary falls
+// strictly inside become the groups (sorted later); bt/btg give every boundary's bin
+// and its group (-1: the boundary is the bin's first rank, the bin is not split).
+__global__ void __launch_bounds__(1024) win_locate(const uint32_t *__restrict__ H,
+                                                   const uint32_t *__restrict__ Hc, int64_t n, int m,
+                                                   SelGroup *__restrict__ groups,
+                                                   int64_t *__restrict__ meta,
+                                                   uint32_t *__restrict__ bt, int32_t *__restrict__ btg) {
+    __shared__ uint32_t ws[32];
+    __shared__ uint32_t pc[kWinCoarse];
+    __shared__ uint32_t sbin[kMaxParts], sP[kMaxParts];
+    __shared__ int32_t sg[kMaxParts];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t v = threadIdx.x < kWinCoarse ? Hc[threadIdx.x] : 0u;
+    const uint32_t ex = block_excl_scan(v, ws, nullptr);
+    if (threadIdx.x < kWinCoarse) pc[threadIdx.x] = ex;
+    __syncthreads();
+    for (int j = 1 + warp; j < m; j += 32) {
+        const uint32_t b = (uint32_t)(((int64_t)j * n + m - 1) / m);
+        int lo = 0, hi = kWinCoarse - 1;   // largest coarse bin with prefix <= b
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (pc[mid] <= b) lo = mid; else hi = mid - 1;
+        }
+        const uint4 *hf = reinterpret_cast<const uint4 *>(H + (size_t)lo * kWinFinePerCoarse + lane * 32);
+        uint32_t hv[32];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const uint4 x = hf[e];
+            hv[4 * e] = x.x; hv[4 * e + 1] = x.y; hv[4 * e + 2] = x.z; hv[4 * e + 3] = x.w;
+        }
+        uint32_t sum = 0;
+#pragma unroll
+        for (int e = 0; e < 32; ++e) sum += hv[e];
+        uint32_t inc = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(NR_FULL, inc, o);
+            if (lane >= o) inc += y;
+        }
+        const uint32_t lex = pc[lo] + inc - sum;   // rank of the first item of this lane's bins
+        if (lex <= b && b < lex + sum) {
+            uint32_t r = lex;
+            int e = 0;
+            for (; e < 31; ++e) {
+                if (b < r + hv[e]) break;
+                r += hv[e];
+            }
+            sbin[j] = (uint32_t)lo * kWinFinePerCoarse + lane * 32 + e;
+            sP[j] = r;
+        }
+    }
+    __syncthreads();
+    // a bin is split if some boundary lies strictly inside it; the boundaries of one
+    // bin are consecutive in j.  Group g = the g-th split bin (leader: its first
+    // boundary), its list at the exclusive sum of the earlier groups' counts.
+    const int j = threadIdx.x;
+    bool leader = false;
+    uint32_t cntb = 0;
+    if (j >= 1 && j < m) {
+        const uint32_t bn = sbin[j];
+        int j0 = j, j1 = j;
+        while (j0 > 1 && sbin[j0 - 1] == bn) --j0;
+        while (j1 + 1 < m && sbin[j1 + 1] == bn) ++j1;
+        bool split = false;
+        for (int jj = j0; jj <= j1; ++jj)
+            split |= sP[jj] < (uint32_t)(((int64_t)jj * n + m - 1) / m);
+        leader = split && j == j0;
+        sg[j] = split ? -2 - j0 : -1;   // (resolved to the leader's group below)
+        if (leader) cntb = H[bn];
+    }
+    uint32_t ng;
+    const uint32_t gi = block_excl_scan(leader ? 1u : 0u, ws, &ng);
+    uint32_t off_tot;
+    const uint32_t go = block_excl_scan(cntb, ws, &off_tot);
+    if (leader) {
+        groups[gi].bin = sbin[j];
+        groups[gi].count = cntb;
+        groups[gi].base = sP[j];
+        groups[gi].cand_off = go;
+        sP[j] = gi;   // (this boundary's rank is no longer needed: hand over the group)
+    }
+    __syncthreads();
+    if (j >= 1 && j < m) {
+        bt[j - 1] = sbin[j];
+        btg[j - 1] = sg[j] <= -2 ? (int32_t)sP[-2 - sg[j]] : -1;
+    }
+    if (j == 0) {
+        meta[0] = ng;
+        meta[1] = off_tot;
+    }
+}
+
+// Items of split bins go to their group's list; every other item's sub-dataset is the
+// number of boundaries whose bin is <= its bin (those all rank at or before it).
+__global__ void __launch_bounds__(256) win_classify(const double *__restrict__ norm2, int64_t n, int m,
+                                                    const unsigned long long *__restrict__ mm,
+                                                    const uint32_t *__restrict__ bt,
+                                                    const int32_t *__restrict__ btg,
+                                                    const SelGroup *__restrict__ groups,
+                                                    uint32_t *__restrict__ fill,
+                                                    uint64_t *__restrict__ out_keys,
+                                                    uint32_t *__restrict__ out_ids,
+                                                    uint8_t *__restrict__ part) {
+    __shared__ uint32_t sbt[kMaxParts];
+    __shared__ int32_t sbg[kMaxParts];
+    __shared__ int64_t goff[kMaxParts];
+    const int nb = m - 1;
+    for (int t = threadIdx.x; t < nb; t += blockDim.x) {
+        sbt[t] = bt[t];
+        const int g = btg[t];
+        sbg[t] = g;
+        if (g >= 0) goff[g] = groups[g].cand_off;
+    }
+    int shift;
+    unsigned long long base;
+    win_params(mm, shift, base);
+    __syncthreads();
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t key = (uint64_t)__double_as_longlong(norm2[i]);
+        const uint32_t b = win_bin(key, shift, base);
+        int lo = 0, hi = nb;   // number of boundary bins <= b
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (sbt[mid] <= b) lo = mid + 1; else hi = mid;
+        }
+        const int g = (lo > 0 && sbt[lo - 1] == b) ? sbg[lo - 1] : -1;
+        // (an item of a split bin gets its exact sub-dataset from the group sort; the
+        // provisional lo keeps part[] in range if that sort is left to the host's
+        // multi-level select — the scatter still runs on it before the redo)
+        part[i] = (uint8_t)lo;
+        if (g >= 0) {
+            const uint32_t slot = atomicAdd(&fill[g], 1u);
+            out_keys[goff[g] + slot] = key;
+            out_ids[goff[g] + slot] = (uint32_t)i;
+        }
+    }
+}
+
 // One level of the exact multi-select, decided on the device: the first digit's
 // histogram, the boundary groups, direct assignment outside them and an in-smem sort
 // of each group (<= kSmallGroup items; continuous norms — every BASELINE config —
 // leave only such groups).  No host synchronisation; *large (device) is set when a
 // group is larger, and the caller then runs partition_percentile.
 int partition_percentile_fast(const double *norm2, int64_t n, int m, uint8_t *part,
-                              unsigned int *large, cudaStream_t s, std::string *err) {
+                              unsigned int *large, cudaStream_t s, std::string *err,
+                              const unsigned long long *mm_in) {
     if (m == 1) {
         cudaMemsetAsync(part, 0, (size_t)n, s);
         return 0;
     }
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    const SelLevel lv = kLevels[0];
-    const int64_t nbins = 1ll << lv.width;
-    DevBuf H(s), P(s), TS(s), G(s), META(s), FILL(s), KB(s), IB(s);
-    if (H.alloc(nbins * 4) || P.alloc(nbins * 4) || TS.alloc(4096 * 4) ||
-        G.alloc(sizeof(SelGroup) * kMaxGroups) || META.alloc(16) || FILL.alloc(kMaxGroups * 4) ||
+    // zeroed scratch: [mm 16 B | Hc | fill | bt | btg | H]
+    const size_t hdr = 16 + (size_t)kWinCoarse * 4 + (size_t)kMaxGroups * 4 + 2 * (size_t)kMaxParts * 4;
+    const size_t zbytes = hdr + ((size_t)1 << kWinBits) * 4;
+    DevBuf Z(s), G(s), META(s), KB(s), IB(s);
+    if (Z.alloc(zbytes) || G.alloc(sizeof(SelGroup) * kMaxGroups) || META.alloc(16) ||
         KB.alloc((size_t)n * 8) || IB.alloc((size_t)n * 4)) {
         *err = "partition: cudaMalloc failed";
         return NRLSH_ENOMEM;
     }
-    cudaMemsetAsync(H.p, 0, nbins * 4, s);
-    cudaMemsetAsync(FILL.p, 0, kMaxGroups * 4, s);
-    const int grid = grid_for(n, 256, sms * 16);
-    sel_hist<true><<<grid, 256, 0, s>>>(norm2, nullptr, nullptr, n, lv.shift, lv.width, H.get<uint32_t>());
-    scan_excl(H.get<uint32_t>(), P.get<uint32_t>(), nbins, TS.get<uint32_t>(), s);
-    sel_locate<<<1, kMaxParts, 0, s>>>(H.get<uint32_t>(), P.get<uint32_t>(), nbins, 0, n, n, m,
-                                       G.get<SelGroup>(), META.get<int64_t>());
-    sel_classify<true><<<grid, 256, 0, s>>>(norm2, nullptr, nullptr, n, lv.shift, lv.width,
-                                            P.get<uint32_t>(), (int64_t)0, n, m, G.get<SelGroup>(),
-                                            META.get<int64_t>(), FILL.get<uint32_t>(),
-                                            KB.get<uint64_t>(), IB.get<uint32_t>(), part);
+    uint8_t *z = Z.get<uint8_t>();
+    unsigned long long *mm = (unsigned long long *)z;
+    uint32_t *Hc = (uint32_t *)(z + 16);
+    uint32_t *fill = Hc + kWinCoarse;
+    uint32_t *bt = fill + kMaxGroups;
+    int32_t *btg = (int32_t *)(bt + kMaxParts);
+    uint32_t *H = (uint32_t *)(z + hdr);
+    cudaMemsetAsync(z, 0, zbytes, s);
+    cudaMemsetAsync(z, 0xff, 8, s);
+    if (mm_in) mm = const_cast<unsigned long long *>(mm_in);   // (the norms pass's min / max)
+    else win_minmax<<<sms * 4, 256, 0, s>>>(norm2, n, mm);
+    const int grid = grid_for(n, 256, sms * 8);
+    win_hist<<<grid, 256, 0, s>>>(norm2, n, mm, H);
+    win_coarse<<<kWinCoarse, kWinFinePerCoarse / 4, 0, s>>>(H, Hc);
+    win_locate<<<1, 1024, 0, s>>>(H, Hc, n, m, G.get<SelGroup>(), META.get<int64_t>(), bt, btg);
+    win_classify<<<grid, 256, 0, s>>>(norm2, n, m, mm, bt, btg, G.get<SelGroup>(), fill,
+                                      KB.get<uint64_t>(), IB.get<uint32_t>(), part);
     sel_resolve_dev<<<kMaxGroups, 1024, 0, s>>>(G.get<SelGroup>(), META.get<int64_t>(), KB.get<uint64_t>(),
                                                IB.get<uint32_t>(), n, m, part, large);
-    note_launch(nbins > 4096 ? 8 : 6);
+    note_launch(mm_in ? 5 : 6);
     return 0;
 }
 
@@ -775,41 +1012,60 @@ __global__ void __launch_bounds__(256) scat_hist(const double *__restrict__ norm
     }
 }
 
-// one block of 256 threads: offsets (exclusive over j) and per-tile bases
-__global__ void __launch_bounds__(256) scat_scan(uint32_t *__restrict__ tile_cnt, int ntiles,
-                                                 int m, int64_t *__restrict__ offsets,
-                                                 const unsigned long long *__restrict__ vmax,
-                                                 double *__restrict__ V) {
+// CTA j: per-tile bases of sub-dataset j (exclusive over tiles, relative to the
+// sub-dataset's start), its size tot[j] and V_j
+__global__ void __launch_bounds__(1024) scat_colscan(uint32_t *__restrict__ tile_cnt, int ntiles, int m,
+                                                     uint32_t *__restrict__ tot,
+                                                     const unsigned long long *__restrict__ vmax,
+                                                     double *__restrict__ V) {
     __shared__ uint32_t ws[32];
-    const int j = threadIdx.x;
-    uint32_t tot = 0;
-    if (j < m)
-        for (int t = 0; t < ntiles; ++t) tot += tile_cnt[(int64_t)t * m + j];
-    uint32_t all;
-    const uint32_t ex = block_excl_scan(tot, ws, &all);
-    if (j < m) {
-        offsets[j] = ex;
-        V[j] = __longlong_as_double((long long)vmax[j]);
-        uint32_t run = ex;
-        for (int t = 0; t < ntiles; ++t) {
-            const uint32_t c = tile_cnt[(int64_t)t * m + j];
-            tile_cnt[(int64_t)t * m + j] = run;
-            run += c;
+    const int j = blockIdx.x;
+    uint32_t run = 0;
+    for (int t0 = 0; t0 < ntiles; t0 += 4 * (int)blockDim.x) {
+        uint32_t v[4], loc = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int t = t0 + threadIdx.x * 4 + e;
+            v[e] = t < ntiles ? tile_cnt[(int64_t)t * m + j] : 0u;
+            loc += v[e];
         }
+        uint32_t all;
+        uint32_t ex = run + block_excl_scan(loc, ws, &all);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int t = t0 + threadIdx.x * 4 + e;
+            if (t < ntiles) tile_cnt[(int64_t)t * m + j] = ex;
+            ex += v[e];
+        }
+        run += all;
     }
-    if (j == 0) offsets[m] = all;
+    if (threadIdx.x == 0) {
+        tot[j] = run;
+        V[j] = __longlong_as_double((long long)vmax[j]);
+    }
 }
 
 __global__ void __launch_bounds__(256) scat_write(const uint8_t *__restrict__ part, int64_t n,
                                                   int m, const uint32_t *__restrict__ tile_base,
+                                                  const uint32_t *__restrict__ tot,
+                                                  int64_t *__restrict__ offsets,
                                                   int32_t *__restrict__ perm,
                                                   int32_t *__restrict__ pos_of_id,
                                                   uint8_t *__restrict__ part_of_pos) {
     __shared__ uint32_t run[kMaxParts];
     __shared__ uint32_t wc[8][kMaxParts];
+    __shared__ uint32_t ws[32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int j = threadIdx.x; j < m; j += blockDim.x)
-        run[j] = tile_base[(int64_t)blockIdx.x * m + j];
+    {   // offsets: exclusive over the sub-dataset sizes (m <= 256 = blockDim)
+        const uint32_t c = (int)threadIdx.x < m ? tot[threadIdx.x] : 0u;
+        uint32_t all;
+        const uint32_t off = block_excl_scan(c, ws, &all);
+        if ((int)threadIdx.x < m) {
+            run[threadIdx.x] = off + tile_base[(int64_t)blockIdx.x * m + threadIdx.x];
+            if (blockIdx.x == 0) offsets[threadIdx.x] = off;
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0) offsets[m] = all;
+    }
     const int64_t base = (int64_t)blockIdx.x * kScatTile;
     for (int round = 0; round < kScatTile / 256; ++round) {
         for (int e = threadIdx.x; e < 8 * kMaxParts; e += blockDim.x) (&wc[0][0])[e] = 0;
@@ -845,18 +1101,18 @@ int partition_scatter(const double *norm2, const uint8_t *part, int64_t n, int m
                       int32_t *pos_of_id, uint8_t *part_of_pos, int64_t *offsets_d, double *V_d,
                       cudaStream_t s, std::string *err) {
     const int ntiles = (int)((n + kScatTile - 1) / kScatTile);
-    DevBuf tc(s), vm(s);
-    if (tc.alloc((size_t)ntiles * m * 4) || vm.alloc((size_t)m * 8)) {
+    DevBuf tc(s), vm(s), tt(s);
+    if (tc.alloc((size_t)ntiles * m * 4) || vm.alloc((size_t)m * 8) || tt.alloc((size_t)m * 4)) {
         *err = "partition: cudaMalloc failed";
         return NRLSH_ENOMEM;
     }
     cudaMemsetAsync(vm.p, 0, (size_t)m * 8, s);
     scat_hist<<<ntiles, 256, 0, s>>>(norm2, part, n, m, tc.get<uint32_t>(),
                                      vm.get<unsigned long long>());
-    scat_scan<<<1, 256, 0, s>>>(tc.get<uint32_t>(), ntiles, m, offsets_d,
-                                vm.get<unsigned long long>(), V_d);
-    scat_write<<<ntiles, 256, 0, s>>>(part, n, m, tc.get<uint32_t>(), perm, pos_of_id,
-                                      part_of_pos);
+    scat_colscan<<<m, 1024, 0, s>>>(tc.get<uint32_t>(), ntiles, m, tt.get<uint32_t>(),
+                                    vm.get<unsigned long long>(), V_d);
+    scat_write<<<ntiles, 256, 0, s>>>(part, n, m, tc.get<uint32_t>(), tt.get<uint32_t>(), offsets_d,
+                                      perm, pos_of_id, part_of_pos);
     note_launch(3);
     return 0;
 }

@@ -69,6 +69,10 @@ __device__ __forceinline__ float float_unorder(uint32_t o) {
 // Block-wide exclusive scan of one uint32 per thread (blockDim.x <= 1024,
 // multiple of 32).  `ws` must hold 32 words.  Returns the exclusive prefix;
 // *total receives the block sum.
+// The radius delta_j(q) is stored as int8 with -1 = "sub-dataset skipped"; a radius of
+// 128 (L = 128, every cell of j within the bound) wraps to -128 and is read back here.
+__device__ __forceinline__ int radius_of(int8_t v) { return v == (int8_t)-1 ? -1 : (int)(uint8_t)v; }
+
 __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t *ws, uint32_t *total) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nw = blockDim.x >> 5;

@@ -43,22 +43,15 @@ struct nrlsh_index {
     double *V_d = nullptr;          // [m]
     uint32_t *codes = nullptr;      // [n x W], partition order
     int8_t *codes_pm = nullptr;     // [n x scan_kp(L)] +-1 int8 code rows, partition order
-                                    //   (the tensor-core scan's B operand)
+                                    //   (the opt-in tensor-core scan's B operand)
     float *A = nullptr;             // [QM x (d+1) x L] row-major (as generated; block j = A_j)
     float *Apad = nullptr;          // [QM x (d+1) x 32W], zero columns >= L
     int4 *ctiles_d = nullptr;       // per-sub-dataset projections: code-kernel tiles
     int32_t nctiles = 0;            //   (j, p0, p1): <= 128 positions of one sub-dataset
     uint16_t *R_d = nullptr;        // [m x (L+1)]
     int4 *chunks_d = nullptr;       // scan work units (j, pos0, pos1, 0)
-    int4 *tiles_d = nullptr;        // tensor-core scan tiles: <= 256 positions of one j
-    int32_t ntiles = 0;
     int32_t *order_d = nullptr;     // [m*(L+1)] structure position -> j*(L+1)+h
     int32_t nchunks = 0;
-    uint32_t *bs_planes = nullptr;  // bit-sliced scan (L <= 64): [32W x bs_G] planes of the
-    int64_t bs_G = 0;               //   groups of 32 positions of one sub-dataset
-    int2 *bs_gdesc = nullptr;       //   [bs_G] (first position, items)
-    int4 *bs_chunks = nullptr;      //   work units (j, g0, g1, first position)
-    int32_t bs_nchunks = 0;
     uint32_t *samp_codes = nullptr; // pilot sample: codes of positions t * stride (compacted)
     uint8_t *samp_part = nullptr;
     int64_t nsamp = 0;
@@ -93,15 +86,19 @@ struct ProfScope {
 
 // ---------------------------------------------------------------- build
 // (Xb != nullptr: also writes bf16 rows [n x dpb] (zero-padded) and |x| rounded up)
-void launch_norms(const float *X, int64_t n, int d, double *norm2, unsigned long long *bad,
-                  void *Xb, int dpb, float *xnorm, cudaStream_t s);
+// (returns true when it also wrote the keys' min / max bits into mm)
+bool launch_norms(const float *X, int64_t n, int d, double *norm2, unsigned long long *bad,
+                  void *Xb, int dpb, float *xnorm, cudaStream_t s, unsigned long long *mm = nullptr);
 // K2 (percentile): fills part_of_id.  Host-orchestrated; may synchronise `s`.
 int partition_percentile(const double *norm2, int64_t n, int m, uint8_t *part_of_id,
                          cudaStream_t s, std::string *err);
 // level 0 + in-smem group sorts, decided on the device (no host sync); sets *large
 // (device flag) when a boundary group exceeds the in-smem sort: then run the above
+// mm: the keys' (smallest positive, largest) bits if the norms pass computed them
+// (nullptr: computed here)
 int partition_percentile_fast(const double *norm2, int64_t n, int m, uint8_t *part_of_id,
-                              unsigned int *large, cudaStream_t s, std::string *err);
+                              unsigned int *large, cudaStream_t s, std::string *err,
+                              const unsigned long long *mm = nullptr);
 // largest-|x| threshold of the filter's first pass: the r-th smallest of nt tile
 // maxima (non-negative floats), radix-selected by one CTA into *out
 void launch_select_kth_float(const float *v, int64_t nt, int64_t r, float *out, cudaStream_t s);
@@ -153,27 +150,20 @@ void launch_gather_sample(const nrlsh_index *ix, int stride, uint32_t *sc, uint8
                           cudaStream_t s);
 void launch_pilot(const nrlsh_index *ix, const uint32_t *qcodes, int Qb, int64_t Tq,
                   int stride, int8_t *delta, uint32_t *cnt, cudaStream_t s);
+// lbc (nullable): [0] pairs the one-POPC lower bound ran on, [1] pairs it decided alone
 void launch_scan(const nrlsh_index *ix, const uint32_t *qcodes, const int8_t *delta, int Qb,
                  unsigned long long *buf, uint32_t *cnt, int64_t C,
-                 unsigned long long *pairs, cudaStream_t s);
-// bit-sliced scan (scan_bs.cu): codes of <= 64 bits, same appends as launch_scan
-int scan_bs_groups_per_chunk();
-bool scan_bs_supported(const nrlsh_index *ix);
-void launch_transpose_groups(const uint32_t *codes, const int2 *gdesc, int64_t G, int W, uint32_t *planes,
-                             cudaStream_t s);
-size_t scan_bs_ws_bytes(const nrlsh_index *ix, int Qb);
-void launch_scan_bs(const nrlsh_index *ix, const uint32_t *qcodes, const int8_t *delta, int Qb,
-                    unsigned long long *buf, uint32_t *cnt, int64_t C, unsigned long long *pairs,
-                    cudaStream_t s, void *ws);
-// cntv: entries of the buffer that are real (the tensor-core scan pads append
-// chunks with ~0 sentinels); == cnt for the popcount scan
+                 unsigned long long *pairs, cudaStream_t s, unsigned long long *lbc = nullptr);
+// cntv: the real entries of each query's buffer (the tensor-core scan pads its append
+// runs with ~0 sentinels, counted in cnt); == cnt for the popcount scan
 // ws: fallback_ws_bytes() of zeroed scratch for the all-SM re-do of failed queries
 // (nullptr: one CTA per failed query only)
 size_t fallback_ws_bytes(const nrlsh_index *ix);
 void launch_fallback(const nrlsh_index *ix, const uint32_t *qcodes, int Qb, int64_t Tq,
                      unsigned long long *buf, uint32_t *cnt, uint32_t *cntv, int64_t C,
                      int *flags, void *ws, cudaStream_t s);
-// tensor-core Hamming scan (scan_tc.cu): +-1 int8 item codes expanded at build
+// tensor-core Hamming scan (scan_tc.cu, NEXT-3, opt-in NRLSH_SCAN_TC=1): +-1 int8 item
+// codes expanded at build
 int scan_kp(int L);
 void launch_expand_pm(const uint32_t *codes, int64_t rows, int W, int L, int8_t *out, cudaStream_t s);
 bool scan_tc_supported(const nrlsh_index *ix);
@@ -206,31 +196,6 @@ void launch_rerank(const float *X, int d, int ldx, const float *Q, int Qb, const
                    int k, unsigned long long *partial, int64_t *out_ids, float *out_scores,
                    cudaStream_t s);
 
-// certified bf16-filter + fp32-rescore variant (same results as launch_rerank)
-void launch_rerank_bf(const float *X, int d, int ldx, const void *Xb, int dpb, const float *xnorm,
-                      const float *Q, int Qb, const int32_t *cand, int64_t ncand, int64_t cand_ld,
-                      const uint32_t *ncand_per_q, int k, unsigned long long *partial,
-                      int64_t *out_ids, float *out_scores, unsigned long long *nexact,
-                      cudaStream_t s, const int32_t *xb_row = nullptr);
-
-// select split in two passes (query_kernels.cu): mode 1 = bound (B, pk, per-sub-dataset
-// candidate counts), mode 2 = emit the candidates outside dense sub-datasets
-void launch_select_split(const nrlsh_index *ix, int Qb, int64_t Tq, const unsigned long long *buf,
-                         const uint32_t *cnt, int64_t C, int mode, uint32_t *sel_B,
-                         uint32_t *sel_pk, uint32_t *cnt_part, const uint8_t *dense,
-                         int32_t *cand, uint32_t *ncand_out, cudaStream_t s);
-// dense re-rank of the hot sub-datasets (rerank_dense.cu)
-bool dense_rerank_supported(int ld, int W, int k);
-int dense_splits(int Qb);
-void launch_dense_decide(const uint32_t *cnt_part, const int64_t *offsets, int m, int Qb,
-                         float frac, uint8_t *dense, int32_t *dinfo, cudaStream_t s);
-void launch_rerank_dense(const float *X, int ld, int dq, const float *Q, const uint32_t *qcodes,
-                         const uint32_t *sel_B, const uint32_t *sel_pk, const nrlsh_index *ix,
-                         int Qb, int k, const int32_t *dinfo, unsigned long long *partial, int S,
-                         cudaStream_t s);
-void launch_dense_merge(const unsigned long long *partial, int S, int k, const int64_t *g_ids,
-                        const float *g_sc, int Qb, int64_t *out_ids, float *out_scores,
-                        cudaStream_t s);
 
 // row gather (dst row r = src row idx[r]) or scatter (dst row idx[r] = src row r);
 // row_bytes a multiple of 4

@@ -201,8 +201,9 @@ __device__ void hist_and_bound(const uint32_t *__restrict__ codes,
             if (bin >= 0 && lane == __ffs(peers) - 1) atomicAdd(&hist[bin], (uint32_t)__popc(peers));
         }
     } else {
-        // (interleaved sample: slot t holds sample (t % per) * 32 + t / per, if any;
-        // slots fit 32 bits.)  PU slots' loads are issued before their atomics.
+        // (interleaved sample: slot s holds sample (s % 32) * per + s / 32 if that is
+        // < ns_real — the 32 slots a warp reads come from positions ~n/32 apart.)  PU
+        // slots' loads are issued before their atomics.
         const uint32_t per32 = (uint32_t)per, nsr = (uint32_t)ns_real;
         constexpr int PU = 4;
         for (int64_t b0 = 0; b0 < ns; b0 += PU * (int64_t)blockDim.x) {
@@ -211,10 +212,9 @@ __device__ void hist_and_bound(const uint32_t *__restrict__ codes,
 #pragma unroll
             for (int u = 0; u < PU; ++u) {
                 const int64_t t = b0 + (int64_t)u * blockDim.x + threadIdx.x;
-                const uint32_t t32 = (uint32_t)t;
-                const bool ok = t < ns && (per32 == 0 || (t32 % per32) * 32u + t32 / per32 < nsr);
                 pt[u] = -1;
-                if (ok) {
+                const uint32_t t32 = (uint32_t)t;
+                if (t < ns && (t32 & 31u) * per32 + (t32 >> 5) < nsr) {
                     load_code<W>(codes, t, c[u]);
                     pt[u] = (int)part[t];
                 }
@@ -252,13 +252,14 @@ template <int W>
 __global__ void gather_sample(const uint32_t *__restrict__ codes, const uint8_t *__restrict__ part,
                               int64_t ns, int stride, uint32_t *__restrict__ sc,
                               uint8_t *__restrict__ sp) {
-    // sample t (position t * stride) goes to slot (t % 32) * per + t / 32: the 32
+    // sample t (position t * stride, t < ns) goes to slot (t % per) * 32 + t / per,
+    // per = ceil(ns / 32): slot s then holds sample (s % 32) * per + s / 32, so the 32
     // slots a warp reads together come from positions ~n/32 apart
     const int64_t per = (ns + 31) / 32;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ns;
          t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t p = t * stride;
-        const int64_t slot = (t % 32) * per + t / 32;
+        const int64_t slot = (t % per) * 32 + t / per;
 #pragma unroll
         for (int w = 0; w < W; ++w) sc[slot * W + w] = codes[p * W + w];
         sp[slot] = part[p];
@@ -373,14 +374,15 @@ constexpr int kSB = kScanIPT >= 16 ? 256 : 128;   // staged appends per (CTA, qu
 // as (code words, radius, index) records read with one 16-byte shared load per
 // word pair, and a thread's pass bits are the sign bits of delta - h (funnel shifts).
 template <int W>
-__global__ void __launch_bounds__(kScanThreads) k6_scan(
+__global__ void __launch_bounds__(kScanThreads, W == 4 ? 4 : 5) k6_scan(
     const uint32_t *__restrict__ codes, const int4 *__restrict__ chunks,
     const uint32_t *__restrict__ qcodes, const int8_t *__restrict__ delta, int Qb, int m,
     const uint16_t *__restrict__ R, int L, unsigned long long *__restrict__ buf,
     uint32_t *__restrict__ cnt, int64_t C, unsigned long long *__restrict__ pairs, int QM,
-    int probe = 0) {
+    int probe, int lbmax, unsigned long long *__restrict__ lbc) {
     pdl_wait();
     constexpr int RW = W <= 2 ? 4 : 8;             // record words: codes, radius, query
+    __shared__ unsigned long long s_lb[2];   // (pairs the lower bound ran on / decided alone)
     __shared__ __align__(16) uint32_t srec[kQG][RW];
     __shared__ uint32_t sbuf[kQG][kSB];
     __shared__ uint32_t scnt[kQG];
@@ -398,7 +400,7 @@ __global__ void __launch_bounds__(kScanThreads) k6_scan(
         for (int t0 = 0; t0 < kQG; t0 += 32) {
             const int t = t0 + threadIdx.x;
             int dl = -1;
-            if (t < nqg) dl = delta[(int64_t)(q0 + t) * m + j];
+            if (t < nqg) dl = radius_of(delta[(int64_t)(q0 + t) * m + j]);
             if (t < kQG) scnt[t] = 0;
             const unsigned bal = __ballot_sync(NR_FULL, dl >= 0);
             if (dl >= 0) {
@@ -417,7 +419,9 @@ __global__ void __launch_bounds__(kScanThreads) k6_scan(
     const int nact = s_nact;
     if (nact == 0) return;
     if (threadIdx.x == 0 && pairs && !probe) atomicAdd(pairs, (unsigned long long)nact * (p1 - p0));
+    if (threadIdx.x == 0) { s_lb[0] = 0ull; s_lb[1] = 0ull; }
     const int lane = threadIdx.x & 31;
+    uint32_t lbt = 0, lbs = 0;   // (this warp: pairs the lower bound ran on / skipped)
     uint32_t nprobe = 0;   // (probe: the XOR/POPC/threshold work alone, no appends)
     uint32_t c[kScanIPT][W];
     uint32_t vmask = 0;   // bit u: item u of this thread exists
@@ -441,6 +445,22 @@ __global__ void __launch_bounds__(kScanThreads) k6_scan(
         uint32_t qc[W];
 #pragma unroll
         for (int w = 0; w < W; ++w) qc[w] = rec[w];
+        if (W >= 2 && dl <= lbmax) {
+            // small radius: a one-POPC lower bound per word pair first,
+            // h = popc(a) + popc(b) >= popc(a | b); where no item of the warp can pass,
+            // the exact distances are skipped (on near-random codes, most warps at
+            // delta <= 16 of 64 bits)
+            int lbmin = 255;
+#pragma unroll
+            for (int u = 0; u < kScanIPT; ++u) {
+                int lb = 0;
+#pragma unroll
+                for (int w = 0; w + 1 < W; w += 2) lb += __popc((c[u][w] ^ qc[w]) | (c[u][w + 1] ^ qc[w + 1]));
+                lbmin = min(lbmin, (vmask >> u & 1u) ? lb : 255);
+            }
+            lbt += 1;
+            if (!__any_sync(NR_FULL, lbmin <= dl)) { lbs += 1; continue; }
+        }
         int hh[kScanIPT];
         uint32_t fail = 0;   // bit u: h_u > delta (the sign of delta - h_u)
 #pragma unroll
@@ -490,7 +510,18 @@ __global__ void __launch_bounds__(kScanThreads) k6_scan(
         if (nprobe) atomicAdd((unsigned int *)pairs, nprobe);
         return;
     }
+    if (lbc && lbt) {   // (per warp: iterations x its items)
+        const uint32_t wv = __reduce_add_sync(NR_FULL, (uint32_t)__popc(vmask));
+        if (lane == 0) {
+            atomicAdd(&s_lb[0], (unsigned long long)lbt * wv);
+            atomicAdd(&s_lb[1], (unsigned long long)lbs * wv);
+        }
+    }
     __syncthreads();
+    if (lbc && threadIdx.x == 0 && s_lb[0]) {
+        atomicAdd(&lbc[0], s_lb[0]);
+        atomicAdd(&lbc[1], s_lb[1]);
+    }
     for (int t = threadIdx.x; t < nqg; t += blockDim.x) {
         const uint32_t nst = min(scnt[t], (uint32_t)kSB);
         sbase[t] = nst ? atomicAdd(&cnt[q0 + t], nst) : 0u;
@@ -512,15 +543,24 @@ __global__ void __launch_bounds__(kScanThreads) k6_scan(
     }
 }
 
+int scan_chunk_items() { return kChunk; }
+
+// ---------------------------------------------------------------- K6 scan, queries in lanes
+
 void launch_scan(const nrlsh_index *ix, const uint32_t *qcodes, const int8_t *delta, int Qb,
                  unsigned long long *buf, uint32_t *cnt, int64_t C, unsigned long long *pairs,
-                 cudaStream_t s) {
+                 cudaStream_t s, unsigned long long *lbc) {
+    // radii up to which the pair lower bound runs first: where a warp's 256 near-random
+    // codes all miss it with probability > 1/2 (Bin(32, 3/4) per word pair; 64 bits:
+    // delta <= 16, 128 bits: delta <= 37); NRLSH_SCAN_LBMAX overrides (-1: off)
+    int lbmax = ix->W == 2 ? 16 : (ix->W == 4 ? 37 : -1);
+    if (getenv("NRLSH_SCAN_LBMAX")) lbmax = atoi(getenv("NRLSH_SCAN_LBMAX"));
     const int64_t ngroups = (Qb + kQG - 1) / kQG;
     const unsigned grid = (unsigned)(ix->nchunks * ngroups);
     switch (ix->W) {
-        case 1: launch_pdl(k6_scan<1>, dim3(grid), dim3(kScanThreads), 0, s, ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs, ix->QM, 0); break;
-        case 2: launch_pdl(k6_scan<2>, dim3(grid), dim3(kScanThreads), 0, s, ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs, ix->QM, 0); break;
-        default: launch_pdl(k6_scan<4>, dim3(grid), dim3(kScanThreads), 0, s, ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs, ix->QM, 0); break;
+        case 1: launch_pdl(k6_scan<1>, dim3(grid), dim3(kScanThreads), 0, s, ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs, ix->QM, 0, lbmax, lbc); break;
+        case 2: launch_pdl(k6_scan<2>, dim3(grid), dim3(kScanThreads), 0, s, ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs, ix->QM, 0, lbmax, lbc); break;
+        default: launch_pdl(k6_scan<4>, dim3(grid), dim3(kScanThreads), 0, s, ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs, ix->QM, 0, lbmax, lbc); break;
     }
     note_launch();
     if (getenv("NRLSH_SCAN_PROBE")) {   // experiment: time the scan without its appends
@@ -528,14 +568,13 @@ void launch_scan(const nrlsh_index *ix, const uint32_t *qcodes, const int8_t *de
         if (!dummy) cudaMalloc(&dummy, 8);
         ProfScope p(SLOT_OTHER, s);
         switch (ix->W) {
-            case 1: k6_scan<1><<<grid, kScanThreads, 0, s>>>(ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, dummy, ix->QM, 1); break;
-            case 2: k6_scan<2><<<grid, kScanThreads, 0, s>>>(ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, dummy, ix->QM, 1); break;
-            default: k6_scan<4><<<grid, kScanThreads, 0, s>>>(ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, dummy, ix->QM, 1); break;
+            case 1: k6_scan<1><<<grid, kScanThreads, 0, s>>>(ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, dummy, ix->QM, 1, lbmax, nullptr); break;
+            case 2: k6_scan<2><<<grid, kScanThreads, 0, s>>>(ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, dummy, ix->QM, 1, lbmax, nullptr); break;
+            default: k6_scan<4><<<grid, kScanThreads, 0, s>>>(ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, dummy, ix->QM, 1, lbmax, nullptr); break;
         }
     }
 }
 
-int scan_chunk_items() { return kChunk; }
 
 // =========================================================================== fallback
 template <int W>
@@ -798,18 +837,15 @@ void launch_fallback(const nrlsh_index *ix, const uint32_t *qcodes, int Qb, int6
 
 // =========================================================================== K7 select
 // mode 0: bound + emit (all candidates); mode 1: bound only — writes the boundary
-// structure position B and tie position bound pk per query and adds every
-// sub-dataset's candidate count of the query to cnt_part; mode 2: emit from the
-// stored (B, pk), skipping sub-datasets flagged dense (they are re-ranked by the
-// dense kernel) and writing the number emitted to ncand_out.
+// structure position B and tie position bound pk per query, and the ks best-ranked
+// candidates (seeds) of the tensor-core re-rank.
 __global__ void __launch_bounds__(1024) k7_select(
     const unsigned long long *__restrict__ buf, const uint32_t *__restrict__ cnt, int64_t C,
     int64_t Tq, int NR, int tie_cap, const uint16_t *__restrict__ R,
     const int32_t *__restrict__ perm, int32_t *__restrict__ cand,
-    uint16_t *__restrict__ cand_rank, int mode, int L, uint32_t *__restrict__ sel_B,
-    uint32_t *__restrict__ sel_pk, uint32_t *__restrict__ cnt_part,
-    const uint8_t *__restrict__ dense, uint32_t *__restrict__ ncand_out,
-    int32_t *__restrict__ seeds, int ks, const int32_t *__restrict__ order) {
+    uint16_t *__restrict__ cand_rank, int mode, uint32_t *__restrict__ sel_B,
+    uint32_t *__restrict__ sel_pk, int32_t *__restrict__ seeds, int ks,
+    const int32_t *__restrict__ order) {
     pdl_wait();
     extern __shared__ uint32_t hist[];   // [max(NR, tie_cap)] + R copy [NR] (uint16)
     uint16_t *sRt = reinterpret_cast<uint16_t *>(hist + tie_cap);
@@ -820,25 +856,6 @@ __global__ void __launch_bounds__(1024) k7_select(
     const int q = blockIdx.x;
     const int64_t c = min((int64_t)cnt[q], C);
     const unsigned long long *b = buf + (int64_t)q * C;
-    if (mode == 2) {
-        for (int e = threadIdx.x; e < NR; e += blockDim.x) sRt[e] = R[e];
-        if (threadIdx.x == 0) s_out = 0;
-        __syncthreads();
-        const uint32_t B = sel_B[q], pk = sel_pk[q];
-        for (int64_t e = threadIdx.x; e < c; e += blockDim.x) {
-            const unsigned long long v = b[e];
-            const uint32_t f = (uint32_t)(v >> 32), pos = (uint32_t)v;
-            if (f >= (uint32_t)NR || dense[f / (L + 1)]) continue;
-            const uint32_t r = sRt[f];
-            if (r < B || (r == B && pos <= pk)) {
-                const uint32_t slot = atomicAdd(&s_out, 1u);
-                if (slot < (uint32_t)Tq) cand[(int64_t)q * Tq + slot] = perm[pos];
-            }
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) ncand_out[q] = min(s_out, (uint32_t)Tq);
-        return;
-    }
     for (int e = threadIdx.x; e < NR; e += blockDim.x) { hist[e] = 0u; sRt[e] = R[e]; }
     if (threadIdx.x == 0) { sB = NR - 1; sLt = 0; s_out = 0; s_bseed = NR - 1; }
     __syncthreads();
@@ -909,17 +926,6 @@ __global__ void __launch_bounds__(1024) k7_select(
     const uint32_t fB = (uint32_t)__ldg(order + B);   // the flat (j, h) cell at the bound
     const uint32_t need_eq = need - sLt;
     const uint32_t n_eq = hist[fB];
-    if (cnt_part) {   // the query's candidates per sub-dataset (hist is still intact here)
-        const int m = NR / (L + 1);
-        for (int j = threadIdx.x; j < m; j += blockDim.x) {
-            uint32_t cj = 0;
-            for (int h = 0; h <= L; ++h) {
-                const uint32_t f = j * (L + 1) + h, r = sRt[f];
-                cj += r < B ? hist[f] : (r == B ? min(need_eq, n_eq) : 0u);
-            }
-            if (cj) atomicAdd(&cnt_part[j], cj);
-        }
-    }
     // the need_eq-th smallest position among the ties (R == B): when they fit, one
     // pass gathers them into shared memory (reusing the histogram's space) and a
     // radix select runs there; otherwise radix select over the buffer, 8 bits/round
@@ -1078,23 +1084,10 @@ void launch_select(const nrlsh_index *ix, int Qb, int64_t Tq, const unsigned lon
     const size_t sm = (size_t)tie_cap * 4 + (size_t)NR * 2;
     cudaFuncSetAttribute(k7_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     launch_pdl(k7_select, dim3(Qb), dim3(1024), sm, s, buf, cnt, C, Tq, NR, tie_cap, ix->R_d, ix->perm, cand, cand_rank,
-                                   0, ix->L, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0, ix->order_d);
+                                   0, nullptr, nullptr, nullptr, 0, ix->order_d);
     note_launch();
 }
 
-
-void launch_select_split(const nrlsh_index *ix, int Qb, int64_t Tq, const unsigned long long *buf,
-                         const uint32_t *cnt, int64_t C, int mode, uint32_t *sel_B,
-                         uint32_t *sel_pk, uint32_t *cnt_part, const uint8_t *dense,
-                         int32_t *cand, uint32_t *ncand_out, cudaStream_t s) {
-    const int NR = ix->m * (ix->L + 1);
-    const int tie_cap = std::max(NR, 16384);
-    const size_t sm = (size_t)tie_cap * 4 + (size_t)NR * 2;
-    cudaFuncSetAttribute(k7_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    launch_pdl(k7_select, dim3(Qb), dim3(1024), sm, s, buf, cnt, C, Tq, NR, tie_cap, ix->R_d, ix->perm, cand, nullptr,
-                                   mode, ix->L, sel_B, sel_pk, cnt_part, dense, ncand_out, nullptr, 0, ix->order_d);
-    note_launch();
-}
 
 void launch_select_seeds(const nrlsh_index *ix, int Qb, int64_t Tq, const unsigned long long *buf,
                          const uint32_t *cnt, int64_t C, uint32_t *sel_B, uint32_t *sel_pk,
@@ -1104,7 +1097,7 @@ void launch_select_seeds(const nrlsh_index *ix, int Qb, int64_t Tq, const unsign
     const size_t sm = (size_t)tie_cap * 4 + (size_t)NR * 2;
     cudaFuncSetAttribute(k7_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     launch_pdl(k7_select, dim3(Qb), dim3(1024), sm, s, buf, cnt, C, Tq, NR, tie_cap, ix->R_d, ix->perm, nullptr, nullptr,
-                                   1, ix->L, sel_B, sel_pk, nullptr, nullptr, nullptr, seeds, ks, ix->order_d);
+                                   1, sel_B, sel_pk, seeds, ks, ix->order_d);
     note_launch();
 }
 
@@ -1563,160 +1556,6 @@ __global__ void __launch_bounds__(kRrThreads) k8_rerank(
     }
 }
 
-// Certified two-pass variant: a bf16 pass (Xb rows, half the bytes; q rounded to
-// bf16) gives s~ with |s~ - q.x| <= eps |q||x|; only candidates whose upper bound
-// s~ + eps |q||x| reaches the CTA's current k-th best exact score are rescored in
-// fp32 from X (the same row_dot as the plain kernel, so the returned scores are
-// identical).  Every candidate that can enter the top-k is rescored, so the
-// result equals the plain kernel's.
-template <int NB>
-__device__ __forceinline__ float row_dot_bf(const uint16_t *__restrict__ xb, const float *qb,
-                                            int sub, int nchunk) {
-    // chunk c (8 bf16 = 16 bytes) of the row goes to lane sub + 8i
-    float acc = 0.f;
-    for (int i0 = 0; i0 * kRrLPR < nchunk; i0 += NB) {
-        uint4 v[NB];
-#pragma unroll
-        for (int u = 0; u < NB; ++u) {
-            const int c = min((i0 + u) * kRrLPR + sub, nchunk - 1);
-            v[u] = __ldg(reinterpret_cast<const uint4 *>(xb) + c);
-        }
-#pragma unroll
-        for (int u = 0; u < NB; ++u) {
-            const int c = (i0 + u) * kRrLPR + sub;
-            const bool ok = c < nchunk;
-            const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const float lo = __uint_as_float(w[e] << 16), hi = __uint_as_float(w[e] & 0xFFFF0000u);
-                const int k = (ok ? c : 0) * 8 + 2 * e;
-                acc = fmaf(qb[k], ok ? lo : 0.f, acc);
-                acc = fmaf(qb[k + 1], ok ? hi : 0.f, acc);
-            }
-        }
-    }
-    return acc;
-}
-
-template <int VEC, int NB>
-__global__ void __launch_bounds__(kRrThreads) k8_rerank_bf(
-    const float *__restrict__ X, int d, int dq, const uint16_t *__restrict__ Xb, int dpb,
-    const float *__restrict__ xnorm, float eps_rel, const float *__restrict__ Q,
-    const int32_t *__restrict__ cand, int64_t cand_ld, int64_t ncand,
-    const uint32_t *__restrict__ ncand_per_q, int k, int cap, int64_t slice,
-    unsigned long long *__restrict__ partial, int64_t *__restrict__ out_ids,
-    float *__restrict__ out_scores, unsigned long long *__restrict__ nexact,
-    const int32_t *__restrict__ xb_row) {
-    extern __shared__ __align__(16) unsigned long long rr_smem[];
-    unsigned long long *buf = rr_smem;                       // [cap]
-    float *sq = reinterpret_cast<float *>(buf + cap);        // [dpad] fp32 q
-    const int dpad = (d + 8 * VEC - 1) / (8 * VEC) * (8 * VEC);
-    float *sqb = sq + dpad;                                  // [dpb] bf16-rounded q
-    __shared__ unsigned int s_cnt;
-    __shared__ unsigned long long s_thr;
-    __shared__ double s_qq[kRrThreads / 32];
-    __shared__ unsigned int s_nex;
-    const int q = blockIdx.x;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int sub = lane & (kRrLPR - 1), grp = lane >> 3;
-    double qq = 0.0;
-    // X rows hold d floats (a zero-padded copy may have d > dq); queries hold dq
-    for (int e = threadIdx.x; e < dpad; e += blockDim.x) {
-        const float v = e < dq ? Q[(int64_t)q * dq + e] : 0.f;
-        sq[e] = v;
-        qq += (double)v * v;
-    }
-    for (int e = threadIdx.x; e < dpb; e += blockDim.x)
-        sqb[e] = e < dq ? __bfloat162float(__float2bfloat16_rn(Q[(int64_t)q * dq + e])) : 0.f;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) qq += __shfl_xor_sync(NR_FULL, qq, o);
-    if (lane == 0) s_qq[warp] = qq;
-    if (threadIdx.x == 0) { s_cnt = 0; s_thr = ~0ull; s_nex = 0; }
-    int64_t nc = ncand;
-    if (ncand_per_q) nc = min((int64_t)ncand_per_q[q], cand_ld);
-    const int64_t t0 = (int64_t)blockIdx.y * slice;
-    const int64_t t1 = min(nc, t0 + slice);
-    const int32_t *cl = cand + (int64_t)q * cand_ld;
-    const float *ql = sq + sub * VEC;
-    const int rem = d - sub * VEC;
-    const int nchunk = dpb / 8;
-    __syncthreads();
-    double qt = 0.0;
-    for (int w = 0; w < kRrThreads / 32; ++w) qt += s_qq[w];
-    // eps |q| rounded up (|q| from an fp64 sum, with margin)
-    const float eq = __fmul_ru(eps_rel, __double2float_ru(sqrt(qt) * (1.0 + 0x1p-50)));
-    unsigned int nex = 0;
-    for (int64_t base = t0; base < t1; base += kRrRound) {
-        const int64_t tw = base + warp * 32 + lane;
-        int myid = -1;
-        if (tw < t1) myid = cl[tw];
-        const float myxn = myid >= 0 ? __ldg(xnorm + myid) : 0.f;
-#pragma unroll 1
-        for (int st = 0; st < 8; ++st) {
-            const int id = __shfl_sync(NR_FULL, myid, st * 4 + grp);
-            const float xn = __shfl_sync(NR_FULL, myxn, st * 4 + grp);
-            float sa = 0.f;
-            if (id >= 0)   // (Xb rows are partition positions: xb_row = pos_of_id)
-                sa = row_dot_bf<NB>(Xb + (int64_t)(xb_row ? __ldg(xb_row + id) : id) * dpb, sqb, sub, nchunk);
-            sa += __shfl_xor_sync(NR_FULL, sa, 1);
-            sa += __shfl_xor_sync(NR_FULL, sa, 2);
-            sa += __shfl_xor_sync(NR_FULL, sa, 4);
-            const unsigned long long thr = *((volatile unsigned long long *)&s_thr);
-            bool pass = id >= 0;
-            if (pass && thr != ~0ull) {
-                const float ub = __fadd_ru(sa, __fmul_ru(eq, xn));
-                pass = ub >= float_unorder(~(uint32_t)(thr >> 32));
-            }
-            if (!__any_sync(NR_FULL, pass)) continue;
-            float acc = 0.f;
-            if (pass) {
-                const float *xl = X + (int64_t)id * d + sub * VEC;
-                acc = row_dot_any<VEC>(xl, ql, rem);
-            }
-            acc += __shfl_xor_sync(NR_FULL, acc, 1);
-            acc += __shfl_xor_sync(NR_FULL, acc, 2);
-            acc += __shfl_xor_sync(NR_FULL, acc, 4);
-            if (sub == 0 && pass) {
-                ++nex;
-                const unsigned long long key = topk_key(acc, (uint32_t)id);
-                if (key < *((volatile unsigned long long *)&s_thr)) {
-                    const unsigned slot = atomicAdd(&s_cnt, 1u);
-                    buf[slot] = key;
-                }
-            }
-        }
-        __syncthreads();
-        if (s_cnt > (unsigned)(cap - kRrRound)) {   // compact: keep the k best
-            const int c = (int)s_cnt;
-            for (int e = c + threadIdx.x; e < cap; e += blockDim.x) buf[e] = ~0ull;
-            __syncthreads();
-            bitonic_sort_smem(buf, cap);
-            if (threadIdx.x == 0) {
-                s_cnt = (unsigned)min(c, k);
-                if (c >= k) s_thr = buf[k - 1];
-            }
-            __syncthreads();
-        }
-    }
-    if (nexact && nex) atomicAdd(&s_nex, nex);
-    __syncthreads();
-    if (nexact && threadIdx.x == 0 && s_nex) atomicAdd(nexact, (unsigned long long)s_nex);
-    const int c = (int)s_cnt;
-    for (int e = c + threadIdx.x; e < cap; e += blockDim.x) buf[e] = ~0ull;
-    __syncthreads();
-    bitonic_sort_smem(buf, cap);
-    if (partial) {
-        unsigned long long *pp = partial + ((int64_t)q * gridDim.y + blockIdx.y) * k;
-        for (int t = threadIdx.x; t < k; t += blockDim.x) pp[t] = t < c ? buf[t] : ~0ull;
-    } else {
-        for (int t = threadIdx.x; t < k; t += blockDim.x) {
-            const unsigned long long v = t < c ? buf[t] : ~0ull;
-            out_ids[(int64_t)q * k + t] = v == ~0ull ? -1 : (int64_t)(uint32_t)v;
-            out_scores[(int64_t)q * k + t] = v == ~0ull ? -INFINITY : float_unorder(~(uint32_t)(v >> 32));
-        }
-    }
-}
-
 // merge the gy partial top-k lists of each query
 __global__ void __launch_bounds__(256) k8_rerank_merge(const unsigned long long *__restrict__ partial,
                                                        int gy, int k, int np2,
@@ -1804,54 +1643,5 @@ void launch_rerank(const float *X, int d, int ldx, const float *Q, int Qb, const
     }
 }
 
-
-void launch_rerank_bf(const float *X, int d, int ldx, const void *Xb, int dpb, const float *xnorm,
-                      const float *Q, int Qb, const int32_t *cand, int64_t ncand, int64_t cand_ld,
-                      const uint32_t *ncand_per_q, int k, unsigned long long *partial,
-                      int64_t *out_ids, float *out_scores, unsigned long long *nexact,
-                      cudaStream_t s, const int32_t *xb_row) {
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    const int64_t rounds = std::max<int64_t>(1, (ncand + kRrRound - 1) / kRrRound);
-    int gy = (int)std::min<int64_t>(rounds, std::max(1, (sms * 8) / std::max(1, Qb)));
-    gy = std::min(gy, std::max(1, 8192 / k));
-    if (!partial) gy = 1;
-    const int64_t slice = ((rounds + gy - 1) / gy) * kRrRound;
-    gy = (int)std::max<int64_t>(1, (ncand + slice - 1) / slice);
-    const int cap = pow2_at_least(k + 2 * kRrRound);
-    const int vec = (ldx % 4 == 0) ? 4 : ((ldx % 2 == 0) ? 2 : 1);
-    const int dpad = (ldx + 8 * vec - 1) / (8 * vec) * (8 * vec);
-    const size_t sm = (size_t)cap * 8 + (size_t)dpad * 4 + (size_t)dpb * 4;
-    unsigned long long *pp = gy > 1 ? partial : nullptr;
-    // certified bound of |bf16 dot - exact dot| / (|q||x|): bf16 operands (2u + u^2,
-    // u = 2^-8) + fp32 accumulation of dpb exact products, x1.05 slack (as the GT filter)
-    const double u = 0x1p-8;
-    const float eps = (float)(1.05 * ((2 * u + u * u) + (1 + u) * (1 + u) * dpb * 0x1p-23));
-    const int nb = std::min(4, (dpb / 8 + kRrLPR - 1) / kRrLPR);
-    dim3 grid(Qb, gy);
-#define NR_RB(V, B)                                                                             \
-    do {                                                                                        \
-        cudaFuncSetAttribute(k8_rerank_bf<V, B>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
-                             (int)sm);                                                          \
-        k8_rerank_bf<V, B><<<grid, kRrThreads, sm, s>>>(                                        \
-            X, ldx, d, (const uint16_t *)Xb, dpb, xnorm, eps, Q, cand, cand_ld, ncand,        \
-            ncand_per_q, k, cap, slice, pp, out_ids, out_scores, nexact, xb_row);               \
-    } while (0)
-#define NR_RB_V(V)                                                   \
-    switch (nb) {                                                    \
-        case 1: NR_RB(V, 1); break;  case 2: NR_RB(V, 2); break;     \
-        case 3: NR_RB(V, 3); break;  default: NR_RB(V, 4); break;    \
-    }
-    if (vec == 4) { NR_RB_V(4) } else if (vec == 2) { NR_RB_V(2) } else { NR_RB_V(1) }
-#undef NR_RB_V
-#undef NR_RB
-    note_launch();
-    if (gy > 1) {
-        const int np2 = pow2_at_least((int64_t)gy * k);
-        cudaFuncSetAttribute(k8_rerank_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, np2 * 8);
-        launch_pdl(k8_rerank_merge, dim3(Qb), dim3(256), (size_t)np2 * 8, s, partial, gy, k, np2, out_ids, out_scores);
-        note_launch();
-    }
-}
 
 }  // namespace nrlsh

@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(256) scan_tile_lists(const int8_t *__restrict_
     const int nv = (q1 - q0) * m;   // the block's delta rows
     for (int e = threadIdx.x; e < nv; e += blockDim.x) {
         const int r = q0 + e / m, j = e % m;
-        if (delta[(int64_t)(qperm ? qperm[r] : r) * m + j] >= 0) act[j] = 1;
+        if (radius_of(delta[(int64_t)(qperm ? qperm[r] : r) * m + j]) >= 0) act[j] = 1;
     }
     __syncthreads();
     const int lane = threadIdx.x & 31;
@@ -513,7 +513,7 @@ __global__ void scan_keys(const int8_t *__restrict__ delta, int Qb, int m, uint3
     const int q = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
     if (q >= Qb) return;
     uint32_t k = 0;
-    for (int j = lane; j < m; j += 32) k += (uint32_t)((int)delta[(int64_t)q * m + j] + 1);
+    for (int j = lane; j < m; j += 32) k += (uint32_t)(radius_of(delta[(int64_t)q * m + j]) + 1);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) k += __shfl_xor_sync(NR_FULL, k, o);
     if (lane == 0) keys[q] = ~k;   // descending activity
@@ -525,7 +525,7 @@ __global__ void scan_thresholds(const int8_t *__restrict__ delta, int Qb, int qb
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows;
          r += (int64_t)gridDim.x * blockDim.x) {
         const int j = (int)(r / qbpad), q = (int)(r % qbpad);
-        const int dl = q < Qb ? (int)delta[(int64_t)(qperm ? qperm[q] : q) * m + j] : -1;
+        const int dl = q < Qb ? radius_of(delta[(int64_t)(qperm ? qperm[q] : q) * m + j]) : -1;
         out[r] = (int16_t)(dl >= 0 ? 2 * dl - L : -(L + 1));
     }
 }

@@ -161,7 +161,6 @@ struct GtArgs {
                             // epilogue arithmetic, 2 = skip the TMEM reads too,
                             // 3 = also skip the MMAs (TMA stream only)
     int prefetch;           // item tiles prefetched into L2 ahead of the ring
-    int kps;                // (pair kernel) K blocks per ring stage: 1 or kblocks
     // candidate-membership mode (the tensor-core re-rank): survivors must also be
     // candidates of their query; the running bound is over candidates only
     int member;
@@ -609,205 +608,6 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
 }
 
 
-// ------------------------------------------------------------ CTA-pair variant
-// The same filter on a CTA pair (cluster of 2, tcgen05 cta_group::2): the pair's
-// M = 256 query rows (128 per CTA, resident in smem) x N = 256 items per MMA; each
-// CTA TMA-loads its 128-item half of every tile (signalled on the leader's
-// barrier) and the leader CTA issues the pair MMAs, which read the B halves of both
-// CTAs — so each CTA receives half the item bytes it multiplies (the L2->SM feed
-// bounds the single-CTA kernel) while the tensor cores run at the N = 256 rate, and
-// each CTA's 128 x 256 accumulator is double-buffered in its TMEM (epilogue overlapped).
-constexpr int GP_HN = 128;                 // items per CTA half tile
-constexpr int GP_PN = 2 * GP_HN;           // items per pair tile (MMA N)
-constexpr int GP_B_BLK = GP_HN * 128;      // 16 KB: one K block of a half tile
-constexpr int GP_MAX_STAGES = 12;
-
-__global__ void __launch_bounds__(GT_THREADS, 1)
-    gt_filter_pair(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmX,
-                   GtArgs a) {
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t *smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
-    uint8_t *sA = smem;                                        // kblocks x 16 KB (this CTA's rows)
-    uint8_t *sB = sA + a.kblocks * GT_A_BLK;                   // stages x 16 KB (this CTA's half)
-    const int SB = a.kps * GP_B_BLK;                           // bytes per stage
-    float *sxn = (float *)(sB + a.stages * SB);                // [2][GP_PN] |x| tiles
-    uint32_t *scode = (uint32_t *)(sxn + 2 * GP_PN);           // [2][GP_PN x W<=4] (member mode)
-    uint8_t *spart = (uint8_t *)(scode + 2 * GP_PN * 4);       // [2][GP_PN]        (member mode)
-    uint64_t *bars = (uint64_t *)(spart + 2 * GP_PN);
-    uint64_t *full = bars, *empty = bars + GP_MAX_STAGES;
-    uint64_t *a_full = bars + 2 * GP_MAX_STAGES, *a_empty = a_full + 1;
-    uint64_t *tfull = a_empty + 1, *tempty = tfull + 2;        // per TMEM buffer
-    uint64_t *xfull = tempty + 2, *xempty = xfull + 2;         // per |x| tile buffer
-    uint32_t *tmem_slot = (uint32_t *)(xempty + 2);
-    float *sheap = reinterpret_cast<float *>(tmem_slot + 4);
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t rank = tc::cluster_ctarank();
-    const bool leader = rank == 0;
-    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < a.stages; ++s) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
-        tc::mbar_init(a_full, 1);
-        tc::mbar_init(a_empty, 1);
-        for (int b = 0; b < 2; ++b) {
-            tc::mbar_init(&tfull[b], 1);
-            tc::mbar_init(&tempty[b], 16);   // 8 epilogue warps x 2 CTAs (leader's is used)
-            tc::mbar_init(&xfull[b], 1);
-            tc::mbar_init(&xempty[b], 8);
-        }
-        tc::fence_mbar_init();
-    }
-    if (warp == 2) tc::tmem_alloc_pair(tmem_slot, 512);
-    if (warp == 0 && lane == 0) { tc::tma_prefetch(&tmQ); tc::tma_prefetch(&tmX); }
-    tc::tc_fence_before();
-    tc::cluster_sync();   // both CTAs' barriers initialised and TMEM allocated
-    tc::tc_fence_after();
-    const uint32_t tmem_base = *tmem_slot;
-    const int nunits = a.nqp * a.nsplit;   // (query group of 256, item split)
-
-    if (warp == 0 && lane == 0) {
-        // ================= TMA producer (both CTAs; completion on the leader's barriers)
-        uint32_t g = 0, ul = 0;
-        const uint32_t a_full_l = tc::mapa_shared(a_full, 0);
-        for (int u = pair; u < nunits; u += npairs, ++ul) {
-            const int qg = u % a.nqp, sp = u / a.nqp;
-            const int64_t ib = (int64_t)sp * a.split_items;
-            const int64_t ie = min(a.n, ib + a.split_items);
-            if (ul > 0) tc::mbar_wait_cluster(a_empty, (ul - 1) & 1);
-            if (leader) tc::mbar_arrive_expect_tx(a_full, 2 * a.kblocks * GT_A_BLK);
-            for (int kb = 0; kb < a.kblocks; ++kb)
-                tc::tma_load_2d_pair(sA + kb * GT_A_BLK, &tmQ, a_full_l, kb * GT_KB,
-                                     qg * 2 * GT_M + (int)rank * GT_M);
-            const int64_t ntu = (ie - ib + GP_PN - 1) / GP_PN;
-            for (int64_t jt = 0; jt < ntu; ++jt) {
-                const int64_t i0 = ib + jt * GP_PN + rank * GP_HN;
-                for (int kb0 = 0; kb0 < a.kblocks; kb0 += a.kps, ++g) {
-                    const uint32_t s = g % a.stages, r = g / a.stages;
-                    tc::mbar_wait_cluster(&empty[s], (r & 1) ^ 1);
-                    if (leader) tc::mbar_arrive_expect_tx(&full[s], 2 * SB);
-                    const uint32_t fb = tc::mapa_shared(&full[s], 0);
-                    for (int e = 0; e < a.kps; ++e)
-                        tc::tma_load_2d_pair(sB + s * SB + e * GP_B_BLK, &tmX, fb, (kb0 + e) * GT_KB, (int)i0);
-                }
-            }
-        }
-    } else if (warp == 1) {
-        // ================= MMA issuer: the leader CTA's warp 1 drives the pair
-        if (leader) {
-            constexpr uint32_t idesc = tc::umma_idesc(1, 2 * GT_M, GP_PN);
-            uint32_t g = 0, t = 0, ul = 0;
-            for (int u = pair; u < nunits; u += npairs, ++ul) {
-                const int sp = u / a.nqp;
-                const int64_t ib = (int64_t)sp * a.split_items;
-                const int64_t ie = min(a.n, ib + a.split_items);
-                tc::mbar_wait_cluster(a_full, ul & 1);
-                tc::tc_fence_after();
-                for (int64_t i0 = ib; i0 < ie; i0 += GP_PN, ++t) {
-                    const uint32_t buf = t & 1, tr = t >> 1;
-                    tc::mbar_wait_cluster(&tempty[buf], (tr & 1) ^ 1);   // both CTAs drained it
-                    tc::tc_fence_after();
-                    const uint32_t dt = tmem_base + buf * GP_PN;
-                    for (int kb0 = 0; kb0 < a.kblocks; kb0 += a.kps, ++g) {
-                        const uint32_t s = g % a.stages, r = g / a.stages;
-                        tc::mbar_wait_cluster(&full[s], r & 1);
-                        tc::tc_fence_after();
-                        for (int e = 0; e < a.kps; ++e) {
-                            const int kb = kb0 + e;
-                            const uint32_t abase = tc::smem_u32(sA + kb * GT_A_BLK);
-                            const uint32_t bbase = tc::smem_u32(sB + s * SB + e * GP_B_BLK);
-                            const int nk = min(GT_KB / 16, (a.d - kb * GT_KB + 15) / 16);
-                            for (int kk = 0; kk < (a.dbg == 3 ? 0 : nk); ++kk)
-                                tc::mma_f16_pair_warp(dt, tc::umma_desc_sw128(abase + kk * 32),
-                                                      tc::umma_desc_sw128(bbase + kk * 32), idesc,
-                                                      (kb | kk) != 0);
-                        }
-                        tc::mma_commit_pair_mc(&empty[s], 3);
-                    }
-                    tc::mma_commit_pair_mc(&tfull[buf], 3);
-                }
-                tc::mma_commit_pair_mc(a_empty, 3);
-            }
-        }
-    } else if (warp == 3 && lane == 0) {
-        // ================= |x| (and member-mode code / sub-dataset) loader: all 256
-        // items of each pair tile, into this CTA's tile buffer
-        uint32_t t = 0;
-        for (int u = pair; u < nunits; u += npairs) {
-            const int sp = u / a.nqp;
-            const int64_t ib = (int64_t)sp * a.split_items;
-            const int64_t ie = min(a.n, ib + a.split_items);
-            for (int64_t i0 = ib; i0 < ie; i0 += GP_PN, ++t) {
-                const uint32_t b = t & 1, tr = t >> 1;
-                tc::mbar_wait(&xempty[b], (tr & 1) ^ 1);
-                tc::mbar_arrive_expect_tx(&xfull[b], GP_PN * 4 + (a.member ? GP_PN * (a.W * 4 + 1) : 0));
-                tc::bulk_load(sxn + b * GP_PN, a.xnorm + i0, GP_PN * 4, &xfull[b]);
-                if (a.member) {
-                    tc::bulk_load(scode + b * GP_PN * 4, a.codes + i0 * a.W, GP_PN * a.W * 4, &xfull[b]);
-                    tc::bulk_load(spart + b * GP_PN, a.part + i0, GP_PN, &xfull[b]);
-                }
-            }
-        }
-    } else if (warp >= 4) {
-        // ================= epilogue: thread <-> (query row = TMEM lane, 128-column half)
-        const int grp = warp & 3;
-        const int half = (warp - 4) >> 2;
-        const int row = grp * 32 + lane;
-        uint32_t t = 0;
-        GtEpiRow er;
-        for (int u = pair; u < nunits; u += npairs) {
-            const int qg = u % a.nqp, sp = u / a.nqp;
-            const int64_t ib = (int64_t)sp * a.split_items;
-            const int64_t ie = min(a.n, ib + a.split_items);
-            const int q = qg * 2 * GT_M + (int)rank * GT_M + row;
-            er.begin(a, q, q < a.Qb,
-                     a.heap_smem ? sheap + (half * GT_M + row) * a.k
-                                 : a.heap + ((int64_t)(blockIdx.x * 2 + half) * GT_M + row) * a.k);
-            for (int64_t i0 = ib; i0 < ie; i0 += GP_PN, ++t) {
-                const uint32_t b = t & 1, tr = t >> 1;
-                const float *xn = sxn + b * GP_PN;
-                uint32_t o_next = 0;
-                const bool share = er.vq && ((t & 3) == 0);
-                if (share) o_next = *((volatile uint32_t *)&a.theta_glob[er.q]);
-                tc::mbar_wait(&xfull[b], tr & 1);
-                tc::mbar_wait_cluster(&tfull[b], tr & 1);
-                tc::tc_fence_after();
-                const uint32_t taddr = tmem_base + ((uint32_t)(grp * 32) << 16) + b * GP_PN + half * 128;
-                const float xm = warp_max128(xn + half * 128, lane);
-#pragma unroll 1
-                for (int c = half * 128; c < half * 128 + 128; c += 64) {
-                    if (a.dbg >= 2) break;
-                    uint32_t r0[32], r1[32];
-                    tc::tmem_ld_32x32b_x32(taddr + (c - half * 128), r0);
-                    tc::tmem_ld_32x32b_x32(taddr + (c - half * 128) + 32, r1);
-                    tc::tmem_ld_wait();
-                    if (!er.vq || a.dbg) continue;
-                    er.chunk(r0, r1, c, xn, xm, i0, scode + b * GP_PN * 4, spart + b * GP_PN);
-                }
-                tc::tc_fence_before();
-                __syncwarp();
-                if (lane == 0) {
-                    tc::mbar_arrive_cluster(tc::mapa_shared(&tempty[b], 0));
-                    tc::mbar_arrive(&xempty[b]);
-                }
-                if (share) er.share(o_next);
-            }
-            er.end();
-        }
-    }
-    __syncthreads();
-    tc::cluster_sync();   // no CTA leaves while its peer may still touch its smem / barriers
-    if (warp == 2) {
-        tc::tc_fence_after();
-        tc::tmem_dealloc_pair(tmem_base, 512);
-    }
-}
-
-static size_t gp_smem_bytes(int kblocks, int stages, int heap_k, int kps = 1) {
-    return 1024 + (size_t)kblocks * GT_A_BLK + (size_t)stages * kps * GP_B_BLK + 2 * GP_PN * 4 +
-           2 * GP_PN * 16 + 2 * GP_PN + (2 * GP_MAX_STAGES + 2 + 8) * 8 + 16 +
-           (size_t)2 * GT_M * heap_k * 4;
-}
-
 static size_t gt_tc_smem_bytes(int nt, int kblocks, int stages, int heap_k) {
     return 1024 + (size_t)GT_QB * kblocks * GT_A_BLK + (size_t)stages * nt * 128 + 2 * nt * 4 +
            2 * nt * 16 + 2 * nt + (2 * GT_MAX_STAGES + 2 + 8 + 4) * 8 + 16 +
@@ -1046,7 +846,7 @@ int launch_gt_filter_tc(const void *Xb, int64_t n, int d, int dp, const void *Qb
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     GtArgs a;
-    a.kps = 1;
+
     a.n = n;
     a.Qb = Qb;
     a.d = d;
@@ -1078,60 +878,6 @@ int launch_gt_filter_tc(const void *Xb, int64_t n, int d, int dp, const void *Qb
     a.sel_B = mb ? mb->sel_B : nullptr;
     a.sel_pk = mb ? mb->sel_pk : nullptr;
     if (mb && (mb->W < 1 || mb->W > 4)) return -1;
-    // CTA-pair kernel: opt-in (NRLSH_GT_PAIR=1) — correct, but measured slower than
-    // the single-CTA N=256 kernel on c4 (0.84 vs 0.72 ms per 1024 queries: ~6.7K
-    // cycles per pair tile against 1.3K of MMA work)
-    const bool use_pair = Qb > GT_M && !mb && !tl && getenv("NRLSH_GT_PAIR") && atoi(getenv("NRLSH_GT_PAIR")) == 1 &&
-                          gp_smem_bytes(kblocks, 4, 0) <= 227 * 1024;
-    if (use_pair) {
-        CUtensorMap tq2, tx2;
-        if (!make_tmap(&tq2, Qb16, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dp, Qb, GT_KB, GT_M) ||
-            !make_tmap(&tx2, Xb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dp, n, GT_KB, GP_HN))
-            return -1;
-        int npairs = sms / 2;
-        a.nqp = (Qb + 2 * GT_M - 1) / (2 * GT_M);   // query groups of 256
-        // one unit per pair when the query groups divide the pairs (the pairs reading
-        // one split then run concurrently and share its L2 fetches)
-        if (npairs >= a.nqp && npairs % a.nqp) npairs -= npairs % a.nqp;
-        if (getenv("NRLSH_GT_PAIRS")) npairs = std::max(1, std::min(sms / 2, atoi(getenv("NRLSH_GT_PAIRS"))));
-        const int64_t ntiles = (n + GP_PN - 1) / GP_PN;
-        int nsplit = std::max(1, npairs / a.nqp);
-        nsplit = (int)std::min<int64_t>(nsplit, ntiles);
-        a.split_items = ((ntiles + nsplit - 1) / nsplit) * GP_PN;
-        a.nsplit = (int)((n + a.split_items - 1) / a.split_items);
-        // whole K per stage (one barrier round trip per tile) when three such stages fit
-        a.kps = (gp_smem_bytes(kblocks, 3, 0, kblocks) <= 227 * 1024) ? kblocks : 1;
-        if (getenv("NRLSH_GT_KPS")) a.kps = atoi(getenv("NRLSH_GT_KPS")) == 1 ? 1 : kblocks;
-        const int smin = a.kps == 1 ? 4 : 3;
-        a.stages = smin;
-        a.heap_smem = 0;
-        for (int st = GP_MAX_STAGES; st >= smin; --st)
-            if (gp_smem_bytes(kblocks, st, k, a.kps) <= 227 * 1024) { a.stages = st; a.heap_smem = 1; break; }
-        if (!a.heap_smem)
-            for (int st = GP_MAX_STAGES; st >= smin; --st)
-                if (gp_smem_bytes(kblocks, st, 0, a.kps) <= 227 * 1024) { a.stages = st; break; }
-        if (getenv("NRLSH_GT_STAGES")) {
-            a.stages = std::max(2, std::min(GP_MAX_STAGES, atoi(getenv("NRLSH_GT_STAGES"))));
-            a.heap_smem = gp_smem_bytes(kblocks, a.stages, k, a.kps) <= 227 * 1024;
-        }
-        const size_t sm = gp_smem_bytes(kblocks, a.stages, a.heap_smem ? k : 0, a.kps);
-        cudaFuncSetAttribute(gt_filter_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(2 * std::min(npairs, a.nqp * a.nsplit));
-        cfg.blockDim = dim3(GT_THREADS);
-        cfg.dynamicSmemBytes = sm;
-        cfg.stream = s;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = 2;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        if (cudaLaunchKernelEx(&cfg, gt_filter_pair, tq2, tx2, a) != cudaSuccess) return -1;
-        note_launch();
-        return 0;
-    }
     a.nqp = (Qb + GT_QB * GT_M - 1) / (GT_QB * GT_M);
     const int64_t ntiles = (n + NT - 1) / NT;
     int nsplit = std::max(1, sms / a.nqp);     // one unit per CTA: no tail wave

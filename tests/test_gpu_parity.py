@@ -543,22 +543,15 @@ def test_full_size_sampled(name, L, m):
         assert_topk_match(gt_ids[qi], gt_sc[qi], a, s, X, Q[qi])
 
 
-@pytest.mark.parametrize("scan", ["tensor", "popcount", "bitsliced"])
 @pytest.mark.parametrize("case", [("c4", 300_000, 32, 64, 128), ("scale", 70_000, 16, 128, 256),
-                                  ("tiny", None, None, 32, 8), ("c4", 300_000, 32, 32, 4),
-                                  ("c3", 40_000, 64, 64, 1)], ids=_ids)
-def test_candidates_parity_both_scans(built, case, scan, monkeypatch):
-    """The Hamming scans — the popcount one (the default), the tcgen05 int8 one
-    (scan_tc.cu, NRLSH_SCAN_TC=1) and the bit-sliced one (scan_bs.cu, NRLSH_SCAN_BS=1)
-    — give the oracle's candidate sets, ranks and
-    (R, id) order (identical codes injected), across budgets from 1 to n."""
-    monkeypatch.setenv("NRLSH_SCAN_TC", "1" if scan == "tensor" else "0")
-    monkeypatch.setenv("NRLSH_SCAN_BS", "1" if scan == "bitsliced" else "0")
+                                  ("tiny", None, None, 32, 8), ("c3", 40_000, 64, 64, 1)], ids=_ids)
+def test_candidates_parity_tensor_scan(built, case, monkeypatch):
+    """NEXT-3: the opt-in tcgen05 int8 Hamming scan (scan_tc.cu, NRLSH_SCAN_TC=1) gives
+    the oracle's candidate sets, ranks and (R, id) order (identical codes injected),
+    across budgets from 1 to n."""
+    monkeypatch.setenv("NRLSH_SCAN_TC", "1")
     cfg, X, Q, Xd, idx, orc = built(*case)
-    if scan == "bitsliced" and case[3] > 64:
-        pytest.skip("the bit-sliced scan covers codes of <= 64 bits")
-    if scan != "popcount":   # their code layouts are made at build time (opt-in)
-        idx = _P().Index(Xd, case[3], case[4], seed=cfg.seed)
+    idx = _P().Index(Xd, case[3], case[4], seed=cfg.seed)   # (its +-1 rows are made at build)
     n = X.shape[0]
     ocodes = orc.codes()
     idx.set_codes(ocodes[orc.perm])
@@ -576,52 +569,41 @@ def test_candidates_parity_both_scans(built, case, scan, monkeypatch):
             assert np.array_equal(grk[qi][order], ork), (T, qi)
 
 
-@pytest.mark.parametrize("case", [("c4", 300_000, 64, 64, 128), ("c2", None, 200, 64, 32),
-                                  ("scale", 70_000, 16, 128, 256)], ids=_ids)
-def test_rerank_bf16_filter_matches_fp32(built, case, monkeypatch):
-    """The certified bf16 first pass of the re-rank only skips candidates that cannot
-    enter the top-k: ids and fp32 scores equal the all-fp32 re-rank's, bit for bit."""
+@pytest.mark.parametrize("bound", ["default", "off", "always"])
+@pytest.mark.parametrize("case", [("c4", 300_000, 32, 64, 128), ("scale", 70_000, 16, 128, 256),
+                                  ("tiny", None, None, 32, 8), ("c4", 300_000, 32, 32, 4),
+                                  ("c3", 40_000, 64, 64, 1)], ids=_ids)
+def test_candidates_parity_scan_bound(built, case, bound, monkeypatch):
+    """The popcount scan's pair lower bound (sum over word pairs of
+    popcount((x_a ^ q_a) | (x_b ^ q_b)) <= h, tried first at small radii) changes no
+    candidate: with the bound at its default radii, off, and tried at every radius,
+    the candidate sets, ranks and (R, id) order equal the oracle's (identical codes
+    injected), across budgets from 1 to n."""
     P = _P()
-    monkeypatch.setenv("NRLSH_NO_DENSE", "1")    # both sides through the gather kernels
-    monkeypatch.setenv("NRLSH_RERANK_TC", "0")
-    cfg, X, Q, Xd, idx, orc = built(*case)
-    n = X.shape[0]
-    Qd = torch.from_numpy(Q[: min(len(Q), 64)]).cuda()
-    for T in sorted(set([cfg.k, max(cfg.k, n // 100), n // 7, n])):
-        monkeypatch.setenv("NRLSH_RERANK_BF16", "1")
-        a, sa = idx.query(Qd, cfg.k, T)
-        resc = P.last_rerank_stats()["rescored_fp32"]
-        monkeypatch.delenv("NRLSH_RERANK_BF16")
-        b, sb = idx.query(Qd, cfg.k, T)
-        assert np.array_equal(a.cpu().numpy(), b.cpu().numpy()), T
-        assert np.array_equal(sa.cpu().numpy(), sb.cpu().numpy()), T
-        assert resc <= Qd.shape[0] * min(T, n)
-
-
-@pytest.mark.parametrize("case", [("c4", 300_000, 64, 64, 128), ("tiny", None, None, 32, 8),
-                                  ("scale", 70_000, 16, 128, 256)], ids=_ids)
-def test_dense_rerank_path(built, case, monkeypatch):
-    """The opt-in dense re-rank of hot sub-datasets (rerank_dense.cu) returns the
-    oracle's top-k (identical codes injected), like the gather path."""
-    monkeypatch.setenv("NRLSH_DENSE", "1")
-    monkeypatch.setenv("NRLSH_DENSE_FRAC", "0.02")    # make several sub-datasets dense
+    monkeypatch.setenv("NRLSH_SCAN_LBMAX", {"default": "", "off": "-1", "always": "255"}[bound])
+    if bound == "default":
+        monkeypatch.delenv("NRLSH_SCAN_LBMAX")
     cfg, X, Q, Xd, idx, orc = built(*case)
     n = X.shape[0]
     ocodes = orc.codes()
     idx.set_codes(ocodes[orc.perm])
-    nq = min(len(Q), 24)
-    Qd = torch.from_numpy(Q[:nq]).cuda()
-    gq = idx.query_codes(Qd).cpu().numpy().view(np.uint32)
-    oq = oracle.query_codes(Q[:nq], orc.A)
-    same = band_mask(gq, oq)
-    for T in sorted(set([cfg.k, (n + 99) // 100, n // 7, n])):
-        ids, sc = idx.query(Qd, cfg.k, T)
-        ids, sc = ids.cpu().numpy(), sc.cpu().numpy()
+    qc = oracle.query_codes(Q, orc.A)
+    nq = min(len(Q), 16)
+    qcd = torch.from_numpy(qc[:nq].view(np.int32)).cuda()
+    for T in _budgets(cfg, n):
+        gid, grk = idx.candidates(T, qcodes=qcd)
+        gid = gid.cpu().numpy()
+        grk = grk.cpu().numpy().view(np.uint16)
         for qi in range(nq):
-            if not same[qi]:
-                continue
-            a, s = oracle.query(X, ocodes, orc.part, orc.R, orc.A, Q[qi], T, cfg.k)
-            assert_topk_match(ids[qi], sc[qi], a, s, X, Q[qi])
+            oid, ork = oracle.candidates(ocodes, orc.part, qc[qi], orc.R, T)
+            order = np.lexsort((gid[qi], grk[qi]))
+            assert np.array_equal(gid[qi][order], oid), (T, qi)
+            assert np.array_equal(grk[qi][order], ork), (T, qi)
+        st = P.last_scan_stats()
+        if bound == "always" and case[3] > 32:
+            assert st["bound_pairs"] > 0
+        if bound == "off" or case[3] <= 32:
+            assert st["bound_pairs"] == 0
 
 
 def test_small_last_sub_batch_large_budget(built):
@@ -699,23 +681,6 @@ def test_rerank_tensor_matches_gather(built, case, monkeypatch):
     monkeypatch.setenv("NRLSH_RERANK_TC", "0")
     gi, gs = idx.query(Qd, cfg.k, T)
     assert torch.equal(gi, ti) and torch.equal(gs.view(torch.int32), ts.view(torch.int32))
-
-
-@pytest.mark.parametrize("name,n,nq,k", [("c4", 300_000, 300, 10), ("c3", 40_000, 260, 100)])
-def test_exact_topk_cta_pair_kernel(name, n, nq, k, monkeypatch):
-    """The opt-in CTA-pair (cta_group::2) ground-truth filter returns exactly the
-    single-CTA kernel's top-k (ids and fp32 scores), over a ragged query count."""
-    P = _P()
-    cfg, X, Q = dataset(workloads.CONFIGS[name], n, nq)
-    Xd, Qd = torch.from_numpy(X).cuda(), torch.from_numpy(Q).cuda()
-    monkeypatch.setenv("NRLSH_GT_PAIR", "0")
-    a, sa = P.exact_topk(Xd, Qd, k)
-    monkeypatch.setenv("NRLSH_GT_PAIR", "1")
-    b, sb = P.exact_topk(Xd, Qd, k)
-    assert torch.equal(a, b) and torch.equal(sa.view(torch.int32), sb.view(torch.int32))
-    for qi in (0, nq - 1):
-        ids, s = oracle.exact_topk(X, Q[qi], k)
-        assert_topk_match(b[qi].cpu().numpy(), sb[qi].cpu().numpy(), ids, s, X, Q[qi])
 
 
 @pytest.mark.parametrize("case", [("c4", 300_000, 32, 64, 128), ("scale", 70_000, 16, 128, 256),

@@ -9,7 +9,7 @@ import json
 import sys
 
 SLOTS = [("k6_pilot", "pilot"), ("k6_scan", "scan"), ("k7_select", "select"), ("k1_norms", "norms"),
-         ("k3_codes_tc", "codes")]
+         ("k3_codes", "codes")]
 
 
 def per_slot(rows, mapping):
