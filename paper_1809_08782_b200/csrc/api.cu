@@ -112,9 +112,13 @@ void make_rank_table(const std::vector<double> &U, int L, double eps, std::vecto
     struct E { double s, u; int j, h; };
     std::vector<E> es;
     es.reserve((size_t)m * (L + 1));
+    // (cos(pi (1 - eps) h / L) depends on h only: evaluated once per h, the same
+    // fp64 value as in the product below)
+    std::vector<double> ch(L + 1);
+    for (int h = 0; h <= L; ++h) ch[h] = std::cos(M_PI * (1.0 - eps) * (double)h / (double)L);
     for (int j = 0; j < m; ++j)
         for (int h = 0; h <= L; ++h)
-            es.push_back({U[j] * std::cos(M_PI * (1.0 - eps) * (double)h / (double)L), U[j], j, h});
+            es.push_back({U[j] * ch[h], U[j], j, h});
     std::sort(es.begin(), es.end(), [](const E &a, const E &b) {
         if (a.s != b.s) return a.s > b.s;
         if (a.u != b.u) return a.u > b.u;
@@ -183,9 +187,11 @@ struct OutBuf {
 namespace nrlsh {
 // Stream-ordered allocations come from a private pool per device (not the
 // process-wide default pool a PyTorch allocator in the same process may rely on).
-// It keeps up to 8 GiB of freed memory cached across calls (query workspaces are
-// ~2.5 GB and are reallocated every call) and returns the rest to the driver at
-// the next synchronisation.
+// It keeps up to 24 GiB of freed memory cached across calls (query workspaces are
+// ~2.5 GB and are reallocated every call, an index of the scale config holds ~5 GB:
+// below the footprint of a build + query + ground-truth cycle the pool would unmap
+// and re-map memory every cycle, ~10-40 ms at scale) and returns the rest to the
+// driver at the next synchronisation.
 cudaError_t dmalloc(void **p, size_t bytes, cudaStream_t s) {
     static std::mutex mu;
     static cudaMemPool_t pools[128] = {};
@@ -202,7 +208,7 @@ cudaError_t dmalloc(void **p, size_t bytes, cudaStream_t s) {
             pr.location.type = cudaMemLocationTypeDevice;
             pr.location.id = dev;
             if ((e = cudaMemPoolCreate(&pools[dev], &pr))) { pools[dev] = nullptr; return e; }
-            uint64_t thr = 8ull << 30;
+            uint64_t thr = 24ull << 30;
             cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &thr);
         }
         pool = pools[dev];
@@ -499,6 +505,7 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
     // K4b (host): the sorted (U_j, l) structure and the work lists
     std::vector<int32_t> order;
     make_rank_table(ix->U, L, ix->eps, ix->R_h, order);
+    tr("rank table");
     // scan work units: chunks of <= scan_chunk_items() positions inside one sub-dataset
     std::vector<int4> chunks;
     const int CH = scan_chunk_items();
@@ -507,20 +514,47 @@ nrlsh_status nrlsh_build_ex(const float *items, int64_t n, int32_t d, int32_t co
             chunks.push_back(make_int4(j, (int)p, (int)std::min<int64_t>(p + CH, ix->offsets[j + 1]), 0));
     ix->nchunks = (int32_t)chunks.size();
     // tiles of <= 128 positions of one sub-dataset: the code kernel's with per-sub-
-    // dataset projections, the (opt-in) tensor-core scan's items
+    // dataset projections, the (opt-in) tensor-core scan's items (built only for them)
     std::vector<int4> ctiles;
-    for (int j = 0; j < m; ++j)
-        for (int64_t p = ix->offsets[j]; p < ix->offsets[j + 1]; p += 128)
-            ctiles.push_back(make_int4(j, (int)p, (int)std::min<int64_t>(p + 128, ix->offsets[j + 1]), 0));
+    if (QM > 1 || ix->codes_pm)
+        for (int j = 0; j < m; ++j)
+            for (int64_t p = ix->offsets[j]; p < ix->offsets[j + 1]; p += 128)
+                ctiles.push_back(make_int4(j, (int)p, (int)std::min<int64_t>(p + 128, ix->offsets[j + 1]), 0));
     ix->nctiles = (int32_t)ctiles.size();
-    NR_ALLOC(ix->ctiles_d, ctiles.size() * sizeof(int4));
+    tr("work lists");
+    if (!ctiles.empty()) NR_ALLOC(ix->ctiles_d, ctiles.size() * sizeof(int4));
     NR_ALLOC(ix->R_d, ix->R_h.size() * 2);
     NR_ALLOC(ix->order_d, order.size() * 4);
     NR_ALLOC(ix->chunks_d, chunks.size() * sizeof(int4));
-    cudaMemcpyAsync(ix->ctiles_d, ctiles.data(), ctiles.size() * sizeof(int4), cudaMemcpyHostToDevice, s);
-    cudaMemcpyAsync(ix->R_d, ix->R_h.data(), ix->R_h.size() * 2, cudaMemcpyHostToDevice, s);
-    cudaMemcpyAsync(ix->order_d, order.data(), order.size() * 4, cudaMemcpyHostToDevice, s);
-    cudaMemcpyAsync(ix->chunks_d, chunks.data(), chunks.size() * sizeof(int4), cudaMemcpyHostToDevice, s);
+    {   // the tables go through pinned staging: a pageable H2D copy larger than the
+        // driver's staging buffer would block the host until the stream reaches it
+        // (after the code kernel), and the launches behind it would wait too
+        const size_t b_ct = ctiles.size() * sizeof(int4), b_R = ix->R_h.size() * 2,
+                     b_or = order.size() * 4, b_ch = chunks.size() * sizeof(int4);
+        const size_t tot = b_ct + b_R + b_or + b_ch + 64;
+        thread_local void *tpin = nullptr;
+        thread_local size_t tpin_bytes = 0;
+        if (tpin_bytes < tot) {
+            if (tpin) cudaFreeHost(tpin);
+            tpin = nullptr;
+            tpin_bytes = 0;
+            if (cudaMallocHost(&tpin, std::max<size_t>(tot, 1 << 20)) != cudaSuccess) {
+                cudaGetLastError();
+                return fail(NRLSH_ENOMEM, "pinned table staging");
+            }
+            tpin_bytes = std::max<size_t>(tot, 1 << 20);
+        }
+        tr("table allocs");
+        uint8_t *h = static_cast<uint8_t *>(tpin);
+        std::memcpy(h, ctiles.data(), b_ct);
+        std::memcpy(h + b_ct, ix->R_h.data(), b_R);
+        std::memcpy(h + b_ct + b_R, order.data(), b_or);
+        std::memcpy(h + b_ct + b_R + b_or, chunks.data(), b_ch);
+        if (b_ct) cudaMemcpyAsync(ix->ctiles_d, h, b_ct, cudaMemcpyHostToDevice, s);
+        cudaMemcpyAsync(ix->R_d, h + b_ct, b_R, cudaMemcpyHostToDevice, s);
+        cudaMemcpyAsync(ix->order_d, h + b_ct + b_R, b_or, cudaMemcpyHostToDevice, s);
+        cudaMemcpyAsync(ix->chunks_d, h + b_ct + b_R + b_or, b_ch, cudaMemcpyHostToDevice, s);
+    }
     if (QM > 1) {   // K3 with per-sub-dataset projections: partition-ordered tiles
         ProfScope p(SLOT_CODES, s);
         launch_item_codes_tc(ix->X, n, d, ix->norm2, ix->part_of_id, ix->V_d, ix->Apad, L, W,
