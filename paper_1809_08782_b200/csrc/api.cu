@@ -638,7 +638,7 @@ void run_candidates(const nrlsh_index *ix, const float *Qd, const uint32_t *qcod
     }
     {
         ProfScope p(SLOT_PILOT, s);
-        launch_pilot(ix, qcodes, Qb, Tq, stride, delta, cnt, s);
+        launch_pilot(ix, qcodes, Qb, Tq, stride, delta, cnt, s, fallback_counter(ix, fb_ws));
     }
     if (getenv("NRLSH_TEST_FORCE_FALLBACK"))   // test switch: empty pilot bound -> fallback
         cudaMemsetAsync(delta, 0xff, (size_t)Qb * ix->m, s);
@@ -1045,7 +1045,8 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
     const int64_t ns = use_tc ? 1 : (n + S - 1) / S;
     const int64_t Cg = use_tc ? std::min<int64_t>(n, std::max<int64_t>(16384, 256 * (int64_t)k))
                               : std::min<int64_t>(n, std::max<int64_t>(4 * (int64_t)S * k + 4096, 2 * k));
-    int Qmax = (int)std::min<int64_t>(1024, nq);
+    const int64_t gt_batch = getenv("NRLSH_GT_BATCH") ? std::max(64, atoi(getenv("NRLSH_GT_BATCH"))) : 1024;
+    int Qmax = (int)std::min<int64_t>(gt_batch, nq);
     while (Qmax > 64 && (int64_t)Qmax * (ns * 4 + Cg * 8) > ((int64_t)2500 << 20)) Qmax >>= 1;
     DBuf xn, qn, ss, lb, tid, tsc, cc, cd, cs, xb, qb, th, pt, hp, tw, gqp, gqb, gqn, gst, gov;
     const int64_t npad = (n + 255) / 256 * 256;   // |x| padded: the tc kernel bulk-loads 1 KB tiles

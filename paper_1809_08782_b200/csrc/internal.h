@@ -129,17 +129,6 @@ void launch_item_codes_tc(const float *X, int64_t n, int d, const double *norm2,
                           const int32_t *perm = nullptr, int m = 0);
 
 // ---------------------------------------------------------------- query
-struct QueryWS {
-    uint32_t *qcodes;   // [Qb x W]
-    int8_t *delta;      // [Qb x m]
-    uint32_t *cnt;      // [Qb]
-    unsigned long long *buf;  // [Qb x C]  (R << 32 | pos)
-    int32_t *cand;      // [Qb x Tq]   item ids
-    uint16_t *cand_rank;// [Qb x Tq]   (optional)
-    float *scores;      // [Qb x Tq]
-    int *flags;         // [4]: zero-norm min index, nonfinite min index, fallback count
-    int64_t C;          // buffer capacity per query
-};
 
 // qcodes [nq x QM x W]: QM = 1 (Apad = A) or m (Apad = [m x (d+1) x 32W], code j under A_j)
 void launch_qcodes(const float *Q, int64_t nq, int d, const float *Apad, int L, int W,
@@ -148,8 +137,9 @@ void launch_qcodes(const float *Q, int64_t nq, int d, const float *Apad, int L, 
 int pilot_stride(int64_t n);
 void launch_gather_sample(const nrlsh_index *ix, int stride, uint32_t *sc, uint8_t *sp,
                           cudaStream_t s);
+// zero_word (nullable): zeroed by the pilot (the fallback's counter, fallback_counter())
 void launch_pilot(const nrlsh_index *ix, const uint32_t *qcodes, int Qb, int64_t Tq,
-                  int stride, int8_t *delta, uint32_t *cnt, cudaStream_t s);
+                  int stride, int8_t *delta, uint32_t *cnt, cudaStream_t s, uint32_t *zero_word = nullptr);
 // lbc (nullable): [0] pairs the one-POPC lower bound ran on, [1] pairs it decided alone
 void launch_scan(const nrlsh_index *ix, const uint32_t *qcodes, const int8_t *delta, int Qb,
                  unsigned long long *buf, uint32_t *cnt, int64_t C,
@@ -159,6 +149,7 @@ void launch_scan(const nrlsh_index *ix, const uint32_t *qcodes, const int8_t *de
 // ws: fallback_ws_bytes() of zeroed scratch for the all-SM re-do of failed queries
 // (nullptr: one CTA per failed query only)
 size_t fallback_ws_bytes(const nrlsh_index *ix);
+uint32_t *fallback_counter(const nrlsh_index *ix, void *ws);
 void launch_fallback(const nrlsh_index *ix, const uint32_t *qcodes, int Qb, int64_t Tq,
                      unsigned long long *buf, uint32_t *cnt, uint32_t *cntv, int64_t C,
                      int *flags, void *ws, cudaStream_t s);

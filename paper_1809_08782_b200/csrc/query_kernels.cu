@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(1024) k6_pilot(
     const uint32_t *__restrict__ qcodes, int L, int m,
     const int32_t *__restrict__ order, const uint16_t *__restrict__ R, uint32_t need,
     int8_t *__restrict__ delta, uint32_t *__restrict__ cnt, int interleaved, int64_t ns_real,
-    int QM) {
+    int QM, uint32_t *__restrict__ zero_word) {
     pdl_wait();
     extern __shared__ uint32_t hist[];   // [NR] (+ [QM x W] query codes, per-sub-dataset A_j)
     __shared__ uint32_t ws[32];
@@ -315,10 +315,12 @@ __global__ void __launch_bounds__(1024) k6_pilot(
         delta[q * m + j] = (int8_t)(c - 1);
     }
     if (threadIdx.x == 0) cnt[q] = 0u;
+    // (the fallback's failed-query counter, zeroed here instead of by a memset node)
+    if (zero_word && q == 0 && threadIdx.x == 0) *zero_word = 0u;
 }
 
 void launch_pilot(const nrlsh_index *ix, const uint32_t *qcodes, int Qb, int64_t Tq, int stride,
-                  int8_t *delta, uint32_t *cnt, cudaStream_t s) {
+                  int8_t *delta, uint32_t *cnt, cudaStream_t s, uint32_t *zero_word) {
     // target: T plus 4 standard deviations of the sampled estimate (+ one stride of
     // discreteness); exact (= T) when stride == 1.
     double target = (double)Tq;
@@ -340,15 +342,15 @@ void launch_pilot(const nrlsh_index *ix, const uint32_t *qcodes, int Qb, int64_t
     switch (ix->W) {
         case 1:
             cudaFuncSetAttribute(k6_pilot<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            launch_pdl(k6_pilot<1>, dim3(Qb), dim3(1024), sm, s, sc, sp, ns, qcodes, ix->L, ix->m, order, ix->R_d, need, delta, cnt, cmp, (ix->n + stride - 1) / stride, ix->QM);
+            launch_pdl(k6_pilot<1>, dim3(Qb), dim3(1024), sm, s, sc, sp, ns, qcodes, ix->L, ix->m, order, ix->R_d, need, delta, cnt, cmp, (ix->n + stride - 1) / stride, ix->QM, zero_word);
             break;
         case 2:
             cudaFuncSetAttribute(k6_pilot<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            launch_pdl(k6_pilot<2>, dim3(Qb), dim3(1024), sm, s, sc, sp, ns, qcodes, ix->L, ix->m, order, ix->R_d, need, delta, cnt, cmp, (ix->n + stride - 1) / stride, ix->QM);
+            launch_pdl(k6_pilot<2>, dim3(Qb), dim3(1024), sm, s, sc, sp, ns, qcodes, ix->L, ix->m, order, ix->R_d, need, delta, cnt, cmp, (ix->n + stride - 1) / stride, ix->QM, zero_word);
             break;
         default:
             cudaFuncSetAttribute(k6_pilot<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            launch_pdl(k6_pilot<4>, dim3(Qb), dim3(1024), sm, s, sc, sp, ns, qcodes, ix->L, ix->m, order, ix->R_d, need, delta, cnt, cmp, (ix->n + stride - 1) / stride, ix->QM);
+            launch_pdl(k6_pilot<4>, dim3(Qb), dim3(1024), sm, s, sc, sp, ns, qcodes, ix->L, ix->m, order, ix->R_d, need, delta, cnt, cmp, (ix->n + stride - 1) / stride, ix->QM, zero_word);
             break;
     }
     note_launch();
@@ -786,6 +788,12 @@ size_t fallback_ws_bytes(const nrlsh_index *ix) {
     return ((size_t)kFbMax * ix->m * (ix->L + 1) + 2 * kFbMax + 64) * 4;
 }
 
+uint32_t *fallback_counter(const nrlsh_index *ix, void *ws) {
+    if (!ws) return nullptr;
+    const int NR = ix->m * (ix->L + 1);
+    return reinterpret_cast<uint32_t *>(ws) + (size_t)kFbMax * NR + 2 * kFbMax;
+}
+
 void launch_fallback(const nrlsh_index *ix, const uint32_t *qcodes, int Qb, int64_t Tq,
                      unsigned long long *buf, uint32_t *cnt, uint32_t *cntv, int64_t C,
                      int *flags, void *ws, cudaStream_t s) {
@@ -798,8 +806,7 @@ void launch_fallback(const nrlsh_index *ix, const uint32_t *qcodes, int Qb, int6
         uint32_t *ghist = reinterpret_cast<uint32_t *>(ws);   // [kFbMax x NR], zero between uses
         int32_t *fl = reinterpret_cast<int32_t *>(ghist + (size_t)kFbMax * NR);
         uint32_t *Bq = reinterpret_cast<uint32_t *>(fl + kFbMax);
-        uint32_t *nf = Bq + kFbMax;
-        cudaMemsetAsync(nf, 0, 4, s);
+        uint32_t *nf = Bq + kFbMax;   // (zeroed by the pilot: fallback_counter)
         launch_pdl(fb_list, dim3((Qb + 255) / 256), dim3(256), 0, s, cnt, cv_sep, Qb, Tq, C, fl, nf, flags);
         const size_t sm = (size_t)NR * 4;
         const int QM = ix->QM;
@@ -852,11 +859,22 @@ __global__ void __launch_bounds__(1024) k7_select(
     __shared__ uint32_t ws[32];
     __shared__ uint32_t h256[256];
     __shared__ int sB, s_bseed;
-    __shared__ uint32_t sLt, s_out, s_pfx, s_kth, s_seed;
+    __shared__ uint32_t sLt, s_out, s_pfx, s_kth, s_seed, s_tlo, s_thi;
     const int q = blockIdx.x;
     const int64_t c = min((int64_t)cnt[q], C);
     const unsigned long long *b = buf + (int64_t)q * C;
-    for (int e = threadIdx.x; e < NR; e += blockDim.x) { hist[e] = 0u; sRt[e] = R[e]; }
+    {   // zero the histogram, copy R (16-byte accesses; R is 16-byte aligned)
+        const int nv = NR / 8;
+        const uint4 *R4 = reinterpret_cast<const uint4 *>(R);
+        uint4 *sR4 = reinterpret_cast<uint4 *>(sRt);
+        uint4 *h4 = reinterpret_cast<uint4 *>(hist);
+        for (int e = threadIdx.x; e < nv; e += blockDim.x) {
+            sR4[e] = __ldg(R4 + e);
+            h4[2 * e] = make_uint4(0u, 0u, 0u, 0u);
+            h4[2 * e + 1] = make_uint4(0u, 0u, 0u, 0u);
+        }
+        for (int e = nv * 8 + threadIdx.x; e < NR; e += blockDim.x) { hist[e] = 0u; sRt[e] = R[e]; }
+    }
     if (threadIdx.x == 0) { sB = NR - 1; sLt = 0; s_out = 0; s_bseed = NR - 1; }
     __syncthreads();
     // entries carry the flat (j, h) index f; the histogram is kept per f (one shared
@@ -929,7 +947,7 @@ __global__ void __launch_bounds__(1024) k7_select(
     // the need_eq-th smallest position among the ties (R == B): when they fit, one
     // pass gathers them into shared memory (reusing the histogram's space) and a
     // radix select runs there; otherwise radix select over the buffer, 8 bits/round
-    if (threadIdx.x == 0) { s_pfx = 0; s_kth = need_eq; s_out = 0; }
+    if (threadIdx.x == 0) { s_pfx = 0; s_kth = need_eq; s_out = 0; s_tlo = 0xffffffffu; s_thi = 0u; }
     __syncthreads();
     uint32_t *teq = hist;   // the histogram is dead once B and n_eq are known
     const bool in_smem = need_eq < n_eq && n_eq <= (uint32_t)tie_cap;
@@ -970,7 +988,29 @@ __global__ void __launch_bounds__(1024) k7_select(
             for (int64_t e = threadIdx.x; e < c; e += blockDim.x) take(b[e]);
         }
         __syncthreads();
-        for (int shift = 24; shift >= 0; shift -= 8) {
+        // the ties share one sub-dataset (a contiguous position range): the radix
+        // select starts at the highest byte where their positions differ, with the
+        // common prefix above it
+        {
+            uint32_t lo = 0xffffffffu, hi = 0u;
+            for (uint32_t e = threadIdx.x; e < n_eq; e += blockDim.x) {
+                const uint32_t pos = teq[e];
+                lo = min(lo, pos);
+                hi = max(hi, pos);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                lo = min(lo, __shfl_xor_sync(NR_FULL, lo, o));
+                hi = max(hi, __shfl_xor_sync(NR_FULL, hi, o));
+            }
+            if ((threadIdx.x & 31) == 0) { atomicMin(&s_tlo, lo); atomicMax(&s_thi, hi); }
+        }
+        __syncthreads();
+        const uint32_t tdiff = s_tlo ^ s_thi;
+        const int shift0 = tdiff ? ((31 - __clz(tdiff)) / 8) * 8 : 0;
+        if (threadIdx.x == 0 && shift0 < 24) s_pfx = s_tlo & (0xffffffffu << (shift0 + 8));
+        __syncthreads();
+        for (int shift = shift0; shift >= 0; shift -= 8) {
             for (int e = threadIdx.x; e < 256; e += blockDim.x) h256[e] = 0;
             __syncthreads();
             const uint32_t pfx = s_pfx;
