@@ -567,6 +567,22 @@ def run_native(args):
              for name, v in prof.items() if v[1] > 0}
     roof, scan_roof, others, build_roof, query_roof = rooflines(r, cfg, L, m, nq, T, args.steps,
                                                                 peaks, peaks_src)
+    # the same kernels with the sub-batches on one stream (after the timed region,
+    # untimed): in the timed region two sub-batches share the GPU, so each kernel's
+    # CUDA-event duration there includes the other stream's work
+    iso = None
+    if world == 1:
+        os.environ["NRLSH_QUERY_SERIAL"] = "1"
+        try:
+            ri = measure_path(P, torch, cfg, L, m, T, Xd, Qd, 2, 1, stream, flush)
+        finally:
+            del os.environ["NRLSH_QUERY_SERIAL"]
+        iroof, iscan, iothers, _, _ = rooflines(ri, cfg, L, m, nq, T, 2, peaks, peaks_src)
+        iso = {"note": "sub-batches serialised on one stream (NRLSH_QUERY_SERIAL=1), 2 untimed "
+                       "steps after the timed region: kernel efficiency without stream overlap",
+               "ms_per_step": ri["ms_step"], "roofline": iroof, "scan_roofline": iscan,
+               "other_rooflines": iothers,
+               "stage_ms_per_step": {nm: v[0] / 2 for nm, v in ri["prof"].items() if v[1] > 0}}
 
     # -------- scale (BASELINE configs[4]) in the same run: a sub-record, not the headline
     scale = None
@@ -617,6 +633,7 @@ def run_native(args):
         "stage_ms_per_step": stage,
         "phase_ms_per_step": {"build": r["build_ms"], "query": r["query_ms"], "ground_truth": r["gt_ms"]},
         "roofline": roof, "scan_roofline": scan_roof, "other_rooflines": others,
+        "rooflines_serial_stream": iso,
         "build_roofline": build_roof, "query_roofline": query_roof,
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(r["launches"]),
         "latency_mode": latency,

@@ -737,11 +737,14 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
     }
     // Sub-batches alternate between two streams with a workspace set each, so one
     // sub-batch's kernels fill the other's gaps and tails (NRLSH_QUERY_SERIAL=1: one)
-    const int NSET = (nq > Qmax && !getenv("NRLSH_QUERY_SERIAL")) ? 2 : 1;
+    // (NRLSH_QUERY_STREAMS: 1-3, default 2)
+    int NSET = getenv("NRLSH_QUERY_STREAMS") ? std::max(1, std::min(3, atoi(getenv("NRLSH_QUERY_STREAMS")))) : 2;
+    if (nq <= Qmax || getenv("NRLSH_QUERY_SERIAL")) NSET = 1;
+    NSET = (int)std::min<int64_t>(NSET, (nq + Qmax - 1) / Qmax);
     struct WSet {
         DBuf qc, dl, cn, cv, ba, bf, cd, pt, fbw;
         DBuf rsb, rspk, rseed, rtid, rtsc, rth, rqb, rqn, rhp, rcd, rcc, rpt, rtl, rqp;
-    } wsets[2];
+    } wsets[3];
     DBuf fl;
     if (fl.alloc(64, s)) return fail(NRLSH_ENOMEM, "query workspace");
     for (int w = 0; w < NSET; ++w) {
@@ -822,22 +825,25 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
     unsigned long long *pairs = (unsigned long long *)(fl.get<int>() + 4);
     const long long launches0 = launch_count();
     // second stream (per thread and device) joined to s by events
-    cudaStream_t st[2] = {s, s};
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-    if (NSET == 2) {
-        thread_local cudaStream_t st2[128] = {};
+    cudaStream_t st[3] = {s, s, s};
+    cudaEvent_t ev_fork = nullptr, ev_join[3] = {nullptr, nullptr, nullptr};
+    if (NSET > 1) {
+        thread_local cudaStream_t extra[128][2] = {};
         int dev = 0;
         cudaGetDevice(&dev);
         if (dev < 0 || dev >= 128) return fail(NRLSH_ECUDA, "device index");
-        if (!st2[dev] && cudaStreamCreateWithFlags(&st2[dev], cudaStreamNonBlocking) != cudaSuccess) {
-            cudaGetLastError();
-            return fail(NRLSH_ECUDA, "stream create");
-        }
-        st[1] = st2[dev];
         cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming);
         cudaEventRecord(ev_fork, s);
-        cudaStreamWaitEvent(st[1], ev_fork, 0);
+        for (int w = 1; w < NSET; ++w) {
+            if (!extra[dev][w - 1] &&
+                cudaStreamCreateWithFlags(&extra[dev][w - 1], cudaStreamNonBlocking) != cudaSuccess) {
+                cudaGetLastError();
+                return fail(NRLSH_ECUDA, "stream create");
+            }
+            st[w] = extra[dev][w - 1];
+            cudaEventCreateWithFlags(&ev_join[w], cudaEventDisableTiming);
+            cudaStreamWaitEvent(st[w], ev_fork, 0);
+        }
     }
     int sbi = 0;
     for (int64_t q0 = 0; q0 < nq; q0 += Qmax, ++sbi) {
@@ -919,11 +925,13 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
                           (float *)os.dev + q0 * k, s);
         }
     }
-    if (NSET == 2) {
-        cudaEventRecord(ev_join, st[1]);
-        cudaStreamWaitEvent(s, ev_join, 0);
+    if (NSET > 1) {
+        for (int w = 1; w < NSET; ++w) {
+            cudaEventRecord(ev_join[w], st[w]);
+            cudaStreamWaitEvent(s, ev_join[w], 0);
+            cudaEventDestroy(ev_join[w]);
+        }
         cudaEventDestroy(ev_fork);
-        cudaEventDestroy(ev_join);
     }
     if (use_rtc) {   // queries whose survivor list overflowed (rare): the gather path
         uint32_t nov = 0;
@@ -1100,27 +1108,39 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
     const int64_t gt_batch = getenv("NRLSH_GT_BATCH") ? std::max(64, atoi(getenv("NRLSH_GT_BATCH"))) : 4096;
     int Qmax = (int)std::min<int64_t>(gt_batch, nq);
     while (Qmax > 64 && (int64_t)Qmax * (ns * 4 + Cg * 8) > ((int64_t)2500 << 20)) Qmax >>= 1;
-    DBuf xn, qn, ss, lb, tid, tsc, cc, cd, cs, xb, qb, th, pt, hp, tw, gqp, gqb, gqn, gst, gov;
+    // sub-batches alternate between two streams with a workspace set each (as the
+    // query's; NRLSH_QUERY_SERIAL=1: one)
+    const int NSET = (nq > Qmax && !getenv("NRLSH_QUERY_SERIAL")) ? 2 : 1;
+    struct GSet { DBuf ss, lb, tid, tsc, cc, cd, cs, th, pt, hp, tw, gqp, gqb, gqn; } gsets[2];
+    DBuf xn, qn, xb, qb, gst, gov;
     const int64_t npad = (n + 255) / 256 * 256;   // |x| padded: the tc kernel bulk-loads 1 KB tiles
-    if (xn.alloc((size_t)npad * 4, s) || qn.alloc((size_t)nq * 4, s) ||
-        ss.alloc((size_t)Qmax * ns * 4, s) || lb.alloc((size_t)Qmax * 4, s) ||
-        tid.alloc((size_t)Qmax * k * 8, s) || tsc.alloc((size_t)Qmax * k * 4, s) ||
-        cc.alloc((size_t)Qmax * 4, s) || cd.alloc((size_t)Qmax * Cg * 4, s) ||
-        cs.alloc((size_t)Qmax * Cg * 4, s) || th.alloc((size_t)Qmax * 4, s) ||
-        pt.alloc(std::max(rerank_partial_bytes(Qmax, Cg, k), rerank_partial_bytes(1, n, k)), s) ||
-        gst.alloc(40, s) || gov.alloc((size_t)nq * 8, s))
+    if (xn.alloc((size_t)npad * 4, s) || qn.alloc((size_t)nq * 4, s) || gst.alloc(40, s) ||
+        gov.alloc((size_t)nq * 8, s))
         return fail(NRLSH_ENOMEM, "exact_topk workspace");
+    for (int w = 0; w < NSET; ++w) {
+        GSet &G = gsets[w];
+        if (G.ss.alloc((size_t)Qmax * ns * 4, s) || G.lb.alloc((size_t)Qmax * 4, s) ||
+            G.tid.alloc((size_t)Qmax * k * 8, s) || G.tsc.alloc((size_t)Qmax * k * 4, s) ||
+            G.cc.alloc((size_t)Qmax * 4, s) || G.cd.alloc((size_t)Qmax * Cg * 4, s) ||
+            G.cs.alloc((size_t)Qmax * Cg * 4, s) || G.th.alloc((size_t)Qmax * 4, s) ||
+            G.pt.alloc(std::max(rerank_partial_bytes(Qmax, Cg, k), rerank_partial_bytes(1, n, k)), s))
+            return fail(NRLSH_ENOMEM, "exact_topk workspace");
+    }
     cudaMemsetAsync(gst.p, 0, 40, s);
     // bf16 item rows and |x|: the index's (written by its build), else prepared here
     const void *Xbp = Xb_ix;
     const float *xnp = xnorm_ix;
     if (use_tc) {
-        if ((!Xbp && xb.alloc((size_t)n * dp * 2, s)) || qb.alloc((size_t)nq * dp * 2, s) ||
-            hp.alloc(gt_heap_bytes(k), s) ||
-            (Xb_ix && tile_xmax_ix &&
-             (tw.alloc(gt_tile_ws_bytes(n, Qmax), s) || gqp.alloc((size_t)Qmax * 4, s) ||
-              gqb.alloc((size_t)Qmax * dp * 2, s) || gqn.alloc((size_t)Qmax * 4, s))))
+        if ((!Xbp && xb.alloc((size_t)n * dp * 2, s)) || qb.alloc((size_t)nq * dp * 2, s))
             return fail(NRLSH_ENOMEM, "exact_topk bf16 workspace");
+        for (int w = 0; w < NSET; ++w) {
+            GSet &G = gsets[w];
+            if (G.hp.alloc(gt_heap_bytes(k), s) ||
+                (Xb_ix && tile_xmax_ix &&
+                 (G.tw.alloc(gt_tile_ws_bytes(n, Qmax), s) || G.gqp.alloc((size_t)Qmax * 4, s) ||
+                  G.gqb.alloc((size_t)Qmax * dp * 2, s) || G.gqn.alloc((size_t)Qmax * 4, s))))
+                return fail(NRLSH_ENOMEM, "exact_topk bf16 workspace");
+        }
         ProfScope p(SLOT_GT_NORMS, s);
         if (!Xbp) {
             cudaMemsetAsync(xn.get<float>() + n, 0, (size_t)(npad - n) * 4, s);
@@ -1138,13 +1158,36 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
     // largest |x| can reach the pair's seeded bound (GtTiles)
     GtTiles gtl;
     gtl.xmax128 = tile_xmax_ix;
-    gtl.ws = tw.get<int32_t>();
+    gtl.ws = nullptr;   // (per workspace set, below)
     gtl.pairs = gst.get<unsigned long long>() + 4;   // (query, item) pairs multiplied
     gtl.xsplit = getenv("NRLSH_GT_ONEPASS") ? 0.f : xsplit_ix;
     gtl.pass = 0;
     gtl.qperm = nullptr;
-    for (int64_t q0 = 0; q0 < nq; q0 += Qmax) {
+    cudaStream_t st[2] = {s, s};
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    if (NSET == 2) {
+        thread_local cudaStream_t extra[128] = {};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev < 0 || dev >= 128) return fail(NRLSH_ECUDA, "device index");
+        if (!extra[dev] && cudaStreamCreateWithFlags(&extra[dev], cudaStreamNonBlocking) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(NRLSH_ECUDA, "stream create");
+        }
+        st[1] = extra[dev];
+        cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming);
+        cudaEventRecord(ev_fork, s);
+        cudaStreamWaitEvent(st[1], ev_fork, 0);
+    }
+    int sbi = 0;
+    for (int64_t q0 = 0; q0 < nq; q0 += Qmax, ++sbi) {
         const int Qb = (int)std::min<int64_t>(Qmax, nq - q0);
+        GSet &G = gsets[sbi % NSET];
+        cudaStream_t s = st[sbi % NSET];   // (this sub-batch's stream)
+        DBuf &ss = G.ss, &lb = G.lb, &tid = G.tid, &tsc = G.tsc, &cc = G.cc, &cd = G.cd, &th = G.th,
+             &pt = G.pt, &hp = G.hp, &gqp = G.gqp, &gqb = G.gqb, &gqn = G.gqn;
+        gtl.ws = G.tw.get<int32_t>();
         const float *Qb_ptr = Q + q0 * d;
         const float *qnb = qn.get<float>() + q0;
         int64_t *oid = (int64_t *)oi.dev + q0 * k;
@@ -1223,6 +1266,12 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
         launch_collect_overflow(cc.get<uint32_t>(), Qb, Cg, q0, gov.get<int64_t>(),
                                 (uint32_t *)(gst.get<unsigned long long>() + 2), s);
     }
+    if (NSET == 2) {
+        cudaEventRecord(ev_join, st[1]);
+        cudaStreamWaitEvent(s, ev_join, 0);
+        cudaEventDestroy(ev_fork);
+        cudaEventDestroy(ev_join);
+    }
     {   // overflowing queries (rare): exact scoring of every item
         unsigned long long hst[5];
         cudaMemcpyAsync(hst, gst.p, 40, cudaMemcpyDeviceToHost, s);
@@ -1238,7 +1287,7 @@ static nrlsh_status exact_impl(const float *items, int64_t n, int32_t d, const f
             cudaMemcpy(ql.data(), gov.p, (size_t)nov * 8, cudaMemcpyDeviceToHost);
             for (int64_t qi : ql)
                 launch_rerank(Xr, d, ldr, Q + qi * d, 1, nullptr, n, n, nullptr, 1, k,
-                              pt.get<unsigned long long>(), (int64_t *)oi.dev + qi * k,
+                              gsets[0].pt.get<unsigned long long>(), (int64_t *)oi.dev + qi * k,
                               (float *)os.dev + qi * k, s);
         }
     }
