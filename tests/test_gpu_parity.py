@@ -467,6 +467,49 @@ def test_rerank_path_selection(built, monkeypatch):
         assert P.last_rerank_path()["path"] == want, (nq, T)
 
 
+def test_sub_batch_streams_identical(built, monkeypatch):
+    """Sub-batches on one, two or three streams (api.cu: a workspace set per stream)
+    give bit-identical answers and candidates, on the tensor-core re-rank (T = 1%) and
+    the gather path (T = 0.1%); the ground truth likewise in sub-batches of 1,024 on
+    one or two streams and of 4,096."""
+    cfg, X, Q, Xd, idx, orc = built("c4", 300_000, 32, 64, 128)
+    P = _P()
+    n = X.shape[0]
+    nq = 2600   # three sub-batches of <= 1,024
+    Qd = torch.from_numpy(np.ascontiguousarray(np.concatenate([Q] * 82)[:nq])).cuda()
+    for T, path in ((n // 100, "tensor"), (n // 1000, "gather")):
+        res = []
+        for env in ({"NRLSH_QUERY_SERIAL": "1"}, {}, {"NRLSH_QUERY_STREAMS": "3"}):
+            for kk in ("NRLSH_QUERY_SERIAL", "NRLSH_QUERY_STREAMS"):
+                monkeypatch.delenv(kk, raising=False)
+            for kk, vv in env.items():
+                monkeypatch.setenv(kk, vv)
+            ids, sc = idx.query(Qd, cfg.k, T)
+            assert P.last_rerank_path()["path"] == path
+            cid, crk = idx.candidates(T, queries=Qd[:1100])
+            res.append((ids.cpu().numpy(), sc.cpu().numpy().view(np.int32),
+                        np.sort(cid.cpu().numpy(), axis=1)))
+        for r in res[1:]:
+            for a, b in zip(res[0], r):
+                assert np.array_equal(a, b), T
+    monkeypatch.delenv("NRLSH_QUERY_STREAMS", raising=False)
+    monkeypatch.delenv("NRLSH_QUERY_SERIAL", raising=False)
+    seeds, _ = idx.query(Qd, cfg.k, n // 100)
+    gts = []
+    for env in ({"NRLSH_GT_BATCH": "1024", "NRLSH_QUERY_SERIAL": "1"}, {"NRLSH_GT_BATCH": "1024"}, {}):
+        for kk in ("NRLSH_GT_BATCH", "NRLSH_QUERY_SERIAL"):
+            monkeypatch.delenv(kk, raising=False)
+        for kk, vv in env.items():
+            monkeypatch.setenv(kk, vv)
+        gi, gsc = idx.exact_topk(Qd, cfg.k, seed_ids=seeds)
+        gts.append((gi.cpu().numpy(), gsc.cpu().numpy().view(np.int32)))
+    for g in gts[1:]:
+        assert np.array_equal(gts[0][0], g[0]) and np.array_equal(gts[0][1], g[1])
+    for qi in (0, nq - 1):
+        a, sa = oracle.exact_topk(X, Q[qi % len(Q)], cfg.k)
+        assert_topk_match(gts[-1][0][qi], gts[-1][1][qi].view(np.float32), a, sa, X, Q[qi % len(Q)])
+
+
 @pytest.mark.parametrize("nq", [513, 700])
 def test_rerank_tensor_multi_pair_matches_gather(built, nq, monkeypatch):
     """Several 256-query pairs per sub-batch with a ragged last pair, under the
