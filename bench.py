@@ -583,6 +583,11 @@ def run_native(args):
                "ms_per_step": ri["ms_step"], "roofline": iroof, "scan_roofline": iscan,
                "other_rooflines": iothers,
                "stage_ms_per_step": {nm: v[0] / 2 for nm, v in ri["prof"].items() if v[1] > 0}}
+        if roof and iroof and roof.get("kernel") == iroof.get("kernel"):
+            roof["frac_serial_stream"] = iroof["frac"]
+            roof["note"] = ("timed region: two sub-batch streams share the GPU, so the kernel's "
+                            "CUDA-event span includes the other stream's work; frac_serial_stream: "
+                            "the same kernel with the sub-batches on one stream")
 
     # -------- scale (BASELINE configs[4]) in the same run: a sub-record, not the headline
     scale = None

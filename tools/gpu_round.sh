@@ -10,4 +10,4 @@ timeout 900 python bench.py > $O/bench.json 2> $O/bench.err; echo bench rc=$? >>
 timeout 300 python bench.py --impl reference --steps 1 --warmup 0 > $O/bench_ref.json 2> $O/bench_ref.err; echo ref rc=$? >> $O/rc.txt
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-scale --no-latency > $O/ncu_launch.log 2>&1; echo ncu1 rc=$? >> $O/rc.txt
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k8_rerank|k6_scan|k6_pilot|k7_select|gt_filter_tc|gt_tile_lists" -c 8 -o $O/prof_query python tools/run_stage.py query --reps 1 > $O/ncu_q.log 2>&1; echo ncu2 rc=$? >> $O/rc.txt
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k1_norms|k3_codes|sel_|scat_" -c 6 -o $O/prof_build python tools/run_stage.py build --reps 1 > $O/ncu_b.log 2>&1; echo ncu3 rc=$? >> $O/rc.txt
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k1_norms|k3_codes|win_|sel_resolve|scat_" -c 10 -o $O/prof_build python tools/run_stage.py build --reps 1 > $O/ncu_b.log 2>&1; echo ncu3 rc=$? >> $O/rc.txt
