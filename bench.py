@@ -191,8 +191,9 @@ def roofline_for(slot, ms_total, count, info, peaks, peaks_src):
         # one bf16 pass over every item per query; the re-rank's member-mode pass
         # multiplies only the tiles of sub-datasets holding candidates (its own count)
         # the pairs each filter actually multiplied (tile pruning skips the rest)
+        # (the counters are already summed over the timed steps)
         pairs = info["gt_filter_pairs"] if slot == "gt_filter" else info["rerank_filter_pairs"]
-        fl = 2.0 * pairs * d * steps / count
+        fl = 2.0 * pairs * d / count
         ach = fl / per_launch_s
         if slot == "rerank":
             pk = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")) * 1e12
