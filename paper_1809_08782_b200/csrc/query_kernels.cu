@@ -463,6 +463,32 @@ void launch_pilot(const nrlsh_index *ix, const uint32_t *qcodes, int Qb, int64_t
     note_launch();
 }
 
+// inclusive warp prefix sum: five shuffles whose in-range predicate guards the add
+__device__ __forceinline__ uint32_t warp_scan_incl(uint32_t v) {
+    asm volatile(
+        "{\n\t.reg .u32 r;\n\t.reg .pred p;\n\t"
+        "shfl.sync.up.b32 r|p, %0, 1, 0, 0xffffffff;\n\t@p add.u32 %0, %0, r;\n\t"
+        "shfl.sync.up.b32 r|p, %0, 2, 0, 0xffffffff;\n\t@p add.u32 %0, %0, r;\n\t"
+        "shfl.sync.up.b32 r|p, %0, 4, 0, 0xffffffff;\n\t@p add.u32 %0, %0, r;\n\t"
+        "shfl.sync.up.b32 r|p, %0, 8, 0, 0xffffffff;\n\t@p add.u32 %0, %0, r;\n\t"
+        "shfl.sync.up.b32 r|p, %0, 16, 0, 0xffffffff;\n\t@p add.u32 %0, %0, r;\n\t}"
+        : "+r"(v));
+    return v;
+}
+// atomics by inline PTX (ptxas still aggregates them per warp at SASS level: a
+// direct ATOMS unless all 32 lanes are active, a shuffle-scan + one atomic then)
+__device__ __forceinline__ uint32_t atom_add_shared(uint32_t *p, uint32_t v) {
+    uint32_t old;
+    asm volatile("atom.shared.add.u32 %0, [%1], %2;"
+                 : "=r"(old) : "r"((uint32_t)__cvta_generic_to_shared(p)), "r"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ uint32_t atom_add_global(uint32_t *p, uint32_t v) {
+    uint32_t old;
+    asm volatile("atom.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+
 // =========================================================================== K6 scan
 constexpr int kScanThreads = 256;
 // items per thread (a work unit = one CTA's chunk of 256 x IPT positions of one
@@ -475,20 +501,33 @@ constexpr int kChunk = kScanThreads * kScanIPT;   // items per work unit
 constexpr int kQG = kScanIPT >= 16 ? 32 : 64;     // queries per CTA
 constexpr int kSB = kScanIPT >= 16 ? 256 : 128;   // staged appends per (CTA, query)
 
-// Appends are staged per query in shared memory as (h << 16 | offset in chunk)
-// — one shared atomic per (warp, query) after a warp prefix sum of the lanes'
-// pass counts — and copied out, expanded to (flat (j, h) << 32 | position), with
-// one global reservation per (CTA, query); a query whose stage fills spills the
-// rest straight to global.  The CTA's active queries (delta_j(q) >= 0) are packed
-// as (code words, radius, index) records read with one 16-byte shared load per
-// word pair, and a thread's pass bits are the sign bits of delta - h (funnel shifts).
+// Appends, two regimes by the cell's radius delta_j(q) (warp-uniform):
+//  - sparse cells (delta < `dense`): each passing lane reserves its own run in the
+//    query's shared-memory stage of packed 4-byte entries (h << 16 | offset in chunk)
+//    with one shared atomic (no warp prefix sum: the order of a row's entries is
+//    free); the stage is copied out, expanded to (flat (j, h) << 32 | position), with
+//    one global reservation per (CTA, query); a lane whose run passes the end of the
+//    stage writes the rest straight to global;
+//  - dense cells: a warp prefix sum of the lanes' pass counts, one global
+//    reservation per warp, and lane-owned runs written straight to the query's row
+//    with predicated stores (no per-entry branches).
+// ncu (instructions executed per SASS line) showed the previous single path — a
+// prefix sum, an aggregated shared atomic and eight branchy per-item bodies for
+// every (warp, query) with a pass, 30% of the bodies spilling past the stage —
+// issuing half of the kernel's instructions at 75% issue-slot use.
+// The CTA's active queries (delta_j(q) >= 0) are packed as (code words, radius,
+// index) records read with one 16-byte shared load per word pair, and a thread's
+// pass bits are the sign bits of delta - h (funnel shifts).
+#ifndef NRLSH_SCAN_MINB
+#define NRLSH_SCAN_MINB 5
+#endif
 template <int W>
-__global__ void __launch_bounds__(kScanThreads, W == 4 ? 4 : 5) k6_scan(
+__global__ void __launch_bounds__(kScanThreads, W == 4 ? 4 : NRLSH_SCAN_MINB) k6_scan(
     const uint32_t *__restrict__ codes, const int4 *__restrict__ chunks,
     const uint32_t *__restrict__ qcodes, const int8_t *__restrict__ delta, int Qb, int m,
     const uint16_t *__restrict__ R, int L, unsigned long long *__restrict__ buf,
     uint32_t *__restrict__ cnt, int64_t C, unsigned long long *__restrict__ pairs, int QM,
-    int probe, int lbmax, unsigned long long *__restrict__ lbc) {
+    int probe, int lbmax, unsigned long long *__restrict__ lbc, int dense) {
     pdl_wait();
     constexpr int RW = W <= 2 ? 4 : 8;             // record words: codes, radius, query
     __shared__ unsigned long long s_lb[2];   // (pairs the lower bound ran on / decided alone)
@@ -503,35 +542,24 @@ __global__ void __launch_bounds__(kScanThreads, W == 4 ? 4 : 5) k6_scan(
     const int j = ch.x, p0 = ch.y, p1 = ch.z;
     const int q0 = (blockIdx.x % ngroups) * kQG;
     const int nqg = min(kQG, Qb - q0);
-    __shared__ int s_nact;
-    if (threadIdx.x < 32) {       // warp 0 packs the group's active queries
-        int base = 0;
-        for (int t0 = 0; t0 < kQG; t0 += 32) {
-            const int t = t0 + threadIdx.x;
-            int dl = -1;
-            if (t < nqg) dl = radius_of(delta[(int64_t)(q0 + t) * m + j]);
-            if (t < kQG) scnt[t] = 0;
-            const unsigned bal = __ballot_sync(NR_FULL, dl >= 0);
-            if (dl >= 0) {
-                uint32_t *r = srec[base + __popc(bal & lanemask_lt())];
-#pragma unroll
-                for (int w = 0; w < W; ++w)   // (per-sub-dataset A_j: the code under A_j)
-                    r[w] = qcodes[((int64_t)(q0 + t) * QM + (QM > 1 ? j : 0)) * W + w];
-                r[W] = (uint32_t)dl;
-                r[W + 1] = (uint32_t)t;
-            }
-            base += __popc(bal);
-        }
-        if (threadIdx.x == 0) s_nact = base;
-    }
-    __syncthreads();
-    const int nact = s_nact;
-    if (nact == 0) return;
-    if (threadIdx.x == 0 && pairs && !probe) atomicAdd(pairs, (unsigned long long)nact * (p1 - p0));
-    if (threadIdx.x == 0) { s_lb[0] = 0ull; s_lb[1] = 0ull; }
+    // every warp reads the group's radii itself (kQG bytes, L1-resident after the first
+    // warp), so it knows the active count without a barrier: an inactive (chunk, group)
+    // exits at once, and an active one issues its code loads while warps 0..kQG/32-1
+    // fetch and pack the active queries' records (one global latency instead of a
+    // serial delta -> ballot -> qcodes chain per 32 queries in warp 0)
     const int lane = threadIdx.x & 31;
-    uint32_t lbt = 0, lbs = 0;   // (this warp: pairs the lower bound ran on / skipped)
-    uint32_t nprobe = 0;   // (probe: the XOR/POPC/threshold work alone, no appends)
+    constexpr int NH = kQG / 32;
+    int dlv[NH];
+    unsigned bal[NH];
+    int nact = 0;
+#pragma unroll
+    for (int h = 0; h < NH; ++h) {
+        const int t = h * 32 + lane;
+        dlv[h] = t < nqg ? radius_of(delta[(int64_t)(q0 + t) * m + j]) : -1;
+        bal[h] = __ballot_sync(NR_FULL, dlv[h] >= 0);
+        nact += __popc(bal[h]);
+    }
+    if (nact == 0) return;
     uint32_t c[kScanIPT][W];
     uint32_t vmask = 0;   // bit u: item u of this thread exists
 #pragma unroll
@@ -545,6 +573,30 @@ __global__ void __launch_bounds__(kScanThreads, W == 4 ? 4 : 5) k6_scan(
             for (int w = 0; w < W; ++w) c[u][w] = 0u;
         }
     }
+    {
+        int base = 0;
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+            if ((int)(threadIdx.x >> 5) == h) {
+                const int t = h * 32 + lane;
+                scnt[t] = 0;
+                if (dlv[h] >= 0) {
+                    uint32_t *r = srec[base + __popc(bal[h] & lanemask_lt())];
+#pragma unroll
+                    for (int w = 0; w < W; ++w)   // (per-sub-dataset A_j: the code under A_j)
+                        r[w] = qcodes[((int64_t)(q0 + t) * QM + (QM > 1 ? j : 0)) * W + w];
+                    r[W] = (uint32_t)dlv[h];
+                    r[W + 1] = (uint32_t)t;
+                }
+            }
+            base += __popc(bal[h]);
+        }
+    }
+    if (threadIdx.x == 0 && pairs && !probe) atomicAdd(pairs, (unsigned long long)nact * (p1 - p0));
+    if (threadIdx.x == 0) { s_lb[0] = 0ull; s_lb[1] = 0ull; }
+    uint32_t lbt = 0, lbs = 0;   // (this warp: pairs the lower bound ran on / skipped)
+    uint32_t nprobe = 0;   // (probe: the XOR/POPC/threshold work alone, no appends)
+    __syncthreads();
     for (int ia = 0; ia < nact; ++ia) {
         uint32_t rec[RW];
         *reinterpret_cast<uint4 *>(rec) = *reinterpret_cast<const uint4 *>(srec[ia]);
@@ -565,54 +617,80 @@ __global__ void __launch_bounds__(kScanThreads, W == 4 ? 4 : 5) k6_scan(
                 int lb = 0;
 #pragma unroll
                 for (int w = 0; w + 1 < W; w += 2) lb += __popc((c[u][w] ^ qc[w]) | (c[u][w + 1] ^ qc[w + 1]));
-                lbmin = min(lbmin, (vmask >> u & 1u) ? lb : 255);
+                lbmin = min(lbmin, lb);   // (an absent item, code 0, can only keep the exact path on)
             }
             lbt += 1;
             if (!__any_sync(NR_FULL, lbmin <= dl)) { lbs += 1; continue; }
         }
-        int hh[kScanIPT];
-        uint32_t fail = 0;   // bit u: h_u > delta (the sign of delta - h_u)
+        // dd_u = delta - h_u in one three-input add per word pair (a pass is dd_u >= 0;
+        // h_u = delta - dd_u is only needed for the entries written)
+        int dd[kScanIPT];
+        uint32_t fail = 0;   // bit u: h_u > delta (the sign of dd_u)
 #pragma unroll
         for (int u = kScanIPT - 1; u >= 0; --u) {
-            hh[u] = hamming<W>(c[u], qc);
-            fail = __funnelshift_l((uint32_t)(dl - hh[u]), fail, 1);
+            int t = dl;
+#pragma unroll
+            for (int w = 0; w < W; ++w) t -= __popc(c[u][w] ^ qc[w]);
+            dd[u] = t;
+            fail = __funnelshift_l((uint32_t)t, fail, 1);
         }
         const uint32_t mask = ~fail & vmask;
         if (probe) { nprobe += __popc(mask); continue; }
         if (!__any_sync(NR_FULL, mask != 0u)) continue;
-        // warp prefix sum of the pass counts -> one shared reservation per warp
-        const int np = __popc(mask);
-        int inc = np;
+        const uint32_t np = (uint32_t)__popc(mask);
+        unsigned long long *row = buf + (int64_t)(q0 + qq) * C;
+        const uint32_t jhd = (uint32_t)(j * (L + 1) + dl);            // + h_u = - dd_u
+        const uint32_t hd16 = ((uint32_t)dl << 16) + threadIdx.x;     // stage entry: h << 16 | offset
+        const uint32_t pt = (uint32_t)p0 + threadIdx.x;
+        if (dl >= dense) {
+            // dense cell (many of a warp's 256 items pass): lane-owned runs straight in
+            // the query's candidate row, one global reservation per warp
+            const uint32_t inc = warp_scan_incl(np);
+            const uint32_t tot = __shfl_sync(NR_FULL, inc, 31);
+            uint32_t gb = 0;
+            if (lane == 31) gb = atom_add_global(&cnt[q0 + qq], tot);
+            gb = __shfl_sync(NR_FULL, gb, 31);
+            unsigned long long *ptr = row + (gb + inc - np);
+            if ((int64_t)gb + tot <= C) {
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(NR_FULL, inc, o);
-            if (lane >= o) inc += y;
-        }
-        const int tot = __shfl_sync(NR_FULL, inc, 31);
-        uint32_t base = 0, gbase = 0;
-        if (lane == 31) {
-            base = atomicAdd(&scnt[qq], (uint32_t)tot);
-            // the part past the stage goes straight to global: one reservation per warp
-            const uint32_t lo = max(base, (uint32_t)kSB), hi = base + (uint32_t)tot;
-            if (hi > lo) gbase = atomicAdd(&cnt[q0 + qq], hi - lo);
-        }
-        base = __shfl_sync(NR_FULL, base, 31);
-        gbase = __shfl_sync(NR_FULL, gbase, 31);
-        const uint32_t glo = max(base, (uint32_t)kSB);
-        uint32_t slot = base + inc - np;
+                for (int u = 0; u < kScanIPT; ++u)
+                    if (mask >> u & 1u)
+                        *ptr++ = ((unsigned long long)(jhd - (uint32_t)dd[u]) << 32) | (pt + kScanThreads * u);
+            } else {   // the row is full (the query is redone with a larger buffer)
+                const unsigned long long *end = row + C;
 #pragma unroll
-        for (int u = 0; u < kScanIPT; ++u) {
-            if (!(mask >> u & 1u)) continue;
-            const uint32_t off = threadIdx.x + kScanThreads * u;
-            if (slot < kSB) {
-                sbuf[qq][slot] = ((uint32_t)hh[u] << 16) | off;
-            } else {   // stage full: direct global append
-                const uint32_t g = gbase + (slot - glo);
-                if (g < C)
-                    buf[(int64_t)(q0 + qq) * C + g] =
-                        ((unsigned long long)(j * (L + 1) + hh[u]) << 32) | (p0 + off);
+                for (int u = 0; u < kScanIPT; ++u)
+                    if (mask >> u & 1u) {
+                        if (ptr < end)
+                            *ptr = ((unsigned long long)(jhd - (uint32_t)dd[u]) << 32) | (pt + kScanThreads * u);
+                        ++ptr;
+                    }
             }
-            ++slot;
+        } else if (mask) {
+            // sparse cell: each passing lane reserves its own run in the query's stage
+            // (no warp prefix sum: the order of a row's entries is free)
+            uint32_t slot = atom_add_shared(&scnt[qq], np);
+            if (slot + np <= (uint32_t)kSB) {
+                uint32_t *sp = &sbuf[qq][slot];
+#pragma unroll
+                for (int u = 0; u < kScanIPT; ++u)
+                    if (mask >> u & 1u) *sp++ = hd16 - ((uint32_t)dd[u] << 16) + kScanThreads * u;
+            } else {   // stage full: the part of this lane's run past it goes straight to global
+                const uint32_t lo = max(slot, (uint32_t)kSB);
+                uint32_t g = atom_add_global(&cnt[q0 + qq], slot + np - lo);
+#pragma unroll
+                for (int u = 0; u < kScanIPT; ++u)
+                    if (mask >> u & 1u) {
+                        if (slot < (uint32_t)kSB) {
+                            sbuf[qq][slot] = hd16 - ((uint32_t)dd[u] << 16) + kScanThreads * u;
+                        } else {
+                            if (g < C)
+                                row[g] = ((unsigned long long)(jhd - (uint32_t)dd[u]) << 32) | (pt + kScanThreads * u);
+                            ++g;
+                        }
+                        ++slot;
+                    }
+            }
         }
     }
     if (probe) {
@@ -664,12 +742,17 @@ void launch_scan(const nrlsh_index *ix, const uint32_t *qcodes, const int8_t *de
     // delta <= 16, 128 bits: delta <= 37); NRLSH_SCAN_LBMAX overrides (-1: off)
     int lbmax = ix->W == 2 ? 16 : (ix->W == 4 ? 37 : -1);
     if (getenv("NRLSH_SCAN_LBMAX")) lbmax = atoi(getenv("NRLSH_SCAN_LBMAX"));
+    // radius from which a cell counts as dense (L/2 - 0.75 sqrt(L): ~8% of random codes
+    // within it; measured optimum 26 at 64 bits, 56 at 128); its appends go straight to
+    // global, the others through the stage
+    int dense = (int)lround(ix->L / 2.0 - 0.75 * sqrt((double)ix->L));
+    if (getenv("NRLSH_SCAN_DENSE")) dense = atoi(getenv("NRLSH_SCAN_DENSE"));
     const int64_t ngroups = (Qb + kQG - 1) / kQG;
     const unsigned grid = (unsigned)(ix->nchunks * ngroups);
     switch (ix->W) {
-        case 1: launch_pdl(k6_scan<1>, dim3(grid), dim3(kScanThreads), 0, s, ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs, ix->QM, 0, lbmax, lbc); break;
-        case 2: launch_pdl(k6_scan<2>, dim3(grid), dim3(kScanThreads), 0, s, ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs, ix->QM, 0, lbmax, lbc); break;
-        default: launch_pdl(k6_scan<4>, dim3(grid), dim3(kScanThreads), 0, s, ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs, ix->QM, 0, lbmax, lbc); break;
+        case 1: launch_pdl(k6_scan<1>, dim3(grid), dim3(kScanThreads), 0, s, ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs, ix->QM, 0, lbmax, lbc, dense); break;
+        case 2: launch_pdl(k6_scan<2>, dim3(grid), dim3(kScanThreads), 0, s, ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs, ix->QM, 0, lbmax, lbc, dense); break;
+        default: launch_pdl(k6_scan<4>, dim3(grid), dim3(kScanThreads), 0, s, ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs, ix->QM, 0, lbmax, lbc, dense); break;
     }
     note_launch();
     if (getenv("NRLSH_SCAN_PROBE")) {   // experiment: time the scan without its appends
@@ -677,9 +760,9 @@ void launch_scan(const nrlsh_index *ix, const uint32_t *qcodes, const int8_t *de
         if (!dummy) cudaMalloc(&dummy, 8);
         ProfScope p(SLOT_OTHER, s);
         switch (ix->W) {
-            case 1: k6_scan<1><<<grid, kScanThreads, 0, s>>>(ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, dummy, ix->QM, 1, lbmax, nullptr); break;
-            case 2: k6_scan<2><<<grid, kScanThreads, 0, s>>>(ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, dummy, ix->QM, 1, lbmax, nullptr); break;
-            default: k6_scan<4><<<grid, kScanThreads, 0, s>>>(ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, dummy, ix->QM, 1, lbmax, nullptr); break;
+            case 1: k6_scan<1><<<grid, kScanThreads, 0, s>>>(ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, dummy, ix->QM, 1, lbmax, nullptr, dense); break;
+            case 2: k6_scan<2><<<grid, kScanThreads, 0, s>>>(ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, dummy, ix->QM, 1, lbmax, nullptr, dense); break;
+            default: k6_scan<4><<<grid, kScanThreads, 0, s>>>(ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, dummy, ix->QM, 1, lbmax, nullptr, dense); break;
         }
     }
 }
