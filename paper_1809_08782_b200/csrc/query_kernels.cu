@@ -498,8 +498,14 @@ constexpr int kScanThreads = 256;
 #endif
 constexpr int kScanIPT = NRLSH_SCAN_IPT;
 constexpr int kChunk = kScanThreads * kScanIPT;   // items per work unit
-constexpr int kQG = kScanIPT >= 16 ? 32 : 64;     // queries per CTA
-constexpr int kSB = kScanIPT >= 16 ? 256 : 128;   // staged appends per (CTA, query)
+#ifndef NRLSH_SCAN_QG
+#define NRLSH_SCAN_QG (NRLSH_SCAN_IPT >= 16 ? 32 : 64)
+#endif
+#ifndef NRLSH_SCAN_SB
+#define NRLSH_SCAN_SB (NRLSH_SCAN_IPT >= 16 ? 256 : 128)
+#endif
+constexpr int kQG = NRLSH_SCAN_QG;     // queries per CTA
+constexpr int kSB = NRLSH_SCAN_SB;     // staged appends per (CTA, query)
 
 // Appends, two regimes by the cell's radius delta_j(q) (warp-uniform):
 //  - sparse cells (delta < `dense`): each passing lane reserves its own run in the
@@ -597,10 +603,16 @@ __global__ void __launch_bounds__(kScanThreads, W == 4 ? 4 : NRLSH_SCAN_MINB) k6
     uint32_t lbt = 0, lbs = 0;   // (this warp: pairs the lower bound ran on / skipped)
     uint32_t nprobe = 0;   // (probe: the XOR/POPC/threshold work alone, no appends)
     __syncthreads();
-    for (int ia = 0; ia < nact; ++ia) {
+    // (the record's shared address is carried in a register: the compiler otherwise
+    // rebuilds it from the CTA's window base with five uniform instructions per query)
+    uint32_t rec_a = (uint32_t)__cvta_generic_to_shared(&srec[0][0]);
+    for (int ia = 0; ia < nact; ++ia, rec_a += RW * 4) {
         uint32_t rec[RW];
-        *reinterpret_cast<uint4 *>(rec) = *reinterpret_cast<const uint4 *>(srec[ia]);
-        if (RW == 8) *reinterpret_cast<uint4 *>(rec + 4) = *reinterpret_cast<const uint4 *>(srec[ia] + 4);
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(rec[0]), "=r"(rec[1]), "=r"(rec[2]), "=r"(rec[3]) : "r"(rec_a));
+        if (RW == 8)
+            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4+16];"
+                         : "=r"(rec[4]), "=r"(rec[5]), "=r"(rec[6]), "=r"(rec[7]) : "r"(rec_a));
         const int dl = (int)rec[W];
         const int qq = (int)rec[W + 1];
         uint32_t qc[W];
