@@ -628,7 +628,7 @@ void run_candidates(const nrlsh_index *ix, const float *Qd, const uint32_t *qcod
                     unsigned long long *pairs, cudaStream_t s, uint32_t *sel_B = nullptr,
                     uint32_t *sel_pk = nullptr,
                     int32_t *seeds = nullptr, int ks = 0, void *fb_ws = nullptr,
-                    unsigned long long *entries = nullptr) {
+                    unsigned long long *entries = nullptr, void *units_ws = nullptr) {
     if (qcodes_in) {
         cudaMemcpyAsync(qcodes, qcodes_in + qbase * ix->QM * ix->W, (size_t)Qb * ix->QM * ix->W * 4,
                         cudaMemcpyDeviceToDevice, s);
@@ -651,7 +651,7 @@ void run_candidates(const nrlsh_index *ix, const float *Qd, const uint32_t *qcod
             cudaMemsetAsync(cntv, 0, (size_t)Qb * 4, s);
             if (launch_scan_tc(ix, qcodes, delta, Qb, scan_ws, buf, cnt, cntv, C, pairs, s)) tc = false;
         }
-        if (!tc) launch_scan(ix, qcodes, delta, Qb, buf, cnt, C, pairs, s, pairs + 4);
+        if (!tc) launch_scan(ix, qcodes, delta, Qb, buf, cnt, C, pairs, s, pairs + 4, units_ws);
     }
     {
         ProfScope p(SLOT_FALLBACK, s);
@@ -742,7 +742,7 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
     if (nq <= Qmax || getenv("NRLSH_QUERY_SERIAL")) NSET = 1;
     NSET = (int)std::min<int64_t>(NSET, (nq + Qmax - 1) / Qmax);
     struct WSet {
-        DBuf qc, dl, cn, cv, ba, bf, cd, pt, fbw;
+        DBuf qc, dl, cn, cv, ba, us, bf, cd, pt, fbw;
         DBuf rsb, rspk, rseed, rtid, rtsc, rth, rqb, rqn, rhp, rcd, rcc, rpt, rtl, rqp;
     } wsets[3];
     DBuf fl;
@@ -752,12 +752,15 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
         if (W_.qc.alloc((size_t)Qmax * ix->QM * ix->W * 4, s) || W_.dl.alloc((size_t)Qmax * ix->m, s) ||
             W_.cn.alloc((size_t)Qmax * 4, s) || W_.cv.alloc((size_t)Qmax * 4, s) ||
             W_.ba.alloc(scan_tc_supported(ix) ? scan_tc_ws_bytes(ix, Qmax) : 16, s) ||
+            W_.us.alloc(scan_units_ws_bytes(ix, Qmax), s) ||
             W_.bf.alloc((size_t)Qmax * C * 8, s) || W_.cd.alloc((size_t)Qmax * Tq * 4, s) ||
             W_.pt.alloc(want_topk ? rerank_partial_bytes(Qmax, Tq, k) : 0, s) ||
             W_.fbw.alloc(fallback_ws_bytes(ix), s))
             return fail(NRLSH_ENOMEM, "query workspace");
         // (histogram rows stay zero between uses)
         cudaMemsetAsync(W_.fbw.p, 0, fallback_ws_bytes(ix), s);
+        // (the scan's unit counters: zero on entry, left zero by every scan)
+        cudaMemsetAsync(W_.us.p, 0, 16, s);
     }
     const float *Xr = ix->Xpad ? ix->Xpad : ix->X;
     const int ldr = ix->Xpad ? ix->dpad : ix->d;
@@ -866,7 +869,7 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
                        use_rtc ? rsb.get<uint32_t>() : nullptr,
                        use_rtc ? rspk.get<uint32_t>() : nullptr,
                        use_rtc ? rseed.get<int32_t>() : nullptr, KS, fbw.p,
-                       (unsigned long long *)(fl.get<int>() + 10));
+                       (unsigned long long *)(fl.get<int>() + 10), W_.us.p);
         if (use_rtc) {
             {
                 ProfScope p(SLOT_SCORE, s);

@@ -141,9 +141,13 @@ void launch_gather_sample(const nrlsh_index *ix, int stride, uint32_t *sc, uint8
 void launch_pilot(const nrlsh_index *ix, const uint32_t *qcodes, int Qb, int64_t Tq,
                   int stride, int8_t *delta, uint32_t *cnt, cudaStream_t s, uint32_t *zero_word = nullptr);
 // lbc (nullable): [0] pairs the one-POPC lower bound ran on, [1] pairs it decided alone
+// units_ws: scan_units_ws_bytes() of scratch whose first 16 bytes are zero (the unit
+// list of the sub-batch and its counters; the scan leaves them zero again)
+size_t scan_units_ws_bytes(const nrlsh_index *ix, int Qmax);
 void launch_scan(const nrlsh_index *ix, const uint32_t *qcodes, const int8_t *delta, int Qb,
                  unsigned long long *buf, uint32_t *cnt, int64_t C,
-                 unsigned long long *pairs, cudaStream_t s, unsigned long long *lbc = nullptr);
+                 unsigned long long *pairs, cudaStream_t s, unsigned long long *lbc,
+                 void *units_ws);
 // cntv: the real entries of each query's buffer (the tensor-core scan pads its append
 // runs with ~0 sentinels, counted in cnt); == cnt for the popcount scan
 // ws: fallback_ws_bytes() of zeroed scratch for the all-SM re-do of failed queries

@@ -533,26 +533,36 @@ __global__ void __launch_bounds__(kScanThreads, W == 4 ? 4 : NRLSH_SCAN_MINB) k6
     const uint32_t *__restrict__ qcodes, const int8_t *__restrict__ delta, int Qb, int m,
     const uint16_t *__restrict__ R, int L, unsigned long long *__restrict__ buf,
     uint32_t *__restrict__ cnt, int64_t C, unsigned long long *__restrict__ pairs, int QM,
-    int probe, int lbmax, unsigned long long *__restrict__ lbc, int dense) {
+    int lbmax, unsigned long long *__restrict__ lbc, int dense, uint32_t *__restrict__ uws) {
     pdl_wait();
     constexpr int RW = W <= 2 ? 4 : 8;             // record words: codes, radius, query
+    __shared__ uint32_t s_unit[2];
     __shared__ unsigned long long s_lb[2];   // (pairs the lower bound ran on / decided alone)
     __shared__ __align__(16) uint32_t srec[kQG][RW];
     __shared__ uint32_t sbuf[kQG][kSB];
     __shared__ uint32_t scnt[kQG];
     __shared__ uint32_t sbase[kQG];
-    // consecutive CTAs share a chunk (different query groups): the chunk's codes
-    // are read from HBM once and re-served from L2
+    // Persistent CTAs take the active (chunk, query group) units that scan_units listed
+    // from a work counter (the next unit's index is fetched while this one runs); the
+    // last CTA to finish resets the counters for the next launch on this workspace.
     const int ngroups = (Qb + kQG - 1) / kQG;
-    const int4 ch = chunks[blockIdx.x / ngroups];
+    const uint32_t nunits = uws[0];
+    const uint32_t *units = uws + 4;
+    if (threadIdx.x == 0) s_unit[0] = atomicAdd(&uws[1], 1u);
+    __syncthreads();
+    uint32_t ui = s_unit[0];
+    for (int upar = 0; ui < nunits; upar ^= 1, ui = s_unit[upar]) {
+    uint32_t nxt = 0;   // (stored after the main loop: the atomic's round trip stays off the path)
+    if (threadIdx.x == 0) nxt = atomicAdd(&uws[1], 1u);
+    const uint32_t unit = units[ui];
+    const int4 ch = chunks[unit / (uint32_t)ngroups];
     const int j = ch.x, p0 = ch.y, p1 = ch.z;
-    const int q0 = (blockIdx.x % ngroups) * kQG;
+    const int q0 = (int)(unit % (uint32_t)ngroups) * kQG;
     const int nqg = min(kQG, Qb - q0);
     // every warp reads the group's radii itself (kQG bytes, L1-resident after the first
-    // warp), so it knows the active count without a barrier: an inactive (chunk, group)
-    // exits at once, and an active one issues its code loads while warps 0..kQG/32-1
-    // fetch and pack the active queries' records (one global latency instead of a
-    // serial delta -> ballot -> qcodes chain per 32 queries in warp 0)
+    // warp), so it knows the active set without a barrier and issues its code loads
+    // while warps 0..kQG/32-1 fetch and pack the active queries' records (one global
+    // latency instead of a serial delta -> ballot -> qcodes chain per 32 queries)
     const int lane = threadIdx.x & 31;
     constexpr int NH = kQG / 32;
     int dlv[NH];
@@ -565,8 +575,7 @@ __global__ void __launch_bounds__(kScanThreads, W == 4 ? 4 : NRLSH_SCAN_MINB) k6
         bal[h] = __ballot_sync(NR_FULL, dlv[h] >= 0);
         nact += __popc(bal[h]);
     }
-    if (nact == 0) return;
-    uint32_t c[kScanIPT][W];
+    uint32_t c[kScanIPT][W];   // (a listed unit has nact >= 1)
     uint32_t vmask = 0;   // bit u: item u of this thread exists
 #pragma unroll
     for (int u = 0; u < kScanIPT; ++u) {
@@ -598,10 +607,9 @@ __global__ void __launch_bounds__(kScanThreads, W == 4 ? 4 : NRLSH_SCAN_MINB) k6
             base += __popc(bal[h]);
         }
     }
-    if (threadIdx.x == 0 && pairs && !probe) atomicAdd(pairs, (unsigned long long)nact * (p1 - p0));
+    if (threadIdx.x == 0 && pairs) atomicAdd(pairs, (unsigned long long)nact * (p1 - p0));
     if (threadIdx.x == 0) { s_lb[0] = 0ull; s_lb[1] = 0ull; }
     uint32_t lbt = 0, lbs = 0;   // (this warp: pairs the lower bound ran on / skipped)
-    uint32_t nprobe = 0;   // (probe: the XOR/POPC/threshold work alone, no appends)
     __syncthreads();
     // (the record's shared address is carried in a register: the compiler otherwise
     // rebuilds it from the CTA's window base with five uniform instructions per query)
@@ -647,7 +655,6 @@ __global__ void __launch_bounds__(kScanThreads, W == 4 ? 4 : NRLSH_SCAN_MINB) k6
             fail = __funnelshift_l((uint32_t)t, fail, 1);
         }
         const uint32_t mask = ~fail & vmask;
-        if (probe) { nprobe += __popc(mask); continue; }
         if (!__any_sync(NR_FULL, mask != 0u)) continue;
         const uint32_t np = (uint32_t)__popc(mask);
         unsigned long long *row = buf + (int64_t)(q0 + qq) * C;
@@ -705,10 +712,6 @@ __global__ void __launch_bounds__(kScanThreads, W == 4 ? 4 : NRLSH_SCAN_MINB) k6
             }
         }
     }
-    if (probe) {
-        if (nprobe) atomicAdd((unsigned int *)pairs, nprobe);
-        return;
-    }
     if (lbc && lbt) {   // (per warp: iterations x its items)
         const uint32_t wv = __reduce_add_sync(NR_FULL, (uint32_t)__popc(vmask));
         if (lane == 0) {
@@ -716,6 +719,7 @@ __global__ void __launch_bounds__(kScanThreads, W == 4 ? 4 : NRLSH_SCAN_MINB) k6
             atomicAdd(&s_lb[1], (unsigned long long)lbs * wv);
         }
     }
+    if (threadIdx.x == 0) s_unit[upar ^ 1] = nxt;
     __syncthreads();
     if (lbc && threadIdx.x == 0 && s_lb[0]) {
         atomicAdd(&lbc[0], s_lb[0]);
@@ -740,15 +744,58 @@ __global__ void __launch_bounds__(kScanThreads, W == 4 ? 4 : NRLSH_SCAN_MINB) k6
             if (g < C) buf[q * C + g] = ((jb + (v >> 16)) << 32) | (uint32_t)(p0 + (v & 0xffffu));
         }
     }
+    __syncthreads();   // (the stage, the records and s_unit are reused by the next unit)
+    }
+    if (threadIdx.x == 0 && atomicAdd(&uws[2], 1u) == gridDim.x - 1) {
+        uws[0] = 0u;
+        uws[1] = 0u;
+        uws[2] = 0u;
+    }
+}
+
+// The active (chunk, query group) units of a sub-batch: a group is active on a
+// sub-dataset iff one of its queries has a radius there (delta != -1).  One CTA per
+// group; ws: [0] unit count, [1] work counter, [2] finished CTAs (all zero on entry,
+// reset by the scan), [4...] units as chunk * ngroups + group.
+__global__ void __launch_bounds__(1024) scan_units(const int8_t *__restrict__ delta, int Qb, int m,
+                                                   const int4 *__restrict__ chunks, int nchunks,
+                                                   uint32_t *__restrict__ ws) {
+    pdl_wait();
+    __shared__ uint8_t act[kMaxParts];
+    const int g = blockIdx.x, ngroups = gridDim.x, q0 = g * kQG;
+    const int nqg = min(kQG, Qb - q0);
+    for (int j = threadIdx.x; j < m; j += blockDim.x) act[j] = 0;
+    __syncthreads();
+    for (int e = threadIdx.x; e < nqg * m; e += blockDim.x)
+        if (delta[(int64_t)q0 * m + e] != (int8_t)-1) act[e % m] = 1;   // (benign race: all write 1)
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    // (listed from the last chunk down: the sub-datasets of largest norm, which are active
+    // for the most queries and hold the dense cells, start first and the cheap units
+    // fill the tail of the persistent CTAs' schedule)
+    for (int c0 = 0; c0 < nchunks; c0 += blockDim.x) {
+        const int c = nchunks - 1 - (c0 + (int)threadIdx.x);
+        const bool f = c >= 0 && act[chunks[c].x];
+        const unsigned bal = __ballot_sync(NR_FULL, f);
+        if (bal) {
+            uint32_t base = 0;
+            if (lane == 0) base = atomicAdd(&ws[0], (uint32_t)__popc(bal));
+            base = __shfl_sync(NR_FULL, base, 0);
+            if (f) ws[4 + base + __popc(bal & lanemask_lt())] = (uint32_t)c * (uint32_t)ngroups + (uint32_t)g;
+        }
+    }
 }
 
 int scan_chunk_items() { return kChunk; }
+size_t scan_units_ws_bytes(const nrlsh_index *ix, int Qmax) {
+    return 16 + (size_t)ix->nchunks * (size_t)((Qmax + kQG - 1) / kQG) * 4;
+}
 
 // ---------------------------------------------------------------- K6 scan, queries in lanes
 
 void launch_scan(const nrlsh_index *ix, const uint32_t *qcodes, const int8_t *delta, int Qb,
                  unsigned long long *buf, uint32_t *cnt, int64_t C, unsigned long long *pairs,
-                 cudaStream_t s, unsigned long long *lbc) {
+                 cudaStream_t s, unsigned long long *lbc, void *units_ws) {
     // radii up to which the pair lower bound runs first: where a warp's 256 near-random
     // codes all miss it with probability > 1/2 (Bin(32, 3/4) per word pair; 64 bits:
     // delta <= 16, 128 bits: delta <= 37); NRLSH_SCAN_LBMAX overrides (-1: off)
@@ -759,24 +806,34 @@ void launch_scan(const nrlsh_index *ix, const uint32_t *qcodes, const int8_t *de
     // global, the others through the stage
     int dense = (int)lround(ix->L / 2.0 - 0.75 * sqrt((double)ix->L));
     if (getenv("NRLSH_SCAN_DENSE")) dense = atoi(getenv("NRLSH_SCAN_DENSE"));
-    const int64_t ngroups = (Qb + kQG - 1) / kQG;
-    const unsigned grid = (unsigned)(ix->nchunks * ngroups);
+    const int ngroups = (Qb + kQG - 1) / kQG;
+    uint32_t *uws = static_cast<uint32_t *>(units_ws);
+    launch_pdl(scan_units, dim3(ngroups), dim3(1024), 0, s, delta, Qb, ix->m, ix->chunks_d,
+               (int)ix->nchunks, uws);
+    // one wave of resident CTAs (NRLSH_SCAN_WAVES: CTAs per resident slot, default 1)
+    static int res[5] = {0, 0, 0, 0, 0};
+    if (!res[ix->W]) {
+        int r = 0;
+        if (ix->W == 1) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, k6_scan<1>, kScanThreads, 0);
+        else if (ix->W == 2) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, k6_scan<2>, kScanThreads, 0);
+        else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, k6_scan<4>, kScanThreads, 0);
+        res[ix->W] = std::max(1, r);
+    }
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    static const int waves = getenv("NRLSH_SCAN_WAVES") ? std::max(1, atoi(getenv("NRLSH_SCAN_WAVES"))) : 1;
+    const unsigned grid = (unsigned)std::min<int64_t>((int64_t)sms * res[ix->W] * waves,
+                                                      (int64_t)ix->nchunks * ngroups);
     switch (ix->W) {
-        case 1: launch_pdl(k6_scan<1>, dim3(grid), dim3(kScanThreads), 0, s, ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs, ix->QM, 0, lbmax, lbc, dense); break;
-        case 2: launch_pdl(k6_scan<2>, dim3(grid), dim3(kScanThreads), 0, s, ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs, ix->QM, 0, lbmax, lbc, dense); break;
-        default: launch_pdl(k6_scan<4>, dim3(grid), dim3(kScanThreads), 0, s, ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs, ix->QM, 0, lbmax, lbc, dense); break;
+        case 1: launch_pdl(k6_scan<1>, dim3(grid), dim3(kScanThreads), 0, s, ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs, ix->QM, lbmax, lbc, dense, uws); break;
+        case 2: launch_pdl(k6_scan<2>, dim3(grid), dim3(kScanThreads), 0, s, ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs, ix->QM, lbmax, lbc, dense, uws); break;
+        default: launch_pdl(k6_scan<4>, dim3(grid), dim3(kScanThreads), 0, s, ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs, ix->QM, lbmax, lbc, dense, uws); break;
     }
-    note_launch();
-    if (getenv("NRLSH_SCAN_PROBE")) {   // experiment: time the scan without its appends
-        static unsigned long long *dummy = nullptr;
-        if (!dummy) cudaMalloc(&dummy, 8);
-        ProfScope p(SLOT_OTHER, s);
-        switch (ix->W) {
-            case 1: k6_scan<1><<<grid, kScanThreads, 0, s>>>(ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, dummy, ix->QM, 1, lbmax, nullptr, dense); break;
-            case 2: k6_scan<2><<<grid, kScanThreads, 0, s>>>(ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, dummy, ix->QM, 1, lbmax, nullptr, dense); break;
-            default: k6_scan<4><<<grid, kScanThreads, 0, s>>>(ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, dummy, ix->QM, 1, lbmax, nullptr, dense); break;
-        }
-    }
+    note_launch(2);
 }
 
 
