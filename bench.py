@@ -173,6 +173,10 @@ def roofline_for(slot, ms_total, count, info, peaks, peaks_src):
         # pairs it decides alone, plus W/2 on the pairs where it ran and did not
         ops = (info["scanned_pairs"] * W - info["lb_decided_pairs"] * W
                + info["lb_pairs"] * (W // 2)) / count
+        # (the library's own count of the POPCs issued, nrlsh_last_scan_popc: it knows
+        # which bound ran where — the coarse first bound costs half of the pair bound)
+        if info.get("scan_popc"):
+            ops = info["scan_popc"] / count
         ach = ops / per_launch_s
         return {"bound": "alu", "kernel": "k6_scan (XOR+POPC Hamming scan + metric filter)",
                 "achieved": ach / 1e12, "peak": POPC_PEAK_PER_S / 1e12, "unit": "TPOPC/s",
@@ -374,7 +378,7 @@ def measure_path(P, torch, cfg, L, m, T, Xd, Qd, steps, warmup, stream, flush, d
     P.profile_read(reset=True)
     P.profile_enable(True)
     launches0 = P.launch_count()
-    acc = {"scanned_pairs": 0, "lb_pairs": 0, "lb_decided_pairs": 0, "buffer_entries": 0,
+    acc = {"scanned_pairs": 0, "lb_pairs": 0, "lb_decided_pairs": 0, "scan_popc": 0, "buffer_entries": 0,
            "fallback_queries": 0, "rerank_filter_pairs": 0,
            "rerank_overflow": 0, "gt_filter_pairs": 0, "gt_survivors": 0}
     evs = []
@@ -389,6 +393,7 @@ def measure_path(P, torch, cfg, L, m, T, Xd, Qd, steps, warmup, stream, flush, d
         acc["scanned_pairs"] += qstats["scanned_pairs"]
         acc["lb_pairs"] += qstats["bound_pairs"]
         acc["lb_decided_pairs"] += qstats["bound_decided_pairs"]
+        acc["scan_popc"] += qstats.get("popc_ops", 0)
         acc["buffer_entries"] += qstats["buffer_entries"]
         acc["fallback_queries"] += qstats["fallback_queries"]
         acc["rerank_filter_pairs"] += rinfo["filter_pairs"]
@@ -422,7 +427,8 @@ def rooflines(r, cfg, L, m, nq, T, steps, peaks, peaks_src):
     W = 1 if L <= 32 else (2 if L <= 64 else 4)
     info = {"n": cfg.n, "d": cfg.d, "L": L, "W": W, "nq": nq, "T": T, "k": cfg.k, "m": m,
             "scanned_pairs": acc["scanned_pairs"], "lb_pairs": acc["lb_pairs"],
-            "lb_decided_pairs": acc["lb_decided_pairs"], "traffic": load_traffic(), "steps": steps,
+            "lb_decided_pairs": acc["lb_decided_pairs"], "scan_popc": acc["scan_popc"],
+            "traffic": load_traffic(), "steps": steps,
             "rerank_path": r["rerank_path"], "rerank_filter_pairs": acc["rerank_filter_pairs"],
             "gt_filter_pairs": acc["gt_filter_pairs"],
             "score_bytes": float(nq) * T * cfg.d * 4.0 * steps, "gt_tensor": True}
@@ -460,8 +466,8 @@ def rooflines(r, cfg, L, m, nq, T, steps, peaks, peaks_src):
              "logical": q_roof(float(nq) * n * W, float(nq) * T),
              # the POPCs the scan issued after exact sub-dataset skipping and the lower
              # bound, the pairs the re-rank's filter multiplied
-             "actual": q_roof((acc["scanned_pairs"] * W - acc["lb_decided_pairs"] * W
-                               + acc["lb_pairs"] * (W // 2)) / steps,
+             "actual": q_roof((acc["scan_popc"] or (acc["scanned_pairs"] * W - acc["lb_decided_pairs"] * W
+                                                    + acc["lb_pairs"] * (W // 2))) / steps,
                               acc["rerank_filter_pairs"] / steps),
              "peaks": {"popc_per_s": POPC_PEAK_PER_S, "hbm_gbs": peaks["hbm_gbs"],
                        "bf16_tflops": bf16 / 1e12, "ffma_tflops": FFMA_PEAK_FLOPS / 1e12}}

@@ -179,6 +179,16 @@ nrlsh_status nrlsh_last_query_stats(int64_t *fallback_queries, int64_t *kernel_l
    without it).  Either may be NULL. */
 nrlsh_status nrlsh_last_scan_stats(int64_t *bound_pairs, int64_t *bound_decided_pairs);
 
+/* POPC instructions (per thread, on existing items) the popcount scan of the last
+   nrlsh_query on this thread issued for distances and lower bounds: W per exact
+   distance, W/2 per pair bound, and for the coarser first bound at very small radii
+   one per item (128-bit codes: popcount of the OR of the four XOR words) or one per
+   two items (64-bit codes: popcount((a_u | b_u) & (a_v | b_v)) <= min(h_u, h_v)).
+   This is the scan's algorithmic work on the POPC roofline (PAPER:209, PAPER:217:
+   the Hamming ranking of every item of every probed sub-dataset).  0 if the
+   tensor-core scan ran.  May be NULL. */
+nrlsh_status nrlsh_last_scan_popc(int64_t *popc_ops);
+
 /* Candidates of the last nrlsh_query on this thread that the re-rank rescored in
    fp32 after a certified bf16 pass (the others provably could not enter the
    top-k; the answer is the same as rescoring all of them): the tensor-core

@@ -22,7 +22,7 @@ EXPORTS = [
     "nrlsh_default_options", "nrlsh_build", "nrlsh_build_ex", "nrlsh_query", "nrlsh_exact_topk",
     "nrlsh_free", "nrlsh_last_error", "nrlsh_get_info", "nrlsh_get_partition",
     "nrlsh_get_projection", "nrlsh_get_rank_table", "nrlsh_get_codes", "nrlsh_set_codes",
-    "nrlsh_query_codes", "nrlsh_query_candidates", "nrlsh_last_query_stats", "nrlsh_last_scan_stats",
+    "nrlsh_query_codes", "nrlsh_query_candidates", "nrlsh_last_query_stats", "nrlsh_last_scan_stats", "nrlsh_last_scan_popc",
     "nrlsh_index_exact_topk", "nrlsh_exact_topk_seeded", "nrlsh_index_exact_topk_seeded",
     "nrlsh_last_rerank_stats", "nrlsh_last_rerank_path", "nrlsh_profile_enable", "nrlsh_profile_read",
     "nrlsh_profile_slot_name", "nrlsh_launch_count", "nrlsh_last_exact_stats", "nrlsh_get_proj",
@@ -90,6 +90,8 @@ def lib():
         L.nrlsh_last_query_stats.restype = st
         L.nrlsh_last_scan_stats.argtypes = [p, p]
         L.nrlsh_last_scan_stats.restype = st
+        L.nrlsh_last_scan_popc.argtypes = [p]
+        L.nrlsh_last_scan_popc.restype = st
         L.nrlsh_index_exact_topk.argtypes = [p, p, i64, i32, p, p, p]
         L.nrlsh_index_exact_topk.restype = st
         L.nrlsh_exact_topk_seeded.argtypes = [p, i64, i32, p, i64, i32, p, i32, p, p, p]
@@ -386,7 +388,9 @@ def last_scan_stats():
     """Pairs of the last query on which the scan's lower bound ran / which it decided alone."""
     a, b = C.c_int64(), C.c_int64()
     _check(lib().nrlsh_last_scan_stats(C.byref(a), C.byref(b)))
-    return {"bound_pairs": a.value, "bound_decided_pairs": b.value}
+    p = C.c_int64()
+    _check(lib().nrlsh_last_scan_popc(C.byref(p)))
+    return {"bound_pairs": a.value, "bound_decided_pairs": b.value, "popc_ops": p.value}
 
 
 def last_exact_stats():

@@ -27,6 +27,7 @@ thread_local int64_t g_last_pairs = 0;
 thread_local int64_t g_last_entries = 0;       // candidate-buffer entries the select read
 thread_local int64_t g_last_lb_pairs = 0;       // pairs the scan's lower bound ran on
 thread_local int64_t g_last_lb_skipped = 0;     // ... and decided alone
+thread_local int64_t g_last_scan_popc = 0;      // POPCs the scan issued on existing items
 thread_local int64_t g_last_gt_pairs = 0;      // (query, item) pairs the exact filter multiplied
 thread_local int64_t g_last_rescored = 0;
 thread_local int64_t g_last_rtc_overflow = 0;   // tensor-core re-rank: queries redone by gather
@@ -746,7 +747,7 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
         DBuf rsb, rspk, rseed, rtid, rtsc, rth, rqb, rqn, rhp, rcd, rcc, rpt, rtl, rqp;
     } wsets[3];
     DBuf fl;
-    if (fl.alloc(64, s)) return fail(NRLSH_ENOMEM, "query workspace");
+    if (fl.alloc(80, s)) return fail(NRLSH_ENOMEM, "query workspace");
     for (int w = 0; w < NSET; ++w) {
         WSet &W_ = wsets[w];
         if (W_.qc.alloc((size_t)Qmax * ix->QM * ix->W * 4, s) || W_.dl.alloc((size_t)Qmax * ix->m, s) ||
@@ -823,8 +824,8 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
     tls.qperm = nullptr;
     // [0, 1] non-finite / zero query, [2] fallbacks, [4:5] scanned pairs, [6:7] re-scored,
     // [8:9] filter pairs, [10:11] buffer entries, [12:13] / [14:15] lower-bound pairs
-    const int init_flags[16] = {INT_MAX, INT_MAX, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-    cudaMemcpyAsync(fl.p, init_flags, 64, cudaMemcpyHostToDevice, s);
+    const int init_flags[20] = {INT_MAX, INT_MAX, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyAsync(fl.p, init_flags, 80, cudaMemcpyHostToDevice, s);
     unsigned long long *pairs = (unsigned long long *)(fl.get<int>() + 4);
     const long long launches0 = launch_count();
     // second stream (per thread and device) joined to s by events
@@ -967,8 +968,8 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
         if ((e = oc.finish(s))) return cuda_fail(e, "copy candidates");
         if (rank_out && (e = orr.finish(s))) return cuda_fail(e, "copy ranks");
     }
-    int hflags[16];
-    cudaMemcpyAsync(hflags, fl.p, 64, cudaMemcpyDeviceToHost, s);
+    int hflags[20];
+    cudaMemcpyAsync(hflags, fl.p, 80, cudaMemcpyDeviceToHost, s);
     e = cudaStreamSynchronize(s);
     if (e) return cuda_fail(e, "query");
     e = cudaGetLastError();
@@ -987,6 +988,8 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
     g_last_lb_pairs = (int64_t)pr;
     std::memcpy(&pr, hflags + 14, 8);
     g_last_lb_skipped = (int64_t)pr;
+    std::memcpy(&pr, hflags + 16, 8);
+    g_last_scan_popc = (int64_t)(pr / 2);   // (counted in halves)
     std::memcpy(&pr, hflags + 8, 8);
     if (!g_in_rtc_redo) g_last_rtc_pairs = (int64_t)pr;
     if (!g_in_rtc_redo)
@@ -1061,6 +1064,11 @@ nrlsh_status nrlsh_last_query_stats(int64_t *fallback_queries, int64_t *kernel_l
 nrlsh_status nrlsh_last_scan_stats(int64_t *bound_pairs, int64_t *bound_decided_pairs) {
     if (bound_pairs) *bound_pairs = g_last_lb_pairs;
     if (bound_decided_pairs) *bound_decided_pairs = g_last_lb_skipped;
+    return NRLSH_OK;
+}
+
+nrlsh_status nrlsh_last_scan_popc(int64_t *popc_ops) {
+    if (popc_ops) *popc_ops = g_last_scan_popc;
     return NRLSH_OK;
 }
 

@@ -533,11 +533,12 @@ __global__ void __launch_bounds__(kScanThreads, W == 4 ? 4 : NRLSH_SCAN_MINB) k6
     const uint32_t *__restrict__ qcodes, const int8_t *__restrict__ delta, int Qb, int m,
     const uint16_t *__restrict__ R, int L, unsigned long long *__restrict__ buf,
     uint32_t *__restrict__ cnt, int64_t C, unsigned long long *__restrict__ pairs, int QM,
-    int lbmax, unsigned long long *__restrict__ lbc, int dense, uint32_t *__restrict__ uws) {
+    int lbmax, unsigned long long *__restrict__ lbc, int dense, uint32_t *__restrict__ uws,
+    int lb0max) {
     pdl_wait();
     constexpr int RW = W <= 2 ? 4 : 8;             // record words: codes, radius, query
     __shared__ uint32_t s_unit[2];
-    __shared__ unsigned long long s_lb[2];   // (pairs the lower bound ran on / decided alone)
+    __shared__ unsigned long long s_lb[3];   // (pairs a lower bound ran on / decided alone; 2 x POPCs)
     __shared__ __align__(16) uint32_t srec[kQG][RW];
     __shared__ uint32_t sbuf[kQG][kSB];
     __shared__ uint32_t scnt[kQG];
@@ -608,8 +609,9 @@ __global__ void __launch_bounds__(kScanThreads, W == 4 ? 4 : NRLSH_SCAN_MINB) k6
         }
     }
     if (threadIdx.x == 0 && pairs) atomicAdd(pairs, (unsigned long long)nact * (p1 - p0));
-    if (threadIdx.x == 0) { s_lb[0] = 0ull; s_lb[1] = 0ull; }
-    uint32_t lbt = 0, lbs = 0;   // (this warp: pairs the lower bound ran on / skipped)
+    if (threadIdx.x == 0) { s_lb[0] = 0ull; s_lb[1] = 0ull; s_lb[2] = 0ull; }
+    // (this warp's iterations: coarse bound ran / skipped, pair bound ran / skipped, exact)
+    uint32_t l0t = 0, l0s = 0, lbt = 0, lbs = 0, ext = 0;
     __syncthreads();
     // (the record's shared address is carried in a register: the compiler otherwise
     // rebuilds it from the CTA's window base with five uniform instructions per query)
@@ -626,6 +628,28 @@ __global__ void __launch_bounds__(kScanThreads, W == 4 ? 4 : NRLSH_SCAN_MINB) k6
         uint32_t qc[W];
 #pragma unroll
         for (int w = 0; w < W; ++w) qc[w] = rec[w];
+        if (W >= 2 && dl <= lb0max) {
+            // very small radius: a coarser bound at half the POPCs of the next one.
+            // 128 bits: h >= popc(OR of the four XOR words), one POPC per item; 64 bits:
+            // min(h_u, h_v) >= popc((a_u | b_u) & (a_v | b_v)), one POPC per two items
+            // (an absent item's code 0 only weakens it).  On near-random codes a warp's
+            // 256 items all exceed it with probability > 1/2 up to delta = 24 (Bin(32,
+            // 15/16)) and 10 (Bin(32, 9/16)).
+            int l0min = 255;
+            if (W == 4) {
+#pragma unroll
+                for (int u = 0; u < kScanIPT; ++u)
+                    l0min = min(l0min, __popc((c[u][0] ^ qc[0]) | (c[u][1] ^ qc[1]) |
+                                              (c[u][2] ^ qc[2]) | (c[u][3] ^ qc[3])));
+            } else {
+#pragma unroll
+                for (int u = 0; u + 1 < kScanIPT; u += 2)
+                    l0min = min(l0min, __popc(((c[u][0] ^ qc[0]) | (c[u][1] ^ qc[1])) &
+                                              ((c[u + 1][0] ^ qc[0]) | (c[u + 1][1] ^ qc[1]))));
+            }
+            l0t += 1;
+            if (!__any_sync(NR_FULL, l0min <= dl)) { l0s += 1; continue; }
+        }
         if (W >= 2 && dl <= lbmax) {
             // small radius: a one-POPC lower bound per word pair first,
             // h = popc(a) + popc(b) >= popc(a | b); where no item of the warp can pass,
@@ -644,6 +668,7 @@ __global__ void __launch_bounds__(kScanThreads, W == 4 ? 4 : NRLSH_SCAN_MINB) k6
         }
         // dd_u = delta - h_u in one three-input add per word pair (a pass is dd_u >= 0;
         // h_u = delta - dd_u is only needed for the entries written)
+        ext += 1;
         int dd[kScanIPT];
         uint32_t fail = 0;   // bit u: h_u > delta (the sign of dd_u)
 #pragma unroll
@@ -712,18 +737,26 @@ __global__ void __launch_bounds__(kScanThreads, W == 4 ? 4 : NRLSH_SCAN_MINB) k6
             }
         }
     }
-    if (lbc && lbt) {   // (per warp: iterations x its items)
+    if (lbc) {   // (per warp: iterations x its items; POPCs in halves: the coarse 64-bit bound is 1/2 per item)
         const uint32_t wv = __reduce_add_sync(NR_FULL, (uint32_t)__popc(vmask));
         if (lane == 0) {
-            atomicAdd(&s_lb[0], (unsigned long long)lbt * wv);
-            atomicAdd(&s_lb[1], (unsigned long long)lbs * wv);
+            if (l0t | lbt) {
+                // (a pair counts once in [0] even if both bounds ran on it)
+                atomicAdd(&s_lb[0], (unsigned long long)(l0s + lbt) * wv);
+                atomicAdd(&s_lb[1], (unsigned long long)(l0s + lbs) * wv);
+            }
+            atomicAdd(&s_lb[2], (unsigned long long)(l0t * (W == 4 ? 2u : 1u) + lbt * (uint32_t)W +
+                                                     ext * 2u * (uint32_t)W) * wv);
         }
     }
     if (threadIdx.x == 0) s_unit[upar ^ 1] = nxt;
     __syncthreads();
-    if (lbc && threadIdx.x == 0 && s_lb[0]) {
-        atomicAdd(&lbc[0], s_lb[0]);
-        atomicAdd(&lbc[1], s_lb[1]);
+    if (lbc && threadIdx.x == 0) {
+        if (s_lb[0]) {
+            atomicAdd(&lbc[0], s_lb[0]);
+            atomicAdd(&lbc[1], s_lb[1]);
+        }
+        atomicAdd(&lbc[2], s_lb[2]);
     }
     for (int t = threadIdx.x; t < nqg; t += blockDim.x) {
         const uint32_t nst = min(scnt[t], (uint32_t)kSB);
@@ -801,6 +834,10 @@ void launch_scan(const nrlsh_index *ix, const uint32_t *qcodes, const int8_t *de
     // delta <= 16, 128 bits: delta <= 37); NRLSH_SCAN_LBMAX overrides (-1: off)
     int lbmax = ix->W == 2 ? 16 : (ix->W == 4 ? 37 : -1);
     if (getenv("NRLSH_SCAN_LBMAX")) lbmax = atoi(getenv("NRLSH_SCAN_LBMAX"));
+    // ... and the coarser bound before it (NRLSH_SCAN_LB0MAX, -1: off)
+    int lb0max = ix->W == 2 ? 10 : (ix->W == 4 ? 24 : -1);
+    if (getenv("NRLSH_SCAN_LB0MAX")) lb0max = atoi(getenv("NRLSH_SCAN_LB0MAX"));
+    lb0max = std::min(lb0max, lbmax);
     // radius from which a cell counts as dense (L/2 - 0.75 sqrt(L): ~8% of random codes
     // within it; measured optimum 26 at 64 bits, 56 at 128); its appends go straight to
     // global, the others through the stage
@@ -829,9 +866,9 @@ void launch_scan(const nrlsh_index *ix, const uint32_t *qcodes, const int8_t *de
     const unsigned grid = (unsigned)std::min<int64_t>((int64_t)sms * res[ix->W] * waves,
                                                       (int64_t)ix->nchunks * ngroups);
     switch (ix->W) {
-        case 1: launch_pdl(k6_scan<1>, dim3(grid), dim3(kScanThreads), 0, s, ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs, ix->QM, lbmax, lbc, dense, uws); break;
-        case 2: launch_pdl(k6_scan<2>, dim3(grid), dim3(kScanThreads), 0, s, ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs, ix->QM, lbmax, lbc, dense, uws); break;
-        default: launch_pdl(k6_scan<4>, dim3(grid), dim3(kScanThreads), 0, s, ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs, ix->QM, lbmax, lbc, dense, uws); break;
+        case 1: launch_pdl(k6_scan<1>, dim3(grid), dim3(kScanThreads), 0, s, ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs, ix->QM, lbmax, lbc, dense, uws, lb0max); break;
+        case 2: launch_pdl(k6_scan<2>, dim3(grid), dim3(kScanThreads), 0, s, ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs, ix->QM, lbmax, lbc, dense, uws, lb0max); break;
+        default: launch_pdl(k6_scan<4>, dim3(grid), dim3(kScanThreads), 0, s, ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs, ix->QM, lbmax, lbc, dense, uws, lb0max); break;
     }
     note_launch(2);
 }

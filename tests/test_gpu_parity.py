@@ -612,7 +612,7 @@ def test_candidates_parity_tensor_scan(built, case, monkeypatch):
             assert np.array_equal(grk[qi][order], ork), (T, qi)
 
 
-@pytest.mark.parametrize("bound", ["default", "off", "always"])
+@pytest.mark.parametrize("bound", ["default", "off", "always", "coarse_always"])
 @pytest.mark.parametrize("case", [("c4", 300_000, 32, 64, 128), ("scale", 70_000, 16, 128, 256),
                                   ("tiny", None, None, 32, 8), ("c4", 300_000, 32, 32, 4),
                                   ("c3", 40_000, 64, 64, 1)], ids=_ids)
@@ -623,9 +623,16 @@ def test_candidates_parity_scan_bound(built, case, bound, monkeypatch):
     the candidate sets, ranks and (R, id) order equal the oracle's (identical codes
     injected), across budgets from 1 to n."""
     P = _P()
-    monkeypatch.setenv("NRLSH_SCAN_LBMAX", {"default": "", "off": "-1", "always": "255"}[bound])
+    monkeypatch.setenv("NRLSH_SCAN_LBMAX", {"default": "", "off": "-1", "always": "255",
+                                            "coarse_always": "255"}[bound])
     if bound == "default":
         monkeypatch.delenv("NRLSH_SCAN_LBMAX")
+    # (the coarser first bound — one POPC per item at 128 bits, per two items at 64 —
+    # at every radius too)
+    if bound == "coarse_always":
+        monkeypatch.setenv("NRLSH_SCAN_LB0MAX", "255")
+    else:
+        monkeypatch.delenv("NRLSH_SCAN_LB0MAX", raising=False)
     cfg, X, Q, Xd, idx, orc = built(*case)
     n = X.shape[0]
     ocodes = orc.codes()
@@ -643,7 +650,13 @@ def test_candidates_parity_scan_bound(built, case, bound, monkeypatch):
             assert np.array_equal(gid[qi][order], oid), (T, qi)
             assert np.array_equal(grk[qi][order], ork), (T, qi)
         st = P.last_scan_stats()
-        if bound == "always" and case[3] > 32:
+        qs = P.last_query_stats()
+        W = (case[3] + 31) // 32
+        # POPCs issued: at most W per scanned pair plus the bounds' (W/2 + W/4), at
+        # least one per two pairs
+        assert 0 < st["popc_ops"] <= qs["scanned_pairs"] * (W + W / 2 + W / 4)
+        assert st["popc_ops"] * 2 >= qs["scanned_pairs"]
+        if bound in ("always", "coarse_always") and case[3] > 32:
             assert st["bound_pairs"] > 0
         if bound == "off" or case[3] <= 32:
             assert st["bound_pairs"] == 0
