@@ -489,6 +489,31 @@ __device__ __forceinline__ uint32_t atom_add_global(uint32_t *p, uint32_t v) {
     return old;
 }
 
+// A lane's run of a dense cell: for each set bit u of mask, *p++ = (hib - dd[u]) << 32 |
+// (lob + 256 u).  Inline PTX, five instructions per item (bit test, two value adds, a
+// predicated store, a predicated 32-bit address add): the compiler's predicated 64-bit
+// pointer increments cost ~11.  The run (<= 64 bytes) must not cross a 4 GB boundary
+// (the caller checks), so only the low address word moves.
+__device__ __forceinline__ void emit_run8(uint32_t mask, unsigned long long *p, uint32_t lob,
+                                          uint32_t hib, const int (&dd)[8]) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\t.reg .u32 lo, hi, t, vl, vh;\n\t.reg .u64 a;\n\t"
+        "mov.b64 {lo, hi}, %1;\n\t"
+#define NR_EMIT(U, BIT, OFF)                                                         \
+        "and.b32 t, %0, " BIT ";\n\tsetp.ne.u32 q, t, 0;\n\t"                        \
+        "add.u32 vl, %2, " OFF ";\n\tsub.u32 vh, %3, " U ";\n\t"                     \
+        "mov.b64 a, {lo, hi};\n\t@q st.global.v2.u32 [a], {vl, vh};\n\t"           \
+        "@q add.u32 lo, lo, 8;\n\t"
+        NR_EMIT("%4", "1", "0") NR_EMIT("%5", "2", "256") NR_EMIT("%6", "4", "512")
+        NR_EMIT("%7", "8", "768") NR_EMIT("%8", "16", "1024") NR_EMIT("%9", "32", "1280")
+        NR_EMIT("%10", "64", "1536") NR_EMIT("%11", "128", "1792")
+#undef NR_EMIT
+        "}"
+        :: "r"(mask), "l"(p), "r"(lob), "r"(hib), "r"(dd[0]), "r"(dd[1]), "r"(dd[2]), "r"(dd[3]),
+           "r"(dd[4]), "r"(dd[5]), "r"(dd[6]), "r"(dd[7])
+        : "memory");
+}
+
 // =========================================================================== K6 scan
 constexpr int kScanThreads = 256;
 // items per thread (a work unit = one CTA's chunk of 256 x IPT positions of one
@@ -689,17 +714,28 @@ __global__ void __launch_bounds__(kScanThreads, W == 4 ? 4 : NRLSH_SCAN_MINB) k6
         if (dl >= dense) {
             // dense cell (many of a warp's 256 items pass): lane-owned runs straight in
             // the query's candidate row, one global reservation per warp
-            const uint32_t inc = warp_scan_incl(np);
-            const uint32_t tot = __shfl_sync(NR_FULL, inc, 31);
+            // (the warp total by one REDUX, so the reservation's round trip to L2 overlaps
+            // the five-step prefix sum)
+            const uint32_t tot = __reduce_add_sync(NR_FULL, np);
             uint32_t gb = 0;
             if (lane == 31) gb = atom_add_global(&cnt[q0 + qq], tot);
+            const uint32_t inc = warp_scan_incl(np);
             gb = __shfl_sync(NR_FULL, gb, 31);
             unsigned long long *ptr = row + (gb + inc - np);
             if ((int64_t)gb + tot <= C) {
+                bool done = false;
+                if constexpr (kScanIPT == 8 && kScanThreads == 256) {
+                    if ((uint32_t)reinterpret_cast<uintptr_t>(ptr) <= 0xffffffbfu) {
+                        emit_run8(mask, ptr, pt, jhd, dd);
+                        done = true;
+                    }
+                }
+                if (!done) {
 #pragma unroll
-                for (int u = 0; u < kScanIPT; ++u)
-                    if (mask >> u & 1u)
-                        *ptr++ = ((unsigned long long)(jhd - (uint32_t)dd[u]) << 32) | (pt + kScanThreads * u);
+                    for (int u = 0; u < kScanIPT; ++u)
+                        if (mask >> u & 1u)
+                            *ptr++ = ((unsigned long long)(jhd - (uint32_t)dd[u]) << 32) | (pt + kScanThreads * u);
+                }
             } else {   // the row is full (the query is redone with a larger buffer)
                 const unsigned long long *end = row + C;
 #pragma unroll
