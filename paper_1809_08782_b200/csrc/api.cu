@@ -710,6 +710,9 @@ static nrlsh_status query_impl(const nrlsh_index *ix, const float *queries,
     int64_t max_part = 0;
     for (int j = 0; j < ix->m; ++j) max_part = std::max(max_part, ix->offsets[j + 1] - ix->offsets[j]);
     int64_t C = buffer_capacity(Tq, stride, n, max_part);
+    // test switch: the smallest capacity the exact fallback still fits in (T + one
+    // sub-dataset), so the scan's rows fill up and its guarded stores run
+    if (getenv("NRLSH_TEST_BUFFER_TIGHT")) C = std::min<int64_t>(C, Tq + max_part + 64);
     int Qmax = (int)std::min<int64_t>(ix->query_batch, nq);
     if (scan_tc_supported(ix)) C += scan_tc_slack(Qmax);   // (its runs' unused tails)
     C = (C + 1) & ~(int64_t)1;   // even: 16-byte-aligned buffer rows (the select's paired loads)

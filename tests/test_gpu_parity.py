@@ -662,6 +662,28 @@ def test_candidates_parity_scan_bound(built, case, bound, monkeypatch):
             assert st["bound_pairs"] == 0
 
 
+def test_scan_rows_full(built, monkeypatch):
+    """Candidate rows too small for the pilot's estimate (NRLSH_TEST_BUFFER_TIGHT: T plus
+    one sub-dataset): the scan's dense runs, lane spills and stage copy-out hit the end of
+    the row (their guarded stores), the counts overflow, and the exact fallback redoes
+    those queries — the candidates still equal the oracle's."""
+    cfg, X, Q, Xd, idx, orc = built("c4", 300_000, 32, 64, 128)
+    P = _P()
+    monkeypatch.setenv("NRLSH_TEST_BUFFER_TIGHT", "1")
+    ocodes = orc.codes()
+    idx.set_codes(ocodes[orc.perm])
+    qc = oracle.query_codes(Q, orc.A)
+    qcd = torch.from_numpy(qc.view(np.int32)).cuda()
+    T = 30_000
+    gid, grk = idx.candidates(T, qcodes=qcd)
+    assert P.last_query_stats()["fallback_queries"] > 0
+    gid, grk = gid.cpu().numpy(), grk.cpu().numpy().view(np.uint16)
+    for qi in range(0, len(Q), 4):
+        oid, ork = oracle.candidates(ocodes, orc.part, qc[qi], orc.R, T)
+        o = np.lexsort((gid[qi], grk[qi]))
+        assert np.array_equal(gid[qi][o], oid) and np.array_equal(grk[qi][o], ork)
+
+
 def test_small_last_sub_batch_large_budget(built):
     """nq = one full sub-batch + a few queries, T spanning several re-rank rounds: the
     short last sub-batch splits its candidates finer than the full one (regression:
