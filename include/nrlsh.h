@@ -172,11 +172,12 @@ nrlsh_status nrlsh_last_query_stats(int64_t *fallback_queries, int64_t *kernel_l
                                     int64_t *scanned_pairs, int64_t *buffer_entries);
 
 /* Of the last nrlsh_query's scanned pairs on this thread (codes of >= 64 bits): the
-   pairs on which the scan first evaluated the lower bound h >= sum over word pairs
-   of popcount((x_a ^ q_a) | (x_b ^ q_b)) (radii delta_j(q) up to 16 for 64-bit
-   codes, 37 for 128-bit codes), and the pairs that bound decided alone (a warp's
-   256 items all above the radius: no exact distance needed, the same candidates as
-   without it).  Either may be NULL. */
+   pairs on which the scan first evaluated a lower bound of h — the pair bound
+   h >= sum over word pairs of popcount((x_a ^ q_a) | (x_b ^ q_b)) (radii delta_j(q)
+   up to 16 for 64-bit codes, 37 for 128-bit codes) or, at very small radii, the
+   coarser bound described under nrlsh_last_scan_popc alone — and the pairs a bound
+   decided alone (a warp's 256 items all above the radius: no exact distance needed,
+   the same candidates as without it).  Either may be NULL. */
 nrlsh_status nrlsh_last_scan_stats(int64_t *bound_pairs, int64_t *bound_decided_pairs);
 
 /* POPC instructions (per thread, on existing items) the popcount scan of the last
