@@ -495,7 +495,7 @@ __device__ __forceinline__ uint32_t atom_add_global(uint32_t *p, uint32_t v) {
 // pointer increments cost ~11.  The run (<= 64 bytes) must not cross a 4 GB boundary
 // (the caller checks), so only the low address word moves.
 __device__ __forceinline__ void emit_run8(uint32_t mask, unsigned long long *p, uint32_t lob,
-                                          uint32_t hib, const int (&dd)[8]) {
+                                          uint32_t hib, const int *dd) {
     asm volatile(
         "{\n\t.reg .pred q;\n\t.reg .u32 lo, hi, t, vl, vh;\n\t.reg .u64 a;\n\t"
         "mov.b64 {lo, hi}, %1;\n\t"
