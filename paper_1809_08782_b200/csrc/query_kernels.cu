@@ -559,7 +559,7 @@ __global__ void __launch_bounds__(kScanThreads, W == 4 ? 4 : NRLSH_SCAN_MINB) k6
     const uint16_t *__restrict__ R, int L, unsigned long long *__restrict__ buf,
     uint32_t *__restrict__ cnt, int64_t C, unsigned long long *__restrict__ pairs, int QM,
     int lbmax, unsigned long long *__restrict__ lbc, int dense, uint32_t *__restrict__ uws,
-    int lb0max) {
+    int lb0max, int all_units) {
     pdl_wait();
     constexpr int RW = W <= 2 ? 4 : 8;             // record words: codes, radius, query
     __shared__ uint32_t s_unit[2];
@@ -572,7 +572,9 @@ __global__ void __launch_bounds__(kScanThreads, W == 4 ? 4 : NRLSH_SCAN_MINB) k6
     // from a work counter (the next unit's index is fetched while this one runs); the
     // last CTA to finish resets the counters for the next launch on this workspace.
     const int ngroups = (Qb + kQG - 1) / kQG;
-    const uint32_t nunits = uws[0];
+    // (all_units > 0: small problems skip the list — every (chunk, group) is a unit, an
+    // inactive one costs a radius read and a barrier)
+    const uint32_t nunits = all_units > 0 ? (uint32_t)all_units : uws[0];
     const uint32_t *units = uws + 4;
     if (threadIdx.x == 0) s_unit[0] = atomicAdd(&uws[1], 1u);
     __syncthreads();
@@ -580,7 +582,7 @@ __global__ void __launch_bounds__(kScanThreads, W == 4 ? 4 : NRLSH_SCAN_MINB) k6
     for (int upar = 0; ui < nunits; upar ^= 1, ui = s_unit[upar]) {
     uint32_t nxt = 0;   // (stored after the main loop: the atomic's round trip stays off the path)
     if (threadIdx.x == 0) nxt = atomicAdd(&uws[1], 1u);
-    const uint32_t unit = units[ui];
+    const uint32_t unit = all_units > 0 ? ui : units[ui];
     const int4 ch = chunks[unit / (uint32_t)ngroups];
     const int j = ch.x, p0 = ch.y, p1 = ch.z;
     const int q0 = (int)(unit % (uint32_t)ngroups) * kQG;
@@ -601,7 +603,12 @@ __global__ void __launch_bounds__(kScanThreads, W == 4 ? 4 : NRLSH_SCAN_MINB) k6
         bal[h] = __ballot_sync(NR_FULL, dlv[h] >= 0);
         nact += __popc(bal[h]);
     }
-    uint32_t c[kScanIPT][W];   // (a listed unit has nact >= 1)
+    if (nact == 0) {   // (only without the list; uniform: every warp computed the same count)
+        if (threadIdx.x == 0) s_unit[upar ^ 1] = nxt;
+        __syncthreads();
+        continue;
+    }
+    uint32_t c[kScanIPT][W];
     uint32_t vmask = 0;   // bit u: item u of this thread exists
 #pragma unroll
     for (int u = 0; u < kScanIPT; ++u) {
@@ -881,8 +888,6 @@ void launch_scan(const nrlsh_index *ix, const uint32_t *qcodes, const int8_t *de
     if (getenv("NRLSH_SCAN_DENSE")) dense = atoi(getenv("NRLSH_SCAN_DENSE"));
     const int ngroups = (Qb + kQG - 1) / kQG;
     uint32_t *uws = static_cast<uint32_t *>(units_ws);
-    launch_pdl(scan_units, dim3(ngroups), dim3(1024), 0, s, delta, Qb, ix->m, ix->chunks_d,
-               (int)ix->nchunks, uws);
     // one wave of resident CTAs (NRLSH_SCAN_WAVES: CTAs per resident slot, default 1)
     static int res[5] = {0, 0, 0, 0, 0};
     if (!res[ix->W]) {
@@ -901,12 +906,19 @@ void launch_scan(const nrlsh_index *ix, const uint32_t *qcodes, const int8_t *de
     static const int waves = getenv("NRLSH_SCAN_WAVES") ? std::max(1, atoi(getenv("NRLSH_SCAN_WAVES"))) : 1;
     const unsigned grid = (unsigned)std::min<int64_t>((int64_t)sms * res[ix->W] * waves,
                                                       (int64_t)ix->nchunks * ngroups);
+    // at most two waves of units: not worth the list's launch (small indexes, a handful
+    // of queries)
+    const int64_t total = (int64_t)ix->nchunks * ngroups;
+    const int all_units = total <= 2 * (int64_t)sms * res[ix->W] ? (int)total : 0;
+    if (!all_units)
+        launch_pdl(scan_units, dim3(ngroups), dim3(1024), 0, s, delta, Qb, ix->m, ix->chunks_d,
+                   (int)ix->nchunks, uws);
     switch (ix->W) {
-        case 1: launch_pdl(k6_scan<1>, dim3(grid), dim3(kScanThreads), 0, s, ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs, ix->QM, lbmax, lbc, dense, uws, lb0max); break;
-        case 2: launch_pdl(k6_scan<2>, dim3(grid), dim3(kScanThreads), 0, s, ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs, ix->QM, lbmax, lbc, dense, uws, lb0max); break;
-        default: launch_pdl(k6_scan<4>, dim3(grid), dim3(kScanThreads), 0, s, ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs, ix->QM, lbmax, lbc, dense, uws, lb0max); break;
+        case 1: launch_pdl(k6_scan<1>, dim3(grid), dim3(kScanThreads), 0, s, ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs, ix->QM, lbmax, lbc, dense, uws, lb0max, all_units); break;
+        case 2: launch_pdl(k6_scan<2>, dim3(grid), dim3(kScanThreads), 0, s, ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs, ix->QM, lbmax, lbc, dense, uws, lb0max, all_units); break;
+        default: launch_pdl(k6_scan<4>, dim3(grid), dim3(kScanThreads), 0, s, ix->codes, ix->chunks_d, qcodes, delta, Qb, ix->m, ix->R_d, ix->L, buf, cnt, C, pairs, ix->QM, lbmax, lbc, dense, uws, lb0max, all_units); break;
     }
-    note_launch(2);
+    note_launch(all_units ? 1 : 2);
 }
 
 
